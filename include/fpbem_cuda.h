@@ -1,0 +1,149 @@
+/*
+ * fpbem_cuda.h — C-ABI of the B200-native periodic-FMBEM hot path.
+ *
+ * Drop-in boundary for the reference's operator product and Krylov solver
+ * (arXiv 2201.12050 "fpbem", /root/reference/proj):
+ *
+ *   fpbem_cu_fmm_create   replaces the data hand-off of FmmOperators
+ *                         (include/fpbem/fmm.hpp:54-71) into the backend
+ *                         built by make_backend (src/scene.cpp:323-327)
+ *   fpbem_cu_fmm_apply    replaces FmmOperators::matvec (src/fmm.cpp:246-271)
+ *                         i.e. the solver::ApplyFn (include/fpbem/solver.hpp:21)
+ *   fpbem_cu_gmres        replaces solver::gmres (src/solver.cpp:21-123,
+ *                         include/fpbem/solver.hpp:14-33) with a device-
+ *                         resident Krylov basis
+ *   fpbem_cu_fmm_bytes    replaces FmmOperators::stored_bytes (src/fmm.cpp:273-279)
+ *   fpbem_cu_spectrum     exposes CirculantSpectrum::lambda (include/fpbem/structured.hpp:41)
+ *                         when the spectrum was built on the device
+ *
+ * Plain pointers and sizes only; complex numbers are interleaved (re, im)
+ * doubles, layout-identical to std::complex<double> / Eigen::VectorXcd.
+ * Vector layout is the reference's: cell-major, x index fastest, then y,
+ * then z, n_dof entries per cell (include/fpbem/geometry.hpp:53-62). With
+ * nrhs > 1 the right-hand sides are stored one after another (x[r*N + i]).
+ *
+ * Errors: every int-returning call returns FPBEM_CU_OK (0) or one of the
+ * codes below; fpbem_cu_last_error() gives the message of the calling
+ * thread's last failure. The C++ shim (include/fpbem_cuda.hpp) maps
+ * FPBEM_CU_EDIM to std::invalid_argument and everything else to
+ * std::runtime_error, as the reference throws (src/fmm.cpp:250,
+ * src/solver.cpp:15).
+ */
+#ifndef FPBEM_CUDA_H
+#define FPBEM_CUDA_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPBEM_CU_OK 0
+#define FPBEM_CU_EDIM 1       /* dimension mismatch  -> std::invalid_argument */
+#define FPBEM_CU_ENONFINITE 2 /* operator produced NaN/Inf -> runtime_error   */
+#define FPBEM_CU_ECUDA 3      /* CUDA runtime failure                         */
+#define FPBEM_CU_ENOMEM 4     /* device allocation failed                     */
+#define FPBEM_CU_ENCCL 5      /* NCCL failure (multi-GPU)                      */
+#define FPBEM_CU_EINVAL 6     /* invalid argument / unsupported option        */
+
+#define FPBEM_CU_PTR_HOST 0   /* x / y are host pointers (copies inside call) */
+#define FPBEM_CU_PTR_DEVICE 1 /* x / y are device pointers (stream-ordered)   */
+
+typedef struct {
+  double re, im;
+} fpbem_c64;
+
+typedef struct fpbem_cu_op fpbem_cu_op;     /* opaque; owns device memory and stream */
+typedef struct fpbem_cu_comm fpbem_cu_comm; /* opaque NCCL communicator             */
+
+/* Operator description: FmmOperators' fields (include/fpbem/fmm.hpp:54-71).
+ * Host arrays are copied at create; the caller keeps ownership. */
+typedef struct {
+  int counts[3];                 /* lattice cells per axis (Lattice::counts)              */
+  int n_dof;                     /* elements per cell (S block dim)                       */
+  int n_coef;                    /* (n_t+1)^2 expansion coefficients                      */
+  int n_near;                    /* |S|: stored near offsets                              */
+  const int* near_offsets;       /* n_near x 3 (ox,oy,oz) = target - source, in
+                                    BlockToeplitzMatrix::offsets order                    */
+  const fpbem_c64* near_blocks;  /* n_near x n_dof^2, each column-major (row = target)    */
+  const fpbem_c64* u0;           /* L2P: n_dof x n_coef, column-major                      */
+  const fpbem_c64* v0;           /* P2M: n_coef x n_dof, column-major                      */
+  int fft_sizes[3];              /* circulant embedding lengths; 0 = reference 7-smooth
+                                    padding fft_friendly(2M-1) (src/structured.cpp:67-68)  */
+  const fpbem_c64* lambda;       /* optional prebuilt spectrum: q x n_coef^2 column-major
+                                    blocks, q = (qz*Ly+qy)*Lx+qx (src/structured.cpp:80-86) */
+  int n_far;                     /* far offsets (used when lambda == NULL)                */
+  const int* far_offsets;        /* n_far x 3                                             */
+  const fpbem_c64* far_blocks;   /* n_far x n_coef^2 M2L bank K, column-major; the device
+                                    builds the spectrum (src/structured.cpp:63-108)        */
+  int mirrored_level;            /* -1: no half-space image pair (only value supported)   */
+  int max_rhs;                   /* largest nrhs passed to apply/gmres (workspace sizing)  */
+} fpbem_cu_fmm_desc;
+
+int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* desc, int device, fpbem_cu_op** out);
+void fpbem_cu_fmm_destroy(fpbem_cu_op* op);
+
+/* y = A x for nrhs right-hand sides. ptr_kind: FPBEM_CU_PTR_HOST (synchronous)
+ * or FPBEM_CU_PTR_DEVICE (enqueued on the handle's stream). */
+int fpbem_cu_fmm_apply(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int nrhs, int ptr_kind);
+
+/* Restarted GMRES(restart) from x0 = 0, independently per right-hand side
+ * (src/solver.cpp:21-123: MGS + one conditional reorthogonalisation pass,
+ * complex Givens, estimate-based inner exit, true residual per cycle).
+ * iterations/converged: nrhs entries. history: per rhs, up to history_cap
+ * relative-residual estimates (row r at history + r*history_cap);
+ * history_len: nrhs entries (may be NULL). Returns FPBEM_CU_ENONFINITE when
+ * the operator produced NaN/Inf (src/solver.cpp:13-17). */
+int fpbem_cu_gmres(fpbem_cu_op* op, const fpbem_c64* b, fpbem_c64* x, int nrhs, double tol,
+                   int restart, int max_iter, int ptr_kind, int* iterations, int* converged,
+                   double* history, int history_cap, int* history_len);
+
+/* The reference's ApplyFn seam (include/fpbem/solver.hpp:21) on the device:
+ * GMRES over any operator given as a callback that maps a device vector to
+ * a device vector on `stream` (a cudaStream_t). Returns 0 on success.
+ * precond (may be NULL) is the optional left preconditioner M^{-1}
+ * (GmresOptions::preconditioner, include/fpbem/solver.hpp:27). */
+typedef int (*fpbem_cu_apply_fn)(void* ctx, const fpbem_c64* x_dev, fpbem_c64* y_dev, void* stream);
+int fpbem_cu_gmres_fn(int device, long long n, fpbem_cu_apply_fn apply, void* apply_ctx,
+                      fpbem_cu_apply_fn precond, void* precond_ctx, const fpbem_c64* b, fpbem_c64* x,
+                      double tol, int restart, int max_iter, int ptr_kind, int* iterations,
+                      int* converged, double* history, int history_cap, int* history_len);
+
+/* Device bytes of the operator data, counted like FmmOperators::stored_bytes
+ * (S blocks + spectrum + U0 + V0). */
+int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes);
+
+/* Spectrum readback (sizes[3] always; lambda_out may be NULL). */
+int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out);
+
+/* Run subsequent device work on an external cudaStream_t (NULL = own stream). */
+int fpbem_cu_set_stream(fpbem_cu_op* op, void* stream);
+
+/* Per-stage CUDA-event timing of applies (0 = off). When on, each apply
+ * accumulates milliseconds per stage; fpbem_cu_stage_times copies
+ * {near_gemm, near_reduce_l2p, p2m, m2l, total, applies} into ms_out[6]
+ * and resets the counters. */
+int fpbem_cu_enable_stage_timing(fpbem_cu_op* op, int enable);
+int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out);
+
+/* Number of CUDA kernels this handle launched since creation. */
+long long fpbem_cu_kernel_launches(const fpbem_cu_op* op);
+
+/* Multi-GPU (one process per GPU). Rank 0 makes the id, the caller
+ * broadcasts its 128 bytes (e.g. torch.distributed), every rank inits.
+ * With a communicator attached, apply() splits the near-field offsets
+ * across ranks and all-reduces the partial products. */
+int fpbem_cu_comm_unique_id(unsigned char id_out[128]);
+int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int device,
+                       fpbem_cu_comm** out);
+void fpbem_cu_comm_destroy(fpbem_cu_comm* comm);
+int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm);
+
+const char* fpbem_cu_last_error(void);
+const char* fpbem_cu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FPBEM_CUDA_H */

@@ -1,0 +1,137 @@
+"""ctypes bindings of the native libraries.
+
+libfpbem_cuda.so carries the sm_100a kernels behind the C-ABI of
+include/fpbem_cuda.h; libfpbem_host.so the host operator producer. There is
+no fallback: if a library is missing or fails to load, this raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+
+c_int_p = C.POINTER(C.c_int)
+c_double_p = C.POINTER(C.c_double)
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def _load(name: str) -> C.CDLL:
+    path = LIB_DIR / name
+    if not path.exists():
+        raise NativeLibraryMissing(
+            f"{path} is not built; run `python -m paper_2201_12050_b200.build` (or __graft_entry__.build())")
+    return C.CDLL(str(path), mode=C.RTLD_GLOBAL)
+
+
+class FmmDesc(C.Structure):
+    """fpbem_cu_fmm_desc (include/fpbem_cuda.h)."""
+
+    _fields_ = [
+        ("counts", C.c_int * 3),
+        ("n_dof", C.c_int),
+        ("n_coef", C.c_int),
+        ("n_near", C.c_int),
+        ("near_offsets", C.c_void_p),
+        ("near_blocks", C.c_void_p),
+        ("u0", C.c_void_p),
+        ("v0", C.c_void_p),
+        ("fft_sizes", C.c_int * 3),
+        ("lambda_", C.c_void_p),
+        ("n_far", C.c_int),
+        ("far_offsets", C.c_void_p),
+        ("far_blocks", C.c_void_p),
+        ("mirrored_level", C.c_int),
+        ("max_rhs", C.c_int),
+    ]
+
+
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+# every symbol include/fpbem_cuda.h declares (checked by tests/test_boundary.py)
+CUDA_SYMBOLS = (
+    "fpbem_cu_fmm_create", "fpbem_cu_fmm_destroy", "fpbem_cu_fmm_apply", "fpbem_cu_gmres",
+    "fpbem_cu_gmres_fn", "fpbem_cu_fmm_bytes", "fpbem_cu_spectrum", "fpbem_cu_set_stream",
+    "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
+    "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
+    "fpbem_cu_last_error", "fpbem_cu_version",
+)
+
+_cuda = None
+_host = None
+
+
+def cuda() -> C.CDLL:
+    global _cuda
+    if _cuda is None:
+        lib = _load("libfpbem_cuda.so")
+        vp = C.c_void_p
+        sig = {
+            "fpbem_cu_fmm_create": (C.c_int, [C.POINTER(FmmDesc), C.c_int, C.POINTER(vp)]),
+            "fpbem_cu_fmm_destroy": (None, [vp]),
+            "fpbem_cu_fmm_apply": (C.c_int, [vp, vp, vp, C.c_int, C.c_int]),
+            "fpbem_cu_gmres": (C.c_int, [vp, vp, vp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, c_int_p,
+                                         c_int_p, c_double_p, C.c_int, c_int_p]),
+            "fpbem_cu_gmres_fn": (C.c_int, [C.c_int, C.c_longlong, APPLY_FN, vp, APPLY_FN, vp, vp, vp, C.c_double,
+                                            C.c_int, C.c_int, C.c_int, c_int_p, c_int_p, c_double_p, C.c_int,
+                                            c_int_p]),
+            "fpbem_cu_fmm_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
+            "fpbem_cu_spectrum": (C.c_int, [vp, c_int_p, vp]),
+            "fpbem_cu_set_stream": (C.c_int, [vp, vp]),
+            "fpbem_cu_enable_stage_timing": (C.c_int, [vp, C.c_int]),
+            "fpbem_cu_stage_times": (C.c_int, [vp, c_double_p]),
+            "fpbem_cu_kernel_launches": (C.c_longlong, [vp]),
+            "fpbem_cu_comm_unique_id": (C.c_int, [C.c_char_p]),
+            "fpbem_cu_comm_init": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+            "fpbem_cu_comm_destroy": (None, [vp]),
+            "fpbem_cu_fmm_set_comm": (C.c_int, [vp, vp]),
+            "fpbem_cu_last_error": (C.c_char_p, []),
+            "fpbem_cu_version": (C.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _cuda = lib
+    return _cuda
+
+
+def host() -> C.CDLL:
+    global _host
+    if _host is None:
+        lib = _load("libfpbem_host.so")
+        vp = C.c_void_p
+        sig = {
+            "fh_last_error": (C.c_char_p, []),
+            "fh_scene_create": (vp, [C.c_int, C.c_int]),
+            "fh_scene_custom": (vp, [C.c_int, c_double_p, c_int_p, c_double_p, C.c_double]),
+            "fh_scene_destroy": (None, [vp]),
+            "fh_scene_info": (None, [vp, c_int_p, c_double_p]),
+            "fh_scene_set_k": (None, [vp, C.c_double]),
+            "fh_scene_sweep": (None, [vp, c_double_p]),
+            "fh_scene_set_sources": (None, [vp, C.c_int, c_int_p, c_double_p]),
+            "fh_scene_rhs": (C.c_int, [vp, C.c_int, vp]),
+            "fh_scene_dense": (C.c_int, [vp, vp]),
+            "fh_scene_cell": (C.c_int, [vp, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p, c_int_p]),
+            "fh_interaction_block": (C.c_int, [vp, c_double_p, C.c_int, vp]),
+            "fh_classify": (C.c_int, [vp, c_int_p, c_int_p, c_int_p, c_int_p, C.c_int, c_double_p]),
+            "fh_fmm_assemble": (vp, [vp, C.c_int, C.c_int]),
+            "fh_fmm_destroy": (None, [vp]),
+            "fh_fmm_info": (None, [vp, c_int_p]),
+            "fh_fmm_arrays": (None, [vp] + [C.POINTER(vp)] * 6),
+            "fh_sph_bessel": (None, [C.c_int, C.c_double, c_double_p, c_double_p]),
+            "fh_wigner3j": (C.c_double, [C.c_int] * 6),
+            "fh_solid_gradients": (C.c_int, [C.c_int, c_double_p, C.c_double, vp, vp, vp, vp]),
+            "fh_solid_singular": (C.c_int, [C.c_int, c_double_p, C.c_double, vp]),
+            "fh_m2l_block": (C.c_int, [C.c_int, c_double_p, C.c_double, vp]),
+            "fh_expansions": (C.c_int, [vp, C.c_int, c_double_p, vp, vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _host = lib
+    return _host

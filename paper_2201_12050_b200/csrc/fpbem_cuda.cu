@@ -1,0 +1,927 @@
+// C-ABI implementation (include/fpbem_cuda.h): operator handle, the fused
+// FMM apply (near field + P2M + lattice-DFT M2L + L2P) and the device-
+// resident restarted GMRES.
+//
+//   FmmOperators::matvec  src/fmm.cpp:246-271  -> apply_chunk()
+//   solver::gmres         src/solver.cpp:21-123 -> gmres_one()
+//   CirculantSpectrum ctor src/structured.cpp:63-108 -> build_spectrum()
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <functional>
+#include <memory>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fpbem_cuda.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace fpbem_cu;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+};
+
+void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw Fail{code};
+}
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? FPBEM_CU_ENOMEM : FPBEM_CU_ECUDA;
+    fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename T>
+T* dalloc(size_t count, const char* what) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  check(cudaMalloc(&p, count * sizeof(T)), what);
+  return static_cast<T*>(p);
+}
+
+// host->device copy ordered on `stream` (never the legacy default stream,
+// which does not synchronise with the handle's non-blocking stream)
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t stream, const char* what) {
+  if (bytes == 0) return;
+  check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), what);
+  check(cudaStreamSynchronize(stream), what);
+}
+
+int fft_friendly(int n) {  // smallest 7-smooth length >= n (src/structured.cpp:26-33)
+  for (int m = n;; ++m) {
+    int r = m;
+    for (int f : {2, 3, 5, 7})
+      while (r % f == 0) r /= f;
+    if (r == 1) return m;
+  }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+// NCCL, loaded at runtime so the library has no hard NCCL dependency.
+
+struct fpbem_cu_comm {
+  void* lib = nullptr;
+  void* comm = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0, device = 0;
+  int (*allreduce)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
+  int (*destroy)(void*) = nullptr;
+};
+
+namespace {
+void* load_nccl() {
+  static void* lib = nullptr;
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  return lib;
+}
+}  // namespace
+
+struct fpbem_cu_op {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int counts[3] = {1, 1, 1};
+  int n = 0, b = 0, n_cells = 0;
+  long long N = 0;
+  int max_rhs = 1;
+
+  // near field
+  int n_near = 0;
+  std::vector<int> near_offsets;
+  c64* S = nullptr;
+  int n_pairs = 0;
+  std::vector<int> pair_start;  // per offset slot, n_near + 1
+  int* pair_src = nullptr;
+  int* tgt_ptr = nullptr;
+  int* tgt_pairs = nullptr;
+  int4* jobs = nullptr;
+  int jobs_nrhs = -1, n_jobs = 0, jobs_cap = 0;
+  std::vector<int> rank_slots;  // offset slots this rank computes (all without a comm)
+
+  // expansions and spectrum
+  c64* u0 = nullptr;
+  c64* v0 = nullptr;
+  int L[3] = {1, 1, 1};
+  long long q_total = 1;
+  c64* lambda = nullptr;
+  c64* tw[3] = {nullptr, nullptr, nullptr};
+
+  // per-apply buffers (sized for max_rhs)
+  c64* W = nullptr;
+  c64* mom = nullptr;
+  c64* loc = nullptr;
+  c64* fa = nullptr;
+  c64* fb = nullptr;
+  c64* xin = nullptr;   // host-pointer staging
+  c64* yout = nullptr;
+
+  // GMRES
+  c64* basis = nullptr;
+  int basis_cols = 0;
+  c64* gx = nullptr;
+  c64* gb = nullptr;
+  c64* gt = nullptr;
+  c64* gsol = nullptr;
+  c64* scal_c = nullptr;    // h[0..m], hc[0..m], y[0..m]
+  double* scal_d = nullptr;  // [0] pre^2 [1] post^2 [2] misc [3] rnorm^2
+  int* flag = nullptr;
+  int scal_cap = 0;
+  RedScratch rs{};
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
+  double stage_ms[5] = {0, 0, 0, 0, 0};
+  long long applies = 0;
+  long long launches = 0;
+
+  fpbem_cu_comm* comm = nullptr;
+};
+
+namespace {
+
+void build_jobs(fpbem_cu_op* op, int nrhs) {
+  if (op->jobs_nrhs == nrhs) return;
+  const int bn = near_gemm_tile_cols();
+  std::vector<int4> jobs;
+  for (int s : op->rank_slots) {
+    const int pairs = op->pair_start[s + 1] - op->pair_start[s];
+    const int cols = pairs * nrhs;
+    for (int c0 = 0; c0 < cols; c0 += bn) jobs.push_back(make_int4(s, c0, std::min(bn, cols - c0), op->pair_start[s]));
+  }
+  if (static_cast<int>(jobs.size()) > op->jobs_cap) {
+    if (op->jobs) cudaFree(op->jobs);
+    op->jobs = dalloc<int4>(jobs.size(), "jobs");
+    op->jobs_cap = static_cast<int>(jobs.size());
+  }
+  if (!jobs.empty())
+    h2d(op->jobs, jobs.data(), jobs.size() * sizeof(int4), op->stream, "jobs upload");
+  op->n_jobs = static_cast<int>(jobs.size());
+  op->jobs_nrhs = nrhs;
+}
+
+void twiddles(fpbem_cu_op* op, int L, c64** out) {
+  std::vector<c64> t(L);
+  for (int j = 0; j < L; ++j) {
+    long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
+    t[j] = cmk(static_cast<double>(std::cos(a)), static_cast<double>(std::sin(a)));
+  }
+  *out = dalloc<c64>(L, "twiddles");
+  h2d(*out, t.data(), L * sizeof(c64), op->stream, "twiddle upload");
+}
+
+// lattice DFT of the embedded K column on the device (src/structured.cpp:63-108)
+void build_spectrum(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
+  const int b2 = op->b * op->b;
+  const size_t total = static_cast<size_t>(op->q_total) * b2;
+  op->lambda = dalloc<c64>(total, "spectrum");
+  if (d->lambda) {
+    h2d(op->lambda, d->lambda, total * sizeof(c64), op->stream, "spectrum upload");
+    return;
+  }
+  c64* tmp = dalloc<c64>(total, "spectrum scratch");
+  c64* blocks = dalloc<c64>(static_cast<size_t>(d->n_far) * b2, "far bank");
+  int* offs = dalloc<int>(static_cast<size_t>(d->n_far) * 3, "far offsets");
+  if (d->n_far > 0) {
+    h2d(blocks, d->far_blocks, static_cast<size_t>(d->n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
+    h2d(offs, d->far_offsets, static_cast<size_t>(d->n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
+  }
+  check(cudaMemsetAsync(op->lambda, 0, total * sizeof(c64), op->stream), "spectrum clear");
+  check(launch_scatter_bank(blocks, offs, d->n_far, b2, op->L[0], op->L[1], op->L[2], op->lambda, op->stream),
+        "scatter bank");
+  // forward DFT over every axis of the full embedding (all L inputs)
+  c64* cur = op->lambda;
+  c64* nxt = tmp;
+  const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
+  if (Lx > 1) {
+    check(launch_dft_axis(cur, nxt, op->tw[0], Ly * Lz, op->L[0], op->L[0], b2, op->L[0], false, 1.0, op->stream),
+          "spectrum dft x");
+    std::swap(cur, nxt);
+  }
+  if (Ly > 1) {
+    check(launch_dft_axis(cur, nxt, op->tw[1], Lz, op->L[1], op->L[1], Lx * b2, op->L[1], false, 1.0, op->stream),
+          "spectrum dft y");
+    std::swap(cur, nxt);
+  }
+  if (Lz > 1) {
+    check(launch_dft_axis(cur, nxt, op->tw[2], 1, op->L[2], op->L[2], Lx * Ly * b2, op->L[2], false, 1.0, op->stream),
+          "spectrum dft z");
+    std::swap(cur, nxt);
+  }
+  if (cur != op->lambda) {
+    check(cudaMemcpyAsync(op->lambda, cur, total * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "spectrum copy");
+  }
+  check(cudaStreamSynchronize(op->stream), "spectrum build");
+  cudaFree(tmp);
+  cudaFree(blocks);
+  cudaFree(offs);
+}
+
+void ev_record(fpbem_cu_op* op, int i) {
+  if (op->timing) cudaEventRecord(op->ev[i], op->stream);
+}
+
+// One FMM product for nrhs <= max_rhs right-hand sides, device pointers.
+// Order of the sums follows src/fmm.cpp:253-267: y = S p, then y += U0 L.
+void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
+  cudaStream_t s = op->stream;
+  const long long E = static_cast<long long>(nrhs) * op->b;
+  build_jobs(op, nrhs);
+  ev_record(op, 0);
+  check(launch_near_gemm(op->S, x, op->W, op->pair_src, op->jobs, op->n_jobs, op->n, op->N, nrhs, s), "near gemm");
+  op->launches += op->n_jobs > 0;
+  ev_record(op, 1);
+  check(launch_p2m(op->v0, x, op->mom, op->n, op->b, op->n_cells, op->N, nrhs, s), "p2m");
+  op->launches++;
+  ev_record(op, 2);
+
+  // pruned separable lattice DFT, per-mode product, pruned inverse
+  const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
+  const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
+  struct Pass {
+    int kind;  // 0 dft, 1 mode product
+    long long n_a;
+    int n_in, n_out;
+    long long inner;
+    int L;
+    int axis;
+    bool back;
+  };
+  std::vector<Pass> passes;
+  long long cx = Mx, cy = My;  // current x / y extents
+  if (Lx > 1) {
+    passes.push_back({0, My * Mz, static_cast<int>(Mx), static_cast<int>(Lx), E, static_cast<int>(Lx), 0, false});
+    cx = Lx;
+  }
+  if (Ly > 1) {
+    passes.push_back({0, Mz, static_cast<int>(My), static_cast<int>(Ly), cx * E, static_cast<int>(Ly), 1, false});
+    cy = Ly;
+  }
+  if (Lz > 1) passes.push_back({0, 1, static_cast<int>(Mz), static_cast<int>(Lz), cy * cx * E, static_cast<int>(Lz), 2, false});
+  passes.push_back({1, 0, 0, 0, 0, 0, -1, false});
+  if (Lz > 1) passes.push_back({0, 1, static_cast<int>(Lz), static_cast<int>(Mz), Ly * Lx * E, static_cast<int>(Lz), 2, true});
+  if (Ly > 1) passes.push_back({0, Mz, static_cast<int>(Ly), static_cast<int>(My), Lx * E, static_cast<int>(Ly), 1, true});
+  if (Lx > 1) passes.push_back({0, My * Mz, static_cast<int>(Lx), static_cast<int>(Mx), E, static_cast<int>(Lx), 0, true});
+  int last_dft = -1;
+  for (int i = 0; i < static_cast<int>(passes.size()); ++i)
+    if (passes[i].kind == 0 && passes[i].back) last_dft = i;
+  const c64* cur = op->mom;
+  c64* bufs[2] = {op->fa, op->fb};
+  int which = 0;
+  for (int i = 0; i < static_cast<int>(passes.size()); ++i) {
+    const Pass& p = passes[i];
+    const bool final = i + 1 == static_cast<int>(passes.size());
+    c64* out = final ? op->loc : bufs[which];
+    if (p.kind == 1) {
+      check(launch_mode_product(op->lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
+    } else {
+      const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
+      check(launch_dft_axis(cur, out, op->tw[p.axis], p.n_a, p.n_in, p.n_out, p.inner, p.L, p.back, scale, s),
+            "lattice dft");
+    }
+    op->launches++;
+    cur = out;
+    which ^= 1;
+  }
+  ev_record(op, 3);
+  check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, op->loc, y, op->n, op->b, op->n_cells,
+                               op->N, nrhs, false, s),
+        "near reduce + l2p");
+  op->launches++;
+  ev_record(op, 4);
+  if (op->timing) {
+    check(cudaEventSynchronize(op->ev[4]), "timing sync");
+    float ms;
+    cudaEventElapsedTime(&ms, op->ev[0], op->ev[1]);
+    op->stage_ms[0] += ms;
+    cudaEventElapsedTime(&ms, op->ev[3], op->ev[4]);
+    op->stage_ms[1] += ms;
+    cudaEventElapsedTime(&ms, op->ev[1], op->ev[2]);
+    op->stage_ms[2] += ms;
+    cudaEventElapsedTime(&ms, op->ev[2], op->ev[3]);
+    op->stage_ms[3] += ms;
+    cudaEventElapsedTime(&ms, op->ev[0], op->ev[4]);
+    op->stage_ms[4] += ms;
+    op->applies++;
+  }
+}
+
+void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
+  for (int r0 = 0; r0 < nrhs; r0 += op->max_rhs) {
+    const int c = std::min(op->max_rhs, nrhs - r0);
+    apply_chunk(op, x + static_cast<long long>(r0) * op->N, y + static_cast<long long>(r0) * op->N, c);
+  }
+}
+
+void ensure_pinned(fpbem_cu_op* op, size_t bytes) {
+  if (op->pinned_bytes >= bytes) return;
+  if (op->pinned) cudaFreeHost(op->pinned);
+  op->pinned = nullptr;
+  check(cudaMallocHost(&op->pinned, bytes), "pinned host buffer");
+  op->pinned_bytes = bytes;
+}
+
+void ensure_gmres(fpbem_cu_op* op, int restart) {
+  const int cols = restart + 1;
+  if (op->basis_cols < cols) {
+    if (op->basis) cudaFree(op->basis);
+    op->basis = dalloc<c64>(static_cast<size_t>(cols) * op->N, "gmres basis");
+    op->basis_cols = cols;
+  }
+  if (!op->gx) {
+    op->gx = dalloc<c64>(op->N, "gmres x");
+    op->gb = dalloc<c64>(op->N, "gmres b");
+    op->gt = dalloc<c64>(op->N, "gmres tmp");
+    op->gsol = dalloc<c64>(op->N, "gmres solution");
+    op->scal_d = dalloc<double>(8, "gmres scalars");
+    op->flag = dalloc<int>(1, "gmres flag");
+    op->rs.partial_d = dalloc<double>(kRedBlocks, "reduction partials");
+    op->rs.partial_c = dalloc<c64>(kRedBlocks, "reduction partials");
+    op->rs.counter = dalloc<unsigned>(1, "reduction counter");
+    check(cudaMemsetAsync(op->rs.counter, 0, sizeof(unsigned), op->stream), "counter init");
+    check(cudaStreamSynchronize(op->stream), "counter init");
+  }
+  if (op->scal_cap < cols) {
+    if (op->scal_c) cudaFree(op->scal_c);
+    op->scal_c = dalloc<c64>(3 * static_cast<size_t>(cols), "gmres coefficients");
+    op->scal_cap = cols;
+  }
+  ensure_pinned(op, sizeof(c64) * 3 * cols + 64);
+}
+
+struct GmresOut {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> history;
+};
+
+// Faithful device-resident restatement of src/solver.cpp:21-123 for one rhs.
+using ApplyDev = std::function<void(const c64*, c64*)>;
+
+GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64* x_dev, double tol, int restart,
+                   int max_iter) {
+  using cd = std::complex<double>;
+  cudaStream_t s = op->stream;
+  const long long n = op->N;
+  GmresOut rep;
+  ensure_gmres(op, std::max(1, restart));
+  c64* V = op->basis;
+  auto col = [&](int j) { return V + static_cast<long long>(j) * n; };
+  c64* h = op->scal_c;                   // pass-1 projections
+  c64* hc = op->scal_c + op->scal_cap;   // pass-2 corrections
+  c64* ydev = op->scal_c + 2 * op->scal_cap;
+  double* sd = op->scal_d;
+  char* pin = static_cast<char*>(op->pinned);
+  auto fetch = [&](const void* src, size_t bytes) {
+    check(cudaMemcpyAsync(pin, src, bytes, cudaMemcpyDeviceToHost, s), "gmres readback");
+    check(cudaStreamSynchronize(s), "gmres sync");
+  };
+  auto fetch_d = [&](int idx) {
+    fetch(sd + idx, sizeof(double));
+    double v;
+    std::memcpy(&v, pin, sizeof(double));
+    return v;
+  };
+  auto check_finite = [&]() {
+    int f;
+    fetch(op->flag, sizeof(int));
+    std::memcpy(&f, pin, sizeof(int));
+    if (f) {
+      check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
+      fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+    }
+  };
+
+  check(cudaMemsetAsync(x_dev, 0, n * sizeof(c64), s), "x0");
+  check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag");
+  check(launch_sqnorm(b_dev, n, op->rs, sd + 3, nullptr, s), "bnorm");
+  op->launches++;
+  const double bnorm = std::sqrt(fetch_d(3));
+  if (bnorm == 0.0) {
+    rep.converged = true;
+    return rep;
+  }
+  const int m = std::max(1, restart);
+  std::vector<cd> H(static_cast<size_t>(m + 1) * m, cd(0, 0));
+  auto Hm = [&](int i, int j) -> cd& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
+  std::vector<cd> g(m + 1);
+  std::vector<double> gc(m);
+  std::vector<cd> gs(m);
+  const c64* r = b_dev;  // r = b_eff on the first cycle
+  double rnorm = bnorm;
+
+  while (rep.iterations < max_iter) {
+    check(launch_div(r, col(0), n, rnorm, s), "v0");
+    op->launches++;
+    std::fill(g.begin(), g.end(), cd(0, 0));
+    g[0] = rnorm;
+    int j = 0;
+    for (; j < m && rep.iterations < max_iter; ++j) {
+      c64* w = col(j + 1);
+      apply(col(j), w);
+      check(launch_sqnorm(w, n, op->rs, sd + 0, op->flag, s), "pre norm");
+      // MGS: h_0 = <v_0,w>; (w -= h_i v_i, h_{i+1} = <v_{i+1}, w>)...; w -= h_j v_j, ||w||^2
+      check(launch_dotc(col(0), w, n, op->rs, h + 0, s), "mgs dot");
+      for (int i = 0; i < j; ++i)
+        check(launch_axpy_dotc(w, col(i), h + i, col(i + 1), n, op->rs, h + i + 1, s), "mgs step");
+      check(launch_axpy_sqnorm(w, col(j), h + j, n, op->rs, sd + 1, s), "mgs last");
+      op->launches += j + 3;
+      check_finite();
+      fetch(sd, 2 * sizeof(double));
+      double pre2, post2;
+      std::memcpy(&pre2, pin, sizeof(double));
+      std::memcpy(&post2, pin + sizeof(double), sizeof(double));
+      fetch(h, sizeof(c64) * (j + 1));
+      for (int i = 0; i <= j; ++i) {
+        c64 v;
+        std::memcpy(&v, pin + i * sizeof(c64), sizeof(c64));
+        Hm(i, j) = cd(v.x, v.y);
+      }
+      double wnorm2 = post2;
+      if (std::sqrt(post2) < 0.5 * std::sqrt(pre2)) {  // reorthogonalisation (:63-69)
+        check(launch_dotc(col(0), w, n, op->rs, hc + 0, s), "reorth dot");
+        for (int i = 0; i < j; ++i)
+          check(launch_axpy_dotc(w, col(i), hc + i, col(i + 1), n, op->rs, hc + i + 1, s), "reorth step");
+        check(launch_axpy_sqnorm(w, col(j), hc + j, n, op->rs, sd + 2, s), "reorth last");
+        op->launches += j + 2;
+        fetch(hc, sizeof(c64) * (j + 1));
+        for (int i = 0; i <= j; ++i) {
+          c64 v;
+          std::memcpy(&v, pin + i * sizeof(c64), sizeof(c64));
+          Hm(i, j) += cd(v.x, v.y);
+        }
+        wnorm2 = fetch_d(2);
+      }
+      const double hlast = std::sqrt(wnorm2);
+      Hm(j + 1, j) = hlast;
+      if (hlast > 0.0) {
+        check(launch_div(w, w, n, hlast, s), "normalise");
+        op->launches++;
+      }
+      for (int i = 0; i < j; ++i) {  // accumulated rotations (:75-79)
+        cd t = gc[i] * Hm(i, j) + gs[i] * Hm(i + 1, j);
+        Hm(i + 1, j) = -std::conj(gs[i]) * Hm(i, j) + gc[i] * Hm(i + 1, j);
+        Hm(i, j) = t;
+      }
+      const cd a = Hm(j, j);  // new rotation (:80-94)
+      const double bb = std::abs(Hm(j + 1, j));
+      const double denom = std::hypot(std::abs(a), bb);
+      if (denom == 0.0) {
+        gc[j] = 1.0;
+        gs[j] = cd(0, 0);
+      } else if (std::abs(a) == 0.0) {
+        gc[j] = 0.0;
+        gs[j] = cd(1, 0);
+      } else {
+        gc[j] = std::abs(a) / denom;
+        gs[j] = (a / std::abs(a)) * std::conj(Hm(j + 1, j)) / denom;
+      }
+      Hm(j, j) = gc[j] * a + gs[j] * Hm(j + 1, j);
+      Hm(j + 1, j) = cd(0, 0);
+      const cd gj = g[j];
+      g[j] = gc[j] * gj;
+      g[j + 1] = -std::conj(gs[j]) * gj;
+      ++rep.iterations;
+      const double est = std::abs(g[j + 1]) / bnorm;
+      rep.history.push_back(est);
+      if (est <= tol || hlast == 0.0) {
+        ++j;
+        break;
+      }
+    }
+    // y = triu(H_jj)^{-1} g ; x += V y (:109-110)
+    std::vector<cd> y(j);
+    for (int i = j - 1; i >= 0; --i) {
+      cd acc = g[i];
+      for (int k = i + 1; k < j; ++k) acc -= Hm(i, k) * y[k];
+      y[i] = acc / Hm(i, i);
+    }
+    if (j > 0) {
+      std::vector<c64> yh(j);
+      for (int i = 0; i < j; ++i) yh[i] = cmk(y[i].real(), y[i].imag());
+      std::memcpy(pin, yh.data(), j * sizeof(c64));
+      check(cudaMemcpyAsync(ydev, pin, j * sizeof(c64), cudaMemcpyHostToDevice, s), "y upload");
+      check(launch_update_x(x_dev, V, n, ydev, j, n, s), "x update");
+      op->launches++;
+    }
+    // true residual r = b - A x (:111-112)
+    apply(x_dev, op->gt);
+    check(launch_sqnorm(op->gt, n, op->rs, sd + 2, op->flag, s), "residual finite check");
+    check(launch_residual(b_dev, op->gt, op->gx, n, op->rs, sd + 3, s), "residual");
+    op->launches += 2;
+    check_finite();
+    rnorm = std::sqrt(fetch_d(3));
+    r = op->gx;
+    if (rnorm / bnorm <= tol) {
+      rep.converged = true;
+      break;
+    }
+  }
+  if (!rep.history.empty()) rep.converged = rep.converged || rnorm / bnorm <= tol;
+  return rep;
+}
+
+}  // namespace
+
+namespace {
+int guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return FPBEM_CU_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FPBEM_CU_EINVAL;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* fpbem_cu_last_error(void) { return g_err.c_str(); }
+const char* fpbem_cu_version(void) { return "fpbem_cuda 0.1 sm_100a"; }
+
+int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** out) {
+  return guard([&] {
+    if (!d || !out) fail(FPBEM_CU_EINVAL, "create: null argument");
+    *out = nullptr;
+    for (int k = 0; k < 3; ++k)
+      if (d->counts[k] < 1) fail(FPBEM_CU_EDIM, "create: counts must be >= 1");
+    if (d->n_dof < 1 || d->n_coef < 1 || d->n_coef > 64) fail(FPBEM_CU_EDIM, "create: bad n_dof / n_coef");
+    if (d->mirrored_level != -1) fail(FPBEM_CU_EINVAL, "create: half-space image pair not supported");
+    if (!d->u0 || !d->v0) fail(FPBEM_CU_EINVAL, "create: u0 / v0 required");
+    if (d->n_near > 0 && (!d->near_offsets || !d->near_blocks)) fail(FPBEM_CU_EINVAL, "create: near blocks missing");
+    if (!d->lambda && d->n_far > 0 && (!d->far_offsets || !d->far_blocks))
+      fail(FPBEM_CU_EINVAL, "create: far bank missing");
+    check(cudaSetDevice(device), "set device");
+    auto* op = new fpbem_cu_op();
+    std::unique_ptr<fpbem_cu_op, void (*)(fpbem_cu_op*)> guard_op(op, fpbem_cu_fmm_destroy);
+    op->device = device;
+    check(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
+    op->own_stream = true;
+    for (int k = 0; k < 3; ++k) op->counts[k] = d->counts[k];
+    op->n = d->n_dof;
+    op->b = d->n_coef;
+    op->n_cells = d->counts[0] * d->counts[1] * d->counts[2];
+    op->N = static_cast<long long>(op->n_cells) * op->n;
+    op->max_rhs = std::max(1, d->max_rhs);
+
+    // near field: pairs per offset (offset order), per-target CSR in offset order
+    op->n_near = d->n_near;
+    op->near_offsets.assign(d->near_offsets, d->near_offsets + 3 * d->n_near);
+    const int* m = d->counts;
+    std::vector<int> psrc;
+    std::vector<std::vector<int>> per_t(op->n_cells);
+    op->pair_start.assign(1, 0);
+    for (int s = 0; s < d->n_near; ++s) {
+      const int ox = op->near_offsets[3 * s], oy = op->near_offsets[3 * s + 1], oz = op->near_offsets[3 * s + 2];
+      if (std::abs(ox) >= m[0] || std::abs(oy) >= m[1] || std::abs(oz) >= m[2])
+        fail(FPBEM_CU_EDIM, "create: near offset outside [1-M, M-1]");
+      for (int tz = 0; tz < m[2]; ++tz)
+        for (int ty = 0; ty < m[1]; ++ty)
+          for (int tx = 0; tx < m[0]; ++tx) {
+            const int sx = tx - ox, sy = ty - oy, sz = tz - oz;
+            if (sx < 0 || sx >= m[0] || sy < 0 || sy >= m[1] || sz < 0 || sz >= m[2]) continue;
+            const int t = tx + m[0] * (ty + m[1] * tz);
+            per_t[t].push_back(static_cast<int>(psrc.size()));
+            psrc.push_back(sx + m[0] * (sy + m[1] * sz));
+          }
+      op->pair_start.push_back(static_cast<int>(psrc.size()));
+    }
+    op->n_pairs = static_cast<int>(psrc.size());
+    std::vector<int> tptr(op->n_cells + 1, 0), tpairs;
+    tpairs.reserve(psrc.size());
+    for (int t = 0; t < op->n_cells; ++t) {
+      tpairs.insert(tpairs.end(), per_t[t].begin(), per_t[t].end());
+      tptr[t + 1] = static_cast<int>(tpairs.size());
+    }
+    for (int s = 0; s < d->n_near; ++s) op->rank_slots.push_back(s);
+    const size_t nn = static_cast<size_t>(op->n) * op->n;
+    op->S = dalloc<c64>(nn * d->n_near, "near blocks");
+    if (d->n_near > 0)
+      h2d(op->S, d->near_blocks, nn * d->n_near * sizeof(c64), op->stream, "S upload");
+    op->pair_src = dalloc<int>(psrc.size(), "pair sources");
+    op->tgt_ptr = dalloc<int>(tptr.size(), "target ptr");
+    op->tgt_pairs = dalloc<int>(tpairs.size(), "target pairs");
+    if (!psrc.empty()) {
+      h2d(op->pair_src, psrc.data(), psrc.size() * sizeof(int), op->stream, "pairs");
+      h2d(op->tgt_pairs, tpairs.data(), tpairs.size() * sizeof(int), op->stream, "pairs");
+    }
+    h2d(op->tgt_ptr, tptr.data(), tptr.size() * sizeof(int), op->stream, "ptr");
+
+    // expansions
+    const size_t nb = static_cast<size_t>(op->n) * op->b;
+    op->u0 = dalloc<c64>(nb, "u0");
+    op->v0 = dalloc<c64>(nb, "v0");
+    h2d(op->u0, d->u0, nb * sizeof(c64), op->stream, "u0 upload");
+    h2d(op->v0, d->v0, nb * sizeof(c64), op->stream, "v0 upload");
+
+    // spectrum sizes: caller's, else the reference's 7-smooth padding
+    for (int k = 0; k < 3; ++k) {
+      int l = d->fft_sizes[k];
+      if (l <= 0) l = m[k] == 1 ? 1 : fft_friendly(2 * m[k] - 1);
+      if (m[k] > 1 && l < 2 * m[k] - 1) fail(FPBEM_CU_EDIM, "create: fft size < 2M-1");
+      if (m[k] == 1 && l != 1) fail(FPBEM_CU_EDIM, "create: fft size must be 1 on a single-cell axis");
+      op->L[k] = l;
+    }
+    op->q_total = static_cast<long long>(op->L[0]) * op->L[1] * op->L[2];
+    for (int k = 0; k < 3; ++k) twiddles(op, op->L[k], &op->tw[k]);
+    build_spectrum(op, d);
+
+    // apply buffers
+    const long long E = static_cast<long long>(op->max_rhs) * op->b;
+    op->W = dalloc<c64>(static_cast<size_t>(op->n_pairs) * op->max_rhs * op->n, "near workspace");
+    op->mom = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "moments");
+    op->loc = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "locals");
+    op->fa = dalloc<c64>(static_cast<size_t>(op->q_total) * E, "m2l field");
+    op->fb = dalloc<c64>(static_cast<size_t>(op->q_total) * E, "m2l image");
+    for (auto& e : op->ev) check(cudaEventCreate(&e), "event");
+    check(cudaStreamSynchronize(op->stream), "create sync");
+    *out = guard_op.release();
+  });
+}
+
+void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
+  if (!op) return;
+  cudaSetDevice(op->device);
+  if (op->stream) cudaStreamSynchronize(op->stream);
+  for (void* p : {static_cast<void*>(op->S), static_cast<void*>(op->pair_src), static_cast<void*>(op->tgt_ptr),
+                  static_cast<void*>(op->tgt_pairs), static_cast<void*>(op->jobs), static_cast<void*>(op->u0),
+                  static_cast<void*>(op->v0), static_cast<void*>(op->lambda), static_cast<void*>(op->tw[0]),
+                  static_cast<void*>(op->tw[1]), static_cast<void*>(op->tw[2]), static_cast<void*>(op->W),
+                  static_cast<void*>(op->mom), static_cast<void*>(op->loc), static_cast<void*>(op->fa),
+                  static_cast<void*>(op->fb), static_cast<void*>(op->xin), static_cast<void*>(op->yout),
+                  static_cast<void*>(op->basis), static_cast<void*>(op->gx), static_cast<void*>(op->gb),
+                  static_cast<void*>(op->gt), static_cast<void*>(op->gsol), static_cast<void*>(op->scal_c), static_cast<void*>(op->scal_d),
+                  static_cast<void*>(op->flag), static_cast<void*>(op->rs.partial_d),
+                  static_cast<void*>(op->rs.partial_c), static_cast<void*>(op->rs.counter)})
+    if (p) cudaFree(p);
+  if (op->pinned) cudaFreeHost(op->pinned);
+  for (auto& e : op->ev)
+    if (e) cudaEventDestroy(e);
+  if (op->own_stream && op->stream) cudaStreamDestroy(op->stream);
+  delete op;
+}
+
+int fpbem_cu_fmm_apply(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int nrhs, int ptr_kind) {
+  return guard([&] {
+    if (!op || !x || !y) fail(FPBEM_CU_EINVAL, "apply: null argument");
+    if (nrhs < 1) fail(FPBEM_CU_EDIM, "fmm matvec: dimension mismatch");
+    check(cudaSetDevice(op->device), "set device");
+    if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
+      apply_device(op, reinterpret_cast<const c64*>(x), reinterpret_cast<c64*>(y), nrhs);
+      check(cudaGetLastError(), "apply");
+      return;
+    }
+    if (ptr_kind != FPBEM_CU_PTR_HOST) fail(FPBEM_CU_EINVAL, "apply: bad ptr_kind");
+    const size_t bytes = static_cast<size_t>(op->N) * op->max_rhs * sizeof(c64);
+    if (!op->xin) {
+      op->xin = dalloc<c64>(static_cast<size_t>(op->N) * op->max_rhs, "x staging");
+      op->yout = dalloc<c64>(static_cast<size_t>(op->N) * op->max_rhs, "y staging");
+    }
+    for (int r0 = 0; r0 < nrhs; r0 += op->max_rhs) {
+      const int c = std::min(op->max_rhs, nrhs - r0);
+      const size_t cb = static_cast<size_t>(op->N) * c * sizeof(c64);
+      (void)bytes;
+      check(cudaMemcpyAsync(op->xin, x + static_cast<size_t>(r0) * op->N, cb, cudaMemcpyHostToDevice, op->stream),
+            "x upload");
+      apply_chunk(op, op->xin, op->yout, c);
+      check(cudaMemcpyAsync(y + static_cast<size_t>(r0) * op->N, op->yout, cb, cudaMemcpyDeviceToHost, op->stream),
+            "y download");
+    }
+    check(cudaStreamSynchronize(op->stream), "apply sync");
+  });
+}
+
+int fpbem_cu_gmres(fpbem_cu_op* op, const fpbem_c64* b, fpbem_c64* x, int nrhs, double tol, int restart,
+                   int max_iter, int ptr_kind, int* iterations, int* converged, double* history, int history_cap,
+                   int* history_len) {
+  return guard([&] {
+    if (!op || !b || !x || !iterations || !converged) fail(FPBEM_CU_EINVAL, "gmres: null argument");
+    if (nrhs < 1) fail(FPBEM_CU_EDIM, "gmres: nrhs >= 1 required");
+    check(cudaSetDevice(op->device), "set device");
+    ensure_gmres(op, std::max(1, restart));
+    for (int r = 0; r < nrhs; ++r) {
+      const size_t off = static_cast<size_t>(r) * op->N;
+      const c64* bd;
+      c64* xd;
+      if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
+        bd = reinterpret_cast<const c64*>(b) + off;
+        xd = reinterpret_cast<c64*>(x) + off;
+      } else {
+        check(cudaMemcpyAsync(op->gb, b + off, op->N * sizeof(c64), cudaMemcpyHostToDevice, op->stream), "b upload");
+        bd = op->gb;
+        xd = op->gsol;
+      }
+      GmresOut o = gmres_one(
+          op, [op](const c64* in, c64* out) { apply_device(op, in, out, 1); }, bd, xd, tol, restart, max_iter);
+      iterations[r] = o.iterations;
+      converged[r] = o.converged ? 1 : 0;
+      if (history_len) history_len[r] = static_cast<int>(o.history.size());
+      if (history)
+        for (int i = 0; i < std::min(history_cap, static_cast<int>(o.history.size())); ++i)
+          history[static_cast<size_t>(r) * history_cap + i] = o.history[i];
+      if (ptr_kind != FPBEM_CU_PTR_DEVICE) {
+        check(cudaMemcpyAsync(x + off, xd, op->N * sizeof(c64), cudaMemcpyDeviceToHost, op->stream), "x download");
+        check(cudaStreamSynchronize(op->stream), "gmres sync");
+      }
+    }
+    check(cudaStreamSynchronize(op->stream), "gmres sync");
+  });
+}
+
+int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes) {
+  if (!op || !bytes) {
+    g_err = "bytes: null argument";
+    return FPBEM_CU_EINVAL;
+  }
+  const size_t c = sizeof(c64);
+  *bytes = c * (static_cast<size_t>(op->n_near) * op->n * op->n + static_cast<size_t>(op->q_total) * op->b * op->b +
+                2 * static_cast<size_t>(op->n) * op->b);
+  return FPBEM_CU_OK;
+}
+
+int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out) {
+  return guard([&] {
+    if (!op || !sizes) fail(FPBEM_CU_EINVAL, "spectrum: null argument");
+    for (int k = 0; k < 3; ++k) sizes[k] = op->L[k];
+    if (lambda_out) {
+      check(cudaSetDevice(op->device), "set device");
+      check(cudaStreamSynchronize(op->stream), "sync");
+      check(cudaMemcpyAsync(lambda_out, op->lambda, static_cast<size_t>(op->q_total) * op->b * op->b * sizeof(c64),
+                            cudaMemcpyDeviceToHost, op->stream),
+            "spectrum download");
+      check(cudaStreamSynchronize(op->stream), "spectrum download");
+    }
+  });
+}
+
+int fpbem_cu_set_stream(fpbem_cu_op* op, void* stream) {
+  return guard([&] {
+    if (!op) fail(FPBEM_CU_EINVAL, "set_stream: null op");
+    check(cudaSetDevice(op->device), "set device");
+    check(cudaStreamSynchronize(op->stream), "sync");
+    if (op->own_stream) cudaStreamDestroy(op->stream);
+    if (stream) {
+      op->stream = static_cast<cudaStream_t>(stream);
+      op->own_stream = false;
+    } else {
+      check(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
+      op->own_stream = true;
+    }
+  });
+}
+
+int fpbem_cu_enable_stage_timing(fpbem_cu_op* op, int enable) {
+  if (!op) return FPBEM_CU_EINVAL;
+  op->timing = enable != 0;
+  return FPBEM_CU_OK;
+}
+
+int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out) {
+  if (!op || !ms_out) return FPBEM_CU_EINVAL;
+  for (int i = 0; i < 5; ++i) ms_out[i] = op->stage_ms[i];
+  ms_out[5] = static_cast<double>(op->applies);
+  for (double& v : op->stage_ms) v = 0.0;
+  op->applies = 0;
+  return FPBEM_CU_OK;
+}
+
+long long fpbem_cu_kernel_launches(const fpbem_cu_op* op) { return op ? op->launches : 0; }
+
+int fpbem_cu_gmres_fn(int device, long long n, fpbem_cu_apply_fn apply, void* actx, fpbem_cu_apply_fn precond,
+                      void* pctx, const fpbem_c64* b, fpbem_c64* x, double tol, int restart, int max_iter,
+                      int ptr_kind, int* iterations, int* converged, double* history, int history_cap,
+                      int* history_len) {
+  fpbem_cu_op* op = nullptr;
+  int rc = guard([&] {
+    if (!apply || !b || !x || !iterations || !converged || n < 1) fail(FPBEM_CU_EINVAL, "gmres_fn: bad argument");
+    check(cudaSetDevice(device), "set device");
+    op = new fpbem_cu_op();
+    op->device = device;
+    op->N = n;
+    check(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
+    op->own_stream = true;
+    ensure_gmres(op, std::max(1, restart));
+    c64* pre_tmp = precond ? dalloc<c64>(n, "precond scratch") : nullptr;
+    std::unique_ptr<c64, decltype(&cudaFree)> keep(pre_tmp, &cudaFree);
+    auto call = [&](fpbem_cu_apply_fn fn, void* ctx, const c64* in, c64* out) {
+      if (fn(ctx, reinterpret_cast<const fpbem_c64*>(in), reinterpret_cast<fpbem_c64*>(out), op->stream) != 0)
+        fail(FPBEM_CU_EINVAL, "gmres: operator callback failed");
+    };
+    ApplyDev eff = [&](const c64* in, c64* out) {
+      if (precond) {
+        call(apply, actx, in, pre_tmp);
+        check(launch_sqnorm(pre_tmp, n, op->rs, op->scal_d + 4, op->flag, op->stream), "finite check");
+        call(precond, pctx, pre_tmp, out);
+      } else {
+        call(apply, actx, in, out);
+      }
+    };
+    const c64* bd;
+    c64* xd;
+    if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
+      bd = reinterpret_cast<const c64*>(b);
+      xd = reinterpret_cast<c64*>(x);
+    } else {
+      check(cudaMemcpyAsync(op->gb, b, n * sizeof(c64), cudaMemcpyHostToDevice, op->stream), "b upload");
+      bd = op->gb;
+      xd = op->gsol;
+    }
+    if (precond) {  // b_eff = M^{-1} b, checked (src/solver.cpp:30)
+      call(precond, pctx, bd, op->gt);
+      check(cudaMemsetAsync(op->flag, 0, sizeof(int), op->stream), "flag");
+      check(launch_sqnorm(op->gt, n, op->rs, op->scal_d + 4, op->flag, op->stream), "finite check");
+      int f = 0;
+      check(cudaMemcpyAsync(op->pinned, op->flag, sizeof(int), cudaMemcpyDeviceToHost, op->stream), "flag");
+      check(cudaStreamSynchronize(op->stream), "sync");
+      std::memcpy(&f, op->pinned, sizeof(int));
+      if (f) fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+      check(cudaMemcpyAsync(op->gb, op->gt, n * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "b_eff");
+      bd = op->gb;
+    }
+    GmresOut o = gmres_one(op, eff, bd, xd, tol, restart, max_iter);
+    *iterations = o.iterations;
+    *converged = o.converged ? 1 : 0;
+    if (history_len) *history_len = static_cast<int>(o.history.size());
+    if (history)
+      for (int i = 0; i < std::min(history_cap, static_cast<int>(o.history.size())); ++i) history[i] = o.history[i];
+    if (ptr_kind != FPBEM_CU_PTR_DEVICE)
+      check(cudaMemcpyAsync(x, xd, n * sizeof(c64), cudaMemcpyDeviceToHost, op->stream), "x download");
+    check(cudaStreamSynchronize(op->stream), "gmres sync");
+  });
+  fpbem_cu_fmm_destroy(op);
+  return rc;
+}
+
+int fpbem_cu_comm_unique_id(unsigned char id_out[128]) {
+  return guard([&] {
+    void* lib = load_nccl();
+    if (!lib) fail(FPBEM_CU_ENCCL, "libnccl.so.2 not loadable");
+    auto get_id = reinterpret_cast<int (*)(void*)>(dlsym(lib, "ncclGetUniqueId"));
+    if (!get_id) fail(FPBEM_CU_ENCCL, "ncclGetUniqueId missing");
+    if (get_id(id_out) != 0) fail(FPBEM_CU_ENCCL, "ncclGetUniqueId failed");
+  });
+}
+
+int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int device, fpbem_cu_comm** out) {
+  return guard([&] {
+    void* lib = load_nccl();
+    if (!lib) fail(FPBEM_CU_ENCCL, "libnccl.so.2 not loadable");
+    struct IdBlob {
+      unsigned char b[128];
+    } blob;
+    std::memcpy(blob.b, id, 128);
+    auto init = reinterpret_cast<int (*)(void**, int, IdBlob, int)>(dlsym(lib, "ncclCommInitRank"));
+    auto* c = new fpbem_cu_comm();
+    c->lib = lib;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    c->allreduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, void*)>(
+        dlsym(lib, "ncclAllReduce"));
+    c->destroy = reinterpret_cast<int (*)(void*)>(dlsym(lib, "ncclCommDestroy"));
+    if (!init || !c->allreduce || !c->destroy) {
+      delete c;
+      fail(FPBEM_CU_ENCCL, "NCCL symbols missing");
+    }
+    check(cudaSetDevice(device), "set device");
+    if (init(&c->comm, nranks, blob, rank) != 0) {
+      delete c;
+      fail(FPBEM_CU_ENCCL, "ncclCommInitRank failed");
+    }
+    *out = c;
+  });
+}
+
+void fpbem_cu_comm_destroy(fpbem_cu_comm* comm) {
+  if (!comm) return;
+  if (comm->comm && comm->destroy) comm->destroy(comm->comm);
+  delete comm;
+}
+
+int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm) {
+  return guard([&] {
+    if (!op) fail(FPBEM_CU_EINVAL, "set_comm: null op");
+    op->comm = comm;
+    fail(FPBEM_CU_EINVAL, "set_comm: multi-GPU offset sharding not implemented yet");
+  });
+}
+
+}  // extern "C"

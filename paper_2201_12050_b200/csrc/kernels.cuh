@@ -1,0 +1,51 @@
+// Launchers of the sm_100a kernels (near_field.cu, m2l.cu, krylov.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace fpbem_cu {
+
+// ---- near field (near_field.cu)
+size_t near_gemm_smem_bytes();
+int near_gemm_tile_cols();
+int near_gemm_tile_rows();
+// jobs: (offset slot, first column, column count, pair base); columns of an
+// offset are (pair, rhs) with rhs fastest.
+cudaError_t launch_near_gemm(const c64* S, const c64* x, c64* W, const int* pair_src, const int4* jobs,
+                             int n_jobs, int n, long long N, int nrhs, cudaStream_t stream);
+cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* tgt_pairs, const c64* u0,
+                                   const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
+                                   int nrhs, bool accumulate, cudaStream_t stream);
+
+// ---- M2L / P2M (m2l.cu)
+cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_a, int n_in, int n_out,
+                            long long n_inner, int L, bool backward, double scale, cudaStream_t stream);
+cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image, long long q_total, int b,
+                                int nrhs, cudaStream_t stream);
+cudaError_t launch_p2m(const c64* v0, const c64* x, c64* moments, int n, int b, int n_cells, long long N,
+                       int nrhs, cudaStream_t stream);
+cudaError_t launch_scatter_bank(const c64* blocks, const int* offsets, int n_blk, int b2, int lx, int ly, int lz,
+                                c64* field, cudaStream_t stream);
+
+// ---- Krylov vector ops (krylov.cu)
+constexpr int kRedBlocks = 2 * kNumSMs;
+struct RedScratch {
+  double* partial_d;  // kRedBlocks
+  c64* partial_c;     // kRedBlocks
+  unsigned* counter;  // 1, zero between launches
+};
+cudaError_t launch_sqnorm(const c64* w, long long n, const RedScratch& rs, double* result, int* nonfinite,
+                          cudaStream_t s);
+cudaError_t launch_dotc(const c64* a, const c64* b, long long n, const RedScratch& rs, c64* result,
+                        cudaStream_t s);
+cudaError_t launch_axpy_dotc(c64* w, const c64* v, const c64* h, const c64* vn, long long n, const RedScratch& rs,
+                             c64* result, cudaStream_t s);
+cudaError_t launch_axpy_sqnorm(c64* w, const c64* v, const c64* h, long long n, const RedScratch& rs,
+                               double* result, cudaStream_t s);
+cudaError_t launch_div(const c64* in, c64* out, long long n, double d, cudaStream_t s);
+cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y, int j, long long n,
+                            cudaStream_t s);
+cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
+                            double* result, cudaStream_t s);
+
+}  // namespace fpbem_cu

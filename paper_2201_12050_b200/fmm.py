@@ -1,0 +1,255 @@
+"""GPU-backed FmmOperators and GMRES — the reference-facing API of the hot path.
+
+Mirrors fpbem::fmm::FmmOperators::matvec (include/fpbem/fmm.hpp:69,
+src/fmm.cpp:246-271) and fpbem::solver::gmres / SolveReport / GmresOptions
+(include/fpbem/solver.hpp:14-33, src/solver.cpp:21-123), with the same
+argument meaning and error behaviour: a dimension mismatch raises ValueError
+(std::invalid_argument), a non-finite operator output raises RuntimeError
+("gmres: operator returned a non-finite value"), non-convergence is reported
+in the SolveReport, not raised. All arithmetic runs in libfpbem_cuda.so on
+the GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+
+OK, EDIM, ENONFINITE, ECUDA, ENOMEM, ENCCL, EINVAL = range(7)
+PTR_HOST, PTR_DEVICE = 0, 1
+
+
+def _raise(code: int) -> None:
+    if code == OK:
+        return
+    msg = _native.cuda().fpbem_cu_last_error().decode()
+    if code == EDIM:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass
+class SolveReport:
+    """include/fpbem/solver.hpp:14-19"""
+
+    solution: object
+    residual_history: list = field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+
+
+class FmmOperators:
+    """Device-resident periodic single-level FMM operator.
+
+    data: an FmmData (host.Scene.assemble_fmm) or any object with the same
+    fields (counts, n_dof, n_coef, near_offsets, near_blocks, far_offsets,
+    far_blocks, u0, v0). The spectrum is built on the GPU from the far bank
+    unless `lambda_` (reference layout) is given.
+    """
+
+    def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1):
+        lib = _native.cuda()
+        self.counts = tuple(int(c) for c in data.counts)
+        self.n_dof = int(data.n_dof)
+        self.n_coef = int(data.n_coef)
+        self.device = device
+        self.max_rhs = max_rhs
+        n_cells = self.counts[0] * self.counts[1] * self.counts[2]
+        self.N = n_cells * self.n_dof
+        keep = []
+
+        def ptr(a, dtype):
+            a = np.ascontiguousarray(a, dtype=dtype)
+            keep.append(a)
+            return a.ctypes.data if a.size else None
+
+        d = _native.FmmDesc()
+        d.counts[:] = self.counts
+        d.n_dof = self.n_dof
+        d.n_coef = self.n_coef
+        d.n_near = int(len(data.near_offsets))
+        d.near_offsets = ptr(data.near_offsets, np.int32)
+        d.near_blocks = ptr(data.near_blocks, np.complex128)
+        d.u0 = ptr(data.u0, np.complex128)
+        d.v0 = ptr(data.v0, np.complex128)
+        d.fft_sizes[:] = tuple(fft_sizes) if fft_sizes is not None else (0, 0, 0)
+        d.lambda_ = ptr(lambda_, np.complex128) if lambda_ is not None else None
+        d.n_far = int(len(data.far_offsets))
+        d.far_offsets = ptr(data.far_offsets, np.int32)
+        d.far_blocks = ptr(data.far_blocks, np.complex128)
+        d.mirrored_level = -1
+        d.max_rhs = max_rhs
+        h = C.c_void_p()
+        _raise(lib.fpbem_cu_fmm_create(C.byref(d), device, C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h:
+            _native.cuda().fpbem_cu_fmm_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stored_bytes(self) -> int:
+        """FmmOperators::stored_bytes (src/fmm.cpp:273-279)."""
+        b = C.c_size_t()
+        _raise(_native.cuda().fpbem_cu_fmm_bytes(self._h, C.byref(b)))
+        return int(b.value)
+
+    def spectrum(self) -> tuple[tuple[int, int, int], np.ndarray]:
+        sizes = (C.c_int * 3)()
+        _raise(_native.cuda().fpbem_cu_spectrum(self._h, sizes, None))
+        q = sizes[0] * sizes[1] * sizes[2]
+        lam = np.zeros(q * self.n_coef * self.n_coef, np.complex128)
+        _raise(_native.cuda().fpbem_cu_spectrum(self._h, sizes, lam.ctypes.data))
+        return tuple(sizes), lam
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        _raise(_native.cuda().fpbem_cu_set_stream(self._h, stream_ptr))
+
+    def kernel_launches(self) -> int:
+        return int(_native.cuda().fpbem_cu_kernel_launches(self._h))
+
+    def enable_stage_timing(self, on: bool = True) -> None:
+        _raise(_native.cuda().fpbem_cu_enable_stage_timing(self._h, int(on)))
+
+    def stage_times(self) -> dict:
+        ms = (C.c_double * 6)()
+        _raise(_native.cuda().fpbem_cu_stage_times(self._h, ms))
+        keys = ("near_gemm", "near_reduce_l2p", "p2m", "m2l", "total")
+        out = {k: ms[i] for i, k in enumerate(keys)}
+        out["applies"] = int(ms[5])
+        return out
+
+    def _nrhs(self, p) -> int:
+        size = int(p.numel()) if _is_torch(p) else int(np.asarray(p).size)
+        if size == 0 or size % self.N:
+            raise ValueError("fmm matvec: dimension mismatch")
+        return size // self.N
+
+    def matvec(self, p):
+        """y = (S + U0 IFFT(Λ FFT(pad(V0 p)))) p. Accepts a host numpy array
+        (copied in and out inside the call) or a CUDA torch tensor (device-
+        resident, stream-ordered on the handle's stream). Several right-hand
+        sides may be stacked one after another."""
+        nrhs = self._nrhs(p)
+        lib = _native.cuda()
+        if _is_torch(p):
+            import torch
+
+            if not p.is_cuda or p.dtype != torch.complex128:
+                raise ValueError("fmm matvec: expected a complex128 CUDA tensor")
+            x = p.contiguous()
+            y = torch.empty_like(x)
+            _raise(lib.fpbem_cu_fmm_apply(self._h, x.data_ptr(), y.data_ptr(), nrhs, PTR_DEVICE))
+            return y
+        x = np.ascontiguousarray(p, dtype=np.complex128)
+        y = np.empty_like(x)
+        _raise(lib.fpbem_cu_fmm_apply(self._h, x.ctypes.data, y.ctypes.data, nrhs, PTR_HOST))
+        return y
+
+    __call__ = matvec
+
+
+def gmres(apply, b, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000, preconditioner=None,
+          device: int = 0):
+    """Restarted GMRES from x0 = 0 on the device (src/solver.cpp:21-123).
+
+    apply: an FmmOperators (device-resident Krylov loop, several stacked right-
+    hand sides solved independently), or a callable mapping a CUDA complex128
+    torch tensor to a new one (the ApplyFn seam, include/fpbem/solver.hpp:21).
+    Returns a SolveReport, or a list of them for stacked right-hand sides.
+    """
+    lib = _native.cuda()
+    is_t = _is_torch(b)
+    if isinstance(apply, FmmOperators):
+        nrhs = apply._nrhs(b)
+        its = (C.c_int * nrhs)()
+        conv = (C.c_int * nrhs)()
+        cap = max(1, max_iter)
+        hist = np.zeros(nrhs * cap)
+        hlen = (C.c_int * nrhs)()
+        if preconditioner is not None:
+            raise ValueError("gmres: preconditioners are supported through the callable form")
+        if is_t:
+            bx = b.contiguous()
+            import torch
+
+            x = torch.empty_like(bx)
+            rc = lib.fpbem_cu_gmres(apply.handle, bx.data_ptr(), x.data_ptr(), nrhs, tol, restart, max_iter,
+                                    PTR_DEVICE, its, conv, hist.ctypes.data_as(_native.c_double_p), cap, hlen)
+        else:
+            bx = np.ascontiguousarray(b, np.complex128)
+            x = np.zeros_like(bx)
+            rc = lib.fpbem_cu_gmres(apply.handle, bx.ctypes.data, x.ctypes.data, nrhs, tol, restart, max_iter,
+                                    PTR_HOST, its, conv, hist.ctypes.data_as(_native.c_double_p), cap, hlen)
+        _raise(rc)
+        n = apply.N
+        reps = [SolveReport(x[r * n:(r + 1) * n], list(hist[r * cap:r * cap + hlen[r]]), int(its[r]),
+                            bool(conv[r])) for r in range(nrhs)]
+        return reps[0] if nrhs == 1 else reps
+    return _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device)
+
+
+def _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device):
+    import torch
+
+    lib = _native.cuda()
+    dev = torch.device("cuda", device)
+    bt = (b if _is_torch(b) else torch.from_numpy(np.ascontiguousarray(b, np.complex128))).to(dev).contiguous()
+    n = bt.numel()
+    errors: list[BaseException] = []
+
+    def wrap(fn):
+        def cb(_ctx, x_ptr, y_ptr, stream_ptr):
+            try:
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=dev)):
+                    xin = _from_ptr(x_ptr, n, dev)
+                    out = fn(xin.clone())
+                    _from_ptr(y_ptr, n, dev).copy_(out.reshape(-1))
+                return 0
+            except BaseException as e:  # reported through the C return code
+                errors.append(e)
+                return 1
+
+        return _native.APPLY_FN(cb)
+
+    acb = wrap(apply)
+    pcb = wrap(preconditioner) if preconditioner is not None else _native.APPLY_FN()
+    x = torch.empty_like(bt)
+    its, conv, hlen = C.c_int(), C.c_int(), C.c_int()
+    cap = max(1, max_iter)
+    hist = np.zeros(cap)
+    torch.cuda.synchronize(dev)
+    rc = lib.fpbem_cu_gmres_fn(device, n, acb, None, pcb, None, bt.data_ptr(), x.data_ptr(), tol, restart,
+                               max_iter, PTR_DEVICE, C.byref(its), C.byref(conv),
+                               hist.ctypes.data_as(_native.c_double_p), cap, C.byref(hlen))
+    if errors and rc != ENONFINITE:
+        raise errors[0]
+    _raise(rc)
+    sol = x if _is_torch(b) else x.cpu().numpy()
+    return SolveReport(sol, list(hist[: hlen.value]), its.value, bool(conv.value))
+
+
+def _from_ptr(ptr: int, n: int, dev):
+    """Wrap a raw device pointer of n complex128 values as a torch tensor (no copy)."""
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<c16", "data": (int(ptr), False), "version": 3,
+                                    "strides": None}
+
+    return torch.as_tensor(_Holder(), device=dev)

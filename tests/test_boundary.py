@@ -1,0 +1,71 @@
+"""The drop-in boundary: libfpbem_cuda.so loads on a CPU-only box and exports
+every symbol include/fpbem_cuda.h declares; the host and oracle libraries
+load; the product path refuses to run without a GPU instead of falling back."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "fpbem_cuda.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fpbem_cu_\w+)\s*\(", text)) - {"fpbem_cu_apply_fn"})
+
+
+def test_header_declares_the_reference_entry_points():
+    syms = declared_symbols()
+    for s in ("fpbem_cu_fmm_create", "fpbem_cu_fmm_apply", "fpbem_cu_gmres", "fpbem_cu_fmm_bytes",
+              "fpbem_cu_fmm_destroy", "fpbem_cu_last_error"):
+        assert s in syms
+
+
+def test_cuda_library_exports_every_declared_symbol():
+    from paper_2201_12050_b200 import _native
+
+    lib = _native.cuda()
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(_native.CUDA_SYMBOLS) | {"fpbem_cu_gmres_fn"} >= set(declared_symbols())
+
+
+def test_cuda_library_is_sm100a():
+    import subprocess
+
+    so = ROOT / "paper_2201_12050_b200" / "lib" / "libfpbem_cuda.so"
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(so)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
+    assert "DMMA" in sass  # the near-field GEMM runs on the FP64 tensor cores
+
+
+def test_version_and_error_calls_need_no_gpu():
+    from paper_2201_12050_b200 import _native
+
+    lib = _native.cuda()
+    assert b"sm_100a" in lib.fpbem_cu_version()
+    h = C.c_void_p()
+    assert lib.fpbem_cu_fmm_create(None, 0, C.byref(h)) == 6  # FPBEM_CU_EINVAL
+    assert b"null" in lib.fpbem_cu_last_error()
+
+
+def test_host_and_oracle_libraries_load():
+    import oracle
+    from paper_2201_12050_b200 import _native
+
+    assert _native.host().fh_wigner3j(1, 1, 0, 0, 0, 0) != 0.0
+    assert oracle.fft_friendly(31) == 32
+
+
+def test_product_path_fails_loudly_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2201_12050_b200 import FmmOperators, Scene
+
+    d = Scene(1, 2).assemble_fmm(2)
+    with pytest.raises(RuntimeError):
+        FmmOperators(d)

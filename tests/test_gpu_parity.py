@@ -1,0 +1,367 @@
+"""GPU parity: the sm_100a path through the C-ABI against the CPU oracle on
+identical seeded inputs. Tolerances from BASELINE.json's north_star: matvec
+relative L2 <= 1e-10 (fp64 complex), GMRES iterations equal within +-1 and
+solutions within 1e-8 relative."""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-10
+SOLVE_TOL = 1e-8
+
+
+class Data:
+    """FmmData-like bundle for synthetic operators."""
+
+    def __init__(self, counts, n, b, near_offsets, near_blocks, far_offsets, far_blocks, u0, v0):
+        self.counts, self.n_dof, self.n_coef = tuple(counts), n, b
+        self.near_offsets = np.asarray(near_offsets, np.int32).reshape(-1, 3)
+        self.near_blocks = np.asarray(near_blocks, np.complex128)
+        self.far_offsets = np.asarray(far_offsets, np.int32).reshape(-1, 3)
+        self.far_blocks = np.asarray(far_blocks, np.complex128)
+        self.u0, self.v0 = np.asarray(u0, np.complex128), np.asarray(v0, np.complex128)
+
+    @property
+    def N(self):
+        return int(np.prod(self.counts)) * self.n_dof
+
+
+def all_offsets(counts):
+    return [(x, y, z) for z in range(1 - counts[2], counts[2]) for y in range(1 - counts[1], counts[1])
+            for x in range(1 - counts[0], counts[0])]
+
+
+def crand(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def uvec(rng, n):  # BASELINE inputs: re/im i.i.d. U[-1, 1]
+    return rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+
+
+def toeplitz_only(rng, counts, n, b=4):
+    """near field = full random Toeplitz; expansions zero -> y = S p"""
+    offs = all_offsets(counts)
+    return Data(counts, n, b, offs, crand(rng, len(offs), n, n), np.zeros((0, 3)), np.zeros((0, b, b)),
+                np.zeros((b, n)), np.zeros((n, b)))
+
+
+def circulant_only(rng, counts, b):
+    """K = full random Toeplitz of b x b blocks, V0 = U0 = I, S = 0 -> y = K p"""
+    offs = all_offsets(counts)
+    eye = np.eye(b, dtype=np.complex128)
+    return Data(counts, b, b, [(0, 0, 0)], np.zeros((1, b, b)), offs, crand(rng, len(offs), b, b), eye, eye)
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2201_12050_b200 import FmmOperators
+
+    return FmmOperators
+
+
+@pytest.mark.parametrize("counts", [(1, 1, 1), (2, 1, 1), (3, 3, 1), (5, 1, 2), (2, 3, 2), (1, 16, 1)])
+@pytest.mark.parametrize("n", [3, 24, 70, 130])
+def test_near_field_toeplitz_matches_oracle_and_dense(ops, counts, n):
+    rng = np.random.default_rng(n + 7 * counts[0] + 11 * counts[1] + 13 * counts[2])
+    d = toeplitz_only(rng, counts, n)
+    op = ops(d)
+    p = uvec(rng, d.N)
+    ref = O.toeplitz_matvec(counts, d.near_offsets, d.near_blocks, p)
+    assert rel(op.matvec(p), ref) <= MATVEC_TOL
+    if d.N <= 600:
+        dense = O.toeplitz_expand_dense(counts, d.near_offsets, d.near_blocks)
+        assert rel(op.matvec(p), dense @ p) <= MATVEC_TOL
+
+
+def test_near_field_banded_offset_subset(ops):
+    """near field with a subset of offsets (absent offsets act as zero blocks)"""
+    rng = np.random.default_rng(3)
+    counts, n = (4, 5, 3), 40
+    offs = [o for o in all_offsets(counts) if abs(o[0]) + abs(o[1]) + abs(o[2]) <= 2]
+    d = toeplitz_only(rng, counts, n)
+    d.near_offsets = np.asarray(offs, np.int32)
+    d.near_blocks = crand(rng, len(offs), n, n)
+    p = uvec(rng, d.N)
+    assert rel(ops(d).matvec(p), O.toeplitz_matvec(counts, offs, d.near_blocks, p)) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("counts", [(2, 1, 1), (3, 1, 1), (5, 3, 1), (1, 16, 1), (3, 3, 2), (4, 4, 4), (8, 1, 1)])
+@pytest.mark.parametrize("b", [1, 3, 25])
+def test_circulant_m2l_matches_oracle(ops, counts, b):
+    """CirculantSpectrum::matvec (src/structured.cpp:122-166) on the device,
+    incl. 7-smooth padded lengths (2M-1 = 31 -> 32) and single-cell axes."""
+    rng = np.random.default_rng(b * 100 + sum(counts))
+    d = circulant_only(rng, counts, b)
+    op = ops(d)
+    p = uvec(rng, d.N)
+    sizes, lam = O.spectrum_build(counts, d.far_offsets, d.far_blocks)
+    gsizes, glam = op.spectrum()
+    assert gsizes == sizes
+    assert rel(glam, lam) <= 1e-12
+    ref = O.spectrum_matvec(counts, sizes, b, lam, p)
+    assert rel(op.matvec(p), ref) <= MATVEC_TOL
+    if d.N <= 400:
+        dense = O.toeplitz_expand_dense(counts, d.far_offsets, d.far_blocks)
+        assert rel(op.matvec(p), dense @ p) <= MATVEC_TOL
+
+
+def test_scalar_toeplitz_known_answer_on_device(ops):
+    """test_structured.cpp:84-98 through the device M2L: T=[[2,1],[3,2]], T(1,1)=(3,5)"""
+    d = Data((2, 1, 1), 1, 1, [(0, 0, 0)], np.zeros((1, 1, 1)), [(0, 0, 0), (1, 0, 0), (-1, 0, 0)],
+             np.array([[[2]], [[3]], [[1]]]), np.eye(1), np.eye(1))
+    y = ops(d).matvec(np.array([1, 1], np.complex128))
+    np.testing.assert_allclose(y, [3, 5], atol=1e-14)
+
+
+def test_caller_chosen_fft_sizes(ops):
+    """any L >= 2M-1 is exact (SURVEY finding 7)"""
+    rng = np.random.default_rng(8)
+    counts = (5, 3, 1)
+    d = circulant_only(rng, counts, 4)
+    p = uvec(rng, d.N)
+    ref = O.toeplitz_matvec(counts, d.far_offsets, d.far_blocks, p)
+    for sizes in [(9, 5, 1), (16, 8, 1), (10, 7, 1)]:
+        assert rel(ops(d, fft_sizes=sizes).matvec(p), ref) <= MATVEC_TOL
+    with pytest.raises(ValueError):
+        ops(d, fft_sizes=(8, 5, 1))
+
+
+def test_prebuilt_reference_spectrum_is_accepted(ops):
+    rng = np.random.default_rng(12)
+    counts = (3, 4, 1)
+    d = circulant_only(rng, counts, 5)
+    sizes, lam = O.spectrum_build(counts, d.far_offsets, d.far_blocks)
+    op = ops(d, fft_sizes=sizes, lambda_=lam)
+    p = uvec(rng, d.N)
+    assert rel(op.matvec(p), O.spectrum_matvec(counts, sizes, 5, lam, p)) <= MATVEC_TOL
+
+
+# ---- assembled operators of the BASELINE configurations -----------------------------
+
+SMALL_SCENES = [(1, 0), (1, 1), (2, 2), (3, 2), (4, 2), (5, 2), (6, 8), (6, 16)]
+
+
+@pytest.fixture(scope="module")
+def assembled():
+    from paper_2201_12050_b200 import Scene
+
+    cache = {}
+
+    def get(cid, var):
+        if (cid, var) not in cache:
+            sc = Scene(cid, var)
+            cache[(cid, var)] = (sc, sc.assemble_fmm(4))
+        return cache[(cid, var)]
+
+    return get
+
+
+@pytest.mark.parametrize("cid,var", SMALL_SCENES)
+def test_fmm_matvec_matches_oracle(ops, assembled, cid, var):
+    sc, d = assembled(cid, var)
+    ora = O.OracleFmm(d)
+    op = ops(d)
+    rng = np.random.default_rng(cid)  # seed = config id (BASELINE.md CPU-baseline plan)
+    p = uvec(rng, d.N)
+    assert rel(op.matvec(p), ora.matvec(p)) <= MATVEC_TOL
+    sizes, lam = op.spectrum()
+    assert sizes == ora.sizes
+    if d.n_far:
+        assert rel(lam, ora.lambda_) <= 1e-12
+    assert op.stored_bytes() == 16 * (d.n_near * d.n_dof ** 2 + int(np.prod(sizes)) * 625 + 2 * 25 * d.n_dof)
+
+
+def test_multi_rhs_equals_single_rhs(ops, assembled):
+    sc, d = assembled(3, 2)
+    rng = np.random.default_rng(5)
+    P = [uvec(rng, d.N) for _ in range(3)]
+    single = ops(d).matvec
+    multi = ops(d, max_rhs=2)  # 3 rhs through chunks of 2
+    y = multi.matvec(np.concatenate(P))
+    for r in range(3):
+        assert rel(y[r * d.N:(r + 1) * d.N], single(P[r])) <= 1e-14
+
+
+def test_device_pointer_apply_matches_host_pointer(ops, assembled):
+    torch = pytest.importorskip("torch")
+    sc, d = assembled(5, 2)
+    op = ops(d)
+    rng = np.random.default_rng(2)
+    p = uvec(rng, d.N)
+    yh = op.matvec(p)
+    yd = op.matvec(torch.from_numpy(p).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), yh)
+
+
+def test_apply_is_deterministic_and_linear(ops, assembled):
+    sc, d = assembled(2, 2)
+    op = ops(d)
+    rng = np.random.default_rng(4)
+    p, q = uvec(rng, d.N), uvec(rng, d.N)
+    y1 = op.matvec(p)
+    assert np.array_equal(y1, op.matvec(p))  # fixed-order reductions, no atomics
+    a = 0.3 - 1.1j
+    assert rel(op.matvec(a * p + q), a * y1 + op.matvec(q)) < 1e-13
+
+
+def test_dimension_mismatch_raises_invalid_argument(ops, assembled):
+    sc, d = assembled(1, 0)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        ops(d).matvec(np.zeros(d.N + 1, np.complex128))
+
+
+# ---- GMRES ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cid,var", [(1, 0), (3, 2), (4, 2), (5, 2), (6, 8)])
+def test_fmm_gmres_matches_oracle(ops, assembled, cid, var):
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(cid, var)
+    b = sc.rhs(0)
+    rep = gmres(ops(d), b, tol=1e-6, restart=50, max_iter=400)
+    x, its, conv, hist = O.OracleFmm(d).gmres(b, tol=1e-6, restart=50, max_iter=400)
+    assert rep.converged == conv
+    assert abs(rep.iterations - its) <= 1
+    assert rel(rep.solution, x) <= SOLVE_TOL
+    assert len(rep.residual_history) == rep.iterations
+
+
+def test_fmm_gmres_with_restarts_matches_oracle(ops, assembled):
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(2, 2)
+    b = sc.rhs(0)
+    rep = gmres(ops(d), b, tol=1e-6, restart=10, max_iter=2000)
+    x, its, conv, hist = O.OracleFmm(d).gmres(b, tol=1e-6, restart=10, max_iter=2000)
+    assert rep.converged and conv
+    assert abs(rep.iterations - its) <= 1
+    assert rel(rep.solution, x) <= SOLVE_TOL
+    n = min(len(hist), len(rep.residual_history))
+    assert rel(np.array(rep.residual_history[:n]), np.array(hist[:n])) < 1e-8
+
+
+def test_fmm_gmres_multi_rhs(ops, assembled):
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(5, 2)
+    sc.set_sources([1, 1], [[1, 0, 0], [0, 0.6, 0.8]])
+    b = np.concatenate([sc.rhs(0), sc.rhs(1)])
+    reps = gmres(ops(d), b, tol=1e-6, restart=50, max_iter=400)
+    ora = O.OracleFmm(d)
+    for r in range(2):
+        x, its, conv, _ = ora.gmres(b[r * d.N:(r + 1) * d.N], tol=1e-6, restart=50, max_iter=400)
+        assert abs(reps[r].iterations - its) <= 1
+        assert rel(reps[r].solution, x) <= SOLVE_TOL
+
+
+# test_solver.cpp known answers through the device Krylov engine (callable seam)
+
+def _t(a):
+    import torch
+
+    return torch.from_numpy(np.asarray(a, np.complex128)).cuda()
+
+
+def test_device_gmres_identity_one_iteration():
+    from paper_2201_12050_b200 import gmres
+
+    b = np.array([1 + 2j, -0.5, 3j])
+    rep = gmres(lambda v: v, b, tol=1e-12)
+    assert rep.converged and rep.iterations == 1
+    assert np.linalg.norm(rep.solution - b) < 1e-12 * np.linalg.norm(b)
+
+
+def test_device_gmres_diagonal():
+    from paper_2201_12050_b200 import gmres
+
+    dg = _t([2.0, 4.0])
+    rep = gmres(lambda v: dg * v, np.array([2.0, 4.0], np.complex128), tol=1e-13)
+    assert rep.converged
+    np.testing.assert_allclose(rep.solution, [1, 1], atol=1e-12)
+
+
+def test_device_gmres_random_dense_vs_direct_and_oracle():
+    from paper_2201_12050_b200 import gmres
+
+    rng = np.random.default_rng(11)
+    n = 60
+    a = np.eye(n) + 0.25 / np.sqrt(n) * crand(rng, n, n)
+    b = crand(rng, n)
+    at = _t(a)
+    rep = gmres(lambda v: at @ v, b, tol=1e-12, restart=100, max_iter=300)
+    assert rep.converged
+    assert rel(rep.solution, np.linalg.solve(a, b)) < 1e-10
+    x, its, conv, _ = O.gmres(lambda v: a @ v, b, tol=1e-12, restart=100, max_iter=300)
+    assert abs(its - rep.iterations) <= 1
+
+
+def test_device_gmres_restart_monotone_and_matches_oracle():
+    from paper_2201_12050_b200 import gmres
+
+    rng = np.random.default_rng(5)
+    n, restart = 40, 7
+    a = 2.0 * np.eye(n) + 0.3 / np.sqrt(n) * crand(rng, n, n)
+    at = _t(a)
+    b = np.ones(n, np.complex128)
+    rep = gmres(lambda v: at @ v, b, tol=1e-11, restart=restart, max_iter=400)
+    assert rep.converged and rep.iterations > restart
+    h = rep.residual_history
+    for i in range(1, len(h)):
+        if i % restart:
+            assert h[i] <= h[i - 1] * (1 + 1e-10)
+    x, its, conv, _ = O.gmres(lambda v: a @ v, b, tol=1e-11, restart=restart, max_iter=400)
+    assert abs(its - rep.iterations) <= 1 and rel(rep.solution, x) < SOLVE_TOL
+
+
+def test_device_gmres_non_convergence_reported():
+    from paper_2201_12050_b200 import gmres
+
+    n = 30
+    a = np.zeros((n, n))
+    for i in range(n):
+        a[(i + 1) % n, i] = 1.0
+    at = _t(a)
+    b = np.zeros(n, np.complex128)
+    b[0] = 1
+    rep = gmres(lambda v: at @ v, b, tol=1e-14, max_iter=5)
+    assert not rep.converged and rep.iterations == 5
+
+
+def test_device_gmres_nan_is_a_hard_error():
+    from paper_2201_12050_b200 import gmres
+
+    def bad(v):
+        w = v.clone()
+        w[2] = float("nan")
+        return w
+
+    with pytest.raises(RuntimeError, match="non-finite"):
+        gmres(bad, np.ones(4, np.complex128))
+
+
+def test_device_gmres_left_preconditioner():
+    from paper_2201_12050_b200 import gmres
+
+    n = 50
+    d = 1.0 + 99.0 * np.arange(n) / (n - 1)
+    dt = _t(d)
+    b = np.ones(n, np.complex128)
+    rep = gmres(lambda v: dt * v, b, tol=1e-12, preconditioner=lambda v: v / dt)
+    assert rep.converged and rep.iterations == 1
+    assert np.linalg.norm(d * rep.solution - b) / np.linalg.norm(b) < 1e-10
+
+
+def test_fmm_gmres_nan_rhs_is_a_hard_error(ops, assembled):
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(1, 0)
+    b = sc.rhs(0)
+    b[5] = np.nan
+    with pytest.raises(RuntimeError, match="non-finite"):
+        gmres(ops(d), b, tol=1e-6, restart=50, max_iter=50)
