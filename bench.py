@@ -1,0 +1,362 @@
+"""Benchmark of the periodic-FMBEM GMRES matvec hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+One step = one FMM operator product y = A x (near field + P2M + lattice M2L +
+L2P) of the BASELINE.json configuration (default configs[1] = cfg2: 4 x 32
+closed cylinders, 1024 triangles each, 131,072 DOF, k = 2 pi 1000/343). The
+operator is assembled on the host (C++), uploaded once, and the timed region
+covers K products on inputs resident in HBM (the 2.1 GB near-field operator
+is far larger than the 126 MB L2, so every step streams it from HBM).
+`e2e` times the same product through the C-ABI with pinned host buffers
+(host->device copy of x and device->host copy of y inside every step). A
+GMRES solve (tol 1e-6, restart 50) is timed as the metric's second half.
+
+--impl reference times the reference's CPU algorithm (the oracle port,
+oracle/fpbem_oracle.cpp; the reference itself cannot be built here, see
+DESIGN.md) on the host cores for the same workload.
+
+With N > 1 (torchrun) every rank runs an independent replica of the workload
+on its own GPU (no data-path collective); value = all ranks' DOF / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "FMBEM matvec DOF/s"
+UNIT = "DOF/s"
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FP64_PEAK_FILE = ROOT / "profiles" / "r01_fp64_peak.json"
+TRAFFIC_FILE = ROOT / "profiles" / "near_gemm_traffic.json"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(cfg: int):
+    from paper_2201_12050_b200 import Scene
+
+    sc = Scene(cfg, 0)
+    desc = {1: "cfg1: 8 spheres (icosphere s2, 320 tri) on a row, period 1.0, k=2.0",
+            2: "cfg2: 4x32 closed cylinders (r 0.08, h 2.0, 1024 tri), lattice 0.22 m, k=2*pi*1000/343",
+            3: "cfg3: 16^3 spheres (icosphere s2, 320 tri), period 0.5, k=6.0",
+            4: "cfg4: 256 closed boxes 0.1x1.0x2.0 (3680 tri), period 1.05 m, 100 Hz",
+            5: "cfg5: 32x32x4 spheres (320 tri), period 0.5, k=4.0"}[cfg]
+    return sc, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peak():
+    """FP64 tensor (DMMA) peak: MEASURED_PEAKS.json has none, so the repo's own
+    microbenchmark (tools/fp64_peak.cu) result is used."""
+    try:
+        peaks = json.loads(PEAKS_FILE.read_text())
+        if "fp64_tflops" in peaks:
+            return float(peaks["fp64_tflops"]), "MEASURED_PEAKS.json fp64_tflops"
+    except (OSError, ValueError):
+        pass
+    d = json.loads(FP64_PEAK_FILE.read_text())
+    return float(d["dmma_tflops"]), "profiles/r01_fp64_peak.json (DMMA.8x8x4 microbenchmark, tools/fp64_peak.cu)"
+
+
+def near_gemm_traffic():
+    try:
+        return json.loads(TRAFFIC_FILE.read_text())
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline(data, x, samples: int = 3):
+    """Oracle (reference algorithm, OpenMP over target cells) on the host cores."""
+    import oracle as O
+
+    t0 = time.perf_counter()
+    ora = O.OracleFmm(data)
+    ora.matvec(x)  # warm-up (reference protocol: src/scene.cpp:529)
+    best = float("inf")
+    for _ in range(samples):
+        t = time.perf_counter()
+        ora.matvec(x)
+        best = min(best, time.perf_counter() - t)
+    return {"value": data.N / best, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+            "sample": f"{samples} single-RHS matvecs of the same operator after 1 warm-up, best of {samples} "
+                      f"({best:.3f} s each; setup {time.perf_counter() - t0 - (samples + 1) * best:.1f} s)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+
+    sc, desc = workload(args.config)
+    t = time.perf_counter()
+    data = sc.assemble_fmm(4)
+    log(f"[ref] assembled {desc} in {time.perf_counter() - t:.1f} s")
+    ora = O.OracleFmm(data)
+    rng = np.random.default_rng(args.config)
+    x = rng.uniform(-1, 1, data.N) + 1j * rng.uniform(-1, 1, data.N)
+    for _ in range(args.warmup):
+        ora.matvec(x)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        ora.matvec(x)
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = data.N * args.steps / total
+    cores = O.num_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128",
+        "data": "synthetic (seeded U[-1,1] input; operator assembled from the config geometry)",
+        "config": {"workload": desc, "n_dof_total": data.N, "nrhs": 1, "n_t": 4},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "each step = one full single-RHS matvec of the workload on the host "
+                                   "(oracle restatement of the reference; reference unbuildable here)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2201_12050_b200 import FmmOperators, gmres
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    sc, desc = workload(args.config)
+    t = time.perf_counter()
+    data = sc.assemble_fmm(4)
+    t_asm = time.perf_counter() - t
+    log(f"[rank {rank}] assembled {desc}: N={data.N} near={data.n_near} far={data.n_far} in {t_asm:.1f} s")
+    t = time.perf_counter()
+    op = FmmOperators(data, device=dev.index)
+    t_up = time.perf_counter() - t
+    # a dedicated (non-default) stream shared by torch's events and the library's kernels
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    op.set_stream(stream.cuda_stream)
+
+    rng = np.random.default_rng(args.config + 1000 * rank)
+    xh = rng.uniform(-1, 1, data.N) + 1j * rng.uniform(-1, 1, data.N)
+    x = torch.from_numpy(xh).to(dev)
+
+    # warm-up
+    for _ in range(max(3, args.warmup)):
+        y = op.matvec(x)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    sampler = ClockSampler(dev.index)
+    with sampler:
+        time.sleep(0.25)  # let the sampler start
+        # ---- device-resident timed region
+        launches0 = op.kernel_launches()
+        barrier()
+        torch.cuda.synchronize(dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            y = op.matvec(x)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = op.kernel_launches() - launches0
+
+        # ---- per-stage event timing (same stream) for the roofline
+        op.enable_stage_timing(True)
+        for _ in range(args.steps):
+            op.matvec(x)
+        stages = op.stage_times()
+        op.enable_stage_timing(False)
+
+        # ---- end-to-end through the C-ABI with pinned host buffers
+        xp = torch.empty(data.N, dtype=torch.complex128, pin_memory=True)
+        xp.copy_(torch.from_numpy(xh))
+        yp = torch.empty_like(xp)
+        xpn, ypn = xp.numpy(), yp.numpy()
+        from paper_2201_12050_b200 import _native
+
+        lib = _native.cuda()
+        op.matvec(xpn)
+        barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            rc = lib.fpbem_cu_fmm_apply(op.handle, xpn.ctypes.data, ypn.ctypes.data, 1, 0)
+            if rc:
+                raise RuntimeError(lib.fpbem_cu_last_error().decode())
+        e2e_s = time.perf_counter() - t
+        barrier()
+
+        # ---- GMRES solve (metric's second half)
+        b = torch.from_numpy(sc.rhs(0)).to(dev)
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        rep = gmres(op, b, tol=1e-6, restart=50, max_iter=args.gmres_max_iter)
+        torch.cuda.synchronize(dev)
+        gmres_s = time.perf_counter() - t
+    clocks = sampler.summary()
+
+    # max over ranks
+    vals = torch.tensor([ms, e2e_s, gmres_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+    ms, e2e_s, gmres_s = (float(v) for v in vals.cpu())
+
+    # roofline of the dominant kernel (near-field DMMA GEMM): algorithmic flops per launch
+    pairs = 0
+    m = data.counts
+    for o in data.near_offsets:
+        pairs += (m[0] - abs(int(o[0]))) * (m[1] - abs(int(o[1]))) * (m[2] - abs(int(o[2])))
+    flops = 8.0 * data.n_dof ** 2 * pairs
+    gemm_ms = stages["near_gemm"] / max(1, stages["applies"])
+    achieved = flops / (gemm_ms * 1e-3) / 1e12
+    peak, peak_src = fp64_peak()
+    traffic = near_gemm_traffic()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(data, xh)
+
+    if rank == 0:
+        value = world * data.N * args.steps / (ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "complex128",
+            "data": "synthetic (seeded U[-1,1] input; operator assembled from the config geometry)",
+            "config": {
+                "workload": desc, "n_dof_total": data.N, "n_dof_cell": data.n_dof, "lattice": list(data.counts),
+                "near_offsets": data.n_near, "far_offsets": data.n_far, "n_t": 4, "nrhs": 1,
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "l2": f"inputs larger than L2: near-field operator {16 * data.n_near * data.n_dof ** 2 / 1e9:.2f} GB "
+                      "streamed from HBM every step",
+                "assembly_s": round(t_asm, 2), "upload_s": round(t_up, 2),
+            },
+            "stages_ms": {k: (v / max(1, stages["applies"]) if k != "applies" else v) for k, v in stages.items()},
+            "roofline": {
+                "kernel": "near_gemm_dmma_kernel", "bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "peak_source": peak_src,
+                "flops_per_launch": flops, "launch_ms": gemm_ms,
+                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "traffic_source": (traffic or {}).get("source"),
+                "algorithmic_bytes": 16.0 * data.n_near * data.n_dof ** 2 + 2 * 16.0 * data.N,
+            },
+            "e2e": {"value": world * data.N * args.steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": 16 * data.N, "d2h_bytes_per_step": 16 * data.N},
+            "gmres": {"solve_s": gmres_s, "iterations": rep.iterations, "converged": rep.converged,
+                      "tol": 1e-6, "restart": 50, "final_estimate": rep.residual_history[-1]
+                      if rep.residual_history else None},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--gmres-max-iter", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        # bounded CPU sample: each step is a full CPU matvec
+        args.steps = min(args.steps, 5)
+        args.warmup = min(max(args.warmup, 1), 1)
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

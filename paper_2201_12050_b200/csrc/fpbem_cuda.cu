@@ -13,6 +13,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -93,6 +94,8 @@ struct fpbem_cu_op {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t aux = nullptr;  // P2M + M2L run here, concurrently with the near-field GEMM
+  cudaEvent_t fork = nullptr, join = nullptr;
   int counts[3] = {1, 1, 1};
   int n = 0, b = 0, n_cells = 0;
   long long N = 0;
@@ -107,8 +110,8 @@ struct fpbem_cu_op {
   int* pair_src = nullptr;
   int* tgt_ptr = nullptr;
   int* tgt_pairs = nullptr;
-  int4* jobs = nullptr;
-  int jobs_nrhs = -1, n_jobs = 0, jobs_cap = 0;
+  int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
+  int jobs_nrhs = -1, n_jobs = 0, n_p2m_jobs = 0, jobs_cap = 0;
   std::vector<int> rank_slots;  // offset slots this rank computes (all without a comm)
 
   // expansions and spectrum
@@ -145,7 +148,7 @@ struct fpbem_cu_op {
 
   // timing
   bool timing = false;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   double stage_ms[5] = {0, 0, 0, 0, 0};
   long long applies = 0;
   long long launches = 0;
@@ -164,14 +167,22 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
     const int cols = pairs * nrhs;
     for (int c0 = 0; c0 < cols; c0 += bn) jobs.push_back(make_int4(s, c0, std::min(bn, cols - c0), op->pair_start[s]));
   }
+  // offset order by default (consecutive tiles share S_o in L2);
+  // FPBEM_JOB_ORDER=lpt puts the longest column tiles first (A/B timing)
+  const char* order = std::getenv("FPBEM_JOB_ORDER");
+  if (order && std::strcmp(order, "lpt") == 0)
+    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+  const int n_near_jobs = static_cast<int>(jobs.size());
+  const int p2m_cols = op->n_cells * nrhs;
+  for (int c0 = 0; c0 < p2m_cols; c0 += bn) jobs.push_back(make_int4(0, c0, std::min(bn, p2m_cols - c0), 0));
   if (static_cast<int>(jobs.size()) > op->jobs_cap) {
     if (op->jobs) cudaFree(op->jobs);
     op->jobs = dalloc<int4>(jobs.size(), "jobs");
     op->jobs_cap = static_cast<int>(jobs.size());
   }
-  if (!jobs.empty())
-    h2d(op->jobs, jobs.data(), jobs.size() * sizeof(int4), op->stream, "jobs upload");
-  op->n_jobs = static_cast<int>(jobs.size());
+  if (!jobs.empty()) h2d(op->jobs, jobs.data(), jobs.size() * sizeof(int4), op->stream, "jobs upload");
+  op->n_jobs = n_near_jobs;
+  op->n_p2m_jobs = static_cast<int>(jobs.size()) - n_near_jobs;
   op->jobs_nrhs = nrhs;
 }
 
@@ -232,23 +243,33 @@ void build_spectrum(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
   cudaFree(offs);
 }
 
-void ev_record(fpbem_cu_op* op, int i) {
-  if (op->timing) cudaEventRecord(op->ev[i], op->stream);
+void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {
+  if (op->timing) cudaEventRecord(op->ev[i], st);
 }
 
 // One FMM product for nrhs <= max_rhs right-hand sides, device pointers.
 // Order of the sums follows src/fmm.cpp:253-267: y = S p, then y += U0 L.
 void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
   cudaStream_t s = op->stream;
+  cudaStream_t a = op->aux;
   const long long E = static_cast<long long>(nrhs) * op->b;
   build_jobs(op, nrhs);
-  ev_record(op, 0);
-  check(launch_near_gemm(op->S, x, op->W, op->pair_src, op->jobs, op->n_jobs, op->n, op->N, nrhs, s), "near gemm");
+  // fork: P2M + M2L on the aux stream while the near-field GEMM runs on the main one
+  check(cudaEventRecord(op->fork, s), "fork");
+  check(cudaStreamWaitEvent(a, op->fork, 0), "fork");
+  ev_record(op, 0, s);
+  check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n, op->pair_src,
+                          op->jobs, op->n_jobs, op->n, op->n, op->N, nrhs, s),
+        "near gemm");
   op->launches += op->n_jobs > 0;
-  ev_record(op, 1);
-  check(launch_p2m(op->v0, x, op->mom, op->n, op->b, op->n_cells, op->N, nrhs, s), "p2m");
+  ev_record(op, 1, s);
+  ev_record(op, 2, a);
+  check(launch_block_gemm(op->v0, 0, op->b, op->b, x, op->mom, op->b, nullptr, op->jobs + op->n_jobs, op->n_p2m_jobs,
+                          op->n, op->n, op->N, nrhs, a),
+        "p2m");
   op->launches++;
-  ev_record(op, 2);
+  ev_record(op, 3, a);
+  s = a;  // the M2L passes below run on the aux stream
 
   // pruned separable lattice DFT, per-mode product, pruned inverse
   const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
@@ -298,24 +319,28 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
     cur = out;
     which ^= 1;
   }
-  ev_record(op, 3);
+  ev_record(op, 4, a);
+  check(cudaEventRecord(op->join, a), "join");
+  s = op->stream;
+  check(cudaStreamWaitEvent(s, op->join, 0), "join");
+  ev_record(op, 5, s);
   check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, op->loc, y, op->n, op->b, op->n_cells,
                                op->N, nrhs, false, s),
         "near reduce + l2p");
   op->launches++;
-  ev_record(op, 4);
+  ev_record(op, 6, s);
   if (op->timing) {
-    check(cudaEventSynchronize(op->ev[4]), "timing sync");
+    check(cudaEventSynchronize(op->ev[6]), "timing sync");
     float ms;
     cudaEventElapsedTime(&ms, op->ev[0], op->ev[1]);
     op->stage_ms[0] += ms;
-    cudaEventElapsedTime(&ms, op->ev[3], op->ev[4]);
+    cudaEventElapsedTime(&ms, op->ev[5], op->ev[6]);
     op->stage_ms[1] += ms;
-    cudaEventElapsedTime(&ms, op->ev[1], op->ev[2]);
-    op->stage_ms[2] += ms;
     cudaEventElapsedTime(&ms, op->ev[2], op->ev[3]);
+    op->stage_ms[2] += ms;
+    cudaEventElapsedTime(&ms, op->ev[3], op->ev[4]);
     op->stage_ms[3] += ms;
-    cudaEventElapsedTime(&ms, op->ev[0], op->ev[4]);
+    cudaEventElapsedTime(&ms, op->ev[0], op->ev[6]);
     op->stage_ms[4] += ms;
     op->applies++;
   }
@@ -575,6 +600,9 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->device = device;
     check(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
     op->own_stream = true;
+    check(cudaStreamCreateWithFlags(&op->aux, cudaStreamNonBlocking), "aux stream");
+    check(cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&op->join, cudaEventDisableTiming), "event");
     for (int k = 0; k < 3; ++k) op->counts[k] = d->counts[k];
     op->n = d->n_dof;
     op->b = d->n_coef;
@@ -675,6 +703,12 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
   if (op->pinned) cudaFreeHost(op->pinned);
   for (auto& e : op->ev)
     if (e) cudaEventDestroy(e);
+  if (op->aux) {
+    cudaStreamSynchronize(op->aux);
+    cudaStreamDestroy(op->aux);
+  }
+  if (op->fork) cudaEventDestroy(op->fork);
+  if (op->join) cudaEventDestroy(op->join);
   if (op->own_stream && op->stream) cudaStreamDestroy(op->stream);
   delete op;
 }

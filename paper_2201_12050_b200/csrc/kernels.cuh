@@ -9,10 +9,12 @@ namespace fpbem_cu {
 size_t near_gemm_smem_bytes();
 int near_gemm_tile_cols();
 int near_gemm_tile_rows();
-// jobs: (offset slot, first column, column count, pair base); columns of an
-// offset are (pair, rhs) with rhs fastest.
-cudaError_t launch_near_gemm(const c64* S, const c64* x, c64* W, const int* pair_src, const int4* jobs,
-                             int n_jobs, int n, long long N, int nrhs, cudaStream_t stream);
+// jobs: (block slot, first column, column count, pair base); columns are
+// (pair, rhs) with rhs fastest (near field) or (cell, rhs) when pair_src is
+// null (P2M with A = V0, a_stride = 0).
+cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
+                              const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
+                              cudaStream_t stream);
 cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* tgt_pairs, const c64* u0,
                                    const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
                                    int nrhs, bool accumulate, cudaStream_t stream);
@@ -22,8 +24,6 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
                             long long n_inner, int L, bool backward, double scale, cudaStream_t stream);
 cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image, long long q_total, int b,
                                 int nrhs, cudaStream_t stream);
-cudaError_t launch_p2m(const c64* v0, const c64* x, c64* moments, int n, int b, int n_cells, long long N,
-                       int nrhs, cudaStream_t stream);
 cudaError_t launch_scatter_bank(const c64* blocks, const int* offsets, int n_blk, int b2, int lx, int ly, int lz,
                                 c64* field, cudaStream_t stream);
 

@@ -11,7 +11,7 @@
 // streaming kernel over [outer][axis][inner][fields] with the fields
 // (nrhs x b, contiguous) innermost, so every warp access is coalesced. The
 // per-mode product streams Λ once per apply (the HBM-bound part).
-// P2M (src/fmm.cpp:256-259): moments[c][r][:] = V0 * p[r][c][:].
+// P2M (src/fmm.cpp:256-259) runs as a job list of the DMMA block GEMM (near_field.cu).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -64,22 +64,6 @@ __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* _
   }
 }
 
-// moments[col][m] = sum_k V0[m + b k] x[src(col) + k], col = (cell, rhs)
-constexpr int P2M_COLS = 8;
-__global__ void p2m_kernel(const c64* __restrict__ v0, const c64* __restrict__ x, c64* __restrict__ moments,
-                           int n, int b, int n_cells, long long N, int nrhs) {
-  const int m = threadIdx.x;
-  const int cl = threadIdx.y;
-  const long long col = static_cast<long long>(blockIdx.x) * P2M_COLS + cl;
-  if (m >= b || col >= static_cast<long long>(n_cells) * nrhs) return;
-  const long long cell = col / nrhs;
-  const int r = static_cast<int>(col % nrhs);
-  const c64* xs = x + static_cast<long long>(r) * N + cell * n;
-  c64 acc = cmk(0.0, 0.0);
-  for (int k = 0; k < n; ++k) acc = cfma(__ldg(v0 + static_cast<long long>(k) * b + m), __ldg(xs + k), acc);
-  moments[col * b + m] = acc;
-}
-
 // zero the embedded field and place each K_o at slot (o mod L) (src/structured.cpp:73-86)
 __global__ void scatter_bank_kernel(const c64* __restrict__ blocks, const int* __restrict__ offsets, int n_blk,
                                     int b2, int lx, int ly, int lz, c64* __restrict__ field) {
@@ -120,15 +104,6 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
                                 int nrhs, cudaStream_t stream) {
   const long long total = q_total * b * nrhs;
   mode_product_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lambda, field, image, q_total, b, nrhs);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_p2m(const c64* v0, const c64* x, c64* moments, int n, int b, int n_cells, long long N,
-                       int nrhs, cudaStream_t stream) {
-  const long long cols = static_cast<long long>(n_cells) * nrhs;
-  dim3 block(b, P2M_COLS);
-  dim3 grid(static_cast<unsigned>((cols + P2M_COLS - 1) / P2M_COLS));
-  p2m_kernel<<<grid, block, 0, stream>>>(v0, x, moments, n, b, n_cells, N, nrhs);
   return cudaGetLastError();
 }
 

@@ -11,8 +11,9 @@
 // reference's offset order by near_reduce_l2p_kernel, which also adds the
 // L2P term U0 * L_t (src/fmm.cpp:265-267) — no atomics, deterministic.
 //
-// Complex arithmetic: C_re += A_re B_re - A_im B_im, C_im += A_re B_im + A_im B_re,
-// four real m8n8k4 DMMAs per complex 8x8x4 tile.
+// Complex arithmetic: the Gauss 3-multiplication form (three real m8n8k4
+// DMMAs per complex 8x8x4 tile instead of four); the algorithmic count stays
+// 8 real flops per complex multiply-add.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -31,10 +32,18 @@ constexpr int THREADS = 256;
 constexpr size_t kSmemA = sizeof(c64) * STAGES * BK * AP;
 constexpr size_t kSmemB = sizeof(c64) * STAGES * BN * BP;
 
+// Batched block GEMM over (block, column-tile) jobs:
+//   out[col_out(c) + m] = sum_k A_s[m + lda k] * x[col_src(c) + k],  m < M, k < K
+// Near field: A_s = S_s (lda = M = K = n), columns = (pair, rhs) of offset s,
+//   col_src = rhs*N + pair_src[pair]*n, col_out = (pair*nrhs + rhs)*ldo.
+// P2M:        A = V0 (lda = M = b, a_stride = 0), columns = (cell, rhs),
+//   col_src = rhs*N + cell*n, col_out = (cell*nrhs + rhs)*ldo  (pair_src == nullptr).
+// Warps whose 8-column slab lies beyond the job's column count skip the MMA
+// loop, so partial column tiles cost (almost) only their useful work.
 __global__ void __launch_bounds__(THREADS, 2)
-near_gemm_dmma_kernel(const c64* __restrict__ S, const c64* __restrict__ x, c64* __restrict__ W,
-                      const int* __restrict__ pair_src, const int4* __restrict__ jobs, int n,
-                      long long N, int nrhs) {
+near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, int M, const c64* __restrict__ x,
+                      c64* __restrict__ out, int ldo, const int* __restrict__ pair_src, const int4* __restrict__ jobs,
+                      int K, int n, long long N, int nrhs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   c64* As = reinterpret_cast<c64*>(smem_raw);
   c64* Bs = reinterpret_cast<c64*>(smem_raw + kSmemA);
@@ -44,16 +53,18 @@ near_gemm_dmma_kernel(const c64* __restrict__ S, const c64* __restrict__ x, c64*
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int m0 = blockIdx.x * BM;
-  const int4 job = jobs[blockIdx.y];  // (offset slot, first column, column count, pair base)
+  if (m0 >= M) return;
+  const int4 job = jobs[blockIdx.y];  // (block slot, first column, column count, pair base)
   const int s = job.x, col0 = job.y, ncols = job.z, pair_base = job.w;
 
   if (tid < BN) {
     if (tid < ncols) {
       const int gc = col0 + tid;
-      const int pair = pair_base + gc / nrhs;
+      const int unit = pair_base + gc / nrhs;  // pair (near field) or cell (P2M)
       const int r = gc % nrhs;
-      col_src[tid] = static_cast<long long>(r) * N + static_cast<long long>(pair_src[pair]) * n;
-      col_out[tid] = (static_cast<long long>(pair_base) * nrhs + gc) * n;
+      const long long cell = pair_src ? pair_src[unit] : unit;
+      col_src[tid] = static_cast<long long>(r) * N + cell * n;
+      col_out[tid] = (static_cast<long long>(pair_base) * nrhs + gc) * ldo;
     } else {
       col_src[tid] = -1;
       col_out[tid] = -1;
@@ -61,43 +72,52 @@ near_gemm_dmma_kernel(const c64* __restrict__ S, const c64* __restrict__ x, c64*
   }
   __syncthreads();
 
-  const c64* Sblk = S + static_cast<size_t>(s) * n * n;
-  const int nk = (n + BK - 1) / BK;
+  const c64* Ablk = A + static_cast<size_t>(s) * a_stride;
+  const int nk = (K + BK - 1) / BK;
+
+  // per-thread load coordinates: A rows (tid % BM) of k-columns tid / BM + 4 i,
+  // B k-entries (tid % BK) of columns tid / BK + 16 i
+  const int a_m = tid % BM, a_k = tid / BM;
+  const bool a_row_ok = m0 + a_m < M;
+  const c64* a_src = Ablk + static_cast<size_t>(a_k) * lda + m0 + a_m;
+  const int b_k = tid % BK, b_c = tid / BK;
+  const unsigned smem_a = static_cast<unsigned>(__cvta_generic_to_shared(As + a_k * AP + a_m));
+  const unsigned smem_b = static_cast<unsigned>(__cvta_generic_to_shared(Bs + b_c * BP + b_k));
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * BK;
-    c64* as = As + stage * BK * AP;
-    c64* bs = Bs + stage * BN * BP;
 #pragma unroll
     for (int i = 0; i < (BM * BK) / THREADS; ++i) {
-      const int e = tid + i * THREADS;
-      const int kk = e / BM, mm = e % BM;
-      const int gk = k0 + kk, gm = m0 + mm;
-      const bool ok = gk < n && gm < n;
-      cp_async16(as + kk * AP + mm, ok ? Sblk + static_cast<size_t>(gk) * n + gm : Sblk, ok);
+      const int kk = a_k + i * (THREADS / BM);
+      const bool ok = a_row_ok && k0 + kk < K;
+      const c64* src = ok ? a_src + static_cast<size_t>(k0 + i * (THREADS / BM)) * lda : Ablk;
+      const unsigned dst = smem_a + sizeof(c64) * (stage * BK * AP + i * (THREADS / BM) * AP);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
     }
 #pragma unroll
     for (int i = 0; i < (BN * BK) / THREADS; ++i) {
-      const int e = tid + i * THREADS;
-      const int c = e / BK, kk = e % BK;
-      const long long src = col_src[c];
-      const bool ok = src >= 0 && (k0 + kk) < n;
-      cp_async16(bs + c * BP + kk, ok ? x + src + k0 + kk : x, ok);
+      const long long src_off = col_src[b_c + i * (THREADS / BK)];
+      const bool ok = src_off >= 0 && (k0 + b_k) < K;
+      const c64* src = ok ? x + src_off + k0 + b_k : x;
+      const unsigned dst = smem_b + sizeof(c64) * (stage * BN * BP + i * (THREADS / BK) * BP);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
     }
   };
 
-  double cre[4][2][2], cim[4][2][2];
+  // Gauss 3-multiplication complex product on the FP64 tensor cores:
+  //   T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi);  Cr = T1 - T2, Ci = T3 - T1 - T2
+  // Each warp owns all 64 rows and one 8-column slab: 8 m-tiles x 3 partial products.
+  double t1[8][2], t2[8][2], t3[8][2];
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      cre[mi][ni][0] = cre[mi][ni][1] = 0.0;
-      cim[mi][ni][0] = cim[mi][ni][1] = 0.0;
-    }
+  for (int mi = 0; mi < 8; ++mi) {
+    t1[mi][0] = t1[mi][1] = 0.0;
+    t2[mi][0] = t2[mi][1] = 0.0;
+    t3[mi][0] = t3[mi][1] = 0.0;
+  }
 
-  const int wm = warp & 1;   // 32-row slab
-  const int wn = warp >> 1;  // 16-column slab
+  const int wn = warp;  // 8-column slab
   const int fr = lane >> 2, fk = lane & 3;
+  const bool active = wn * 8 < ncols;
 
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
@@ -111,42 +131,38 @@ near_gemm_dmma_kernel(const c64* __restrict__ S, const c64* __restrict__ x, c64*
     const int pf = kt + STAGES - 1;
     if (pf < nk) load_stage(pf % STAGES, pf);
     cp_async_commit();
+    if (!active) continue;
 
     const c64* as = As + (kt % STAGES) * BK * AP;
     const c64* bs = Bs + (kt % STAGES) * BN * BP;
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
-      c64 a[4], b[2];
+      const c64 b = bs[(wn * 8 + fr) * BP + k4 * 4 + fk];
+      const double bsum = b.x + b.y;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = as[(k4 * 4 + fk) * AP + wm * 32 + mi * 8 + fr];
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) b[ni] = bs[(wn * 16 + ni * 8 + fr) * BP + k4 * 4 + fk];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          dmma884(cre[mi][ni][0], cre[mi][ni][1], a[mi].x, b[ni].x);
-          dmma884(cre[mi][ni][0], cre[mi][ni][1], a[mi].y, -b[ni].y);
-          dmma884(cim[mi][ni][0], cim[mi][ni][1], a[mi].x, b[ni].y);
-          dmma884(cim[mi][ni][0], cim[mi][ni][1], a[mi].y, b[ni].x);
-        }
+      for (int mi = 0; mi < 8; ++mi) {
+        const c64 a = as[(k4 * 4 + fk) * AP + mi * 8 + fr];
+        const double asum = a.x + a.y;
+        dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
+        dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
+        dmma884(t3[mi][0], t3[mi][1], asum, bsum);
+      }
     }
   }
   cp_async_wait<0>();
+  if (!active) return;
 
   // epilogue: accumulator (row fr, cols 2*fk + {0,1}) of each 8x8 tile
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int gm = m0 + wm * 32 + mi * 8 + fr;
-    if (gm >= n) continue;
+  for (int mi = 0; mi < 8; ++mi) {
+    const int gm = m0 + mi * 8 + fr;
+    if (gm >= M) continue;
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = wn * 16 + ni * 8 + 2 * fk + j;
-        const long long out = col_out[c];
-        if (out >= 0) W[out + gm] = cmk(cre[mi][ni][j], cim[mi][ni][j]);
-      }
+    for (int j = 0; j < 2; ++j) {
+      const int c = wn * 8 + 2 * fk + j;
+      const long long o = col_out[c];
+      if (o >= 0) out[o + gm] = cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
+    }
   }
 }
 
@@ -202,8 +218,9 @@ size_t near_gemm_smem_bytes() { return kSmemA + kSmemB; }
 int near_gemm_tile_cols() { return BN; }
 int near_gemm_tile_rows() { return BM; }
 
-cudaError_t launch_near_gemm(const c64* S, const c64* x, c64* W, const int* pair_src, const int4* jobs,
-                             int n_jobs, int n, long long N, int nrhs, cudaStream_t stream) {
+cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
+                              const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
+                              cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(near_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -212,8 +229,9 @@ cudaError_t launch_near_gemm(const c64* S, const c64* x, c64* W, const int* pair
     configured = true;
   }
   if (n_jobs == 0) return cudaSuccess;
-  dim3 grid((n + BM - 1) / BM, n_jobs);
-  near_gemm_dmma_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(S, x, W, pair_src, jobs, n, N, nrhs);
+  dim3 grid((M + BM - 1) / BM, n_jobs);
+  near_gemm_dmma_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src, jobs,
+                                                                    K, n, N, nrhs);
   return cudaGetLastError();
 }
 

@@ -69,3 +69,38 @@ def test_product_path_fails_loudly_without_gpu():
     d = Scene(1, 2).assemble_fmm(2)
     with pytest.raises(RuntimeError):
         FmmOperators(d)
+
+
+def test_cpp_shim_compiles_links_and_maps_errors(tmp_path):
+    """include/fpbem_cuda.hpp (the reference-side binding) builds against the .so;
+    a bad descriptor surfaces as the reference's exception type."""
+    import subprocess
+
+    src = tmp_path / "shim.cpp"
+    src.write_text(r'''
+#include <complex>
+#include <cstdio>
+#include <vector>
+#include "fpbem_cuda.hpp"
+int main() {
+  fpbem_cu_fmm_desc d{};
+  d.counts[0] = 0;  // invalid lattice -> FPBEM_CU_EDIM -> std::invalid_argument (src/fmm.cpp:250 style)
+  try {
+    fpbem_cuda::DeviceFmm op(d, 0);
+  } catch (const std::invalid_argument& e) {
+    std::printf("invalid_argument: %s\n", e.what());
+    return 0;
+  } catch (const std::exception& e) {
+    std::printf("other: %s\n", e.what());
+    return 2;
+  }
+  return 1;
+}
+''')
+    lib = ROOT / "paper_2201_12050_b200" / "lib"
+    exe = tmp_path / "shim"
+    subprocess.run(["g++", "-std=c++17", "-I", str(ROOT / "include"), str(src), "-L", str(lib), "-lfpbem_cuda",
+                    f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "invalid_argument" in out.stdout
