@@ -139,6 +139,15 @@ int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int de
 void fpbem_cu_comm_destroy(fpbem_cu_comm* comm);
 int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm);
 
+/* The same offset partition without a communicator: apply() returns this
+ * rank's partial product (near field of its offsets; rank 0 adds the far
+ * field). Summing the nranks partial products gives the full product. */
+int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks);
+
+/* The partition rule itself (host only, no GPU): offsets weighted by work[s]
+ * (= pairs(o)) assigned longest-first to the least-loaded rank. */
+int fpbem_cu_partition_offsets(int n_near, const long long* work, int nranks, int* owner);
+
 const char* fpbem_cu_last_error(void);
 const char* fpbem_cu_version(void);
 

@@ -112,7 +112,9 @@ struct fpbem_cu_op {
   int* tgt_pairs = nullptr;
   int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
   int jobs_nrhs = -1, n_jobs = 0, n_p2m_jobs = 0, jobs_cap = 0;
-  std::vector<int> rank_slots;  // offset slots this rank computes (all without a comm)
+  std::vector<int> rank_slots;  // offset slots this rank computes (all without a partition)
+  std::vector<int> pair_tgt;    // host copy: target cell of every pair
+  int rank = 0, nranks = 1;     // near-field offset partition
 
   // expansions and spectrum
   c64* u0 = nullptr;
@@ -157,6 +159,57 @@ struct fpbem_cu_op {
 };
 
 namespace {
+
+// Work-balanced offset partition: longest-processing-time greedy over
+// pairs(o) (every offset's GEMM costs n_dof^2 * pairs(o)); deterministic.
+std::vector<int> partition_offsets(const std::vector<long long>& work, int nranks) {
+  std::vector<int> order(work.size()), owner(work.size(), 0);
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+  std::vector<long long> load(nranks, 0);
+  for (int s : order) {
+    int best = 0;
+    for (int r = 1; r < nranks; ++r)
+      if (load[r] < load[best]) best = r;
+    owner[s] = best;
+    load[best] += work[s];
+  }
+  return owner;
+}
+
+// per-target CSR of the pairs this rank owns, in offset order (the reduction order)
+void build_target_csr(fpbem_cu_op* op) {
+  std::vector<char> owned(op->n_near, 0);
+  for (int s : op->rank_slots) owned[s] = 1;
+  std::vector<std::vector<int>> per_t(op->n_cells);
+  for (int s = 0; s < op->n_near; ++s) {
+    if (!owned[s]) continue;
+    for (int p = op->pair_start[s]; p < op->pair_start[s + 1]; ++p) per_t[op->pair_tgt[p]].push_back(p);
+  }
+  std::vector<int> tptr(op->n_cells + 1, 0), tpairs;
+  for (int t = 0; t < op->n_cells; ++t) {
+    tpairs.insert(tpairs.end(), per_t[t].begin(), per_t[t].end());
+    tptr[t + 1] = static_cast<int>(tpairs.size());
+  }
+  if (!op->tgt_ptr) op->tgt_ptr = dalloc<int>(op->n_cells + 1, "target ptr");
+  if (!op->tgt_pairs) op->tgt_pairs = dalloc<int>(std::max(op->n_pairs, 1), "target pairs");
+  h2d(op->tgt_ptr, tptr.data(), tptr.size() * sizeof(int), op->stream, "target ptr");
+  if (!tpairs.empty()) h2d(op->tgt_pairs, tpairs.data(), tpairs.size() * sizeof(int), op->stream, "target pairs");
+}
+
+void set_partition(fpbem_cu_op* op, int rank, int nranks) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(FPBEM_CU_EINVAL, "partition: bad rank / nranks");
+  std::vector<long long> work(op->n_near);
+  for (int s = 0; s < op->n_near; ++s) work[s] = op->pair_start[s + 1] - op->pair_start[s];
+  std::vector<int> owner = partition_offsets(work, nranks);
+  op->rank_slots.clear();
+  for (int s = 0; s < op->n_near; ++s)
+    if (owner[s] == rank) op->rank_slots.push_back(s);
+  op->rank = rank;
+  op->nranks = nranks;
+  op->jobs_nrhs = -1;  // rebuild the GEMM job list
+  build_target_csr(op);
+}
 
 void build_jobs(fpbem_cu_op* op, int nrhs) {
   if (op->jobs_nrhs == nrhs) return;
@@ -247,31 +300,11 @@ void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {
   if (op->timing) cudaEventRecord(op->ev[i], st);
 }
 
-// One FMM product for nrhs <= max_rhs right-hand sides, device pointers.
-// Order of the sums follows src/fmm.cpp:253-267: y = S p, then y += U0 L.
-void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
-  cudaStream_t s = op->stream;
-  cudaStream_t a = op->aux;
+// Pruned separable lattice DFT, per-mode product, pruned inverse:
+// moments (op->mom) -> locals (op->loc), CirculantSpectrum::matvec restated
+// (src/structured.cpp:122-166), everything enqueued on `s`.
+void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
   const long long E = static_cast<long long>(nrhs) * op->b;
-  build_jobs(op, nrhs);
-  // fork: P2M + M2L on the aux stream while the near-field GEMM runs on the main one
-  check(cudaEventRecord(op->fork, s), "fork");
-  check(cudaStreamWaitEvent(a, op->fork, 0), "fork");
-  ev_record(op, 0, s);
-  check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n, op->pair_src,
-                          op->jobs, op->n_jobs, op->n, op->n, op->N, nrhs, s),
-        "near gemm");
-  op->launches += op->n_jobs > 0;
-  ev_record(op, 1, s);
-  ev_record(op, 2, a);
-  check(launch_block_gemm(op->v0, 0, op->b, op->b, x, op->mom, op->b, nullptr, op->jobs + op->n_jobs, op->n_p2m_jobs,
-                          op->n, op->n, op->N, nrhs, a),
-        "p2m");
-  op->launches++;
-  ev_record(op, 3, a);
-  s = a;  // the M2L passes below run on the aux stream
-
-  // pruned separable lattice DFT, per-mode product, pruned inverse
   const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
   struct Pass {
@@ -319,15 +352,50 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
     cur = out;
     which ^= 1;
   }
+}
+
+// One FMM product for nrhs <= max_rhs right-hand sides, device pointers.
+// Order of the sums follows src/fmm.cpp:253-267: y = S p, then y += U0 L.
+// With an offset partition (nranks > 1) this rank computes the product of
+// its own near-field offsets; rank 0 also adds the far field (P2M, M2L,
+// L2P); with a communicator the partial products are all-reduced.
+void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
+  cudaStream_t s = op->stream;
+  cudaStream_t a = op->aux;
+  const bool far_here = op->rank == 0;
+  build_jobs(op, nrhs);
+  // fork: P2M + M2L on the aux stream while the near-field GEMM runs on the main one
+  check(cudaEventRecord(op->fork, s), "fork");
+  check(cudaStreamWaitEvent(a, op->fork, 0), "fork");
+  ev_record(op, 0, s);
+  check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n, op->pair_src,
+                          op->jobs, op->n_jobs, op->n, op->n, op->N, nrhs, s),
+        "near gemm");
+  op->launches += op->n_jobs > 0;
+  ev_record(op, 1, s);
+  ev_record(op, 2, a);
+  if (far_here) {
+    check(launch_block_gemm(op->v0, 0, op->b, op->b, x, op->mom, op->b, nullptr, op->jobs + op->n_jobs,
+                            op->n_p2m_jobs, op->n, op->n, op->N, nrhs, a),
+          "p2m");
+    op->launches++;
+  }
+  ev_record(op, 3, a);
+  if (far_here) m2l_apply(op, nrhs, a);
   ev_record(op, 4, a);
   check(cudaEventRecord(op->join, a), "join");
   s = op->stream;
   check(cudaStreamWaitEvent(s, op->join, 0), "join");
   ev_record(op, 5, s);
-  check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, op->loc, y, op->n, op->b, op->n_cells,
-                               op->N, nrhs, false, s),
+  check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, far_here ? op->loc : nullptr, y, op->n,
+                               op->b, op->n_cells, op->N, nrhs, false, s),
         "near reduce + l2p");
   op->launches++;
+  if (op->comm) {  // sum the ranks' partial products, in place, on the same stream
+    const int rc = op->comm->allreduce(y, y, static_cast<size_t>(2) * op->N * nrhs, /*ncclFloat64*/ 8,
+                                       /*ncclSum*/ 0, op->comm->comm, s);
+    if (rc != 0) fail(FPBEM_CU_ENCCL, "ncclAllReduce failed: " + std::to_string(rc));
+  }
   ev_record(op, 6, s);
   if (op->timing) {
     check(cudaEventSynchronize(op->ev[6]), "timing sync");
@@ -615,7 +683,6 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->near_offsets.assign(d->near_offsets, d->near_offsets + 3 * d->n_near);
     const int* m = d->counts;
     std::vector<int> psrc;
-    std::vector<std::vector<int>> per_t(op->n_cells);
     op->pair_start.assign(1, 0);
     for (int s = 0; s < d->n_near; ++s) {
       const int ox = op->near_offsets[3 * s], oy = op->near_offsets[3 * s + 1], oz = op->near_offsets[3 * s + 2];
@@ -626,32 +693,20 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
           for (int tx = 0; tx < m[0]; ++tx) {
             const int sx = tx - ox, sy = ty - oy, sz = tz - oz;
             if (sx < 0 || sx >= m[0] || sy < 0 || sy >= m[1] || sz < 0 || sz >= m[2]) continue;
-            const int t = tx + m[0] * (ty + m[1] * tz);
-            per_t[t].push_back(static_cast<int>(psrc.size()));
+            op->pair_tgt.push_back(tx + m[0] * (ty + m[1] * tz));
             psrc.push_back(sx + m[0] * (sy + m[1] * sz));
           }
       op->pair_start.push_back(static_cast<int>(psrc.size()));
     }
     op->n_pairs = static_cast<int>(psrc.size());
-    std::vector<int> tptr(op->n_cells + 1, 0), tpairs;
-    tpairs.reserve(psrc.size());
-    for (int t = 0; t < op->n_cells; ++t) {
-      tpairs.insert(tpairs.end(), per_t[t].begin(), per_t[t].end());
-      tptr[t + 1] = static_cast<int>(tpairs.size());
-    }
     for (int s = 0; s < d->n_near; ++s) op->rank_slots.push_back(s);
     const size_t nn = static_cast<size_t>(op->n) * op->n;
     op->S = dalloc<c64>(nn * d->n_near, "near blocks");
     if (d->n_near > 0)
       h2d(op->S, d->near_blocks, nn * d->n_near * sizeof(c64), op->stream, "S upload");
     op->pair_src = dalloc<int>(psrc.size(), "pair sources");
-    op->tgt_ptr = dalloc<int>(tptr.size(), "target ptr");
-    op->tgt_pairs = dalloc<int>(tpairs.size(), "target pairs");
-    if (!psrc.empty()) {
-      h2d(op->pair_src, psrc.data(), psrc.size() * sizeof(int), op->stream, "pairs");
-      h2d(op->tgt_pairs, tpairs.data(), tpairs.size() * sizeof(int), op->stream, "pairs");
-    }
-    h2d(op->tgt_ptr, tptr.data(), tptr.size() * sizeof(int), op->stream, "ptr");
+    if (!psrc.empty()) h2d(op->pair_src, psrc.data(), psrc.size() * sizeof(int), op->stream, "pairs");
+    build_target_csr(op);
 
     // expansions
     const size_t nb = static_cast<size_t>(op->n) * op->b;
@@ -953,8 +1008,31 @@ void fpbem_cu_comm_destroy(fpbem_cu_comm* comm) {
 int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm) {
   return guard([&] {
     if (!op) fail(FPBEM_CU_EINVAL, "set_comm: null op");
+    check(cudaSetDevice(op->device), "set device");
+    if (!comm) {
+      op->comm = nullptr;
+      set_partition(op, 0, 1);
+      return;
+    }
+    set_partition(op, comm->rank, comm->nranks);
     op->comm = comm;
-    fail(FPBEM_CU_EINVAL, "set_comm: multi-GPU offset sharding not implemented yet");
+  });
+}
+
+int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks) {
+  return guard([&] {
+    if (!op) fail(FPBEM_CU_EINVAL, "set_partition: null op");
+    check(cudaSetDevice(op->device), "set device");
+    set_partition(op, rank, nranks);
+  });
+}
+
+int fpbem_cu_partition_offsets(int n_near, const long long* work, int nranks, int* owner) {
+  return guard([&] {
+    if (n_near < 0 || nranks < 1 || (n_near > 0 && (!work || !owner))) fail(FPBEM_CU_EINVAL, "partition: bad args");
+    std::vector<long long> w(work, work + n_near);
+    std::vector<int> o = partition_offsets(w, nranks);
+    std::copy(o.begin(), o.end(), owner);
   });
 }
 

@@ -55,9 +55,9 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int m0 = blockIdx.x * BM;
-  if (m0 >= M) return;
-  const int4 job = jobs[blockIdx.y];  // (block slot, first column, column count, pair base)
+  const int m_tiles = (M + BM - 1) / BM;
+  const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
+  const int4 job = jobs[blockIdx.x / m_tiles];  // (block slot, first column, column count, pair base)
   const int s = job.x, col0 = job.y, ncols = job.z, pair_base = job.w;
 
   if (tid < BN) {
@@ -191,9 +191,9 @@ near_gemm_mbar_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int m0 = blockIdx.x * BM;
-  if (m0 >= M) return;
-  const int4 job = jobs[blockIdx.y];
+  const int m_tiles = (M + BM - 1) / BM;
+  const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
+  const int4 job = jobs[blockIdx.x / m_tiles];
   const int s = job.x, col0 = job.y, ncols = job.z, pair_base = job.w;
 
   if (tid < BN) {
@@ -318,12 +318,13 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
                        const c64* __restrict__ local, c64* __restrict__ y, int n, int n_coef,
                        long long N, int nrhs, int accumulate) {
   __shared__ c64 loc[MAX_COEF];
-  const int tr = blockIdx.y;  // t * nrhs + r
+  const int row_tiles = (n + RED_THREADS - 1) / RED_THREADS;
+  const int tr = static_cast<int>(blockIdx.x / row_tiles);  // t * nrhs + r
   const int t = tr / nrhs, r = tr % nrhs;
   if (local != nullptr && threadIdx.x < n_coef)
     loc[threadIdx.x] = local[static_cast<size_t>(tr) * n_coef + threadIdx.x];
   __syncthreads();
-  const int i = blockIdx.x * RED_THREADS + threadIdx.x;
+  const int i = static_cast<int>(blockIdx.x % row_tiles) * RED_THREADS + threadIdx.x;
   if (i >= n) return;
   const int p0 = tgt_ptr[t], p1 = tgt_ptr[t + 1];
   c64 acc = cmk(0.0, 0.0);
@@ -379,7 +380,10 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
     configured = true;
   }
   if (n_jobs == 0) return cudaSuccess;
-  dim3 grid((M + BM - 1) / BM, n_jobs);
+  // 1-D grid, m-tiles of one job adjacent (they share the job's B columns in L2)
+  const long long ctas = static_cast<long long>((M + BM - 1) / BM) * n_jobs;
+  if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
+  dim3 grid(static_cast<unsigned>(ctas));
   if (use_mbar) {
     near_gemm_mbar_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src,
                                                                        jobs, K, n, N, nrhs);
@@ -394,7 +398,7 @@ cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* 
                                    const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
                                    int nrhs, bool accumulate, cudaStream_t stream) {
   if (n_coef > MAX_COEF) return cudaErrorInvalidValue;
-  dim3 grid((n + RED_THREADS - 1) / RED_THREADS, n_cells * nrhs);
+  dim3 grid(static_cast<unsigned>(static_cast<long long>((n + RED_THREADS - 1) / RED_THREADS) * n_cells * nrhs));
   near_reduce_l2p_kernel<<<grid, RED_THREADS, 0, stream>>>(W, tgt_ptr, tgt_pairs, u0, local, y, n, n_coef, N,
                                                            nrhs, accumulate ? 1 : 0);
   return cudaGetLastError();

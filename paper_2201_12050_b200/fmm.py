@@ -35,6 +35,40 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+def partition_offsets(work, nranks: int) -> np.ndarray:
+    """The library's offset-partition rule (host only): owner rank per offset."""
+    w = np.ascontiguousarray(work, np.int64)
+    owner = np.zeros(len(w), np.int32)
+    _raise(_native.cuda().fpbem_cu_partition_offsets(len(w), w.ctypes.data_as(C.POINTER(C.c_longlong)), nranks,
+                                                     owner.ctypes.data_as(_native.c_int_p)))
+    return owner
+
+
+class Communicator:
+    """NCCL communicator of the library (one process per GPU). The 128-byte
+    unique id travels over an initialised torch.distributed process group."""
+
+    def __init__(self, device: int, group=None):
+        import torch.distributed as dist
+
+        lib = _native.cuda()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _raise(lib.fpbem_cu_comm_unique_id(uid))
+        box = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = C.create_string_buffer(box[0], 128)
+        h = C.c_void_p()
+        _raise(lib.fpbem_cu_comm_init(uid, world, rank, device, C.byref(h)))
+        self.handle, self.rank, self.nranks = h, rank, world
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _native.cuda().fpbem_cu_comm_destroy(self.handle)
+            self.handle = None
+
+
 @dataclass
 class SolveReport:
     """include/fpbem/solver.hpp:14-19"""
@@ -119,6 +153,17 @@ class FmmOperators:
 
     def set_stream(self, stream_ptr: int | None) -> None:
         _raise(_native.cuda().fpbem_cu_set_stream(self._h, stream_ptr))
+
+    def set_partition(self, rank: int, nranks: int) -> None:
+        """Near-field offset partition without communication: matvec returns
+        this rank's partial product (rank 0 includes the far field)."""
+        _raise(_native.cuda().fpbem_cu_fmm_set_partition(self._h, rank, nranks))
+
+    def set_comm(self, comm) -> None:
+        """Attach a Communicator: offsets split across its ranks, partial
+        products all-reduced over NCCL inside every matvec."""
+        _raise(_native.cuda().fpbem_cu_fmm_set_comm(self._h, comm.handle if comm is not None else None))
+        self._comm = comm
 
     def kernel_launches(self) -> int:
         return int(_native.cuda().fpbem_cu_kernel_launches(self._h))

@@ -365,3 +365,54 @@ def test_fmm_gmres_nan_rhs_is_a_hard_error(ops, assembled):
     b[5] = np.nan
     with pytest.raises(RuntimeError, match="non-finite"):
         gmres(ops(d), b, tol=1e-6, restart=50, max_iter=50)
+
+
+# ---- multi-GPU decomposition, exercised on one GPU -------------------------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_partial_products_of_an_offset_partition_sum_to_the_product(ops, assembled, nranks):
+    """fpbem_cu_fmm_set_partition: every rank's partial product (own near-field
+    offsets; rank 0 adds P2M/M2L/L2P) summed over ranks == the full product.
+    Ranks run one after another on one GPU (no rank waits on another)."""
+    sc, d = assembled(3, 2)
+    rng = np.random.default_rng(3)
+    p = uvec(rng, d.N)
+    full = ops(d).matvec(p)
+    total = np.zeros_like(full)
+    for r in range(nranks):
+        op = ops(d)
+        op.set_partition(r, nranks)
+        total += op.matvec(p)
+        op.close()
+    assert rel(total, full) < 1e-13
+    assert rel(total, O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+def test_nccl_communicator_single_rank_path(ops, assembled):
+    """The NCCL all-reduce path of apply() with a 1-rank communicator."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2201_12050_b200.fmm import Communicator
+
+    sc, d = assembled(2, 2)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Communicator(device=0)
+        op = ops(d)
+        p = uvec(np.random.default_rng(9), d.N)
+        y0 = op.matvec(p)
+        op.set_comm(comm)
+        assert np.array_equal(op.matvec(p), y0)
+        from paper_2201_12050_b200 import gmres
+
+        rep = gmres(op, sc.rhs(0), tol=1e-6, restart=50, max_iter=400)
+        assert rep.converged
+        op.set_comm(None)
+        op.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
