@@ -211,23 +211,46 @@ void set_partition(fpbem_cu_op* op, int rank, int nranks) {
   build_target_csr(op);
 }
 
+// Column tiles of one offset (or of the P2M columns): as many 64-wide tiles as
+// fit, then the remainder as one 64- (49..63), 32+16- (33..48), 32- (17..32)
+// or 16-wide (1..16) tile. job.z = column count | width class << 8.
+void tile_columns(std::vector<int4>& jobs, int s, int cols, int pair_base, bool narrow) {
+  int c0 = 0;
+  auto push = [&](int w, int cls) {
+    jobs.push_back(make_int4(s, c0, w | (cls << 8), pair_base));
+    c0 += w;
+  };
+  while (cols - c0 >= 64) push(64, 0);
+  const int r = cols - c0;
+  if (r == 0) return;
+  if (!narrow || r > 48) {
+    push(r, 0);
+  } else if (r > 32) {
+    push(32, 1);
+    push(r - 32, 2);
+  } else if (r > 16) {
+    push(r, 1);
+  } else {
+    push(r, 2);
+  }
+}
+
 void build_jobs(fpbem_cu_op* op, int nrhs) {
   if (op->jobs_nrhs == nrhs) return;
-  const int bn = near_gemm_tile_cols();
+  const char* nv = std::getenv("FPBEM_NARROW_TILES");
+  const bool narrow = !(nv && std::strcmp(nv, "0") == 0) && !gemm_uses_mbar();
   std::vector<int4> jobs;
   for (int s : op->rank_slots) {
     const int pairs = op->pair_start[s + 1] - op->pair_start[s];
-    const int cols = pairs * nrhs;
-    for (int c0 = 0; c0 < cols; c0 += bn) jobs.push_back(make_int4(s, c0, std::min(bn, cols - c0), op->pair_start[s]));
+    tile_columns(jobs, s, pairs * nrhs, op->pair_start[s], narrow);
   }
   // offset order by default (consecutive tiles share S_o in L2);
   // FPBEM_JOB_ORDER=lpt puts the longest column tiles first (A/B timing)
   const char* order = std::getenv("FPBEM_JOB_ORDER");
   if (order && std::strcmp(order, "lpt") == 0)
-    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return (a.z & 0xff) > (b.z & 0xff); });
   const int n_near_jobs = static_cast<int>(jobs.size());
-  const int p2m_cols = op->n_cells * nrhs;
-  for (int c0 = 0; c0 < p2m_cols; c0 += bn) jobs.push_back(make_int4(0, c0, std::min(bn, p2m_cols - c0), 0));
+  tile_columns(jobs, 0, op->n_cells * nrhs, 0, narrow);
   if (static_cast<int>(jobs.size()) > op->jobs_cap) {
     if (op->jobs) cudaFree(op->jobs);
     op->jobs = dalloc<int4>(jobs.size(), "jobs");

@@ -35,6 +35,72 @@ constexpr int THREADS = 256;
 constexpr size_t kSmemA = sizeof(c64) * STAGES * BK * AP;
 constexpr size_t kSmemB = sizeof(c64) * STAGES * BN * BP;
 
+// K loop + epilogue of one CTA tile. Gauss 3-multiplication complex product
+// on the FP64 tensor cores: T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi);
+// Cr = T1 - T2, Ci = T3 - T1 - T2. MI 8x8 m-tiles per warp: warps form
+// (8 / MI) row groups x MI column slabs of 8, covering 64 rows x 8*MI columns.
+template <int MI, typename Loader>
+__device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& load_stage, int nk, int warp, int lane,
+                                          int ncols, int m0, int M, const long long* col_out, c64* __restrict__ out) {
+  constexpr int G = 8 / MI;  // row groups
+  const int wm = warp % G, wn = warp / G;
+  const int fr = lane >> 2, fk = lane & 3;
+  const bool active = wn * 8 < ncols;
+  double t1[MI][2], t2[MI][2], t3[MI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    t1[mi][0] = t1[mi][1] = 0.0;
+    t2[mi][0] = t2[mi][1] = 0.0;
+    t3[mi][0] = t3[mi][1] = 0.0;
+  }
+
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) load_stage(st, st);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int pf = kt + STAGES - 1;
+    if (pf < nk) load_stage(pf % STAGES, pf);
+    cp_async_commit();
+    if (!active) continue;
+
+    const c64* as = As + (kt % STAGES) * BK * AP + wm * (8 * MI);
+    const c64* bs = Bs + (kt % STAGES) * BN * BP;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const c64 b = bs[(wn * 8 + fr) * BP + k4 * 4 + fk];
+      const double bsum = b.x + b.y;
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const c64 a = as[(k4 * 4 + fk) * AP + mi * 8 + fr];
+        const double asum = a.x + a.y;
+        dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
+        dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
+        dmma884(t3[mi][0], t3[mi][1], asum, bsum);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (!active) return;
+
+  // epilogue: accumulator (row fr, cols 2*fk + {0,1}) of each 8x8 tile
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int gm = m0 + wm * (8 * MI) + mi * 8 + fr;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = wn * 8 + 2 * fk + j;
+      const long long o = col_out[c];
+      if (o >= 0) out[o + gm] = cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
+    }
+  }
+}
+
 // Batched block GEMM over (block, column-tile) jobs:
 //   out[col_out(c) + m] = sum_k A_s[m + lda k] * x[col_src(c) + k],  m < M, k < K
 // Near field: A_s = S_s (lda = M = K = n), columns = (pair, rhs) of offset s,
@@ -57,8 +123,8 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   const int lane = tid & 31, warp = tid >> 5;
   const int m_tiles = (M + BM - 1) / BM;
   const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
-  const int4 job = jobs[blockIdx.x / m_tiles];  // (block slot, first column, column count, pair base)
-  const int s = job.x, col0 = job.y, ncols = job.z, pair_base = job.w;
+  const int4 job = jobs[blockIdx.x / m_tiles];  // (block slot, first column, count | class << 8, pair base)
+  const int s = job.x, col0 = job.y, ncols = job.z & 0xff, cls = job.z >> 8, pair_base = job.w;
 
   if (tid < BN) {
     if (tid < ncols) {
@@ -107,65 +173,19 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
     }
   };
 
-  // Gauss 3-multiplication complex product on the FP64 tensor cores:
-  //   T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi);  Cr = T1 - T2, Ci = T3 - T1 - T2
-  // Each warp owns all 64 rows and one 8-column slab: 8 m-tiles x 3 partial products.
-  double t1[8][2], t2[8][2], t3[8][2];
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    t1[mi][0] = t1[mi][1] = 0.0;
-    t2[mi][0] = t2[mi][1] = 0.0;
-    t3[mi][0] = t3[mi][1] = 0.0;
-  }
-
-  const int wn = warp;  // 8-column slab
-  const int fr = lane >> 2, fk = lane & 3;
-  const bool active = wn * 8 < ncols;
-
-#pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage(st, st);
-    cp_async_commit();
-  }
-
-  for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int pf = kt + STAGES - 1;
-    if (pf < nk) load_stage(pf % STAGES, pf);
-    cp_async_commit();
-    if (!active) continue;
-
-    const c64* as = As + (kt % STAGES) * BK * AP;
-    const c64* bs = Bs + (kt % STAGES) * BN * BP;
-#pragma unroll
-    for (int k4 = 0; k4 < BK / 4; ++k4) {
-      const c64 b = bs[(wn * 8 + fr) * BP + k4 * 4 + fk];
-      const double bsum = b.x + b.y;
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const c64 a = as[(k4 * 4 + fk) * AP + mi * 8 + fr];
-        const double asum = a.x + a.y;
-        dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
-        dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
-        dmma884(t3[mi][0], t3[mi][1], asum, bsum);
-      }
-    }
-  }
-  cp_async_wait<0>();
-  if (!active) return;
-
-  // epilogue: accumulator (row fr, cols 2*fk + {0,1}) of each 8x8 tile
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    const int gm = m0 + mi * 8 + fr;
-    if (gm >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = wn * 8 + 2 * fk + j;
-      const long long o = col_out[c];
-      if (o >= 0) out[o + gm] = cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
-    }
+  // width class of the column tile: 0 -> 64 columns (each warp 64 rows x 8),
+  // 1 -> 32 columns (32 rows x 8), 2 -> 16 columns (16 rows x 8): narrow
+  // tiles keep all 8 warps busy instead of idling most of them
+  switch (cls) {
+    case 0:
+      gemm_main<8>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out);
+      break;
+    case 1:
+      gemm_main<4>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out);
+      break;
+    default:
+      gemm_main<2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out);
+      break;
   }
 }
 
@@ -194,7 +214,7 @@ near_gemm_mbar_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   const int m_tiles = (M + BM - 1) / BM;
   const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
   const int4 job = jobs[blockIdx.x / m_tiles];
-  const int s = job.x, col0 = job.y, ncols = job.z, pair_base = job.w;
+  const int s = job.x, col0 = job.y, ncols = job.z & 0xff, pair_base = job.w;  // width class ignored: 64-wide
 
   if (tid < BN) {
     if (tid < ncols) {
@@ -359,6 +379,10 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 size_t near_gemm_smem_bytes() { return kSmemA + kSmemB; }
 int near_gemm_tile_cols() { return BN; }
 int near_gemm_tile_rows() { return BM; }
+bool gemm_uses_mbar() {
+  const char* v = std::getenv("FPBEM_GEMM");
+  return v && std::strcmp(v, "mbar") == 0;
+}
 
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
