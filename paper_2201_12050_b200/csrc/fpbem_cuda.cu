@@ -331,7 +331,7 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
   const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
   struct Pass {
-    int kind;  // 0 dft, 1 mode product
+    int kind;  // 0 dft, 1 mode product, 2 fused z-dft + mode product + inverse z-dft
     long long n_a;
     int n_in, n_out;
     long long inner;
@@ -341,6 +341,11 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
   };
   std::vector<Pass> passes;
   long long cx = Mx, cy = My;  // current x / y extents
+  // z forward + mode product + z inverse fused into one kernel when the
+  // column's fields fit in shared memory (FPBEM_M2L_FUSE=0 disables)
+  const char* fz = std::getenv("FPBEM_M2L_FUSE");
+  const bool fuse_z = Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
+                      m2l_zfused_smem(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E)) <= 160 * 1024;
   if (Lx > 1) {
     passes.push_back({0, My * Mz, static_cast<int>(Mx), static_cast<int>(Lx), E, static_cast<int>(Lx), 0, false});
     cx = Lx;
@@ -349,14 +354,20 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
     passes.push_back({0, Mz, static_cast<int>(My), static_cast<int>(Ly), cx * E, static_cast<int>(Ly), 1, false});
     cy = Ly;
   }
-  if (Lz > 1) passes.push_back({0, 1, static_cast<int>(Mz), static_cast<int>(Lz), cy * cx * E, static_cast<int>(Lz), 2, false});
-  passes.push_back({1, 0, 0, 0, 0, 0, -1, false});
-  if (Lz > 1) passes.push_back({0, 1, static_cast<int>(Lz), static_cast<int>(Mz), Ly * Lx * E, static_cast<int>(Lz), 2, true});
+  if (fuse_z) {
+    passes.push_back({2, 0, 0, 0, 0, static_cast<int>(Lz), 2, false});
+  } else {
+    if (Lz > 1)
+      passes.push_back({0, 1, static_cast<int>(Mz), static_cast<int>(Lz), cy * cx * E, static_cast<int>(Lz), 2, false});
+    passes.push_back({1, 0, 0, 0, 0, 0, -1, false});
+    if (Lz > 1)
+      passes.push_back({0, 1, static_cast<int>(Lz), static_cast<int>(Mz), Ly * Lx * E, static_cast<int>(Lz), 2, true});
+  }
   if (Ly > 1) passes.push_back({0, Mz, static_cast<int>(Ly), static_cast<int>(My), Lx * E, static_cast<int>(Ly), 1, true});
   if (Lx > 1) passes.push_back({0, My * Mz, static_cast<int>(Lx), static_cast<int>(Mx), E, static_cast<int>(Lx), 0, true});
-  int last_dft = -1;
+  int last_dft = -1;  // the pass that applies the 1/q scale
   for (int i = 0; i < static_cast<int>(passes.size()); ++i)
-    if (passes[i].kind == 0 && passes[i].back) last_dft = i;
+    if ((passes[i].kind == 0 && passes[i].back) || passes[i].kind == 2) last_dft = i;
   const c64* cur = op->mom;
   c64* bufs[2] = {op->fa, op->fb};
   int which = 0;
@@ -366,6 +377,11 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
     c64* out = final ? op->loc : bufs[which];
     if (p.kind == 1) {
       check(launch_mode_product(op->lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
+    } else if (p.kind == 2) {
+      const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
+      check(launch_m2l_zfused(cur, out, op->lambda, op->tw[2], static_cast<int>(Mz), static_cast<int>(Lz), Ly * Lx,
+                              static_cast<int>(E), op->b, scale, s),
+            "m2l z-fused");
     } else {
       const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
       check(launch_dft_axis(cur, out, op->tw[p.axis], p.n_a, p.n_in, p.n_out, p.inner, p.L, p.back, scale, s),
@@ -691,7 +707,12 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->device = device;
     check(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
     op->own_stream = true;
-    check(cudaStreamCreateWithFlags(&op->aux, cudaStreamNonBlocking), "aux stream");
+    {  // aux stream (P2M + M2L) at the highest priority: its few CTAs are
+       // scheduled ahead of the near-field GEMM's as SM slots free up
+      int lo = 0, hi = 0;
+      check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+      check(cudaStreamCreateWithPriority(&op->aux, cudaStreamNonBlocking, hi), "aux stream");
+    }
     check(cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming), "event");
     check(cudaEventCreateWithFlags(&op->join, cudaEventDisableTiming), "event");
     for (int k = 0; k < 3; ++k) op->counts[k] = d->counts[k];

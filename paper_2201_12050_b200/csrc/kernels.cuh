@@ -25,6 +25,10 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
                             long long n_inner, int L, bool backward, double scale, cudaStream_t stream);
 cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image, long long q_total, int b,
                                 int nrhs, cudaStream_t stream);
+// fused forward-z DFT + mode product + inverse-z DFT, one CTA per (qy, qx) column
+size_t m2l_zfused_smem(int Mz, int Lz, int E);
+cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
+                              long long plane, int E, int b, double scale, cudaStream_t stream);
 cudaError_t launch_scatter_bank(const c64* blocks, const int* offsets, int n_blk, int b2, int lx, int ly, int lz,
                                 c64* field, cudaStream_t stream);
 

@@ -34,8 +34,25 @@ __global__ void dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ ou
     const c64* src = in + (a * n_in) * n_inner + inner;
     c64 acc = cmk(0.0, 0.0);
     int idx = 0;  // (j * qo) mod L, advanced incrementally
-    for (int j = 0; j < n_in; ++j) {
-      c64 w = tw[idx];
+    int j = 0;
+    // batches of 8 independent loads, accumulated in j order
+    for (; j + 8 <= n_in; j += 8) {
+      c64 v[8], w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = src[static_cast<long long>(j + u) * n_inner];
+        w[u] = __ldg(tw + idx);
+        idx += qo;
+        if (idx >= L) idx -= L;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (backward) w[u].y = -w[u].y;
+        acc = cfma(w[u], v[u], acc);
+      }
+    }
+    for (; j < n_in; ++j) {
+      c64 w = __ldg(tw + idx);
       if (backward) w.y = -w.y;
       acc = cfma(w, src[static_cast<long long>(j) * n_inner], acc);
       idx += qo;
@@ -61,6 +78,74 @@ __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* _
 #pragma unroll 5
     for (int j = 0; j < b; ++j) acc = cfma(__ldg(lam + static_cast<long long>(j) * b), f[j], acc);
     image[g] = acc;
+  }
+}
+
+// Last-axis fusion: forward DFT along z (Mz nonzero inputs -> Lz modes), the
+// per-mode product with Λ_q, and the pruned inverse along z (Lz modes -> Mz
+// kept outputs), for one (qy, qx) column per CTA. The z-extended field never
+// touches HBM; Λ is streamed once.
+//   in  : F2[iz][plane][E]   (iz < Mz)      out: H2[iz][plane][E] (iz < Mz)
+//   E = nrhs * b fields, plane = Ly * Lx columns, lambda[q][b*b], q = qz*plane + column
+__global__ void __launch_bounds__(256)
+m2l_zfused_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
+                  const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, double scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  c64* f_in = reinterpret_cast<c64*>(smem_raw);  // Mz x E
+  c64* f_z = f_in + Mz * E;                       // Lz x E  (forward along z)
+  c64* g_z = f_z + Lz * E;                        // Lz x E  (after the mode product)
+  const long long col = blockIdx.x;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < Mz * E; e += blockDim.x) {
+    const int iz = e / E, f = e % E;
+    f_in[e] = in[(static_cast<long long>(iz) * plane + col) * E + f];
+  }
+  __syncthreads();
+  for (int e = tid; e < Lz * E; e += blockDim.x) {
+    const int qz = e / E, f = e % E;
+    c64 acc = cmk(0.0, 0.0);
+    int idx = 0;
+    for (int iz = 0; iz < Mz; ++iz) {
+      acc = cfma(__ldg(tw + idx), f_in[iz * E + f], acc);
+      idx += qz;
+      if (idx >= Lz) idx -= Lz;
+    }
+    f_z[e] = acc;
+  }
+  __syncthreads();
+  // mode product: g[qz][r*b + i] = sum_c Λ_q[i + b c] f[qz][r*b + c]; lanes over i read Λ contiguously
+  const int nrhs = E / b;
+  for (int e = tid; e < Lz * E; e += blockDim.x) {
+    const int qz = e / E, ri = e % E;
+    const int r = ri / b, i = ri % b;
+    const c64* lam = lambda + (static_cast<long long>(qz) * plane + col) * b * b + i;
+    const c64* f = f_z + qz * E + r * b;
+    c64 acc = cmk(0.0, 0.0);
+    int c = 0;
+    for (; c + 5 <= b; c += 5) {
+      c64 l[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) l[u] = __ldg(lam + static_cast<long long>(c + u) * b);
+#pragma unroll
+      for (int u = 0; u < 5; ++u) acc = cfma(l[u], f[c + u], acc);
+    }
+    for (; c < b; ++c) acc = cfma(__ldg(lam + static_cast<long long>(c) * b), f[c], acc);
+    g_z[e] = acc;
+  }
+  (void)nrhs;
+  __syncthreads();
+  for (int e = tid; e < Mz * E; e += blockDim.x) {
+    const int iz = e / E, f = e % E;
+    c64 acc = cmk(0.0, 0.0);
+    int idx = 0;
+    for (int qz = 0; qz < Lz; ++qz) {
+      c64 w = __ldg(tw + idx);
+      w.y = -w.y;
+      acc = cfma(w, g_z[qz * E + f], acc);
+      idx += iz;
+      if (idx >= Lz) idx -= Lz;
+    }
+    out[(static_cast<long long>(iz) * plane + col) * E + f] = cscale(acc, scale);
   }
 }
 
@@ -104,6 +189,23 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
                                 int nrhs, cudaStream_t stream) {
   const long long total = q_total * b * nrhs;
   mode_product_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lambda, field, image, q_total, b, nrhs);
+  return cudaGetLastError();
+}
+
+size_t m2l_zfused_smem(int Mz, int Lz, int E) { return sizeof(c64) * static_cast<size_t>(Mz + 2 * Lz) * E; }
+
+cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
+                              long long plane, int E, int b, double scale, cudaStream_t stream) {
+  const size_t smem = m2l_zfused_smem(Mz, Lz, E);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(m2l_zfused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  m2l_zfused_kernel<<<static_cast<unsigned>(plane), 256, smem, stream>>>(in, out, lambda, tw, Mz, Lz, plane, E, b,
+                                                                         scale);
   return cudaGetLastError();
 }
 
