@@ -480,20 +480,23 @@ void ensure_gmres(fpbem_cu_op* op, int restart) {
     op->gb = dalloc<c64>(op->N, "gmres b");
     op->gt = dalloc<c64>(op->N, "gmres tmp");
     op->gsol = dalloc<c64>(op->N, "gmres solution");
-    op->scal_d = dalloc<double>(8, "gmres scalars");
-    op->flag = dalloc<int>(1, "gmres flag");
-    op->rs.partial_d = dalloc<double>(kRedBlocks, "reduction partials");
-    op->rs.partial_c = dalloc<c64>(kRedBlocks, "reduction partials");
+    op->rs.partial_d = dalloc<double>(2 * kRedBlocks, "reduction partials");
+    op->rs.partial_c = dalloc<c64>(2 * kRedBlocks, "reduction partials");
     op->rs.counter = dalloc<unsigned>(1, "reduction counter");
     check(cudaMemsetAsync(op->rs.counter, 0, sizeof(unsigned), op->stream), "counter init");
     check(cudaStreamSynchronize(op->stream), "counter init");
   }
   if (op->scal_cap < cols) {
+    // one contiguous block so a single read-back per Arnoldi step returns the
+    // non-finite flag, both norms and the projections: 128-byte header
+    // (doubles 0..7, int flag at byte 64), then h[cols], hc[cols], y[cols]
     if (op->scal_c) cudaFree(op->scal_c);
-    op->scal_c = dalloc<c64>(3 * static_cast<size_t>(cols), "gmres coefficients");
+    op->scal_c = dalloc<c64>(8 + 3 * static_cast<size_t>(cols), "gmres scalars");
     op->scal_cap = cols;
+    op->scal_d = reinterpret_cast<double*>(op->scal_c);
+    op->flag = reinterpret_cast<int*>(op->scal_d + 8);
   }
-  ensure_pinned(op, sizeof(c64) * 3 * cols + 64);
+  ensure_pinned(op, sizeof(c64) * (8 + 3 * static_cast<size_t>(cols)) + 64);
 }
 
 struct GmresOut {
@@ -514,9 +517,9 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
   ensure_gmres(op, std::max(1, restart));
   c64* V = op->basis;
   auto col = [&](int j) { return V + static_cast<long long>(j) * n; };
-  c64* h = op->scal_c;                   // pass-1 projections
-  c64* hc = op->scal_c + op->scal_cap;   // pass-2 corrections
-  c64* ydev = op->scal_c + 2 * op->scal_cap;
+  c64* h = op->scal_c + 8;                    // pass-1 projections (after the 128-byte header)
+  c64* hc = h + op->scal_cap;                  // pass-2 corrections
+  c64* ydev = hc + op->scal_cap;
   double* sd = op->scal_d;
   char* pin = static_cast<char*>(op->pinned);
   auto fetch = [&](const void* src, size_t bytes) {
@@ -528,15 +531,6 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
     double v;
     std::memcpy(&v, pin, sizeof(double));
     return v;
-  };
-  auto check_finite = [&]() {
-    int f;
-    fetch(op->flag, sizeof(int));
-    std::memcpy(&f, pin, sizeof(int));
-    if (f) {
-      check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
-      fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
-    }
   };
 
   check(cudaMemsetAsync(x_dev, 0, n * sizeof(c64), s), "x0");
@@ -566,31 +560,50 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
     for (; j < m && rep.iterations < max_iter; ++j) {
       c64* w = col(j + 1);
       apply(col(j), w);
-      check(launch_sqnorm(w, n, op->rs, sd + 0, op->flag, s), "pre norm");
-      // MGS: h_0 = <v_0,w>; (w -= h_i v_i, h_{i+1} = <v_{i+1}, w>)...; w -= h_j v_j, ||w||^2
-      check(launch_dotc(col(0), w, n, op->rs, h + 0, s), "mgs dot");
-      for (int i = 0; i < j; ++i)
-        check(launch_axpy_dotc(w, col(i), h + i, col(i + 1), n, op->rs, h + i + 1, s), "mgs step");
-      check(launch_axpy_sqnorm(w, col(j), h + j, n, op->rs, sd + 1, s), "mgs last");
-      op->launches += j + 3;
-      check_finite();
-      fetch(sd, 2 * sizeof(double));
+      const bool fused = mgs_fused_supported(n);
+      if (fused) {  // pre-norm + all j+1 MGS steps + post-norm in one cooperative launch
+        check(launch_mgs_fused(w, V, n, j, n, h, sd, op->flag, op->rs, true, s), "mgs fused");
+        op->launches++;
+      } else {
+        check(launch_sqnorm(w, n, op->rs, sd + 0, op->flag, s), "pre norm");
+        // MGS: h_0 = <v_0,w>; (w -= h_i v_i, h_{i+1} = <v_{i+1}, w>)...; w -= h_j v_j, ||w||^2
+        check(launch_dotc(col(0), w, n, op->rs, h + 0, s), "mgs dot");
+        for (int i = 0; i < j; ++i)
+          check(launch_axpy_dotc(w, col(i), h + i, col(i + 1), n, op->rs, h + i + 1, s), "mgs step");
+        check(launch_axpy_sqnorm(w, col(j), h + j, n, op->rs, sd + 1, s), "mgs last");
+        op->launches += j + 3;
+      }
+      // one read-back: flag, ||w||^2 before and after MGS, h_0..h_j
+      fetch(sd, 128 + sizeof(c64) * (j + 1));
+      {
+        int fl;
+        std::memcpy(&fl, pin + 64, sizeof(int));
+        if (fl) {
+          check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
+          fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+        }
+      }
       double pre2, post2;
       std::memcpy(&pre2, pin, sizeof(double));
       std::memcpy(&post2, pin + sizeof(double), sizeof(double));
-      fetch(h, sizeof(c64) * (j + 1));
       for (int i = 0; i <= j; ++i) {
         c64 v;
-        std::memcpy(&v, pin + i * sizeof(c64), sizeof(c64));
+        std::memcpy(&v, pin + 128 + i * sizeof(c64), sizeof(c64));
         Hm(i, j) = cd(v.x, v.y);
       }
       double wnorm2 = post2;
       if (std::sqrt(post2) < 0.5 * std::sqrt(pre2)) {  // reorthogonalisation (:63-69)
-        check(launch_dotc(col(0), w, n, op->rs, hc + 0, s), "reorth dot");
-        for (int i = 0; i < j; ++i)
-          check(launch_axpy_dotc(w, col(i), hc + i, col(i + 1), n, op->rs, hc + i + 1, s), "reorth step");
-        check(launch_axpy_sqnorm(w, col(j), hc + j, n, op->rs, sd + 2, s), "reorth last");
-        op->launches += j + 2;
+        if (fused) {
+          check(launch_mgs_fused(w, V, n, j, n, hc, sd + 4, op->flag, op->rs, false, s), "reorth fused");
+          check(cudaMemcpyAsync(sd + 2, sd + 5, sizeof(double), cudaMemcpyDeviceToDevice, s), "reorth norm");
+          op->launches++;
+        } else {
+          check(launch_dotc(col(0), w, n, op->rs, hc + 0, s), "reorth dot");
+          for (int i = 0; i < j; ++i)
+            check(launch_axpy_dotc(w, col(i), hc + i, col(i + 1), n, op->rs, hc + i + 1, s), "reorth step");
+          check(launch_axpy_sqnorm(w, col(j), hc + j, n, op->rs, sd + 2, s), "reorth last");
+          op->launches += j + 2;
+        }
         fetch(hc, sizeof(c64) * (j + 1));
         for (int i = 0; i <= j; ++i) {
           c64 v;
@@ -656,8 +669,18 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
     check(launch_sqnorm(op->gt, n, op->rs, sd + 2, op->flag, s), "residual finite check");
     check(launch_residual(b_dev, op->gt, op->gx, n, op->rs, sd + 3, s), "residual");
     op->launches += 2;
-    check_finite();
-    rnorm = std::sqrt(fetch_d(3));
+    fetch(sd, 128);  // flag + ||r||^2 in one read-back
+    {
+      int fl;
+      std::memcpy(&fl, pin + 64, sizeof(int));
+      if (fl) {
+        check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
+        fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+      }
+      double r2;
+      std::memcpy(&r2, pin + 3 * sizeof(double), sizeof(double));
+      rnorm = std::sqrt(r2);
+    }
     r = op->gx;
     if (rnorm / bnorm <= tol) {
       rep.converged = true;
@@ -795,8 +818,7 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
                   static_cast<void*>(op->mom), static_cast<void*>(op->loc), static_cast<void*>(op->fa),
                   static_cast<void*>(op->fb), static_cast<void*>(op->xin), static_cast<void*>(op->yout),
                   static_cast<void*>(op->basis), static_cast<void*>(op->gx), static_cast<void*>(op->gb),
-                  static_cast<void*>(op->gt), static_cast<void*>(op->gsol), static_cast<void*>(op->scal_c), static_cast<void*>(op->scal_d),
-                  static_cast<void*>(op->flag), static_cast<void*>(op->rs.partial_d),
+                  static_cast<void*>(op->gt), static_cast<void*>(op->gsol), static_cast<void*>(op->scal_c), static_cast<void*>(op->rs.partial_d),
                   static_cast<void*>(op->rs.partial_c), static_cast<void*>(op->rs.counter)})
     if (p) cudaFree(p);
   if (op->pinned) cudaFreeHost(op->pinned);

@@ -50,6 +50,11 @@ cudaError_t launch_axpy_sqnorm(c64* w, const c64* v, const c64* h, long long n, 
 cudaError_t launch_div(const c64* in, c64* out, long long n, double d, cudaStream_t s);
 cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y, int j, long long n,
                             cudaStream_t s);
+// whole MGS sequence of one Arnoldi step in one cooperative launch:
+// norms[0] = ||w||^2 (if do_pre, + non-finite flag), h_out[0..j], norms[1] = ||w||^2 after
+bool mgs_fused_supported(long long n);
+cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
+                             int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s);
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
                             double* result, cudaStream_t s);
 

@@ -5,8 +5,12 @@
 // last block to finish (counter) sums the per-block partials in index order.
 // The MGS step is fused so that the update w -= h_i v_i and the next
 // projection <v_{i+1}, w> (or the norm ||w|| after the last one) are one pass.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fpbem_cu {
 
@@ -60,19 +64,35 @@ __device__ void finish_reduce(T block_sum, T* partials, unsigned* counter, T* re
   }
 }
 
+// Grid-stride loops are unrolled by 4 (independent loads in flight); the
+// per-thread partial sums are still accumulated in a fixed order.
+#define GRID_STRIDE_4(i, n, BODY)                                                        \
+  {                                                                                      \
+    const long long stride_ = static_cast<long long>(gridDim.x) * RT;                    \
+    long long i0_ = blockIdx.x * static_cast<long long>(RT) + threadIdx.x;               \
+    for (; i0_ + 3 * stride_ < (n); i0_ += 4 * stride_) {                                \
+      _Pragma("unroll") for (int u_ = 0; u_ < 4; ++u_) {                                 \
+        const long long i = i0_ + u_ * stride_;                                          \
+        BODY                                                                             \
+      }                                                                                  \
+    }                                                                                    \
+    for (long long i = i0_; i < (n); i += stride_) {                                     \
+      BODY                                                                               \
+    }                                                                                    \
+  }
+
 // result = ||w||^2 ; flag |= non-finite entry present
 __global__ void __launch_bounds__(RT) sqnorm_kernel(const c64* __restrict__ w, long long n, double* partials,
                                                     unsigned* counter, double* result, int* nonfinite) {
   __shared__ double sh[RT];
   double s = 0.0;
   bool bad = false;
-  for (long long i = blockIdx.x * static_cast<long long>(RT) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * RT) {
+  GRID_STRIDE_4(i, n, {
     c64 v = w[i];
     bad |= !isfinite(v.x) || !isfinite(v.y);
     s = fma(v.x, v.x, s);
     s = fma(v.y, v.y, s);
-  }
+  })
   if (bad && nonfinite) atomicOr(nonfinite, 1);
   double b = block_reduce(s, sh);
   finish_reduce(b, partials, counter, result, sh);
@@ -83,9 +103,7 @@ __global__ void __launch_bounds__(RT) dotc_kernel(const c64* __restrict__ a, con
                                                   long long n, c64* partials, unsigned* counter, c64* result) {
   __shared__ c64 sh[RT];
   c64 s = cmk(0.0, 0.0);
-  for (long long i = blockIdx.x * static_cast<long long>(RT) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * RT)
-    s = cfma_conj(a[i], b[i], s);
+  GRID_STRIDE_4(i, n, { s = cfma_conj(a[i], b[i], s); })
   c64 t = block_reduce(s, sh);
   finish_reduce(t, partials, counter, result, sh);
 }
@@ -98,12 +116,11 @@ __global__ void __launch_bounds__(RT) axpy_dotc_kernel(c64* __restrict__ w, cons
   __shared__ c64 sh[RT];
   const c64 hh = *h;
   c64 s = cmk(0.0, 0.0);
-  for (long long i = blockIdx.x * static_cast<long long>(RT) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * RT) {
+  GRID_STRIDE_4(i, n, {
     c64 wi = csub(w[i], cmul(hh, v[i]));
     w[i] = wi;
     s = cfma_conj(vn[i], wi, s);
-  }
+  })
   c64 t = block_reduce(s, sh);
   finish_reduce(t, partials, counter, result, sh);
 }
@@ -115,13 +132,12 @@ __global__ void __launch_bounds__(RT) axpy_sqnorm_kernel(c64* __restrict__ w, co
   __shared__ double sh[RT];
   const c64 hh = *h;
   double s = 0.0;
-  for (long long i = blockIdx.x * static_cast<long long>(RT) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * RT) {
+  GRID_STRIDE_4(i, n, {
     c64 wi = csub(w[i], cmul(hh, v[i]));
     w[i] = wi;
     s = fma(wi.x, wi.x, s);
     s = fma(wi.y, wi.y, s);
-  }
+  })
   double t = block_reduce(s, sh);
   finish_reduce(t, partials, counter, result, sh);
 }
@@ -152,15 +168,117 @@ __global__ void __launch_bounds__(RT) residual_kernel(const c64* __restrict__ b,
                                                       unsigned* counter, double* result) {
   __shared__ double sh[RT];
   double s = 0.0;
-  for (long long i = blockIdx.x * static_cast<long long>(RT) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * RT) {
+  GRID_STRIDE_4(i, n, {
     c64 v = csub(b[i], ax[i]);
     r[i] = v;
     s = fma(v.x, v.x, s);
     s = fma(v.y, v.y, s);
-  }
+  })
   double t = block_reduce(s, sh);
   finish_reduce(t, partials, counter, result, sh);
+}
+
+// ---------------------------------------------------------------------------
+// Fused modified Gram-Schmidt of one Arnoldi step in a single cooperative
+// launch: ||w||^2 (+ non-finite flag), then for i = 0..j
+//   h_i = <v_i, w>;  w -= h_i v_i          (src/solver.cpp:58-62, same order)
+// and finally ||w||^2. Each block keeps its contiguous chunk of w in shared
+// memory for the whole sequence, each step streams v_i once; a grid-wide sync
+// separates a dot from its update. Every block folds all block partials in
+// index order, so h_i is bitwise identical everywhere and deterministic.
+__global__ void __launch_bounds__(RT, 2)
+mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, int j, long long n, long long chunk,
+                 c64* __restrict__ h_out, double* __restrict__ norms, int* __restrict__ nonfinite,
+                 c64* __restrict__ part_c, double* __restrict__ part_d, int do_pre) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  c64* ws = reinterpret_cast<c64*>(smem_raw);
+  __shared__ c64 shc[RT];
+  __shared__ double shd[RT];
+  __shared__ c64 bcast_c;
+  __shared__ double bcast_d;
+  const int G = gridDim.x;
+  const long long start = blockIdx.x * chunk;
+  const int len = static_cast<int>(max(0LL, min(chunk, n - start)));
+  for (int e = threadIdx.x; e < len; e += RT) ws[e] = w[start + e];
+  __syncthreads();
+
+  auto fold_d = [&](double v, double* slot) -> double {  // block partial -> grid total
+    const double b = block_reduce(v, shd);
+    if (threadIdx.x == 0) slot[blockIdx.x] = b;
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double acc = 0.0;
+      for (int i = threadIdx.x; i < G; i += 32) acc += slot[i];
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+      if (threadIdx.x == 0) bcast_d = acc;
+    }
+    __syncthreads();
+    return bcast_d;
+  };
+
+  if (do_pre) {
+    double s = 0.0;
+    bool bad = false;
+    for (int e = threadIdx.x; e < len; e += RT) {
+      const c64 v = ws[e];
+      bad |= !isfinite(v.x) || !isfinite(v.y);
+      s = fma(v.x, v.x, s);
+      s = fma(v.y, v.y, s);
+    }
+    if (bad) atomicOr(nonfinite, 1);
+    const double tot = fold_d(s, part_d);
+    if (blockIdx.x == 0 && threadIdx.x == 0) norms[0] = tot;
+  }
+
+  for (int i = 0; i <= j; ++i) {
+    const c64* vi = V + static_cast<long long>(i) * ld + start;
+    c64 s = cmk(0.0, 0.0);
+    int e = threadIdx.x;
+    for (; e + 3 * RT < len; e += 4 * RT) {
+      c64 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = vi[e + u * RT];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s = cfma_conj(v[u], ws[e + u * RT], s);
+    }
+    for (; e < len; e += RT) s = cfma_conj(vi[e], ws[e], s);
+    const c64 b = block_reduce(s, shc);
+    c64* slot = part_c + (i & 1) * G;
+    if (threadIdx.x == 0) slot[blockIdx.x] = b;
+    grid.sync();
+    if (threadIdx.x < 32) {
+      c64 acc = cmk(0.0, 0.0);
+      for (int q = threadIdx.x; q < G; q += 32) acc = cadd(acc, slot[q]);
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.x += __shfl_down_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_down_sync(0xffffffffu, acc.y, off);
+      }
+      if (threadIdx.x == 0) bcast_c = acc;
+    }
+    __syncthreads();
+    const c64 h = bcast_c;
+    if (blockIdx.x == 0 && threadIdx.x == 0) h_out[i] = h;
+    for (e = threadIdx.x; e + 3 * RT < len; e += 4 * RT) {
+      c64 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = vi[e + u * RT];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ws[e + u * RT] = csub(ws[e + u * RT], cmul(h, v[u]));
+    }
+    for (; e < len; e += RT) ws[e] = csub(ws[e], cmul(h, vi[e]));
+    // each thread only touches its own ws entries: no barrier needed before the next dot
+  }
+
+  double s = 0.0;
+  for (int e = threadIdx.x; e < len; e += RT) {
+    const c64 v = ws[e];
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+    w[start + e] = v;
+  }
+  const double tot = fold_d(s, part_d + G);
+  if (blockIdx.x == 0 && threadIdx.x == 0) norms[1] = tot;
 }
 
 int ew_grid(long long n) {
@@ -201,6 +319,36 @@ cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y
   update_x_kernel<<<ew_grid(n), 256, 0, s>>>(x, basis, ld, y, j, n);
   return cudaGetLastError();
 }
+namespace {
+constexpr long long kMgsMaxChunk = 6500;  // complex per block: 2 x (104 KB + 6 KB static) smem per SM
+}
+
+bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kRedBlocks) * kMgsMaxChunk; }
+
+cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
+                             int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s) {
+  // cooperative launch: every block co-resident (2 per SM)
+  long long blocks = (n + 1023) / 1024;
+  if (blocks > kRedBlocks) blocks = kRedBlocks;
+  if (blocks < 1) blocks = 1;
+  long long chunk = (n + blocks - 1) / blocks;
+  if (chunk > kMgsMaxChunk) return cudaErrorInvalidValue;
+  size_t smem = static_cast<size_t>(chunk) * sizeof(c64);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(mgs_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMgsMaxChunk * sizeof(c64)));
+    if (e != cudaSuccess) return e;
+    configured = kMgsMaxChunk * sizeof(c64);
+  }
+  int pre = do_pre ? 1 : 0;
+  c64* pc = rs.partial_c;
+  double* pd = rs.partial_d;
+  void* args[] = {&w, const_cast<c64**>(&V), &ld, &j, &n, &chunk, &h_out, &norms, &nonfinite, &pc, &pd, &pre};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&mgs_fused_kernel), dim3(static_cast<unsigned>(blocks)),
+                                     dim3(RT), args, smem, s);
+}
+
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
                             double* result, cudaStream_t s) {
   residual_kernel<<<kRedBlocks, RT, 0, s>>>(b, ax, r, n, rs.partial_d, rs.counter, result);

@@ -1,0 +1,37 @@
+"""Profiling driver: one GMRES solve (capped iterations) of a configuration."""
+import argparse
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from tools.profile_matvec import Synthetic  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--restart", type=int, default=50)
+    args = ap.parse_args()
+    import torch
+
+    from paper_2201_12050_b200 import FmmOperators, Scene, gmres
+
+    sc = Scene(args.config, 0)
+    data = sc.assemble_fmm(4)
+    op = FmmOperators(data)
+    b = torch.from_numpy(sc.rhs(0)).cuda()
+    gmres(op, b, tol=1e-12, restart=args.restart, max_iter=3)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    rep = gmres(op, b, tol=1e-12, restart=args.restart, max_iter=args.iters)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    print(f"{rep.iterations} iterations in {dt * 1e3:.2f} ms = {dt / rep.iterations * 1e3:.3f} ms/iteration")
+
+
+if __name__ == "__main__":
+    main()
