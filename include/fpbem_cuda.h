@@ -76,8 +76,18 @@ typedef struct {
   const int* far_offsets;        /* n_far x 3                                             */
   const fpbem_c64* far_blocks;   /* n_far x n_coef^2 M2L bank K, column-major; the device
                                     builds the spectrum (src/structured.cpp:63-108)        */
-  int mirrored_level;            /* -1: no half-space image pair (only value supported)   */
+  int mirrored_level;            /* -1: no half-space image pair; else the mirrored level  */
   int max_rhs;                   /* largest nrhs passed to apply/gmres (workspace sizing)  */
+  /* half-space image pair (FmmOperators::near_field_image / k_image_spectrum,
+   * include/fpbem/fmm.hpp:66-68), used when mirrored_level >= 0. Indices are
+   * the reference's BlockHankelMatrix indices: the cell-index SUM in
+   * [0, 2M-2] along the mirrored level, offsets target - source elsewhere. */
+  int n_hat;                     /* S_hat blocks                                           */
+  const int* hat_indices;        /* n_hat x 3                                              */
+  const fpbem_c64* hat_blocks;   /* n_hat x n_dof^2, column-major                          */
+  int n_far_hat;                 /* K_hat bank (the device builds the spectrum of K_hat P) */
+  const int* far_hat_indices;    /* n_far_hat x 3                                          */
+  const fpbem_c64* far_hat_blocks; /* n_far_hat x n_coef^2                                 */
 } fpbem_cu_fmm_desc;
 
 int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* desc, int device, fpbem_cu_op** out);

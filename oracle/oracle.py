@@ -184,6 +184,21 @@ class OracleFmm:
         self.N = int(np.prod(data.counts)) * int(data.n_dof)
         self._h = C.c_void_p(lib().oracle_fmm_create(cp, int(data.n_dof), int(data.n_coef), len(no), nop, nbp, u0p,
                                                       v0p, szp, lamp))
+        level = int(getattr(data, "mirrored_level", -1))
+        if level >= 0:
+            # S_hat (block Hankel) and the spectrum of K_hat P (src/structured.cpp:185-198):
+            # offsets o = idx with o[level] = idx[level] - (M - 1)
+            counts = tuple(int(c) for c in data.counts)
+            hi, hip = _i(np.asarray(data.hat_indices).reshape(-1, 3))
+            hb, hbp = _c(data.hat_blocks)
+            offs = np.asarray(data.far_hat_indices, np.int32).reshape(-1, 3).copy()
+            offs[:, level] -= counts[level] - 1
+            isz, ilam = spectrum_build(counts, offs, data.far_hat_blocks)
+            iszv, iszp = _i(isz)
+            il, ilp = _c(ilam)
+            self.image_sizes, self.image_lambda = isz, il
+            self._keep += [hi, hb, iszv, il]
+            _check(lib().oracle_fmm_set_image(self._h, level, len(hi), hip, hbp, iszp, ilp))
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -46,6 +46,12 @@ class FmmDesc(C.Structure):
         ("far_blocks", C.c_void_p),
         ("mirrored_level", C.c_int),
         ("max_rhs", C.c_int),
+        ("n_hat", C.c_int),
+        ("hat_indices", C.c_void_p),
+        ("hat_blocks", C.c_void_p),
+        ("n_far_hat", C.c_int),
+        ("far_hat_indices", C.c_void_p),
+        ("far_hat_blocks", C.c_void_p),
     ]
 
 
@@ -114,6 +120,9 @@ def host() -> C.CDLL:
             "fh_scene_destroy": (None, [vp]),
             "fh_scene_info": (None, [vp, c_int_p, c_double_p]),
             "fh_scene_set_k": (None, [vp, C.c_double]),
+            "fh_scene_set_halfspace": (None, [vp, C.c_int, C.c_double, C.c_double, C.c_double]),
+            "fh_scene_shift_cell": (None, [vp, c_double_p]),
+            "fh_fmm_image_arrays": (None, [vp] + [C.POINTER(vp)] * 4),
             "fh_scene_sweep": (None, [vp, c_double_p]),
             "fh_scene_set_sources": (None, [vp, C.c_int, c_int_p, c_double_p]),
             "fh_scene_rhs": (C.c_int, [vp, C.c_int, vp]),

@@ -123,6 +123,13 @@ struct fpbem_cu_op {
   long long q_total = 1;
   c64* lambda = nullptr;
   c64* tw[3] = {nullptr, nullptr, nullptr};
+  // half-space image pair: S_hat blocks live in S after the n_near Toeplitz
+  // slots (Hankel-indexed pairs); lambda_hat is the spectrum of K_hat P
+  int mirrored_level = -1;
+  int n_hat = 0;
+  c64* lambda_hat = nullptr;
+  c64* mom_perm = nullptr;
+  c64* loc_hat = nullptr;
 
   // per-apply buffers (sized for max_rhs)
   c64* W = nullptr;
@@ -272,27 +279,28 @@ void twiddles(fpbem_cu_op* op, int L, c64** out) {
   h2d(*out, t.data(), L * sizeof(c64), op->stream, "twiddle upload");
 }
 
-// lattice DFT of the embedded K column on the device (src/structured.cpp:63-108)
-void build_spectrum(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
+// lattice DFT of the embedded K column on the device (src/structured.cpp:63-108):
+// scatter the n_far bank blocks to slot (o mod L), DFT over every axis
+void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fpbem_c64* far_blocks,
+                    const fpbem_c64* prebuilt, c64** out) {
   const int b2 = op->b * op->b;
   const size_t total = static_cast<size_t>(op->q_total) * b2;
-  op->lambda = dalloc<c64>(total, "spectrum");
-  if (d->lambda) {
-    h2d(op->lambda, d->lambda, total * sizeof(c64), op->stream, "spectrum upload");
+  c64* lam = dalloc<c64>(total, "spectrum");
+  *out = lam;
+  if (prebuilt) {
+    h2d(lam, prebuilt, total * sizeof(c64), op->stream, "spectrum upload");
     return;
   }
   c64* tmp = dalloc<c64>(total, "spectrum scratch");
-  c64* blocks = dalloc<c64>(static_cast<size_t>(d->n_far) * b2, "far bank");
-  int* offs = dalloc<int>(static_cast<size_t>(d->n_far) * 3, "far offsets");
-  if (d->n_far > 0) {
-    h2d(blocks, d->far_blocks, static_cast<size_t>(d->n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
-    h2d(offs, d->far_offsets, static_cast<size_t>(d->n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
+  c64* blocks = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
+  int* offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
+  if (n_far > 0) {
+    h2d(blocks, far_blocks, static_cast<size_t>(n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
+    h2d(offs, far_offsets, static_cast<size_t>(n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
   }
-  check(cudaMemsetAsync(op->lambda, 0, total * sizeof(c64), op->stream), "spectrum clear");
-  check(launch_scatter_bank(blocks, offs, d->n_far, b2, op->L[0], op->L[1], op->L[2], op->lambda, op->stream),
-        "scatter bank");
-  // forward DFT over every axis of the full embedding (all L inputs)
-  c64* cur = op->lambda;
+  check(cudaMemsetAsync(lam, 0, total * sizeof(c64), op->stream), "spectrum clear");
+  check(launch_scatter_bank(blocks, offs, n_far, b2, op->L[0], op->L[1], op->L[2], lam, op->stream), "scatter bank");
+  c64* cur = lam;
   c64* nxt = tmp;
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
   if (Lx > 1) {
@@ -310,9 +318,8 @@ void build_spectrum(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
           "spectrum dft z");
     std::swap(cur, nxt);
   }
-  if (cur != op->lambda) {
-    check(cudaMemcpyAsync(op->lambda, cur, total * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "spectrum copy");
-  }
+  if (cur != lam)
+    check(cudaMemcpyAsync(lam, cur, total * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "spectrum copy");
   check(cudaStreamSynchronize(op->stream), "spectrum build");
   cudaFree(tmp);
   cudaFree(blocks);
@@ -326,7 +333,7 @@ void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {
 // Pruned separable lattice DFT, per-mode product, pruned inverse:
 // moments (op->mom) -> locals (op->loc), CirculantSpectrum::matvec restated
 // (src/structured.cpp:122-166), everything enqueued on `s`.
-void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
+void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, const c64* lambda, c64* locals) {
   const long long E = static_cast<long long>(nrhs) * op->b;
   const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
@@ -368,18 +375,18 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s) {
   int last_dft = -1;  // the pass that applies the 1/q scale
   for (int i = 0; i < static_cast<int>(passes.size()); ++i)
     if ((passes[i].kind == 0 && passes[i].back) || passes[i].kind == 2) last_dft = i;
-  const c64* cur = op->mom;
+  const c64* cur = moments;
   c64* bufs[2] = {op->fa, op->fb};
   int which = 0;
   for (int i = 0; i < static_cast<int>(passes.size()); ++i) {
     const Pass& p = passes[i];
     const bool final = i + 1 == static_cast<int>(passes.size());
-    c64* out = final ? op->loc : bufs[which];
+    c64* out = final ? locals : bufs[which];
     if (p.kind == 1) {
-      check(launch_mode_product(op->lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
+      check(launch_mode_product(lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
     } else if (p.kind == 2) {
       const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
-      check(launch_m2l_zfused(cur, out, op->lambda, op->tw[2], static_cast<int>(Mz), static_cast<int>(Lz), Ly * Lx,
+      check(launch_m2l_zfused(cur, out, lambda, op->tw[2], static_cast<int>(Mz), static_cast<int>(Lz), Ly * Lx,
                               static_cast<int>(E), op->b, scale, s),
             "m2l z-fused");
     } else {
@@ -420,7 +427,16 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
     op->launches++;
   }
   ev_record(op, 3, a);
-  if (far_here) m2l_apply(op, nrhs, a);
+  if (far_here) {
+    m2l_apply(op, nrhs, a, op->mom, op->lambda, op->loc);
+    if (op->mirrored_level >= 0) {  // local += hankel_matvec(K_hat spectrum, mirror_permute(moments)) (src/fmm.cpp:262-263)
+      const long long E = static_cast<long long>(nrhs) * op->b;
+      check(launch_mirror_permute(op->mom, op->mom_perm, op->counts, op->mirrored_level, E, a), "mirror permute");
+      m2l_apply(op, nrhs, a, op->mom_perm, op->lambda_hat, op->loc_hat);
+      check(launch_add(op->loc, op->loc_hat, static_cast<long long>(op->n_cells) * E, a), "local image add");
+      op->launches += 2;
+    }
+  }
   ev_record(op, 4, a);
   check(cudaEventRecord(op->join, a), "join");
   s = op->stream;
@@ -718,8 +734,11 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     *out = nullptr;
     for (int k = 0; k < 3; ++k)
       if (d->counts[k] < 1) fail(FPBEM_CU_EDIM, "create: counts must be >= 1");
-    if (d->n_dof < 1 || d->n_coef < 1 || d->n_coef > 64) fail(FPBEM_CU_EDIM, "create: bad n_dof / n_coef");
-    if (d->mirrored_level != -1) fail(FPBEM_CU_EINVAL, "create: half-space image pair not supported");
+    if (d->n_dof < 1 || d->n_coef < 1 || d->n_coef > 256) fail(FPBEM_CU_EDIM, "create: bad n_dof / n_coef (n_t <= 15)");
+    if (d->mirrored_level < -1 || d->mirrored_level > 2) fail(FPBEM_CU_EINVAL, "create: mirrored_level in [-1, 2]");
+    if (d->mirrored_level >= 0 && ((d->n_hat > 0 && (!d->hat_indices || !d->hat_blocks)) ||
+                                   (d->n_far_hat > 0 && (!d->far_hat_indices || !d->far_hat_blocks))))
+      fail(FPBEM_CU_EINVAL, "create: half-space image pair missing");
     if (!d->u0 || !d->v0) fail(FPBEM_CU_EINVAL, "create: u0 / v0 required");
     if (d->n_near > 0 && (!d->near_offsets || !d->near_blocks)) fail(FPBEM_CU_EINVAL, "create: near blocks missing");
     if (!d->lambda && d->n_far > 0 && (!d->far_offsets || !d->far_blocks))
@@ -765,12 +784,38 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
           }
       op->pair_start.push_back(static_cast<int>(psrc.size()));
     }
+    // S_hat slots follow: Hankel pairs, src[a] = idx[a] - t[a], src[d] = t[d] - idx[d]
+    // (BlockHankelMatrix::matvec, src/assembly.cpp:152-178)
+    op->mirrored_level = d->mirrored_level;
+    op->n_hat = d->mirrored_level >= 0 ? d->n_hat : 0;
+    for (int h = 0; h < op->n_hat; ++h) {
+      const int* idx = d->hat_indices + 3 * h;
+      for (int tz = 0; tz < m[2]; ++tz)
+        for (int ty = 0; ty < m[1]; ++ty)
+          for (int tx = 0; tx < m[0]; ++tx) {
+            const int t[3] = {tx, ty, tz};
+            int src[3];
+            bool ok = true;
+            for (int k = 0; k < 3 && ok; ++k) {
+              src[k] = k == op->mirrored_level ? idx[k] - t[k] : t[k] - idx[k];
+              ok = src[k] >= 0 && src[k] < m[k];
+            }
+            if (!ok) continue;
+            op->pair_tgt.push_back(tx + m[0] * (ty + m[1] * tz));
+            psrc.push_back(src[0] + m[0] * (src[1] + m[1] * src[2]));
+          }
+      op->pair_start.push_back(static_cast<int>(psrc.size()));
+    }
     op->n_pairs = static_cast<int>(psrc.size());
-    for (int s = 0; s < d->n_near; ++s) op->rank_slots.push_back(s);
+    const int n_slots = d->n_near + op->n_hat;
+    op->n_near = n_slots;  // slot count seen by the GEMM / reduction / partition
+    for (int s = 0; s < n_slots; ++s) op->rank_slots.push_back(s);
     const size_t nn = static_cast<size_t>(op->n) * op->n;
-    op->S = dalloc<c64>(nn * d->n_near, "near blocks");
+    op->S = dalloc<c64>(nn * n_slots, "near blocks");
     if (d->n_near > 0)
       h2d(op->S, d->near_blocks, nn * d->n_near * sizeof(c64), op->stream, "S upload");
+    if (op->n_hat > 0)
+      h2d(op->S + nn * d->n_near, d->hat_blocks, nn * op->n_hat * sizeof(c64), op->stream, "S_hat upload");
     op->pair_src = dalloc<int>(psrc.size(), "pair sources");
     if (!psrc.empty()) h2d(op->pair_src, psrc.data(), psrc.size() * sizeof(int), op->stream, "pairs");
     build_target_csr(op);
@@ -792,7 +837,15 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     }
     op->q_total = static_cast<long long>(op->L[0]) * op->L[1] * op->L[2];
     for (int k = 0; k < 3; ++k) twiddles(op, op->L[k], &op->tw[k]);
-    build_spectrum(op, d);
+    build_spectrum(op, d->n_far, d->far_offsets, d->far_blocks, d->lambda, &op->lambda);
+    if (op->mirrored_level >= 0) {
+      // spectrum of K_hat P: Toeplitz offsets o = idx with o[a] = idx[a] - (M_a - 1)
+      // (hankel_spectrum, src/structured.cpp:185-198)
+      const int a = op->mirrored_level;
+      std::vector<int> offs(d->far_hat_indices, d->far_hat_indices + 3 * d->n_far_hat);
+      for (int s = 0; s < d->n_far_hat; ++s) offs[3 * s + a] -= m[a] - 1;
+      build_spectrum(op, d->n_far_hat, offs.data(), d->far_hat_blocks, nullptr, &op->lambda_hat);
+    }
 
     // apply buffers
     const long long E = static_cast<long long>(op->max_rhs) * op->b;
@@ -801,6 +854,10 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->loc = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "locals");
     op->fa = dalloc<c64>(static_cast<size_t>(op->q_total) * E, "m2l field");
     op->fb = dalloc<c64>(static_cast<size_t>(op->q_total) * E, "m2l image");
+    if (op->mirrored_level >= 0) {
+      op->mom_perm = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "permuted moments");
+      op->loc_hat = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "image locals");
+    }
     for (auto& e : op->ev) check(cudaEventCreate(&e), "event");
     check(cudaStreamSynchronize(op->stream), "create sync");
     *out = guard_op.release();
@@ -813,7 +870,8 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
   if (op->stream) cudaStreamSynchronize(op->stream);
   for (void* p : {static_cast<void*>(op->S), static_cast<void*>(op->pair_src), static_cast<void*>(op->tgt_ptr),
                   static_cast<void*>(op->tgt_pairs), static_cast<void*>(op->jobs), static_cast<void*>(op->u0),
-                  static_cast<void*>(op->v0), static_cast<void*>(op->lambda), static_cast<void*>(op->tw[0]),
+                  static_cast<void*>(op->v0), static_cast<void*>(op->lambda), static_cast<void*>(op->lambda_hat),
+                  static_cast<void*>(op->mom_perm), static_cast<void*>(op->loc_hat), static_cast<void*>(op->tw[0]),
                   static_cast<void*>(op->tw[1]), static_cast<void*>(op->tw[2]), static_cast<void*>(op->W),
                   static_cast<void*>(op->mom), static_cast<void*>(op->loc), static_cast<void*>(op->fa),
                   static_cast<void*>(op->fb), static_cast<void*>(op->xin), static_cast<void*>(op->yout),
@@ -907,8 +965,10 @@ int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes) {
     return FPBEM_CU_EINVAL;
   }
   const size_t c = sizeof(c64);
-  *bytes = c * (static_cast<size_t>(op->n_near) * op->n * op->n + static_cast<size_t>(op->q_total) * op->b * op->b +
-                2 * static_cast<size_t>(op->n) * op->b);
+  // S (+ S_hat, counted in n_near slots) + spectrum (+ image spectrum) + U0 + V0 (src/fmm.cpp:273-279)
+  const size_t spectra = op->lambda_hat ? 2 : 1;
+  *bytes = c * (static_cast<size_t>(op->n_near) * op->n * op->n +
+                spectra * static_cast<size_t>(op->q_total) * op->b * op->b + 2 * static_cast<size_t>(op->n) * op->b);
   return FPBEM_CU_OK;
 }
 

@@ -29,6 +29,9 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
 size_t m2l_zfused_smem(int Mz, int Lz, int E);
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
                               long long plane, int E, int b, double scale, cudaStream_t stream);
+cudaError_t launch_mirror_permute(const c64* in, c64* out, const int counts[3], int level, long long E,
+                                  cudaStream_t stream);
+cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream);
 cudaError_t launch_scatter_bank(const c64* blocks, const int* offsets, int n_blk, int b2, int lx, int ly, int lz,
                                 c64* field, cudaStream_t stream);
 

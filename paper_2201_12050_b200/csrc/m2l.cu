@@ -166,6 +166,28 @@ __global__ void scatter_bank_kernel(const c64* __restrict__ blocks, const int* _
   }
 }
 
+// out[cell'] = in[cell] with the cell index reversed along `level`
+// (mirror_permute, src/structured.cpp:168-183); E fields per cell
+__global__ void mirror_permute_kernel(const c64* __restrict__ in, c64* __restrict__ out, int mx, int my, int mz,
+                                      int level, long long E) {
+  const long long total = static_cast<long long>(mx) * my * mz * E;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long cell = g / E, f = g % E;
+    int c[3] = {static_cast<int>(cell % mx), static_cast<int>((cell / mx) % my), static_cast<int>(cell / (static_cast<long long>(mx) * my))};
+    const int m[3] = {mx, my, mz};
+    c[level] = m[level] - 1 - c[level];
+    const long long from = c[0] + static_cast<long long>(mx) * (c[1] + static_cast<long long>(my) * c[2]);
+    out[g] = in[from * E + f];
+  }
+}
+
+__global__ void add_kernel(c64* __restrict__ acc, const c64* __restrict__ v, long long n) {
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < n;
+       g += static_cast<long long>(gridDim.x) * blockDim.x)
+    acc[g] = cadd(acc[g], v[g]);
+}
+
 int grid_for(long long total, int threads) {
   long long blocks = (total + threads - 1) / threads;
   const long long cap = static_cast<long long>(kNumSMs) * 16;
@@ -189,6 +211,18 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
                                 int nrhs, cudaStream_t stream) {
   const long long total = q_total * b * nrhs;
   mode_product_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lambda, field, image, q_total, b, nrhs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mirror_permute(const c64* in, c64* out, const int counts[3], int level, long long E,
+                                  cudaStream_t stream) {
+  const long long total = static_cast<long long>(counts[0]) * counts[1] * counts[2] * E;
+  mirror_permute_kernel<<<grid_for(total, 256), 256, 0, stream>>>(in, out, counts[0], counts[1], counts[2], level, E);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream) {
+  add_kernel<<<grid_for(n, 256), 256, 0, stream>>>(acc, v, n);
   return cudaGetLastError();
 }
 

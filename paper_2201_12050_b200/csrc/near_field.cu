@@ -330,7 +330,7 @@ near_gemm_mbar_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
 // y[r,t,i] = sum_{pairs of t, offset order} W[pair, r, i]  +  sum_m U0[i, m] L[t, r, m]
 // One thread per row i; grid (row tiles, target cells * nrhs).
 constexpr int RED_THREADS = 128;
-constexpr int MAX_COEF = 64;
+constexpr int MAX_COEF = 256;  // n_t <= 15
 
 __global__ void __launch_bounds__(RED_THREADS)
 near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_ptr,

@@ -118,8 +118,16 @@ class FmmOperators:
         d.n_far = int(len(data.far_offsets))
         d.far_offsets = ptr(data.far_offsets, np.int32)
         d.far_blocks = ptr(data.far_blocks, np.complex128)
-        d.mirrored_level = -1
+        level = int(getattr(data, "mirrored_level", -1))
+        d.mirrored_level = level
         d.max_rhs = max_rhs
+        if level >= 0:
+            d.n_hat = int(len(data.hat_indices))
+            d.hat_indices = ptr(data.hat_indices, np.int32)
+            d.hat_blocks = ptr(data.hat_blocks, np.complex128)
+            d.n_far_hat = int(len(data.far_hat_indices))
+            d.far_hat_indices = ptr(data.far_hat_indices, np.int32)
+            d.far_hat_blocks = ptr(data.far_hat_blocks, np.complex128)
         h = C.c_void_p()
         _raise(lib.fpbem_cu_fmm_create(C.byref(d), device, C.byref(h)))
         self._h = h

@@ -100,6 +100,16 @@ class Scene:
     def wavenumber(self, k: float) -> None:
         _native.host().fh_scene_set_k(self._h, float(k))
 
+    def set_halfspace(self, axis: int, offset: float, reflection: complex) -> None:
+        """Mirror plane x_axis = offset with a complex reflection coefficient
+        (geometry.hpp:66-78); reflection 0 switches it off."""
+        r = complex(reflection)
+        _native.host().fh_scene_set_halfspace(self._h, int(axis), float(offset), r.real, r.imag)
+
+    def shift_cell(self, shift) -> None:
+        s = np.asarray(shift, np.float64)
+        _native.host().fh_scene_shift_cell(self._h, _dp(s))
+
     def sweep_hz(self) -> list[float]:
         n = int(self._info()[0][5])
         out = np.zeros(max(n, 1), np.float64)
@@ -181,7 +191,7 @@ class FmmData:
     def __init__(self, handle):
         self._h = C.c_void_p(handle)
         lib = _native.host()
-        info = np.zeros(8, np.int32)
+        info = np.zeros(11, np.int32)
         lib.fh_fmm_info(self._h, _ip(info))
         self.counts = tuple(int(v) for v in info[:3])
         self.n_dof = int(info[3])
@@ -208,6 +218,16 @@ class FmmData:
         self.far_blocks = view(ptrs[3], self.n_far * b * b, np.complex128, (self.n_far, b, b))
         self.u0 = view(ptrs[4], n * b, np.complex128, (b, n))  # column-major n x b -> (col, row)
         self.v0 = view(ptrs[5], n * b, np.complex128, (n, b))  # column-major b x n -> (col, row)
+        # half-space image pair (block Hankel along mirrored_level; -1 = none)
+        self.mirrored_level = int(info[8])
+        self.n_hat, self.n_far_hat = int(info[9]), int(info[10])
+        iptrs = [C.c_void_p() for _ in range(4)]
+        lib.fh_fmm_image_arrays(self._h, *[C.byref(p) for p in iptrs])
+        nh = self.n_hat if self.has_near_values else 0
+        self.hat_indices = view(iptrs[0], 3 * self.n_hat, np.int32, (self.n_hat, 3))
+        self.hat_blocks = view(iptrs[1], nh * n * n, np.complex128, (nh, n, n))
+        self.far_hat_indices = view(iptrs[2], 3 * self.n_far_hat, np.int32, (self.n_far_hat, 3))
+        self.far_hat_blocks = view(iptrs[3], self.n_far_hat * b * b, np.complex128, (self.n_far_hat, b, b))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -91,7 +91,51 @@ void classify_offsets(const Mesh& cell, const Lattice& lat, std::vector<int>& ne
       }
 }
 
-FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_t, bool skip_near_values) {
+void mirror_parity_map(int n_t, int axis, cd* out) {  // fmm.cpp:108-123
+  const int p = coef_count(n_t);
+  std::fill(out, out + static_cast<size_t>(p) * p, cd(0.0, 0.0));
+  for (int n = 0; n <= n_t; ++n)
+    for (int m = -n; m <= n; ++m) {
+      const int row = flat(n, m);
+      int col;
+      double v;
+      if (axis == 2) {
+        col = row;
+        v = ((n + m) & 1) ? -1.0 : 1.0;
+      } else {
+        col = flat(n, -m);
+        v = (axis == 0 && (m & 1)) ? -1.0 : 1.0;
+      }
+      out[static_cast<size_t>(col) * p + row] = v;
+    }
+}
+
+namespace {
+// c = a * b for p x p column-major blocks
+void matmul(int p, const cd* a, const cd* b, cd* c) {
+  for (int j = 0; j < p; ++j)
+    for (int i = 0; i < p; ++i) {
+      cd s(0.0, 0.0);
+      for (int k = 0; k < p; ++k) s += a[static_cast<size_t>(k) * p + i] * b[static_cast<size_t>(j) * p + k];
+      c[static_cast<size_t>(j) * p + i] = s;
+    }
+}
+Mesh shifted(const Mesh& m, const V3& s) {
+  Mesh out = m;
+  for (Element& e : out.el) {
+    for (V3& c : e.c) c = c + s;
+    e.centroid = e.centroid + s;
+  }
+  return out;
+}
+}  // namespace
+
+// assemble_periodic_fmm (fmm.cpp:125-244): offsets in z, y, x order split by
+// admissibility into the near blocks S_o and the M2L bank K_o; a half space
+// parallel to every periodic direction folds its image into S and K, one
+// whose axis is periodic yields the block-Hankel image pair (S_hat, K_hat).
+FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_t, bool skip_near_values,
+                     const HalfSpace* hs) {
   if (n_t < 0 || n_t > 30) throw std::invalid_argument("assemble_fmm: n_t in [0, 30] required");
   for (int d = 0; d < 3; ++d)
     if (lat.counts[d] < 1) throw std::invalid_argument("assemble_fmm: counts must be >= 1");
@@ -103,36 +147,108 @@ FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_
   op.grid = make_box_grid(cell, lat);
   const Mesh bie = bie_oriented(cell);
   classify_offsets(cell, lat, op.near_offsets, op.far_offsets);
-
+  const bool with_image = hs && hs->active();
+  const bool split = with_image && lat.counts[hs->axis] > 1;
+  const bool folded = with_image && !split;
   const int b = op.n_dof, p = op.n_coef;
+  const size_t bb = static_cast<size_t>(b) * b, pp = static_cast<size_t>(p) * p;
+  std::vector<cd> parity;
+  Mesh image_cell;
+  if (with_image) {
+    parity.resize(pp);
+    mirror_parity_map(n_t, hs->axis, parity.data());
+    image_cell = mirror_mesh(bie, *hs);
+  }
+
   if (!skip_near_values) {
-    op.near_blocks.resize(static_cast<size_t>(op.n_near()) * b * b);
+    op.near_blocks.resize(static_cast<size_t>(op.n_near()) * bb);
+    std::vector<cd> tmp(folded ? bb : 0);
     for (int s = 0; s < op.n_near(); ++s) {
       const int* o = &op.near_offsets[3 * s];
       const bool self = o[0] == 0 && o[1] == 0 && o[2] == 0;
-      interaction_block(w, bie, lat.shift(o[0], o[1], o[2]), bie, self,
-                        op.near_blocks.data() + static_cast<size_t>(s) * b * b);
+      cd* blk = op.near_blocks.data() + s * bb;
+      const V3 delta = lat.shift(o[0], o[1], o[2]);
+      interaction_block(w, bie, delta, bie, self, blk);
+      if (folded) {
+        interaction_block(w, bie, delta, image_cell, false, tmp.data());
+        for (size_t e = 0; e < bb; ++e) blk[e] += hs->reflection * tmp[e];
+      }
     }
   }
   const Translation& tt = table(n_t);
-  op.far_blocks.resize(static_cast<size_t>(op.n_far()) * p * p);
+  op.far_blocks.resize(static_cast<size_t>(op.n_far()) * pp);
 #pragma omp parallel for schedule(static)
   for (int s = 0; s < op.n_far(); ++s) {
     const int* o = &op.far_offsets[3 * s];
-    tt.m2l(lat.shift(o[0], o[1], o[2]), w.k, op.far_blocks.data() + static_cast<size_t>(s) * p * p);
+    cd* blk = op.far_blocks.data() + s * pp;
+    tt.m2l(lat.shift(o[0], o[1], o[2]), w.k, blk);
+    if (folded) {  // image boxes of far cells are at least as far as the cells
+      const V3 center = op.grid.base_center + lat.shift(o[0], o[1], o[2]);
+      std::vector<cd> k_img(pp), prod(pp);
+      tt.m2l(center - mirror_point(op.grid.base_center, *hs), w.k, k_img.data());
+      matmul(p, k_img.data(), parity.data(), prod.data());
+      for (size_t e = 0; e < pp; ++e) blk[e] += hs->reflection * prod[e];
+    }
   }
   op.u0.resize(static_cast<size_t>(b) * p);
   op.v0.resize(static_cast<size_t>(b) * p);
   l2p_matrix(bie, w, n_t, op.grid.base_center, op.u0.data());
   p2m_matrix(bie, w, n_t, op.grid.base_center, op.v0.data());
+
+  if (split) {  // fmm.cpp:192-242
+    const int ax = hs->axis;
+    const auto& m = lat.counts;
+    op.mirrored_level = ax;
+    int lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = d == ax ? 0 : 1 - m[d];
+      hi[d] = d == ax ? 2 * m[d] - 2 : m[d] - 1;
+    }
+    const V3 base_image = mirror_point(op.grid.base_center, *hs);
+    std::vector<cd> k_img(pp), prod(pp);
+    for (int i2 = lo[2]; i2 <= hi[2]; ++i2)
+      for (int i1 = lo[1]; i1 <= hi[1]; ++i1)
+        for (int i0 = lo[0]; i0 <= hi[0]; ++i0) {
+          int idx[3] = {i0, i1, i2};
+          int tgt[3] = {i0, i1, i2}, src[3] = {0, 0, 0};
+          tgt[ax] = std::min(idx[ax], m[ax] - 1);
+          src[ax] = idx[ax] - tgt[ax];
+          const V3 tshift = lat.shift(tgt[0], tgt[1], tgt[2]);
+          const V3 sshift = lat.shift(src[0], src[1], src[2]);
+          const V3 target_center = op.grid.base_center + tshift;
+          V3 image_center = base_image;
+          for (int d = 0; d < 3; ++d) image_center[d] += d == ax ? -sshift[d] : sshift[d];
+          if (admissible(target_center, image_center, op.grid.radius)) {
+            tt.m2l(target_center - image_center, w.k, k_img.data());
+            matmul(p, k_img.data(), parity.data(), prod.data());
+            op.far_hat_indices.insert(op.far_hat_indices.end(), {i0, i1, i2});
+            for (size_t e = 0; e < pp; ++e) op.far_hat_blocks.push_back(hs->reflection * prod[e]);
+          } else {
+            op.hat_indices.insert(op.hat_indices.end(), {i0, i1, i2});
+            if (skip_near_values) continue;
+            const Mesh src_image = mirror_mesh(shifted(bie, sshift), *hs);
+            const size_t at = op.hat_blocks.size();
+            op.hat_blocks.resize(at + bb);
+            interaction_block(w, bie, tshift, src_image, false, op.hat_blocks.data() + at);
+            for (size_t e = 0; e < bb; ++e) op.hat_blocks[at + e] *= hs->reflection;
+          }
+        }
+  }
   return op;
 }
 
-std::vector<cd> assemble_dense(const Mesh& full, const Wave& w) {
+std::vector<cd> assemble_dense(const Mesh& full, const Wave& w, const HalfSpace* hs) {
   const Mesh bie = bie_oriented(full);
   const size_t n = static_cast<size_t>(full.size());
   std::vector<cd> a(n * n);
   interaction_block(w, bie, V3{0, 0, 0}, bie, true, a.data());
+  if (hs && hs->active()) {  // assembly.cpp:260-271
+    const Mesh image = mirror_mesh(bie, *hs);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (long long i = 0; i < static_cast<long long>(n); ++i)
+      for (size_t j = 0; j < n; ++j)
+        a[j * n + i] += hs->reflection * bm_entry(w, image.el[j], bie.el[i].centroid, bie.el[i].normal, false);
+  }
   return a;
 }
 

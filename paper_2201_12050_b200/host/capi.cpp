@@ -86,6 +86,23 @@ void fh_scene_info(void* hp, int* info, double* dinfo) {
 
 void fh_scene_set_k(void* hp, double k) { static_cast<SceneH*>(hp)->s.wave = Wave::from_k(k); }
 
+// half space: mirror axis, plane offset, complex reflection (0 disables)
+void fh_scene_set_halfspace(void* hp, int axis, double offset, double re, double im) {
+  HalfSpace& h = static_cast<SceneH*>(hp)->s.half_space;
+  h.axis = axis;
+  h.offset = offset;
+  h.reflection = cd(re, im);
+}
+
+// shift the unit cell (e.g. raise it above a ground plane)
+void fh_scene_shift_cell(void* hp, const double* s) {
+  Mesh& m = static_cast<SceneH*>(hp)->s.cell;
+  for (Element& e : m.el) {
+    for (V3& c : e.c) c = c + V3{s[0], s[1], s[2]};
+    e.centroid = e.centroid + V3{s[0], s[1], s[2]};
+  }
+}
+
 void fh_scene_sweep(void* hp, double* hz) {
   const Scene& s = static_cast<SceneH*>(hp)->s;
   for (size_t i = 0; i < s.sweep_hz.size(); ++i) hz[i] = s.sweep_hz[i];
@@ -105,7 +122,7 @@ int fh_scene_rhs(void* hp, int field, double* out) {
   return guarded([&] {
     const Scene& s = static_cast<SceneH*>(hp)->s;
     Mesh full = replicate(s.cell, s.lat);
-    std::vector<cd> r = assemble_rhs(full, s.wave, s.rhs_fields.at(field));
+    std::vector<cd> r = assemble_rhs(full, s.wave, s.rhs_fields.at(field), &s.half_space);
     std::memcpy(out, r.data(), r.size() * sizeof(cd));
   });
 }
@@ -113,7 +130,7 @@ int fh_scene_rhs(void* hp, int field, double* out) {
 int fh_scene_dense(void* hp, double* out) {
   return guarded([&] {
     const Scene& s = static_cast<SceneH*>(hp)->s;
-    std::vector<cd> a = assemble_dense(replicate(s.cell, s.lat), s.wave);
+    std::vector<cd> a = assemble_dense(replicate(s.cell, s.lat), s.wave, &s.half_space);
     std::memcpy(out, a.data(), a.size() * sizeof(cd));
   });
 }
@@ -169,14 +186,14 @@ void* fh_fmm_assemble(void* hp, int n_t, int skip_near) {
   FmmH* h = nullptr;
   guarded([&] {
     const Scene& s = static_cast<SceneH*>(hp)->s;
-    h = new FmmH{assemble_fmm(s.cell, s.lat, s.wave, n_t, skip_near != 0)};
+    h = new FmmH{assemble_fmm(s.cell, s.lat, s.wave, n_t, skip_near != 0, &s.half_space)};
   });
   return h;
 }
 
 void fh_fmm_destroy(void* h) { delete static_cast<FmmH*>(h); }
 
-// info: counts[3], n_dof, n_coef, n_near, n_far, has_near_values
+// info: counts[3], n_dof, n_coef, n_near, n_far, has_near_values, mirrored_level, n_hat, n_far_hat
 void fh_fmm_info(void* hp, int* info) {
   const FmmData& d = static_cast<FmmH*>(hp)->d;
   for (int k = 0; k < 3; ++k) info[k] = d.counts[k];
@@ -185,6 +202,18 @@ void fh_fmm_info(void* hp, int* info) {
   info[5] = d.n_near();
   info[6] = d.n_far();
   info[7] = d.near_blocks.empty() ? 0 : 1;
+  info[8] = d.mirrored_level;
+  info[9] = d.n_hat();
+  info[10] = d.n_far_hat();
+}
+
+void fh_fmm_image_arrays(void* hp, const int** hat_idx, const double** hat_blk, const int** far_hat_idx,
+                         const double** far_hat_blk) {
+  const FmmData& d = static_cast<FmmH*>(hp)->d;
+  *hat_idx = d.hat_indices.data();
+  *hat_blk = reinterpret_cast<const double*>(d.hat_blocks.data());
+  *far_hat_idx = d.far_hat_indices.data();
+  *far_hat_blk = reinterpret_cast<const double*>(d.far_hat_blocks.data());
 }
 
 // borrowed pointers into the handle (valid until fh_fmm_destroy)

@@ -94,6 +94,18 @@ struct Lattice {
 };
 
 Mesh replicate(const Mesh& cell, const Lattice& lat);
+
+// Axis-aligned mirror plane with a constant complex reflection coefficient
+// (geometry.hpp:66-78); mirror_mesh reverses the corner loop and keeps the
+// source orientation with the mirrored normal (geometry.cpp:157-178).
+struct HalfSpace {
+  int axis = 2;
+  double offset = 0.0;
+  cd reflection{0.0, 0.0};
+  bool active() const { return reflection != cd(0.0, 0.0); }
+};
+V3 mirror_point(const V3& p, const HalfSpace& hs);
+Mesh mirror_mesh(const Mesh& m, const HalfSpace& hs);
 Mesh bie_oriented(const Mesh& m);  // normals flipped once (assembly.cpp:17-21)
 
 struct BoxGrid {  // geometry.cpp:180-191
@@ -131,9 +143,11 @@ struct Source {
   V3 v;  // unit direction or position
   cd amp{1.0, 0.0};
 };
-void incident(const std::vector<Source>& src, double k, const V3& x, const V3& nx, cd& p, cd& dpdn);
+void incident(const std::vector<Source>& src, double k, const V3& x, const V3& nx, cd& p, cd& dpdn,
+              const HalfSpace* hs = nullptr);
 // rhs = p_inc + alpha dp_inc/dn at centroids with BIE normals (assembly.cpp:241-251)
-std::vector<cd> assemble_rhs(const Mesh& full, const Wave& w, const std::vector<Source>& src);
+std::vector<cd> assemble_rhs(const Mesh& full, const Wave& w, const std::vector<Source>& src,
+                             const HalfSpace* hs = nullptr);
 
 // special functions (specfun.hpp)
 inline constexpr int flat(int n, int m) { return n * n + n + m; }
@@ -189,8 +203,17 @@ struct FmmData {
   std::vector<int> far_offsets;   // 3 per block
   std::vector<cd> far_blocks;     // n_far * n_coef^2
   std::vector<cd> u0, v0;
+  // half space whose mirror axis is periodic: block Hankel image pair
+  // (S_hat, K_hat), indexed by the cell-index sum along the mirrored level
+  int mirrored_level = -1;
+  std::vector<int> hat_indices;      // 3 per S_hat block
+  std::vector<cd> hat_blocks;        // n_hat * n_dof^2
+  std::vector<int> far_hat_indices;  // 3 per K_hat block
+  std::vector<cd> far_hat_blocks;    // n_far_hat * n_coef^2
   int n_near() const { return static_cast<int>(near_offsets.size() / 3); }
   int n_far() const { return static_cast<int>(far_offsets.size() / 3); }
+  int n_hat() const { return static_cast<int>(hat_indices.size() / 3); }
+  int n_far_hat() const { return static_cast<int>(far_hat_indices.size() / 3); }
 };
 
 // Offset classification only (no block values); same loop as the assembly.
@@ -200,10 +223,13 @@ void classify_offsets(const Mesh& cell, const Lattice& lat, std::vector<int>& ne
 // assemble_periodic_fmm without a half space (fmm.cpp:125-190). If
 // skip_near_values is set the near blocks are left empty (shape-only runs).
 FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_t,
-                     bool skip_near_values = false);
+                     bool skip_near_values = false, const HalfSpace* hs = nullptr);
 
-// Dense collocation matrix of a full mesh (assembly.cpp:253-276, no half space)
-std::vector<cd> assemble_dense(const Mesh& full, const Wave& w);
+// action of an axis mirror on moment vectors (fmm.cpp:108-123); b x b column-major
+void mirror_parity_map(int n_t, int axis, cd* out);
+
+// Dense collocation matrix of a full mesh (assembly.cpp:253-276)
+std::vector<cd> assemble_dense(const Mesh& full, const Wave& w, const HalfSpace* hs = nullptr);
 
 // The five BASELINE.json configurations (and reference-pinned quad variants).
 struct Scene {
@@ -213,6 +239,7 @@ struct Scene {
   Wave wave;
   std::vector<std::vector<Source>> rhs_fields;  // one field per right-hand side
   std::vector<double> sweep_hz;                 // cfg4 frequency sweep (empty otherwise)
+  HalfSpace half_space;                         // inactive unless reflection != 0
   double sound_speed = 343.0;
 };
 Scene make_scene(int config_id, int variant);

@@ -228,6 +228,32 @@ Mesh replicate(const Mesh& cell, const Lattice& lat) {
   return m;
 }
 
+V3 mirror_point(const V3& p, const HalfSpace& hs) {
+  V3 q = p;
+  q[hs.axis] = 2.0 * hs.offset - p[hs.axis];
+  return q;
+}
+
+// mirrored copy with reversed corner loop; the stored normal is the mirrored
+// source normal, so BIE-flipped meshes stay flipped (geometry.cpp:164-178)
+Mesh mirror_mesh(const Mesh& m, const HalfSpace& hs) {
+  Mesh out;
+  out.el.reserve(m.el.size());
+  for (const Element& e : m.el) {
+    Element t;
+    if (e.nv == 3)
+      t = make_tri(mirror_point(e.c[0], hs), mirror_point(e.c[2], hs), mirror_point(e.c[1], hs), e.beta);
+    else
+      t = make_quad(mirror_point(e.c[0], hs), mirror_point(e.c[3], hs), mirror_point(e.c[2], hs),
+                    mirror_point(e.c[1], hs), e.beta);
+    V3 n = e.normal;
+    n[hs.axis] = -n[hs.axis];
+    t.normal = n;
+    out.el.push_back(t);
+  }
+  return out;
+}
+
 Mesh bie_oriented(const Mesh& m) {
   Mesh out = m;
   for (Element& e : out.el) e.normal = -e.normal;

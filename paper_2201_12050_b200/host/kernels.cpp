@@ -216,31 +216,51 @@ cd bm_entry(const Wave& w, const Element& src, const V3& x, const V3& nx, bool s
   return p.h - ikb * p.g;
 }
 
-void incident(const std::vector<Source>& src, double k, const V3& x, const V3& nx, cd& p, cd& dpdn) {
+namespace {
+void add_source(const Source& s, double k, const V3& x, const V3& nx, cd& p, cd& dpdn) {
+  if (s.plane) {  // kernels.cpp:289-292
+    cd e = s.amp * std::exp(kI * (k * dot(s.v, x)));
+    p += e;
+    dpdn += kI * k * dot(s.v, nx) * e;
+  } else {  // monopole normalised to |p| = amp at 1 m (kernels.cpp:293-300)
+    V3 d = x - s.v;
+    double r = norm(d);
+    if (r <= 0.0) throw std::domain_error("incident: point coincides with a monopole");
+    cd e = s.amp * std::exp(kI * (k * r)) / r;
+    p += e;
+    dpdn += (kI * k - 1.0 / r) * e * (dot(d, nx) / r);
+  }
+}
+}  // namespace
+
+// superposition with optional mirror images (kernels.cpp:302-325)
+void incident(const std::vector<Source>& src, double k, const V3& x, const V3& nx, cd& p, cd& dpdn,
+              const HalfSpace* hs) {
   p = dpdn = cd(0.0, 0.0);
   for (const Source& s : src) {
-    if (s.plane) {  // kernels.cpp:289-292
-      cd e = s.amp * std::exp(kI * (k * dot(s.v, x)));
-      p += e;
-      dpdn += kI * k * dot(s.v, nx) * e;
-    } else {  // monopole normalised to |p| = amp at 1 m (kernels.cpp:293-300)
-      V3 d = x - s.v;
-      double r = norm(d);
-      if (r <= 0.0) throw std::domain_error("incident: point coincides with a monopole");
-      cd e = s.amp * std::exp(kI * (k * r)) / r;
-      p += e;
-      dpdn += (kI * k - 1.0 / r) * e * (dot(d, nx) / r);
+    add_source(s, k, x, nx, p, dpdn);
+    if (hs && hs->active()) {
+      Source img = s;
+      img.amp *= hs->reflection;
+      if (s.plane) {  // mirrored direction with the plane-offset phase
+        img.v[hs->axis] = -img.v[hs->axis];
+        img.amp *= std::exp(kI * (k * 2.0 * hs->offset * s.v[hs->axis]));
+      } else {
+        img.v = mirror_point(s.v, *hs);
+      }
+      add_source(img, k, x, nx, p, dpdn);
     }
   }
 }
 
-std::vector<cd> assemble_rhs(const Mesh& full, const Wave& w, const std::vector<Source>& src) {
+std::vector<cd> assemble_rhs(const Mesh& full, const Wave& w, const std::vector<Source>& src,
+                             const HalfSpace* hs) {
   std::vector<cd> rhs(full.size());
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < full.size(); ++i) {
     const Element& e = full.el[i];
     cd p, dpdn;
-    incident(src, w.k, e.centroid, -e.normal, p, dpdn);
+    incident(src, w.k, e.centroid, -e.normal, p, dpdn, hs);
     rhs[i] = p + w.alpha * dpdn;
   }
   return rhs;

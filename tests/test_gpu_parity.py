@@ -416,3 +416,65 @@ def test_nccl_communicator_single_rank_path(ops, assembled):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+# ---- half space: folded image and the block-Hankel image pair (§8 a9) -----------
+
+def _halfspace_scene(counts, pitch, lift, refl, n_t=4):
+    from paper_2201_12050_b200 import Scene
+
+    sc = Scene.custom("cube_sphere", [0.1, 2], counts, pitch, 2 * np.pi * 400 / 343)
+    sc.shift_cell([0, 0, lift])
+    sc.set_halfspace(2, 0.0, refl)
+    return sc, sc.assemble_fmm(n_t)
+
+
+@pytest.mark.parametrize("counts,pitch,lift", [((1, 2, 2), (0.0, 0.35, 0.35), 0.25),
+                                               ((2, 1, 3), (0.35, 0.0, 0.35), 0.3),
+                                               ((3, 2, 4), (0.35, 0.35, 0.35), 0.25)])
+def test_hankel_image_pair_matches_oracle(ops, counts, pitch, lift):
+    """FmmOperators::matvec with near_field_image + k_image_spectrum (src/fmm.cpp:262-269)."""
+    sc, d = _halfspace_scene(counts, pitch, lift, 0.8 - 0.3j)
+    assert d.mirrored_level == 2 and d.n_hat + d.n_far_hat > 0
+    op = ops(d)
+    rng = np.random.default_rng(sum(counts))
+    p = uvec(rng, d.N)
+    ora = O.OracleFmm(d)
+    assert rel(op.matvec(p), ora.matvec(p)) <= MATVEC_TOL
+    assert op.stored_bytes() == 16 * ((d.n_near + d.n_hat) * d.n_dof ** 2
+                                      + 2 * int(np.prod(ora.sizes)) * 625 + 2 * 25 * d.n_dof)
+
+
+def test_hankel_image_pair_near_dense_and_gmres(ops):
+    """reference test_fmm.cpp:264-278 on the device: < 1e-5 vs dense at n_t = 8; GMRES parity."""
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = _halfspace_scene((1, 2, 2), (0.0, 0.35, 0.35), 0.25, 1.0, n_t=8)
+    op = ops(d)
+    rng = np.random.default_rng(5)
+    p = uvec(rng, d.N)
+    assert rel(op.matvec(p), sc.dense() @ p) < 1e-5
+    b = sc.rhs(0)
+    rep = gmres(op, b, tol=1e-8, restart=50, max_iter=300)
+    x, its, conv, _ = O.OracleFmm(d).gmres(b, tol=1e-8, restart=50, max_iter=300)
+    assert rep.converged and conv and abs(rep.iterations - its) <= 1
+    assert rel(rep.solution, x) <= SOLVE_TOL
+
+
+def test_folded_half_space_matches_oracle(ops):
+    sc, d = _halfspace_scene((2, 2, 1), (0.35, 0.35, 0.0), 0.6, 0.9 + 0.2j)
+    assert d.mirrored_level == -1
+    p = uvec(np.random.default_rng(6), d.N)
+    assert rel(ops(d).matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+def test_hankel_partition_sums_to_product(ops):
+    sc, d = _halfspace_scene((3, 2, 4), (0.35, 0.35, 0.35), 0.25, 0.7)
+    p = uvec(np.random.default_rng(8), d.N)
+    full = ops(d).matvec(p)
+    total = np.zeros_like(full)
+    for r in range(3):
+        op = ops(d)
+        op.set_partition(r, 3)
+        total += op.matvec(p)
+    assert rel(total, full) < 1e-13

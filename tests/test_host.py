@@ -143,3 +143,50 @@ def test_rhs_plane_wave_at_centroids():
     x = c["centroid"][:, 0]
     ref = np.exp(1j * k * x) * (1 + (-1j / k) * 1j * k * (-c["normal"][:, 0]))
     assert rel(r[: sc.n_dof], ref) < 1e-14
+
+
+# --- half space (tests/test_fmm.cpp:234-278) ---------------------------------------
+
+def _raised_scene(counts, pitch, lift):
+    k = 2 * np.pi * 400 / 343
+    sc = Scene.custom("cube_sphere", [0.1, 2], counts, pitch, k)
+    sc.shift_cell([0, 0, lift])
+    return sc
+
+
+def test_half_space_parallel_to_the_periodicity_folds_into_toeplitz():
+    # test_fmm.cpp:234-262: mirror z=0 under a 2x2 array at z = 0.6, n_t = 8, < 1e-5 vs dense
+    sc = _raised_scene((2, 2, 1), [0.35, 0.35, 0.0], 0.6)
+    sc.set_halfspace(2, 0.0, 0.9 + 0.2j)
+    d = sc.assemble_fmm(8)
+    assert d.mirrored_level == -1 and d.n_hat == 0
+    rng = np.random.default_rng(4)
+    p = rng.uniform(-1, 1, sc.N) + 1j * rng.uniform(-1, 1, sc.N)
+    assert rel(O.OracleFmm(d).matvec(p), sc.dense() @ p) < 1e-5
+    # zero reflection gives the plain operators
+    sc.set_halfspace(2, 0.0, 0.0)
+    plain = O.OracleFmm(sc.assemble_fmm(4)).matvec(p)
+    assert np.array_equal(plain, O.OracleFmm(sc.assemble_fmm(4)).matvec(p))
+
+
+def test_half_space_perpendicular_to_the_periodicity_splits_into_hankel():
+    # test_fmm.cpp:264-278: 1x2x2 array, mirror z=0 with the z axis periodic, n_t = 8, < 1e-5
+    sc = _raised_scene((1, 2, 2), [0.0, 0.35, 0.35], 0.25)
+    sc.set_halfspace(2, 0.0, 1.0)
+    d = sc.assemble_fmm(8)
+    assert d.mirrored_level == 2 and d.n_hat + d.n_far_hat == 3 * 3 * 1
+    rng = np.random.default_rng(5)
+    p = rng.uniform(-1, 1, sc.N) + 1j * rng.uniform(-1, 1, sc.N)
+    assert rel(O.OracleFmm(d).matvec(p), sc.dense() @ p) < 1e-5
+
+
+def test_mirrored_mesh_keeps_orientation_and_index():
+    sc = Scene.custom("icosphere", [0.1, 1], (1, 1, 1), [0, 0, 0], 1.0)
+    sc.shift_cell([0, 0, 0.5])
+    c = sc.cell()
+    # a mirrored triangle mesh through the dense image terms: a zero-reflection half space changes nothing
+    sc.set_halfspace(2, 0.0, 0.0)
+    a0 = sc.dense()
+    sc.set_halfspace(2, 0.0, 1e-300)
+    assert rel(sc.dense(), a0) < 1e-12
+    assert c["nv"][0] == 3
