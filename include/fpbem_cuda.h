@@ -88,6 +88,9 @@ typedef struct {
   int n_far_hat;                 /* K_hat bank (the device builds the spectrum of K_hat P) */
   const int* far_hat_indices;    /* n_far_hat x 3                                          */
   const fpbem_c64* far_hat_blocks; /* n_far_hat x n_coef^2                                 */
+  const fpbem_c64* lambda_hat;   /* optional prebuilt spectrum of K_hat P (the reference's
+                                    k_image_spectrum, same layout as lambda); else built
+                                    from the K_hat bank                                    */
 } fpbem_cu_fmm_desc;
 
 int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* desc, int device, fpbem_cu_op** out);

@@ -52,6 +52,7 @@ class FmmDesc(C.Structure):
         ("n_far_hat", C.c_int),
         ("far_hat_indices", C.c_void_p),
         ("far_hat_blocks", C.c_void_p),
+        ("lambda_hat", C.c_void_p),
     ]
 
 

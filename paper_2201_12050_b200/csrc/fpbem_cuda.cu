@@ -737,7 +737,7 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     if (d->n_dof < 1 || d->n_coef < 1 || d->n_coef > 256) fail(FPBEM_CU_EDIM, "create: bad n_dof / n_coef (n_t <= 15)");
     if (d->mirrored_level < -1 || d->mirrored_level > 2) fail(FPBEM_CU_EINVAL, "create: mirrored_level in [-1, 2]");
     if (d->mirrored_level >= 0 && ((d->n_hat > 0 && (!d->hat_indices || !d->hat_blocks)) ||
-                                   (d->n_far_hat > 0 && (!d->far_hat_indices || !d->far_hat_blocks))))
+                                   (!d->lambda_hat && d->n_far_hat > 0 && (!d->far_hat_indices || !d->far_hat_blocks))))
       fail(FPBEM_CU_EINVAL, "create: half-space image pair missing");
     if (!d->u0 || !d->v0) fail(FPBEM_CU_EINVAL, "create: u0 / v0 required");
     if (d->n_near > 0 && (!d->near_offsets || !d->near_blocks)) fail(FPBEM_CU_EINVAL, "create: near blocks missing");
@@ -844,7 +844,7 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
       const int a = op->mirrored_level;
       std::vector<int> offs(d->far_hat_indices, d->far_hat_indices + 3 * d->n_far_hat);
       for (int s = 0; s < d->n_far_hat; ++s) offs[3 * s + a] -= m[a] - 1;
-      build_spectrum(op, d->n_far_hat, offs.data(), d->far_hat_blocks, nullptr, &op->lambda_hat);
+      build_spectrum(op, d->n_far_hat, offs.data(), d->far_hat_blocks, d->lambda_hat, &op->lambda_hat);
     }
 
     // apply buffers

@@ -88,7 +88,7 @@ class FmmOperators:
     unless `lambda_` (reference layout) is given.
     """
 
-    def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1):
+    def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1, lambda_hat=None):
         lib = _native.cuda()
         self.counts = tuple(int(c) for c in data.counts)
         self.n_dof = int(data.n_dof)
@@ -128,6 +128,7 @@ class FmmOperators:
             d.n_far_hat = int(len(data.far_hat_indices))
             d.far_hat_indices = ptr(data.far_hat_indices, np.int32)
             d.far_hat_blocks = ptr(data.far_hat_blocks, np.complex128)
+            d.lambda_hat = ptr(lambda_hat, np.complex128) if lambda_hat is not None else None
         h = C.c_void_p()
         _raise(lib.fpbem_cu_fmm_create(C.byref(d), device, C.byref(h)))
         self._h = h

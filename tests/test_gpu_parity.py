@@ -461,6 +461,15 @@ def test_hankel_image_pair_near_dense_and_gmres(ops):
     assert rel(rep.solution, x) <= SOLVE_TOL
 
 
+def test_prebuilt_image_spectrum_is_accepted(ops):
+    """the reference's k_image_spectrum handed over as lambda_hat"""
+    sc, d = _halfspace_scene((1, 2, 2), (0.0, 0.35, 0.35), 0.25, 0.6)
+    ora = O.OracleFmm(d)
+    op = ops(d, lambda_=ora.lambda_, fft_sizes=ora.sizes, lambda_hat=ora.image_lambda)
+    p = uvec(np.random.default_rng(11), d.N)
+    assert rel(op.matvec(p), ora.matvec(p)) <= MATVEC_TOL
+
+
 def test_folded_half_space_matches_oracle(ops):
     sc, d = _halfspace_scene((2, 2, 1), (0.35, 0.35, 0.0), 0.6, 0.9 + 0.2j)
     assert d.mirrored_level == -1
