@@ -91,7 +91,39 @@ typedef struct {
   const fpbem_c64* lambda_hat;   /* optional prebuilt spectrum of K_hat P (the reference's
                                     k_image_spectrum, same layout as lambda); else built
                                     from the K_hat bank                                    */
+  int blocks_on_device;          /* 1: near_blocks / hat_blocks are device pointers on
+                                    `device` (e.g. from fpbem_cu_assemble_near)            */
 } fpbem_cu_fmm_desc;
+
+/* Unit cell for the device assembly, BIE-oriented (assembly::bie_oriented,
+ * src/assembly.cpp:17-21): flat quads, or triangles with corner 3 == corner 2. */
+typedef struct {
+  int n;                    /* elements                                    */
+  const double* corners;    /* n x 4 x 3                                   */
+  const int* nv;            /* n: 4 (quad) or 3 (triangle)                 */
+  const double* centroid;   /* n x 3                                       */
+  const double* normal;     /* n x 3, BIE orientation                      */
+  const double* diameter;   /* n                                           */
+  const fpbem_c64* beta;    /* n normalised admittances, or NULL (rigid)   */
+} fpbem_cu_cell;
+
+/* Near-field blocks of assemble_periodic_fmm on the device (src/fmm.cpp:156-179,
+ * src/assembly.cpp:214-239): out[s] = interaction_block(cell, shift(offsets[s]),
+ * cell, self = (offset == 0)), n x n column-major, plus
+ * hs_reflection * interaction_block(cell, shift, mirror(cell)) when fold != 0
+ * (half space parallel to every periodic axis). ptr_kind: FPBEM_CU_PTR_HOST or
+ * FPBEM_CU_PTR_DEVICE (out on `device`). */
+int fpbem_cu_assemble_near(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, const double pitch[3],
+                           int n_off, const int* offsets, int fold, int hs_axis, double hs_offset,
+                           fpbem_c64 hs_reflection, int device, fpbem_c64* out, int ptr_kind);
+
+/* S_hat blocks of a split half space (src/fmm.cpp:204-231): for Hankel index
+ * idx, target shift = shift(tgt), source = mirror(cell shifted by shift(src))
+ * with tgt/src as the reference picks them, scaled by hs_reflection. */
+int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, const double pitch[3],
+                          const int counts[3], int n_hat, const int* hat_indices, int hs_axis,
+                          double hs_offset, fpbem_c64 hs_reflection, int device, fpbem_c64* out,
+                          int ptr_kind);
 
 int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* desc, int device, fpbem_cu_op** out);
 void fpbem_cu_fmm_destroy(fpbem_cu_op* op);

@@ -53,7 +53,26 @@ class FmmDesc(C.Structure):
         ("far_hat_indices", C.c_void_p),
         ("far_hat_blocks", C.c_void_p),
         ("lambda_hat", C.c_void_p),
+        ("blocks_on_device", C.c_int),
     ]
+
+
+class Cell(C.Structure):
+    """fpbem_cu_cell (include/fpbem_cuda.h)."""
+
+    _fields_ = [
+        ("n", C.c_int),
+        ("corners", C.c_void_p),
+        ("nv", C.c_void_p),
+        ("centroid", C.c_void_p),
+        ("normal", C.c_void_p),
+        ("diameter", C.c_void_p),
+        ("beta", C.c_void_p),
+    ]
+
+
+class C64(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
 
 
 APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -64,7 +83,7 @@ CUDA_SYMBOLS = (
     "fpbem_cu_gmres_fn", "fpbem_cu_fmm_bytes", "fpbem_cu_spectrum", "fpbem_cu_set_stream",
     "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
     "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
-    "fpbem_cu_fmm_set_partition", "fpbem_cu_partition_offsets",
+    "fpbem_cu_fmm_set_partition", "fpbem_cu_partition_offsets", "fpbem_cu_assemble_near", "fpbem_cu_assemble_hat",
     "fpbem_cu_last_error", "fpbem_cu_version",
 )
 
@@ -100,6 +119,10 @@ def cuda() -> C.CDLL:
             "fpbem_cu_partition_offsets": (C.c_int, [C.c_int, C.POINTER(C.c_longlong), C.c_int, c_int_p]),
             "fpbem_cu_last_error": (C.c_char_p, []),
             "fpbem_cu_version": (C.c_char_p, []),
+            "fpbem_cu_assemble_near": (C.c_int, [C.POINTER(Cell), C.c_double, C64, c_double_p, C.c_int, c_int_p,
+                                                 C.c_int, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
+            "fpbem_cu_assemble_hat": (C.c_int, [C.POINTER(Cell), C.c_double, C64, c_double_p, c_int_p, C.c_int,
+                                                c_int_p, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

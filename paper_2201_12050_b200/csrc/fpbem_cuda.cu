@@ -812,10 +812,17 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     for (int s = 0; s < n_slots; ++s) op->rank_slots.push_back(s);
     const size_t nn = static_cast<size_t>(op->n) * op->n;
     op->S = dalloc<c64>(nn * n_slots, "near blocks");
-    if (d->n_near > 0)
-      h2d(op->S, d->near_blocks, nn * d->n_near * sizeof(c64), op->stream, "S upload");
-    if (op->n_hat > 0)
-      h2d(op->S + nn * d->n_near, d->hat_blocks, nn * op->n_hat * sizeof(c64), op->stream, "S_hat upload");
+    auto put = [&](c64* dst, const fpbem_c64* src, size_t count, const char* what) {
+      if (count == 0) return;
+      if (d->blocks_on_device) {
+        check(cudaMemcpyAsync(dst, src, count * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), what);
+        check(cudaStreamSynchronize(op->stream), what);
+      } else {
+        h2d(dst, src, count * sizeof(c64), op->stream, what);
+      }
+    };
+    put(op->S, d->near_blocks, nn * d->n_near, "S upload");
+    put(op->S + nn * d->n_near, d->hat_blocks, nn * op->n_hat, "S_hat upload");
     op->pair_src = dalloc<int>(psrc.size(), "pair sources");
     if (!psrc.empty()) h2d(op->pair_src, psrc.data(), psrc.size() * sizeof(int), op->stream, "pairs");
     build_target_csr(op);
@@ -1083,6 +1090,161 @@ int fpbem_cu_gmres_fn(int device, long long n, fpbem_cu_apply_fn apply, void* ac
   });
   fpbem_cu_fmm_destroy(op);
   return rc;
+}
+
+namespace {
+
+// Gauss-Legendre nodes/weights by Newton on P_n (the host rule, kernels.cpp:162-194)
+void gauss_rule(int n, double* x, double* w) {
+  for (int i = 0; i < (n + 1) / 2; ++i) {
+    double z = std::cos(3.14159265358979323846 * (i + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = 0.0;
+      for (int j = 0; j < n; ++j) {
+        const double p2 = p1;
+        p1 = p0;
+        p0 = ((2.0 * j + 1.0) * z * p1 - j * p2) / (j + 1);
+      }
+      dp = n * (z * p0 - p1) / (z * z - 1.0);
+      const double dz = p0 / dp;
+      z -= dz;
+      if (std::abs(dz) < 1e-15) break;
+    }
+    x[i] = -z;
+    x[n - 1 - i] = z;
+    w[i] = w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+struct CellDev {
+  double* corners = nullptr;
+  int* nv = nullptr;
+  double* cen = nullptr;
+  double* nrm = nullptr;
+  double* diam = nullptr;
+  c64* beta = nullptr;
+  ~CellDev() {
+    for (void* p : {static_cast<void*>(corners), static_cast<void*>(nv), static_cast<void*>(cen),
+                    static_cast<void*>(nrm), static_cast<void*>(diam), static_cast<void*>(beta)})
+      if (p) cudaFree(p);
+  }
+};
+
+void upload_cell(const fpbem_cu_cell* c, CellDev& d, cudaStream_t s) {
+  if (!c || c->n < 1 || !c->corners || !c->nv || !c->centroid || !c->normal || !c->diameter)
+    fail(FPBEM_CU_EINVAL, "assemble: bad cell");
+  const size_t n = static_cast<size_t>(c->n);
+  d.corners = dalloc<double>(12 * n, "cell corners");
+  d.nv = dalloc<int>(n, "cell nv");
+  d.cen = dalloc<double>(3 * n, "cell centroids");
+  d.nrm = dalloc<double>(3 * n, "cell normals");
+  d.diam = dalloc<double>(n, "cell diameters");
+  h2d(d.corners, c->corners, 12 * n * sizeof(double), s, "cell upload");
+  h2d(d.nv, c->nv, n * sizeof(int), s, "cell upload");
+  h2d(d.cen, c->centroid, 3 * n * sizeof(double), s, "cell upload");
+  h2d(d.nrm, c->normal, 3 * n * sizeof(double), s, "cell upload");
+  h2d(d.diam, c->diameter, n * sizeof(double), s, "cell upload");
+  if (c->beta) {
+    d.beta = dalloc<c64>(n, "cell beta");
+    h2d(d.beta, c->beta, n * sizeof(c64), s, "cell upload");
+  }
+  double x6[6], w6[6], x8[8], w8[8];
+  gauss_rule(6, x6, w6);
+  gauss_rule(8, x8, w8);
+  check(assembly_set_rules(x6, w6, x8, w8), "quadrature rules");
+}
+
+// run the slots (two passes: plain, then accumulated images) into out
+void run_assembly(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, int hs_axis, double hs_offset,
+                  const std::vector<AssemblySlot>& plain, const std::vector<AssemblySlot>& images, int device,
+                  fpbem_c64* out, int ptr_kind) {
+  check(cudaSetDevice(device), "set device");
+  cudaStream_t s;
+  check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
+  CellDev dc;
+  upload_cell(cell, dc, s);
+  const size_t n = static_cast<size_t>(cell->n);
+  const size_t total = plain.size() * n * n;
+  c64* dst = reinterpret_cast<c64*>(out);
+  c64* tmp = nullptr;
+  if (ptr_kind != FPBEM_CU_PTR_DEVICE) dst = tmp = dalloc<c64>(total, "assembly output");
+  std::unique_ptr<c64, decltype(&cudaFree)> keep_tmp(tmp, &cudaFree);
+  AssemblySlot* ds = dalloc<AssemblySlot>(plain.size() + images.size(), "assembly slots");
+  std::unique_ptr<AssemblySlot, decltype(&cudaFree)> keep_ds(ds, &cudaFree);
+  h2d(ds, plain.data(), plain.size() * sizeof(AssemblySlot), s, "slots");
+  if (!images.empty()) h2d(ds + plain.size(), images.data(), images.size() * sizeof(AssemblySlot), s, "slots");
+  const c64 al = cmk(alpha.re, alpha.im);
+  // z-chunks of at most 65535 slots per launch (grid.z limit)
+  for (size_t s0 = 0; s0 < plain.size(); s0 += 65535) {
+    const int cnt = static_cast<int>(std::min<size_t>(65535, plain.size() - s0));
+    check(launch_assemble(dc.corners, dc.nv, dc.cen, dc.nrm, dc.diam, dc.beta, cell->n, ds + s0, cnt, k, al, hs_axis,
+                          hs_offset, dst + s0 * n * n, false, s),
+          "assemble");
+  }
+  for (size_t s0 = 0; s0 < images.size(); s0 += 65535) {
+    const int cnt = static_cast<int>(std::min<size_t>(65535, images.size() - s0));
+    check(launch_assemble(dc.corners, dc.nv, dc.cen, dc.nrm, dc.diam, dc.beta, cell->n, ds + plain.size() + s0, cnt, k,
+                          al, hs_axis, hs_offset, dst + s0 * n * n, true, s),
+          "assemble images");
+  }
+  if (ptr_kind != FPBEM_CU_PTR_DEVICE)
+    check(cudaMemcpyAsync(out, dst, total * sizeof(c64), cudaMemcpyDeviceToHost, s), "assembly download");
+  check(cudaStreamSynchronize(s), "assembly");
+}
+
+AssemblySlot make_slot(const double t[3], const double src[3], c64 scale, int mirror, int self) {
+  AssemblySlot sl;
+  for (int d = 0; d < 3; ++d) {
+    sl.tshift[d] = t[d];
+    sl.sshift[d] = src[d];
+  }
+  sl.scale = scale;
+  sl.mirror = mirror;
+  sl.self = self;
+  return sl;
+}
+
+}  // namespace
+
+int fpbem_cu_assemble_near(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, const double pitch[3], int n_off,
+                           const int* offsets, int fold, int hs_axis, double hs_offset, fpbem_c64 hs_reflection,
+                           int device, fpbem_c64* out, int ptr_kind) {
+  return guard([&] {
+    if (!pitch || (n_off > 0 && (!offsets || !out))) fail(FPBEM_CU_EINVAL, "assemble_near: null argument");
+    std::vector<AssemblySlot> plain, images;
+    const double zero[3] = {0, 0, 0};
+    const bool with_image = fold && (hs_reflection.re != 0.0 || hs_reflection.im != 0.0);
+    for (int s = 0; s < n_off; ++s) {
+      const int* o = offsets + 3 * s;
+      const double t[3] = {o[0] * pitch[0], o[1] * pitch[1], o[2] * pitch[2]};
+      const int self = o[0] == 0 && o[1] == 0 && o[2] == 0;
+      plain.push_back(make_slot(t, zero, cmk(1.0, 0.0), 0, self));
+      if (with_image) images.push_back(make_slot(t, zero, cmk(hs_reflection.re, hs_reflection.im), 1, 0));
+    }
+    run_assembly(cell, k, alpha, hs_axis, hs_offset, plain, images, device, out, ptr_kind);
+  });
+}
+
+int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, const double pitch[3],
+                          const int counts[3], int n_hat, const int* hat_indices, int hs_axis, double hs_offset,
+                          fpbem_c64 hs_reflection, int device, fpbem_c64* out, int ptr_kind) {
+  return guard([&] {
+    if (!pitch || !counts || (n_hat > 0 && (!hat_indices || !out))) fail(FPBEM_CU_EINVAL, "assemble_hat: null");
+    if (hs_axis < 0 || hs_axis > 2) fail(FPBEM_CU_EINVAL, "assemble_hat: bad axis");
+    std::vector<AssemblySlot> plain, images;
+    for (int h = 0; h < n_hat; ++h) {
+      const int* idx = hat_indices + 3 * h;
+      int tgt[3] = {idx[0], idx[1], idx[2]}, src[3] = {0, 0, 0};
+      tgt[hs_axis] = std::min(idx[hs_axis], counts[hs_axis] - 1);
+      src[hs_axis] = idx[hs_axis] - tgt[hs_axis];
+      const double t[3] = {tgt[0] * pitch[0], tgt[1] * pitch[1], tgt[2] * pitch[2]};
+      const double sv[3] = {src[0] * pitch[0], src[1] * pitch[1], src[2] * pitch[2]};
+      plain.push_back(make_slot(t, sv, cmk(hs_reflection.re, hs_reflection.im), 1, 0));
+    }
+    run_assembly(cell, k, alpha, hs_axis, hs_offset, plain, images, device, out, ptr_kind);
+  });
 }
 
 int fpbem_cu_comm_unique_id(unsigned char id_out[128]) {

@@ -35,6 +35,20 @@ cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream)
 cudaError_t launch_scatter_bank(const c64* blocks, const int* offsets, int n_blk, int b2, int lx, int ly, int lz,
                                 c64* field, cudaStream_t stream);
 
+// ---- near-field block assembly (assembly.cu)
+struct AssemblySlot {
+  double tshift[3];  // target (collocation point) shift
+  double sshift[3];  // source element shift, applied before the optional mirror
+  c64 scale;         // entry multiplier (1, or the reflection coefficient)
+  int mirror;        // source element mirrored in the half-space plane
+  int self;          // slot holds the self block (i == j -> singular self term)
+};
+cudaError_t assembly_set_rules(const double* x6, const double* w6, const double* x8, const double* w8);
+cudaError_t launch_assemble(const double* corners, const int* nv, const double* cen, const double* nrm,
+                            const double* diam, const c64* beta, int n, const AssemblySlot* slots, int n_slots,
+                            double k, c64 alpha, int hs_axis, double hs_offset, c64* out, bool accumulate,
+                            cudaStream_t stream);
+
 // ---- Krylov vector ops (krylov.cu)
 constexpr int kRedBlocks = 2 * kNumSMs;
 struct RedScratch {

@@ -88,7 +88,8 @@ class FmmOperators:
     unless `lambda_` (reference layout) is given.
     """
 
-    def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1, lambda_hat=None):
+    def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1, lambda_hat=None,
+                 near_blocks=None, hat_blocks=None):
         lib = _native.cuda()
         self.counts = tuple(int(c) for c in data.counts)
         self.n_dof = int(data.n_dof)
@@ -110,7 +111,13 @@ class FmmOperators:
         d.n_coef = self.n_coef
         d.n_near = int(len(data.near_offsets))
         d.near_offsets = ptr(data.near_offsets, np.int32)
-        d.near_blocks = ptr(data.near_blocks, np.complex128)
+        on_device = near_blocks is not None
+        if on_device:  # CUDA tensors, e.g. from assemble_near_gpu
+            keep.append(near_blocks)
+            d.near_blocks = near_blocks.data_ptr()
+            d.blocks_on_device = 1
+        else:
+            d.near_blocks = ptr(data.near_blocks, np.complex128)
         d.u0 = ptr(data.u0, np.complex128)
         d.v0 = ptr(data.v0, np.complex128)
         d.fft_sizes[:] = tuple(fft_sizes) if fft_sizes is not None else (0, 0, 0)
@@ -124,7 +131,11 @@ class FmmOperators:
         if level >= 0:
             d.n_hat = int(len(data.hat_indices))
             d.hat_indices = ptr(data.hat_indices, np.int32)
-            d.hat_blocks = ptr(data.hat_blocks, np.complex128)
+            if on_device:
+                keep.append(hat_blocks)
+                d.hat_blocks = hat_blocks.data_ptr() if hat_blocks is not None and d.n_hat else None
+            else:
+                d.hat_blocks = ptr(data.hat_blocks, np.complex128)
             d.n_far_hat = int(len(data.far_hat_indices))
             d.far_hat_indices = ptr(data.far_hat_indices, np.int32)
             d.far_hat_blocks = ptr(data.far_hat_blocks, np.complex128)
@@ -256,6 +267,74 @@ def gmres(apply, b, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000,
                             bool(conv[r])) for r in range(nrhs)]
         return reps[0] if nrhs == 1 else reps
     return _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device)
+
+
+def _cell_struct(scene, keep):
+    c = scene.cell()
+    n = len(c["area"])
+    arrs = {
+        "corners": np.ascontiguousarray(c["corners"], np.float64),
+        "nv": np.ascontiguousarray(c["nv"], np.int32),
+        "centroid": np.ascontiguousarray(c["centroid"], np.float64),
+        "normal": np.ascontiguousarray(-c["normal"], np.float64),  # BIE orientation (assembly.cpp:17-21)
+        "diameter": np.ascontiguousarray(c["diameter"], np.float64),
+    }
+    keep.append(arrs)
+    cs = _native.Cell()
+    cs.n = n
+    for k, a in arrs.items():
+        setattr(cs, k, a.ctypes.data)
+    cs.beta = None  # rigid scenes
+    return cs, n
+
+
+def assemble_near_gpu(scene, data, device: int = 0, halfspace=None):
+    """Near-field blocks S_o of `data`'s offsets assembled on the GPU
+    (fpbem_cu_assemble_near); returns a CUDA complex128 tensor (n_near, n, n)
+    holding column-major blocks, ready for FmmOperators(near_blocks=...).
+    halfspace=(axis, offset, reflection) folds the image terms (mirror axis
+    not periodic)."""
+    import torch
+
+    keep = []
+    cs, n = _cell_struct(scene, keep)
+    k = float(scene.wavenumber)
+    alpha = _native.C64(0.0, -1.0 / k)
+    pitch = np.ascontiguousarray(scene.pitch, np.float64)
+    offs = np.ascontiguousarray(data.near_offsets, np.int32)
+    out = torch.empty((len(offs), n, n), dtype=torch.complex128, device=f"cuda:{device}")
+    fold, axis, off, refl = 0, 2, 0.0, 0j
+    if halfspace is not None:
+        fold = 1
+        axis, off, refl = halfspace
+    rc = _native.cuda().fpbem_cu_assemble_near(C.byref(cs), k, alpha, pitch.ctypes.data_as(_native.c_double_p),
+                                               len(offs), offs.ctypes.data_as(_native.c_int_p), fold, int(axis),
+                                               float(off), _native.C64(complex(refl).real, complex(refl).imag),
+                                               device, out.data_ptr(), PTR_DEVICE)
+    _raise(rc)
+    return out
+
+
+def assemble_hat_gpu(scene, data, halfspace, device: int = 0):
+    """S_hat blocks of a split half space on the GPU (fpbem_cu_assemble_hat)."""
+    import torch
+
+    keep = []
+    cs, n = _cell_struct(scene, keep)
+    k = float(scene.wavenumber)
+    pitch = np.ascontiguousarray(scene.pitch, np.float64)
+    counts = np.ascontiguousarray(data.counts, np.int32)
+    idx = np.ascontiguousarray(data.hat_indices, np.int32)
+    out = torch.empty((max(len(idx), 1), n, n), dtype=torch.complex128, device=f"cuda:{device}")
+    axis, off, refl = halfspace
+    rc = _native.cuda().fpbem_cu_assemble_hat(C.byref(cs), k, _native.C64(0.0, -1.0 / k),
+                                              pitch.ctypes.data_as(_native.c_double_p),
+                                              counts.ctypes.data_as(_native.c_int_p), len(idx),
+                                              idx.ctypes.data_as(_native.c_int_p), int(axis), float(off),
+                                              _native.C64(complex(refl).real, complex(refl).imag), device,
+                                              out.data_ptr(), PTR_DEVICE)
+    _raise(rc)
+    return out[: len(idx)]
 
 
 def _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device):

@@ -487,3 +487,30 @@ def test_hankel_partition_sums_to_product(ops):
         op.set_partition(r, 3)
         total += op.matvec(p)
     assert rel(total, full) < 1e-13
+
+
+# ---- near-field assembly on the device ---------------------
+
+@pytest.mark.parametrize("cid,var", [(1, 0), (2, 2), (3, 2), (4, 2), (6, 8)])
+def test_device_assembly_matches_host_assembly(ops, assembled, cid, var):
+    from paper_2201_12050_b200.fmm import assemble_near_gpu
+
+    sc, d = assembled(cid, var)
+    blocks = assemble_near_gpu(sc, d)
+    host = np.asarray(d.near_blocks)
+    dev = blocks.cpu().numpy()
+    assert rel(dev, host) < 1e-12
+    # the operator built from device-assembled blocks
+    p = uvec(np.random.default_rng(cid), d.N)
+    assert rel(ops(d, near_blocks=blocks).matvec(p), O.OracleFmm(d).matvec(p)) < 1e-12
+
+
+def test_device_assembly_of_half_space_images():
+    from paper_2201_12050_b200.fmm import assemble_hat_gpu, assemble_near_gpu
+
+    sc, d = _halfspace_scene((2, 2, 1), (0.35, 0.35, 0.0), 0.6, 0.9 + 0.2j)
+    dev = assemble_near_gpu(sc, d, halfspace=(2, 0.0, 0.9 + 0.2j)).cpu().numpy()
+    assert rel(dev, np.asarray(d.near_blocks)) < 1e-12
+    sc, d = _halfspace_scene((1, 2, 2), (0.0, 0.35, 0.35), 0.25, 0.8 - 0.3j)
+    dev = assemble_hat_gpu(sc, d, (2, 0.0, 0.8 - 0.3j)).cpu().numpy()
+    assert rel(dev, np.asarray(d.hat_blocks)) < 1e-12
