@@ -707,6 +707,297 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
   return rep;
 }
 
+// ---------------------------------------------------------------------------
+// Lockstep batched GMRES: G right-hand sides advance one Arnoldi step together
+// (one batched matvec, batched MGS with per-RHS reductions); every RHS follows
+// exactly the control flow of src/solver.cpp:21-123 on its own scalars (host),
+// leaves its cycle's inner loop on its own estimate, and leaves the batch when
+// converged or out of iterations. Basis layout: column j of RHS r at
+// V + (j * G + r) * N, so column j of all RHS is one contiguous batch.
+struct BatchOut {
+  std::vector<int> iterations;
+  std::vector<char> converged;
+  std::vector<std::vector<double>> history;
+};
+
+BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double tol, int restart, int max_iter) {
+  using cd = std::complex<double>;
+  cudaStream_t s = op->stream;
+  const long long n = op->N;
+  const int m = std::max(1, restart);
+  BatchOut out;
+  out.iterations.assign(G, 0);
+  out.converged.assign(G, 0);
+  out.history.assign(G, {});
+
+  std::vector<void*> owned;  // device buffers scoped to the call
+  struct Free {
+    std::vector<void*>& v;
+    ~Free() {
+      for (void* p : v) cudaFree(p);
+    }
+  } free_all{owned};
+  auto alloc = [&](size_t bytes, const char* what) {
+    void* p = nullptr;
+    check(cudaMalloc(&p, bytes), what);
+    owned.push_back(p);
+    return p;
+  };
+  const size_t vecb = static_cast<size_t>(n) * sizeof(c64);
+  c64* V = static_cast<c64*>(alloc(vecb * G * (m + 1), "batched basis"));
+  c64* R = static_cast<c64*>(alloc(vecb * G, "batched residual"));
+  c64* T = static_cast<c64*>(alloc(vecb * G, "batched A x"));
+  c64* P = static_cast<c64*>(alloc(vecb * G, "batched pack in"));
+  c64* Q = static_cast<c64*>(alloc(vecb * G, "batched pack out"));
+  // scalars: [flags G int (8 B slots)][pre2 G][post2 G][post2b G][rn2 G][bn2 G][d G]
+  //          [h (m+1)G c64][hc (m+1)G][y mG][jr G int][mask G int][idx G int]
+  const size_t g8 = 8 * static_cast<size_t>((G + 1) & ~1);  // even count: c64 sections stay 16-byte aligned
+  const size_t o_flag = 0, o_pre = g8, o_post = o_pre + g8, o_post2 = o_post + g8, o_rn = o_post2 + g8,
+               o_bn = o_rn + g8, o_d = o_bn + g8, o_h = o_d + g8, o_hc = o_h + 2 * g8 * (m + 1),
+               o_y = o_hc + 2 * g8 * (m + 1), o_jr = o_y + 2 * g8 * m, o_mask = o_jr + g8 / 2,
+               o_idx = o_mask + g8 / 2, total = o_idx + g8 / 2;
+  char* sc = static_cast<char*>(alloc(total, "batched scalars"));
+  int* d_flag = reinterpret_cast<int*>(sc + o_flag);
+  double* d_pre = reinterpret_cast<double*>(sc + o_pre);
+  double* d_post = reinterpret_cast<double*>(sc + o_post);
+  double* d_post2 = reinterpret_cast<double*>(sc + o_post2);
+  double* d_rn = reinterpret_cast<double*>(sc + o_rn);
+  double* d_bn = reinterpret_cast<double*>(sc + o_bn);
+  double* d_d = reinterpret_cast<double*>(sc + o_d);
+  c64* d_h = reinterpret_cast<c64*>(sc + o_h);
+  c64* d_hc = reinterpret_cast<c64*>(sc + o_hc);
+  c64* d_y = reinterpret_cast<c64*>(sc + o_y);
+  int* d_jr = reinterpret_cast<int*>(sc + o_jr);
+  int* d_mask = reinterpret_cast<int*>(sc + o_mask);
+  int* d_idx = reinterpret_cast<int*>(sc + o_idx);
+  BatchScratch bs;
+  bs.partial_d = static_cast<double*>(alloc(sizeof(double) * kBatchBlocks * G, "batch partials"));
+  bs.partial_c = static_cast<c64*>(alloc(sizeof(c64) * kBatchBlocks * G, "batch partials"));
+  bs.counter = static_cast<unsigned*>(alloc(sizeof(unsigned) * G, "batch counters"));
+  check(cudaMemsetAsync(bs.counter, 0, sizeof(unsigned) * G, s), "counters");
+  check(cudaMemsetAsync(d_flag, 0, g8, s), "flags");
+  ensure_pinned(op, total + 64);
+  char* pin = static_cast<char*>(op->pinned);
+  auto fetch = [&](size_t off, size_t bytes) {
+    check(cudaMemcpyAsync(pin + off, sc + off, bytes, cudaMemcpyDeviceToHost, s), "batched readback");
+    check(cudaStreamSynchronize(s), "batched sync");
+  };
+  auto put = [&](size_t off, const void* src, size_t bytes) {
+    // pinned staging is reused: the previous upload must have been consumed
+    check(cudaStreamSynchronize(s), "batched sync");
+    std::memcpy(pin + off, src, bytes);
+    check(cudaMemcpyAsync(sc + off, pin + off, bytes, cudaMemcpyHostToDevice, s), "batched upload");
+  };
+  auto get_d = [&](size_t off, int r) {
+    double v;
+    std::memcpy(&v, pin + off + 8 * static_cast<size_t>(r), 8);
+    return v;
+  };
+  auto get_c = [&](size_t off, size_t idx) {
+    c64 v;
+    std::memcpy(&v, pin + off + 16 * idx, 16);
+    return cd(v.x, v.y);
+  };
+  auto set_mask = [&](const std::vector<int>& on) {
+    std::vector<int> mk(G, 0);
+    for (int r : on) mk[r] = 1;
+    put(o_mask, mk.data(), 4 * static_cast<size_t>(G));
+  };
+  auto flags_of = [&](const std::vector<int>& rs) {
+    for (int r : rs) {
+      int fl;
+      std::memcpy(&fl, pin + o_flag + 4 * static_cast<size_t>(r), 4);
+      if (fl) fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+    }
+  };
+  // y = A x for the listed RHS (packed unless the list is 0..G-1)
+  auto apply_set = [&](const c64* src_base, c64* dst_base, const std::vector<int>& rs) {
+    const int cnt = static_cast<int>(rs.size());
+    bool all = cnt == G;
+    for (int q = 0; all && q < cnt; ++q) all = rs[q] == q;
+    if (all) {
+      apply_device(op, src_base, dst_base, G);
+      return;
+    }
+    put(o_idx, rs.data(), 4 * static_cast<size_t>(cnt));
+    check(launch_b_pack(src_base, P, d_idx, cnt, n, true, s), "pack");
+    apply_device(op, P, Q, cnt);
+    check(launch_b_pack(Q, dst_base, d_idx, cnt, n, false, s), "unpack");
+    op->launches += 2;
+  };
+
+  check(cudaMemsetAsync(Xd, 0, vecb * G, s), "x0");
+  std::vector<int> all(G);
+  for (int r = 0; r < G; ++r) all[r] = r;
+  set_mask(all);
+  check(launch_b_sqnorm(Bd, n, n, G, d_mask, bs, d_bn, nullptr, s), "bnorm");
+  fetch(o_bn, g8);
+  std::vector<double> bnorm(G), rnorm(G);
+  std::vector<char> done(G, 0);
+  for (int r = 0; r < G; ++r) {
+    bnorm[r] = std::sqrt(get_d(o_bn, r));
+    rnorm[r] = bnorm[r];
+    if (bnorm[r] == 0.0) {
+      out.converged[r] = 1;
+      done[r] = 1;
+    }
+  }
+  const size_t hsz = static_cast<size_t>(m + 1) * m;
+  std::vector<std::vector<cd>> H(G, std::vector<cd>(hsz)), g(G, std::vector<cd>(m + 1));
+  std::vector<std::vector<double>> gc(G, std::vector<double>(m));
+  std::vector<std::vector<cd>> gs(G, std::vector<cd>(m));
+  std::vector<int> jr(G, 0);
+  std::vector<char> inner(G, 0);
+  const c64* rsrc = Bd;
+
+  while (true) {
+    std::vector<int> act;
+    for (int r = 0; r < G; ++r)
+      if (!done[r] && out.iterations[r] < max_iter) act.push_back(r);
+    if (act.empty()) break;
+    set_mask(act);
+    put(o_d, rnorm.data(), g8);
+    check(launch_b_div(rsrc, V, n, n, G, d_mask, d_d, s), "v0");  // v0 = r / ||r||
+    for (int r : act) {
+      std::fill(g[r].begin(), g[r].end(), cd(0, 0));
+      g[r][0] = rnorm[r];
+      std::fill(H[r].begin(), H[r].end(), cd(0, 0));
+      jr[r] = 0;
+      inner[r] = 1;
+    }
+    for (int j = 0; j < m; ++j) {
+      std::vector<int> it;
+      for (int r : act)
+        if (inner[r] && out.iterations[r] < max_iter) it.push_back(r);
+      if (it.empty()) break;
+      c64* Vj = V + static_cast<long long>(j) * G * n;
+      c64* W = V + static_cast<long long>(j + 1) * G * n;
+      apply_set(Vj, W, it);
+      set_mask(it);
+      check(launch_b_sqnorm(W, n, n, G, d_mask, bs, d_pre, d_flag, s), "pre norm");
+      check(launch_b_dotc(V, W, n, n, G, d_mask, bs, d_h, s), "mgs dot");
+      for (int i = 0; i < j; ++i)
+        check(launch_b_axpy_dotc(W, V + static_cast<long long>(i) * G * n, d_h + static_cast<long long>(i) * G,
+                                 V + static_cast<long long>(i + 1) * G * n, n, n, G, d_mask, bs,
+                                 d_h + static_cast<long long>(i + 1) * G, s),
+              "mgs step");
+      check(launch_b_axpy_sqnorm(W, Vj, d_h + static_cast<long long>(j) * G, n, n, G, d_mask, bs, d_post, s),
+            "mgs last");
+      op->launches += j + 3;
+      fetch(0, o_h + 16 * static_cast<size_t>(j + 1) * G);  // flags, norms and h_0..h_j of every RHS
+      flags_of(it);
+      std::vector<int> reo;
+      std::vector<double> wn2(G, 0.0);
+      for (int r : it) {
+        for (int i = 0; i <= j; ++i)
+          H[r][static_cast<size_t>(j) * (m + 1) + i] = get_c(o_h, static_cast<size_t>(i) * G + r);
+        wn2[r] = get_d(o_post, r);
+        if (std::sqrt(wn2[r]) < 0.5 * std::sqrt(get_d(o_pre, r))) reo.push_back(r);  // (:63-69)
+      }
+      if (!reo.empty()) {
+        set_mask(reo);
+        check(launch_b_dotc(V, W, n, n, G, d_mask, bs, d_hc, s), "reorth dot");
+        for (int i = 0; i < j; ++i)
+          check(launch_b_axpy_dotc(W, V + static_cast<long long>(i) * G * n, d_hc + static_cast<long long>(i) * G,
+                                   V + static_cast<long long>(i + 1) * G * n, n, n, G, d_mask, bs,
+                                   d_hc + static_cast<long long>(i + 1) * G, s),
+                "reorth step");
+        check(launch_b_axpy_sqnorm(W, Vj, d_hc + static_cast<long long>(j) * G, n, n, G, d_mask, bs, d_post2, s),
+              "reorth last");
+        op->launches += j + 2;
+        fetch(o_post2, g8);
+        fetch(o_hc, 16 * static_cast<size_t>(j + 1) * G);
+        for (int r : reo) {
+          for (int i = 0; i <= j; ++i)
+            H[r][static_cast<size_t>(j) * (m + 1) + i] += get_c(o_hc, static_cast<size_t>(i) * G + r);
+          wn2[r] = get_d(o_post2, r);
+        }
+      }
+      std::vector<double> hl(G, 1.0);
+      std::vector<int> norm_set;
+      for (int r : it) {
+        hl[r] = std::sqrt(wn2[r]);
+        if (hl[r] > 0.0) norm_set.push_back(r);
+      }
+      if (!norm_set.empty()) {
+        set_mask(norm_set);
+        put(o_d, hl.data(), g8);
+        check(launch_b_div(W, W, n, n, G, d_mask, d_d, s), "normalise");
+        op->launches++;
+      }
+      for (int r : it) {  // rotations, Givens, estimate (:74-105), per RHS
+        auto Hm = [&](int a, int b) -> cd& { return H[r][static_cast<size_t>(b) * (m + 1) + a]; };
+        const double hlast = hl[r];
+        Hm(j + 1, j) = hlast;
+        for (int i = 0; i < j; ++i) {
+          cd t = gc[r][i] * Hm(i, j) + gs[r][i] * Hm(i + 1, j);
+          Hm(i + 1, j) = -std::conj(gs[r][i]) * Hm(i, j) + gc[r][i] * Hm(i + 1, j);
+          Hm(i, j) = t;
+        }
+        const cd a = Hm(j, j);
+        const double bb = std::abs(Hm(j + 1, j));
+        const double denom = std::hypot(std::abs(a), bb);
+        if (denom == 0.0) {
+          gc[r][j] = 1.0;
+          gs[r][j] = cd(0, 0);
+        } else if (std::abs(a) == 0.0) {
+          gc[r][j] = 0.0;
+          gs[r][j] = cd(1, 0);
+        } else {
+          gc[r][j] = std::abs(a) / denom;
+          gs[r][j] = (a / std::abs(a)) * std::conj(Hm(j + 1, j)) / denom;
+        }
+        Hm(j, j) = gc[r][j] * a + gs[r][j] * Hm(j + 1, j);
+        Hm(j + 1, j) = cd(0, 0);
+        const cd gj = g[r][j];
+        g[r][j] = gc[r][j] * gj;
+        g[r][j + 1] = -std::conj(gs[r][j]) * gj;
+        ++out.iterations[r];
+        const double est = std::abs(g[r][j + 1]) / bnorm[r];
+        out.history[r].push_back(est);
+        jr[r] = j + 1;
+        if (est <= tol || hlast == 0.0) inner[r] = 0;
+      }
+    }
+    // x_r += V_r y_r for every RHS of the cycle, then the true residuals (:109-116)
+    std::vector<c64> yh(static_cast<size_t>(m) * G, cmk(0.0, 0.0));
+    for (int r : act) {
+      auto Hm = [&](int a, int b) -> cd& { return H[r][static_cast<size_t>(b) * (m + 1) + a]; };
+      const int jj = jr[r];
+      std::vector<cd> y(jj);
+      for (int i = jj - 1; i >= 0; --i) {
+        cd acc = g[r][i];
+        for (int k = i + 1; k < jj; ++k) acc -= Hm(i, k) * y[k];
+        y[i] = acc / Hm(i, i);
+      }
+      for (int i = 0; i < jj; ++i) yh[static_cast<size_t>(r) * m + i] = cmk(y[i].real(), y[i].imag());
+    }
+    put(o_y, yh.data(), 16 * yh.size());
+    put(o_jr, jr.data(), 4 * static_cast<size_t>(G));
+    set_mask(act);
+    check(launch_b_update_x(Xd, V, G, n, d_y, m, d_jr, n, d_mask, s), "x update");
+    apply_set(Xd, T, act);
+    set_mask(act);
+    check(launch_b_residual(Bd, T, R, n, n, G, d_mask, bs, d_rn, d_flag, s), "residual");
+    op->launches += 2;
+    fetch(0, o_pre);
+    flags_of(act);
+    fetch(o_rn, g8);
+    for (int r : act) {
+      rnorm[r] = std::sqrt(get_d(o_rn, r));
+      if (rnorm[r] / bnorm[r] <= tol) {
+        out.converged[r] = 1;
+        done[r] = 1;
+      }
+    }
+    rsrc = R;
+  }
+  for (int r = 0; r < G; ++r)
+    if (!out.history[r].empty()) out.converged[r] = out.converged[r] || rnorm[r] / bnorm[r] <= tol;
+  check(cudaStreamSynchronize(s), "batched gmres");
+  return out;
+}
+
 }  // namespace
 
 namespace {
@@ -937,6 +1228,39 @@ int fpbem_cu_gmres(fpbem_cu_op* op, const fpbem_c64* b, fpbem_c64* x, int nrhs, 
     if (nrhs < 1) fail(FPBEM_CU_EDIM, "gmres: nrhs >= 1 required");
     check(cudaSetDevice(op->device), "set device");
     ensure_gmres(op, std::max(1, restart));
+    const char* lock = std::getenv("FPBEM_GMRES_BATCHED");
+    const bool batched = nrhs > 1 && !(lock && std::strcmp(lock, "0") == 0);
+    if (batched) {  // lockstep batch over all right-hand sides
+      const size_t bytes = static_cast<size_t>(op->N) * nrhs * sizeof(c64);
+      const c64* bd;
+      c64* xd;
+      c64* tmp_b = nullptr;
+      c64* tmp_x = nullptr;
+      if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
+        bd = reinterpret_cast<const c64*>(b);
+        xd = reinterpret_cast<c64*>(x);
+      } else {
+        tmp_b = dalloc<c64>(static_cast<size_t>(op->N) * nrhs, "batched b");
+        tmp_x = dalloc<c64>(static_cast<size_t>(op->N) * nrhs, "batched x");
+        h2d(tmp_b, b, bytes, op->stream, "b upload");
+        bd = tmp_b;
+        xd = tmp_x;
+      }
+      std::unique_ptr<c64, decltype(&cudaFree)> kb(tmp_b, &cudaFree), kx(tmp_x, &cudaFree);
+      BatchOut o = gmres_batched(op, bd, xd, nrhs, tol, restart, max_iter);
+      for (int r = 0; r < nrhs; ++r) {
+        iterations[r] = o.iterations[r];
+        converged[r] = o.converged[r];
+        if (history_len) history_len[r] = static_cast<int>(o.history[r].size());
+        if (history)
+          for (int i = 0; i < std::min(history_cap, static_cast<int>(o.history[r].size())); ++i)
+            history[static_cast<size_t>(r) * history_cap + i] = o.history[r][i];
+      }
+      if (ptr_kind != FPBEM_CU_PTR_DEVICE)
+        check(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, op->stream), "x download");
+      check(cudaStreamSynchronize(op->stream), "gmres sync");
+      return;
+    }
     for (int r = 0; r < nrhs; ++r) {
       const size_t off = static_cast<size_t>(r) * op->N;
       const c64* bd;

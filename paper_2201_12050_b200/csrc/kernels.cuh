@@ -72,6 +72,29 @@ cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y
 bool mgs_fused_supported(long long n);
 cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
                              int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s);
+// ---- batched (lockstep multi-RHS) vector ops: G right-hand sides at stride ld
+constexpr int kBatchBlocks = 64;  // blocks per RHS (upper bound)
+struct BatchScratch {
+  double* partial_d;  // G * kBatchBlocks
+  c64* partial_c;     // G * kBatchBlocks
+  unsigned* counter;  // G, zero between launches
+};
+cudaError_t launch_b_sqnorm(const c64* w, long long ld, long long n, int G, const int* mask, const BatchScratch& bs,
+                            double* result, int* nonfinite, cudaStream_t s);
+cudaError_t launch_b_dotc(const c64* a, const c64* b, long long ld, long long n, int G, const int* mask,
+                          const BatchScratch& bs, c64* result, cudaStream_t s);
+cudaError_t launch_b_axpy_dotc(c64* w, const c64* v, const c64* h, const c64* vn, long long ld, long long n, int G,
+                               const int* mask, const BatchScratch& bs, c64* result, cudaStream_t s);
+cudaError_t launch_b_axpy_sqnorm(c64* w, const c64* v, const c64* h, long long ld, long long n, int G,
+                                 const int* mask, const BatchScratch& bs, double* result, cudaStream_t s);
+cudaError_t launch_b_div(const c64* in, c64* out, long long ld, long long n, int G, const int* mask, const double* d,
+                         cudaStream_t s);
+cudaError_t launch_b_update_x(c64* x, const c64* basis, int G, long long ld, const c64* y, int ystride,
+                              const int* jr, long long n, const int* mask, cudaStream_t s);
+cudaError_t launch_b_residual(const c64* b, const c64* ax, c64* res, long long ld, long long n, int G, const int* mask,
+                              const BatchScratch& bs, double* result, int* nonfinite, cudaStream_t s);
+cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, long long n, bool gather,
+                          cudaStream_t s);
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
                             double* result, cudaStream_t s);
 

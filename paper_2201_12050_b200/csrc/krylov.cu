@@ -281,6 +281,176 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
   if (blockIdx.x == 0 && threadIdx.x == 0) norms[1] = tot;
 }
 
+// ---------------------------------------------------------------------------
+// Batched (lockstep multi-RHS) variants: blockIdx.y = right-hand side r, the
+// vectors of RHS r at base + r * ld; per-RHS deterministic reductions
+// (partials[r * gridDim.x + b], counter[r]); RHS with mask[r] == 0 are skipped.
+
+template <typename T>
+__device__ void finish_reduce_b(T block_sum, T* partials, unsigned* counter, T* result, T* sh) {
+  __shared__ bool last;
+  const int r = blockIdx.y;
+  if (threadIdx.x == 0) {
+    partials[r * gridDim.x + blockIdx.x] = block_sum;
+    __threadfence();
+    const unsigned done = atomicAdd(counter + r, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  T v = zero_v<T>();
+  for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += RT) v = add_v(v, partials[r * gridDim.x + i]);
+  T total = block_reduce(v, sh);
+  if (threadIdx.x == 0) {
+    result[r] = total;
+    counter[r] = 0u;
+  }
+}
+
+#define RHS_GUARD()                       \
+  const int r_ = blockIdx.y;              \
+  if (mask && !mask[r_]) return;          \
+  const long long off_ = r_ * ld;
+
+__global__ void __launch_bounds__(RT) b_sqnorm_kernel(const c64* __restrict__ w, long long ld, long long n,
+                                                      const int* __restrict__ mask, double* partials,
+                                                      unsigned* counter, double* result, int* nonfinite) {
+  RHS_GUARD();
+  __shared__ double sh[RT];
+  double s = 0.0;
+  bool bad = false;
+  const c64* wr = w + off_;
+  GRID_STRIDE_4(i, n, {
+    c64 v = wr[i];
+    bad |= !isfinite(v.x) || !isfinite(v.y);
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+  })
+  if (bad && nonfinite) atomicOr(nonfinite + r_, 1);
+  double b = block_reduce(s, sh);
+  finish_reduce_b(b, partials, counter, result, sh);
+}
+
+__global__ void __launch_bounds__(RT) b_dotc_kernel(const c64* __restrict__ a, const c64* __restrict__ b, long long ld,
+                                                    long long n, const int* __restrict__ mask, c64* partials,
+                                                    unsigned* counter, c64* result) {
+  RHS_GUARD();
+  __shared__ c64 sh[RT];
+  c64 s = cmk(0.0, 0.0);
+  const c64* ar = a + off_;
+  const c64* br = b + off_;
+  GRID_STRIDE_4(i, n, { s = cfma_conj(ar[i], br[i], s); })
+  c64 t = block_reduce(s, sh);
+  finish_reduce_b(t, partials, counter, result, sh);
+}
+
+// w_r -= h[r] v_r ; result[r] = <vn_r, w_r>  (vn == null: result[r] = ||w_r||^2 into dres)
+__global__ void __launch_bounds__(RT) b_axpy_dotc_kernel(c64* __restrict__ w, const c64* __restrict__ v,
+                                                         const c64* __restrict__ h, const c64* __restrict__ vn,
+                                                         long long ld, long long n, const int* __restrict__ mask,
+                                                         c64* partials, unsigned* counter, c64* result) {
+  RHS_GUARD();
+  __shared__ c64 sh[RT];
+  const c64 hh = h[r_];
+  c64 s = cmk(0.0, 0.0);
+  c64* wr = w + off_;
+  const c64* vr = v + off_;
+  const c64* vnr = vn + off_;
+  GRID_STRIDE_4(i, n, {
+    c64 wi = csub(wr[i], cmul(hh, vr[i]));
+    wr[i] = wi;
+    s = cfma_conj(vnr[i], wi, s);
+  })
+  c64 t = block_reduce(s, sh);
+  finish_reduce_b(t, partials, counter, result, sh);
+}
+
+__global__ void __launch_bounds__(RT) b_axpy_sqnorm_kernel(c64* __restrict__ w, const c64* __restrict__ v,
+                                                           const c64* __restrict__ h, long long ld, long long n,
+                                                           const int* __restrict__ mask, double* partials,
+                                                           unsigned* counter, double* result) {
+  RHS_GUARD();
+  __shared__ double sh[RT];
+  const c64 hh = h[r_];
+  double s = 0.0;
+  c64* wr = w + off_;
+  const c64* vr = v + off_;
+  GRID_STRIDE_4(i, n, {
+    c64 wi = csub(wr[i], cmul(hh, vr[i]));
+    wr[i] = wi;
+    s = fma(wi.x, wi.x, s);
+    s = fma(wi.y, wi.y, s);
+  })
+  double t = block_reduce(s, sh);
+  finish_reduce_b(t, partials, counter, result, sh);
+}
+
+// out_r = in_r / d[r]
+__global__ void b_div_kernel(const c64* __restrict__ in, c64* __restrict__ out, long long ld, long long n,
+                             const int* __restrict__ mask, const double* __restrict__ d) {
+  RHS_GUARD();
+  const double dr = d[r_];
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const c64 v = in[off_ + i];
+    out[off_ + i] = cmk(v.x / dr, v.y / dr);
+  }
+}
+
+// x_r += sum_{i < jr[r]} V[i][r] y[r][i]; V column i of RHS r at basis + (i * G + r) * n
+__global__ void b_update_x_kernel(c64* __restrict__ x, const c64* __restrict__ basis, int G, long long ld,
+                                  const c64* __restrict__ y, int ystride, const int* __restrict__ jr, long long n,
+                                  const int* __restrict__ mask) {
+  RHS_GUARD();
+  const int j = jr[r_];
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    c64 acc = cmk(0.0, 0.0);
+    for (int i = 0; i < j; ++i)
+      acc = cfma(basis[(static_cast<long long>(i) * G + r_) * ld + k], __ldg(y + r_ * ystride + i), acc);
+    x[off_ + k] = cadd(x[off_ + k], acc);
+  }
+}
+
+// r_r = b_r - ax_r ; result[r] = ||r_r||^2 (+ non-finite flag of ax_r)
+__global__ void __launch_bounds__(RT) b_residual_kernel(const c64* __restrict__ b, const c64* __restrict__ ax,
+                                                        c64* __restrict__ res, long long ld, long long n,
+                                                        const int* __restrict__ mask, double* partials,
+                                                        unsigned* counter, double* result, int* nonfinite) {
+  RHS_GUARD();
+  __shared__ double sh[RT];
+  double s = 0.0;
+  bool bad = false;
+  GRID_STRIDE_4(i, n, {
+    const c64 a = ax[off_ + i];
+    bad |= !isfinite(a.x) || !isfinite(a.y);
+    c64 v = csub(b[off_ + i], a);
+    res[off_ + i] = v;
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+  })
+  if (bad && nonfinite) atomicOr(nonfinite + r_, 1);
+  double t = block_reduce(s, sh);
+  finish_reduce_b(t, partials, counter, result, sh);
+}
+
+// dst[q] = src[idx[q]] (gather = 1) or dst[idx[q]] = src[q] (gather = 0), vectors of length n
+__global__ void b_pack_kernel(const c64* __restrict__ src, c64* __restrict__ dst, const int* __restrict__ idx,
+                              long long n, int gather) {
+  const int q = blockIdx.y;
+  const long long from = (gather ? idx[q] : q) * n, to = (gather ? q : idx[q]) * n;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[to + i] = src[from + i];
+}
+
+int b_grid(long long n) {  // blocks per RHS
+  long long blocks = (n + 4 * 256 - 1) / (4 * 256);
+  if (blocks > 64) blocks = 64;
+  return static_cast<int>(blocks < 1 ? 1 : blocks);
+}
+
 int ew_grid(long long n) {
   long long blocks = (n + 255) / 256;
   const long long cap = static_cast<long long>(kNumSMs) * 8;
@@ -321,6 +491,49 @@ cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y
 }
 namespace {
 constexpr long long kMgsMaxChunk = 6500;  // complex per block: 2 x (104 KB + 6 KB static) smem per SM
+}
+
+cudaError_t launch_b_sqnorm(const c64* w, long long ld, long long n, int G, const int* mask, const BatchScratch& bs,
+                            double* result, int* nonfinite, cudaStream_t s) {
+  b_sqnorm_kernel<<<dim3(b_grid(n), G), RT, 0, s>>>(w, ld, n, mask, bs.partial_d, bs.counter, result, nonfinite);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_dotc(const c64* a, const c64* b, long long ld, long long n, int G, const int* mask,
+                          const BatchScratch& bs, c64* result, cudaStream_t s) {
+  b_dotc_kernel<<<dim3(b_grid(n), G), RT, 0, s>>>(a, b, ld, n, mask, bs.partial_c, bs.counter, result);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_axpy_dotc(c64* w, const c64* v, const c64* h, const c64* vn, long long ld, long long n, int G,
+                               const int* mask, const BatchScratch& bs, c64* result, cudaStream_t s) {
+  b_axpy_dotc_kernel<<<dim3(b_grid(n), G), RT, 0, s>>>(w, v, h, vn, ld, n, mask, bs.partial_c, bs.counter, result);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_axpy_sqnorm(c64* w, const c64* v, const c64* h, long long ld, long long n, int G,
+                                 const int* mask, const BatchScratch& bs, double* result, cudaStream_t s) {
+  b_axpy_sqnorm_kernel<<<dim3(b_grid(n), G), RT, 0, s>>>(w, v, h, ld, n, mask, bs.partial_d, bs.counter, result);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_div(const c64* in, c64* out, long long ld, long long n, int G, const int* mask, const double* d,
+                         cudaStream_t s) {
+  b_div_kernel<<<dim3(b_grid(n), G), 256, 0, s>>>(in, out, ld, n, mask, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_update_x(c64* x, const c64* basis, int G, long long ld, const c64* y, int ystride,
+                              const int* jr, long long n, const int* mask, cudaStream_t s) {
+  b_update_x_kernel<<<dim3(b_grid(n), G), 256, 0, s>>>(x, basis, G, ld, y, ystride, jr, n, mask);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_residual(const c64* b, const c64* ax, c64* res, long long ld, long long n, int G, const int* mask,
+                              const BatchScratch& bs, double* result, int* nonfinite, cudaStream_t s) {
+  b_residual_kernel<<<dim3(b_grid(n), G), RT, 0, s>>>(b, ax, res, ld, n, mask, bs.partial_d, bs.counter, result,
+                                                      nonfinite);
+  return cudaGetLastError();
+}
+cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, long long n, bool gather,
+                          cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  b_pack_kernel<<<dim3(b_grid(n), count), 256, 0, s>>>(src, dst, idx, n, gather ? 1 : 0);
+  return cudaGetLastError();
 }
 
 bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kRedBlocks) * kMgsMaxChunk; }

@@ -514,3 +514,60 @@ def test_device_assembly_of_half_space_images():
     sc, d = _halfspace_scene((1, 2, 2), (0.0, 0.35, 0.35), 0.25, 0.8 - 0.3j)
     dev = assemble_hat_gpu(sc, d, (2, 0.0, 0.8 - 0.3j)).cpu().numpy()
     assert rel(dev, np.asarray(d.hat_blocks)) < 1e-12
+
+
+# ---- lockstep batched GMRES (cfg5's 64 right-hand sides) -------------------------
+
+def test_batched_gmres_matches_per_rhs_oracle_with_restarts(ops, assembled):
+    """several RHS in lockstep, restart 7 so every RHS runs several cycles and the
+    RHS leave the batch at different iterations; each equals its own single-RHS
+    reference solve (src/solver.cpp:21-123)."""
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(5, 2)
+    dirs = [[1, 0, 0], [0, 0.6, 0.8], [0.3, -0.4, 0.866], [-1, 0.2, 0.1], [0, 0, 1]]
+    sc.set_sources([1] * len(dirs), dirs)
+    b = np.concatenate([sc.rhs(r) for r in range(len(dirs))])
+    op = ops(d, max_rhs=len(dirs))
+    reps = gmres(op, b, tol=1e-7, restart=7, max_iter=400)
+    ora = O.OracleFmm(d)
+    its = []
+    for r in range(len(dirs)):
+        x, it, conv, hist = ora.gmres(b[r * d.N:(r + 1) * d.N], tol=1e-7, restart=7, max_iter=400)
+        assert reps[r].converged == conv
+        assert abs(reps[r].iterations - it) <= 1
+        assert rel(reps[r].solution, x) <= SOLVE_TOL
+        its.append(it)
+    assert len(set(its)) > 1  # the RHS really leave the batch at different times
+
+
+def test_batched_gmres_equals_sequential_solves(ops, assembled):
+    import os
+
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(3, 2)
+    sc.set_sources([1, 1, 1], [[1, 1, 1], [1, 0, 0], [0, 1, 0]])
+    b = np.concatenate([sc.rhs(r) for r in range(3)])
+    op = ops(d, max_rhs=3)
+    batched = gmres(op, b, tol=1e-6, restart=20, max_iter=300)
+    os.environ["FPBEM_GMRES_BATCHED"] = "0"
+    try:
+        seq = gmres(op, b, tol=1e-6, restart=20, max_iter=300)
+    finally:
+        del os.environ["FPBEM_GMRES_BATCHED"]
+    for a, s in zip(batched, seq):
+        assert abs(a.iterations - s.iterations) <= 1
+        assert rel(a.solution, s.solution) < 1e-10
+
+
+def test_batched_gmres_max_iter_and_nan(ops, assembled):
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(1, 0)
+    b = np.concatenate([sc.rhs(0), 2 * sc.rhs(0)])
+    reps = gmres(ops(d, max_rhs=2), b, tol=1e-14, restart=5, max_iter=12)
+    assert all(r.iterations == 12 and not r.converged for r in reps)
+    b[d.N + 7] = np.nan
+    with pytest.raises(RuntimeError, match="non-finite"):
+        gmres(ops(d, max_rhs=2), b, tol=1e-6, restart=5, max_iter=12)

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--restart", type=int, default=50)
+    ap.add_argument("--nrhs", type=int, default=1)
     args = ap.parse_args()
     import torch
 
@@ -22,15 +23,16 @@ def main():
 
     sc = Scene(args.config, 0)
     data = sc.assemble_fmm(4)
-    op = FmmOperators(data)
-    b = torch.from_numpy(sc.rhs(0)).cuda()
+    op = FmmOperators(data, max_rhs=args.nrhs)
+    b = torch.from_numpy(np.concatenate([sc.rhs(f % sc.n_rhs) for f in range(args.nrhs)])).cuda()
     gmres(op, b, tol=1e-12, restart=args.restart, max_iter=3)
     torch.cuda.synchronize()
     t = time.perf_counter()
     rep = gmres(op, b, tol=1e-12, restart=args.restart, max_iter=args.iters)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
-    print(f"{rep.iterations} iterations in {dt * 1e3:.2f} ms = {dt / rep.iterations * 1e3:.3f} ms/iteration")
+    its = rep.iterations if args.nrhs == 1 else max(r.iterations for r in rep)
+    print(f"{its} iterations in {dt * 1e3:.2f} ms = {dt / its * 1e3:.3f} ms/iteration (nrhs {args.nrhs})")
 
 
 if __name__ == "__main__":
