@@ -16,8 +16,8 @@ GMRES solve (tol 1e-6, restart 50) is timed as the metric's second half.
 oracle/fpbem_oracle.cpp; the reference itself cannot be built here, see
 DESIGN.md) on the host cores for the same workload.
 
-With N > 1 (torchrun) the near-field offsets are split across the GPUs
-(work-balanced) and the partial products are all-reduced over NCCL inside
+With N > 1 (torchrun) the near-field (offset, target) pairs are split evenly
+across the GPUs and the partial products are all-reduced over NCCL inside
 every matvec (SURVEY §8e, cfg2): same total work, "scaling": "strong";
 value = DOF / max-over-ranks time. --parallelism replicas runs independent
 copies instead (weak scaling).
@@ -239,9 +239,9 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     op.set_stream(stream.cuda_stream)
     comm = None
-    if world > 1 and args.parallelism == "offsets":
-        # near-field offsets split across the GPUs, partial products
-        # all-reduced over NCCL inside every matvec (same total work: strong scaling)
+    if world > 1 and args.parallelism == "pairs":
+        # near-field (offset, target) pairs split evenly across the GPUs,
+        # partial products all-reduced over NCCL inside every matvec (strong scaling)
         from paper_2201_12050_b200.fmm import Communicator
 
         comm = Communicator(dev.index)
@@ -319,13 +319,14 @@ def run_ours(args):
 
     # roofline of the dominant kernel (near-field DMMA GEMM): algorithmic flops per launch
     m = data.counts
-    per_off = np.array([(m[0] - abs(int(o[0]))) * (m[1] - abs(int(o[1]))) * (m[2] - abs(int(o[2])))
-                        for o in data.near_offsets])
-    if comm is not None:  # rank 0's share of the offsets
-        from paper_2201_12050_b200.fmm import partition_offsets
+    n_pairs = int(sum((m[0] - abs(int(o[0]))) * (m[1] - abs(int(o[1]))) * (m[2] - abs(int(o[2])))
+                      for o in data.near_offsets))
+    if comm is not None:  # rank 0's share of the near-field pairs
+        from paper_2201_12050_b200.fmm import partition_pairs
 
-        per_off = per_off[partition_offsets(per_off, world) == rank]
-    flops = 8.0 * data.n_dof ** 2 * float(per_off.sum())
+        lo, hi = partition_pairs(n_pairs, world, rank)
+        n_pairs = hi - lo
+    flops = 8.0 * data.n_dof ** 2 * float(n_pairs)
     gemm_ms = stages["near_gemm"] / max(1, stages["applies"])
     achieved = flops / (gemm_ms * 1e-3) / 1e12
     peak, peak_src = fp64_peak()
@@ -346,7 +347,7 @@ def run_ours(args):
             "config": {
                 "workload": desc, "n_dof_total": data.N, "n_dof_cell": data.n_dof, "lattice": list(data.counts),
                 "near_offsets": data.n_near, "far_offsets": data.n_far, "n_t": 4, "nrhs": 1,
-                "parallelism": (f"near-field offsets split over {world} GPUs + NCCL all-reduce of y" if strong
+                "parallelism": (f"near-field pairs split over {world} GPUs + NCCL all-reduce of y" if strong
                                 else f"replicas x{world}" if world > 1 else "single GPU"),
                 "l2": f"inputs larger than L2: near-field operator {16 * data.n_near * data.n_dof ** 2 / 1e9:.2f} GB "
                       "streamed from HBM every step",
@@ -390,8 +391,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--gmres-max-iter", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--parallelism", choices=["offsets", "replicas"], default="offsets",
-                    help="N>1: split the near-field offsets (NCCL all-reduce) or run independent replicas")
+    ap.add_argument("--parallelism", choices=["pairs", "replicas"], default="pairs",
+                    help="N>1: split the near-field pairs (NCCL all-reduce) or run independent replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         # bounded CPU sample: each step is a full CPU matvec

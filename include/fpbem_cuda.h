@@ -176,7 +176,7 @@ long long fpbem_cu_kernel_launches(const fpbem_cu_op* op);
 
 /* Multi-GPU (one process per GPU). Rank 0 makes the id, the caller
  * broadcasts its 128 bytes (e.g. torch.distributed), every rank inits.
- * With a communicator attached, apply() splits the near-field offsets
+ * With a communicator attached, apply() splits the near-field pairs
  * across ranks and all-reduces the partial products. */
 int fpbem_cu_comm_unique_id(unsigned char id_out[128]);
 int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int device,
@@ -184,14 +184,15 @@ int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int de
 void fpbem_cu_comm_destroy(fpbem_cu_comm* comm);
 int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm);
 
-/* The same offset partition without a communicator: apply() returns this
- * rank's partial product (near field of its offsets; rank 0 adds the far
- * field). Summing the nranks partial products gives the full product. */
+/* The same partition without a communicator: apply() returns this rank's
+ * partial product (its near-field pairs; rank 0 adds the far field). Summing
+ * the nranks partial products gives the full product. */
 int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks);
 
-/* The partition rule itself (host only, no GPU): offsets weighted by work[s]
- * (= pairs(o)) assigned longest-first to the least-loaded rank. */
-int fpbem_cu_partition_offsets(int n_near, const long long* work, int nranks, int* owner);
+/* The partition rule itself (host only, no GPU): the near-field (offset,
+ * target) pairs, in offset-major order, split into nranks equal contiguous
+ * ranges [lo, hi) — every pair costs the same n_dof^2 complex MACs. */
+int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, long long* lo, long long* hi);
 
 const char* fpbem_cu_last_error(void);
 const char* fpbem_cu_version(void);

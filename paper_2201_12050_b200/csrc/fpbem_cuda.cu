@@ -112,7 +112,7 @@ struct fpbem_cu_op {
   int* tgt_pairs = nullptr;
   int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
   int jobs_nrhs = -1, n_jobs = 0, n_p2m_jobs = 0, jobs_cap = 0;
-  std::vector<int> rank_slots;  // offset slots this rank computes (all without a partition)
+  long long pair_lo = 0, pair_hi = 0;  // global pair range this rank computes (all without a partition)
   std::vector<int> pair_tgt;    // host copy: target cell of every pair
   int rank = 0, nranks = 1;     // near-field offset partition
 
@@ -167,32 +167,18 @@ struct fpbem_cu_op {
 
 namespace {
 
-// Work-balanced offset partition: longest-processing-time greedy over
-// pairs(o) (every offset's GEMM costs n_dof^2 * pairs(o)); deterministic.
-std::vector<int> partition_offsets(const std::vector<long long>& work, int nranks) {
-  std::vector<int> order(work.size()), owner(work.size(), 0);
-  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
-  std::vector<long long> load(nranks, 0);
-  for (int s : order) {
-    int best = 0;
-    for (int r = 1; r < nranks; ++r)
-      if (load[r] < load[best]) best = r;
-    owner[s] = best;
-    load[best] += work[s];
-  }
-  return owner;
+// Multi-GPU work split: every near-field pair (offset, target)
+// costs the same n_dof^2 MACs, so ranks take equal contiguous ranges of the
+// global pair order (offset-major) — balanced whatever the offset count.
+void pair_range(long long n_pairs, int nranks, int rank, long long& lo, long long& hi) {
+  lo = n_pairs * rank / nranks;
+  hi = n_pairs * (rank + 1) / nranks;
 }
 
 // per-target CSR of the pairs this rank owns, in offset order (the reduction order)
 void build_target_csr(fpbem_cu_op* op) {
-  std::vector<char> owned(op->n_near, 0);
-  for (int s : op->rank_slots) owned[s] = 1;
   std::vector<std::vector<int>> per_t(op->n_cells);
-  for (int s = 0; s < op->n_near; ++s) {
-    if (!owned[s]) continue;
-    for (int p = op->pair_start[s]; p < op->pair_start[s + 1]; ++p) per_t[op->pair_tgt[p]].push_back(p);
-  }
+  for (long long p = op->pair_lo; p < op->pair_hi; ++p) per_t[op->pair_tgt[p]].push_back(static_cast<int>(p));
   std::vector<int> tptr(op->n_cells + 1, 0), tpairs;
   for (int t = 0; t < op->n_cells; ++t) {
     tpairs.insert(tpairs.end(), per_t[t].begin(), per_t[t].end());
@@ -206,12 +192,7 @@ void build_target_csr(fpbem_cu_op* op) {
 
 void set_partition(fpbem_cu_op* op, int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) fail(FPBEM_CU_EINVAL, "partition: bad rank / nranks");
-  std::vector<long long> work(op->n_near);
-  for (int s = 0; s < op->n_near; ++s) work[s] = op->pair_start[s + 1] - op->pair_start[s];
-  std::vector<int> owner = partition_offsets(work, nranks);
-  op->rank_slots.clear();
-  for (int s = 0; s < op->n_near; ++s)
-    if (owner[s] == rank) op->rank_slots.push_back(s);
+  pair_range(op->n_pairs, nranks, rank, op->pair_lo, op->pair_hi);
   op->rank = rank;
   op->nranks = nranks;
   op->jobs_nrhs = -1;  // rebuild the GEMM job list
@@ -247,9 +228,10 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
   const char* nv = std::getenv("FPBEM_NARROW_TILES");
   const bool narrow = !(nv && std::strcmp(nv, "0") == 0) && !gemm_uses_mbar();
   std::vector<int4> jobs;
-  for (int s : op->rank_slots) {
-    const int pairs = op->pair_start[s + 1] - op->pair_start[s];
-    tile_columns(jobs, s, pairs * nrhs, op->pair_start[s], narrow);
+  for (int s = 0; s < op->n_near; ++s) {  // this rank's share of every offset's pairs
+    const long long a = std::max<long long>(op->pair_start[s], op->pair_lo);
+    const long long b = std::min<long long>(op->pair_start[s + 1], op->pair_hi);
+    if (a < b) tile_columns(jobs, s, static_cast<int>(b - a) * nrhs, static_cast<int>(a), narrow);
   }
   // offset order by default (consecutive tiles share S_o in L2);
   // FPBEM_JOB_ORDER=lpt puts the longest column tiles first (A/B timing)
@@ -1100,7 +1082,8 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->n_pairs = static_cast<int>(psrc.size());
     const int n_slots = d->n_near + op->n_hat;
     op->n_near = n_slots;  // slot count seen by the GEMM / reduction / partition
-    for (int s = 0; s < n_slots; ++s) op->rank_slots.push_back(s);
+    op->pair_lo = 0;
+    op->pair_hi = op->n_pairs;
     const size_t nn = static_cast<size_t>(op->n) * op->n;
     op->S = dalloc<c64>(nn * n_slots, "near blocks");
     auto put = [&](c64* dst, const fpbem_c64* src, size_t count, const char* what) {
@@ -1639,12 +1622,11 @@ int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks) {
   });
 }
 
-int fpbem_cu_partition_offsets(int n_near, const long long* work, int nranks, int* owner) {
+int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, long long* lo, long long* hi) {
   return guard([&] {
-    if (n_near < 0 || nranks < 1 || (n_near > 0 && (!work || !owner))) fail(FPBEM_CU_EINVAL, "partition: bad args");
-    std::vector<long long> w(work, work + n_near);
-    std::vector<int> o = partition_offsets(w, nranks);
-    std::copy(o.begin(), o.end(), owner);
+    if (n_pairs < 0 || nranks < 1 || rank < 0 || rank >= nranks || !lo || !hi)
+      fail(FPBEM_CU_EINVAL, "partition: bad args");
+    pair_range(n_pairs, nranks, rank, *lo, *hi);
   });
 }
 

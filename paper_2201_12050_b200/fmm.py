@@ -35,13 +35,28 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def partition_offsets(work, nranks: int) -> np.ndarray:
-    """The library's offset-partition rule (host only): owner rank per offset."""
-    w = np.ascontiguousarray(work, np.int64)
-    owner = np.zeros(len(w), np.int32)
-    _raise(_native.cuda().fpbem_cu_partition_offsets(len(w), w.ctypes.data_as(C.POINTER(C.c_longlong)), nranks,
-                                                     owner.ctypes.data_as(_native.c_int_p)))
-    return owner
+def partition_pairs(n_pairs: int, nranks: int, rank: int) -> tuple[int, int]:
+    """The library's multi-GPU split (host only): this rank's [lo, hi) range of
+    the near-field (offset, target) pairs in offset-major order."""
+    lo, hi = C.c_longlong(), C.c_longlong()
+    _raise(_native.cuda().fpbem_cu_partition_pairs(int(n_pairs), int(nranks), int(rank), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def near_pairs(counts, near_offsets):
+    """(offset slot, target cell, source cell) of every near-field pair in the
+    library's order: offsets in order, targets x-fastest (BlockToeplitzMatrix
+    matvec terms, src/assembly.cpp:62-84)."""
+    m = counts
+    out = []
+    for s, (ox, oy, oz) in enumerate(np.asarray(near_offsets).reshape(-1, 3)):
+        for tz in range(m[2]):
+            for ty in range(m[1]):
+                for tx in range(m[0]):
+                    sx, sy, sz = tx - ox, ty - oy, tz - oz
+                    if 0 <= sx < m[0] and 0 <= sy < m[1] and 0 <= sz < m[2]:
+                        out.append((s, tx + m[0] * (ty + m[1] * tz), sx + m[0] * (sy + m[1] * sz)))
+    return out
 
 
 class Communicator:
@@ -175,13 +190,13 @@ class FmmOperators:
         _raise(_native.cuda().fpbem_cu_set_stream(self._h, stream_ptr))
 
     def set_partition(self, rank: int, nranks: int) -> None:
-        """Near-field offset partition without communication: matvec returns
+        """Near-field pair partition without communication: matvec returns
         this rank's partial product (rank 0 includes the far field)."""
         _raise(_native.cuda().fpbem_cu_fmm_set_partition(self._h, rank, nranks))
 
     def set_comm(self, comm) -> None:
-        """Attach a Communicator: offsets split across its ranks, partial
-        products all-reduced over NCCL inside every matvec."""
+        """Attach a Communicator: near-field pairs split across its ranks,
+        partial products all-reduced over NCCL inside every matvec."""
         _raise(_native.cuda().fpbem_cu_fmm_set_comm(self._h, comm.handle if comm is not None else None))
         self._comm = comm
 
