@@ -571,3 +571,43 @@ def test_batched_gmres_max_iter_and_nan(ops, assembled):
     b[d.N + 7] = np.nan
     with pytest.raises(RuntimeError, match="non-finite"):
         gmres(ops(d, max_rhs=2), b, tol=1e-6, restart=5, max_iter=12)
+
+
+# ---- BASELINE sizes ----------------------------------------------------------------
+
+@pytest.mark.parametrize("cid", [2, 3, 4])
+def test_full_size_matvec_parity_and_properties(ops, cid):
+    """configs[cid-1] at the stated size: operator assembled on the GPU, product
+    against the oracle (seed = config id), linearity, determinism, and the
+    8-way pair partition summing back to the product."""
+    from paper_2201_12050_b200 import Scene
+    from paper_2201_12050_b200.fmm import assemble_near_gpu
+
+    sc = Scene(cid, 0)
+    d = sc.assemble_fmm(4, skip_near_values=True)
+    near = assemble_near_gpu(sc, d)
+
+    class WithNear:
+        def __init__(self, d, blocks):
+            self._d, self.near_blocks = d, blocks
+
+        def __getattr__(self, k):
+            return getattr(self._d, k)
+
+    full = WithNear(d, near.cpu().numpy())
+    op = ops(d, near_blocks=near)
+    rng = np.random.default_rng(cid)
+    p, q = uvec(rng, d.N), uvec(rng, d.N)
+    y = op.matvec(p)
+    assert rel(y, O.OracleFmm(full).matvec(p)) <= MATVEC_TOL
+    assert np.array_equal(y, op.matvec(p))
+    a = 0.7 - 0.2j
+    assert rel(op.matvec(a * p + q), a * y + op.matvec(q)) < 1e-13
+    if cid == 3:
+        total = np.zeros_like(y)
+        for r in range(8):
+            part = ops(d, near_blocks=near)
+            part.set_partition(r, 8)
+            total += part.matvec(p)
+            part.close()
+        assert rel(total, y) < 1e-13
