@@ -334,7 +334,7 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   // column's fields fit in shared memory (FPBEM_M2L_FUSE=0 disables)
   const char* fz = std::getenv("FPBEM_M2L_FUSE");
   const bool fuse_z = Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
-                      m2l_zfused_smem(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E)) <= 160 * 1024;
+                      m2l_zfused_ring(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E), op->b) > 0;
   if (Lx > 1) {
     passes.push_back({0, My * Mz, static_cast<int>(Mx), static_cast<int>(Lx), E, static_cast<int>(Lx), 0, false});
     cx = Lx;
@@ -389,7 +389,12 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
 // L2P); with a communicator the partial products are all-reduced.
 void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
   cudaStream_t s = op->stream;
-  cudaStream_t a = op->aux;
+  // FPBEM_SERIAL=1 runs P2M + M2L on the main stream (exact per-stage timing)
+  static const bool serial = [] {
+    const char* v = std::getenv("FPBEM_SERIAL");
+    return v && std::strcmp(v, "1") == 0;
+  }();
+  cudaStream_t a = serial ? op->stream : op->aux;
   const bool far_here = op->rank == 0;
   build_jobs(op, nrhs);
   // fork: P2M + M2L on the aux stream while the near-field GEMM runs on the main one

@@ -26,7 +26,9 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
 cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image, long long q_total, int b,
                                 int nrhs, cudaStream_t stream);
 // fused forward-z DFT + mode product + inverse-z DFT, one CTA per (qy, qx) column
-size_t m2l_zfused_smem(int Mz, int Lz, int E);
+// ring depth (Λ mode blocks in shared memory) of the fused z kernel, 0 when
+// the column's fields leave no room for >= 4 (then the unfused passes run)
+int m2l_zfused_ring(int Mz, int Lz, int E, int b);
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
                               long long plane, int E, int b, double scale, cudaStream_t stream);
 cudaError_t launch_mirror_permute(const c64* in, c64* out, const int counts[3], int level, long long E,

@@ -12,6 +12,8 @@
 // (nrhs x b, contiguous) innermost, so every warp access is coalesced. The
 // per-mode product streams Λ once per apply (the HBM-bound part).
 // P2M (src/fmm.cpp:256-259) runs as a job list of the DMMA block GEMM (near_field.cu).
+#include <cstdio>
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -21,44 +23,62 @@ namespace {
 
 // out[a][qo][bi][e] = scale * sum_{j < n_in} tw[(j*qo*sign) mod L] * in[a][j][bi][e]
 // with tw[k] = exp(-2 pi i k / L); sign = +1 forward, -1 backward (conjugate).
-__global__ void dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ tw,
-                                long long n_a, int n_in, int n_out, long long n_inner, int L, int backward,
-                                double scale) {
-  const long long total = n_a * n_out * n_inner;
+// One thread owns kQG consecutive outputs qo of one (a, inner) column, so each
+// input is read once per kQG outputs (not once per output); consecutive
+// threads take consecutive inner indices (coalesced loads and stores). Each
+// output is still summed in j order.
+template <int kQG>
+__global__ void __launch_bounds__(256)
+dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ tw, long long n_a,
+                int n_in, int n_out, long long n_inner, int L, int backward, double scale) {
+  extern __shared__ __align__(16) unsigned char dft_smem[];
+  c64* tw_s = reinterpret_cast<c64*>(dft_smem);  // the L twiddles, conjugated for the backward pass
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    c64 w = tw[k];
+    if (backward) w.y = -w.y;
+    tw_s[k] = w;
+  }
+  __syncthreads();
+  const int n_grp = (n_out + kQG - 1) / kQG;
+  const long long total = n_a * n_grp * n_inner;
   for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
        g += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long inner = g % n_inner;
     const long long rest = g / n_inner;
-    const int qo = static_cast<int>(rest % n_out);
-    const long long a = rest / n_out;
+    const int q0 = static_cast<int>(rest % n_grp) * kQG;
+    const long long a = rest / n_grp;
     const c64* src = in + (a * n_in) * n_inner + inner;
-    c64 acc = cmk(0.0, 0.0);
-    int idx = 0;  // (j * qo) mod L, advanced incrementally
-    int j = 0;
-    // batches of 8 independent loads, accumulated in j order
-    for (; j + 8 <= n_in; j += 8) {
-      c64 v[8], w[8];
+    c64 acc[kQG];
+    int idx[kQG], step[kQG];  // (j * qo) mod L per output, advanced incrementally
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        v[u] = src[static_cast<long long>(j + u) * n_inner];
-        w[u] = __ldg(tw + idx);
-        idx += qo;
-        if (idx >= L) idx -= L;
-      }
+    for (int o = 0; o < kQG; ++o) {
+      acc[o] = cmk(0.0, 0.0);
+      idx[o] = 0;
+      step[o] = (q0 + o) % L;  // padded outputs (q0 + o >= n_out) may exceed L
+    }
+    // 4 inputs and their twiddles are loaded before the FMAs (latency of the
+    // dependent loads otherwise dominates); zero-padded tail: fma(w, 0, acc) == acc
+    for (int j0 = 0; j0 < n_in; j0 += 4) {
+      c64 v[4], w[kQG][4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (backward) w[u].y = -w[u].y;
-        acc = cfma(w[u], v[u], acc);
-      }
+      for (int u = 0; u < 4; ++u) v[u] = (j0 + u < n_in) ? src[static_cast<long long>(j0 + u) * n_inner] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int o = 0; o < kQG; ++o)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          w[o][u] = tw_s[idx[o]];
+          idx[o] += step[o];
+          if (idx[o] >= L) idx[o] -= L;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int o = 0; o < kQG; ++o) acc[o] = cfma(w[o][u], v[u], acc[o]);
     }
-    for (; j < n_in; ++j) {
-      c64 w = __ldg(tw + idx);
-      if (backward) w.y = -w.y;
-      acc = cfma(w, src[static_cast<long long>(j) * n_inner], acc);
-      idx += qo;
-      if (idx >= L) idx -= L;
-    }
-    out[g] = cscale(acc, scale);
+    c64* dst = out + (a * n_out + q0) * n_inner + inner;
+#pragma unroll
+    for (int o = 0; o < kQG; ++o)
+      if (q0 + o < n_out) dst[static_cast<long long>(o) * n_inner] = cscale(acc[o], scale);
   }
 }
 
@@ -83,70 +103,237 @@ __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* _
 
 // Last-axis fusion: forward DFT along z (Mz nonzero inputs -> Lz modes), the
 // per-mode product with Λ_q, and the pruned inverse along z (Lz modes -> Mz
-// kept outputs), for one (qy, qx) column per CTA. The z-extended field never
-// touches HBM; Λ is streamed once.
+// kept outputs) for one (qy, qx) column at a time; the z-extended field never
+// touches HBM. Persistent, one CTA per SM walking columns blockIdx.x,
+// +gridDim.x, ..., warp-specialised:
+//   warp 0 (lane 0) produces: Λ (the only large operand, read exactly once)
+//     streams through a ring of `ring` mode blocks (each b x b block is
+//     contiguous: one cp.async.bulk per mode, landing on full[slot]); a slot is
+//     refilled as soon as its consumer releases it (empty[slot]), so the stream
+//     runs on across column boundaries. Input columns (Mz rows of E contiguous
+//     values) arrive the same way in kInBufs rotating buffers.
+//   warps 1..n_cons consume (ring = 2 n_cons, or n_cons when the ring is
+//     short): consumer warp w owns slots w and w + n_cons and takes the modes
+//     g = w (mod n_cons), so consecutive modes of a warp alternate between its
+//     two slots (one refill in flight while it computes on the other) and a
+//     warp never waits more than one phase ahead on a slot; forward DFT and
+//     inverse DFT are shared by all consumer warps between named barriers.
+// Measured: this producer/consumer split streams at HBM speed with one CTA
+// per SM, where barrier-separated refill rounds reached only ~55% of it
+// (tools/bulk_stream_bench.cu).
 //   in  : F2[iz][plane][E]   (iz < Mz)      out: H2[iz][plane][E] (iz < Mz)
 //   E = nrhs * b fields, plane = Ly * Lx columns, lambda[q][b*b], q = qz*plane + column
-__global__ void __launch_bounds__(256)
-m2l_zfused_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
-                  const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, double scale) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  c64* f_in = reinterpret_cast<c64*>(smem_raw);  // Mz x E
-  c64* f_z = f_in + Mz * E;                       // Lz x E  (forward along z)
-  c64* g_z = f_z + Lz * E;                        // Lz x E  (after the mode product)
-  const long long col = blockIdx.x;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < Mz * E; e += blockDim.x) {
-    const int iz = e / E, f = e % E;
-    f_in[e] = in[(static_cast<long long>(iz) * plane + col) * E + f];
-  }
-  __syncthreads();
-  for (int e = tid; e < Lz * E; e += blockDim.x) {
-    const int qz = e / E, f = e % E;
-    c64 acc = cmk(0.0, 0.0);
-    int idx = 0;
-    for (int iz = 0; iz < Mz; ++iz) {
-      acc = cfma(__ldg(tw + idx), f_in[iz * E + f], acc);
-      idx += qz;
-      if (idx >= Lz) idx -= Lz;
+constexpr int kMaxRing = 16;
+constexpr int kInBufs = 4;
+constexpr size_t kZfSmemMax = 225 * 1024;  // dynamic; static barriers + driver share take the rest
+
+__device__ __forceinline__ void consumer_sync(int n_threads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(n_threads) : "memory");
+}
+
+// One z-DFT phase of the fused kernel, over the consumer threads:
+//   dst[o][f] = scale * sum_{j < n_in} w(j*o mod L) src[j][f],  o < n_out
+// w = tw (forward) or conj(tw) (backward; results go to global `out` rows
+// (o*plane + col)*E). A thread owns G consecutive outputs of one field
+// (independent chains sharing each input load); G = 1 uses two partial sums.
+__device__ __forceinline__ int zdft_group(int outputs, int threads) {
+  return outputs >= 3 * threads ? 4 : (outputs >= 3 * threads / 2 ? 2 : 1);
+}
+
+template <int G, bool kBack>
+__device__ __forceinline__ void zdft(const c64* __restrict__ src, c64* __restrict__ dst, const c64* __restrict__ tw_s,
+                                     int n_in, int n_out, int L, int E, int ct, int n_ct, double scale,
+                                     c64* __restrict__ out, long long plane, long long col) {
+  // shared-load latency (~60 cycles) dominates a naive loop: inputs and
+  // twiddles of 4 terms are loaded before their FMAs, and even / odd terms
+  // feed separate partial sums
+  const int n_g = (n_out + G - 1) / G;
+  for (int e = ct; e < n_g * E; e += n_ct) {
+    const int g = e / E, f = e - g * E, o0 = g * G;
+    c64 acc[G][2];
+    int idx[G], step[G];
+#pragma unroll
+    for (int o = 0; o < G; ++o) {
+      acc[o][0] = acc[o][1] = cmk(0.0, 0.0);
+      idx[o] = 0;
+      step[o] = (o0 + o) % L;  // padded outputs (o0 + o >= n_out) may exceed L
     }
-    f_z[e] = acc;
+    int j = 0;
+    for (; j + 4 <= n_in; j += 4) {
+      c64 v[4], w[G][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = src[(j + u) * E + f];
+#pragma unroll
+      for (int o = 0; o < G; ++o)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          w[o][u] = tw_s[idx[o]];
+          idx[o] += step[o];
+          if (idx[o] >= L) idx[o] -= L;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int o = 0; o < G; ++o) {
+          c64 t = w[o][u];
+          if (kBack) t.y = -t.y;
+          acc[o][u & 1] = cfma(t, v[u], acc[o][u & 1]);
+        }
+    }
+    for (; j < n_in; ++j) {
+      const c64 v = src[j * E + f];
+#pragma unroll
+      for (int o = 0; o < G; ++o) {
+        c64 t = tw_s[idx[o]];
+        if (kBack) t.y = -t.y;
+        acc[o][0] = cfma(t, v, acc[o][0]);
+        idx[o] += step[o];
+        if (idx[o] >= L) idx[o] -= L;
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < G; ++o) {
+      if (o0 + o >= n_out) continue;
+      const c64 r = cadd(acc[o][0], acc[o][1]);
+      if (kBack)
+        out[(static_cast<long long>(o0 + o) * plane + col) * E + f] = cscale(r, scale);
+      else
+        dst[(o0 + o) * E + f] = r;
+    }
   }
-  __syncthreads();
-  // mode product: g[qz][r*b + i] = sum_c Λ_q[i + b c] f[qz][r*b + c]; lanes over i read Λ contiguously
-  const int nrhs = E / b;
-  for (int e = tid; e < Lz * E; e += blockDim.x) {
-    const int qz = e / E, ri = e % E;
-    const int r = ri / b, i = ri % b;
-    const c64* lam = lambda + (static_cast<long long>(qz) * plane + col) * b * b + i;
-    const c64* f = f_z + qz * E + r * b;
-    c64 acc = cmk(0.0, 0.0);
+}
+
+// one mode's product for the lanes of a warp: g[ri] = sum_c lam[i + b c] f[r b + c]
+__device__ __forceinline__ void mode_product_warp(const c64* __restrict__ lam_blk, const c64* __restrict__ f_mode,
+                                                  c64* __restrict__ g_mode, int E, int b, int lane) {
+  for (int ri = lane; ri < E; ri += 32) {
+    const int r = ri / b, i = ri - r * b;
+    const c64* lam = lam_blk + i;
+    const c64* f = f_mode + r * b;
+    c64 acc0 = cmk(0.0, 0.0), acc1 = cmk(0.0, 0.0);
     int c = 0;
-    for (; c + 5 <= b; c += 5) {
-      c64 l[5];
+    for (; c + 4 <= b; c += 4) {
+      c64 l[4], v[4];
 #pragma unroll
-      for (int u = 0; u < 5; ++u) l[u] = __ldg(lam + static_cast<long long>(c + u) * b);
-#pragma unroll
-      for (int u = 0; u < 5; ++u) acc = cfma(l[u], f[c + u], acc);
+      for (int u = 0; u < 4; ++u) {
+        l[u] = lam[(c + u) * b];
+        v[u] = f[c + u];
+      }
+      acc0 = cfma(l[0], v[0], acc0);
+      acc1 = cfma(l[1], v[1], acc1);
+      acc0 = cfma(l[2], v[2], acc0);
+      acc1 = cfma(l[3], v[3], acc1);
     }
-    for (; c < b; ++c) acc = cfma(__ldg(lam + static_cast<long long>(c) * b), f[c], acc);
-    g_z[e] = acc;
+    for (; c < b; ++c) acc0 = cfma(lam[c * b], f[c], acc0);
+    g_mode[ri] = cadd(acc0, acc1);
   }
-  (void)nrhs;
+}
+
+__global__ void __launch_bounds__(32 * (kMaxRing + 1))
+m2l_zfused_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
+                  const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, int ring,
+                  int n_cons, double scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b2 = b * b;
+  c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
+  c64* f_in0 = ring_buf + ring * b2;                  // kInBufs x Mz x E
+  c64* f_z = f_in0 + kInBufs * Mz * E;                // Lz x E  (forward along z)
+  c64* g_z = f_z + Lz * E;                            // Lz x E  (after the mode product)
+  c64* tw_s = g_z + Lz * E;                           // Lz twiddles exp(-2 pi i k / Lz)
+  __shared__ __align__(8) unsigned long long full[kMaxRing], empty[kMaxRing];
+  __shared__ __align__(8) unsigned long long in_full[kInBufs], in_empty[kInBufs];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_cols = static_cast<int>((plane - blockIdx.x + gridDim.x - 1) / gridDim.x);  // this CTA's columns
+  if (tid == 0) {
+    for (int s = 0; s < ring; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int s = 0; s < kInBufs; ++s) {
+      mbar_init(smem_u32(&in_full[s]), 1);
+      mbar_init(smem_u32(&in_empty[s]), 1);
+    }
+    mbar_fence_init();
+  }
+  for (int k = tid; k < Lz; k += blockDim.x) tw_s[k] = tw[k];
   __syncthreads();
-  for (int e = tid; e < Mz * E; e += blockDim.x) {
-    const int iz = e / E, f = e % E;
-    c64 acc = cmk(0.0, 0.0);
-    int idx = 0;
-    for (int qz = 0; qz < Lz; ++qz) {
-      c64 w = __ldg(tw + idx);
-      w.y = -w.y;
-      acc = cfma(w, g_z[qz * E + f], acc);
-      idx += iz;
-      if (idx >= Lz) idx -= Lz;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer
+      const unsigned lam_bytes = static_cast<unsigned>(b2 * sizeof(c64));
+      const unsigned row_bytes = static_cast<unsigned>(E * sizeof(c64));
+      auto issue_input = [&](int k) {
+        if (k >= n_cols) return;
+        const int buf = k % kInBufs;
+        if (k >= kInBufs) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / kInBufs - 1) & 1));
+        const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
+        const unsigned bar = smem_u32(&in_full[buf]);
+        c64* dst = f_in0 + buf * Mz * E;
+        mbar_arrive_expect_tx(bar, row_bytes * Mz);
+        for (int iz = 0; iz < Mz; ++iz) bulk_g2s(smem_u32(dst + iz * E), in + (iz * plane + col) * E, row_bytes, bar);
+      };
+      issue_input(0);
+      int slot = 0;
+      unsigned phase = 0;  // phase of the ring pass being filled
+      long long g = 0;     // global mode counter
+      const c64* col_lam = lambda + static_cast<long long>(blockIdx.x) * b2;
+      const long long col_step = static_cast<long long>(gridDim.x) * b2, mode_step = plane * b2;
+      for (int k = 0; k < n_cols; ++k, col_lam += col_step) {
+        issue_input(k + 1);
+        for (int qz = 0; qz < Lz; ++qz, ++g) {
+          if (g >= ring) mbar_wait(smem_u32(&empty[slot]), phase ^ 1u);
+          const unsigned bar = smem_u32(&full[slot]);
+          mbar_arrive_expect_tx(bar, lam_bytes);
+          bulk_g2s(smem_u32(ring_buf + slot * b2), col_lam + qz * mode_step, lam_bytes, bar);
+          if (++slot == ring) {
+            slot = 0;
+            phase ^= 1u;
+          }
+        }
+      }
     }
-    out[(static_cast<long long>(iz) * plane + col) * E + f] = cscale(acc, scale);
+  } else {  // ---- consumers
+    const int cw = warp - 1, ct = tid - 32, n_ct = n_cons * 32;
+    for (int k = 0; k < n_cols; ++k) {
+      const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
+      const int buf = k % kInBufs;
+      const c64* f_in = f_in0 + buf * Mz * E;
+      mbar_wait(smem_u32(&in_full[buf]), static_cast<unsigned>((k / kInBufs) & 1));
+      // forward along z: f_z[qz][f] = sum_iz tw[iz*qz mod Lz] f_in[iz][f]
+      {
+        const int G = zdft_group(Lz * E, n_ct);
+        if (G == 4) zdft<4, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, ct, n_ct, 1.0, nullptr, 0, 0);
+        else if (G == 2) zdft<2, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, ct, n_ct, 1.0, nullptr, 0, 0);
+        else zdft<1, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, ct, n_ct, 1.0, nullptr, 0, 0);
+      }
+      consumer_sync(n_ct);  // f_z complete, input buffer released
+      if (ct == 0) mbar_arrive(smem_u32(&in_empty[buf]));
+      // this warp's modes of column k: global g = k*Lz + qz with g % n_cons == cw
+      const long long g_first = static_cast<long long>(k) * Lz;
+      int qz = static_cast<int>(((cw - g_first) % n_cons + n_cons) % n_cons);
+      for (; qz < Lz; qz += n_cons) {
+        const long long g = g_first + qz;
+        const int slot = static_cast<int>(g % ring);
+        mbar_wait(smem_u32(&full[slot]), static_cast<unsigned>((g / ring) & 1));
+        // g[qz][r*b + i] = sum_c Λ_q[i + b c] f[qz][r*b + c]
+        mode_product_warp(ring_buf + slot * b2, f_z + qz * E, g_z + qz * E, E, b, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
+      }
+      consumer_sync(n_ct);  // g_z complete
+      // inverse along z, kept outputs only: out[iz][f] = scale sum_qz conj(tw[iz*qz mod Lz]) g_z[qz][f]
+      {
+        const int G = zdft_group(Mz * E, n_ct);
+        if (G == 4) zdft<4, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, ct, n_ct, scale, out, plane, col);
+        else if (G == 2) zdft<2, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, ct, n_ct, scale, out, plane, col);
+        else zdft<1, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, ct, n_ct, scale, out, plane, col);
+      }
+      // the next column's forward pass writes f_z only (no reader left after
+      // the barrier above); its mode products write g_z only after the next
+      // barrier, which every thread reaches after finishing this inverse pass
+    }
   }
+  __syncthreads();  // the producer stays resident until every copy it issued has landed
 }
 
 // zero the embedded field and place each K_o at slot (o mod L) (src/structured.cpp:73-86)
@@ -200,10 +387,31 @@ int grid_for(long long total, int threads) {
 
 cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_a, int n_in, int n_out,
                             long long n_inner, int L, bool backward, double scale, cudaStream_t stream) {
-  const long long total = n_a * n_out * n_inner;
-  if (total == 0) return cudaSuccess;
-  dft_axis_kernel<<<grid_for(total, 256), 256, 0, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L,
-                                                            backward ? 1 : 0, scale);
+  if (n_a * n_out * n_inner == 0) return cudaSuccess;
+  // widest output group that still gives >= 2 x 256 threads per SM
+  const long long want = 2LL * kNumSMs * 256;
+  int qg = 8;
+  while (qg > 1 && n_a * ((n_out + qg - 1) / qg) * n_inner < want) qg /= 2;
+  const long long total = n_a * ((n_out + qg - 1) / qg) * n_inner;
+  const int grid = grid_for(total, 256), bw = backward ? 1 : 0;
+  const size_t smem = sizeof(c64) * static_cast<size_t>(L);
+  if (smem > 48 * 1024) {  // L > 3072: raise the dynamic shared-memory limit once per instantiation
+    static bool raised = false;
+    if (!raised) {
+      for (auto fn : {dft_axis_kernel<8>, dft_axis_kernel<4>, dft_axis_kernel<2>, dft_axis_kernel<1>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+      }
+      raised = true;
+    }
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  }
+  switch (qg) {
+    case 8: dft_axis_kernel<8><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
+    case 4: dft_axis_kernel<4><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
+    case 2: dft_axis_kernel<2><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
+    default: dft_axis_kernel<1><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
+  }
   return cudaGetLastError();
 }
 
@@ -226,11 +434,62 @@ cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream)
   return cudaGetLastError();
 }
 
-size_t m2l_zfused_smem(int Mz, int Lz, int E) { return sizeof(c64) * static_cast<size_t>(Mz + 2 * Lz) * E; }
+namespace {
+size_t zfused_fields_bytes(int Mz, int Lz, int E) {
+  return sizeof(c64) * (static_cast<size_t>(kInBufs * Mz + 2 * Lz) * E + Lz);
+}
+}  // namespace
+
+namespace {
+int zfused_ring_for(int Mz, int Lz, int E, int b, int ctas);
+
+// CTAs per SM: two when a whole column's modes fit the smaller ring (then the
+// two CTAs' DFT phases and streams interleave), else one with the deeper ring
+// (measured: cfg5 Lz = 7 prefers two, cfg3 Lz = 32 one). FPBEM_ZF_CTAS=1|2 overrides.
+int zfused_ctas_per_sm(int Mz, int Lz, int E, int b) {
+  static const int forced = [] {
+    const char* s = std::getenv("FPBEM_ZF_CTAS");
+    return s ? std::atoi(s) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  const int r2 = zfused_ring_for(Mz, Lz, E, b, 2);
+  return (r2 >= 4 && r2 >= Lz) ? 2 : 1;
+}
+
+int zfused_ring_for(int Mz, int Lz, int E, int b, int ctas) {
+  const size_t budget = kZfSmemMax / ctas - (ctas > 1 ? 2048 : 0);
+  const size_t fields = zfused_fields_bytes(Mz, Lz, E);
+  const size_t per_mode = sizeof(c64) * static_cast<size_t>(b) * b;
+  if (fields >= budget) return 0;
+  long long r = static_cast<long long>((budget - fields) / per_mode);
+  if (r > kMaxRing) r = kMaxRing;
+  return r >= 4 ? static_cast<int>(r) : 0;
+}
+}  // namespace
+
+int m2l_zfused_ring(int Mz, int Lz, int E, int b) {
+  const int r = zfused_ring_for(Mz, Lz, E, b, zfused_ctas_per_sm(Mz, Lz, E, b));
+  return r > 0 ? r : zfused_ring_for(Mz, Lz, E, b, 1);
+}
 
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
                               long long plane, int E, int b, double scale, cudaStream_t stream) {
-  const size_t smem = m2l_zfused_smem(Mz, Lz, E);
+  int ctas = zfused_ctas_per_sm(Mz, Lz, E, b);
+  int ring = zfused_ring_for(Mz, Lz, E, b, ctas);
+  if (ring == 0) {
+    ctas = 1;
+    ring = zfused_ring_for(Mz, Lz, E, b, 1);
+  }
+  if (ring == 0) return cudaErrorInvalidValue;
+  // two slots per consumer warp when the ring is deep enough (FPBEM_ZF_SLOTS=1 forces one)
+  static const int slots_per_warp = [] {
+    const char* s = std::getenv("FPBEM_ZF_SLOTS");
+    return (s && s[0] == '1') ? 1 : 2;
+  }();
+  const bool two = slots_per_warp == 2 && ring >= 8;
+  const int n_cons = two ? ring / 2 : ring;
+  ring = two ? 2 * n_cons : ring;
+  const size_t smem = zfused_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(m2l_zfused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -238,8 +497,10 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  m2l_zfused_kernel<<<static_cast<unsigned>(plane), 256, smem, stream>>>(in, out, lambda, tw, Mz, Lz, plane, E, b,
-                                                                         scale);
+  const long long slots = static_cast<long long>(kNumSMs) * ctas;
+  const long long grid = plane < slots ? plane : slots;
+  m2l_zfused_kernel<<<static_cast<unsigned>(grid), 32 * (n_cons + 1), smem, stream>>>(
+      in, out, lambda, tw, Mz, Lz, plane, E, b, ring, n_cons, scale);
   return cudaGetLastError();
 }
 
