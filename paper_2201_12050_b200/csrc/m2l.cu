@@ -124,7 +124,7 @@ __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* _
 //   in  : F2[iz][plane][E]   (iz < Mz)      out: H2[iz][plane][E] (iz < Mz)
 //   E = nrhs * b fields, plane = Ly * Lx columns, lambda[q][b*b], q = qz*plane + column
 constexpr int kMaxRing = 16;
-constexpr int kInBufs = 4;
+constexpr int kInBufs = 3;
 constexpr size_t kZfSmemMax = 225 * 1024;  // dynamic; static barriers + driver share take the rest
 
 __device__ __forceinline__ void consumer_sync(int n_threads) {
@@ -336,6 +336,167 @@ m2l_zfused_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* 
   __syncthreads();  // the producer stays resident until every copy it issued has landed
 }
 
+// Three-role variant of the fused z kernel (same math, same layouts): the
+// z-DFTs move off the streaming warps so the Λ stream never waits on them.
+//   warp 0 lane 0      producer (Λ ring + input columns), as above
+//   n_mw mode warps    stream column after column: warp w owns ring slots w and
+//                      w + n_mw and takes the modes g = w (mod n_mw); reads
+//                      f_z[k%2], writes g_z[k%2]
+//   n_dw DFT warps     iteration k: forward DFT of column k into f_z[k%2], then
+//                      inverse DFT of column k-1 from g_z[(k-1)%2]
+// Hand-offs (mbarriers, phases by column parity):
+//   fwd_done[c%2]  DFT -> mode   f_z of column c ready          (count 1)
+//   col_done[c%2]  mode -> DFT   modes of column c finished:    (count n_mw)
+//                                g_z complete, f_z free again
+//   inv_done[c%2]  DFT -> mode   inverse of column c read g_z   (count 1)
+// While the mode warps stream column k, the DFT warps compute column k+1's
+// forward pass and column k-1's inverse.
+constexpr int kPipeMaxModeWarps = 8;
+constexpr int kPipeMaxRing = 16;
+constexpr int kPipeMaxDftWarps = 8;
+
+__device__ __forceinline__ void dft_sync(int n_threads) {
+  asm volatile("bar.sync 2, %0;\n" ::"r"(n_threads) : "memory");
+}
+
+__global__ void __launch_bounds__(32 * (1 + kPipeMaxModeWarps + kPipeMaxDftWarps), 1)
+m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
+                 const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, int n_mw,
+                 int ring, int n_dw, double scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b2 = b * b;
+  c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
+  c64* f_in0 = ring_buf + ring * b2;                  // kInBufs x Mz x E
+  c64* f_z0 = f_in0 + kInBufs * Mz * E;               // 2 x Lz x E
+  c64* g_z0 = f_z0 + 2 * Lz * E;                      // 2 x Lz x E
+  c64* tw_s = g_z0 + 2 * Lz * E;                      // Lz twiddles
+  __shared__ __align__(8) unsigned long long full[kPipeMaxRing], empty[kPipeMaxRing];
+  __shared__ __align__(8) unsigned long long in_full[kInBufs], in_empty[kInBufs];
+  __shared__ __align__(8) unsigned long long fwd_done[2], col_done[2], inv_done[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_cols = static_cast<int>((plane - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  if (tid == 0) {
+    for (int s = 0; s < ring; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int s = 0; s < kInBufs; ++s) {
+      mbar_init(smem_u32(&in_full[s]), 1);
+      mbar_init(smem_u32(&in_empty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&fwd_done[s]), 1);
+      mbar_init(smem_u32(&col_done[s]), n_mw);
+      mbar_init(smem_u32(&inv_done[s]), 1);
+    }
+    mbar_fence_init();
+  }
+  for (int k = tid; k < Lz; k += blockDim.x) tw_s[k] = tw[k];
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer
+      const unsigned lam_bytes = static_cast<unsigned>(b2 * sizeof(c64));
+      const unsigned row_bytes = static_cast<unsigned>(E * sizeof(c64));
+      auto issue_input = [&](int k) {
+        if (k >= n_cols) return;
+        const int buf = k % kInBufs;
+        if (k >= kInBufs) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / kInBufs - 1) & 1));
+        const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
+        const unsigned bar = smem_u32(&in_full[buf]);
+        c64* dst = f_in0 + buf * Mz * E;
+        mbar_arrive_expect_tx(bar, row_bytes * Mz);
+        for (int iz = 0; iz < Mz; ++iz) bulk_g2s(smem_u32(dst + iz * E), in + (iz * plane + col) * E, row_bytes, bar);
+      };
+      issue_input(0);
+      issue_input(1);
+      int slot = 0;
+      unsigned phase = 0;
+      long long g = 0;
+      const c64* col_lam = lambda + static_cast<long long>(blockIdx.x) * b2;
+      const long long col_step = static_cast<long long>(gridDim.x) * b2, mode_step = plane * b2;
+      for (int k = 0; k < n_cols; ++k, col_lam += col_step) {
+        issue_input(k + 2);
+        for (int qz = 0; qz < Lz; ++qz, ++g) {
+          if (g >= ring) mbar_wait(smem_u32(&empty[slot]), phase ^ 1u);
+          const unsigned bar = smem_u32(&full[slot]);
+          mbar_arrive_expect_tx(bar, lam_bytes);
+          bulk_g2s(smem_u32(ring_buf + slot * b2), col_lam + qz * mode_step, lam_bytes, bar);
+          if (++slot == ring) {
+            slot = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp <= n_mw) {  // ---- mode warps
+    const int w = warp - 1;
+    // this warp's modes are the global g = w, w + n_mw, w + 2 n_mw, ...
+    // (ring = spw * n_mw): the j-th lands in slot w + (j % spw) n_mw, phase (j / spw) & 1
+    const int spw = ring / n_mw;
+    long long g = w;
+    int jm = 0;             // j % spw
+    unsigned jphase = 0;    // (j / spw) & 1
+    for (int k = 0; k < n_cols; ++k) {
+      const int buf = k & 1;
+      const unsigned use = static_cast<unsigned>((k >> 1) & 1);
+      mbar_wait(smem_u32(&fwd_done[buf]), use);                                   // f_z[buf] holds column k
+      if (k >= 2) mbar_wait(smem_u32(&inv_done[buf]), use ^ 1u);                  // g_z[buf] read by inverse(k-2)
+      const c64* f_z = f_z0 + buf * Lz * E;
+      c64* g_z = g_z0 + buf * Lz * E;
+      const long long g_end = static_cast<long long>(k + 1) * Lz;
+      for (; g < g_end; g += n_mw) {
+        const int qz = static_cast<int>(g - static_cast<long long>(k) * Lz);
+        const int slot = w + jm * n_mw;
+        mbar_wait(smem_u32(&full[slot]), jphase);
+        if (++jm == spw) {
+          jm = 0;
+          jphase ^= 1u;
+        }
+        mode_product_warp(ring_buf + slot * b2, f_z + qz * E, g_z + qz * E, E, b, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&col_done[buf]));
+    }
+  } else {  // ---- DFT warps
+    const int dt = tid - 32 * (1 + n_mw), n_dt = 32 * n_dw;
+    auto inverse = [&](int c) {  // inverse z of column c (its modes are finished)
+      const int buf = c & 1;
+      mbar_wait(smem_u32(&col_done[buf]), static_cast<unsigned>((c >> 1) & 1));
+      const long long col = blockIdx.x + static_cast<long long>(c) * gridDim.x;
+      const c64* g_z = g_z0 + buf * Lz * E;
+      const int G = zdft_group(Mz * E, n_dt);
+      if (G == 4) zdft<4, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+      else if (G == 2) zdft<2, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+      else zdft<1, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+      dft_sync(n_dt);
+      if (dt == 0) mbar_arrive(smem_u32(&inv_done[buf]));
+    };
+    for (int k = 0; k < n_cols; ++k) {
+      const int buf = k & 1, ib = k % kInBufs;
+      // f_z[buf] was last read by the modes of column k-2, whose col_done the
+      // inverse of column k-2 (previous iteration's tail) already waited for
+      mbar_wait(smem_u32(&in_full[ib]), static_cast<unsigned>((k / kInBufs) & 1));
+      c64* f_z = f_z0 + buf * Lz * E;
+      const c64* f_in = f_in0 + ib * Mz * E;
+      const int G = zdft_group(Lz * E, n_dt);
+      if (G == 4) zdft<4, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+      else if (G == 2) zdft<2, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+      else zdft<1, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+      dft_sync(n_dt);
+      if (dt == 0) {
+        mbar_arrive(smem_u32(&fwd_done[buf]));
+        mbar_arrive(smem_u32(&in_empty[ib]));
+      }
+      if (k >= 1) inverse(k - 1);
+    }
+    if (n_cols >= 1) inverse(n_cols - 1);
+  }
+  __syncthreads();  // the producer stays resident until every copy it issued has landed
+}
+
 // zero the embedded field and place each K_o at slot (o mod L) (src/structured.cpp:73-86)
 __global__ void scatter_bank_kernel(const c64* __restrict__ blocks, const int* __restrict__ offsets, int n_blk,
                                     int b2, int lx, int ly, int lz, c64* __restrict__ field) {
@@ -467,13 +628,70 @@ int zfused_ring_for(int Mz, int Lz, int E, int b, int ctas) {
 }
 }  // namespace
 
+namespace {
+size_t zpipe_fields_bytes(int Mz, int Lz, int E) {
+  return sizeof(c64) * (static_cast<size_t>(kInBufs * Mz + 4 * Lz) * E + Lz);
+}
+int zpipe_max_ring(int Mz, int Lz, int E, int b) {
+  const size_t fields = zpipe_fields_bytes(Mz, Lz, E), per_mode = sizeof(c64) * static_cast<size_t>(b) * b;
+  if (fields >= kZfSmemMax) return 0;
+  long long r = static_cast<long long>((kZfSmemMax - fields) / per_mode);
+  return static_cast<int>(r > kPipeMaxRing ? kPipeMaxRing : r);
+}
+// mode warps: FPBEM_ZF_MW (default 7); ring = the largest multiple of it that
+// fits, at least two slots per warp (0: the pipelined kernel does not fit)
+int zpipe_mode_warps(int Mz, int Lz, int E, int b) {
+  static const int want = [] {
+    const char* s = std::getenv("FPBEM_ZF_MW");
+    const int v = s ? std::atoi(s) : 7;  // measured best on cfg3 / cfg5 (profiles/r01_m2l_probes.md)
+    return v < 2 ? 2 : (v > kPipeMaxModeWarps ? kPipeMaxModeWarps : v);
+  }();
+  const int r = zpipe_max_ring(Mz, Lz, E, b);
+  for (int w = want; w >= 2; --w)
+    if (r >= 2 * w) return w;
+  return 0;
+}
+int zpipe_ring(int Mz, int Lz, int E, int b) {
+  const int w = zpipe_mode_warps(Mz, Lz, E, b);
+  return w ? (zpipe_max_ring(Mz, Lz, E, b) / w) * w : 0;
+}
+}  // namespace
+
 int m2l_zfused_ring(int Mz, int Lz, int E, int b) {
+  if (zpipe_mode_warps(Mz, Lz, E, b) > 0) return zpipe_ring(Mz, Lz, E, b);
   const int r = zfused_ring_for(Mz, Lz, E, b, zfused_ctas_per_sm(Mz, Lz, E, b));
   return r > 0 ? r : zfused_ring_for(Mz, Lz, E, b, 1);
 }
 
+
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
                               long long plane, int E, int b, double scale, cudaStream_t stream) {
+  // three-role pipelined kernel unless FPBEM_ZF=2 (or it does not fit)
+  static const bool use_pipe = [] {
+    const char* s = std::getenv("FPBEM_ZF");
+    return !(s && s[0] == '2');
+  }();
+  const int n_mw = use_pipe ? zpipe_mode_warps(Mz, Lz, E, b) : 0;
+  if (n_mw > 0) {
+    const int ring = zpipe_ring(Mz, Lz, E, b);
+    const size_t smem = zpipe_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
+    static size_t configured_pipe = 0;
+    if (smem > 48 * 1024 && smem > configured_pipe) {
+      cudaError_t e = cudaFuncSetAttribute(m2l_zpipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      configured_pipe = smem;
+    }
+    const long long grid = plane < kNumSMs ? plane : kNumSMs;
+    static const int n_dw = [] {  // FPBEM_ZF_DFT_WARPS (4..12, default 8)
+      const char* s = std::getenv("FPBEM_ZF_DFT_WARPS");
+      const int v = s ? std::atoi(s) : 8;
+      return v < 4 ? 4 : (v > kPipeMaxDftWarps ? kPipeMaxDftWarps : v);
+    }();
+    m2l_zpipe_kernel<<<static_cast<unsigned>(grid), 32 * (1 + n_mw + n_dw), smem, stream>>>(
+        in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, n_dw, scale);
+    return cudaGetLastError();
+  }
   int ctas = zfused_ctas_per_sm(Mz, Lz, E, b);
   int ring = zfused_ring_for(Mz, Lz, E, b, ctas);
   if (ring == 0) {
