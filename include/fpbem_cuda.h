@@ -93,6 +93,8 @@ typedef struct {
                                     from the K_hat bank                                    */
   int blocks_on_device;          /* 1: near_blocks / hat_blocks are device pointers on
                                     `device` (e.g. from fpbem_cu_assemble_near)            */
+  int far_on_device;             /* 1: far_blocks / far_hat_blocks are device pointers on
+                                    `device` (e.g. from fpbem_cu_m2l_bank)                 */
 } fpbem_cu_fmm_desc;
 
 /* Unit cell for the device assembly, BIE-oriented (assembly::bie_oriented,
@@ -124,6 +126,19 @@ int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, 
                           const int counts[3], int n_hat, const int* hat_indices, int hs_axis,
                           double hs_offset, fpbem_c64 hs_reflection, int device, fpbem_c64* out,
                           int ptr_kind);
+
+/* M2L translation blocks on the device: TranslationTable::m2l
+ * (src/specfun.cpp:332-351) batched over n_blk translation vectors,
+ *   out[s] = K(delta[s]) + reflection * K(image_delta[s]) P_axis,
+ * each b x b column-major, b = (n_t+1)^2 (n_t <= 15). delta == NULL drops the
+ * first term, image_delta == NULL the second; P_axis is the mirror parity map
+ * of parity_axis (src/fmm.cpp:108-123). delta, image_delta: host n_blk x 3.
+ * The far bank of assemble_periodic_fmm (src/fmm.cpp:180-191) is
+ * delta = shift(o); a folded half space adds image_delta = center(o) -
+ * mirror(base_center); the split-half-space K_hat bank (src/fmm.cpp:204-242)
+ * is image_delta only. Replaces the host loop over far offsets. */
+int fpbem_cu_m2l_bank(int n_t, double k, int n_blk, const double* delta, const double* image_delta,
+                      int parity_axis, fpbem_c64 reflection, int device, fpbem_c64* out, int ptr_kind);
 
 int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* desc, int device, fpbem_cu_op** out);
 void fpbem_cu_fmm_destroy(fpbem_cu_op* op);

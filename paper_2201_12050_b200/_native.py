@@ -54,6 +54,7 @@ class FmmDesc(C.Structure):
         ("far_hat_blocks", C.c_void_p),
         ("lambda_hat", C.c_void_p),
         ("blocks_on_device", C.c_int),
+        ("far_on_device", C.c_int),
     ]
 
 
@@ -84,7 +85,7 @@ CUDA_SYMBOLS = (
     "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
     "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
     "fpbem_cu_fmm_set_partition", "fpbem_cu_partition_pairs", "fpbem_cu_assemble_near", "fpbem_cu_assemble_hat",
-    "fpbem_cu_last_error", "fpbem_cu_version",
+    "fpbem_cu_m2l_bank", "fpbem_cu_last_error", "fpbem_cu_version",
 )
 
 _cuda = None
@@ -124,6 +125,8 @@ def cuda() -> C.CDLL:
                                                  C.c_int, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
             "fpbem_cu_assemble_hat": (C.c_int, [C.POINTER(Cell), C.c_double, C64, c_double_p, c_int_p, C.c_int,
                                                 c_int_p, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
+            "fpbem_cu_m2l_bank": (C.c_int, [C.c_int, C.c_double, C.c_int, c_double_p, c_double_p, C.c_int, C64,
+                                            C.c_int, vp, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -21,7 +21,7 @@ ORACLE = ROOT / "oracle"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["near_field.cu", "m2l.cu", "krylov.cu", "assembly.cu", "fpbem_cuda.cu"]
+CUDA_SOURCES = ["near_field.cu", "m2l.cu", "krylov.cu", "assembly.cu", "far_bank.cu", "fpbem_cuda.cu"]
 HOST_SOURCES = ["geometry.cpp", "kernels.cpp", "specfun.cpp", "assembly.cpp", "capi.cpp"]
 # portable x86-64 ISA level: the GPU box CPU may differ from the build container's
 CPU_FLAGS = ["-O3", "-march=x86-64-v3", "-fPIC", "-fopenmp", "-std=c++17"]
@@ -44,7 +44,8 @@ def _stale(target: Path, sources: list[Path]) -> bool:
 def build_cuda(force: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libfpbem_cuda.so"
-    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "fpbem_cuda.h"]
+    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [
+        ROOT / "include" / "fpbem_cuda.h"]
     if force or _stale(out, deps):
         objs = []
         for s in CUDA_SOURCES:
@@ -61,7 +62,7 @@ def build_cuda(force: bool = False) -> Path:
 def build_host(force: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libfpbem_host.so"
-    deps = [HOST / s for s in HOST_SOURCES] + list(HOST.glob("*.hpp"))
+    deps = [HOST / s for s in HOST_SOURCES] + list(HOST.glob("*.hpp")) + [CSRC / "gaunt.hpp"]
     if force or _stale(out, deps):
         _run(["g++", *CPU_FLAGS, "-shared", "-o", str(out), *[str(HOST / s) for s in HOST_SOURCES]])
     return out

@@ -264,7 +264,7 @@ void twiddles(fpbem_cu_op* op, int L, c64** out) {
 // lattice DFT of the embedded K column on the device (src/structured.cpp:63-108):
 // scatter the n_far bank blocks to slot (o mod L), DFT over every axis
 void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fpbem_c64* far_blocks,
-                    const fpbem_c64* prebuilt, c64** out) {
+                    bool blocks_on_device, const fpbem_c64* prebuilt, c64** out) {
   const int b2 = op->b * op->b;
   const size_t total = static_cast<size_t>(op->q_total) * b2;
   c64* lam = dalloc<c64>(total, "spectrum");
@@ -274,12 +274,17 @@ void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fp
     return;
   }
   c64* tmp = dalloc<c64>(total, "spectrum scratch");
-  c64* blocks = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
-  int* offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
-  if (n_far > 0) {
-    h2d(blocks, far_blocks, static_cast<size_t>(n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
-    h2d(offs, far_offsets, static_cast<size_t>(n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
+  const c64* blocks = reinterpret_cast<const c64*>(far_blocks);  // device bank (fpbem_cu_m2l_bank)
+  c64* staged = nullptr;
+  if (!blocks_on_device) {
+    staged = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
+    if (n_far > 0)
+      h2d(staged, far_blocks, static_cast<size_t>(n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
+    blocks = staged;
   }
+  int* offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
+  if (n_far > 0)
+    h2d(offs, far_offsets, static_cast<size_t>(n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
   check(cudaMemsetAsync(lam, 0, total * sizeof(c64), op->stream), "spectrum clear");
   check(launch_scatter_bank(blocks, offs, n_far, b2, op->L[0], op->L[1], op->L[2], lam, op->stream), "scatter bank");
   c64* cur = lam;
@@ -304,7 +309,7 @@ void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fp
     check(cudaMemcpyAsync(lam, cur, total * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "spectrum copy");
   check(cudaStreamSynchronize(op->stream), "spectrum build");
   cudaFree(tmp);
-  cudaFree(blocks);
+  if (staged) cudaFree(staged);
   cudaFree(offs);
 }
 
@@ -1123,14 +1128,15 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     }
     op->q_total = static_cast<long long>(op->L[0]) * op->L[1] * op->L[2];
     for (int k = 0; k < 3; ++k) twiddles(op, op->L[k], &op->tw[k]);
-    build_spectrum(op, d->n_far, d->far_offsets, d->far_blocks, d->lambda, &op->lambda);
+    build_spectrum(op, d->n_far, d->far_offsets, d->far_blocks, d->far_on_device != 0, d->lambda, &op->lambda);
     if (op->mirrored_level >= 0) {
       // spectrum of K_hat P: Toeplitz offsets o = idx with o[a] = idx[a] - (M_a - 1)
       // (hankel_spectrum, src/structured.cpp:185-198)
       const int a = op->mirrored_level;
       std::vector<int> offs(d->far_hat_indices, d->far_hat_indices + 3 * d->n_far_hat);
       for (int s = 0; s < d->n_far_hat; ++s) offs[3 * s + a] -= m[a] - 1;
-      build_spectrum(op, d->n_far_hat, offs.data(), d->far_hat_blocks, d->lambda_hat, &op->lambda_hat);
+      build_spectrum(op, d->n_far_hat, offs.data(), d->far_hat_blocks, d->far_on_device != 0, d->lambda_hat,
+                     &op->lambda_hat);
     }
 
     // apply buffers
@@ -1556,6 +1562,52 @@ int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, 
       plain.push_back(make_slot(t, sv, cmk(hs_reflection.re, hs_reflection.im), 1, 0));
     }
     run_assembly(cell, k, alpha, hs_axis, hs_offset, plain, images, device, out, ptr_kind);
+  });
+}
+
+int fpbem_cu_m2l_bank(int n_t, double k, int n_blk, const double* delta, const double* image_delta,
+                      int parity_axis, fpbem_c64 reflection, int device, fpbem_c64* out, int ptr_kind) {
+  return guard([&] {
+    if (n_t < 0 || n_t > far_bank_max_nt()) fail(FPBEM_CU_EINVAL, "m2l_bank: n_t out of range");
+    if (n_blk < 0 || (n_blk > 0 && (!out || (!delta && !image_delta))))
+      fail(FPBEM_CU_EINVAL, "m2l_bank: null argument");
+    if (image_delta && (parity_axis < 0 || parity_axis > 2)) fail(FPBEM_CU_EINVAL, "m2l_bank: bad parity axis");
+    if (!std::isfinite(k) || k <= 0.0) fail(FPBEM_CU_EINVAL, "m2l_bank: wavenumber must be positive");
+    for (const double* v : {delta, image_delta}) {
+      if (!v) continue;
+      for (int s = 0; s < n_blk; ++s) {
+        const double r2 = v[3 * s] * v[3 * s] + v[3 * s + 1] * v[3 * s + 1] + v[3 * s + 2] * v[3 * s + 2];
+        if (!(r2 > 0.0) || !std::isfinite(r2))  // solid_singular: evaluation at the singularity
+          fail(FPBEM_CU_EINVAL, "m2l_bank: zero or non-finite translation vector");
+      }
+    }
+    if (n_blk == 0) return;
+    check(cudaSetDevice(device), "set device");
+    cudaStream_t s;
+    check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
+    const size_t b = static_cast<size_t>(n_t + 1) * (n_t + 1), total = static_cast<size_t>(n_blk) * b * b;
+    double* dd = nullptr;
+    double* di = nullptr;
+    if (delta) {
+      dd = dalloc<double>(3 * static_cast<size_t>(n_blk), "bank deltas");
+      h2d(dd, delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank deltas");
+    }
+    std::unique_ptr<double, decltype(&cudaFree)> keep_d(dd, &cudaFree);
+    if (image_delta) {
+      di = dalloc<double>(3 * static_cast<size_t>(n_blk), "bank image deltas");
+      h2d(di, image_delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank image deltas");
+    }
+    std::unique_ptr<double, decltype(&cudaFree)> keep_i(di, &cudaFree);
+    c64* dst = reinterpret_cast<c64*>(out);
+    c64* tmp = nullptr;
+    if (ptr_kind != FPBEM_CU_PTR_DEVICE) dst = tmp = dalloc<c64>(total, "bank output");
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_tmp(tmp, &cudaFree);
+    check(launch_far_bank(device, n_t, k, n_blk, dd, di, parity_axis, cmk(reflection.re, reflection.im), dst, s),
+          "m2l bank");
+    if (ptr_kind != FPBEM_CU_PTR_DEVICE)
+      check(cudaMemcpyAsync(out, dst, total * sizeof(c64), cudaMemcpyDeviceToHost, s), "bank download");
+    check(cudaStreamSynchronize(s), "m2l bank");
   });
 }
 

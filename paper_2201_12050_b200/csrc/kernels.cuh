@@ -100,4 +100,9 @@ cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, l
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
                             double* result, cudaStream_t s);
 
+// device M2L bank (csrc/far_bank.cu): out[s] = [K(delta_s)] + refl K(image_s) P_axis
+int far_bank_max_nt();
+cudaError_t launch_far_bank(int device, int n_t, double k, int n_blk, const double* delta, const double* image,
+                            int parity_axis, c64 refl, c64* out, cudaStream_t stream);
+
 }  // namespace fpbem_cu

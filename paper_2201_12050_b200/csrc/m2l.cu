@@ -683,11 +683,7 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
       configured_pipe = smem;
     }
     const long long grid = plane < kNumSMs ? plane : kNumSMs;
-    static const int n_dw = [] {  // FPBEM_ZF_DFT_WARPS (4..12, default 8)
-      const char* s = std::getenv("FPBEM_ZF_DFT_WARPS");
-      const int v = s ? std::atoi(s) : 8;
-      return v < 4 ? 4 : (v > kPipeMaxDftWarps ? kPipeMaxDftWarps : v);
-    }();
+    const int n_dw = kPipeMaxDftWarps;
     m2l_zpipe_kernel<<<static_cast<unsigned>(grid), 32 * (1 + n_mw + n_dw), smem, stream>>>(
         in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, n_dw, scale);
     return cudaGetLastError();
@@ -699,12 +695,8 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
     ring = zfused_ring_for(Mz, Lz, E, b, 1);
   }
   if (ring == 0) return cudaErrorInvalidValue;
-  // two slots per consumer warp when the ring is deep enough (FPBEM_ZF_SLOTS=1 forces one)
-  static const int slots_per_warp = [] {
-    const char* s = std::getenv("FPBEM_ZF_SLOTS");
-    return (s && s[0] == '1') ? 1 : 2;
-  }();
-  const bool two = slots_per_warp == 2 && ring >= 8;
+  // two slots per consumer warp when the ring is deep enough
+  const bool two = ring >= 8;
   const int n_cons = two ? ring / 2 : ring;
   ring = two ? 2 * n_cons : ring;
   const size_t smem = zfused_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;

@@ -104,7 +104,7 @@ class FmmOperators:
     """
 
     def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1, lambda_hat=None,
-                 near_blocks=None, hat_blocks=None):
+                 near_blocks=None, hat_blocks=None, far_blocks=None, far_hat_blocks=None):
         lib = _native.cuda()
         self.counts = tuple(int(c) for c in data.counts)
         self.n_dof = int(data.n_dof)
@@ -139,7 +139,12 @@ class FmmOperators:
         d.lambda_ = ptr(lambda_, np.complex128) if lambda_ is not None else None
         d.n_far = int(len(data.far_offsets))
         d.far_offsets = ptr(data.far_offsets, np.int32)
-        d.far_blocks = ptr(data.far_blocks, np.complex128)
+        if far_blocks is not None:  # CUDA tensors, e.g. from assemble_far_gpu
+            keep.append(far_blocks)
+            d.far_blocks = far_blocks.data_ptr() if d.n_far else None
+            d.far_on_device = 1
+        else:
+            d.far_blocks = ptr(data.far_blocks, np.complex128)
         level = int(getattr(data, "mirrored_level", -1))
         d.mirrored_level = level
         d.max_rhs = max_rhs
@@ -153,7 +158,11 @@ class FmmOperators:
                 d.hat_blocks = ptr(data.hat_blocks, np.complex128)
             d.n_far_hat = int(len(data.far_hat_indices))
             d.far_hat_indices = ptr(data.far_hat_indices, np.int32)
-            d.far_hat_blocks = ptr(data.far_hat_blocks, np.complex128)
+            if far_blocks is not None:
+                keep.append(far_hat_blocks)
+                d.far_hat_blocks = far_hat_blocks.data_ptr() if far_hat_blocks is not None and d.n_far_hat else None
+            else:
+                d.far_hat_blocks = ptr(data.far_hat_blocks, np.complex128)
             d.lambda_hat = ptr(lambda_hat, np.complex128) if lambda_hat is not None else None
         h = C.c_void_p()
         _raise(lib.fpbem_cu_fmm_create(C.byref(d), device, C.byref(h)))
@@ -350,6 +359,74 @@ def assemble_hat_gpu(scene, data, halfspace, device: int = 0):
                                               out.data_ptr(), PTR_DEVICE)
     _raise(rc)
     return out[: len(idx)]
+
+
+def m2l_bank_gpu(n_t: int, k: float, delta=None, image_delta=None, parity_axis: int = 2, reflection=0.0,
+                 device: int = 0):
+    """K blocks on the GPU (fpbem_cu_m2l_bank): for each row s of the (n, 3)
+    translation vectors, K(delta_s) [+ reflection K(image_delta_s) P_axis].
+    Returns a CUDA complex128 tensor (n, b, b) of column-major b x b blocks
+    (index [s, col, row]), b = (n_t + 1)^2 — TranslationTable::m2l
+    (src/specfun.cpp:332-351) for many offsets at once."""
+    import torch
+
+    dl = None if delta is None else np.ascontiguousarray(delta, np.float64).reshape(-1, 3)
+    im = None if image_delta is None else np.ascontiguousarray(image_delta, np.float64).reshape(-1, 3)
+    n = len(dl) if dl is not None else (len(im) if im is not None else 0)
+    if dl is not None and im is not None and len(im) != n:
+        raise ValueError("m2l_bank_gpu: delta and image_delta lengths differ")
+    b = (n_t + 1) ** 2
+    out = torch.empty((max(n, 1), b, b), dtype=torch.complex128, device=f"cuda:{device}")
+    r = complex(reflection)
+    _raise(_native.cuda().fpbem_cu_m2l_bank(
+        int(n_t), float(k), n, dl.ctypes.data_as(_native.c_double_p) if dl is not None else None,
+        im.ctypes.data_as(_native.c_double_p) if im is not None else None, int(parity_axis),
+        _native.C64(r.real, r.imag), device, out.data_ptr(), PTR_DEVICE))
+    return out[:n]
+
+
+def far_translation_vectors(scene, data, halfspace=None):
+    """Translation vectors of the far K bank of `data`, as assemble_periodic_fmm
+    uses them (src/fmm.cpp:180-191, 204-242): returns (delta, image_delta,
+    hat_image_delta); image terms only for a half space (axis, offset,
+    reflection) — folded when data.mirrored_level < 0, split otherwise."""
+    pitch = np.asarray(scene.pitch, np.float64)
+    _, _, base, _ = scene.classify()
+    offs = np.asarray(data.far_offsets, np.float64).reshape(-1, 3)
+    delta = offs * pitch
+    image = hat = None
+    if halfspace is not None:
+        axis, off, _ = halfspace
+        mirror = base.copy()
+        mirror[axis] = 2.0 * off - base[axis]
+        level = int(getattr(data, "mirrored_level", -1))
+        if level < 0:  # folded: center(o) - mirror(base_center)
+            image = base + delta - mirror
+        else:  # split: target_center - image_center over the far Hankel indices
+            idx = np.asarray(data.far_hat_indices, np.int64).reshape(-1, 3)
+            m = np.asarray(data.counts, np.int64)
+            tgt = idx.copy()
+            tgt[:, axis] = np.minimum(idx[:, axis], m[axis] - 1)
+            src = np.zeros_like(idx)
+            src[:, axis] = idx[:, axis] - tgt[:, axis]
+            sshift = src * pitch
+            sshift[:, axis] = -sshift[:, axis]
+            hat = (base + tgt * pitch) - (mirror + sshift)
+    return delta, image, hat
+
+
+def assemble_far_gpu(scene, data, n_t: int = 4, halfspace=None, device: int = 0):
+    """K bank (and K_hat bank of a split half space) of `data` on the GPU:
+    returns (far_blocks, far_hat_blocks or None) as CUDA tensors for
+    FmmOperators(far_blocks=..., far_hat_blocks=...). `data` may come from
+    Scene.assemble_fmm(..., skip_far_values=True)."""
+    k = float(scene.wavenumber)
+    delta, image, hat = far_translation_vectors(scene, data, halfspace)
+    refl = complex(halfspace[2]) if halfspace is not None else 0.0
+    axis = int(halfspace[0]) if halfspace is not None else 2
+    far = m2l_bank_gpu(n_t, k, delta, image, axis, refl, device)
+    far_hat = m2l_bank_gpu(n_t, k, None, hat, axis, refl, device) if hat is not None else None
+    return far, far_hat
 
 
 def _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device):

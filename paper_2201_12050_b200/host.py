@@ -177,8 +177,11 @@ class Scene:
             raise ValueError(_err())
         return u0, v0
 
-    def assemble_fmm(self, n_t: int = 4, skip_near_values: bool = False) -> "FmmData":
-        h = _native.host().fh_fmm_assemble(self._h, n_t, int(skip_near_values))
+    def assemble_fmm(self, n_t: int = 4, skip_near_values: bool = False, skip_far_values: bool = False) -> "FmmData":
+        """assemble_periodic_fmm on the host. skip_near_values / skip_far_values
+        leave the near (S, S_hat) / far (K bank, K_hat) values empty for
+        device assembly (fmm.assemble_near_gpu / fmm.assemble_far_gpu)."""
+        h = _native.host().fh_fmm_assemble(self._h, n_t, int(bool(skip_near_values)) | (int(bool(skip_far_values)) << 1))
         if not h:
             raise ValueError(_err())
         return FmmData(h)
@@ -191,7 +194,7 @@ class FmmData:
     def __init__(self, handle):
         self._h = C.c_void_p(handle)
         lib = _native.host()
-        info = np.zeros(11, np.int32)
+        info = np.zeros(12, np.int32)
         lib.fh_fmm_info(self._h, _ip(info))
         self.counts = tuple(int(v) for v in info[:3])
         self.n_dof = int(info[3])
@@ -215,7 +218,9 @@ class FmmData:
         self.near_blocks = view(ptrs[1], self.n_near * n * n if self.has_near_values else 0, np.complex128,
                                 (self.n_near, n, n) if self.has_near_values else (0, n, n))
         self.far_offsets = view(ptrs[2], 3 * self.n_far, np.int32, (self.n_far, 3))
-        self.far_blocks = view(ptrs[3], self.n_far * b * b, np.complex128, (self.n_far, b, b))
+        self.has_far_values = bool(info[11])
+        nf = self.n_far if self.has_far_values else 0
+        self.far_blocks = view(ptrs[3], nf * b * b, np.complex128, (nf, b, b))
         self.u0 = view(ptrs[4], n * b, np.complex128, (b, n))  # column-major n x b -> (col, row)
         self.v0 = view(ptrs[5], n * b, np.complex128, (n, b))  # column-major b x n -> (col, row)
         # half-space image pair (block Hankel along mirrored_level; -1 = none)
@@ -227,7 +232,8 @@ class FmmData:
         self.hat_indices = view(iptrs[0], 3 * self.n_hat, np.int32, (self.n_hat, 3))
         self.hat_blocks = view(iptrs[1], nh * n * n, np.complex128, (nh, n, n))
         self.far_hat_indices = view(iptrs[2], 3 * self.n_far_hat, np.int32, (self.n_far_hat, 3))
-        self.far_hat_blocks = view(iptrs[3], self.n_far_hat * b * b, np.complex128, (self.n_far_hat, b, b))
+        nfh = self.n_far_hat if self.has_far_values else 0
+        self.far_hat_blocks = view(iptrs[3], nfh * b * b, np.complex128, (nfh, b, b))
 
     def __del__(self):
         h = getattr(self, "_h", None)

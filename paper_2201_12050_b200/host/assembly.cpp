@@ -135,7 +135,7 @@ Mesh shifted(const Mesh& m, const V3& s) {
 // parallel to every periodic direction folds its image into S and K, one
 // whose axis is periodic yields the block-Hankel image pair (S_hat, K_hat).
 FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_t, bool skip_near_values,
-                     const HalfSpace* hs) {
+                     const HalfSpace* hs, bool skip_far_values) {
   if (n_t < 0 || n_t > 30) throw std::invalid_argument("assemble_fmm: n_t in [0, 30] required");
   for (int d = 0; d < 3; ++d)
     if (lat.counts[d] < 1) throw std::invalid_argument("assemble_fmm: counts must be >= 1");
@@ -176,9 +176,9 @@ FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_
     }
   }
   const Translation& tt = table(n_t);
-  op.far_blocks.resize(static_cast<size_t>(op.n_far()) * pp);
+  op.far_blocks.resize(skip_far_values ? 0 : static_cast<size_t>(op.n_far()) * pp);
 #pragma omp parallel for schedule(static)
-  for (int s = 0; s < op.n_far(); ++s) {
+  for (int s = 0; s < (skip_far_values ? 0 : op.n_far()); ++s) {
     const int* o = &op.far_offsets[3 * s];
     cd* blk = op.far_blocks.data() + s * pp;
     tt.m2l(lat.shift(o[0], o[1], o[2]), w.k, blk);
@@ -219,9 +219,10 @@ FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_
           V3 image_center = base_image;
           for (int d = 0; d < 3; ++d) image_center[d] += d == ax ? -sshift[d] : sshift[d];
           if (admissible(target_center, image_center, op.grid.radius)) {
+            op.far_hat_indices.insert(op.far_hat_indices.end(), {i0, i1, i2});
+            if (skip_far_values) continue;
             tt.m2l(target_center - image_center, w.k, k_img.data());
             matmul(p, k_img.data(), parity.data(), prod.data());
-            op.far_hat_indices.insert(op.far_hat_indices.end(), {i0, i1, i2});
             for (size_t e = 0; e < pp; ++e) op.far_hat_blocks.push_back(hs->reflection * prod[e]);
           } else {
             op.hat_indices.insert(op.hat_indices.end(), {i0, i1, i2});

@@ -182,11 +182,12 @@ int fh_classify(void* hp, int* n_near, int* n_far, int* near, int* far, int cap,
   });
 }
 
-void* fh_fmm_assemble(void* hp, int n_t, int skip_near) {
+// flags: 1 = leave the near / S_hat values empty, 2 = leave the K bank / K_hat values empty
+void* fh_fmm_assemble(void* hp, int n_t, int flags) {
   FmmH* h = nullptr;
   guarded([&] {
     const Scene& s = static_cast<SceneH*>(hp)->s;
-    h = new FmmH{assemble_fmm(s.cell, s.lat, s.wave, n_t, skip_near != 0, &s.half_space)};
+    h = new FmmH{assemble_fmm(s.cell, s.lat, s.wave, n_t, (flags & 1) != 0, &s.half_space, (flags & 2) != 0)};
   });
   return h;
 }
@@ -205,6 +206,7 @@ void fh_fmm_info(void* hp, int* info) {
   info[8] = d.mirrored_level;
   info[9] = d.n_hat();
   info[10] = d.n_far_hat();
+  info[11] = (d.far_blocks.empty() && d.n_far() > 0) || (d.far_hat_blocks.empty() && d.n_far_hat() > 0) ? 0 : 1;
 }
 
 void fh_fmm_image_arrays(void* hp, const int** hat_idx, const double** hat_blk, const int** far_hat_idx,

@@ -220,10 +220,11 @@ struct FmmData {
 void classify_offsets(const Mesh& cell, const Lattice& lat, std::vector<int>& near,
                       std::vector<int>& far);
 
-// assemble_periodic_fmm without a half space (fmm.cpp:125-190). If
-// skip_near_values is set the near blocks are left empty (shape-only runs).
+// assemble_periodic_fmm (fmm.cpp:125-242). skip_near_values leaves the near
+// (and S_hat) blocks empty, skip_far_values the K bank (and K_hat) blocks, for
+// runs that assemble those on the device; offsets and indices are always set.
 FmmData assemble_fmm(const Mesh& cell, const Lattice& lat, const Wave& w, int n_t,
-                     bool skip_near_values = false, const HalfSpace* hs = nullptr);
+                     bool skip_near_values = false, const HalfSpace* hs = nullptr, bool skip_far_values = false);
 
 // action of an axis mirror on moment vectors (fmm.cpp:108-123); b x b column-major
 void mirror_parity_map(int n_t, int axis, cd* out);

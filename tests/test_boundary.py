@@ -52,6 +52,28 @@ def test_version_and_error_calls_need_no_gpu():
     assert b"null" in lib.fpbem_cu_last_error()
 
 
+def test_m2l_bank_validates_before_touching_the_device():
+    """fpbem_cu_m2l_bank rejects what TranslationTable::m2l rejects (evaluation
+    at the singularity, src/specfun.cpp) with EINVAL, GPU or not."""
+    import numpy as np
+
+    from paper_2201_12050_b200 import _native
+
+    lib = _native.cuda()
+    out = np.zeros(25 * 25 * 2, np.complex128)
+    zero = np.zeros(3)
+    one = np.array([0.0, 0.0, 1.0])
+    call = lambda n_t, k, d, im: lib.fpbem_cu_m2l_bank(  # noqa: E731
+        n_t, k, 1, d.ctypes.data_as(_native.c_double_p) if d is not None else None,
+        im.ctypes.data_as(_native.c_double_p) if im is not None else None, 2, _native.C64(1.0, 0.0), 0,
+        out.ctypes.data, 0)
+    assert call(4, 2.0, zero, None) == 6 and b"translation vector" in lib.fpbem_cu_last_error()
+    assert call(4, 2.0, one, zero) == 6
+    assert call(4, 2.0, None, None) == 6
+    assert call(16, 2.0, one, None) == 6 and b"n_t" in lib.fpbem_cu_last_error()
+    assert call(4, 0.0, one, None) == 6
+
+
 def test_host_and_oracle_libraries_load():
     import oracle
     from paper_2201_12050_b200 import _native

@@ -516,6 +516,77 @@ def test_device_assembly_of_half_space_images():
     assert rel(dev, np.asarray(d.hat_blocks)) < 1e-12
 
 
+# ---- M2L bank on the device ---------------------------------
+
+@pytest.mark.parametrize("cid,var", [(1, 0), (2, 2), (3, 2), (4, 2), (5, 2)])
+def test_device_m2l_bank_matches_host_bank(ops, assembled, cid, var):
+    """fpbem_cu_m2l_bank = TranslationTable::m2l over the far offsets (host
+    restatement, pinned by tests/test_host.py), and the operator built from the
+    device bank reproduces the oracle product."""
+    from paper_2201_12050_b200.fmm import assemble_far_gpu
+
+    sc, d = assembled(cid, var)
+    far, far_hat = assemble_far_gpu(sc, d)
+    assert far_hat is None and far.shape == (d.n_far, d.n_coef, d.n_coef)
+    if d.n_far:  # the shrunk variants can have every offset near
+        assert rel(far.cpu().numpy(), np.asarray(d.far_blocks)) < 1e-13
+    p = uvec(np.random.default_rng(cid + 40), d.N)
+    assert rel(ops(d, far_blocks=far).matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+def test_device_m2l_bank_without_host_bank_values(ops):
+    """skip_near_values + skip_far_values: the host only classifies; S and the
+    K bank come from the device; the product equals the fully host-assembled one."""
+    from paper_2201_12050_b200 import Scene
+    from paper_2201_12050_b200.fmm import assemble_far_gpu, assemble_near_gpu
+
+    sc = Scene(5, 2)
+    full = sc.assemble_fmm(4)
+    shape = sc.assemble_fmm(4, skip_near_values=True, skip_far_values=True)
+    assert not shape.has_far_values and shape.far_blocks.shape[0] == 0
+    far, _ = assemble_far_gpu(sc, shape)
+    near = assemble_near_gpu(sc, shape)
+    p = uvec(np.random.default_rng(3), full.N)
+    assert rel(ops(shape, near_blocks=near, far_blocks=far).matvec(p), O.OracleFmm(full).matvec(p)) <= MATVEC_TOL
+
+
+def test_device_m2l_bank_half_space_images(ops):
+    """folded image term K(center - mirror(base)) P (src/fmm.cpp:186-190) and the
+    split-half-space K_hat bank (src/fmm.cpp:204-242) on the device."""
+    from paper_2201_12050_b200.fmm import assemble_far_gpu
+
+    hs = (2, 0.0, 0.9 + 0.2j)
+    sc, d = _halfspace_scene((4, 4, 1), (0.35, 0.35, 0.0), 0.6, hs[2])
+    far, far_hat = assemble_far_gpu(sc, d, halfspace=hs)
+    assert d.mirrored_level == -1 and far_hat is None and d.n_far > 0
+    assert rel(far.cpu().numpy(), np.asarray(d.far_blocks)) < 1e-13
+    p = uvec(np.random.default_rng(13), d.N)
+    assert rel(ops(d, far_blocks=far).matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+    hs = (2, 0.0, 0.8 - 0.3j)
+    sc, d = _halfspace_scene((3, 2, 4), (0.35, 0.35, 0.35), 0.25, hs[2])
+    far, far_hat = assemble_far_gpu(sc, d, halfspace=hs)
+    assert d.mirrored_level == 2 and d.n_far_hat > 0
+    assert rel(far.cpu().numpy(), np.asarray(d.far_blocks)) < 1e-13
+    assert rel(far_hat.cpu().numpy(), np.asarray(d.far_hat_blocks)) < 1e-13
+    p = uvec(np.random.default_rng(12), d.N)
+    op = ops(d, far_blocks=far, far_hat_blocks=far_hat)
+    assert rel(op.matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+def test_device_m2l_bank_other_orders():
+    """n_t = 1..8 against the host TranslationTable (host.m2l_block)."""
+    from paper_2201_12050_b200.fmm import m2l_bank_gpu
+    from paper_2201_12050_b200.host import m2l_block
+
+    rng = np.random.default_rng(21)
+    deltas = rng.uniform(-3, 3, (7, 3)) + np.array([0.0, 0.0, 4.0])
+    for n_t in (1, 2, 5, 8):
+        dev = m2l_bank_gpu(n_t, 3.1, deltas).cpu().numpy()
+        for s, dl in enumerate(deltas):
+            host = m2l_block(n_t, dl, 3.1)
+            assert rel(dev[s].T, host) < 1e-13
+
+
 # ---- lockstep batched GMRES (cfg5's 64 right-hand sides) -------------------------
 
 def test_batched_gmres_matches_per_rhs_oracle_with_restarts(ops, assembled):
