@@ -127,6 +127,20 @@ int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, 
                           double hs_offset, fpbem_c64 hs_reflection, int device, fpbem_c64* out,
                           int ptr_kind);
 
+/* Pressure at observation points by the representation formula
+ * (postproc::evaluate_field, src/postproc.cpp:39-62): for each point x,
+ *   out = p_incident + sum_j int_{e_j} [-dG/dn_y p_j + G i k beta_j p_j]
+ *         (+ hs_reflection x the same over the mirrored mesh when hs_reflection != 0),
+ * over the replicated mesh (cell-major, x fastest) of the BIE-oriented unit
+ * cell, with the influence quadrature of src/kernels.cpp:205-212 (order 6,
+ * adaptive subdivision near x). solution: N = n x cells pressures;
+ * p_incident: n_points values or NULL (0); points: host n_points x 3.
+ * ptr_kind applies to solution, p_incident and out. */
+int fpbem_cu_evaluate_field(const fpbem_cu_cell* cell, double k, const double pitch[3], const int counts[3],
+                            const fpbem_c64* solution, int n_points, const double* points,
+                            const fpbem_c64* p_incident, int hs_axis, double hs_offset, fpbem_c64 hs_reflection,
+                            int device, fpbem_c64* out, int ptr_kind);
+
 /* M2L translation blocks on the device: TranslationTable::m2l
  * (src/specfun.cpp:332-351) batched over n_blk translation vectors,
  *   out[s] = K(delta[s]) + reflection * K(image_delta[s]) P_axis,

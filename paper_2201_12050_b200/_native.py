@@ -85,7 +85,7 @@ CUDA_SYMBOLS = (
     "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
     "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
     "fpbem_cu_fmm_set_partition", "fpbem_cu_partition_pairs", "fpbem_cu_assemble_near", "fpbem_cu_assemble_hat",
-    "fpbem_cu_m2l_bank", "fpbem_cu_last_error", "fpbem_cu_version",
+    "fpbem_cu_m2l_bank", "fpbem_cu_evaluate_field", "fpbem_cu_last_error", "fpbem_cu_version",
 )
 
 _cuda = None
@@ -125,6 +125,8 @@ def cuda() -> C.CDLL:
                                                  C.c_int, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
             "fpbem_cu_assemble_hat": (C.c_int, [C.POINTER(Cell), C.c_double, C64, c_double_p, c_int_p, C.c_int,
                                                 c_int_p, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
+            "fpbem_cu_evaluate_field": (C.c_int, [C.POINTER(Cell), C.c_double, c_double_p, c_int_p, vp, C.c_int,
+                                                  c_double_p, vp, C.c_int, C.c_double, C64, C.c_int, vp, C.c_int]),
             "fpbem_cu_m2l_bank": (C.c_int, [C.c_int, C.c_double, C.c_int, c_double_p, c_double_p, C.c_int, C64,
                                             C.c_int, vp, C.c_int]),
         }
@@ -154,6 +156,9 @@ def host() -> C.CDLL:
             "fh_scene_sweep": (None, [vp, c_double_p]),
             "fh_scene_set_sources": (None, [vp, C.c_int, c_int_p, c_double_p]),
             "fh_scene_rhs": (C.c_int, [vp, C.c_int, vp]),
+            "fh_scene_incident": (C.c_int, [vp, C.c_int, C.c_int, c_double_p, vp]),
+            "fh_scene_field": (C.c_int, [vp, C.c_int, vp, C.c_int, c_double_p, vp]),
+            "fh_insertion_loss": (C.c_int, [C.c_int, vp, vp, vp]),
             "fh_scene_dense": (C.c_int, [vp, vp]),
             "fh_scene_cell": (C.c_int, [vp, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p, c_int_p]),
             "fh_interaction_block": (C.c_int, [vp, c_double_p, C.c_int, vp]),

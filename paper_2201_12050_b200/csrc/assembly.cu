@@ -26,13 +26,15 @@ constexpr int kRegular = 6;
 constexpr int kSelf = 8;
 constexpr double kNear = 3.0;
 constexpr int kMaxDepth = 6;
+constexpr int kFieldThreads = 128;
+constexpr int kFieldPerThread = 8;
 
 __constant__ double c_gx6[kRegular], c_gw6[kRegular], c_gx8[kSelf], c_gw8[kSelf];
 
 struct P3 {
   double x, y, z;
 };
-__device__ __forceinline__ P3 p3(double x, double y, double z) { return {x, y, z}; }
+__host__ __device__ __forceinline__ P3 p3(double x, double y, double z) { return {x, y, z}; }
 __device__ __forceinline__ P3 operator+(P3 a, P3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
 __device__ __forceinline__ P3 operator-(P3 a, P3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
 __device__ __forceinline__ P3 operator*(double s, P3 a) { return {s * a.x, s * a.y, s * a.z}; }
@@ -54,6 +56,9 @@ struct Elem {
 };
 
 // sum over the 6x6 tensor rule of one bilinear patch of the BM integrands
+// (kBM = false: the plain layer potentials, h = int dG/dn_y, g = int G, as the
+// representation formula of src/postproc.cpp:18-35 needs them)
+template <bool kBM = true>
 __device__ void tensor_accum(const Quad& q, P3 x, P3 nx, P3 ny, double k, c64 alpha, c64& h, c64& g) {
   const double nxny = dot3(nx, ny);
   for (int i = 0; i < kRegular; ++i) {
@@ -76,6 +81,11 @@ __device__ void tensor_accum(const Quad& q, P3 x, P3 nx, P3 ny, double k, c64 al
       const c64 qd = cmk(-inv, k);                                             // dG/dr = q G
       const c64 qg = cmul(qd, gg);
       const c64 dgdny = cscale(qg, -cy);
+      if (!kBM) {
+        h = cadd(h, cscale(dgdny, w));
+        g = cadd(g, cscale(gg, w));
+        continue;
+      }
       const c64 dgdnx = cscale(qg, cx);
       // d2G = G (k^2 + 3ik/r - 3/r^2) cx cy - G q / r nx.ny
       const c64 f1 = cmk(k * k - 3.0 * inv * inv, 3.0 * k * inv);
@@ -88,10 +98,11 @@ __device__ void tensor_accum(const Quad& q, P3 x, P3 nx, P3 ny, double k, c64 al
 
 // influence of one element seen from x: tensor rule, or adaptive quartering
 // (depth-first, the host's recursion order) when x is near (kernels.cpp:98-128, 214-226)
+template <bool kBM = true>
 __device__ void influence(const Elem& e, P3 x, P3 nx, double k, c64 alpha, c64& h, c64& g) {
   h = g = cmk(0.0, 0.0);
   if (len3(x - e.cen) >= kNear * e.diam) {
-    tensor_accum(e.q, x, nx, e.nrm, k, alpha, h, g);
+    tensor_accum<kBM>(e.q, x, nx, e.nrm, k, alpha, h, g);
     return;
   }
   Quad stack[3 * kMaxDepth + 1];
@@ -106,7 +117,7 @@ __device__ void influence(const Elem& e, P3 x, P3 nx, double k, c64 alpha, c64& 
     const P3 mid = 0.25 * (q.c[0] + q.c[1] + q.c[2] + q.c[3]);
     const double diam = fmax(len3(q.c[2] - q.c[0]), len3(q.c[3] - q.c[1]));
     if (dep <= 0 || len3(x - mid) >= kNear * diam) {
-      tensor_accum(q, x, nx, e.nrm, k, alpha, h, g);
+      tensor_accum<kBM>(q, x, nx, e.nrm, k, alpha, h, g);
       continue;
     }
     const P3 m01 = 0.5 * (q.c[0] + q.c[1]), m12 = 0.5 * (q.c[1] + q.c[2]), m23 = 0.5 * (q.c[2] + q.c[3]),
@@ -262,7 +273,116 @@ assemble_kernel(const double* __restrict__ corners, const int* __restrict__ nv, 
   *dst = accumulate ? cadd(*dst, val) : val;
 }
 
+// element j of the replicated mesh (cell-major, x fastest; src/geometry.cpp
+// replicate): the unit-cell element j % n shifted by the lattice vector of cell
+// j / n, optionally mirrored (mirror_mesh: mirrored corners, reversed loop,
+// mirrored normal)
+__device__ Elem full_element(const double* __restrict__ corners, const int* __restrict__ nv,
+                             const double* __restrict__ cen, const double* __restrict__ nrm,
+                             const double* __restrict__ diam, const c64* __restrict__ beta, int n, int cx, int cy,
+                             P3 pitch, long long j, bool mirror, int hs_axis, double hs_offset) {
+  const long long cell = j / n;
+  const int e = static_cast<int>(j - cell * n);
+  const int ix = static_cast<int>(cell % cx), iy = static_cast<int>((cell / cx) % cy),
+            iz = static_cast<int>(cell / (static_cast<long long>(cx) * cy));
+  const P3 sh = p3(ix * pitch.x, iy * pitch.y, iz * pitch.z);
+  Elem el;
+  P3 c[4];
+  for (int a = 0; a < 4; ++a) c[a] = load_p3(corners, 4LL * e + a) + sh;
+  el.cen = load_p3(cen, e) + sh;
+  el.nrm = load_p3(nrm, e);
+  el.diam = diam[e];
+  el.beta = beta ? beta[e] : cmk(0.0, 0.0);
+  if (mirror) {
+    for (int a = 0; a < 4; ++a) c[a] = mirror_p(c[a], hs_axis, hs_offset);
+    el.cen = mirror_p(el.cen, hs_axis, hs_offset);
+    if (hs_axis == 0) el.nrm.x = -el.nrm.x;
+    if (hs_axis == 1) el.nrm.y = -el.nrm.y;
+    if (hs_axis == 2) el.nrm.z = -el.nrm.z;
+    el.q = nv[e] == 3 ? Quad{{c[0], c[2], c[1], c[1]}} : Quad{{c[0], c[3], c[2], c[1]}};
+  } else {
+    el.q = Quad{{c[0], c[1], c[2], c[3]}};
+  }
+  return el;
+}
+
+// representation-formula contribution of one element (postproc.cpp:18-35):
+// int [-dG/dn_y p + G i k beta p]
+__device__ __forceinline__ c64 field_contribution(const Elem& e, P3 x, double k, c64 pressure) {
+  c64 h, g;
+  influence<false>(e, x, p3(0.0, 0.0, 1.0), k, cmk(0.0, 0.0), h, g);
+  const c64 ikb_p = cmul(cmul(cmk(0.0, k), e.beta), pressure);
+  return cadd(cmul(csub(cmk(0.0, 0.0), h), pressure), cmul(g, ikb_p));
+}
+
+// partial[chunk][pt] = sum over the chunk's elements of the contributions at
+// point pt (+ reflection x the mirrored elements'); fixed order: each thread
+// sums its strided elements, then a fixed tree over the CTA
+__global__ void __launch_bounds__(kFieldThreads)
+field_kernel(const double* __restrict__ corners, const int* __restrict__ nv, const double* __restrict__ cen,
+             const double* __restrict__ nrm, const double* __restrict__ diam, const c64* __restrict__ beta, int n,
+             int cx, int cy, P3 pitch, long long n_total, const c64* __restrict__ sol, const double* __restrict__ pts,
+             int n_pts, double k, int with_image, int hs_axis, double hs_offset, c64 refl,
+             c64* __restrict__ partial) {
+  __shared__ c64 red[kFieldThreads];
+  const int pt = blockIdx.y;
+  const P3 x = load_p3(pts, pt);
+  const long long j0 = static_cast<long long>(blockIdx.x) * kFieldThreads * kFieldPerThread;
+  c64 acc = cmk(0.0, 0.0);
+  for (int u = 0; u < kFieldPerThread; ++u) {
+    const long long j = j0 + static_cast<long long>(u) * kFieldThreads + threadIdx.x;
+    if (j >= n_total) break;
+    const c64 pj = sol[j];
+    acc = cadd(acc, field_contribution(full_element(corners, nv, cen, nrm, diam, beta, n, cx, cy, pitch, j, false,
+                                                    hs_axis, hs_offset), x, k, pj));
+    if (with_image)
+      acc = cadd(acc, cmul(refl, field_contribution(full_element(corners, nv, cen, nrm, diam, beta, n, cx, cy, pitch,
+                                                                 j, true, hs_axis, hs_offset), x, k, pj)));
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kFieldThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = cadd(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[static_cast<long long>(blockIdx.x) * n_pts + pt] = red[0];
+}
+
+// out[pt] = p_inc[pt] + sum over chunks, in chunk order
+__global__ void field_sum_kernel(const c64* __restrict__ partial, int n_chunks, int n_pts,
+                                 const c64* __restrict__ p_inc, c64* __restrict__ out) {
+  const int pt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pt >= n_pts) return;
+  c64 acc = p_inc ? p_inc[pt] : cmk(0.0, 0.0);
+  for (int c = 0; c < n_chunks; ++c) acc = cadd(acc, partial[static_cast<long long>(c) * n_pts + pt]);
+  out[pt] = acc;
+}
+
 }  // namespace
+
+int field_chunks(long long n_total) {
+  return static_cast<int>((n_total + kFieldThreads * kFieldPerThread - 1) / (kFieldThreads * kFieldPerThread));
+}
+
+cudaError_t launch_field(const double* corners, const int* nv, const double* cen, const double* nrm,
+                         const double* diam, const c64* beta, int n, const int counts[3], const double pitch[3],
+                         const c64* solution, const double* pts, int n_pts, const c64* p_inc, double k,
+                         bool with_image, int hs_axis, double hs_offset, c64 refl, c64* partial, c64* out,
+                         cudaStream_t stream) {
+  if (n_pts == 0) return cudaSuccess;
+  const long long n_total = static_cast<long long>(n) * counts[0] * counts[1] * counts[2];
+  const int chunks = field_chunks(n_total);
+  for (int p0 = 0; p0 < n_pts; p0 += 65535) {  // grid.y limit
+    const int np = n_pts - p0 < 65535 ? n_pts - p0 : 65535;
+    field_kernel<<<dim3(chunks, np), kFieldThreads, 0, stream>>>(
+        corners, nv, cen, nrm, diam, beta, n, counts[0], counts[1], p3(pitch[0], pitch[1], pitch[2]), n_total,
+        solution, pts + 3LL * p0, n_pts, k, with_image ? 1 : 0, hs_axis, hs_offset, refl, partial + p0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  field_sum_kernel<<<(n_pts + 127) / 128, 128, 0, stream>>>(partial, chunks, n_pts, p_inc, out);
+  return cudaGetLastError();
+}
 
 cudaError_t assembly_set_rules(const double* x6, const double* w6, const double* x8, const double* w8) {
   cudaError_t e = cudaMemcpyToSymbol(c_gx6, x6, sizeof(double) * kRegular);

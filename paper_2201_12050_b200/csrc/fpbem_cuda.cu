@@ -1565,6 +1565,61 @@ int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, 
   });
 }
 
+int fpbem_cu_evaluate_field(const fpbem_cu_cell* cell, double k, const double pitch[3], const int counts[3],
+                            const fpbem_c64* solution, int n_points, const double* points,
+                            const fpbem_c64* p_incident, int hs_axis, double hs_offset, fpbem_c64 hs_reflection,
+                            int device, fpbem_c64* out, int ptr_kind) {
+  return guard([&] {
+    if (!cell || !pitch || !counts || (n_points > 0 && (!points || !out || !solution)))
+      fail(FPBEM_CU_EINVAL, "evaluate_field: null argument");
+    if (n_points < 0 || counts[0] < 1 || counts[1] < 1 || counts[2] < 1)
+      fail(FPBEM_CU_EDIM, "evaluate_field: bad counts or point count");
+    const bool with_image = hs_reflection.re != 0.0 || hs_reflection.im != 0.0;
+    if (with_image && (hs_axis < 0 || hs_axis > 2)) fail(FPBEM_CU_EINVAL, "evaluate_field: bad half-space axis");
+    if (n_points == 0) return;
+    check(cudaSetDevice(device), "set device");
+    cudaStream_t s;
+    check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
+    CellDev dc;
+    upload_cell(cell, dc, s);
+    const long long n_total = static_cast<long long>(cell->n) * counts[0] * counts[1] * counts[2];
+    const bool dev = ptr_kind == FPBEM_CU_PTR_DEVICE;
+    double* dp = dalloc<double>(3 * static_cast<size_t>(n_points), "field points");
+    std::unique_ptr<double, decltype(&cudaFree)> keep_p(dp, &cudaFree);
+    h2d(dp, points, 3 * static_cast<size_t>(n_points) * sizeof(double), s, "field points");
+    const c64* sol = reinterpret_cast<const c64*>(solution);
+    c64* sol_tmp = nullptr;
+    if (!dev) {
+      sol_tmp = dalloc<c64>(static_cast<size_t>(n_total), "field solution");
+      h2d(sol_tmp, solution, static_cast<size_t>(n_total) * sizeof(c64), s, "field solution");
+      sol = sol_tmp;
+    }
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_sol(sol_tmp, &cudaFree);
+    const c64* pinc = reinterpret_cast<const c64*>(p_incident);
+    c64* pinc_tmp = nullptr;
+    if (!dev && p_incident) {
+      pinc_tmp = dalloc<c64>(static_cast<size_t>(n_points), "incident values");
+      h2d(pinc_tmp, p_incident, static_cast<size_t>(n_points) * sizeof(c64), s, "incident values");
+      pinc = pinc_tmp;
+    }
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_pinc(pinc_tmp, &cudaFree);
+    c64* partial = dalloc<c64>(static_cast<size_t>(field_chunks(n_total)) * n_points, "field partial sums");
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_part(partial, &cudaFree);
+    c64* dst = reinterpret_cast<c64*>(out);
+    c64* out_tmp = nullptr;
+    if (!dev) dst = out_tmp = dalloc<c64>(static_cast<size_t>(n_points), "field output");
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_out(out_tmp, &cudaFree);
+    check(launch_field(dc.corners, dc.nv, dc.cen, dc.nrm, dc.diam, dc.beta, cell->n, counts, pitch, sol, dp, n_points,
+                       pinc, k, with_image, hs_axis, hs_offset, cmk(hs_reflection.re, hs_reflection.im), partial, dst,
+                       s),
+          "field evaluation");
+    if (!dev) check(cudaMemcpyAsync(out, dst, static_cast<size_t>(n_points) * sizeof(c64), cudaMemcpyDeviceToHost, s),
+                    "field download");
+    check(cudaStreamSynchronize(s), "field evaluation");
+  });
+}
+
 int fpbem_cu_m2l_bank(int n_t, double k, int n_blk, const double* delta, const double* image_delta,
                       int parity_axis, fpbem_c64 reflection, int device, fpbem_c64* out, int ptr_kind) {
   return guard([&] {

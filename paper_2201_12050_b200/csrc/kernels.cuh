@@ -100,6 +100,16 @@ cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, l
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
                             double* result, cudaStream_t s);
 
+// field evaluation (csrc/assembly.cu): out[p] = p_inc[p] + sum over the replicated
+// mesh (+ reflection x its mirror) of the representation-formula contributions;
+// partial: field_chunks(n * cells) x n_pts scratch
+int field_chunks(long long n_total);
+cudaError_t launch_field(const double* corners, const int* nv, const double* cen, const double* nrm,
+                         const double* diam, const c64* beta, int n, const int counts[3], const double pitch[3],
+                         const c64* solution, const double* pts, int n_pts, const c64* p_inc, double k,
+                         bool with_image, int hs_axis, double hs_offset, c64 refl, c64* partial, c64* out,
+                         cudaStream_t stream);
+
 // device M2L bank (csrc/far_bank.cu): out[s] = [K(delta_s)] + refl K(image_s) P_axis
 int far_bank_max_nt();
 cudaError_t launch_far_bank(int device, int n_t, double k, int n_blk, const double* delta, const double* image,

@@ -429,6 +429,42 @@ def assemble_far_gpu(scene, data, n_t: int = 4, halfspace=None, device: int = 0)
     return far, far_hat
 
 
+def evaluate_field_gpu(scene, solution, points, field: int = 0, p_incident=None, device: int = 0):
+    """Pressure at observation points (postproc::evaluate_field,
+    src/postproc.cpp:39-62) on the GPU: p_inc (host incident field of `field`,
+    with the scene's half-space images, unless given) + the representation
+    formula over the replicated mesh and, with a half space, its mirror image.
+    solution: numpy array (host) or CUDA tensor; returns the same kind."""
+    import torch
+
+    keep = []
+    cs, n = _cell_struct(scene, keep)
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    pitch = np.ascontiguousarray(scene.pitch, np.float64)
+    counts = np.ascontiguousarray(scene.counts, np.int32)
+    hs = getattr(scene, "halfspace", None)
+    axis, off, refl = hs if hs is not None else (2, 0.0, 0j)
+    if p_incident is None:
+        p_incident = scene.incident(pts, field)
+    lib = _native.cuda()
+    if _is_torch(solution):
+        sol = solution.to(torch.complex128).contiguous()
+        pinc = (p_incident if _is_torch(p_incident) else torch.from_numpy(np.asarray(p_incident, np.complex128))).to(
+            sol.device).contiguous()
+        out = torch.empty(len(pts), dtype=torch.complex128, device=sol.device)
+        args = (sol.data_ptr(), pinc.data_ptr(), out.data_ptr(), PTR_DEVICE, sol.device.index)
+    else:
+        sol = np.ascontiguousarray(solution, np.complex128)
+        pinc = np.ascontiguousarray(p_incident, np.complex128)
+        out = np.zeros(len(pts), np.complex128)
+        args = (sol.ctypes.data, pinc.ctypes.data, out.ctypes.data, PTR_HOST, device)
+    _raise(lib.fpbem_cu_evaluate_field(C.byref(cs), float(scene.wavenumber), pitch.ctypes.data_as(_native.c_double_p),
+                                       counts.ctypes.data_as(_native.c_int_p), args[0], len(pts),
+                                       pts.ctypes.data_as(_native.c_double_p), args[1], int(axis), float(off),
+                                       _native.C64(complex(refl).real, complex(refl).imag), args[4], args[2], args[3]))
+    return out
+
+
 def _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device):
     import torch
 

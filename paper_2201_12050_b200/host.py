@@ -43,6 +43,7 @@ class Scene:
         self._h = C.c_void_p(h)
         self.config_id = config_id
         self.variant = variant
+        self.halfspace = None  # (axis, offset, reflection) once set_halfspace activates one
 
     @classmethod
     def custom(cls, kind: str, params, counts, pitch, k: float) -> "Scene":
@@ -105,6 +106,28 @@ class Scene:
         (geometry.hpp:66-78); reflection 0 switches it off."""
         r = complex(reflection)
         _native.host().fh_scene_set_halfspace(self._h, int(axis), float(offset), r.real, r.imag)
+        self.halfspace = (int(axis), float(offset), r) if r != 0 else None
+
+    def incident(self, points, field: int = 0) -> np.ndarray:
+        """incident_values(field, x, .).first at each point, with the half-space
+        image sources (src/kernels.cpp:305-325)."""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        out = np.zeros(len(pts), np.complex128)
+        if _native.host().fh_scene_incident(self._h, field, len(pts), _dp(pts), out.ctypes.data):
+            raise ValueError(_err())
+        return out
+
+    def field_host(self, solution, points, field: int = 0) -> np.ndarray:
+        """postproc::evaluate_field on the host (src/postproc.cpp:39-62), all
+        host threads: the checker for fmm.evaluate_field_gpu."""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        sol = np.ascontiguousarray(solution, np.complex128)
+        if sol.size != self.N:
+            raise ValueError("evaluate_field: solution length mismatch")
+        out = np.zeros(len(pts), np.complex128)
+        if _native.host().fh_scene_field(self._h, field, sol.ctypes.data, len(pts), _dp(pts), out.ctypes.data):
+            raise ValueError(_err())
+        return out
 
     def shift_cell(self, shift) -> None:
         s = np.asarray(shift, np.float64)
@@ -248,6 +271,29 @@ class FmmData:
     @property
     def N(self) -> int:
         return self.n_cells * self.n_dof
+
+
+def insertion_loss(p_inc, p) -> float:
+    """postproc::insertion_loss (src/postproc.cpp:64-72): 20 log10(sum|p_inc| / sum|p|)."""
+    a = np.ascontiguousarray(p_inc, np.complex128)
+    b = np.ascontiguousarray(p, np.complex128)
+    il = C.c_double()
+    if a.size != b.size or _native.host().fh_insertion_loss(a.size, a.ctypes.data, b.ctypes.data, C.byref(il)):
+        raise ValueError(_err() if a.size == b.size else "insertion_loss: paired non-empty vectors required")
+    return float(il.value)
+
+
+def grid_points(lo, hi, counts) -> np.ndarray:
+    """postproc::grid_points (src/postproc.cpp:118-133): z slowest, x fastest;
+    a single-point axis sits at the midpoint."""
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    if any(c < 1 for c in counts):
+        raise ValueError("grid_points: counts must be >= 1")
+    axes = [np.array([0.5 * (lo[d] + hi[d])]) if counts[d] == 1 else
+            lo[d] + (hi[d] - lo[d]) * np.arange(counts[d]) / (counts[d] - 1.0) for d in range(3)]
+    z, y, x = np.meshgrid(axes[2], axes[1], axes[0], indexing="ij")
+    return np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1)
 
 
 def m2l_block(n_t: int, delta, k: float) -> np.ndarray:

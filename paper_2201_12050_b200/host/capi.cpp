@@ -127,6 +127,42 @@ int fh_scene_rhs(void* hp, int field, double* out) {
   });
 }
 
+// incident pressure of field `field` at n points (incident_values(...).first, kernels.cpp:305-325)
+int fh_scene_incident(void* hp, int field, int n, const double* pts, double* out) {
+  return guarded([&] {
+    const Scene& s = static_cast<SceneH*>(hp)->s;
+    const std::vector<Source>& src = s.rhs_fields.at(field);
+    for (int i = 0; i < n; ++i) {
+      cd p, dpdn;
+      incident(src, s.wave.k, V3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]}, V3{0.0, 0.0, 1.0}, p, dpdn,
+               &s.half_space);
+      out[2 * i] = p.real();
+      out[2 * i + 1] = p.imag();
+    }
+  });
+}
+
+// evaluate_field on the host (postproc.cpp:39-62): the checker for fpbem_cu_evaluate_field
+int fh_scene_field(void* hp, int field, const double* solution, int n, const double* pts, double* out) {
+  return guarded([&] {
+    const Scene& s = static_cast<SceneH*>(hp)->s;
+    const Mesh full = replicate(s.cell, s.lat);
+    std::vector<cd> sol(reinterpret_cast<const cd*>(solution), reinterpret_cast<const cd*>(solution) + full.size());
+    std::vector<V3> points(n);
+    for (int i = 0; i < n; ++i) points[i] = V3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    const std::vector<cd> r = evaluate_field(full, sol, s.wave, s.rhs_fields.at(field), points, &s.half_space);
+    std::memcpy(out, r.data(), r.size() * sizeof(cd));
+  });
+}
+
+int fh_insertion_loss(int n, const double* p_inc, const double* p, double* il) {
+  return guarded([&] {
+    std::vector<cd> a(reinterpret_cast<const cd*>(p_inc), reinterpret_cast<const cd*>(p_inc) + n);
+    std::vector<cd> b(reinterpret_cast<const cd*>(p), reinterpret_cast<const cd*>(p) + n);
+    *il = insertion_loss(a, b);
+  });
+}
+
 int fh_scene_dense(void* hp, double* out) {
   return guarded([&] {
     const Scene& s = static_cast<SceneH*>(hp)->s;

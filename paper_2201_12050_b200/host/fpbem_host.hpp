@@ -149,6 +149,13 @@ void incident(const std::vector<Source>& src, double k, const V3& x, const V3& n
 std::vector<cd> assemble_rhs(const Mesh& full, const Wave& w, const std::vector<Source>& src,
                              const HalfSpace* hs = nullptr);
 
+// representation formula at observation points and the insertion loss
+// (postproc.cpp:18-81); `full` is the replicated mesh in its stored orientation
+std::vector<cd> evaluate_field(const Mesh& full, const std::vector<cd>& solution, const Wave& w,
+                               const std::vector<Source>& src, const std::vector<V3>& points,
+                               const HalfSpace* hs = nullptr);
+double insertion_loss(const std::vector<cd>& p_inc, const std::vector<cd>& p);
+
 // special functions (specfun.hpp)
 inline constexpr int flat(int n, int m) { return n * n + n + m; }
 inline constexpr int coef_count(int n_t) { return (n_t + 1) * (n_t + 1); }

@@ -74,6 +74,19 @@ def test_m2l_bank_validates_before_touching_the_device():
     assert call(4, 0.0, one, None) == 6
 
 
+def test_evaluate_field_validates_before_touching_the_device():
+    from paper_2201_12050_b200 import _native
+
+    lib = _native.cuda()
+    pitch = (C.c_double * 3)(1, 1, 1)
+    bad = (C.c_int * 3)(0, 1, 1)
+    assert lib.fpbem_cu_evaluate_field(None, 1.0, pitch, bad, None, 0, None, None, 2, 0.0,
+                                       _native.C64(0, 0), 0, None, 0) == 6  # null cell
+    cell = _native.Cell()
+    assert lib.fpbem_cu_evaluate_field(C.byref(cell), 1.0, pitch, bad, None, 0, None, None, 2, 0.0,
+                                       _native.C64(0, 0), 0, None, 0) == 1  # EDIM: counts < 1
+
+
 def test_host_and_oracle_libraries_load():
     import oracle
     from paper_2201_12050_b200 import _native

@@ -587,6 +587,68 @@ def test_device_m2l_bank_other_orders():
             assert rel(dev[s].T, host) < 1e-13
 
 
+# ---- field evaluation on the device --------------------------
+
+def _field_points(sc, n_far=12):
+    """a grid in front of the array plus points within 3 element diameters of the
+    surface (the adaptive-subdivision branch of the influence quadrature)"""
+    from paper_2201_12050_b200.host import grid_points
+
+    c = sc.cell()
+    lo = np.min(c["centroid"], axis=0)
+    hi = np.max(c["centroid"], axis=0) + np.asarray(sc.pitch) * (np.asarray(sc.counts) - 1)
+    far = grid_points(lo - 0.6, hi + 0.6, (3, 2, 2))[:n_far]
+    i = np.arange(0, len(c["centroid"]), max(1, len(c["centroid"]) // 5))[:5]
+    near = c["centroid"][i] + 0.3 * c["diameter"][i, None] * c["normal"][i]  # just outside the surface
+    return np.concatenate([far, near])
+
+
+@pytest.mark.parametrize("cid,var", [(1, 0), (2, 2), (5, 2)])
+def test_device_field_matches_host_evaluate_field(cid, var):
+    from paper_2201_12050_b200 import Scene
+    from paper_2201_12050_b200.fmm import evaluate_field_gpu
+
+    sc = Scene(cid, var)
+    pts = _field_points(sc)
+    sol = uvec(np.random.default_rng(cid + 70), sc.N)
+    host = sc.field_host(sol, pts)
+    dev = evaluate_field_gpu(sc, sol, pts)
+    assert rel(dev, host) < 1e-12
+    # device pointers in, device tensor out
+    import torch
+
+    dev_t = evaluate_field_gpu(sc, torch.from_numpy(sol).cuda(), pts)
+    assert dev_t.is_cuda and rel(dev_t.cpu().numpy(), host) < 1e-12
+
+
+def test_device_field_with_half_space_images():
+    from paper_2201_12050_b200.fmm import evaluate_field_gpu
+
+    sc, d = _halfspace_scene((2, 2, 1), (0.35, 0.35, 0.0), 0.6, 0.9 + 0.2j)
+    assert sc.halfspace is not None
+    pts = _field_points(sc)
+    sol = uvec(np.random.default_rng(77), sc.N)
+    assert rel(evaluate_field_gpu(sc, sol, pts), sc.field_host(sol, pts)) < 1e-12
+
+
+def test_solve_then_field_then_insertion_loss(ops, assembled):
+    """run_scene's post-solve chain (src/scene.cpp:456-465) on the device:
+    GMRES solution -> evaluate_field -> insertion_loss, against the host chain."""
+    from paper_2201_12050_b200 import gmres
+    from paper_2201_12050_b200.fmm import evaluate_field_gpu
+    from paper_2201_12050_b200.host import insertion_loss
+
+    sc, d = assembled(1, 0)
+    rep = gmres(ops(d), sc.rhs(0), tol=1e-8, restart=50, max_iter=300)
+    assert rep.converged
+    pts = _field_points(sc)
+    p_inc = sc.incident(pts)
+    p_dev = evaluate_field_gpu(sc, rep.solution, pts, p_incident=p_inc)
+    p_host = sc.field_host(rep.solution, pts)
+    assert rel(p_dev, p_host) < 1e-12
+    assert abs(insertion_loss(p_inc, p_dev) - insertion_loss(p_inc, p_host)) < 1e-10
+
+
 # ---- lockstep batched GMRES (cfg5's 64 right-hand sides) -------------------------
 
 def test_batched_gmres_matches_per_rhs_oracle_with_restarts(ops, assembled):
