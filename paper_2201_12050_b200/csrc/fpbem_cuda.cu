@@ -111,7 +111,7 @@ struct fpbem_cu_op {
   int* tgt_ptr = nullptr;
   int* tgt_pairs = nullptr;
   int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
-  int jobs_nrhs = -1, n_jobs = 0, n_p2m_jobs = 0, jobs_cap = 0;
+  int jobs_nrhs = -1, n_jobs = 0, jobs_cap = 0;
   long long pair_lo = 0, pair_hi = 0;  // global pair range this rank computes (all without a partition)
   std::vector<int> pair_tgt;    // host copy: target cell of every pair
   int rank = 0, nranks = 1;     // near-field offset partition
@@ -119,6 +119,7 @@ struct fpbem_cu_op {
   // expansions and spectrum
   c64* u0 = nullptr;
   c64* v0 = nullptr;
+  c64* v0t = nullptr;  // V0^T (b rows of n), for the P2M kernel
   int L[3] = {1, 1, 1};
   long long q_total = 1;
   c64* lambda = nullptr;
@@ -238,16 +239,13 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
   const char* order = std::getenv("FPBEM_JOB_ORDER");
   if (order && std::strcmp(order, "lpt") == 0)
     std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return (a.z & 0xff) > (b.z & 0xff); });
-  const int n_near_jobs = static_cast<int>(jobs.size());
-  tile_columns(jobs, 0, op->n_cells * nrhs, 0, narrow);
   if (static_cast<int>(jobs.size()) > op->jobs_cap) {
     if (op->jobs) cudaFree(op->jobs);
     op->jobs = dalloc<int4>(jobs.size(), "jobs");
     op->jobs_cap = static_cast<int>(jobs.size());
   }
   if (!jobs.empty()) h2d(op->jobs, jobs.data(), jobs.size() * sizeof(int4), op->stream, "jobs upload");
-  op->n_jobs = n_near_jobs;
-  op->n_p2m_jobs = static_cast<int>(jobs.size()) - n_near_jobs;
+  op->n_jobs = static_cast<int>(jobs.size());
   op->jobs_nrhs = nrhs;
 }
 
@@ -413,9 +411,7 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
   ev_record(op, 1, s);
   ev_record(op, 2, a);
   if (far_here) {
-    check(launch_block_gemm(op->v0, 0, op->b, op->b, x, op->mom, op->b, nullptr, op->jobs + op->n_jobs,
-                            op->n_p2m_jobs, op->n, op->n, op->N, nrhs, a),
-          "p2m");
+    check(launch_p2m(op->v0t, x, op->mom, op->n, op->b, op->N, nrhs, op->n_cells, a), "p2m");
     op->launches++;
   }
   ev_record(op, 3, a);
@@ -1117,6 +1113,13 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->v0 = dalloc<c64>(nb, "v0");
     h2d(op->u0, d->u0, nb * sizeof(c64), op->stream, "u0 upload");
     h2d(op->v0, d->v0, nb * sizeof(c64), op->stream, "v0 upload");
+    {
+      std::vector<fpbem_c64> t(nb);  // V0 is b x n column-major: v0[c + b j] -> v0t[c n + j]
+      for (int j = 0; j < op->n; ++j)
+        for (int c = 0; c < op->b; ++c) t[static_cast<size_t>(c) * op->n + j] = d->v0[static_cast<size_t>(j) * op->b + c];
+      op->v0t = dalloc<c64>(nb, "v0t");
+      h2d(op->v0t, t.data(), nb * sizeof(c64), op->stream, "v0t upload");
+    }
 
     // spectrum sizes: caller's, else the reference's 7-smooth padding
     for (int k = 0; k < 3; ++k) {
@@ -1162,7 +1165,7 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
   if (op->stream) cudaStreamSynchronize(op->stream);
   for (void* p : {static_cast<void*>(op->S), static_cast<void*>(op->pair_src), static_cast<void*>(op->tgt_ptr),
                   static_cast<void*>(op->tgt_pairs), static_cast<void*>(op->jobs), static_cast<void*>(op->u0),
-                  static_cast<void*>(op->v0), static_cast<void*>(op->lambda), static_cast<void*>(op->lambda_hat),
+                  static_cast<void*>(op->v0), static_cast<void*>(op->v0t), static_cast<void*>(op->lambda), static_cast<void*>(op->lambda_hat),
                   static_cast<void*>(op->mom_perm), static_cast<void*>(op->loc_hat), static_cast<void*>(op->tw[0]),
                   static_cast<void*>(op->tw[1]), static_cast<void*>(op->tw[2]), static_cast<void*>(op->W),
                   static_cast<void*>(op->mom), static_cast<void*>(op->loc), static_cast<void*>(op->fa),

@@ -110,6 +110,10 @@ cudaError_t launch_field(const double* corners, const int* nv, const double* cen
                          bool with_image, int hs_axis, double hs_offset, c64 refl, c64* partial, c64* out,
                          cudaStream_t stream);
 
+// P2M (csrc/m2l.cu): mom[(cell * nrhs + r) * b + c] = sum_j V0[c][j] x[r * N + cell * n + j], v0t = V0^T rows
+cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, long long N, int nrhs, int cells,
+                       cudaStream_t stream);
+
 // device M2L bank (csrc/far_bank.cu): out[s] = [K(delta_s)] + refl K(image_s) P_axis
 int far_bank_max_nt();
 cudaError_t launch_far_bank(int device, int n_t, double k, int n_blk, const double* delta, const double* image,

@@ -82,6 +82,61 @@ dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __
   }
 }
 
+// P2M: mom[(cell * nrhs + r) * b + c] = sum_j V0[c][j] x[r * N + cell * n + j]
+// (src/fmm.cpp:256-259). CTA (cell * nrhs + r, coefficient group g of 8 CPW):
+// warp w carries the coefficients c = 8 CPW g + w + 8 u, u < CPW (independent
+// partial sums sharing every x load) over lane-strided j, four j per step with
+// all loads issued before the FMAs, reading rows of V0^T (v0t[c * n + j],
+// contiguous); fixed-order shuffle reductions. CPW = 4 when there are enough
+// (cell, rhs) pairs to fill the GPU, else 1 (more CTAs per cell).
+template <int CPW>
+__global__ void __launch_bounds__(256)
+p2m_kernel(const c64* __restrict__ v0t, const c64* __restrict__ x, c64* __restrict__ mom, int n, int b,
+           long long N, int nrhs) {
+  const int cr = blockIdx.x;
+  const int cell = cr / nrhs, r = cr - cell * nrhs;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.y * 8 * CPW + w;
+  const int nc = min(CPW, (b - c0 + 7) / 8);  // this warp's coefficients
+  if (nc <= 0) return;
+  const c64* xv = x + static_cast<long long>(r) * N + static_cast<long long>(cell) * n;
+  const c64* vr = v0t + static_cast<long long>(c0) * n;
+  c64 acc[CPW];
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) acc[u] = cmk(0.0, 0.0);
+  int j = lane;
+  for (; j + 96 < n; j += 128) {
+    c64 xj[4], v[CPW][4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) xj[t] = xv[j + 32 * t];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u)
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        v[u][t] = u < nc ? __ldg(vr + static_cast<long long>(8 * u) * n + j + 32 * t) : cmk(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) acc[u] = cfma(v[u][t], xj[t], acc[u]);
+  }
+  for (; j < n; j += 32) {
+    const c64 xj = xv[j];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u)
+      if (u < nc) acc[u] = cfma(__ldg(vr + static_cast<long long>(8 * u) * n + j), xj, acc[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    c64 t = acc[u];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      t.x += __shfl_xor_sync(0xffffffffu, t.x, off);
+      t.y += __shfl_xor_sync(0xffffffffu, t.y, off);
+    }
+    if (lane == 0 && u < nc) mom[static_cast<long long>(cr) * b + c0 + 8 * u] = t;
+  }
+}
+
 // image[q][r][i] = sum_j Λ_q[i + b j] field[q][r][j]; one thread per (q, r, i)
 __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* __restrict__ field,
                                     c64* __restrict__ image, long long q_total, int b, int nrhs) {
@@ -572,6 +627,19 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     case 4: dft_axis_kernel<4><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
     case 2: dft_axis_kernel<2><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
     default: dft_axis_kernel<1><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, long long N, int nrhs, int cells,
+                       cudaStream_t stream) {
+  if (cells == 0 || nrhs == 0) return cudaSuccess;
+  const long long blocks = static_cast<long long>(cells) * nrhs;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  if (blocks >= 4LL * kNumSMs) {
+    p2m_kernel<4><<<dim3(static_cast<unsigned>(blocks), (b + 31) / 32), 256, 0, stream>>>(v0t, x, mom, n, b, N, nrhs);
+  } else {
+    p2m_kernel<1><<<dim3(static_cast<unsigned>(blocks), (b + 7) / 8), 256, 0, stream>>>(v0t, x, mom, n, b, N, nrhs);
   }
   return cudaGetLastError();
 }
