@@ -321,10 +321,9 @@ def run_ours(args):
     m = data.counts
     n_pairs = int(sum((m[0] - abs(int(o[0]))) * (m[1] - abs(int(o[1]))) * (m[2] - abs(int(o[2])))
                       for o in data.near_offsets))
-    if comm is not None:  # rank 0's share of the near-field pairs
-        from paper_2201_12050_b200.fmm import partition_pairs
-
-        lo, hi = partition_pairs(n_pairs, world, rank)
+    far_pairs = 0.0
+    if comm is not None:  # rank 0's share of the near-field pairs (balanced against its far field)
+        lo, hi, far_pairs = op.partition()
         n_pairs = hi - lo
     flops = 8.0 * data.n_dof ** 2 * float(n_pairs)
     gemm_ms = stages["near_gemm"] / max(1, stages["applies"])
@@ -347,7 +346,8 @@ def run_ours(args):
             "config": {
                 "workload": desc, "n_dof_total": data.N, "n_dof_cell": data.n_dof, "lattice": list(data.counts),
                 "near_offsets": data.n_near, "far_offsets": data.n_far, "n_t": 4, "nrhs": 1,
-                "parallelism": (f"near-field pairs split over {world} GPUs + NCCL all-reduce of y" if strong
+                "parallelism": (f"near-field pairs split over {world} GPUs (rank 0 {n_pairs} pairs, "
+                                f"{far_pairs:.0f} fewer for its far field) + NCCL all-reduce of y" if strong
                                 else f"replicas x{world}" if world > 1 else "single GPU"),
                 "l2": f"inputs larger than L2: near-field operator {16 * data.n_near * data.n_dof ** 2 / 1e9:.2f} GB "
                       "streamed from HBM every step",

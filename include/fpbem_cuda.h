@@ -206,7 +206,10 @@ long long fpbem_cu_kernel_launches(const fpbem_cu_op* op);
 /* Multi-GPU (one process per GPU). Rank 0 makes the id, the caller
  * broadcasts its 128 bytes (e.g. torch.distributed), every rank inits.
  * With a communicator attached, apply() splits the near-field pairs
- * across ranks and all-reduces the partial products. */
+ * across ranks and all-reduces the partial products;
+ * set_comm measures the far field's cost (fpbem_cu_fmm_far_pairs), averages
+ * it over the ranks and gives rank 0 (which runs the far field) that many
+ * fewer pairs. */
 int fpbem_cu_comm_unique_id(unsigned char id_out[128]);
 int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int device,
                        fpbem_cu_comm** out);
@@ -215,13 +218,23 @@ int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm);
 
 /* The same partition without a communicator: apply() returns this rank's
  * partial product (its near-field pairs; rank 0 adds the far field). Summing
- * the nranks partial products gives the full product. */
-int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks);
+ * the nranks partial products gives the full product. far_pairs: rank 0's
+ * deficit (0 = equal shares; every rank must pass the same value). */
+int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs);
+
+/* This handle's current pair range [lo, hi) and rank-0 deficit. */
+int fpbem_cu_fmm_partition(const fpbem_cu_op* op, long long* lo, long long* hi, double* far_pairs);
+
+/* The far field's cost (P2M + M2L) in near-field pair equivalents, measured on
+ * the handle's device: t_far / t_near(all pairs) x n_pairs. */
+int fpbem_cu_fmm_far_pairs(fpbem_cu_op* op, double* far_pairs);
 
 /* The partition rule itself (host only, no GPU): the near-field (offset,
- * target) pairs, in offset-major order, split into nranks equal contiguous
- * ranges [lo, hi) — every pair costs the same n_dof^2 complex MACs. */
-int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, long long* lo, long long* hi);
+ * target) pairs, in offset-major order, split into nranks contiguous ranges
+ * [lo, hi) — every pair costs the same n_dof^2 complex MACs — equal, except
+ * that rank 0 takes round(far_pairs) fewer and ranks 1.. share the rest. */
+int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, double far_pairs, long long* lo,
+                             long long* hi);
 
 const char* fpbem_cu_last_error(void);
 const char* fpbem_cu_version(void);

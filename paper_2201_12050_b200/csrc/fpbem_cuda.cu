@@ -112,6 +112,7 @@ struct fpbem_cu_op {
   int* tgt_pairs = nullptr;
   int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
   int jobs_nrhs = -1, n_jobs = 0, jobs_cap = 0;
+  double far_pairs = 0.0;  // rank 0's deficit under the pair partition (calibrate_far_pairs)
   long long pair_lo = 0, pair_hi = 0;  // global pair range this rank computes (all without a partition)
   std::vector<int> pair_tgt;    // host copy: target cell of every pair
   int rank = 0, nranks = 1;     // near-field offset partition
@@ -171,9 +172,25 @@ namespace {
 // Multi-GPU work split: every near-field pair (offset, target)
 // costs the same n_dof^2 MACs, so ranks take equal contiguous ranges of the
 // global pair order (offset-major) — balanced whatever the offset count.
-void pair_range(long long n_pairs, int nranks, int rank, long long& lo, long long& hi) {
-  lo = n_pairs * rank / nranks;
-  hi = n_pairs * (rank + 1) / nranks;
+// Contiguous ranges of the (offset, target) pairs: equal shares, except that
+// rank 0 (which also runs the far field) takes `far_pairs` fewer, the other
+// ranks sharing the rest equally; every pair is owned exactly once.
+void pair_range(long long n_pairs, int nranks, int rank, double far_pairs, long long& lo, long long& hi) {
+  long long d = far_pairs > 0.0 && nranks > 1 ? std::llround(far_pairs) : 0;
+  if (d == 0) {
+    lo = n_pairs * rank / nranks;
+    hi = n_pairs * (rank + 1) / nranks;
+    return;
+  }
+  const long long h0 = std::max(0LL, (n_pairs + d) / nranks - d);  // rank 0's share
+  if (rank == 0) {
+    lo = 0;
+    hi = h0;
+    return;
+  }
+  const long long rest = n_pairs - h0;
+  lo = h0 + rest * (rank - 1) / (nranks - 1);
+  hi = h0 + rest * rank / (nranks - 1);
 }
 
 // per-target CSR of the pairs this rank owns, in offset order (the reduction order)
@@ -191,9 +208,11 @@ void build_target_csr(fpbem_cu_op* op) {
   if (!tpairs.empty()) h2d(op->tgt_pairs, tpairs.data(), tpairs.size() * sizeof(int), op->stream, "target pairs");
 }
 
-void set_partition(fpbem_cu_op* op, int rank, int nranks) {
+void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
   if (nranks < 1 || rank < 0 || rank >= nranks) fail(FPBEM_CU_EINVAL, "partition: bad rank / nranks");
-  pair_range(op->n_pairs, nranks, rank, op->pair_lo, op->pair_hi);
+  if (!(far_pairs >= 0.0)) fail(FPBEM_CU_EINVAL, "partition: far_pairs must be >= 0");
+  pair_range(op->n_pairs, nranks, rank, far_pairs, op->pair_lo, op->pair_hi);
+  op->far_pairs = far_pairs;
   op->rank = rank;
   op->nranks = nranks;
   op->jobs_nrhs = -1;  // rebuild the GEMM job list
@@ -385,6 +404,65 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   }
 }
 
+// Far field of one product: P2M (events 2-3) and M2L into op->loc (events 3-4);
+// the Hankel image pair adds the K_hat term (src/fmm.cpp:256-263)
+void far_field(fpbem_cu_op* op, const c64* x, int nrhs, cudaStream_t a) {
+  ev_record(op, 2, a);
+  check(launch_p2m(op->v0t, x, op->mom, op->n, op->b, op->N, nrhs, op->n_cells, a), "p2m");
+  op->launches++;
+  ev_record(op, 3, a);
+  m2l_apply(op, nrhs, a, op->mom, op->lambda, op->loc);
+  if (op->mirrored_level >= 0) {  // local += hankel_matvec(K_hat spectrum, mirror_permute(moments)) (src/fmm.cpp:262-263)
+    const long long E = static_cast<long long>(nrhs) * op->b;
+    check(launch_mirror_permute(op->mom, op->mom_perm, op->counts, op->mirrored_level, E, a), "mirror permute");
+    m2l_apply(op, nrhs, a, op->mom_perm, op->lambda_hat, op->loc_hat);
+    check(launch_add(op->loc, op->loc_hat, static_cast<long long>(op->n_cells) * E, a), "local image add");
+    op->launches += 2;
+  }
+  ev_record(op, 4, a);
+}
+
+// Cost of the far field in near-field pair equivalents, measured on this
+// device: t(P2M + M2L) / t(near GEMM over all pairs) x n_pairs, single RHS,
+// all on the handle's stream (best of 3 after a warm-up). Rank 0 carries the
+// far field under the pair partition, so it gets this many fewer pairs.
+double calibrate_far_pairs(fpbem_cu_op* op) {
+  if (op->n_pairs == 0) return 0.0;
+  const int rank = op->rank, nranks = op->nranks;
+  const double far_pairs = op->far_pairs;
+  set_partition(op, 0, 1, 0.0);
+  cudaStream_t s = op->stream;
+  c64* x = dalloc<c64>(static_cast<size_t>(op->N), "calibration input");
+  std::unique_ptr<c64, decltype(&cudaFree)> keep_x(x, &cudaFree);
+  check(cudaMemsetAsync(x, 0, static_cast<size_t>(op->N) * sizeof(c64), s), "calibration input");
+  cudaEvent_t e[3];
+  for (auto& ev : e) check(cudaEventCreate(&ev), "calibration events");
+  std::unique_ptr<cudaEvent_t, void (*)(cudaEvent_t*)> keep_e(e, [](cudaEvent_t* v) {
+    for (int i = 0; i < 3; ++i) cudaEventDestroy(v[i]);
+  });
+  build_jobs(op, 1);
+  float best_near = 1e30f, best_far = 1e30f;
+  for (int it = 0; it < 4; ++it) {
+    check(cudaEventRecord(e[0], s), "calibration");
+    check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n, op->pair_src,
+                            op->jobs, op->n_jobs, op->n, op->n, op->N, 1, s),
+          "calibration gemm");
+    check(cudaEventRecord(e[1], s), "calibration");
+    far_field(op, x, 1, s);
+    check(cudaEventRecord(e[2], s), "calibration");
+    check(cudaEventSynchronize(e[2]), "calibration");
+    float t_near, t_far;
+    cudaEventElapsedTime(&t_near, e[0], e[1]);
+    cudaEventElapsedTime(&t_far, e[1], e[2]);
+    if (it > 0) {
+      best_near = std::min(best_near, t_near);
+      best_far = std::min(best_far, t_far);
+    }
+  }
+  set_partition(op, rank, nranks, far_pairs);
+  return best_near > 0.0f ? static_cast<double>(best_far) / best_near * static_cast<double>(op->n_pairs) : 0.0;
+}
+
 // One FMM product for nrhs <= max_rhs right-hand sides, device pointers.
 // Order of the sums follows src/fmm.cpp:253-267: y = S p, then y += U0 L.
 // With an offset partition (nranks > 1) this rank computes the product of
@@ -409,23 +487,7 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
         "near gemm");
   op->launches += op->n_jobs > 0;
   ev_record(op, 1, s);
-  ev_record(op, 2, a);
-  if (far_here) {
-    check(launch_p2m(op->v0t, x, op->mom, op->n, op->b, op->N, nrhs, op->n_cells, a), "p2m");
-    op->launches++;
-  }
-  ev_record(op, 3, a);
-  if (far_here) {
-    m2l_apply(op, nrhs, a, op->mom, op->lambda, op->loc);
-    if (op->mirrored_level >= 0) {  // local += hankel_matvec(K_hat spectrum, mirror_permute(moments)) (src/fmm.cpp:262-263)
-      const long long E = static_cast<long long>(nrhs) * op->b;
-      check(launch_mirror_permute(op->mom, op->mom_perm, op->counts, op->mirrored_level, E, a), "mirror permute");
-      m2l_apply(op, nrhs, a, op->mom_perm, op->lambda_hat, op->loc_hat);
-      check(launch_add(op->loc, op->loc_hat, static_cast<long long>(op->n_cells) * E, a), "local image add");
-      op->launches += 2;
-    }
-  }
-  ev_record(op, 4, a);
+  if (far_here) far_field(op, x, nrhs, a);
   check(cudaEventRecord(op->join, a), "join");
   s = op->stream;
   check(cudaStreamWaitEvent(s, op->join, 0), "join");
@@ -1721,27 +1783,58 @@ int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm) {
     check(cudaSetDevice(op->device), "set device");
     if (!comm) {
       op->comm = nullptr;
-      set_partition(op, 0, 1);
+      set_partition(op, 0, 1, 0.0);
       return;
     }
-    set_partition(op, comm->rank, comm->nranks);
+    // rank 0's far-field cost in pair equivalents, averaged over the ranks so
+    // that every rank derives the same partition
+    double f = comm->nranks > 1 ? calibrate_far_pairs(op) : 0.0;
+    if (comm->nranks > 1) {
+      double* df = dalloc<double>(1, "far pairs");
+      std::unique_ptr<double, decltype(&cudaFree)> keep_df(df, &cudaFree);
+      h2d(df, &f, sizeof(double), op->stream, "far pairs");
+      const int rc = comm->allreduce(df, df, 1, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm->comm, op->stream);
+      if (rc != 0) fail(FPBEM_CU_ENCCL, "ncclAllReduce failed: " + std::to_string(rc));
+      check(cudaMemcpyAsync(&f, df, sizeof(double), cudaMemcpyDeviceToHost, op->stream), "far pairs");
+      check(cudaStreamSynchronize(op->stream), "far pairs");
+      f /= comm->nranks;
+    }
+    set_partition(op, comm->rank, comm->nranks, f);
     op->comm = comm;
   });
 }
 
-int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks) {
+int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
   return guard([&] {
     if (!op) fail(FPBEM_CU_EINVAL, "set_partition: null op");
     check(cudaSetDevice(op->device), "set device");
-    set_partition(op, rank, nranks);
+    set_partition(op, rank, nranks, far_pairs);
   });
 }
 
-int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, long long* lo, long long* hi) {
+int fpbem_cu_fmm_partition(const fpbem_cu_op* op, long long* lo, long long* hi, double* far_pairs) {
   return guard([&] {
-    if (n_pairs < 0 || nranks < 1 || rank < 0 || rank >= nranks || !lo || !hi)
+    if (!op || !lo || !hi || !far_pairs) fail(FPBEM_CU_EINVAL, "partition: null argument");
+    *lo = op->pair_lo;
+    *hi = op->pair_hi;
+    *far_pairs = op->far_pairs;
+  });
+}
+
+int fpbem_cu_fmm_far_pairs(fpbem_cu_op* op, double* far_pairs) {
+  return guard([&] {
+    if (!op || !far_pairs) fail(FPBEM_CU_EINVAL, "far_pairs: null argument");
+    check(cudaSetDevice(op->device), "set device");
+    *far_pairs = calibrate_far_pairs(op);
+  });
+}
+
+int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, double far_pairs, long long* lo,
+                             long long* hi) {
+  return guard([&] {
+    if (n_pairs < 0 || nranks < 1 || rank < 0 || rank >= nranks || !lo || !hi || !(far_pairs >= 0.0))
       fail(FPBEM_CU_EINVAL, "partition: bad args");
-    pair_range(n_pairs, nranks, rank, *lo, *hi);
+    pair_range(n_pairs, nranks, rank, far_pairs, *lo, *hi);
   });
 }
 

@@ -35,11 +35,13 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def partition_pairs(n_pairs: int, nranks: int, rank: int) -> tuple[int, int]:
+def partition_pairs(n_pairs: int, nranks: int, rank: int, far_pairs: float = 0.0) -> tuple[int, int]:
     """The library's multi-GPU split (host only): this rank's [lo, hi) range of
-    the near-field (offset, target) pairs in offset-major order."""
+    the near-field (offset, target) pairs in offset-major order; rank 0, which
+    also runs the far field, takes round(far_pairs) fewer."""
     lo, hi = C.c_longlong(), C.c_longlong()
-    _raise(_native.cuda().fpbem_cu_partition_pairs(int(n_pairs), int(nranks), int(rank), C.byref(lo), C.byref(hi)))
+    _raise(_native.cuda().fpbem_cu_partition_pairs(int(n_pairs), int(nranks), int(rank), float(far_pairs),
+                                                   C.byref(lo), C.byref(hi)))
     return lo.value, hi.value
 
 
@@ -198,10 +200,24 @@ class FmmOperators:
     def set_stream(self, stream_ptr: int | None) -> None:
         _raise(_native.cuda().fpbem_cu_set_stream(self._h, stream_ptr))
 
-    def set_partition(self, rank: int, nranks: int) -> None:
+    def set_partition(self, rank: int, nranks: int, far_pairs: float = 0.0) -> None:
         """Near-field pair partition without communication: matvec returns
-        this rank's partial product (rank 0 includes the far field)."""
-        _raise(_native.cuda().fpbem_cu_fmm_set_partition(self._h, rank, nranks))
+        this rank's partial product (rank 0 includes the far field and takes
+        round(far_pairs) fewer pairs; every rank must pass the same value)."""
+        _raise(_native.cuda().fpbem_cu_fmm_set_partition(self._h, rank, nranks, float(far_pairs)))
+
+    def partition(self) -> tuple[int, int, float]:
+        """(lo, hi, far_pairs): this handle's pair range and rank-0 deficit."""
+        lo, hi, f = C.c_longlong(), C.c_longlong(), C.c_double()
+        _raise(_native.cuda().fpbem_cu_fmm_partition(self._h, C.byref(lo), C.byref(hi), C.byref(f)))
+        return lo.value, hi.value, f.value
+
+    def far_pairs(self) -> float:
+        """The far field's cost in near-field pair equivalents, measured on
+        this device (what set_comm balances rank 0 by)."""
+        f = C.c_double()
+        _raise(_native.cuda().fpbem_cu_fmm_far_pairs(self._h, C.byref(f)))
+        return f.value
 
     def set_comm(self, comm) -> None:
         """Attach a Communicator: near-field pairs split across its ranks,

@@ -477,6 +477,27 @@ def test_folded_half_space_matches_oracle(ops):
     assert rel(ops(d).matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
 
 
+def test_balanced_partition_partials_sum_to_product(ops, assembled):
+    """set_partition with a rank-0 deficit (the far field's measured cost in
+    pair equivalents): partial products still sum to the product, rank 0 owns
+    fewer pairs"""
+    sc, d = assembled(2, 2)
+    op = ops(d)
+    far = op.far_pairs()
+    assert far > 0.0
+    p = uvec(np.random.default_rng(31), d.N)
+    full = op.matvec(p)
+    total = np.zeros_like(full)
+    sizes = []
+    for r in range(4):
+        op.set_partition(r, 4, far_pairs=max(far, 3.0))
+        lo, hi, f = op.partition()
+        sizes.append(hi - lo)
+        total += op.matvec(p)
+    assert rel(total, full) < 1e-13
+    assert sizes[0] < sizes[1]
+
+
 def test_hankel_partition_sums_to_product(ops):
     sc, d = _halfspace_scene((3, 2, 4), (0.35, 0.35, 0.35), 0.25, 0.7)
     p = uvec(np.random.default_rng(8), d.N)

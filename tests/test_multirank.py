@@ -81,6 +81,26 @@ def test_partition_rule_covers_every_pair_once():
         assert max(sizes) - min(sizes) <= 1
 
 
+@pytest.mark.parametrize("n_pairs,world,far", [(8012, 8, 246.4), (70336, 8, 800.0), (8012, 2, 246.0),
+                                               (22, 4, 100.0), (1274, 8, 0.4), (5, 3, 2.0)])
+def test_balanced_partition_gives_rank0_its_far_field_deficit(n_pairs, world, far):
+    """rank 0 runs the far field: it takes round(far) fewer pairs (never fewer
+    than 0), ranks 1.. share the rest equally, every pair owned once"""
+    from paper_2201_12050_b200.fmm import partition_pairs
+
+    ranges = [partition_pairs(n_pairs, world, r, far) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n_pairs
+    for (l0, h0), (l1, h1) in zip(ranges, ranges[1:]):
+        assert h0 == l1
+    sizes = [h - l for l, h in ranges]
+    assert min(sizes) >= 0 and max(sizes[1:]) - min(sizes[1:]) <= 1
+    d = round(far)
+    if d and sizes[0] > 0:  # rank 0 short by the deficit, within rounding of the equal shares
+        assert abs((sizes[1] - sizes[0]) - d) <= 2 + d // (world - 1)
+    # equal split when the far field is free
+    assert partition_pairs(n_pairs, world, 0, 0.0) == (0, n_pairs // world)
+
+
 def test_near_pairs_order_matches_the_device_count():
     from paper_2201_12050_b200 import Scene
     from paper_2201_12050_b200.fmm import near_pairs
