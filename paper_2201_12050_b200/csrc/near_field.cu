@@ -31,28 +31,37 @@ constexpr int STAGES = 3;
 constexpr int AP = BM + 2;  // smem pitch (complex) of the [k][m] A tile: 16B-bank conflict free
 constexpr int BP = BK + 4;  // smem pitch (complex) of the [n][k] B tile
 constexpr int THREADS = 256;
+#ifndef FPBEM_WARP_NI
+#define FPBEM_WARP_NI 2
+#endif
+constexpr int kWarpNI = FPBEM_WARP_NI;  // n-tiles per warp (1: the previous 64x8 warp tile)
 
 constexpr size_t kSmemA = sizeof(c64) * STAGES * BK * AP;
 constexpr size_t kSmemB = sizeof(c64) * STAGES * BN * BP;
 
 // K loop + epilogue of one CTA tile. Gauss 3-multiplication complex product
 // on the FP64 tensor cores: T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi);
-// Cr = T1 - T2, Ci = T3 - T1 - T2. MI 8x8 m-tiles per warp: warps form
-// (8 / MI) row groups x MI column slabs of 8, covering 64 rows x 8*MI columns.
-template <int MI, typename Loader>
+// Cr = T1 - T2, Ci = T3 - T1 - T2. A warp owns MI x NI 8x8 tiles: warps form
+// (8 / MI) row groups of 8 MI rows x MI column groups of 8 NI columns, covering
+// 64 rows x 8 MI NI columns. Per 4-deep k step a warp loads MI + NI fragments
+// from shared memory for 3 MI NI DMMAs (NI = 2 halves the A re-reads of NI = 1,
+// where every warp loaded all 64 rows: shared-memory bandwidth was the limiter).
+template <int MI, int NI, typename Loader>
 __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& load_stage, int nk, int warp, int lane,
                                           int ncols, int m0, int M, const long long* col_out, c64* __restrict__ out) {
   constexpr int G = 8 / MI;  // row groups
   const int wm = warp % G, wn = warp / G;
   const int fr = lane >> 2, fk = lane & 3;
-  const bool active = wn * 8 < ncols;
-  double t1[MI][2], t2[MI][2], t3[MI][2];
+  const bool active = wn * 8 * NI < ncols;
+  double t1[MI][NI][2], t2[MI][NI][2], t3[MI][NI][2];
 #pragma unroll
-  for (int mi = 0; mi < MI; ++mi) {
-    t1[mi][0] = t1[mi][1] = 0.0;
-    t2[mi][0] = t2[mi][1] = 0.0;
-    t3[mi][0] = t3[mi][1] = 0.0;
-  }
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      t1[mi][ni][0] = t1[mi][ni][1] = 0.0;
+      t2[mi][ni][0] = t2[mi][ni][1] = 0.0;
+      t3[mi][ni][0] = t3[mi][ni][1] = 0.0;
+    }
 
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
@@ -69,19 +78,29 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
     if (!active) continue;
 
     const c64* as = As + (kt % STAGES) * BK * AP + wm * (8 * MI);
-    const c64* bs = Bs + (kt % STAGES) * BN * BP;
+    const c64* bs = Bs + (kt % STAGES) * BN * BP + wn * (8 * NI) * BP;
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
-      const c64 b = bs[(wn * 8 + fr) * BP + k4 * 4 + fk];
-      const double bsum = b.x + b.y;
+      c64 b[NI], a[MI];
+      double bsum[NI], asum[MI];
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        b[ni] = bs[(ni * 8 + fr) * BP + k4 * 4 + fk];
+        bsum[ni] = b[ni].x + b[ni].y;
+      }
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) {
-        const c64 a = as[(k4 * 4 + fk) * AP + mi * 8 + fr];
-        const double asum = a.x + a.y;
-        dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
-        dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
-        dmma884(t3[mi][0], t3[mi][1], asum, bsum);
+        a[mi] = as[(k4 * 4 + fk) * AP + mi * 8 + fr];
+        asum[mi] = a[mi].x + a[mi].y;
       }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          dmma884(t1[mi][ni][0], t1[mi][ni][1], a[mi].x, b[ni].x);
+          dmma884(t2[mi][ni][0], t2[mi][ni][1], a[mi].y, b[ni].y);
+          dmma884(t3[mi][ni][0], t3[mi][ni][1], asum[mi], bsum[ni]);
+        }
     }
   }
   cp_async_wait<0>();
@@ -93,11 +112,13 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
     const int gm = m0 + wm * (8 * MI) + mi * 8 + fr;
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = wn * 8 + 2 * fk + j;
-      const long long o = col_out[c];
-      if (o >= 0) out[o + gm] = cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
-    }
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = wn * 8 * NI + ni * 8 + 2 * fk + j;
+        const long long o = col_out[c];
+        if (o >= 0) out[o + gm] = cmk(t1[mi][ni][j] - t2[mi][ni][j], t3[mi][ni][j] - t1[mi][ni][j] - t2[mi][ni][j]);
+      }
   }
 }
 
@@ -176,16 +197,18 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   // width class of the column tile: 0 -> 64 columns (each warp 64 rows x 8),
   // 1 -> 32 columns (32 rows x 8), 2 -> 16 columns (16 rows x 8): narrow
   // tiles keep all 8 warps busy instead of idling most of them
-  switch (cls) {
-    case 0:
-      gemm_main<8>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out);
-      break;
-    case 1:
-      gemm_main<4>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out);
-      break;
-    default:
-      gemm_main<2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out);
-      break;
+  if (kWarpNI == 2) {
+    switch (cls) {
+      case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+      case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+      default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+    }
+  } else {
+    switch (cls) {
+      case 0: gemm_main<8, 1>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+      case 1: gemm_main<4, 1>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+      default: gemm_main<2, 1>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+    }
   }
 }
 
