@@ -342,7 +342,8 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
   struct Pass {
-    int kind;  // 0 dft, 1 mode product, 2 fused z-dft + mode product + inverse z-dft
+    int kind;  // 0 dft, 1 mode product, 2 fused z-dft + mode product + inverse z-dft,
+               // 3 / 4 forward / inverse x+y plane DFTs (one kernel each)
     long long n_a;
     int n_in, n_out;
     long long inner;
@@ -357,13 +358,32 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   const char* fz = std::getenv("FPBEM_M2L_FUSE");
   const bool fuse_z = Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
                       m2l_zfused_ring(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E), op->b) > 0;
-  if (Lx > 1) {
-    passes.push_back({0, My * Mz, static_cast<int>(Mx), static_cast<int>(Lx), E, static_cast<int>(Lx), 0, false});
+  // x and y together in shared memory per z-plane when the plane fits (FPBEM_M2L_XY=0: per-axis passes)
+  static const bool xy_env = [] {
+    const char* v = std::getenv("FPBEM_M2L_XY");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  // where it measured faster than the per-axis passes: enough (plane, field)
+  // CTAs to fill the GPU without splitting (cfg3), or small planes with both axes periodic (cfg2)
+  const bool xy_wins = Mz * E >= 2LL * 148 || (Lx > 1 && Ly > 1 && Lx * Ly <= 1024);
+  const bool fuse_xy = xy_env && xy_wins && (Lx > 1 || Ly > 1) &&
+                       xy_plane_smem(static_cast<int>(Mx), static_cast<int>(My), static_cast<int>(Lx),
+                                     static_cast<int>(Ly), true) <= 200 * 1024 &&
+                       xy_plane_smem(static_cast<int>(Mx), static_cast<int>(My), static_cast<int>(Lx),
+                                     static_cast<int>(Ly), false) <= 200 * 1024;
+  if (fuse_xy) {
+    passes.push_back({3, 0, 0, 0, 0, 0, -1, false});
     cx = Lx;
-  }
-  if (Ly > 1) {
-    passes.push_back({0, Mz, static_cast<int>(My), static_cast<int>(Ly), cx * E, static_cast<int>(Ly), 1, false});
     cy = Ly;
+  } else {
+    if (Lx > 1) {
+      passes.push_back({0, My * Mz, static_cast<int>(Mx), static_cast<int>(Lx), E, static_cast<int>(Lx), 0, false});
+      cx = Lx;
+    }
+    if (Ly > 1) {
+      passes.push_back({0, Mz, static_cast<int>(My), static_cast<int>(Ly), cx * E, static_cast<int>(Ly), 1, false});
+      cy = Ly;
+    }
   }
   if (fuse_z) {
     passes.push_back({2, 0, 0, 0, 0, static_cast<int>(Lz), 2, false});
@@ -374,11 +394,17 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
     if (Lz > 1)
       passes.push_back({0, 1, static_cast<int>(Lz), static_cast<int>(Mz), Ly * Lx * E, static_cast<int>(Lz), 2, true});
   }
-  if (Ly > 1) passes.push_back({0, Mz, static_cast<int>(Ly), static_cast<int>(My), Lx * E, static_cast<int>(Ly), 1, true});
-  if (Lx > 1) passes.push_back({0, My * Mz, static_cast<int>(Lx), static_cast<int>(Mx), E, static_cast<int>(Lx), 0, true});
+  if (fuse_xy) {
+    passes.push_back({4, 0, 0, 0, 0, 0, -1, true});
+  } else {
+    if (Ly > 1)
+      passes.push_back({0, Mz, static_cast<int>(Ly), static_cast<int>(My), Lx * E, static_cast<int>(Ly), 1, true});
+    if (Lx > 1)
+      passes.push_back({0, My * Mz, static_cast<int>(Lx), static_cast<int>(Mx), E, static_cast<int>(Lx), 0, true});
+  }
   int last_dft = -1;  // the pass that applies the 1/q scale
   for (int i = 0; i < static_cast<int>(passes.size()); ++i)
-    if ((passes[i].kind == 0 && passes[i].back) || passes[i].kind == 2) last_dft = i;
+    if ((passes[i].kind == 0 && passes[i].back) || passes[i].kind == 2 || passes[i].kind == 4) last_dft = i;
   const c64* cur = moments;
   c64* bufs[2] = {op->fa, op->fb};
   int which = 0;
@@ -386,7 +412,13 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
     const Pass& p = passes[i];
     const bool final = i + 1 == static_cast<int>(passes.size());
     c64* out = final ? locals : bufs[which];
-    if (p.kind == 1) {
+    if (p.kind == 3 || p.kind == 4) {
+      const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
+      check(launch_xy_plane(cur, out, op->tw[0], op->tw[1], static_cast<int>(Mx), static_cast<int>(My),
+                            static_cast<int>(Lx), static_cast<int>(Ly), static_cast<int>(Mz), static_cast<int>(E),
+                            p.kind == 4, scale, s),
+            "lattice xy dft");
+    } else if (p.kind == 1) {
       check(launch_mode_product(lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
     } else if (p.kind == 2) {
       const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;

@@ -110,6 +110,13 @@ cudaError_t launch_field(const double* corners, const int* nv, const double* cen
                          bool with_image, int hs_axis, double hs_offset, c64 refl, c64* partial, c64* out,
                          cudaStream_t stream);
 
+// x and y lattice DFTs of every z-plane and field in one kernel (csrc/m2l.cu):
+// forward moments [iz][iy][ix][E] -> [iz][qy][qx][E]; inverse the reverse with
+// the scale; xy_plane_smem bytes of shared memory per CTA
+size_t xy_plane_smem(int Mx, int My, int Lx, int Ly, bool inverse);
+cudaError_t launch_xy_plane(const c64* in, c64* out, const c64* twx, const c64* twy, int Mx, int My, int Lx, int Ly,
+                            int Mz, int E, bool inverse, double scale, cudaStream_t stream);
+
 // P2M (csrc/m2l.cu): mom[(cell * nrhs + r) * b + c] = sum_j V0[c][j] x[r * N + cell * n + j], v0t = V0^T rows
 cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, long long N, int nrhs, int cells,
                        cudaStream_t stream);

@@ -56,22 +56,26 @@ dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __
       idx[o] = 0;
       step[o] = (q0 + o) % L;  // padded outputs (q0 + o >= n_out) may exceed L
     }
-    // 4 inputs and their twiddles are loaded before the FMAs (latency of the
-    // dependent loads otherwise dominates); zero-padded tail: fma(w, 0, acc) == acc
-    for (int j0 = 0; j0 < n_in; j0 += 4) {
-      c64 v[4], w[kQG][4];
+    // kB inputs and their twiddles are loaded before the FMAs (latency of the
+    // dependent loads otherwise dominates; 8 deep when a thread owns few
+    // outputs, e.g. the 256-term lines of a 1 x 256 lattice); zero-padded
+    // tail: fma(w, 0, acc) == acc
+    constexpr int kB = kQG <= 2 ? 8 : 4;
+    for (int j0 = 0; j0 < n_in; j0 += kB) {
+      c64 v[kB], w[kQG][kB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (j0 + u < n_in) ? src[static_cast<long long>(j0 + u) * n_inner] : cmk(0.0, 0.0);
+      for (int u = 0; u < kB; ++u)
+        v[u] = (j0 + u < n_in) ? src[static_cast<long long>(j0 + u) * n_inner] : cmk(0.0, 0.0);
 #pragma unroll
       for (int o = 0; o < kQG; ++o)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kB; ++u) {
           w[o][u] = tw_s[idx[o]];
           idx[o] += step[o];
           if (idx[o] >= L) idx[o] -= L;
         }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kB; ++u)
 #pragma unroll
         for (int o = 0; o < kQG; ++o) acc[o] = cfma(w[o][u], v[u], acc[o]);
     }
@@ -79,6 +83,125 @@ dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __
 #pragma unroll
     for (int o = 0; o < kQG; ++o)
       if (q0 + o < n_out) dst[static_cast<long long>(o) * n_inner] = cscale(acc[o], scale);
+  }
+}
+
+// x and y lattice DFTs of one z-plane and one field in shared memory (the two
+// per-axis passes fused; pruned as they are).
+//   forward : in = moments [iz][iy][ix][E] (iy < My, ix < Mx)
+//             X[iy][qx] = sum_ix Wx[qx][ix] in[iy][ix]            (all My x Lx)
+//             out[iz][qy][qx][E] = sum_iy Wy[qy][iy] X[iy][qx]     (this CTA's qy range)
+//   inverse : in = [iz][qy][qx][E] (all Ly x Lx)
+//             Y[iy][qx] = sum_qy conj Wy[qy][iy] in[qy][qx]        (this CTA's iy range)
+//             out[iz][iy][ix][E] = scale sum_qx conj Wx[qx][ix] Y[iy][qx]
+// with W[q][j] = exp(-2 pi i (j q mod L) / L) expanded once per CTA into
+// shared matrices (odd row pitch: conflict-free column access), so the inner
+// loops are two shared loads and one complex FMA per term. Each thread owns
+// two outputs that share their input loads; each output sums in index order
+// with even / odd partial sums. CTA (iz * E + e, part): the second (forward)
+// or first (inverse) phase is split over `parts` CTAs to fill the GPU.
+__device__ __forceinline__ int odd_pitch(int n) { return n | 1; }
+
+template <bool kInverse>
+__global__ void __launch_bounds__(256)
+xy_plane_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ twx,
+                const c64* __restrict__ twy, int Mx, int My, int Lx, int Ly, int E, int parts, double scale) {
+  extern __shared__ __align__(16) unsigned char xy_smem[];
+  // matrices indexed [output index][summation index]
+  //   forward: A1 = Wx (Lx x Mx), A2 = Wy (Ly x My); inverse: A1 = conj Wy^T (My x Ly), A2 = conj Wx^T (Mx x Lx)
+  const int r1 = kInverse ? My : Lx, c1 = kInverse ? Ly : Mx, L1 = kInverse ? Ly : Lx;
+  const int r2 = kInverse ? Mx : Ly, c2 = kInverse ? Lx : My, L2 = kInverse ? Lx : Ly;
+  const int p1 = odd_pitch(c1), p2 = odd_pitch(c2);
+  c64* A1 = reinterpret_cast<c64*>(xy_smem);
+  c64* A2 = A1 + r1 * p1;
+  c64* a = A2 + r2 * p2;  // input plane: forward My x Mx, inverse Ly x Lx
+  const int rows_in = kInverse ? Ly : My, cols_in = kInverse ? Lx : Mx;
+  c64* mid = a + rows_in * cols_in;  // forward X (My x Lx); inverse Y (this CTA's iy rows x Lx)
+  const int iz = blockIdx.x / E, e = blockIdx.x - iz * E, part = blockIdx.y;
+  const c64* t1 = kInverse ? twy : twx;
+  const c64* t2 = kInverse ? twx : twy;
+  for (int k = threadIdx.x; k < r1 * c1; k += blockDim.x) {
+    const int q = k / c1, j = k - q * c1;
+    c64 w = t1[(j * q) % L1];
+    if (kInverse) w.y = -w.y;
+    A1[q * p1 + j] = w;
+  }
+  for (int k = threadIdx.x; k < r2 * c2; k += blockDim.x) {
+    const int q = k / c2, j = k - q * c2;
+    c64 w = t2[(j * q) % L2];
+    if (kInverse) w.y = -w.y;
+    A2[q * p2 + j] = w;
+  }
+  const long long plane_in = static_cast<long long>(iz) * rows_in * cols_in;
+  for (int k = threadIdx.x; k < rows_in * cols_in; k += blockDim.x) a[k] = in[(plane_in + k) * E + e];
+  const int split_n = kInverse ? My : Ly;
+  const int s0 = static_cast<int>(static_cast<long long>(split_n) * part / parts);
+  const int s1 = static_cast<int>(static_cast<long long>(split_n) * (part + 1) / parts);
+  __syncthreads();
+
+  // two outputs sharing the inputs: sum_j w0[j] src[j * stride], sum_j w1[j] src[j * stride]
+  auto dot2 = [&](const c64* src, int stride, int n, const c64* w0, const c64* w1, c64& o0, c64& o1) {
+    c64 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0), b0 = cmk(0.0, 0.0), b1 = cmk(0.0, 0.0);
+    int j = 0;
+    for (; j + 2 <= n; j += 2) {
+      const c64 v0 = src[j * stride], v1 = src[(j + 1) * stride];
+      const c64 x0 = w0[j], x1 = w0[j + 1], y0 = w1[j], y1 = w1[j + 1];
+      a0 = cfma(x0, v0, a0);
+      a1 = cfma(x1, v1, a1);
+      b0 = cfma(y0, v0, b0);
+      b1 = cfma(y1, v1, b1);
+    }
+    if (j < n) {
+      const c64 v = src[j * stride];
+      a0 = cfma(w0[j], v, a0);
+      b0 = cfma(w1[j], v, b0);
+    }
+    o0 = cadd(a0, a1);
+    o1 = cadd(b0, b1);
+  };
+
+  if (!kInverse) {
+    // X[iy][qx], qx in pairs (qx, qx + Lx/2 rounded up)
+    const int h1 = (Lx + 1) / 2;
+    for (int o = threadIdx.x; o < My * h1; o += blockDim.x) {
+      const int iy = o / h1, qa = o - iy * h1, qb = qa + h1;
+      c64 xa, xb;
+      dot2(a + iy * Mx, 1, Mx, A1 + qa * p1, A1 + (qb < Lx ? qb : qa) * p1, xa, xb);
+      mid[iy * Lx + qa] = xa;
+      if (qb < Lx) mid[iy * Lx + qb] = xb;
+    }
+    __syncthreads();
+    // out[qy][qx], qy in pairs within [s0, s1)
+    const int n_q = s1 - s0, h2 = (n_q + 1) / 2;
+    for (int o = threadIdx.x; o < h2 * Lx; o += blockDim.x) {
+      const int k = o / Lx, qx = o - k * Lx;
+      const int qa = s0 + k, qb = qa + h2;
+      c64 ya, yb;
+      dot2(mid + qx, Lx, My, A2 + qa * p2, A2 + (qb < s1 ? qb : qa) * p2, ya, yb);
+      out[((static_cast<long long>(iz) * Ly + qa) * Lx + qx) * E + e] = ya;
+      if (qb < s1) out[((static_cast<long long>(iz) * Ly + qb) * Lx + qx) * E + e] = yb;
+    }
+  } else {
+    // Y[iy][qx] for iy in [s0, s1), in pairs
+    const int n_i = s1 - s0, h1 = (n_i + 1) / 2;
+    for (int o = threadIdx.x; o < h1 * Lx; o += blockDim.x) {
+      const int k = o / Lx, qx = o - k * Lx;
+      const int ia = s0 + k, ib = ia + h1;
+      c64 ya, yb;
+      dot2(a + qx, Lx, Ly, A1 + ia * p1, A1 + (ib < s1 ? ib : ia) * p1, ya, yb);
+      mid[(ia - s0) * Lx + qx] = ya;
+      if (ib < s1) mid[(ib - s0) * Lx + qx] = yb;
+    }
+    __syncthreads();
+    // out[iy][ix], ix in pairs
+    const int h2 = (Mx + 1) / 2;
+    for (int o = threadIdx.x; o < n_i * h2; o += blockDim.x) {
+      const int r = o / h2, xa = o - r * h2, xb = xa + h2;
+      c64 va, vb;
+      dot2(mid + r * Lx, 1, Lx, A2 + xa * p2, A2 + (xb < Mx ? xb : xa) * p2, va, vb);
+      out[((static_cast<long long>(iz) * My + s0 + r) * Mx + xa) * E + e] = cscale(va, scale);
+      if (xb < Mx) out[((static_cast<long long>(iz) * My + s0 + r) * Mx + xb) * E + e] = cscale(vb, scale);
+    }
   }
 }
 
@@ -134,6 +257,55 @@ p2m_kernel(const c64* __restrict__ v0t, const c64* __restrict__ x, c64* __restri
       t.y += __shfl_xor_sync(0xffffffffu, t.y, off);
     }
     if (lane == 0 && u < nc) mom[static_cast<long long>(cr) * b + c0 + 8 * u] = t;
+  }
+}
+
+// Long lines with few outputs (e.g. the 256 -> 512 line of a 1 x 256 lattice):
+// one warp per output (a, qo, inner); lane l sums the terms j = l, l + 32, ...
+// then a fixed shuffle tree combines the lanes (deterministic).
+__global__ void __launch_bounds__(256)
+dft_axis_warp_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ tw, long long n_a,
+                     int n_in, int n_out, long long n_inner, int L, int backward, double scale) {
+  const long long total = n_a * n_out * n_inner;
+  const int lane = threadIdx.x & 31;
+  for (long long g = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; g < total;
+       g += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const long long inner = g % n_inner;
+    const long long rest = g / n_inner;
+    const int qo = static_cast<int>(rest % n_out);
+    const long long a = rest / n_out;
+    const c64* src = in + (a * n_in) * n_inner + inner;
+    const int step = static_cast<int>((32LL * qo) % L);
+    int idx = static_cast<int>((static_cast<long long>(lane) * qo) % L);
+    c64 acc0 = cmk(0.0, 0.0), acc1 = cmk(0.0, 0.0);
+    int j = lane;
+    for (; j + 32 < n_in; j += 64) {
+      c64 w0 = __ldg(tw + idx);
+      int idx1 = idx + step;
+      if (idx1 >= L) idx1 -= L;
+      c64 w1 = __ldg(tw + idx1);
+      const c64 v0 = src[static_cast<long long>(j) * n_inner], v1 = src[static_cast<long long>(j + 32) * n_inner];
+      if (backward) {
+        w0.y = -w0.y;
+        w1.y = -w1.y;
+      }
+      acc0 = cfma(w0, v0, acc0);
+      acc1 = cfma(w1, v1, acc1);
+      idx = idx1 + step;
+      if (idx >= L) idx -= L;
+    }
+    if (j < n_in) {
+      c64 w = __ldg(tw + idx);
+      if (backward) w.y = -w.y;
+      acc0 = cfma(w, src[static_cast<long long>(j) * n_inner], acc0);
+    }
+    c64 t = cadd(acc0, acc1);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      t.x += __shfl_xor_sync(0xffffffffu, t.x, off);
+      t.y += __shfl_xor_sync(0xffffffffu, t.y, off);
+    }
+    if (lane == 0) out[(a * n_out + qo) * n_inner + inner] = cscale(t, scale);
   }
 }
 
@@ -606,6 +778,14 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
   if (n_a * n_out * n_inner == 0) return cudaSuccess;
   // widest output group that still gives >= 2 x 256 threads per SM
   const long long want = 2LL * kNumSMs * 256;
+  if (n_in >= 64 && n_a * n_out * n_inner < want) {  // long lines, few outputs: a warp per output
+    const long long warps = n_a * n_out * n_inner;
+    long long blocks = (warps * 32 + 255) / 256;
+    if (blocks > 16LL * kNumSMs) blocks = 16LL * kNumSMs;
+    dft_axis_warp_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L,
+                                                                       backward ? 1 : 0, scale);
+    return cudaGetLastError();
+  }
   int qg = 8;
   while (qg > 1 && n_a * ((n_out + qg - 1) / qg) * n_inner < want) qg /= 2;
   const long long total = n_a * ((n_out + qg - 1) / qg) * n_inner;
@@ -628,6 +808,40 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     case 2: dft_axis_kernel<2><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
     default: dft_axis_kernel<1><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
   }
+  return cudaGetLastError();
+}
+
+size_t xy_plane_smem(int Mx, int My, int Lx, int Ly, bool inverse) {
+  const size_t r1 = inverse ? My : Lx, c1 = inverse ? Ly : Mx, r2 = inverse ? Mx : Ly, c2 = inverse ? Lx : My;
+  const size_t plane = inverse ? static_cast<size_t>(Ly) * Lx : static_cast<size_t>(My) * Mx;
+  const size_t c = r1 * (c1 | 1) + r2 * (c2 | 1) + plane + static_cast<size_t>(My) * Lx;
+  return c * sizeof(c64);
+}
+
+cudaError_t launch_xy_plane(const c64* in, c64* out, const c64* twx, const c64* twy, int Mx, int My, int Lx, int Ly,
+                            int Mz, int E, bool inverse, double scale, cudaStream_t stream) {
+  const size_t smem = xy_plane_smem(Mx, My, Lx, Ly, inverse);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static size_t raised[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > raised[inverse]) {
+    cudaError_t e = cudaFuncSetAttribute(inverse ? xy_plane_kernel<true> : xy_plane_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    raised[inverse] = smem;
+  }
+  const long long planes = static_cast<long long>(Mz) * E;
+  if (planes > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int split_n = inverse ? My : Ly;
+  long long parts = (2LL * kNumSMs + planes - 1) / planes;  // fill >= 2 CTAs per SM
+  if (parts > split_n) parts = split_n;
+  if (parts < 1) parts = 1;
+  const dim3 grid(static_cast<unsigned>(planes), static_cast<unsigned>(parts));
+  if (inverse)
+    xy_plane_kernel<true><<<grid, 256, smem, stream>>>(in, out, twx, twy, Mx, My, Lx, Ly, E, static_cast<int>(parts),
+                                                       scale);
+  else
+    xy_plane_kernel<false><<<grid, 256, smem, stream>>>(in, out, twx, twy, Mx, My, Lx, Ly, E, static_cast<int>(parts),
+                                                        scale);
   return cudaGetLastError();
 }
 
