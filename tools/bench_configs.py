@@ -100,7 +100,9 @@ def run_config(cid, args, out):
     lam_bytes = 16.0 * q * 625
     rec["m2l_lambda_gb_per_s"] = lam_bytes / (st["m2l"] * 1e-3) / 1e9
     rec["m2l_frac_of_hbm_lambda_only"] = lam_bytes / (st["m2l"] * 1e-3) / HBM
-    rec["kernel_launches_per_apply"] = op.kernel_launches()
+    k0 = op.kernel_launches()
+    op.matvec(x)
+    rec["kernel_launches_per_apply"] = op.kernel_launches() - k0
     out.write(json.dumps(rec) + "\n")
     out.flush()
     print(json.dumps(rec), flush=True)
