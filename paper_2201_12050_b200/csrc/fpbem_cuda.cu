@@ -284,50 +284,57 @@ void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fp
                     bool blocks_on_device, const fpbem_c64* prebuilt, c64** out) {
   const int b2 = op->b * op->b;
   const size_t total = static_cast<size_t>(op->q_total) * b2;
-  c64* lam = dalloc<c64>(total, "spectrum");
-  *out = lam;
-  if (prebuilt) {
-    h2d(lam, prebuilt, total * sizeof(c64), op->stream, "spectrum upload");
-    return;
-  }
-  c64* tmp = dalloc<c64>(total, "spectrum scratch");
-  const c64* blocks = reinterpret_cast<const c64*>(far_blocks);  // device bank (fpbem_cu_m2l_bank)
-  c64* staged = nullptr;
-  if (!blocks_on_device) {
-    staged = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
-    if (n_far > 0)
-      h2d(staged, far_blocks, static_cast<size_t>(n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
-    blocks = staged;
-  }
-  int* offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
-  if (n_far > 0)
-    h2d(offs, far_offsets, static_cast<size_t>(n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
-  check(cudaMemsetAsync(lam, 0, total * sizeof(c64), op->stream), "spectrum clear");
-  check(launch_scatter_bank(blocks, offs, n_far, b2, op->L[0], op->L[1], op->L[2], lam, op->stream), "scatter bank");
-  c64* cur = lam;
-  c64* nxt = tmp;
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
-  if (Lx > 1) {
-    check(launch_dft_axis(cur, nxt, op->tw[0], Ly * Lz, op->L[0], op->L[0], b2, op->L[0], false, 1.0, op->stream),
-          "spectrum dft x");
-    std::swap(cur, nxt);
+  c64* work = dalloc<c64>(total, "spectrum");
+  c64* cur = work;
+  c64* tmp = nullptr;
+  int* offs = nullptr;
+  c64* staged = nullptr;
+  if (prebuilt) {
+    h2d(work, prebuilt, total * sizeof(c64), op->stream, "spectrum upload");
+  } else {
+    tmp = dalloc<c64>(total, "spectrum scratch");
+    const c64* blocks = reinterpret_cast<const c64*>(far_blocks);  // device bank (fpbem_cu_m2l_bank)
+    if (!blocks_on_device) {
+      staged = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
+      if (n_far > 0)
+        h2d(staged, far_blocks, static_cast<size_t>(n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
+      blocks = staged;
+    }
+    offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
+    if (n_far > 0)
+      h2d(offs, far_offsets, static_cast<size_t>(n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
+    check(cudaMemsetAsync(work, 0, total * sizeof(c64), op->stream), "spectrum clear");
+    check(launch_scatter_bank(blocks, offs, n_far, b2, op->L[0], op->L[1], op->L[2], work, op->stream),
+          "scatter bank");
+    c64* nxt = tmp;
+    if (Lx > 1) {
+      check(launch_dft_axis(cur, nxt, op->tw[0], Ly * Lz, op->L[0], op->L[0], b2, op->L[0], false, 1.0, op->stream),
+            "spectrum dft x");
+      std::swap(cur, nxt);
+    }
+    if (Ly > 1) {
+      check(launch_dft_axis(cur, nxt, op->tw[1], Lz, op->L[1], op->L[1], Lx * b2, op->L[1], false, 1.0, op->stream),
+            "spectrum dft y");
+      std::swap(cur, nxt);
+    }
+    if (Lz > 1) {
+      check(launch_dft_axis(cur, nxt, op->tw[2], 1, op->L[2], op->L[2], Lx * Ly * b2, op->L[2], false, 1.0,
+                            op->stream),
+            "spectrum dft z");
+      std::swap(cur, nxt);
+    }
   }
-  if (Ly > 1) {
-    check(launch_dft_axis(cur, nxt, op->tw[1], Lz, op->L[1], op->L[1], Lx * b2, op->L[1], false, 1.0, op->stream),
-          "spectrum dft y");
-    std::swap(cur, nxt);
-  }
-  if (Lz > 1) {
-    check(launch_dft_axis(cur, nxt, op->tw[2], 1, op->L[2], op->L[2], Lx * Ly * b2, op->L[2], false, 1.0, op->stream),
-          "spectrum dft z");
-    std::swap(cur, nxt);
-  }
-  if (cur != lam)
-    check(cudaMemcpyAsync(lam, cur, total * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "spectrum copy");
   check(cudaStreamSynchronize(op->stream), "spectrum build");
-  cudaFree(tmp);
+  if (cur == work) {
+    if (tmp) cudaFree(tmp);
+    *out = work;
+  } else {
+    cudaFree(work);
+    *out = tmp;
+  }
   if (staged) cudaFree(staged);
-  cudaFree(offs);
+  if (offs) cudaFree(offs);
 }
 
 void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {

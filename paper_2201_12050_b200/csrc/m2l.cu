@@ -21,6 +21,8 @@ namespace fpbem_cu {
 
 namespace {
 
+
+
 // out[a][qo][bi][e] = scale * sum_{j < n_in} tw[(j*qo*sign) mod L] * in[a][j][bi][e]
 // with tw[k] = exp(-2 pi i k / L); sign = +1 forward, -1 backward (conjugate).
 // One thread owns kQG consecutive outputs qo of one (a, inner) column, so each
@@ -328,35 +330,7 @@ __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* _
   }
 }
 
-// Last-axis fusion: forward DFT along z (Mz nonzero inputs -> Lz modes), the
-// per-mode product with Λ_q, and the pruned inverse along z (Lz modes -> Mz
-// kept outputs) for one (qy, qx) column at a time; the z-extended field never
-// touches HBM. Persistent, one CTA per SM walking columns blockIdx.x,
-// +gridDim.x, ..., warp-specialised:
-//   warp 0 (lane 0) produces: Λ (the only large operand, read exactly once)
-//     streams through a ring of `ring` mode blocks (each b x b block is
-//     contiguous: one cp.async.bulk per mode, landing on full[slot]); a slot is
-//     refilled as soon as its consumer releases it (empty[slot]), so the stream
-//     runs on across column boundaries. Input columns (Mz rows of E contiguous
-//     values) arrive the same way in kInBufs rotating buffers.
-//   warps 1..n_cons consume (ring = 2 n_cons, or n_cons when the ring is
-//     short): consumer warp w owns slots w and w + n_cons and takes the modes
-//     g = w (mod n_cons), so consecutive modes of a warp alternate between its
-//     two slots (one refill in flight while it computes on the other) and a
-//     warp never waits more than one phase ahead on a slot; forward DFT and
-//     inverse DFT are shared by all consumer warps between named barriers.
-// Measured: this producer/consumer split streams at HBM speed with one CTA
-// per SM, where barrier-separated refill rounds reached only ~55% of it
-// (tools/bulk_stream_bench.cu).
-//   in  : F2[iz][plane][E]   (iz < Mz)      out: H2[iz][plane][E] (iz < Mz)
-//   E = nrhs * b fields, plane = Ly * Lx columns, lambda[q][b*b], q = qz*plane + column
-constexpr int kMaxRing = 16;
-constexpr int kInBufs = 3;
 constexpr size_t kZfSmemMax = 225 * 1024;  // dynamic; static barriers + driver share take the rest
-
-__device__ __forceinline__ void consumer_sync(int n_threads) {
-  asm volatile("bar.sync 1, %0;\n" ::"r"(n_threads) : "memory");
-}
 
 // One z-DFT phase of the fused kernel, over the consumer threads:
 //   dst[o][f] = scale * sum_{j < n_in} w(j*o mod L) src[j][f],  o < n_out
@@ -456,116 +430,17 @@ __device__ __forceinline__ void mode_product_warp(const c64* __restrict__ lam_bl
   }
 }
 
-__global__ void __launch_bounds__(32 * (kMaxRing + 1))
-m2l_zfused_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
-                  const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, int ring,
-                  int n_cons, double scale) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int b2 = b * b;
-  c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
-  c64* f_in0 = ring_buf + ring * b2;                  // kInBufs x Mz x E
-  c64* f_z = f_in0 + kInBufs * Mz * E;                // Lz x E  (forward along z)
-  c64* g_z = f_z + Lz * E;                            // Lz x E  (after the mode product)
-  c64* tw_s = g_z + Lz * E;                           // Lz twiddles exp(-2 pi i k / Lz)
-  __shared__ __align__(8) unsigned long long full[kMaxRing], empty[kMaxRing];
-  __shared__ __align__(8) unsigned long long in_full[kInBufs], in_empty[kInBufs];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_cols = static_cast<int>((plane - blockIdx.x + gridDim.x - 1) / gridDim.x);  // this CTA's columns
-  if (tid == 0) {
-    for (int s = 0; s < ring; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-    }
-    for (int s = 0; s < kInBufs; ++s) {
-      mbar_init(smem_u32(&in_full[s]), 1);
-      mbar_init(smem_u32(&in_empty[s]), 1);
-    }
-    mbar_fence_init();
-  }
-  for (int k = tid; k < Lz; k += blockDim.x) tw_s[k] = tw[k];
-  __syncthreads();
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---- producer
-      const unsigned lam_bytes = static_cast<unsigned>(b2 * sizeof(c64));
-      const unsigned row_bytes = static_cast<unsigned>(E * sizeof(c64));
-      auto issue_input = [&](int k) {
-        if (k >= n_cols) return;
-        const int buf = k % kInBufs;
-        if (k >= kInBufs) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / kInBufs - 1) & 1));
-        const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
-        const unsigned bar = smem_u32(&in_full[buf]);
-        c64* dst = f_in0 + buf * Mz * E;
-        mbar_arrive_expect_tx(bar, row_bytes * Mz);
-        for (int iz = 0; iz < Mz; ++iz) bulk_g2s(smem_u32(dst + iz * E), in + (iz * plane + col) * E, row_bytes, bar);
-      };
-      issue_input(0);
-      int slot = 0;
-      unsigned phase = 0;  // phase of the ring pass being filled
-      long long g = 0;     // global mode counter
-      const c64* col_lam = lambda + static_cast<long long>(blockIdx.x) * b2;
-      const long long col_step = static_cast<long long>(gridDim.x) * b2, mode_step = plane * b2;
-      for (int k = 0; k < n_cols; ++k, col_lam += col_step) {
-        issue_input(k + 1);
-        for (int qz = 0; qz < Lz; ++qz, ++g) {
-          if (g >= ring) mbar_wait(smem_u32(&empty[slot]), phase ^ 1u);
-          const unsigned bar = smem_u32(&full[slot]);
-          mbar_arrive_expect_tx(bar, lam_bytes);
-          bulk_g2s(smem_u32(ring_buf + slot * b2), col_lam + qz * mode_step, lam_bytes, bar);
-          if (++slot == ring) {
-            slot = 0;
-            phase ^= 1u;
-          }
-        }
-      }
-    }
-  } else {  // ---- consumers
-    const int cw = warp - 1, ct = tid - 32, n_ct = n_cons * 32;
-    for (int k = 0; k < n_cols; ++k) {
-      const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
-      const int buf = k % kInBufs;
-      const c64* f_in = f_in0 + buf * Mz * E;
-      mbar_wait(smem_u32(&in_full[buf]), static_cast<unsigned>((k / kInBufs) & 1));
-      // forward along z: f_z[qz][f] = sum_iz tw[iz*qz mod Lz] f_in[iz][f]
-      {
-        const int G = zdft_group(Lz * E, n_ct);
-        if (G == 4) zdft<4, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, ct, n_ct, 1.0, nullptr, 0, 0);
-        else if (G == 2) zdft<2, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, ct, n_ct, 1.0, nullptr, 0, 0);
-        else zdft<1, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, ct, n_ct, 1.0, nullptr, 0, 0);
-      }
-      consumer_sync(n_ct);  // f_z complete, input buffer released
-      if (ct == 0) mbar_arrive(smem_u32(&in_empty[buf]));
-      // this warp's modes of column k: global g = k*Lz + qz with g % n_cons == cw
-      const long long g_first = static_cast<long long>(k) * Lz;
-      int qz = static_cast<int>(((cw - g_first) % n_cons + n_cons) % n_cons);
-      for (; qz < Lz; qz += n_cons) {
-        const long long g = g_first + qz;
-        const int slot = static_cast<int>(g % ring);
-        mbar_wait(smem_u32(&full[slot]), static_cast<unsigned>((g / ring) & 1));
-        // g[qz][r*b + i] = sum_c Λ_q[i + b c] f[qz][r*b + c]
-        mode_product_warp(ring_buf + slot * b2, f_z + qz * E, g_z + qz * E, E, b, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
-      }
-      consumer_sync(n_ct);  // g_z complete
-      // inverse along z, kept outputs only: out[iz][f] = scale sum_qz conj(tw[iz*qz mod Lz]) g_z[qz][f]
-      {
-        const int G = zdft_group(Mz * E, n_ct);
-        if (G == 4) zdft<4, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, ct, n_ct, scale, out, plane, col);
-        else if (G == 2) zdft<2, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, ct, n_ct, scale, out, plane, col);
-        else zdft<1, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, ct, n_ct, scale, out, plane, col);
-      }
-      // the next column's forward pass writes f_z only (no reader left after
-      // the barrier above); its mode products write g_z only after the next
-      // barrier, which every thread reaches after finishing this inverse pass
-    }
-  }
-  __syncthreads();  // the producer stays resident until every copy it issued has landed
-}
-
-// Three-role variant of the fused z kernel (same math, same layouts): the
-// z-DFTs move off the streaming warps so the Λ stream never waits on them.
-//   warp 0 lane 0      producer (Λ ring + input columns), as above
+// Last-axis fusion: forward DFT along z (Mz nonzero inputs -> Lz modes), the
+// per-mode product with Λ_q, and the pruned inverse along z (Lz modes -> Mz
+// kept outputs) per (qy, qx) column; the z-extended field never touches HBM.
+// Persistent (one CTA per SM walking columns blockIdx.x + k gridDim.x) and
+// warp-specialised in three roles, so the Λ stream (the only large operand,
+// read exactly once) never waits on a DFT phase:
+//   warp 0 lane 0      producer: each mode's b x b Λ block (contiguous) with one
+//                      cp.async.bulk into a ring of `ring` shared-memory slots
+//                      (full / empty mbarriers), refilled as soon as a slot is
+//                      released, running on across columns; input columns (Mz
+//                      rows of E contiguous values) the same way, double-buffered
 //   n_mw mode warps    stream column after column: warp w owns ring slots w and
 //                      w + n_mw and takes the modes g = w (mod n_mw); reads
 //                      f_z[k%2], writes g_z[k%2]
@@ -577,8 +452,15 @@ m2l_zfused_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* 
 //                                g_z complete, f_z free again
 //   inv_done[c%2]  DFT -> mode   inverse of column c read g_z   (count 1)
 // While the mode warps stream column k, the DFT warps compute column k+1's
-// forward pass and column k-1's inverse.
+// forward pass and column k-1's inverse. A warp owning fixed ring slots never
+// waits more than one phase ahead on a slot.
+//   in  : F2[iz][plane][E]   (iz < Mz)      out: H2[iz][plane][E] (iz < Mz)
+//   E = nrhs * b fields, plane = Ly * Lx columns, lambda[q][b*b], q = qz*plane + column
+// Measured route (profiles/r01_m2l_probes.md): producer/consumer mbarriers
+// instead of barrier-separated refills (3.5 -> 6.7 TB/s in the probe) and the
+// z-DFTs on their own warps.
 constexpr int kPipeMaxModeWarps = 8;
+constexpr int kPipeInBufs = 2;  // input columns in flight (double buffer)
 constexpr int kPipeMaxRing = 16;
 constexpr int kPipeMaxDftWarps = 8;
 
@@ -593,12 +475,12 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b2 = b * b;
   c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
-  c64* f_in0 = ring_buf + ring * b2;                  // kInBufs x Mz x E
-  c64* f_z0 = f_in0 + kInBufs * Mz * E;               // 2 x Lz x E
+  c64* f_in0 = ring_buf + ring * b2;                  // kPipeInBufs x Mz x E
+  c64* f_z0 = f_in0 + kPipeInBufs * Mz * E;               // 2 x Lz x E
   c64* g_z0 = f_z0 + 2 * Lz * E;                      // 2 x Lz x E
   c64* tw_s = g_z0 + 2 * Lz * E;                      // Lz twiddles
   __shared__ __align__(8) unsigned long long full[kPipeMaxRing], empty[kPipeMaxRing];
-  __shared__ __align__(8) unsigned long long in_full[kInBufs], in_empty[kInBufs];
+  __shared__ __align__(8) unsigned long long in_full[kPipeInBufs], in_empty[kPipeInBufs];
   __shared__ __align__(8) unsigned long long fwd_done[2], col_done[2], inv_done[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_cols = static_cast<int>((plane - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -607,7 +489,7 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    for (int s = 0; s < kInBufs; ++s) {
+    for (int s = 0; s < kPipeInBufs; ++s) {
       mbar_init(smem_u32(&in_full[s]), 1);
       mbar_init(smem_u32(&in_empty[s]), 1);
     }
@@ -627,8 +509,8 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
       const unsigned row_bytes = static_cast<unsigned>(E * sizeof(c64));
       auto issue_input = [&](int k) {
         if (k >= n_cols) return;
-        const int buf = k % kInBufs;
-        if (k >= kInBufs) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / kInBufs - 1) & 1));
+        const int buf = k % kPipeInBufs;
+        if (k >= kPipeInBufs) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / kPipeInBufs - 1) & 1));
         const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
         const unsigned bar = smem_u32(&in_full[buf]);
         c64* dst = f_in0 + buf * Mz * E;
@@ -636,14 +518,14 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
         for (int iz = 0; iz < Mz; ++iz) bulk_g2s(smem_u32(dst + iz * E), in + (iz * plane + col) * E, row_bytes, bar);
       };
       issue_input(0);
-      issue_input(1);
+      issue_input(1);  // then column k + 1's input after column k's first Λ blocks
       int slot = 0;
       unsigned phase = 0;
       long long g = 0;
       const c64* col_lam = lambda + static_cast<long long>(blockIdx.x) * b2;
       const long long col_step = static_cast<long long>(gridDim.x) * b2, mode_step = plane * b2;
       for (int k = 0; k < n_cols; ++k, col_lam += col_step) {
-        issue_input(k + 2);
+        if (k > 0) issue_input(k + 1);  // buffer of column k - 1: its forward pass is done by now
         for (int qz = 0; qz < Lz; ++qz, ++g) {
           if (g >= ring) mbar_wait(smem_u32(&empty[slot]), phase ^ 1u);
           const unsigned bar = smem_u32(&full[slot]);
@@ -702,10 +584,10 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
       if (dt == 0) mbar_arrive(smem_u32(&inv_done[buf]));
     };
     for (int k = 0; k < n_cols; ++k) {
-      const int buf = k & 1, ib = k % kInBufs;
+      const int buf = k & 1, ib = k % kPipeInBufs;
       // f_z[buf] was last read by the modes of column k-2, whose col_done the
       // inverse of column k-2 (previous iteration's tail) already waited for
-      mbar_wait(smem_u32(&in_full[ib]), static_cast<unsigned>((k / kInBufs) & 1));
+      mbar_wait(smem_u32(&in_full[ib]), static_cast<unsigned>((k / kPipeInBufs) & 1));
       c64* f_z = f_z0 + buf * Lz * E;
       const c64* f_in = f_in0 + ib * Mz * E;
       const int G = zdft_group(Lz * E, n_dt);
@@ -878,41 +760,8 @@ cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream)
 }
 
 namespace {
-size_t zfused_fields_bytes(int Mz, int Lz, int E) {
-  return sizeof(c64) * (static_cast<size_t>(kInBufs * Mz + 2 * Lz) * E + Lz);
-}
-}  // namespace
-
-namespace {
-int zfused_ring_for(int Mz, int Lz, int E, int b, int ctas);
-
-// CTAs per SM: two when a whole column's modes fit the smaller ring (then the
-// two CTAs' DFT phases and streams interleave), else one with the deeper ring
-// (measured: cfg5 Lz = 7 prefers two, cfg3 Lz = 32 one). FPBEM_ZF_CTAS=1|2 overrides.
-int zfused_ctas_per_sm(int Mz, int Lz, int E, int b) {
-  static const int forced = [] {
-    const char* s = std::getenv("FPBEM_ZF_CTAS");
-    return s ? std::atoi(s) : 0;
-  }();
-  if (forced == 1 || forced == 2) return forced;
-  const int r2 = zfused_ring_for(Mz, Lz, E, b, 2);
-  return (r2 >= 4 && r2 >= Lz) ? 2 : 1;
-}
-
-int zfused_ring_for(int Mz, int Lz, int E, int b, int ctas) {
-  const size_t budget = kZfSmemMax / ctas - (ctas > 1 ? 2048 : 0);
-  const size_t fields = zfused_fields_bytes(Mz, Lz, E);
-  const size_t per_mode = sizeof(c64) * static_cast<size_t>(b) * b;
-  if (fields >= budget) return 0;
-  long long r = static_cast<long long>((budget - fields) / per_mode);
-  if (r > kMaxRing) r = kMaxRing;
-  return r >= 4 ? static_cast<int>(r) : 0;
-}
-}  // namespace
-
-namespace {
 size_t zpipe_fields_bytes(int Mz, int Lz, int E) {
-  return sizeof(c64) * (static_cast<size_t>(kInBufs * Mz + 4 * Lz) * E + Lz);
+  return sizeof(c64) * (static_cast<size_t>(kPipeInBufs * Mz + 4 * Lz) * E + Lz);
 }
 int zpipe_max_ring(int Mz, int Lz, int E, int b) {
   const size_t fields = zpipe_fields_bytes(Mz, Lz, E), per_mode = sizeof(c64) * static_cast<size_t>(b) * b;
@@ -921,7 +770,7 @@ int zpipe_max_ring(int Mz, int Lz, int E, int b) {
   return static_cast<int>(r > kPipeMaxRing ? kPipeMaxRing : r);
 }
 // mode warps: FPBEM_ZF_MW (default 7); ring = the largest multiple of it that
-// fits, at least two slots per warp (0: the pipelined kernel does not fit)
+// fits, at least two slots per warp (0: the fused kernel does not fit)
 int zpipe_mode_warps(int Mz, int Lz, int E, int b) {
   static const int want = [] {
     const char* s = std::getenv("FPBEM_ZF_MW");
@@ -933,66 +782,29 @@ int zpipe_mode_warps(int Mz, int Lz, int E, int b) {
     if (r >= 2 * w) return w;
   return 0;
 }
-int zpipe_ring(int Mz, int Lz, int E, int b) {
-  const int w = zpipe_mode_warps(Mz, Lz, E, b);
-  return w ? (zpipe_max_ring(Mz, Lz, E, b) / w) * w : 0;
-}
 }  // namespace
 
 int m2l_zfused_ring(int Mz, int Lz, int E, int b) {
-  if (zpipe_mode_warps(Mz, Lz, E, b) > 0) return zpipe_ring(Mz, Lz, E, b);
-  const int r = zfused_ring_for(Mz, Lz, E, b, zfused_ctas_per_sm(Mz, Lz, E, b));
-  return r > 0 ? r : zfused_ring_for(Mz, Lz, E, b, 1);
+  const int w = zpipe_mode_warps(Mz, Lz, E, b);
+  return w ? (zpipe_max_ring(Mz, Lz, E, b) / w) * w : 0;
 }
-
 
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
                               long long plane, int E, int b, double scale, cudaStream_t stream) {
-  // three-role pipelined kernel unless FPBEM_ZF=2 (or it does not fit)
-  static const bool use_pipe = [] {
-    const char* s = std::getenv("FPBEM_ZF");
-    return !(s && s[0] == '2');
-  }();
-  const int n_mw = use_pipe ? zpipe_mode_warps(Mz, Lz, E, b) : 0;
-  if (n_mw > 0) {
-    const int ring = zpipe_ring(Mz, Lz, E, b);
-    const size_t smem = zpipe_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
-    static size_t configured_pipe = 0;
-    if (smem > 48 * 1024 && smem > configured_pipe) {
-      cudaError_t e = cudaFuncSetAttribute(m2l_zpipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      configured_pipe = smem;
-    }
-    const long long grid = plane < kNumSMs ? plane : kNumSMs;
-    const int n_dw = kPipeMaxDftWarps;
-    m2l_zpipe_kernel<<<static_cast<unsigned>(grid), 32 * (1 + n_mw + n_dw), smem, stream>>>(
-        in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, n_dw, scale);
-    return cudaGetLastError();
-  }
-  int ctas = zfused_ctas_per_sm(Mz, Lz, E, b);
-  int ring = zfused_ring_for(Mz, Lz, E, b, ctas);
-  if (ring == 0) {
-    ctas = 1;
-    ring = zfused_ring_for(Mz, Lz, E, b, 1);
-  }
-  if (ring == 0) return cudaErrorInvalidValue;
-  // two slots per consumer warp when the ring is deep enough
-  const bool two = ring >= 8;
-  const int n_cons = two ? ring / 2 : ring;
-  ring = two ? 2 * n_cons : ring;
-  const size_t smem = zfused_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
+  const int n_mw = zpipe_mode_warps(Mz, Lz, E, b);
+  if (n_mw == 0) return cudaErrorInvalidValue;
+  const int ring = m2l_zfused_ring(Mz, Lz, E, b);
+  const size_t smem = zpipe_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(m2l_zfused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(m2l_zpipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  const long long slots = static_cast<long long>(kNumSMs) * ctas;
-  const long long grid = plane < slots ? plane : slots;
-  m2l_zfused_kernel<<<static_cast<unsigned>(grid), 32 * (n_cons + 1), smem, stream>>>(
-      in, out, lambda, tw, Mz, Lz, plane, E, b, ring, n_cons, scale);
+  const long long grid = plane < kNumSMs ? plane : kNumSMs;  // persistent: one CTA per SM
+  m2l_zpipe_kernel<<<static_cast<unsigned>(grid), 32 * (1 + n_mw + kPipeMaxDftWarps), smem, stream>>>(
+      in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, kPipeMaxDftWarps, scale);
   return cudaGetLastError();
 }
 

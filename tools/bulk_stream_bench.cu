@@ -1,6 +1,6 @@
 // Streaming-bandwidth probe for the M2L Λ stream: every CTA pulls chunks of
 // `chunk` bytes through a `ring`-deep shared-memory ring with cp.async.bulk +
-// mbarrier (the m2l_zfused_kernel pattern), touching one value per chunk so
+// mbarrier (the m2l_zpipe_kernel pattern), touching one value per chunk so
 // the copies cannot be elided. Also an LDG.128 grid-stride reference.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/bsb tools/bulk_stream_bench.cu
 #include <cstdio>
@@ -76,7 +76,8 @@ __device__ bool wait_bounded(unsigned bar, unsigned par, int who, unsigned i) {
 
 // warp-specialised: warp 0 lane 0 produces (waits `empty`, issues), the
 // other warps consume modes round-robin and release each slot on `empty`
-__global__ void bulk_ws(const char* __restrict__ src, unsigned n_chunks, int chunk, int ring, double* sink) {
+__global__ void bulk_ws(const char* __restrict__ src, unsigned n_chunks, int chunk, int ring, double* sink,
+                        int work = 0, int lz = 0) {
   extern __shared__ __align__(128) char buf[];
   __shared__ __align__(8) unsigned long long full[32], empty[32];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, n_cons = blockDim.x / 32 - 1;
@@ -89,6 +90,16 @@ __global__ void bulk_ws(const char* __restrict__ src, unsigned n_chunks, int chu
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
+  // lz > 0: the m2l_zpipe_kernel order — this CTA's columns b, b + grid, ..., each column's lz modes at a
+  // stride of plane = n_chunks / lz chunks; else CTA-interleaved consecutive chunks
+  auto chunk_index = [&](unsigned i) -> size_t {
+    if (lz == 0) return (size_t)blockIdx.x + (size_t)i * gridDim.x;
+    const int l = lz > 0 ? lz : -lz;
+    const size_t col = blockIdx.x + (size_t)(i / l) * gridDim.x;
+    if (lz < 0) return col * l + i % l;  // column-contiguous layout [column][qz]
+    const size_t plane = n_chunks / l;
+    return (size_t)(i % l) * plane + col;
+  };
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
@@ -100,7 +111,7 @@ __global__ void bulk_ws(const char* __restrict__ src, unsigned n_chunks, int chu
         const unsigned bar = su32(&full[s]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(chunk));
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         su32(buf + (size_t)s * chunk)), "l"(src + ((size_t)blockIdx.x + (size_t)i * gridDim.x) * chunk), "r"(chunk), "r"(bar) : "memory");
+                         su32(buf + (size_t)s * chunk)), "l"(src + chunk_index(i) * chunk), "r"(chunk), "r"(bar) : "memory");
         if (++s == ring) { s = 0; ph ^= 1u; }
       }
     }
@@ -111,7 +122,18 @@ __global__ void bulk_ws(const char* __restrict__ src, unsigned n_chunks, int chu
   unsigned ph = (cw / ring) & 1;
   for (unsigned i = cw; i < mine; i += n_cons) {
     if (!wait_bounded(su32(&full[s]), ph, cw, i)) break;
-    for (int k = lane; k < chunk / 16; k += 32) acc += reinterpret_cast<const double2*>(buf + (size_t)s * chunk)[k].x;
+    if (work > 0) {  // mode-product-like consumer: a dependent FMA chain over the chunk (25 lanes x 25 terms)
+      const double2* blk = reinterpret_cast<const double2*>(buf + (size_t)s * chunk);
+      double a0 = 0, a1 = 0;
+      for (int c = 0; c < work; ++c) {
+        const double2 v = blk[(lane % 25) + 25 * (c % 25)];
+        a0 = fma(v.x, a1 + 1.0, a0);
+        a1 = fma(v.y, a0, a1);
+      }
+      acc += a0 + a1;
+    } else {
+      for (int k = lane; k < chunk / 16; k += 32) acc += reinterpret_cast<const double2*>(buf + (size_t)s * chunk)[k].x;
+    }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
     s += n_cons;
@@ -182,6 +204,23 @@ int main(int argc, char** argv) {
     ms = time([&] { bulk_ws<<<148, wthreads[t], smem>>>(src, n_chunks, chunk, ring, sink); });
     printf("ws   chunk=%5d ring=%2d threads=%d  %.1f us  %.0f GB/s\n", chunk, ring, wthreads[t], ms * 1e3,
            (double)n_chunks * chunk / ms / 1e6);
+  }
+  for (int work : {25, 50, 100}) {  // 7 consumer warps x 2 slots (ring 14), like m2l_zpipe_kernel's mode warps
+    const int chunk = 10000 / 16 * 16, ring = 14;
+    const unsigned n_chunks = bytes / chunk;
+    ms = time([&] { bulk_ws<<<148, 32 * 8, (size_t)chunk * ring>>>(src, n_chunks, chunk, ring, sink, work); });
+    printf("ws+work %3d  chunk=%5d ring=%2d consumers=7  %.1f us  %.0f GB/s\n", work, chunk, ring, ms * 1e3,
+           (double)n_chunks * chunk / ms / 1e6);
+  }
+  for (int lz : {32, 7, -32, -7}) {
+    const int chunk = 10000 / 16 * 16, ring = 14;
+    const unsigned plane = (lz == 32 || lz == -32 ? 1024 : 3969), n_chunks = plane * (lz > 0 ? lz : -lz);
+    if ((size_t)n_chunks * chunk > bytes) continue;
+    for (int work : {0, 25}) {
+      ms = time([&] { bulk_ws<<<148, 32 * 8, (size_t)chunk * ring>>>(src, n_chunks, chunk, ring, sink, work, lz); });
+      printf("ws zpipe-order lz=%3d (%s) work=%2d  %.1f us  %.0f GB/s\n", lz, lz > 0 ? "[qz][col]" : "[col][qz]", work, ms * 1e3,
+             (double)n_chunks * chunk / ms / 1e6);
+    }
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
