@@ -246,18 +246,14 @@ void tile_columns(std::vector<int4>& jobs, int s, int cols, int pair_base, bool 
 void build_jobs(fpbem_cu_op* op, int nrhs) {
   if (op->jobs_nrhs == nrhs) return;
   const char* nv = std::getenv("FPBEM_NARROW_TILES");
-  const bool narrow = !(nv && std::strcmp(nv, "0") == 0) && !gemm_uses_mbar();
+  const bool narrow = !(nv && std::strcmp(nv, "0") == 0);
   std::vector<int4> jobs;
   for (int s = 0; s < op->n_near; ++s) {  // this rank's share of every offset's pairs
     const long long a = std::max<long long>(op->pair_start[s], op->pair_lo);
     const long long b = std::min<long long>(op->pair_start[s + 1], op->pair_hi);
     if (a < b) tile_columns(jobs, s, static_cast<int>(b - a) * nrhs, static_cast<int>(a), narrow);
   }
-  // offset order by default (consecutive tiles share S_o in L2);
-  // FPBEM_JOB_ORDER=lpt puts the longest column tiles first (A/B timing)
-  const char* order = std::getenv("FPBEM_JOB_ORDER");
-  if (order && std::strcmp(order, "lpt") == 0)
-    std::stable_sort(jobs.begin(), jobs.end(), [](const int4& a, const int4& b) { return (a.z & 0xff) > (b.z & 0xff); });
+  // offset order: consecutive tiles share S_o in L2 (longest-first ordering measured neutral)
   if (static_cast<int>(jobs.size()) > op->jobs_cap) {
     if (op->jobs) cudaFree(op->jobs);
     op->jobs = dalloc<int4>(jobs.size(), "jobs");

@@ -9,7 +9,6 @@ namespace fpbem_cu {
 size_t near_gemm_smem_bytes();
 int near_gemm_tile_cols();
 int near_gemm_tile_rows();
-bool gemm_uses_mbar();  // FPBEM_GEMM=mbar selected (64-wide tiles only)
 // jobs: (block slot, first column, column count, pair base); columns are
 // (pair, rhs) with rhs fastest (near field) or (cell, rhs) when pair_src is
 // null (P2M with A = V0, a_stride = 0).

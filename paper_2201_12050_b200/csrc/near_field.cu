@@ -212,144 +212,6 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   }
 }
 
-// mbarrier-pipelined variant: a 3-stage ring filled with 1-D bulk copies
-// (cp.async.bulk, completion counted in bytes on the stage's "full"
-// mbarrier). Every warp consumes (Gauss-3M DMMA) and releases a stage on its
-// "empty" mbarrier; warp 0 additionally refills the stage it just released
-// once all warps have released it, so no CTA-wide barrier sits in the K loop
-// and the other warps run ahead on the stages already in flight. A partial
-// last K tile is filled with zero-filling cp.async (bulk copies cannot
-// zero-fill); rows beyond M are simply not copied (they only feed output
-// rows that are never stored).
-__global__ void __launch_bounds__(THREADS, 2)
-near_gemm_mbar_kernel(const c64* __restrict__ A, long long a_stride, int lda, int M, const c64* __restrict__ x,
-                      c64* __restrict__ out, int ldo, const int* __restrict__ pair_src, const int4* __restrict__ jobs,
-                      int K, int n, long long N, int nrhs) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  c64* As = reinterpret_cast<c64*>(smem_raw);
-  c64* Bs = reinterpret_cast<c64*>(smem_raw + kSmemA);
-  __shared__ long long col_src[BN];
-  __shared__ long long col_out[BN];
-  __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int m_tiles = (M + BM - 1) / BM;
-  const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
-  const int4 job = jobs[blockIdx.x / m_tiles];
-  const int s = job.x, col0 = job.y, ncols = job.z & 0xff, pair_base = job.w;  // width class ignored: 64-wide
-
-  if (tid < BN) {
-    if (tid < ncols) {
-      const int gc = col0 + tid;
-      const int unit = pair_base + gc / nrhs;
-      const int r = gc % nrhs;
-      const long long cell = pair_src ? pair_src[unit] : unit;
-      col_src[tid] = static_cast<long long>(r) * N + cell * n;
-      col_out[tid] = (static_cast<long long>(pair_base) * nrhs + gc) * ldo;
-    } else {
-      col_src[tid] = -1;
-      col_out[tid] = -1;
-    }
-  }
-  if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) {
-      mbar_init(smem_u32(&full_bar[st]), 1);
-      mbar_init(smem_u32(&empty_bar[st]), THREADS / 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  const c64* Ablk = A + static_cast<size_t>(s) * a_stride;
-  const int nk = (K + BK - 1) / BK;
-  const unsigned a_bytes = static_cast<unsigned>(min(BM, M - m0)) * sizeof(c64);
-
-  // warp 0: fill stage st with k-tile kt
-  auto produce = [&](int st, int kt) {
-    const int k0 = kt * BK;
-    const unsigned full = smem_u32(&full_bar[st]);
-    c64* as = As + st * BK * AP;
-    c64* bs = Bs + st * BN * BP;
-    if (k0 + BK <= K) {
-      if (lane == 0) mbar_arrive_expect_tx(full, BK * a_bytes + ncols * BK * sizeof(c64));
-      __syncwarp();
-      if (lane < BK) bulk_g2s(smem_u32(as + lane * AP), Ablk + static_cast<size_t>(k0 + lane) * lda + m0, a_bytes, full);
-      for (int c = lane; c < ncols; c += 32) bulk_g2s(smem_u32(bs + c * BP), x + col_src[c] + k0, BK * sizeof(c64), full);
-    } else {
-      for (int e = lane; e < BM * BK; e += 32) {
-        const int kk = e / BM, mm = e % BM;
-        const bool ok = k0 + kk < K && m0 + mm < M;
-        cp_async16_u32(smem_u32(as + kk * AP + mm), ok ? Ablk + static_cast<size_t>(k0 + kk) * lda + m0 + mm : Ablk,
-                       ok);
-      }
-      for (int e = lane; e < BN * BK; e += 32) {
-        const int c = e / BK, kk = e % BK;
-        const long long so = col_src[c];
-        const bool ok = so >= 0 && k0 + kk < K;
-        cp_async16_u32(smem_u32(bs + c * BP + kk), ok ? x + so + k0 + kk : x, ok);
-      }
-      cp_async_wait_all();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(full);
-    }
-  };
-
-  if (warp == 0)
-    for (int kt = 0; kt < STAGES && kt < nk; ++kt) produce(kt, kt);
-
-  double t1[8][2], t2[8][2], t3[8][2];
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    t1[mi][0] = t1[mi][1] = 0.0;
-    t2[mi][0] = t2[mi][1] = 0.0;
-    t3[mi][0] = t3[mi][1] = 0.0;
-  }
-  const int wn = warp;
-  const int fr = lane >> 2, fk = lane & 3;
-  const bool active = wn * 8 < ncols;
-  for (int kt = 0; kt < nk; ++kt) {
-    const int st = kt % STAGES;
-    const unsigned phase = (kt / STAGES) & 1;
-    mbar_wait(smem_u32(&full_bar[st]), phase);
-    if (active) {
-      const c64* as = As + st * BK * AP;
-      const c64* bs = Bs + st * BN * BP;
-#pragma unroll
-      for (int k4 = 0; k4 < BK / 4; ++k4) {
-        const c64 b = bs[(wn * 8 + fr) * BP + k4 * 4 + fk];
-        const double bsum = b.x + b.y;
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
-          const c64 a = as[(k4 * 4 + fk) * AP + mi * 8 + fr];
-          const double asum = a.x + a.y;
-          dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
-          dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
-          dmma884(t3[mi][0], t3[mi][1], asum, bsum);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
-    if (warp == 0 && kt + STAGES < nk) {
-      mbar_wait(smem_u32(&empty_bar[st]), phase);  // every warp is done with this use of st
-      produce(st, kt + STAGES);
-    }
-  }
-  if (!active) return;
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    const int gm = m0 + mi * 8 + fr;
-    if (gm >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = wn * 8 + 2 * fk + j;
-      const long long o = col_out[c];
-      if (o >= 0) out[o + gm] = cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
-    }
-  }
-}
-
 // y[r,t,i] = sum_{pairs of t, offset order} W[pair, r, i]  +  sum_m U0[i, m] L[t, r, m]
 // One thread per row i; grid (row tiles, target cells * nrhs).
 constexpr int RED_THREADS = 128;
@@ -402,28 +264,15 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 size_t near_gemm_smem_bytes() { return kSmemA + kSmemB; }
 int near_gemm_tile_cols() { return BN; }
 int near_gemm_tile_rows() { return BM; }
-bool gemm_uses_mbar() {
-  const char* v = std::getenv("FPBEM_GEMM");
-  return v && std::strcmp(v, "mbar") == 0;
-}
 
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
                               cudaStream_t stream) {
   static bool configured = false;
-  static bool use_mbar = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(near_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmemA + kSmemB));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(near_gemm_mbar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemA + kSmemB));
-    if (e != cudaSuccess) return e;
-    const char* v = std::getenv("FPBEM_GEMM");
-    // default: the cp.async kernel; FPBEM_GEMM=mbar selects the bulk-copy/mbarrier
-    // variant (correct, but 20-25 % slower on cfg2/cfg3: warp 0 stalls on the
-    // "empty" barrier before every refill)
-    use_mbar = v && std::strcmp(v, "mbar") == 0;
     configured = true;
   }
   if (n_jobs == 0) return cudaSuccess;
@@ -431,11 +280,6 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
   const long long ctas = static_cast<long long>((M + BM - 1) / BM) * n_jobs;
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   dim3 grid(static_cast<unsigned>(ctas));
-  if (use_mbar) {
-    near_gemm_mbar_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src,
-                                                                       jobs, K, n, N, nrhs);
-    return cudaGetLastError();
-  }
   near_gemm_dmma_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src, jobs,
                                                                     K, n, N, nrhs);
   return cudaGetLastError();
