@@ -281,23 +281,27 @@ void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fp
   const int b2 = op->b * op->b;
   const size_t total = static_cast<size_t>(op->q_total) * b2;
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
+  using DevPtr = std::unique_ptr<void, decltype(&cudaFree)>;  // temporaries freed on every exit path
   c64* work = dalloc<c64>(total, "spectrum");
+  DevPtr keep_work(work, &cudaFree);
+  DevPtr keep_tmp(nullptr, &cudaFree), keep_offs(nullptr, &cudaFree), keep_staged(nullptr, &cudaFree);
   c64* cur = work;
   c64* tmp = nullptr;
-  int* offs = nullptr;
-  c64* staged = nullptr;
   if (prebuilt) {
     h2d(work, prebuilt, total * sizeof(c64), op->stream, "spectrum upload");
   } else {
     tmp = dalloc<c64>(total, "spectrum scratch");
+    keep_tmp.reset(tmp);
     const c64* blocks = reinterpret_cast<const c64*>(far_blocks);  // device bank (fpbem_cu_m2l_bank)
     if (!blocks_on_device) {
-      staged = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
+      c64* staged = dalloc<c64>(static_cast<size_t>(n_far) * b2, "far bank");
+      keep_staged.reset(staged);
       if (n_far > 0)
         h2d(staged, far_blocks, static_cast<size_t>(n_far) * b2 * sizeof(c64), op->stream, "far bank upload");
       blocks = staged;
     }
-    offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
+    int* offs = dalloc<int>(static_cast<size_t>(n_far) * 3, "far offsets");
+    keep_offs.reset(offs);
     if (n_far > 0)
       h2d(offs, far_offsets, static_cast<size_t>(n_far) * 3 * sizeof(int), op->stream, "far offsets upload");
     check(cudaMemsetAsync(work, 0, total * sizeof(c64), op->stream), "spectrum clear");
@@ -322,15 +326,12 @@ void build_spectrum(fpbem_cu_op* op, int n_far, const int* far_offsets, const fp
     }
   }
   check(cudaStreamSynchronize(op->stream), "spectrum build");
-  if (cur == work) {
-    if (tmp) cudaFree(tmp);
-    *out = work;
-  } else {
-    cudaFree(work);
-    *out = tmp;
-  }
-  if (staged) cudaFree(staged);
-  if (offs) cudaFree(offs);
+  // the result stays in whichever buffer the last pass wrote
+  if (cur == work)
+    keep_work.release();
+  else
+    keep_tmp.release();
+  *out = cur;
 }
 
 void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {
@@ -358,7 +359,7 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   long long cx = Mx, cy = My;  // current x / y extents
   // z forward + mode product + z inverse fused into one kernel when the
   // column's fields fit in shared memory (FPBEM_M2L_FUSE=0 disables)
-  const char* fz = std::getenv("FPBEM_M2L_FUSE");
+  static const char* fz = std::getenv("FPBEM_M2L_FUSE");
   const bool fuse_z = Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
                       m2l_zfused_ring(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E), op->b) > 0;
   // x and y together in shared memory per z-plane when the plane fits (FPBEM_M2L_XY=0: per-axis passes)
@@ -1689,21 +1690,19 @@ int fpbem_cu_evaluate_field(const fpbem_cu_cell* cell, double k, const double pi
     std::unique_ptr<double, decltype(&cudaFree)> keep_p(dp, &cudaFree);
     h2d(dp, points, 3 * static_cast<size_t>(n_points) * sizeof(double), s, "field points");
     const c64* sol = reinterpret_cast<const c64*>(solution);
-    c64* sol_tmp = nullptr;
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_sol(nullptr, &cudaFree);
     if (!dev) {
-      sol_tmp = dalloc<c64>(static_cast<size_t>(n_total), "field solution");
-      h2d(sol_tmp, solution, static_cast<size_t>(n_total) * sizeof(c64), s, "field solution");
-      sol = sol_tmp;
+      keep_sol.reset(dalloc<c64>(static_cast<size_t>(n_total), "field solution"));
+      h2d(keep_sol.get(), solution, static_cast<size_t>(n_total) * sizeof(c64), s, "field solution");
+      sol = keep_sol.get();
     }
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_sol(sol_tmp, &cudaFree);
     const c64* pinc = reinterpret_cast<const c64*>(p_incident);
-    c64* pinc_tmp = nullptr;
+    std::unique_ptr<c64, decltype(&cudaFree)> keep_pinc(nullptr, &cudaFree);
     if (!dev && p_incident) {
-      pinc_tmp = dalloc<c64>(static_cast<size_t>(n_points), "incident values");
-      h2d(pinc_tmp, p_incident, static_cast<size_t>(n_points) * sizeof(c64), s, "incident values");
-      pinc = pinc_tmp;
+      keep_pinc.reset(dalloc<c64>(static_cast<size_t>(n_points), "incident values"));
+      h2d(keep_pinc.get(), p_incident, static_cast<size_t>(n_points) * sizeof(c64), s, "incident values");
+      pinc = keep_pinc.get();
     }
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_pinc(pinc_tmp, &cudaFree);
     c64* partial = dalloc<c64>(static_cast<size_t>(field_chunks(n_total)) * n_points, "field partial sums");
     std::unique_ptr<c64, decltype(&cudaFree)> keep_part(partial, &cudaFree);
     c64* dst = reinterpret_cast<c64*>(out);
@@ -1742,18 +1741,17 @@ int fpbem_cu_m2l_bank(int n_t, double k, int n_blk, const double* delta, const d
     check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
     const size_t b = static_cast<size_t>(n_t + 1) * (n_t + 1), total = static_cast<size_t>(n_blk) * b * b;
-    double* dd = nullptr;
-    double* di = nullptr;
+    std::unique_ptr<double, decltype(&cudaFree)> keep_d(nullptr, &cudaFree), keep_i(nullptr, &cudaFree);
     if (delta) {
-      dd = dalloc<double>(3 * static_cast<size_t>(n_blk), "bank deltas");
-      h2d(dd, delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank deltas");
+      keep_d.reset(dalloc<double>(3 * static_cast<size_t>(n_blk), "bank deltas"));
+      h2d(keep_d.get(), delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank deltas");
     }
-    std::unique_ptr<double, decltype(&cudaFree)> keep_d(dd, &cudaFree);
     if (image_delta) {
-      di = dalloc<double>(3 * static_cast<size_t>(n_blk), "bank image deltas");
-      h2d(di, image_delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank image deltas");
+      keep_i.reset(dalloc<double>(3 * static_cast<size_t>(n_blk), "bank image deltas"));
+      h2d(keep_i.get(), image_delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank image deltas");
     }
-    std::unique_ptr<double, decltype(&cudaFree)> keep_i(di, &cudaFree);
+    const double* dd = keep_d.get();
+    const double* di = keep_i.get();
     c64* dst = reinterpret_cast<c64*>(out);
     c64* tmp = nullptr;
     if (ptr_kind != FPBEM_CU_PTR_DEVICE) dst = tmp = dalloc<c64>(total, "bank output");
