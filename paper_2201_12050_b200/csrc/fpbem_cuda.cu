@@ -363,14 +363,14 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   const bool fuse_z = Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
                       m2l_zfused_ring(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E), op->b) > 0;
   // x and y together in shared memory per z-plane when the plane fits (FPBEM_M2L_XY=0: per-axis passes)
-  static const bool xy_env = [] {
+  static const int xy_env = [] {  // 0: per-axis passes; 2: plane kernels wherever they fit; else the rule below
     const char* v = std::getenv("FPBEM_M2L_XY");
-    return !(v && std::strcmp(v, "0") == 0);
+    return v ? std::atoi(v) : 1;
   }();
   // where it measured faster than the per-axis passes: enough (plane, field)
   // CTAs to fill the GPU without splitting (cfg3), or small planes with both axes periodic (cfg2)
   const bool xy_wins = Mz * E >= 2LL * 148 || (Lx > 1 && Ly > 1 && Lx * Ly <= 1024);
-  const bool fuse_xy = xy_env && xy_wins && (Lx > 1 || Ly > 1) &&
+  const bool fuse_xy = xy_env != 0 && (xy_wins || xy_env == 2) && (Lx > 1 || Ly > 1) &&
                        xy_plane_smem(static_cast<int>(Mx), static_cast<int>(My), static_cast<int>(Lx),
                                      static_cast<int>(Ly), true) <= 200 * 1024 &&
                        xy_plane_smem(static_cast<int>(Mx), static_cast<int>(My), static_cast<int>(Lx),

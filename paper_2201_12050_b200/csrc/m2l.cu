@@ -97,11 +97,11 @@ dft_axis_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __
 //             Y[iy][qx] = sum_qy conj Wy[qy][iy] in[qy][qx]        (this CTA's iy range)
 //             out[iz][iy][ix][E] = scale sum_qx conj Wx[qx][ix] Y[iy][qx]
 // with W[q][j] = exp(-2 pi i (j q mod L) / L) expanded once per CTA into
-// shared matrices (odd row pitch: conflict-free column access), so the inner
-// loops are two shared loads and one complex FMA per term. Each thread owns
-// two outputs that share their input loads; each output sums in index order
-// with even / odd partial sums. CTA (iz * E + e, part): the second (forward)
-// or first (inverse) phase is split over `parts` CTAs to fill the GPU.
+// shared matrices (odd row pitch), and both phases run as small complex GEMMs
+// on the FP64 tensor cores (DMMA m8n8k4, Gauss 3M): two fragment loads per
+// three MMAs instead of two shared loads per complex FMA, which made the
+// DFMA version shared-memory bound. CTA (iz * E + e, part): the second
+// (forward) or first (inverse) phase is split over `parts` CTAs to fill the GPU.
 __device__ __forceinline__ int odd_pitch(int n) { return n | 1; }
 
 template <bool kInverse>
@@ -141,69 +141,52 @@ xy_plane_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __
   const int s1 = static_cast<int>(static_cast<long long>(split_n) * (part + 1) / parts);
   __syncthreads();
 
-  // two outputs sharing the inputs: sum_j w0[j] src[j * stride], sum_j w1[j] src[j * stride]
-  auto dot2 = [&](const c64* src, int stride, int n, const c64* w0, const c64* w1, c64& o0, c64& o1) {
-    c64 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0), b0 = cmk(0.0, 0.0), b1 = cmk(0.0, 0.0);
-    int j = 0;
-    for (; j + 2 <= n; j += 2) {
-      const c64 v0 = src[j * stride], v1 = src[(j + 1) * stride];
-      const c64 x0 = w0[j], x1 = w0[j + 1], y0 = w1[j], y1 = w1[j + 1];
-      a0 = cfma(x0, v0, a0);
-      a1 = cfma(x1, v1, a1);
-      b0 = cfma(y0, v0, b0);
-      b1 = cfma(y1, v1, b1);
+  // C = A B on the FP64 tensor cores (complex, Gauss 3M as in near_field.cu),
+  // 8 x 8 output tiles over the warps, k in steps of 4; out-of-range rows,
+  // columns and k are zero-filled
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  auto cgemm = [&](int M, int N, int K, auto a_at, auto b_at, auto store) {
+    const int tn_count = (N + 7) / 8, tiles = ((M + 7) / 8) * tn_count;
+    for (int t = warp; t < tiles; t += n_warps) {
+      const int tm = t / tn_count, tn = t - tm * tn_count;
+      double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
+      const int am = tm * 8 + fr, bn = tn * 8 + fr;
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        const int k = k0 + fk;
+        const c64 av = (am < M && k < K) ? a_at(am, k) : cmk(0.0, 0.0);
+        const c64 bv = (k < K && bn < N) ? b_at(k, bn) : cmk(0.0, 0.0);
+        dmma884(t1[0], t1[1], av.x, bv.x);
+        dmma884(t2[0], t2[1], av.y, bv.y);
+        dmma884(t3[0], t3[1], av.x + av.y, bv.x + bv.y);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = tn * 8 + 2 * fk + j;
+        if (am < M && n < N) store(am, n, cmk(t1[j] - t2[j], t3[j] - t1[j] - t2[j]));
+      }
     }
-    if (j < n) {
-      const c64 v = src[j * stride];
-      a0 = cfma(w0[j], v, a0);
-      b0 = cfma(w1[j], v, b0);
-    }
-    o0 = cadd(a0, a1);
-    o1 = cadd(b0, b1);
   };
 
   if (!kInverse) {
-    // X[iy][qx], qx in pairs (qx, qx + Lx/2 rounded up)
-    const int h1 = (Lx + 1) / 2;
-    for (int o = threadIdx.x; o < My * h1; o += blockDim.x) {
-      const int iy = o / h1, qa = o - iy * h1, qb = qa + h1;
-      c64 xa, xb;
-      dot2(a + iy * Mx, 1, Mx, A1 + qa * p1, A1 + (qb < Lx ? qb : qa) * p1, xa, xb);
-      mid[iy * Lx + qa] = xa;
-      if (qb < Lx) mid[iy * Lx + qb] = xb;
-    }
+    // X[iy][qx] = sum_ix in[iy][ix] Wx[qx][ix]      (M = My, N = Lx, K = Mx)
+    cgemm(My, Lx, Mx, [&](int m, int k) { return a[m * Mx + k]; }, [&](int k, int n) { return A1[n * p1 + k]; },
+          [&](int m, int n, c64 v) { mid[m * Lx + n] = v; });
     __syncthreads();
-    // out[qy][qx], qy in pairs within [s0, s1)
-    const int n_q = s1 - s0, h2 = (n_q + 1) / 2;
-    for (int o = threadIdx.x; o < h2 * Lx; o += blockDim.x) {
-      const int k = o / Lx, qx = o - k * Lx;
-      const int qa = s0 + k, qb = qa + h2;
-      c64 ya, yb;
-      dot2(mid + qx, Lx, My, A2 + qa * p2, A2 + (qb < s1 ? qb : qa) * p2, ya, yb);
-      out[((static_cast<long long>(iz) * Ly + qa) * Lx + qx) * E + e] = ya;
-      if (qb < s1) out[((static_cast<long long>(iz) * Ly + qb) * Lx + qx) * E + e] = yb;
-    }
+    // out[qy][qx] = sum_iy Wy[qy][iy] X[iy][qx]     (M = this CTA's qy, N = Lx, K = My)
+    cgemm(s1 - s0, Lx, My, [&](int m, int k) { return A2[(s0 + m) * p2 + k]; },
+          [&](int k, int n) { return mid[k * Lx + n]; },
+          [&](int m, int n, c64 v) { out[((static_cast<long long>(iz) * Ly + s0 + m) * Lx + n) * E + e] = v; });
   } else {
-    // Y[iy][qx] for iy in [s0, s1), in pairs
-    const int n_i = s1 - s0, h1 = (n_i + 1) / 2;
-    for (int o = threadIdx.x; o < h1 * Lx; o += blockDim.x) {
-      const int k = o / Lx, qx = o - k * Lx;
-      const int ia = s0 + k, ib = ia + h1;
-      c64 ya, yb;
-      dot2(a + qx, Lx, Ly, A1 + ia * p1, A1 + (ib < s1 ? ib : ia) * p1, ya, yb);
-      mid[(ia - s0) * Lx + qx] = ya;
-      if (ib < s1) mid[(ib - s0) * Lx + qx] = yb;
-    }
+    // Y[iy][qx] = sum_qy conj Wy[qy][iy] in[qy][qx] (M = this CTA's iy, N = Lx, K = Ly)
+    cgemm(s1 - s0, Lx, Ly, [&](int m, int k) { return A1[(s0 + m) * p1 + k]; },
+          [&](int k, int n) { return a[k * Lx + n]; }, [&](int m, int n, c64 v) { mid[m * Lx + n] = v; });
     __syncthreads();
-    // out[iy][ix], ix in pairs
-    const int h2 = (Mx + 1) / 2;
-    for (int o = threadIdx.x; o < n_i * h2; o += blockDim.x) {
-      const int r = o / h2, xa = o - r * h2, xb = xa + h2;
-      c64 va, vb;
-      dot2(mid + r * Lx, 1, Lx, A2 + xa * p2, A2 + (xb < Mx ? xb : xa) * p2, va, vb);
-      out[((static_cast<long long>(iz) * My + s0 + r) * Mx + xa) * E + e] = cscale(va, scale);
-      if (xb < Mx) out[((static_cast<long long>(iz) * My + s0 + r) * Mx + xb) * E + e] = cscale(vb, scale);
-    }
+    // out[iy][ix] = scale sum_qx Y[iy][qx] conj Wx[qx][ix]   (M = this CTA's iy, N = Mx, K = Lx)
+    cgemm(s1 - s0, Mx, Lx, [&](int m, int k) { return mid[m * Lx + k]; }, [&](int k, int n) { return A2[n * p2 + k]; },
+          [&](int m, int n, c64 v) {
+            out[((static_cast<long long>(iz) * My + s0 + m) * Mx + n) * E + e] = cscale(v, scale);
+          });
   }
 }
 
