@@ -357,6 +357,23 @@ def test_device_gmres_left_preconditioner():
     assert np.linalg.norm(d * rep.solution - b) / np.linalg.norm(b) < 1e-10
 
 
+def test_fmm_gmres_zero_rhs_returns_immediately(ops, assembled):
+    """src/solver.cpp:32-36: ||b|| == 0 -> converged, 0 iterations, x = 0, no history;
+    also for one zero right-hand side inside a lockstep batch"""
+    from paper_2201_12050_b200 import gmres
+
+    sc, d = assembled(1, 0)
+    rep = gmres(ops(d), np.zeros(d.N, np.complex128), tol=1e-6, restart=50, max_iter=100)
+    assert rep.converged and rep.iterations == 0 and not np.any(rep.solution) and len(rep.residual_history) == 0
+    b1 = sc.rhs(0)
+    B = np.concatenate([b1, np.zeros(d.N, np.complex128), 2.0 * b1])
+    reps = gmres(ops(d, max_rhs=3), B, tol=1e-8, restart=50, max_iter=200)
+    assert reps[1].converged and reps[1].iterations == 0 and not np.any(reps[1].solution)
+    single = gmres(ops(d), b1, tol=1e-8, restart=50, max_iter=200)
+    assert reps[0].iterations == single.iterations and rel(reps[0].solution, single.solution) <= SOLVE_TOL
+    assert reps[2].iterations == single.iterations and rel(reps[2].solution, 2.0 * single.solution) <= SOLVE_TOL
+
+
 def test_fmm_gmres_nan_rhs_is_a_hard_error(ops, assembled):
     from paper_2201_12050_b200 import gmres
 
