@@ -130,6 +130,8 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
 //   col_src = rhs*N + cell*n, col_out = (cell*nrhs + rhs)*ldo  (pair_src == nullptr).
 // Warps whose 8-column slab lies beyond the job's column count skip the MMA
 // loop, so partial column tiles cost (almost) only their useful work.
+// 2 CTAs per SM (128 registers): measured 15-17 % faster than one CTA with the
+// 154 registers the compiler takes when uncapped
 __global__ void __launch_bounds__(THREADS, 2)
 near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, int M, const c64* __restrict__ x,
                       c64* __restrict__ out, int ldo, const int* __restrict__ pair_src, const int4* __restrict__ jobs,
