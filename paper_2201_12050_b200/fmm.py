@@ -309,6 +309,47 @@ def gmres(apply, b, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000,
     return _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device)
 
 
+def rhs_shard(n_rhs: int, world: int, rank: int) -> list[int]:
+    """Right-hand sides this rank solves when independent solves are sharded
+    (SURVEY §8e, cfg5): round-robin, so ranks differ by at most one solve."""
+    if world < 1 or not 0 <= rank < world or n_rhs < 0:
+        raise ValueError("rhs_shard: bad world / rank / count")
+    return list(range(rank, n_rhs, world))
+
+
+def gmres_sharded(op, b, n_rhs: int, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000, group=None,
+                  solve=None):
+    """Independent GMRES solves of n_rhs stacked right-hand sides `b` (numpy,
+    every rank holding all of them) sharded over the ranks of a
+    torch.distributed group: each rank solves its rhs_shard in one lockstep
+    batch (FmmOperators with max_rhs >= its share) and the reports are
+    gathered, so every rank returns all n_rhs SolveReports in order. No
+    collective inside the solves (the operator is replicated). `solve`
+    overrides the per-rank solver (for tests)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    bb = np.ascontiguousarray(b, np.complex128).reshape(n_rhs, -1)
+    mine = rhs_shard(n_rhs, world, rank)
+    if solve is None:
+        def solve(rhs):
+            reps = gmres(op, np.ascontiguousarray(rhs).reshape(-1), tol=tol, restart=restart, max_iter=max_iter)
+            return reps if isinstance(reps, list) else [reps]
+    local = solve(bb[mine]) if mine else []
+    payload = [(i, np.asarray(r.solution), list(r.residual_history), r.iterations, r.converged)
+               for i, r in zip(mine, local)]
+    gathered = [payload]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, payload, group=group)
+    out = [None] * n_rhs
+    for part in gathered:
+        for i, sol, hist, its, conv in part:
+            out[i] = SolveReport(sol, hist, its, conv)
+    return out
+
+
 def _cell_struct(scene, keep):
     c = scene.cell()
     n = len(c["area"])

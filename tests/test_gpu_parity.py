@@ -712,6 +712,23 @@ def test_batched_gmres_matches_per_rhs_oracle_with_restarts(ops, assembled):
     assert len(set(its)) > 1  # the RHS really leave the batch at different times
 
 
+def test_rhs_sharded_solve_single_process_equals_batch(ops, assembled):
+    """gmres_sharded without a process group: one shard = the lockstep batch"""
+    from paper_2201_12050_b200 import gmres
+    from paper_2201_12050_b200.fmm import gmres_sharded
+
+    sc, d = assembled(5, 2)
+    dirs = [[1, 0, 0], [0, 0.6, 0.8], [0.3, -0.4, 0.866]]
+    sc.set_sources([1] * len(dirs), dirs)
+    B = np.concatenate([sc.rhs(r) for r in range(len(dirs))])
+    op = ops(d, max_rhs=len(dirs))
+    sharded = gmres_sharded(op, B, len(dirs), tol=1e-7, restart=30, max_iter=300)
+    batch = gmres(op, B, tol=1e-7, restart=30, max_iter=300)
+    for a, b in zip(sharded, batch):
+        assert a.iterations == b.iterations and a.converged == b.converged
+        assert np.array_equal(a.solution, b.solution)
+
+
 def test_batched_gmres_equals_sequential_solves(ops, assembled):
     import os
 

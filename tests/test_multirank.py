@@ -108,3 +108,59 @@ def test_near_pairs_order_matches_the_device_count():
     sc = Scene(2, 0)
     near, _, _, _ = sc.classify()
     assert len(near_pairs(sc.counts, near)) == 8012
+
+
+def _sharded_worker(rank, world, port, result_path):
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_2201_12050_b200 import Scene
+    from paper_2201_12050_b200.fmm import gmres_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sc = Scene(1, 2)
+    d = sc.assemble_fmm(3)
+    ora = O.OracleFmm(d)
+    dirs = [[1, 0, 0], [0, 1, 0], [0, 0, 1], [0.6, 0.8, 0], [0, 0.6, 0.8]]
+    sc.set_sources([1] * len(dirs), dirs)
+    B = np.concatenate([sc.rhs(r) for r in range(len(dirs))])
+
+    def solve(rhs):  # the oracle stands in for the device batch on this CPU-only box
+        from paper_2201_12050_b200.fmm import SolveReport
+
+        reps = []
+        for r in rhs:
+            x, its, conv, hist = ora.gmres(r, tol=1e-8, restart=20, max_iter=200)
+            reps.append(SolveReport(x, list(hist), its, conv))
+        return reps
+
+    reps = gmres_sharded(None, B, len(dirs), solve=solve)
+    if rank == 0:
+        errs = []
+        for r, rep in enumerate(reps):
+            x, its, conv, _ = ora.gmres(B.reshape(len(dirs), -1)[r], tol=1e-8, restart=20, max_iter=200)
+            errs.append(float(np.linalg.norm(rep.solution - x)) + abs(rep.iterations - its) + (rep.converged != conv))
+        np.save(result_path, np.array(errs))
+    dist.destroy_process_group()
+
+
+def test_rhs_sharded_solves_gather_in_order(tmp_path):
+    """cfg5's multi-GPU mode: independent solves round-robin over the
+    ranks, gathered back in right-hand-side order on every rank"""
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "sharded.npy")
+    mp.spawn(_sharded_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    errs = np.load(out)
+    assert len(errs) == 5 and np.all(errs == 0.0)
+
+
+def test_rhs_shard_rule():
+    from paper_2201_12050_b200.fmm import rhs_shard
+
+    for n, world in [(64, 8), (64, 3), (5, 8), (0, 2)]:
+        parts = [rhs_shard(n, world, r) for r in range(world)]
+        assert sorted(i for p in parts for i in p) == list(range(n))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
