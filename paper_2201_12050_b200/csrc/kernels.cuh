@@ -1,4 +1,4 @@
-// Launchers of the sm_100a kernels (near_field.cu, m2l.cu, krylov.cu).
+// Launchers of the sm_100a kernels (near_field.cu, m2l.cu, krylov.cu, assembly.cu, far_bank.cu).
 #pragma once
 
 #include "common.cuh"
@@ -6,12 +6,8 @@
 namespace fpbem_cu {
 
 // ---- near field (near_field.cu)
-size_t near_gemm_smem_bytes();
-int near_gemm_tile_cols();
-int near_gemm_tile_rows();
-// jobs: (block slot, first column, column count, pair base); columns are
-// (pair, rhs) with rhs fastest (near field) or (cell, rhs) when pair_src is
-// null (P2M with A = V0, a_stride = 0).
+// jobs: (block slot, first column, column count | width class << 8, pair base);
+// columns are (pair, rhs) with rhs fastest, or (cell, rhs) when pair_src is null.
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
                               cudaStream_t stream);

@@ -263,9 +263,6 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 
 }  // namespace
 
-size_t near_gemm_smem_bytes() { return kSmemA + kSmemB; }
-int near_gemm_tile_cols() { return BN; }
-int near_gemm_tile_rows() { return BM; }
 
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
