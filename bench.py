@@ -287,7 +287,7 @@ def run_ours(args):
         # ---- end-to-end through the C-ABI with pinned host buffers
         xp = torch.empty(data.N, dtype=torch.complex128, pin_memory=True)
         xp.copy_(torch.from_numpy(xh))
-        yp = torch.empty_like(xp)
+        yp = torch.empty(data.N, dtype=torch.complex128, pin_memory=True)  # empty_like would not pin
         xpn, ypn = xp.numpy(), yp.numpy()
         from paper_2201_12050_b200 import _native
 
