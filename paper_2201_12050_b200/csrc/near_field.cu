@@ -31,10 +31,6 @@ constexpr int STAGES = 3;
 constexpr int AP = BM + 2;  // smem pitch (complex) of the [k][m] A tile: 16B-bank conflict free
 constexpr int BP = BK + 4;  // smem pitch (complex) of the [n][k] B tile
 constexpr int THREADS = 256;
-#ifndef FPBEM_WARP_NI
-#define FPBEM_WARP_NI 2
-#endif
-constexpr int kWarpNI = FPBEM_WARP_NI;  // n-tiles per warp (1: the previous 64x8 warp tile)
 
 constexpr size_t kSmemA = sizeof(c64) * STAGES * BK * AP;
 constexpr size_t kSmemB = sizeof(c64) * STAGES * BN * BP;
@@ -125,9 +121,8 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
 // Batched block GEMM over (block, column-tile) jobs:
 //   out[col_out(c) + m] = sum_k A_s[m + lda k] * x[col_src(c) + k],  m < M, k < K
 // Near field: A_s = S_s (lda = M = K = n), columns = (pair, rhs) of offset s,
-//   col_src = rhs*N + pair_src[pair]*n, col_out = (pair*nrhs + rhs)*ldo.
-// P2M:        A = V0 (lda = M = b, a_stride = 0), columns = (cell, rhs),
-//   col_src = rhs*N + cell*n, col_out = (cell*nrhs + rhs)*ldo  (pair_src == nullptr).
+//   col_src = rhs*N + pair_src[pair]*n, col_out = (pair*nrhs + rhs)*ldo;
+// with pair_src == nullptr the columns are (cell, rhs) of one block.
 // Warps whose 8-column slab lies beyond the job's column count skip the MMA
 // loop, so partial column tiles cost (almost) only their useful work.
 // 2 CTAs per SM (128 registers): measured 15-17 % faster than one CTA with the
@@ -196,21 +191,13 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
     }
   };
 
-  // width class of the column tile: 0 -> 64 columns (each warp 64 rows x 8),
-  // 1 -> 32 columns (32 rows x 8), 2 -> 16 columns (16 rows x 8): narrow
-  // tiles keep all 8 warps busy instead of idling most of them
-  if (kWarpNI == 2) {
-    switch (cls) {
-      case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-      case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-      default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-    }
-  } else {
-    switch (cls) {
-      case 0: gemm_main<8, 1>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-      case 1: gemm_main<4, 1>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-      default: gemm_main<2, 1>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-    }
+  // width class of the column tile: 0 -> 64 columns (warps 32 rows x 16),
+  // 1 -> 32 columns (16 x 16), 2 -> 16 columns (8 x 16): narrow tiles keep
+  // all 8 warps busy instead of idling most of them
+  switch (cls) {
+    case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+    case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+    default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
   }
 }
 
