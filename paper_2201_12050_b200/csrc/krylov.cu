@@ -231,19 +231,41 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
     if (blockIdx.x == 0 && threadIdx.x == 0) norms[0] = tot;
   }
 
-  for (int i = 0; i <= j; ++i) {
-    const c64* vi = V + static_cast<long long>(i) * ld + start;
+  // projection i: h_i = <v_i, w> (grid fold), then w -= h_i v_i. The update of
+  // projection i and the dot of projection i + 1 share one pass over the chunk
+  // (same per-thread order as two separate passes, so the same bits).
+  auto dot_pass = [&](const c64* vd, const c64* vu, c64 h) -> c64 {  // vu: update with h first (or null)
     c64 s = cmk(0.0, 0.0);
     int e = threadIdx.x;
     for (; e + 3 * RT < len; e += 4 * RT) {
-      c64 v[4];
+      c64 a[4], b[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = vi[e + u * RT];
+      for (int u = 0; u < 4; ++u) {
+        if (vu) a[u] = vu[e + u * RT];
+        b[u] = vd[e + u * RT];
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) s = cfma_conj(v[u], ws[e + u * RT], s);
+      for (int u = 0; u < 4; ++u) {
+        c64 wv = ws[e + u * RT];
+        if (vu) {
+          wv = csub(wv, cmul(h, a[u]));
+          ws[e + u * RT] = wv;
+        }
+        s = cfma_conj(b[u], wv, s);
+      }
     }
-    for (; e < len; e += RT) s = cfma_conj(vi[e], ws[e], s);
-    const c64 b = block_reduce(s, shc);
+    for (; e < len; e += RT) {
+      c64 wv = ws[e];
+      if (vu) {
+        wv = csub(wv, cmul(h, vu[e]));
+        ws[e] = wv;
+      }
+      s = cfma_conj(vd[e], wv, s);
+    }
+    return s;
+  };
+  auto fold_c = [&](c64 partial, int i) -> c64 {
+    const c64 b = block_reduce(partial, shc);
     c64* slot = part_c + (i & 1) * G;
     if (threadIdx.x == 0) slot[blockIdx.x] = b;
     grid.sync();
@@ -257,17 +279,20 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
       if (threadIdx.x == 0) bcast_c = acc;
     }
     __syncthreads();
-    const c64 h = bcast_c;
-    if (blockIdx.x == 0 && threadIdx.x == 0) h_out[i] = h;
-    for (e = threadIdx.x; e + 3 * RT < len; e += 4 * RT) {
-      c64 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = vi[e + u * RT];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) ws[e + u * RT] = csub(ws[e + u * RT], cmul(h, v[u]));
-    }
-    for (; e < len; e += RT) ws[e] = csub(ws[e], cmul(h, vi[e]));
-    // each thread only touches its own ws entries: no barrier needed before the next dot
+    return bcast_c;
+  };
+
+  c64 h = fold_c(dot_pass(V + start, nullptr, cmk(0.0, 0.0)), 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) h_out[0] = h;
+  for (int i = 0; i < j; ++i) {
+    const c64* vi = V + static_cast<long long>(i) * ld + start;
+    const c64* vn = vi + ld;
+    h = fold_c(dot_pass(vn, vi, h), i + 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) h_out[i + 1] = h;
+  }
+  {  // the last update, w -= h_j v_j
+    const c64* vj = V + static_cast<long long>(j) * ld + start;
+    for (int e = threadIdx.x; e < len; e += RT) ws[e] = csub(ws[e], cmul(h, vj[e]));
   }
 
   double s = 0.0;
