@@ -1,65 +1,26 @@
-// C-ABI implementation (include/fpbem_cuda.h): operator handle, the fused
-// FMM apply (near field + P2M + lattice-DFT M2L + L2P) and the device-
-// resident restarted GMRES.
+// C-ABI implementation (include/fpbem_cuda.h), part 1: the operator handle —
+// create / destroy, the FMM apply (near field + P2M + lattice-DFT M2L + L2P),
+// the spectrum, streams and stage timing. The device GMRES is gmres.cu, the
+// device assembly / M2L bank / field evaluation device_assembly.cu, NCCL and the
+// multi-GPU partition comm.cu; the shared handle is handle.cuh.
 //
 //   FmmOperators::matvec  src/fmm.cpp:246-271  -> apply_chunk()
-//   solver::gmres         src/solver.cpp:21-123 -> gmres_one()
 //   CirculantSpectrum ctor src/structured.cpp:63-108 -> build_spectrum()
-#include <dlfcn.h>
-
 #include <algorithm>
-#include <functional>
-#include <memory>
 #include <cmath>
 #include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
-#include "../../include/fpbem_cuda.h"
-#include "common.cuh"
-#include "kernels.cuh"
+#include "handle.cuh"
 
 using namespace fpbem_cu;
 
 namespace {
-
-thread_local std::string g_err;
-
-struct Fail {
-  int code;
-};
-
-void fail(int code, const std::string& msg) {
-  g_err = msg;
-  throw Fail{code};
-}
-
-void check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    const int code = (e == cudaErrorMemoryAllocation) ? FPBEM_CU_ENOMEM : FPBEM_CU_ECUDA;
-    fail(code, std::string(what) + ": " + cudaGetErrorString(e));
-  }
-}
-
-template <typename T>
-T* dalloc(size_t count, const char* what) {
-  void* p = nullptr;
-  if (count == 0) count = 1;
-  check(cudaMalloc(&p, count * sizeof(T)), what);
-  return static_cast<T*>(p);
-}
-
-// host->device copy ordered on `stream` (never the legacy default stream,
-// which does not synchronise with the handle's non-blocking stream)
-void h2d(void* dst, const void* src, size_t bytes, cudaStream_t stream, const char* what) {
-  if (bytes == 0) return;
-  check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), what);
-  check(cudaStreamSynchronize(stream), what);
-}
-
 int fft_friendly(int n) {  // smallest 7-smooth length >= n (src/structured.cpp:26-33)
   for (int m = n;; ++m) {
     int r = m;
@@ -68,106 +29,9 @@ int fft_friendly(int n) {  // smallest 7-smooth length >= n (src/structured.cpp:
     if (r == 1) return m;
   }
 }
-
 }  // namespace
 
-// --------------------------------------------------------------------------
-// NCCL, loaded at runtime so the library has no hard NCCL dependency.
-
-struct fpbem_cu_comm {
-  void* lib = nullptr;
-  void* comm = nullptr;  // ncclComm_t
-  int nranks = 1, rank = 0, device = 0;
-  int (*allreduce)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
-  int (*destroy)(void*) = nullptr;
-};
-
-namespace {
-void* load_nccl() {
-  static void* lib = nullptr;
-  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  return lib;
-}
-}  // namespace
-
-struct fpbem_cu_op {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  cudaStream_t aux = nullptr;  // P2M + M2L run here, concurrently with the near-field GEMM
-  cudaEvent_t fork = nullptr, join = nullptr;
-  int counts[3] = {1, 1, 1};
-  int n = 0, b = 0, n_cells = 0;
-  long long N = 0;
-  int max_rhs = 1;
-
-  // near field
-  int n_near = 0;
-  std::vector<int> near_offsets;
-  c64* S = nullptr;
-  int n_pairs = 0;
-  std::vector<int> pair_start;  // per offset slot, n_near + 1
-  int* pair_src = nullptr;
-  int* tgt_ptr = nullptr;
-  int* tgt_pairs = nullptr;
-  int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
-  int jobs_nrhs = -1, n_jobs = 0, jobs_cap = 0;
-  double far_pairs = 0.0;  // rank 0's deficit under the pair partition (calibrate_far_pairs)
-  long long pair_lo = 0, pair_hi = 0;  // global pair range this rank computes (all without a partition)
-  std::vector<int> pair_tgt;    // host copy: target cell of every pair
-  int rank = 0, nranks = 1;     // near-field offset partition
-
-  // expansions and spectrum
-  c64* u0 = nullptr;
-  c64* v0 = nullptr;
-  c64* v0t = nullptr;  // V0^T (b rows of n), for the P2M kernel
-  int L[3] = {1, 1, 1};
-  long long q_total = 1;
-  c64* lambda = nullptr;
-  c64* tw[3] = {nullptr, nullptr, nullptr};
-  // half-space image pair: S_hat blocks live in S after the n_near Toeplitz
-  // slots (Hankel-indexed pairs); lambda_hat is the spectrum of K_hat P
-  int mirrored_level = -1;
-  int n_hat = 0;
-  c64* lambda_hat = nullptr;
-  c64* mom_perm = nullptr;
-  c64* loc_hat = nullptr;
-
-  // per-apply buffers (sized for max_rhs)
-  c64* W = nullptr;
-  c64* mom = nullptr;
-  c64* loc = nullptr;
-  c64* fa = nullptr;
-  c64* fb = nullptr;
-  c64* xin = nullptr;   // host-pointer staging
-  c64* yout = nullptr;
-
-  // GMRES
-  c64* basis = nullptr;
-  int basis_cols = 0;
-  c64* gx = nullptr;
-  c64* gb = nullptr;
-  c64* gt = nullptr;
-  c64* gsol = nullptr;
-  c64* scal_c = nullptr;    // h[0..m], hc[0..m], y[0..m]
-  double* scal_d = nullptr;  // [0] pre^2 [1] post^2 [2] misc [3] rnorm^2
-  int* flag = nullptr;
-  int scal_cap = 0;
-  RedScratch rs{};
-  void* pinned = nullptr;
-  size_t pinned_bytes = 0;
-
-  // timing
-  bool timing = false;
-  cudaEvent_t ev[8] = {};
-  double stage_ms[5] = {0, 0, 0, 0, 0};
-  long long applies = 0;
-  long long launches = 0;
-
-  fpbem_cu_comm* comm = nullptr;
-};
-
-namespace {
+namespace fpbem_cu {
 
 // Multi-GPU work split: every near-field pair (offset, target)
 // costs the same n_dof^2 MACs, so ranks take equal contiguous ranges of the
@@ -570,535 +434,7 @@ void ensure_pinned(fpbem_cu_op* op, size_t bytes) {
   op->pinned_bytes = bytes;
 }
 
-void ensure_gmres(fpbem_cu_op* op, int restart) {
-  const int cols = restart + 1;
-  if (op->basis_cols < cols) {
-    if (op->basis) cudaFree(op->basis);
-    op->basis = dalloc<c64>(static_cast<size_t>(cols) * op->N, "gmres basis");
-    op->basis_cols = cols;
-  }
-  if (!op->gx) {
-    op->gx = dalloc<c64>(op->N, "gmres x");
-    op->gb = dalloc<c64>(op->N, "gmres b");
-    op->gt = dalloc<c64>(op->N, "gmres tmp");
-    op->gsol = dalloc<c64>(op->N, "gmres solution");
-    op->rs.partial_d = dalloc<double>(2 * kRedBlocks, "reduction partials");
-    op->rs.partial_c = dalloc<c64>(2 * kRedBlocks, "reduction partials");
-    op->rs.counter = dalloc<unsigned>(1, "reduction counter");
-    check(cudaMemsetAsync(op->rs.counter, 0, sizeof(unsigned), op->stream), "counter init");
-    check(cudaStreamSynchronize(op->stream), "counter init");
-  }
-  if (op->scal_cap < cols) {
-    // one contiguous block so a single read-back per Arnoldi step returns the
-    // non-finite flag, both norms and the projections: 128-byte header
-    // (doubles 0..7, int flag at byte 64), then h[cols], hc[cols], y[cols]
-    if (op->scal_c) cudaFree(op->scal_c);
-    op->scal_c = dalloc<c64>(8 + 3 * static_cast<size_t>(cols), "gmres scalars");
-    op->scal_cap = cols;
-    op->scal_d = reinterpret_cast<double*>(op->scal_c);
-    op->flag = reinterpret_cast<int*>(op->scal_d + 8);
-  }
-  ensure_pinned(op, sizeof(c64) * (8 + 3 * static_cast<size_t>(cols)) + 64);
-}
-
-struct GmresOut {
-  int iterations = 0;
-  bool converged = false;
-  std::vector<double> history;
-};
-
-// Faithful device-resident restatement of src/solver.cpp:21-123 for one rhs.
-using ApplyDev = std::function<void(const c64*, c64*)>;
-
-GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64* x_dev, double tol, int restart,
-                   int max_iter) {
-  using cd = std::complex<double>;
-  cudaStream_t s = op->stream;
-  const long long n = op->N;
-  GmresOut rep;
-  ensure_gmres(op, std::max(1, restart));
-  c64* V = op->basis;
-  auto col = [&](int j) { return V + static_cast<long long>(j) * n; };
-  c64* h = op->scal_c + 8;                    // pass-1 projections (after the 128-byte header)
-  c64* hc = h + op->scal_cap;                  // pass-2 corrections
-  c64* ydev = hc + op->scal_cap;
-  double* sd = op->scal_d;
-  char* pin = static_cast<char*>(op->pinned);
-  auto fetch = [&](const void* src, size_t bytes) {
-    check(cudaMemcpyAsync(pin, src, bytes, cudaMemcpyDeviceToHost, s), "gmres readback");
-    check(cudaStreamSynchronize(s), "gmres sync");
-  };
-  auto fetch_d = [&](int idx) {
-    fetch(sd + idx, sizeof(double));
-    double v;
-    std::memcpy(&v, pin, sizeof(double));
-    return v;
-  };
-
-  check(cudaMemsetAsync(x_dev, 0, n * sizeof(c64), s), "x0");
-  check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag");
-  check(launch_sqnorm(b_dev, n, op->rs, sd + 3, nullptr, s), "bnorm");
-  op->launches++;
-  const double bnorm = std::sqrt(fetch_d(3));
-  if (bnorm == 0.0) {
-    rep.converged = true;
-    return rep;
-  }
-  const int m = std::max(1, restart);
-  std::vector<cd> H(static_cast<size_t>(m + 1) * m, cd(0, 0));
-  auto Hm = [&](int i, int j) -> cd& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
-  std::vector<cd> g(m + 1);
-  std::vector<double> gc(m);
-  std::vector<cd> gs(m);
-  const c64* r = b_dev;  // r = b_eff on the first cycle
-  double rnorm = bnorm;
-
-  while (rep.iterations < max_iter) {
-    check(launch_div(r, col(0), n, rnorm, s), "v0");
-    op->launches++;
-    std::fill(g.begin(), g.end(), cd(0, 0));
-    g[0] = rnorm;
-    int j = 0;
-    for (; j < m && rep.iterations < max_iter; ++j) {
-      c64* w = col(j + 1);
-      apply(col(j), w);
-      const bool fused = mgs_fused_supported(n);
-      if (fused) {  // pre-norm + all j+1 MGS steps + post-norm in one cooperative launch
-        check(launch_mgs_fused(w, V, n, j, n, h, sd, op->flag, op->rs, true, s), "mgs fused");
-        op->launches++;
-      } else {
-        check(launch_sqnorm(w, n, op->rs, sd + 0, op->flag, s), "pre norm");
-        // MGS: h_0 = <v_0,w>; (w -= h_i v_i, h_{i+1} = <v_{i+1}, w>)...; w -= h_j v_j, ||w||^2
-        check(launch_dotc(col(0), w, n, op->rs, h + 0, s), "mgs dot");
-        for (int i = 0; i < j; ++i)
-          check(launch_axpy_dotc(w, col(i), h + i, col(i + 1), n, op->rs, h + i + 1, s), "mgs step");
-        check(launch_axpy_sqnorm(w, col(j), h + j, n, op->rs, sd + 1, s), "mgs last");
-        op->launches += j + 3;
-      }
-      // one read-back: flag, ||w||^2 before and after MGS, h_0..h_j
-      fetch(sd, 128 + sizeof(c64) * (j + 1));
-      {
-        int fl;
-        std::memcpy(&fl, pin + 64, sizeof(int));
-        if (fl) {
-          check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
-          fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
-        }
-      }
-      double pre2, post2;
-      std::memcpy(&pre2, pin, sizeof(double));
-      std::memcpy(&post2, pin + sizeof(double), sizeof(double));
-      for (int i = 0; i <= j; ++i) {
-        c64 v;
-        std::memcpy(&v, pin + 128 + i * sizeof(c64), sizeof(c64));
-        Hm(i, j) = cd(v.x, v.y);
-      }
-      double wnorm2 = post2;
-      if (std::sqrt(post2) < 0.5 * std::sqrt(pre2)) {  // reorthogonalisation (:63-69)
-        if (fused) {
-          check(launch_mgs_fused(w, V, n, j, n, hc, sd + 4, op->flag, op->rs, false, s), "reorth fused");
-          check(cudaMemcpyAsync(sd + 2, sd + 5, sizeof(double), cudaMemcpyDeviceToDevice, s), "reorth norm");
-          op->launches++;
-        } else {
-          check(launch_dotc(col(0), w, n, op->rs, hc + 0, s), "reorth dot");
-          for (int i = 0; i < j; ++i)
-            check(launch_axpy_dotc(w, col(i), hc + i, col(i + 1), n, op->rs, hc + i + 1, s), "reorth step");
-          check(launch_axpy_sqnorm(w, col(j), hc + j, n, op->rs, sd + 2, s), "reorth last");
-          op->launches += j + 2;
-        }
-        fetch(hc, sizeof(c64) * (j + 1));
-        for (int i = 0; i <= j; ++i) {
-          c64 v;
-          std::memcpy(&v, pin + i * sizeof(c64), sizeof(c64));
-          Hm(i, j) += cd(v.x, v.y);
-        }
-        wnorm2 = fetch_d(2);
-      }
-      const double hlast = std::sqrt(wnorm2);
-      Hm(j + 1, j) = hlast;
-      if (hlast > 0.0) {
-        check(launch_div(w, w, n, hlast, s), "normalise");
-        op->launches++;
-      }
-      for (int i = 0; i < j; ++i) {  // accumulated rotations (:75-79)
-        cd t = gc[i] * Hm(i, j) + gs[i] * Hm(i + 1, j);
-        Hm(i + 1, j) = -std::conj(gs[i]) * Hm(i, j) + gc[i] * Hm(i + 1, j);
-        Hm(i, j) = t;
-      }
-      const cd a = Hm(j, j);  // new rotation (:80-94)
-      const double bb = std::abs(Hm(j + 1, j));
-      const double denom = std::hypot(std::abs(a), bb);
-      if (denom == 0.0) {
-        gc[j] = 1.0;
-        gs[j] = cd(0, 0);
-      } else if (std::abs(a) == 0.0) {
-        gc[j] = 0.0;
-        gs[j] = cd(1, 0);
-      } else {
-        gc[j] = std::abs(a) / denom;
-        gs[j] = (a / std::abs(a)) * std::conj(Hm(j + 1, j)) / denom;
-      }
-      Hm(j, j) = gc[j] * a + gs[j] * Hm(j + 1, j);
-      Hm(j + 1, j) = cd(0, 0);
-      const cd gj = g[j];
-      g[j] = gc[j] * gj;
-      g[j + 1] = -std::conj(gs[j]) * gj;
-      ++rep.iterations;
-      const double est = std::abs(g[j + 1]) / bnorm;
-      rep.history.push_back(est);
-      if (est <= tol || hlast == 0.0) {
-        ++j;
-        break;
-      }
-    }
-    // y = triu(H_jj)^{-1} g ; x += V y (:109-110)
-    std::vector<cd> y(j);
-    for (int i = j - 1; i >= 0; --i) {
-      cd acc = g[i];
-      for (int k = i + 1; k < j; ++k) acc -= Hm(i, k) * y[k];
-      y[i] = acc / Hm(i, i);
-    }
-    if (j > 0) {
-      std::vector<c64> yh(j);
-      for (int i = 0; i < j; ++i) yh[i] = cmk(y[i].real(), y[i].imag());
-      std::memcpy(pin, yh.data(), j * sizeof(c64));
-      check(cudaMemcpyAsync(ydev, pin, j * sizeof(c64), cudaMemcpyHostToDevice, s), "y upload");
-      check(launch_update_x(x_dev, V, n, ydev, j, n, s), "x update");
-      op->launches++;
-    }
-    // true residual r = b - A x (:111-112)
-    apply(x_dev, op->gt);
-    check(launch_sqnorm(op->gt, n, op->rs, sd + 2, op->flag, s), "residual finite check");
-    check(launch_residual(b_dev, op->gt, op->gx, n, op->rs, sd + 3, s), "residual");
-    op->launches += 2;
-    fetch(sd, 128);  // flag + ||r||^2 in one read-back
-    {
-      int fl;
-      std::memcpy(&fl, pin + 64, sizeof(int));
-      if (fl) {
-        check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
-        fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
-      }
-      double r2;
-      std::memcpy(&r2, pin + 3 * sizeof(double), sizeof(double));
-      rnorm = std::sqrt(r2);
-    }
-    r = op->gx;
-    if (rnorm / bnorm <= tol) {
-      rep.converged = true;
-      break;
-    }
-  }
-  if (!rep.history.empty()) rep.converged = rep.converged || rnorm / bnorm <= tol;
-  return rep;
-}
-
-// ---------------------------------------------------------------------------
-// Lockstep batched GMRES: G right-hand sides advance one Arnoldi step together
-// (one batched matvec, batched MGS with per-RHS reductions); every RHS follows
-// exactly the control flow of src/solver.cpp:21-123 on its own scalars (host),
-// leaves its cycle's inner loop on its own estimate, and leaves the batch when
-// converged or out of iterations. Basis layout: column j of RHS r at
-// V + (j * G + r) * N, so column j of all RHS is one contiguous batch.
-struct BatchOut {
-  std::vector<int> iterations;
-  std::vector<char> converged;
-  std::vector<std::vector<double>> history;
-};
-
-BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double tol, int restart, int max_iter) {
-  using cd = std::complex<double>;
-  cudaStream_t s = op->stream;
-  const long long n = op->N;
-  const int m = std::max(1, restart);
-  BatchOut out;
-  out.iterations.assign(G, 0);
-  out.converged.assign(G, 0);
-  out.history.assign(G, {});
-
-  std::vector<void*> owned;  // device buffers scoped to the call
-  struct Free {
-    std::vector<void*>& v;
-    ~Free() {
-      for (void* p : v) cudaFree(p);
-    }
-  } free_all{owned};
-  auto alloc = [&](size_t bytes, const char* what) {
-    void* p = nullptr;
-    check(cudaMalloc(&p, bytes), what);
-    owned.push_back(p);
-    return p;
-  };
-  const size_t vecb = static_cast<size_t>(n) * sizeof(c64);
-  c64* V = static_cast<c64*>(alloc(vecb * G * (m + 1), "batched basis"));
-  c64* R = static_cast<c64*>(alloc(vecb * G, "batched residual"));
-  c64* T = static_cast<c64*>(alloc(vecb * G, "batched A x"));
-  c64* P = static_cast<c64*>(alloc(vecb * G, "batched pack in"));
-  c64* Q = static_cast<c64*>(alloc(vecb * G, "batched pack out"));
-  // scalars: [flags G int (8 B slots)][pre2 G][post2 G][post2b G][rn2 G][bn2 G][d G]
-  //          [h (m+1)G c64][hc (m+1)G][y mG][jr G int][mask G int][idx G int]
-  const size_t g8 = 8 * static_cast<size_t>((G + 1) & ~1);  // even count: c64 sections stay 16-byte aligned
-  const size_t o_flag = 0, o_pre = g8, o_post = o_pre + g8, o_post2 = o_post + g8, o_rn = o_post2 + g8,
-               o_bn = o_rn + g8, o_d = o_bn + g8, o_h = o_d + g8, o_hc = o_h + 2 * g8 * (m + 1),
-               o_y = o_hc + 2 * g8 * (m + 1), o_jr = o_y + 2 * g8 * m, o_mask = o_jr + g8 / 2,
-               o_idx = o_mask + g8 / 2, total = o_idx + g8 / 2;
-  char* sc = static_cast<char*>(alloc(total, "batched scalars"));
-  int* d_flag = reinterpret_cast<int*>(sc + o_flag);
-  double* d_pre = reinterpret_cast<double*>(sc + o_pre);
-  double* d_post = reinterpret_cast<double*>(sc + o_post);
-  double* d_post2 = reinterpret_cast<double*>(sc + o_post2);
-  double* d_rn = reinterpret_cast<double*>(sc + o_rn);
-  double* d_bn = reinterpret_cast<double*>(sc + o_bn);
-  double* d_d = reinterpret_cast<double*>(sc + o_d);
-  c64* d_h = reinterpret_cast<c64*>(sc + o_h);
-  c64* d_hc = reinterpret_cast<c64*>(sc + o_hc);
-  c64* d_y = reinterpret_cast<c64*>(sc + o_y);
-  int* d_jr = reinterpret_cast<int*>(sc + o_jr);
-  int* d_mask = reinterpret_cast<int*>(sc + o_mask);
-  int* d_idx = reinterpret_cast<int*>(sc + o_idx);
-  BatchScratch bs;
-  bs.partial_d = static_cast<double*>(alloc(sizeof(double) * kBatchBlocks * G, "batch partials"));
-  bs.partial_c = static_cast<c64*>(alloc(sizeof(c64) * kBatchBlocks * G, "batch partials"));
-  bs.counter = static_cast<unsigned*>(alloc(sizeof(unsigned) * G, "batch counters"));
-  check(cudaMemsetAsync(bs.counter, 0, sizeof(unsigned) * G, s), "counters");
-  check(cudaMemsetAsync(d_flag, 0, g8, s), "flags");
-  ensure_pinned(op, total + 64);
-  char* pin = static_cast<char*>(op->pinned);
-  auto fetch = [&](size_t off, size_t bytes) {
-    check(cudaMemcpyAsync(pin + off, sc + off, bytes, cudaMemcpyDeviceToHost, s), "batched readback");
-    check(cudaStreamSynchronize(s), "batched sync");
-  };
-  auto put = [&](size_t off, const void* src, size_t bytes) {
-    // pinned staging is reused: the previous upload must have been consumed
-    check(cudaStreamSynchronize(s), "batched sync");
-    std::memcpy(pin + off, src, bytes);
-    check(cudaMemcpyAsync(sc + off, pin + off, bytes, cudaMemcpyHostToDevice, s), "batched upload");
-  };
-  auto get_d = [&](size_t off, int r) {
-    double v;
-    std::memcpy(&v, pin + off + 8 * static_cast<size_t>(r), 8);
-    return v;
-  };
-  auto get_c = [&](size_t off, size_t idx) {
-    c64 v;
-    std::memcpy(&v, pin + off + 16 * idx, 16);
-    return cd(v.x, v.y);
-  };
-  auto set_mask = [&](const std::vector<int>& on) {
-    std::vector<int> mk(G, 0);
-    for (int r : on) mk[r] = 1;
-    put(o_mask, mk.data(), 4 * static_cast<size_t>(G));
-  };
-  auto flags_of = [&](const std::vector<int>& rs) {
-    for (int r : rs) {
-      int fl;
-      std::memcpy(&fl, pin + o_flag + 4 * static_cast<size_t>(r), 4);
-      if (fl) fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
-    }
-  };
-  // y = A x for the listed RHS (packed unless the list is 0..G-1)
-  auto apply_set = [&](const c64* src_base, c64* dst_base, const std::vector<int>& rs) {
-    const int cnt = static_cast<int>(rs.size());
-    bool all = cnt == G;
-    for (int q = 0; all && q < cnt; ++q) all = rs[q] == q;
-    if (all) {
-      apply_device(op, src_base, dst_base, G);
-      return;
-    }
-    put(o_idx, rs.data(), 4 * static_cast<size_t>(cnt));
-    check(launch_b_pack(src_base, P, d_idx, cnt, n, true, s), "pack");
-    apply_device(op, P, Q, cnt);
-    check(launch_b_pack(Q, dst_base, d_idx, cnt, n, false, s), "unpack");
-    op->launches += 2;
-  };
-
-  check(cudaMemsetAsync(Xd, 0, vecb * G, s), "x0");
-  std::vector<int> all(G);
-  for (int r = 0; r < G; ++r) all[r] = r;
-  set_mask(all);
-  check(launch_b_sqnorm(Bd, n, n, G, d_mask, bs, d_bn, nullptr, s), "bnorm");
-  fetch(o_bn, g8);
-  std::vector<double> bnorm(G), rnorm(G);
-  std::vector<char> done(G, 0);
-  for (int r = 0; r < G; ++r) {
-    bnorm[r] = std::sqrt(get_d(o_bn, r));
-    rnorm[r] = bnorm[r];
-    if (bnorm[r] == 0.0) {
-      out.converged[r] = 1;
-      done[r] = 1;
-    }
-  }
-  const size_t hsz = static_cast<size_t>(m + 1) * m;
-  std::vector<std::vector<cd>> H(G, std::vector<cd>(hsz)), g(G, std::vector<cd>(m + 1));
-  std::vector<std::vector<double>> gc(G, std::vector<double>(m));
-  std::vector<std::vector<cd>> gs(G, std::vector<cd>(m));
-  std::vector<int> jr(G, 0);
-  std::vector<char> inner(G, 0);
-  const c64* rsrc = Bd;
-
-  while (true) {
-    std::vector<int> act;
-    for (int r = 0; r < G; ++r)
-      if (!done[r] && out.iterations[r] < max_iter) act.push_back(r);
-    if (act.empty()) break;
-    set_mask(act);
-    put(o_d, rnorm.data(), g8);
-    check(launch_b_div(rsrc, V, n, n, G, d_mask, d_d, s), "v0");  // v0 = r / ||r||
-    for (int r : act) {
-      std::fill(g[r].begin(), g[r].end(), cd(0, 0));
-      g[r][0] = rnorm[r];
-      std::fill(H[r].begin(), H[r].end(), cd(0, 0));
-      jr[r] = 0;
-      inner[r] = 1;
-    }
-    for (int j = 0; j < m; ++j) {
-      std::vector<int> it;
-      for (int r : act)
-        if (inner[r] && out.iterations[r] < max_iter) it.push_back(r);
-      if (it.empty()) break;
-      c64* Vj = V + static_cast<long long>(j) * G * n;
-      c64* W = V + static_cast<long long>(j + 1) * G * n;
-      apply_set(Vj, W, it);
-      set_mask(it);
-      check(launch_b_sqnorm(W, n, n, G, d_mask, bs, d_pre, d_flag, s), "pre norm");
-      check(launch_b_dotc(V, W, n, n, G, d_mask, bs, d_h, s), "mgs dot");
-      for (int i = 0; i < j; ++i)
-        check(launch_b_axpy_dotc(W, V + static_cast<long long>(i) * G * n, d_h + static_cast<long long>(i) * G,
-                                 V + static_cast<long long>(i + 1) * G * n, n, n, G, d_mask, bs,
-                                 d_h + static_cast<long long>(i + 1) * G, s),
-              "mgs step");
-      check(launch_b_axpy_sqnorm(W, Vj, d_h + static_cast<long long>(j) * G, n, n, G, d_mask, bs, d_post, s),
-            "mgs last");
-      op->launches += j + 3;
-      fetch(0, o_h + 16 * static_cast<size_t>(j + 1) * G);  // flags, norms and h_0..h_j of every RHS
-      flags_of(it);
-      std::vector<int> reo;
-      std::vector<double> wn2(G, 0.0);
-      for (int r : it) {
-        for (int i = 0; i <= j; ++i)
-          H[r][static_cast<size_t>(j) * (m + 1) + i] = get_c(o_h, static_cast<size_t>(i) * G + r);
-        wn2[r] = get_d(o_post, r);
-        if (std::sqrt(wn2[r]) < 0.5 * std::sqrt(get_d(o_pre, r))) reo.push_back(r);  // (:63-69)
-      }
-      if (!reo.empty()) {
-        set_mask(reo);
-        check(launch_b_dotc(V, W, n, n, G, d_mask, bs, d_hc, s), "reorth dot");
-        for (int i = 0; i < j; ++i)
-          check(launch_b_axpy_dotc(W, V + static_cast<long long>(i) * G * n, d_hc + static_cast<long long>(i) * G,
-                                   V + static_cast<long long>(i + 1) * G * n, n, n, G, d_mask, bs,
-                                   d_hc + static_cast<long long>(i + 1) * G, s),
-                "reorth step");
-        check(launch_b_axpy_sqnorm(W, Vj, d_hc + static_cast<long long>(j) * G, n, n, G, d_mask, bs, d_post2, s),
-              "reorth last");
-        op->launches += j + 2;
-        fetch(o_post2, g8);
-        fetch(o_hc, 16 * static_cast<size_t>(j + 1) * G);
-        for (int r : reo) {
-          for (int i = 0; i <= j; ++i)
-            H[r][static_cast<size_t>(j) * (m + 1) + i] += get_c(o_hc, static_cast<size_t>(i) * G + r);
-          wn2[r] = get_d(o_post2, r);
-        }
-      }
-      std::vector<double> hl(G, 1.0);
-      std::vector<int> norm_set;
-      for (int r : it) {
-        hl[r] = std::sqrt(wn2[r]);
-        if (hl[r] > 0.0) norm_set.push_back(r);
-      }
-      if (!norm_set.empty()) {
-        set_mask(norm_set);
-        put(o_d, hl.data(), g8);
-        check(launch_b_div(W, W, n, n, G, d_mask, d_d, s), "normalise");
-        op->launches++;
-      }
-      for (int r : it) {  // rotations, Givens, estimate (:74-105), per RHS
-        auto Hm = [&](int a, int b) -> cd& { return H[r][static_cast<size_t>(b) * (m + 1) + a]; };
-        const double hlast = hl[r];
-        Hm(j + 1, j) = hlast;
-        for (int i = 0; i < j; ++i) {
-          cd t = gc[r][i] * Hm(i, j) + gs[r][i] * Hm(i + 1, j);
-          Hm(i + 1, j) = -std::conj(gs[r][i]) * Hm(i, j) + gc[r][i] * Hm(i + 1, j);
-          Hm(i, j) = t;
-        }
-        const cd a = Hm(j, j);
-        const double bb = std::abs(Hm(j + 1, j));
-        const double denom = std::hypot(std::abs(a), bb);
-        if (denom == 0.0) {
-          gc[r][j] = 1.0;
-          gs[r][j] = cd(0, 0);
-        } else if (std::abs(a) == 0.0) {
-          gc[r][j] = 0.0;
-          gs[r][j] = cd(1, 0);
-        } else {
-          gc[r][j] = std::abs(a) / denom;
-          gs[r][j] = (a / std::abs(a)) * std::conj(Hm(j + 1, j)) / denom;
-        }
-        Hm(j, j) = gc[r][j] * a + gs[r][j] * Hm(j + 1, j);
-        Hm(j + 1, j) = cd(0, 0);
-        const cd gj = g[r][j];
-        g[r][j] = gc[r][j] * gj;
-        g[r][j + 1] = -std::conj(gs[r][j]) * gj;
-        ++out.iterations[r];
-        const double est = std::abs(g[r][j + 1]) / bnorm[r];
-        out.history[r].push_back(est);
-        jr[r] = j + 1;
-        if (est <= tol || hlast == 0.0) inner[r] = 0;
-      }
-    }
-    // x_r += V_r y_r for every RHS of the cycle, then the true residuals (:109-116)
-    std::vector<c64> yh(static_cast<size_t>(m) * G, cmk(0.0, 0.0));
-    for (int r : act) {
-      auto Hm = [&](int a, int b) -> cd& { return H[r][static_cast<size_t>(b) * (m + 1) + a]; };
-      const int jj = jr[r];
-      std::vector<cd> y(jj);
-      for (int i = jj - 1; i >= 0; --i) {
-        cd acc = g[r][i];
-        for (int k = i + 1; k < jj; ++k) acc -= Hm(i, k) * y[k];
-        y[i] = acc / Hm(i, i);
-      }
-      for (int i = 0; i < jj; ++i) yh[static_cast<size_t>(r) * m + i] = cmk(y[i].real(), y[i].imag());
-    }
-    put(o_y, yh.data(), 16 * yh.size());
-    put(o_jr, jr.data(), 4 * static_cast<size_t>(G));
-    set_mask(act);
-    check(launch_b_update_x(Xd, V, G, n, d_y, m, d_jr, n, d_mask, s), "x update");
-    apply_set(Xd, T, act);
-    set_mask(act);
-    check(launch_b_residual(Bd, T, R, n, n, G, d_mask, bs, d_rn, d_flag, s), "residual");
-    op->launches += 2;
-    fetch(0, o_pre);
-    flags_of(act);
-    fetch(o_rn, g8);
-    for (int r : act) {
-      rnorm[r] = std::sqrt(get_d(o_rn, r));
-      if (rnorm[r] / bnorm[r] <= tol) {
-        out.converged[r] = 1;
-        done[r] = 1;
-      }
-    }
-    rsrc = R;
-  }
-  for (int r = 0; r < G; ++r)
-    if (!out.history[r].empty()) out.converged[r] = out.converged[r] || rnorm[r] / bnorm[r] <= tol;
-  check(cudaStreamSynchronize(s), "batched gmres");
-  return out;
-}
-
-}  // namespace
-
-namespace {
-int guard(const std::function<void()>& fn) {
-  try {
-    fn();
-    return FPBEM_CU_OK;
-  } catch (const Fail& f) {
-    return f.code;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return FPBEM_CU_EINVAL;
-  }
-}
-}  // namespace
+}  // namespace fpbem_cu
 
 extern "C" {
 
@@ -1315,76 +651,6 @@ int fpbem_cu_fmm_apply(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int nr
   });
 }
 
-int fpbem_cu_gmres(fpbem_cu_op* op, const fpbem_c64* b, fpbem_c64* x, int nrhs, double tol, int restart,
-                   int max_iter, int ptr_kind, int* iterations, int* converged, double* history, int history_cap,
-                   int* history_len) {
-  return guard([&] {
-    if (!op || !b || !x || !iterations || !converged) fail(FPBEM_CU_EINVAL, "gmres: null argument");
-    if (nrhs < 1) fail(FPBEM_CU_EDIM, "gmres: nrhs >= 1 required");
-    check(cudaSetDevice(op->device), "set device");
-    ensure_gmres(op, std::max(1, restart));
-    const char* lock = std::getenv("FPBEM_GMRES_BATCHED");
-    const bool batched = nrhs > 1 && !(lock && std::strcmp(lock, "0") == 0);
-    if (batched) {  // lockstep batch over all right-hand sides
-      const size_t bytes = static_cast<size_t>(op->N) * nrhs * sizeof(c64);
-      const c64* bd;
-      c64* xd;
-      c64* tmp_b = nullptr;
-      c64* tmp_x = nullptr;
-      if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
-        bd = reinterpret_cast<const c64*>(b);
-        xd = reinterpret_cast<c64*>(x);
-      } else {
-        tmp_b = dalloc<c64>(static_cast<size_t>(op->N) * nrhs, "batched b");
-        tmp_x = dalloc<c64>(static_cast<size_t>(op->N) * nrhs, "batched x");
-        h2d(tmp_b, b, bytes, op->stream, "b upload");
-        bd = tmp_b;
-        xd = tmp_x;
-      }
-      std::unique_ptr<c64, decltype(&cudaFree)> kb(tmp_b, &cudaFree), kx(tmp_x, &cudaFree);
-      BatchOut o = gmres_batched(op, bd, xd, nrhs, tol, restart, max_iter);
-      for (int r = 0; r < nrhs; ++r) {
-        iterations[r] = o.iterations[r];
-        converged[r] = o.converged[r];
-        if (history_len) history_len[r] = static_cast<int>(o.history[r].size());
-        if (history)
-          for (int i = 0; i < std::min(history_cap, static_cast<int>(o.history[r].size())); ++i)
-            history[static_cast<size_t>(r) * history_cap + i] = o.history[r][i];
-      }
-      if (ptr_kind != FPBEM_CU_PTR_DEVICE)
-        check(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, op->stream), "x download");
-      check(cudaStreamSynchronize(op->stream), "gmres sync");
-      return;
-    }
-    for (int r = 0; r < nrhs; ++r) {
-      const size_t off = static_cast<size_t>(r) * op->N;
-      const c64* bd;
-      c64* xd;
-      if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
-        bd = reinterpret_cast<const c64*>(b) + off;
-        xd = reinterpret_cast<c64*>(x) + off;
-      } else {
-        check(cudaMemcpyAsync(op->gb, b + off, op->N * sizeof(c64), cudaMemcpyHostToDevice, op->stream), "b upload");
-        bd = op->gb;
-        xd = op->gsol;
-      }
-      GmresOut o = gmres_one(
-          op, [op](const c64* in, c64* out) { apply_device(op, in, out, 1); }, bd, xd, tol, restart, max_iter);
-      iterations[r] = o.iterations;
-      converged[r] = o.converged ? 1 : 0;
-      if (history_len) history_len[r] = static_cast<int>(o.history.size());
-      if (history)
-        for (int i = 0; i < std::min(history_cap, static_cast<int>(o.history.size())); ++i)
-          history[static_cast<size_t>(r) * history_cap + i] = o.history[i];
-      if (ptr_kind != FPBEM_CU_PTR_DEVICE) {
-        check(cudaMemcpyAsync(x + off, xd, op->N * sizeof(c64), cudaMemcpyDeviceToHost, op->stream), "x download");
-        check(cudaStreamSynchronize(op->stream), "gmres sync");
-      }
-    }
-    check(cudaStreamSynchronize(op->stream), "gmres sync");
-  });
-}
-
 int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes) {
   if (!op || !bytes) {
     g_err = "bytes: null argument";
@@ -1445,430 +711,5 @@ int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out) {
 }
 
 long long fpbem_cu_kernel_launches(const fpbem_cu_op* op) { return op ? op->launches : 0; }
-
-int fpbem_cu_gmres_fn(int device, long long n, fpbem_cu_apply_fn apply, void* actx, fpbem_cu_apply_fn precond,
-                      void* pctx, const fpbem_c64* b, fpbem_c64* x, double tol, int restart, int max_iter,
-                      int ptr_kind, int* iterations, int* converged, double* history, int history_cap,
-                      int* history_len) {
-  fpbem_cu_op* op = nullptr;
-  int rc = guard([&] {
-    if (!apply || !b || !x || !iterations || !converged || n < 1) fail(FPBEM_CU_EINVAL, "gmres_fn: bad argument");
-    check(cudaSetDevice(device), "set device");
-    op = new fpbem_cu_op();
-    op->device = device;
-    op->N = n;
-    check(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
-    op->own_stream = true;
-    ensure_gmres(op, std::max(1, restart));
-    c64* pre_tmp = precond ? dalloc<c64>(n, "precond scratch") : nullptr;
-    std::unique_ptr<c64, decltype(&cudaFree)> keep(pre_tmp, &cudaFree);
-    auto call = [&](fpbem_cu_apply_fn fn, void* ctx, const c64* in, c64* out) {
-      if (fn(ctx, reinterpret_cast<const fpbem_c64*>(in), reinterpret_cast<fpbem_c64*>(out), op->stream) != 0)
-        fail(FPBEM_CU_EINVAL, "gmres: operator callback failed");
-    };
-    ApplyDev eff = [&](const c64* in, c64* out) {
-      if (precond) {
-        call(apply, actx, in, pre_tmp);
-        check(launch_sqnorm(pre_tmp, n, op->rs, op->scal_d + 4, op->flag, op->stream), "finite check");
-        call(precond, pctx, pre_tmp, out);
-      } else {
-        call(apply, actx, in, out);
-      }
-    };
-    const c64* bd;
-    c64* xd;
-    if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
-      bd = reinterpret_cast<const c64*>(b);
-      xd = reinterpret_cast<c64*>(x);
-    } else {
-      check(cudaMemcpyAsync(op->gb, b, n * sizeof(c64), cudaMemcpyHostToDevice, op->stream), "b upload");
-      bd = op->gb;
-      xd = op->gsol;
-    }
-    if (precond) {  // b_eff = M^{-1} b, checked (src/solver.cpp:30)
-      call(precond, pctx, bd, op->gt);
-      check(cudaMemsetAsync(op->flag, 0, sizeof(int), op->stream), "flag");
-      check(launch_sqnorm(op->gt, n, op->rs, op->scal_d + 4, op->flag, op->stream), "finite check");
-      int f = 0;
-      check(cudaMemcpyAsync(op->pinned, op->flag, sizeof(int), cudaMemcpyDeviceToHost, op->stream), "flag");
-      check(cudaStreamSynchronize(op->stream), "sync");
-      std::memcpy(&f, op->pinned, sizeof(int));
-      if (f) fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
-      check(cudaMemcpyAsync(op->gb, op->gt, n * sizeof(c64), cudaMemcpyDeviceToDevice, op->stream), "b_eff");
-      bd = op->gb;
-    }
-    GmresOut o = gmres_one(op, eff, bd, xd, tol, restart, max_iter);
-    *iterations = o.iterations;
-    *converged = o.converged ? 1 : 0;
-    if (history_len) *history_len = static_cast<int>(o.history.size());
-    if (history)
-      for (int i = 0; i < std::min(history_cap, static_cast<int>(o.history.size())); ++i) history[i] = o.history[i];
-    if (ptr_kind != FPBEM_CU_PTR_DEVICE)
-      check(cudaMemcpyAsync(x, xd, n * sizeof(c64), cudaMemcpyDeviceToHost, op->stream), "x download");
-    check(cudaStreamSynchronize(op->stream), "gmres sync");
-  });
-  fpbem_cu_fmm_destroy(op);
-  return rc;
-}
-
-namespace {
-
-// Gauss-Legendre nodes/weights by Newton on P_n (the host rule, kernels.cpp:162-194)
-void gauss_rule(int n, double* x, double* w) {
-  for (int i = 0; i < (n + 1) / 2; ++i) {
-    double z = std::cos(3.14159265358979323846 * (i + 0.75) / (n + 0.5));
-    double dp = 0.0;
-    for (int it = 0; it < 100; ++it) {
-      double p0 = 1.0, p1 = 0.0;
-      for (int j = 0; j < n; ++j) {
-        const double p2 = p1;
-        p1 = p0;
-        p0 = ((2.0 * j + 1.0) * z * p1 - j * p2) / (j + 1);
-      }
-      dp = n * (z * p0 - p1) / (z * z - 1.0);
-      const double dz = p0 / dp;
-      z -= dz;
-      if (std::abs(dz) < 1e-15) break;
-    }
-    x[i] = -z;
-    x[n - 1 - i] = z;
-    w[i] = w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
-  }
-}
-
-struct CellDev {
-  double* corners = nullptr;
-  int* nv = nullptr;
-  double* cen = nullptr;
-  double* nrm = nullptr;
-  double* diam = nullptr;
-  c64* beta = nullptr;
-  ~CellDev() {
-    for (void* p : {static_cast<void*>(corners), static_cast<void*>(nv), static_cast<void*>(cen),
-                    static_cast<void*>(nrm), static_cast<void*>(diam), static_cast<void*>(beta)})
-      if (p) cudaFree(p);
-  }
-};
-
-void upload_cell(const fpbem_cu_cell* c, CellDev& d, cudaStream_t s) {
-  if (!c || c->n < 1 || !c->corners || !c->nv || !c->centroid || !c->normal || !c->diameter)
-    fail(FPBEM_CU_EINVAL, "assemble: bad cell");
-  const size_t n = static_cast<size_t>(c->n);
-  d.corners = dalloc<double>(12 * n, "cell corners");
-  d.nv = dalloc<int>(n, "cell nv");
-  d.cen = dalloc<double>(3 * n, "cell centroids");
-  d.nrm = dalloc<double>(3 * n, "cell normals");
-  d.diam = dalloc<double>(n, "cell diameters");
-  h2d(d.corners, c->corners, 12 * n * sizeof(double), s, "cell upload");
-  h2d(d.nv, c->nv, n * sizeof(int), s, "cell upload");
-  h2d(d.cen, c->centroid, 3 * n * sizeof(double), s, "cell upload");
-  h2d(d.nrm, c->normal, 3 * n * sizeof(double), s, "cell upload");
-  h2d(d.diam, c->diameter, n * sizeof(double), s, "cell upload");
-  if (c->beta) {
-    d.beta = dalloc<c64>(n, "cell beta");
-    h2d(d.beta, c->beta, n * sizeof(c64), s, "cell upload");
-  }
-  double x6[6], w6[6], x8[8], w8[8];
-  gauss_rule(6, x6, w6);
-  gauss_rule(8, x8, w8);
-  check(assembly_set_rules(x6, w6, x8, w8), "quadrature rules");
-}
-
-// run the slots (two passes: plain, then accumulated images) into out
-void run_assembly(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, int hs_axis, double hs_offset,
-                  const std::vector<AssemblySlot>& plain, const std::vector<AssemblySlot>& images, int device,
-                  fpbem_c64* out, int ptr_kind) {
-  check(cudaSetDevice(device), "set device");
-  cudaStream_t s;
-  check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-  std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
-  CellDev dc;
-  upload_cell(cell, dc, s);
-  const size_t n = static_cast<size_t>(cell->n);
-  const size_t total = plain.size() * n * n;
-  c64* dst = reinterpret_cast<c64*>(out);
-  c64* tmp = nullptr;
-  if (ptr_kind != FPBEM_CU_PTR_DEVICE) dst = tmp = dalloc<c64>(total, "assembly output");
-  std::unique_ptr<c64, decltype(&cudaFree)> keep_tmp(tmp, &cudaFree);
-  AssemblySlot* ds = dalloc<AssemblySlot>(plain.size() + images.size(), "assembly slots");
-  std::unique_ptr<AssemblySlot, decltype(&cudaFree)> keep_ds(ds, &cudaFree);
-  h2d(ds, plain.data(), plain.size() * sizeof(AssemblySlot), s, "slots");
-  if (!images.empty()) h2d(ds + plain.size(), images.data(), images.size() * sizeof(AssemblySlot), s, "slots");
-  const c64 al = cmk(alpha.re, alpha.im);
-  // z-chunks of at most 65535 slots per launch (grid.z limit)
-  for (size_t s0 = 0; s0 < plain.size(); s0 += 65535) {
-    const int cnt = static_cast<int>(std::min<size_t>(65535, plain.size() - s0));
-    check(launch_assemble(dc.corners, dc.nv, dc.cen, dc.nrm, dc.diam, dc.beta, cell->n, ds + s0, cnt, k, al, hs_axis,
-                          hs_offset, dst + s0 * n * n, false, s),
-          "assemble");
-  }
-  for (size_t s0 = 0; s0 < images.size(); s0 += 65535) {
-    const int cnt = static_cast<int>(std::min<size_t>(65535, images.size() - s0));
-    check(launch_assemble(dc.corners, dc.nv, dc.cen, dc.nrm, dc.diam, dc.beta, cell->n, ds + plain.size() + s0, cnt, k,
-                          al, hs_axis, hs_offset, dst + s0 * n * n, true, s),
-          "assemble images");
-  }
-  if (ptr_kind != FPBEM_CU_PTR_DEVICE)
-    check(cudaMemcpyAsync(out, dst, total * sizeof(c64), cudaMemcpyDeviceToHost, s), "assembly download");
-  check(cudaStreamSynchronize(s), "assembly");
-}
-
-AssemblySlot make_slot(const double t[3], const double src[3], c64 scale, int mirror, int self) {
-  AssemblySlot sl;
-  for (int d = 0; d < 3; ++d) {
-    sl.tshift[d] = t[d];
-    sl.sshift[d] = src[d];
-  }
-  sl.scale = scale;
-  sl.mirror = mirror;
-  sl.self = self;
-  return sl;
-}
-
-}  // namespace
-
-int fpbem_cu_assemble_near(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, const double pitch[3], int n_off,
-                           const int* offsets, int fold, int hs_axis, double hs_offset, fpbem_c64 hs_reflection,
-                           int device, fpbem_c64* out, int ptr_kind) {
-  return guard([&] {
-    if (!pitch || (n_off > 0 && (!offsets || !out))) fail(FPBEM_CU_EINVAL, "assemble_near: null argument");
-    std::vector<AssemblySlot> plain, images;
-    const double zero[3] = {0, 0, 0};
-    const bool with_image = fold && (hs_reflection.re != 0.0 || hs_reflection.im != 0.0);
-    for (int s = 0; s < n_off; ++s) {
-      const int* o = offsets + 3 * s;
-      const double t[3] = {o[0] * pitch[0], o[1] * pitch[1], o[2] * pitch[2]};
-      const int self = o[0] == 0 && o[1] == 0 && o[2] == 0;
-      plain.push_back(make_slot(t, zero, cmk(1.0, 0.0), 0, self));
-      if (with_image) images.push_back(make_slot(t, zero, cmk(hs_reflection.re, hs_reflection.im), 1, 0));
-    }
-    run_assembly(cell, k, alpha, hs_axis, hs_offset, plain, images, device, out, ptr_kind);
-  });
-}
-
-int fpbem_cu_assemble_hat(const fpbem_cu_cell* cell, double k, fpbem_c64 alpha, const double pitch[3],
-                          const int counts[3], int n_hat, const int* hat_indices, int hs_axis, double hs_offset,
-                          fpbem_c64 hs_reflection, int device, fpbem_c64* out, int ptr_kind) {
-  return guard([&] {
-    if (!pitch || !counts || (n_hat > 0 && (!hat_indices || !out))) fail(FPBEM_CU_EINVAL, "assemble_hat: null");
-    if (hs_axis < 0 || hs_axis > 2) fail(FPBEM_CU_EINVAL, "assemble_hat: bad axis");
-    std::vector<AssemblySlot> plain, images;
-    for (int h = 0; h < n_hat; ++h) {
-      const int* idx = hat_indices + 3 * h;
-      int tgt[3] = {idx[0], idx[1], idx[2]}, src[3] = {0, 0, 0};
-      tgt[hs_axis] = std::min(idx[hs_axis], counts[hs_axis] - 1);
-      src[hs_axis] = idx[hs_axis] - tgt[hs_axis];
-      const double t[3] = {tgt[0] * pitch[0], tgt[1] * pitch[1], tgt[2] * pitch[2]};
-      const double sv[3] = {src[0] * pitch[0], src[1] * pitch[1], src[2] * pitch[2]};
-      plain.push_back(make_slot(t, sv, cmk(hs_reflection.re, hs_reflection.im), 1, 0));
-    }
-    run_assembly(cell, k, alpha, hs_axis, hs_offset, plain, images, device, out, ptr_kind);
-  });
-}
-
-int fpbem_cu_evaluate_field(const fpbem_cu_cell* cell, double k, const double pitch[3], const int counts[3],
-                            const fpbem_c64* solution, int n_points, const double* points,
-                            const fpbem_c64* p_incident, int hs_axis, double hs_offset, fpbem_c64 hs_reflection,
-                            int device, fpbem_c64* out, int ptr_kind) {
-  return guard([&] {
-    if (!cell || !pitch || !counts || (n_points > 0 && (!points || !out || !solution)))
-      fail(FPBEM_CU_EINVAL, "evaluate_field: null argument");
-    if (n_points < 0 || counts[0] < 1 || counts[1] < 1 || counts[2] < 1)
-      fail(FPBEM_CU_EDIM, "evaluate_field: bad counts or point count");
-    const bool with_image = hs_reflection.re != 0.0 || hs_reflection.im != 0.0;
-    if (with_image && (hs_axis < 0 || hs_axis > 2)) fail(FPBEM_CU_EINVAL, "evaluate_field: bad half-space axis");
-    if (n_points == 0) return;
-    check(cudaSetDevice(device), "set device");
-    cudaStream_t s;
-    check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
-    CellDev dc;
-    upload_cell(cell, dc, s);
-    const long long n_total = static_cast<long long>(cell->n) * counts[0] * counts[1] * counts[2];
-    const bool dev = ptr_kind == FPBEM_CU_PTR_DEVICE;
-    double* dp = dalloc<double>(3 * static_cast<size_t>(n_points), "field points");
-    std::unique_ptr<double, decltype(&cudaFree)> keep_p(dp, &cudaFree);
-    h2d(dp, points, 3 * static_cast<size_t>(n_points) * sizeof(double), s, "field points");
-    const c64* sol = reinterpret_cast<const c64*>(solution);
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_sol(nullptr, &cudaFree);
-    if (!dev) {
-      keep_sol.reset(dalloc<c64>(static_cast<size_t>(n_total), "field solution"));
-      h2d(keep_sol.get(), solution, static_cast<size_t>(n_total) * sizeof(c64), s, "field solution");
-      sol = keep_sol.get();
-    }
-    const c64* pinc = reinterpret_cast<const c64*>(p_incident);
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_pinc(nullptr, &cudaFree);
-    if (!dev && p_incident) {
-      keep_pinc.reset(dalloc<c64>(static_cast<size_t>(n_points), "incident values"));
-      h2d(keep_pinc.get(), p_incident, static_cast<size_t>(n_points) * sizeof(c64), s, "incident values");
-      pinc = keep_pinc.get();
-    }
-    c64* partial = dalloc<c64>(static_cast<size_t>(field_chunks(n_total)) * n_points, "field partial sums");
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_part(partial, &cudaFree);
-    c64* dst = reinterpret_cast<c64*>(out);
-    c64* out_tmp = nullptr;
-    if (!dev) dst = out_tmp = dalloc<c64>(static_cast<size_t>(n_points), "field output");
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_out(out_tmp, &cudaFree);
-    check(launch_field(dc.corners, dc.nv, dc.cen, dc.nrm, dc.diam, dc.beta, cell->n, counts, pitch, sol, dp, n_points,
-                       pinc, k, with_image, hs_axis, hs_offset, cmk(hs_reflection.re, hs_reflection.im), partial, dst,
-                       s),
-          "field evaluation");
-    if (!dev) check(cudaMemcpyAsync(out, dst, static_cast<size_t>(n_points) * sizeof(c64), cudaMemcpyDeviceToHost, s),
-                    "field download");
-    check(cudaStreamSynchronize(s), "field evaluation");
-  });
-}
-
-int fpbem_cu_m2l_bank(int n_t, double k, int n_blk, const double* delta, const double* image_delta,
-                      int parity_axis, fpbem_c64 reflection, int device, fpbem_c64* out, int ptr_kind) {
-  return guard([&] {
-    if (n_t < 0 || n_t > far_bank_max_nt()) fail(FPBEM_CU_EINVAL, "m2l_bank: n_t out of range");
-    if (n_blk < 0 || (n_blk > 0 && (!out || (!delta && !image_delta))))
-      fail(FPBEM_CU_EINVAL, "m2l_bank: null argument");
-    if (image_delta && (parity_axis < 0 || parity_axis > 2)) fail(FPBEM_CU_EINVAL, "m2l_bank: bad parity axis");
-    if (!std::isfinite(k) || k <= 0.0) fail(FPBEM_CU_EINVAL, "m2l_bank: wavenumber must be positive");
-    for (const double* v : {delta, image_delta}) {
-      if (!v) continue;
-      for (int s = 0; s < n_blk; ++s) {
-        const double r2 = v[3 * s] * v[3 * s] + v[3 * s + 1] * v[3 * s + 1] + v[3 * s + 2] * v[3 * s + 2];
-        if (!(r2 > 0.0) || !std::isfinite(r2))  // solid_singular: evaluation at the singularity
-          fail(FPBEM_CU_EINVAL, "m2l_bank: zero or non-finite translation vector");
-      }
-    }
-    if (n_blk == 0) return;
-    check(cudaSetDevice(device), "set device");
-    cudaStream_t s;
-    check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> keep_s(s, [](cudaStream_t st) { cudaStreamDestroy(st); });
-    const size_t b = static_cast<size_t>(n_t + 1) * (n_t + 1), total = static_cast<size_t>(n_blk) * b * b;
-    std::unique_ptr<double, decltype(&cudaFree)> keep_d(nullptr, &cudaFree), keep_i(nullptr, &cudaFree);
-    if (delta) {
-      keep_d.reset(dalloc<double>(3 * static_cast<size_t>(n_blk), "bank deltas"));
-      h2d(keep_d.get(), delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank deltas");
-    }
-    if (image_delta) {
-      keep_i.reset(dalloc<double>(3 * static_cast<size_t>(n_blk), "bank image deltas"));
-      h2d(keep_i.get(), image_delta, 3 * static_cast<size_t>(n_blk) * sizeof(double), s, "bank image deltas");
-    }
-    const double* dd = keep_d.get();
-    const double* di = keep_i.get();
-    c64* dst = reinterpret_cast<c64*>(out);
-    c64* tmp = nullptr;
-    if (ptr_kind != FPBEM_CU_PTR_DEVICE) dst = tmp = dalloc<c64>(total, "bank output");
-    std::unique_ptr<c64, decltype(&cudaFree)> keep_tmp(tmp, &cudaFree);
-    check(launch_far_bank(device, n_t, k, n_blk, dd, di, parity_axis, cmk(reflection.re, reflection.im), dst, s),
-          "m2l bank");
-    if (ptr_kind != FPBEM_CU_PTR_DEVICE)
-      check(cudaMemcpyAsync(out, dst, total * sizeof(c64), cudaMemcpyDeviceToHost, s), "bank download");
-    check(cudaStreamSynchronize(s), "m2l bank");
-  });
-}
-
-int fpbem_cu_comm_unique_id(unsigned char id_out[128]) {
-  return guard([&] {
-    void* lib = load_nccl();
-    if (!lib) fail(FPBEM_CU_ENCCL, "libnccl.so.2 not loadable");
-    auto get_id = reinterpret_cast<int (*)(void*)>(dlsym(lib, "ncclGetUniqueId"));
-    if (!get_id) fail(FPBEM_CU_ENCCL, "ncclGetUniqueId missing");
-    if (get_id(id_out) != 0) fail(FPBEM_CU_ENCCL, "ncclGetUniqueId failed");
-  });
-}
-
-int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int device, fpbem_cu_comm** out) {
-  return guard([&] {
-    void* lib = load_nccl();
-    if (!lib) fail(FPBEM_CU_ENCCL, "libnccl.so.2 not loadable");
-    struct IdBlob {
-      unsigned char b[128];
-    } blob;
-    std::memcpy(blob.b, id, 128);
-    auto init = reinterpret_cast<int (*)(void**, int, IdBlob, int)>(dlsym(lib, "ncclCommInitRank"));
-    auto* c = new fpbem_cu_comm();
-    c->lib = lib;
-    c->nranks = nranks;
-    c->rank = rank;
-    c->device = device;
-    c->allreduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, void*)>(
-        dlsym(lib, "ncclAllReduce"));
-    c->destroy = reinterpret_cast<int (*)(void*)>(dlsym(lib, "ncclCommDestroy"));
-    if (!init || !c->allreduce || !c->destroy) {
-      delete c;
-      fail(FPBEM_CU_ENCCL, "NCCL symbols missing");
-    }
-    check(cudaSetDevice(device), "set device");
-    if (init(&c->comm, nranks, blob, rank) != 0) {
-      delete c;
-      fail(FPBEM_CU_ENCCL, "ncclCommInitRank failed");
-    }
-    *out = c;
-  });
-}
-
-void fpbem_cu_comm_destroy(fpbem_cu_comm* comm) {
-  if (!comm) return;
-  if (comm->comm && comm->destroy) comm->destroy(comm->comm);
-  delete comm;
-}
-
-int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm) {
-  return guard([&] {
-    if (!op) fail(FPBEM_CU_EINVAL, "set_comm: null op");
-    check(cudaSetDevice(op->device), "set device");
-    if (!comm) {
-      op->comm = nullptr;
-      set_partition(op, 0, 1, 0.0);
-      return;
-    }
-    // rank 0's far-field cost in pair equivalents, averaged over the ranks so
-    // that every rank derives the same partition
-    double f = comm->nranks > 1 ? calibrate_far_pairs(op) : 0.0;
-    if (comm->nranks > 1) {
-      double* df = dalloc<double>(1, "far pairs");
-      std::unique_ptr<double, decltype(&cudaFree)> keep_df(df, &cudaFree);
-      h2d(df, &f, sizeof(double), op->stream, "far pairs");
-      const int rc = comm->allreduce(df, df, 1, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm->comm, op->stream);
-      if (rc != 0) fail(FPBEM_CU_ENCCL, "ncclAllReduce failed: " + std::to_string(rc));
-      check(cudaMemcpyAsync(&f, df, sizeof(double), cudaMemcpyDeviceToHost, op->stream), "far pairs");
-      check(cudaStreamSynchronize(op->stream), "far pairs");
-      f /= comm->nranks;
-    }
-    set_partition(op, comm->rank, comm->nranks, f);
-    op->comm = comm;
-  });
-}
-
-int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
-  return guard([&] {
-    if (!op) fail(FPBEM_CU_EINVAL, "set_partition: null op");
-    check(cudaSetDevice(op->device), "set device");
-    set_partition(op, rank, nranks, far_pairs);
-  });
-}
-
-int fpbem_cu_fmm_partition(const fpbem_cu_op* op, long long* lo, long long* hi, double* far_pairs) {
-  return guard([&] {
-    if (!op || !lo || !hi || !far_pairs) fail(FPBEM_CU_EINVAL, "partition: null argument");
-    *lo = op->pair_lo;
-    *hi = op->pair_hi;
-    *far_pairs = op->far_pairs;
-  });
-}
-
-int fpbem_cu_fmm_far_pairs(fpbem_cu_op* op, double* far_pairs) {
-  return guard([&] {
-    if (!op || !far_pairs) fail(FPBEM_CU_EINVAL, "far_pairs: null argument");
-    check(cudaSetDevice(op->device), "set device");
-    *far_pairs = calibrate_far_pairs(op);
-  });
-}
-
-int fpbem_cu_partition_pairs(long long n_pairs, int nranks, int rank, double far_pairs, long long* lo,
-                             long long* hi) {
-  return guard([&] {
-    if (n_pairs < 0 || nranks < 1 || rank < 0 || rank >= nranks || !lo || !hi || !(far_pairs >= 0.0))
-      fail(FPBEM_CU_EINVAL, "partition: bad args");
-    pair_range(n_pairs, nranks, rank, far_pairs, *lo, *hi);
-  });
-}
 
 }  // extern "C"

@@ -1,0 +1,165 @@
+// Internal to libfpbem_cuda.so (not installed): the operator handle shared by
+// the C-ABI translation units — fpbem_cuda.cu (operator create / apply /
+// spectrum), gmres.cu (device GMRES), device_assembly.cu (near-field blocks,
+// M2L bank, field evaluation) and comm.cu (NCCL, multi-GPU partition).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../include/fpbem_cuda.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fpbem_cu {
+
+inline thread_local std::string g_err;  // fpbem_cu_last_error
+
+struct Fail {
+  int code;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw Fail{code};
+}
+
+inline void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? FPBEM_CU_ENOMEM : FPBEM_CU_ECUDA;
+    fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename T>
+T* dalloc(size_t count, const char* what) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  check(cudaMalloc(&p, count * sizeof(T)), what);
+  return static_cast<T*>(p);
+}
+
+// host->device copy ordered on `stream` (never the legacy default stream,
+// which does not synchronise with the handle's non-blocking stream)
+inline void h2d(void* dst, const void* src, size_t bytes, cudaStream_t stream, const char* what) {
+  if (bytes == 0) return;
+  check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), what);
+  check(cudaStreamSynchronize(stream), what);
+}
+
+// C-ABI body: error code for the caller, message in g_err
+inline int guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return FPBEM_CU_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FPBEM_CU_EINVAL;
+  }
+}
+
+}  // namespace fpbem_cu
+
+using namespace fpbem_cu;  // internal header: the handle below is written in the kernel types
+
+// --------------------------------------------------------------------------
+// NCCL, loaded at runtime so the library has no hard NCCL dependency.
+
+struct fpbem_cu_comm {
+  void* lib = nullptr;
+  void* comm = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0, device = 0;
+  int (*allreduce)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
+  int (*destroy)(void*) = nullptr;
+};
+
+struct fpbem_cu_op {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t aux = nullptr;  // P2M + M2L run here, concurrently with the near-field GEMM
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int counts[3] = {1, 1, 1};
+  int n = 0, b = 0, n_cells = 0;
+  long long N = 0;
+  int max_rhs = 1;
+
+  // near field
+  int n_near = 0;
+  std::vector<int> near_offsets;
+  c64* S = nullptr;
+  int n_pairs = 0;
+  std::vector<int> pair_start;  // per offset slot, n_near + 1
+  int* pair_src = nullptr;
+  int* tgt_ptr = nullptr;
+  int* tgt_pairs = nullptr;
+  int4* jobs = nullptr;  // near-field GEMM jobs followed by the P2M jobs
+  int jobs_nrhs = -1, n_jobs = 0, jobs_cap = 0;
+  double far_pairs = 0.0;  // rank 0's deficit under the pair partition (calibrate_far_pairs)
+  long long pair_lo = 0, pair_hi = 0;  // global pair range this rank computes (all without a partition)
+  std::vector<int> pair_tgt;    // host copy: target cell of every pair
+  int rank = 0, nranks = 1;     // near-field offset partition
+
+  // expansions and spectrum
+  c64* u0 = nullptr;
+  c64* v0 = nullptr;
+  c64* v0t = nullptr;  // V0^T (b rows of n), for the P2M kernel
+  int L[3] = {1, 1, 1};
+  long long q_total = 1;
+  c64* lambda = nullptr;
+  c64* tw[3] = {nullptr, nullptr, nullptr};
+  // half-space image pair: S_hat blocks live in S after the n_near Toeplitz
+  // slots (Hankel-indexed pairs); lambda_hat is the spectrum of K_hat P
+  int mirrored_level = -1;
+  int n_hat = 0;
+  c64* lambda_hat = nullptr;
+  c64* mom_perm = nullptr;
+  c64* loc_hat = nullptr;
+
+  // per-apply buffers (sized for max_rhs)
+  c64* W = nullptr;
+  c64* mom = nullptr;
+  c64* loc = nullptr;
+  c64* fa = nullptr;
+  c64* fb = nullptr;
+  c64* xin = nullptr;   // host-pointer staging
+  c64* yout = nullptr;
+
+  // GMRES
+  c64* basis = nullptr;
+  int basis_cols = 0;
+  c64* gx = nullptr;
+  c64* gb = nullptr;
+  c64* gt = nullptr;
+  c64* gsol = nullptr;
+  c64* scal_c = nullptr;    // h[0..m], hc[0..m], y[0..m]
+  double* scal_d = nullptr;  // [0] pre^2 [1] post^2 [2] misc [3] rnorm^2
+  int* flag = nullptr;
+  int scal_cap = 0;
+  RedScratch rs{};
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  double stage_ms[5] = {0, 0, 0, 0, 0};
+  long long applies = 0;
+  long long launches = 0;
+
+  fpbem_cu_comm* comm = nullptr;
+};
+
+namespace fpbem_cu {
+// operator internals (fpbem_cuda.cu) used by the other translation units
+void pair_range(long long n_pairs, int nranks, int rank, double far_pairs, long long& lo, long long& hi);
+void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs);
+double calibrate_far_pairs(fpbem_cu_op* op);
+void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs);
+void ensure_pinned(fpbem_cu_op* op, size_t bytes);
+}  // namespace fpbem_cu
