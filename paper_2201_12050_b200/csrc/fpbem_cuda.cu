@@ -290,8 +290,11 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
       check(launch_mode_product(lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
     } else if (p.kind == 2) {
       const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
+      // the main spectrum's mirror parity lets one Λ stream serve a column and its mirror
+      const bool paired = lambda == op->lambda && op->lam_paired;
       check(launch_m2l_zfused(cur, out, lambda, op->tw[2], static_cast<int>(Mz), static_cast<int>(Lz), Ly * Lx,
-                              static_cast<int>(E), op->b, scale, s),
+                              static_cast<int>(E), op->b, scale, paired ? op->z_items_pair : op->z_items_single,
+                              paired ? op->n_z_items_pair : op->n_z_items_single, s),
             "m2l z-fused");
     } else {
       const double scale = (i == last_dft) ? 1.0 / static_cast<double>(op->q_total) : 1.0;
@@ -566,6 +569,35 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
     op->q_total = static_cast<long long>(op->L[0]) * op->L[1] * op->L[2];
     for (int k = 0; k < 3; ++k) twiddles(op, op->L[k], &op->tw[k]);
     build_spectrum(op, d->n_far, d->far_offsets, d->far_blocks, d->far_on_device != 0, d->lambda, &op->lambda);
+    if (op->L[2] > 1) {  // work items of the fused z kernel
+      const int Lx = op->L[0], Ly = op->L[1];
+      std::vector<int2> pairs, singles;
+      for (int qy = 0; qy < Ly; ++qy)
+        for (int qx = 0; qx < Lx; ++qx) {
+          const int c = qy * Lx + qx, cm = ((Ly - qy) % Ly) * Lx + (Lx - qx) % Lx;
+          singles.push_back(make_int2(c, -1));
+          if (c < cm) pairs.push_back(make_int2(c, cm));
+          if (c == cm) pairs.push_back(make_int2(c, -1));
+        }
+      op->z_items_pair = dalloc<int2>(pairs.size(), "z items");
+      op->z_items_single = dalloc<int2>(singles.size(), "z items");
+      h2d(op->z_items_pair, pairs.data(), pairs.size() * sizeof(int2), op->stream, "z items");
+      h2d(op->z_items_single, singles.data(), singles.size() * sizeof(int2), op->stream, "z items");
+      op->n_z_items_pair = static_cast<int>(pairs.size());
+      op->n_z_items_single = static_cast<int>(singles.size());
+      // parity Λ(-q) = D Λ(q) D of the spectrum actually built (or handed over)
+      unsigned long long* dv = dalloc<unsigned long long>(2, "parity check");
+      std::unique_ptr<unsigned long long, decltype(&cudaFree)> keep_dv(dv, &cudaFree);
+      check(cudaMemsetAsync(dv, 0, 2 * sizeof(unsigned long long), op->stream), "parity check");
+      check(launch_lambda_parity(op->lambda, op->L, op->b, dv, op->stream), "parity check");
+      unsigned long long hv[2];
+      check(cudaMemcpyAsync(hv, dv, sizeof(hv), cudaMemcpyDeviceToHost, op->stream), "parity check");
+      check(cudaStreamSynchronize(op->stream), "parity check");
+      double dev, amax;
+      std::memcpy(&dev, &hv[0], sizeof(double));
+      std::memcpy(&amax, &hv[1], sizeof(double));
+      op->lam_paired = amax > 0.0 && dev <= 1e-12 * amax;
+    }
     if (op->mirrored_level >= 0) {
       // spectrum of K_hat P: Toeplitz offsets o = idx with o[a] = idx[a] - (M_a - 1)
       // (hankel_spectrum, src/structured.cpp:185-198)
@@ -599,7 +631,8 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
   if (op->stream) cudaStreamSynchronize(op->stream);
   for (void* p : {static_cast<void*>(op->S), static_cast<void*>(op->pair_src), static_cast<void*>(op->tgt_ptr),
                   static_cast<void*>(op->tgt_pairs), static_cast<void*>(op->jobs), static_cast<void*>(op->u0),
-                  static_cast<void*>(op->v0), static_cast<void*>(op->v0t), static_cast<void*>(op->lambda), static_cast<void*>(op->lambda_hat),
+                  static_cast<void*>(op->v0), static_cast<void*>(op->v0t), static_cast<void*>(op->z_items_pair),
+                  static_cast<void*>(op->z_items_single), static_cast<void*>(op->lambda), static_cast<void*>(op->lambda_hat),
                   static_cast<void*>(op->mom_perm), static_cast<void*>(op->loc_hat), static_cast<void*>(op->tw[0]),
                   static_cast<void*>(op->tw[1]), static_cast<void*>(op->tw[2]), static_cast<void*>(op->W),
                   static_cast<void*>(op->mom), static_cast<void*>(op->loc), static_cast<void*>(op->fa),

@@ -109,6 +109,13 @@ struct fpbem_cu_op {
   c64* u0 = nullptr;
   c64* v0 = nullptr;
   c64* v0t = nullptr;  // V0^T (b rows of n), for the P2M kernel
+  // work items of the fused z kernel: column pairs (c, mirror) when Λ has the
+  // parity Λ(-q) = D Λ(q) D (checked on the device at create), single columns
+  // otherwise (and always for the image spectrum)
+  int2* z_items_pair = nullptr;
+  int2* z_items_single = nullptr;
+  int n_z_items_pair = 0, n_z_items_single = 0;
+  bool lam_paired = false;
   int L[3] = {1, 1, 1};
   long long q_total = 1;
   c64* lambda = nullptr;

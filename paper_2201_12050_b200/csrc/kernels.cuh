@@ -25,7 +25,10 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
 // the column's fields leave no room for >= 4 (then the unfused passes run)
 int m2l_zfused_ring(int Mz, int Lz, int E, int b);
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
-                              long long plane, int E, int b, double scale, cudaStream_t stream);
+                              long long plane, int E, int b, double scale, const int2* items, int n_items,
+                              cudaStream_t stream);
+// Λ(-q) = D Λ(q) D check (D = diag((-1)^n)): out2[0] = max deviation, out2[1] = max |Λ|, as double bits
+cudaError_t launch_lambda_parity(const c64* lam, const int L[3], int b, unsigned long long* out2, cudaStream_t stream);
 cudaError_t launch_mirror_permute(const c64* in, c64* out, const int counts[3], int level, long long E,
                                   cudaStream_t stream);
 cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream);

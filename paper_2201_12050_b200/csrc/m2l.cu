@@ -443,7 +443,6 @@ __device__ __forceinline__ void mode_product_warp(const c64* __restrict__ lam_bl
 // instead of barrier-separated refills (3.5 -> 6.7 TB/s in the probe) and the
 // z-DFTs on their own warps.
 constexpr int kPipeMaxModeWarps = 8;
-constexpr int kPipeInBufs = 2;  // input columns in flight (double buffer)
 constexpr int kPipeMaxRing = 16;
 constexpr int kPipeMaxDftWarps = 8;
 
@@ -451,64 +450,157 @@ __device__ __forceinline__ void dft_sync(int n_threads) {
   asm volatile("bar.sync 2, %0;\n" ::"r"(n_threads) : "memory");
 }
 
+// In-place mode product on the E = nrhs * b fields of one mode:
+//   f <- Λ f,  or  f <- D Λ D f  (conj: the mirror column's mode, see below)
+// with D = diag((-1)^n) over the coefficients (n, m). Each right-hand side's b
+// outputs are formed in registers before any is written back.
+__device__ __forceinline__ void mode_inplace(const c64* __restrict__ lam_blk, c64* __restrict__ f_mode, int E, int b,
+                                             int lane, bool conj, const double* __restrict__ dsg) {
+  constexpr int kMaxPerLane = 8;  // b <= 256
+  for (int r0 = 0; r0 < E; r0 += b) {
+    c64* f = f_mode + r0;
+    c64 res[kMaxPerLane];
+#pragma unroll
+    for (int k = 0; k < kMaxPerLane; ++k) {
+      const int i = lane + 32 * k;
+      res[k] = cmk(0.0, 0.0);
+      if (i >= b) continue;
+      const c64* lam = lam_blk + i;
+      c64 acc0 = cmk(0.0, 0.0), acc1 = cmk(0.0, 0.0);
+      int c = 0;
+      for (; c + 4 <= b; c += 4) {
+        c64 l[4], v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          l[u] = lam[(c + u) * b];
+          v[u] = f[c + u];
+          if (conj) v[u] = cscale(v[u], dsg[c + u]);
+        }
+        acc0 = cfma(l[0], v[0], acc0);
+        acc1 = cfma(l[1], v[1], acc1);
+        acc0 = cfma(l[2], v[2], acc0);
+        acc1 = cfma(l[3], v[3], acc1);
+      }
+      for (; c < b; ++c) acc0 = cfma(lam[c * b], conj ? cscale(f[c], dsg[c]) : f[c], acc0);
+      res[k] = cadd(acc0, acc1);
+      if (conj) res[k] = cscale(res[k], dsg[i]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kMaxPerLane; ++k)
+      if (lane + 32 * k < b) f[lane + 32 * k] = res[k];
+    __syncwarp();
+  }
+}
+
+// The common case b <= 32 (n_t <= 4): one output per lane. f1 <- Λ f1 and, when
+// f2 is given, f2 <- D Λ D f2 in the same pass, the two sums sharing every Λ load.
+template <bool kPair>
+__device__ __forceinline__ void mode_pair_small(const c64* __restrict__ lam_blk, c64* __restrict__ f1,
+                                                c64* __restrict__ f2, int E, int b, int lane,
+                                                const double* __restrict__ dsg) {
+  const bool active = lane < b;
+  const c64* lam = lam_blk + (active ? lane : 0);
+  for (int r0 = 0; r0 < E; r0 += b) {
+    c64 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0), p0 = cmk(0.0, 0.0), p1 = cmk(0.0, 0.0);
+    const c64* x1 = f1 + r0;
+    const c64* x2 = kPair ? f2 + r0 : nullptr;
+    int c = 0;
+    for (; c + 2 <= b; c += 2) {
+      const c64 l0 = lam[c * b], l1 = lam[(c + 1) * b];
+      a0 = cfma(l0, x1[c], a0);
+      a1 = cfma(l1, x1[c + 1], a1);
+      if (kPair) {
+        p0 = cfma(l0, cscale(x2[c], dsg[c]), p0);
+        p1 = cfma(l1, cscale(x2[c + 1], dsg[c + 1]), p1);
+      }
+    }
+    if (c < b) {
+      const c64 l0 = lam[c * b];
+      a0 = cfma(l0, x1[c], a0);
+      if (kPair) p0 = cfma(l0, cscale(x2[c], dsg[c]), p0);
+    }
+    __syncwarp();  // every lane has read f1 / f2 of this right-hand side
+    if (active) {
+      f1[r0 + lane] = cadd(a0, a1);
+      if (kPair) f2[r0 + lane] = cscale(cadd(p0, p1), dsg[lane]);
+    }
+    __syncwarp();
+  }
+}
+
+// Work items: one column (qy, qx), or a column and its mirror (-qy, -qx) when
+// Λ has the K-bank parity Λ(-q) = D Λ(q) D (K(-δ) = D K(δ) D: solid harmonics
+// of degree l change sign by (-1)^l and the Gaunt rule makes n + n' + l even;
+// the far offsets are symmetric). Then each Λ block (qz, c) is streamed once
+// and used for mode qz of c and, conjugated by D, for mode -qz of the mirror:
+// half the Λ bytes. items[k] = (c, mirror or -1).
 __global__ void __launch_bounds__(32 * (1 + kPipeMaxModeWarps + kPipeMaxDftWarps), 1)
 m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
                  const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, int n_mw,
-                 int ring, int n_dw, double scale) {
+                 int ring, int n_dw, double scale, const int2* __restrict__ items, int n_items_total) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b2 = b * b;
   c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
-  c64* f_in0 = ring_buf + ring * b2;                  // kPipeInBufs x Mz x E
-  c64* f_z0 = f_in0 + kPipeInBufs * Mz * E;               // 2 x Lz x E
-  c64* g_z0 = f_z0 + 2 * Lz * E;                      // 2 x Lz x E
-  c64* tw_s = g_z0 + 2 * Lz * E;                      // Lz twiddles
+  c64* f_in0 = ring_buf + ring * b2;                  // [buffer 2][column 2][Mz][E]
+  c64* f_z0 = f_in0 + 4 * Mz * E;                     // [buffer 2][column 2][Lz][E] (g in place)
+  c64* tw_s = f_z0 + 4 * Lz * E;                      // Lz twiddles
+  __shared__ double dsg[256];                         // (-1)^n of coefficient (n, m)
   __shared__ __align__(8) unsigned long long full[kPipeMaxRing], empty[kPipeMaxRing];
-  __shared__ __align__(8) unsigned long long in_full[kPipeInBufs], in_empty[kPipeInBufs];
-  __shared__ __align__(8) unsigned long long fwd_done[2], col_done[2], inv_done[2];
+  __shared__ __align__(8) unsigned long long in_full[2], in_empty[2];
+  __shared__ __align__(8) unsigned long long fwd_done[2], col_done[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_cols = static_cast<int>((plane - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int n_items = static_cast<int>((n_items_total - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  auto item = [&](int k) { return items[blockIdx.x + static_cast<long long>(k) * gridDim.x]; };
   if (tid == 0) {
     for (int s = 0; s < ring; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    for (int s = 0; s < kPipeInBufs; ++s) {
+    for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&in_full[s]), 1);
       mbar_init(smem_u32(&in_empty[s]), 1);
-    }
-    for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&fwd_done[s]), 1);
       mbar_init(smem_u32(&col_done[s]), n_mw);
-      mbar_init(smem_u32(&inv_done[s]), 1);
     }
     mbar_fence_init();
   }
   for (int k = tid; k < Lz; k += blockDim.x) tw_s[k] = tw[k];
+  for (int i = tid; i < b; i += blockDim.x) {
+    int n = 0;
+    while ((n + 1) * (n + 1) <= i) ++n;
+    dsg[i] = (n & 1) ? -1.0 : 1.0;
+  }
   __syncthreads();
 
   if (warp == 0) {
     if (lane == 0) {  // ---- producer
       const unsigned lam_bytes = static_cast<unsigned>(b2 * sizeof(c64));
       const unsigned row_bytes = static_cast<unsigned>(E * sizeof(c64));
-      auto issue_input = [&](int k) {
-        if (k >= n_cols) return;
-        const int buf = k % kPipeInBufs;
-        if (k >= kPipeInBufs) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / kPipeInBufs - 1) & 1));
-        const long long col = blockIdx.x + static_cast<long long>(k) * gridDim.x;
+      auto issue_input = [&](int k) {  // both columns of item k -> buffer k % 2
+        if (k >= n_items) return;
+        const int buf = k & 1;
+        if (k >= 2) mbar_wait(smem_u32(&in_empty[buf]), static_cast<unsigned>((k / 2 - 1) & 1));
+        const int2 it = item(k);
+        const int nc = it.y >= 0 ? 2 : 1;
         const unsigned bar = smem_u32(&in_full[buf]);
-        c64* dst = f_in0 + buf * Mz * E;
-        mbar_arrive_expect_tx(bar, row_bytes * Mz);
-        for (int iz = 0; iz < Mz; ++iz) bulk_g2s(smem_u32(dst + iz * E), in + (iz * plane + col) * E, row_bytes, bar);
+        mbar_arrive_expect_tx(bar, row_bytes * Mz * nc);
+        for (int s = 0; s < nc; ++s) {
+          const long long col = s ? it.y : it.x;
+          c64* dst = f_in0 + (buf * 2 + s) * Mz * E;
+          for (int iz = 0; iz < Mz; ++iz)
+            bulk_g2s(smem_u32(dst + iz * E), in + (iz * plane + col) * E, row_bytes, bar);
+        }
       };
       issue_input(0);
-      issue_input(1);  // then column k + 1's input after column k's first Λ blocks
+      issue_input(1);
       int slot = 0;
       unsigned phase = 0;
       long long g = 0;
-      const c64* col_lam = lambda + static_cast<long long>(blockIdx.x) * b2;
-      const long long col_step = static_cast<long long>(gridDim.x) * b2, mode_step = plane * b2;
-      for (int k = 0; k < n_cols; ++k, col_lam += col_step) {
-        if (k > 0) issue_input(k + 1);  // buffer of column k - 1: its forward pass is done by now
+      const long long mode_step = plane * b2;
+      for (int k = 0; k < n_items; ++k) {
+        if (k > 0) issue_input(k + 1);  // buffer of item k - 1: its forward pass is done by now
+        const c64* col_lam = lambda + static_cast<long long>(item(k).x) * b2;
         for (int qz = 0; qz < Lz; ++qz, ++g) {
           if (g >= ring) mbar_wait(smem_u32(&empty[slot]), phase ^ 1u);
           const unsigned bar = smem_u32(&full[slot]);
@@ -523,19 +615,17 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
     }
   } else if (warp <= n_mw) {  // ---- mode warps
     const int w = warp - 1;
-    // this warp's modes are the global g = w, w + n_mw, w + 2 n_mw, ...
-    // (ring = spw * n_mw): the j-th lands in slot w + (j % spw) n_mw, phase (j / spw) & 1
+    // this warp's modes are the global g = w, w + n_mw, ... (ring = spw * n_mw):
+    // the j-th lands in slot w + (j % spw) n_mw, phase (j / spw) & 1
     const int spw = ring / n_mw;
     long long g = w;
-    int jm = 0;             // j % spw
-    unsigned jphase = 0;    // (j / spw) & 1
-    for (int k = 0; k < n_cols; ++k) {
+    int jm = 0;
+    unsigned jphase = 0;
+    for (int k = 0; k < n_items; ++k) {
       const int buf = k & 1;
-      const unsigned use = static_cast<unsigned>((k >> 1) & 1);
-      mbar_wait(smem_u32(&fwd_done[buf]), use);                                   // f_z[buf] holds column k
-      if (k >= 2) mbar_wait(smem_u32(&inv_done[buf]), use ^ 1u);                  // g_z[buf] read by inverse(k-2)
-      const c64* f_z = f_z0 + buf * Lz * E;
-      c64* g_z = g_z0 + buf * Lz * E;
+      const bool pair = item(k).y >= 0;
+      mbar_wait(smem_u32(&fwd_done[buf]), static_cast<unsigned>((k >> 1) & 1));  // f_z[buf] holds item k
+      c64* fz = f_z0 + buf * 2 * Lz * E;
       const long long g_end = static_cast<long long>(k + 1) * Lz;
       for (; g < g_end; g += n_mw) {
         const int qz = static_cast<int>(g - static_cast<long long>(k) * Lz);
@@ -545,7 +635,18 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
           jm = 0;
           jphase ^= 1u;
         }
-        mode_product_warp(ring_buf + slot * b2, f_z + qz * E, g_z + qz * E, E, b, lane);
+        const c64* blk = ring_buf + slot * b2;
+        c64* m1 = fz + qz * E;
+        c64* m2 = fz + (Lz + (qz ? Lz - qz : 0)) * E;  // the mirror column's mode -qz
+        if (b <= 32) {
+          if (pair)
+            mode_pair_small<true>(blk, m1, m2, E, b, lane, dsg);
+          else
+            mode_pair_small<false>(blk, m1, nullptr, E, b, lane, dsg);
+        } else {
+          mode_inplace(blk, m1, E, b, lane, false, dsg);
+          if (pair) mode_inplace(blk, m2, E, b, lane, true, dsg);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
       }
@@ -554,37 +655,42 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
     }
   } else {  // ---- DFT warps
     const int dt = tid - 32 * (1 + n_mw), n_dt = 32 * n_dw;
-    auto inverse = [&](int c) {  // inverse z of column c (its modes are finished)
+    auto inverse = [&](int c) {  // inverse z of item c (its modes are finished)
       const int buf = c & 1;
       mbar_wait(smem_u32(&col_done[buf]), static_cast<unsigned>((c >> 1) & 1));
-      const long long col = blockIdx.x + static_cast<long long>(c) * gridDim.x;
-      const c64* g_z = g_z0 + buf * Lz * E;
-      const int G = zdft_group(Mz * E, n_dt);
-      if (G == 4) zdft<4, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
-      else if (G == 2) zdft<2, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
-      else zdft<1, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+      const int2 it = item(c);
+      for (int s = 0; s < (it.y >= 0 ? 2 : 1); ++s) {
+        const long long col = s ? it.y : it.x;
+        const c64* g_z = f_z0 + (buf * 2 + s) * Lz * E;
+        const int G = zdft_group(Mz * E, n_dt);
+        if (G == 4) zdft<4, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+        else if (G == 2) zdft<2, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+        else zdft<1, true>(g_z, nullptr, tw_s, Lz, Mz, Lz, E, dt, n_dt, scale, out, plane, col);
+      }
       dft_sync(n_dt);
-      if (dt == 0) mbar_arrive(smem_u32(&inv_done[buf]));
     };
-    for (int k = 0; k < n_cols; ++k) {
-      const int buf = k & 1, ib = k % kPipeInBufs;
-      // f_z[buf] was last read by the modes of column k-2, whose col_done the
-      // inverse of column k-2 (previous iteration's tail) already waited for
-      mbar_wait(smem_u32(&in_full[ib]), static_cast<unsigned>((k / kPipeInBufs) & 1));
-      c64* f_z = f_z0 + buf * Lz * E;
-      const c64* f_in = f_in0 + ib * Mz * E;
-      const int G = zdft_group(Lz * E, n_dt);
-      if (G == 4) zdft<4, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
-      else if (G == 2) zdft<2, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
-      else zdft<1, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+    for (int k = 0; k < n_items; ++k) {
+      const int buf = k & 1;
+      // f_z[buf] was last used by item k - 2: its modes finished (col_done waited
+      // in inverse(k - 2)) and its inverse ran before this forward pass
+      mbar_wait(smem_u32(&in_full[buf]), static_cast<unsigned>((k >> 1) & 1));
+      const int nc = item(k).y >= 0 ? 2 : 1;
+      for (int s = 0; s < nc; ++s) {
+        c64* f_z = f_z0 + (buf * 2 + s) * Lz * E;
+        const c64* f_in = f_in0 + (buf * 2 + s) * Mz * E;
+        const int G = zdft_group(Lz * E, n_dt);
+        if (G == 4) zdft<4, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+        else if (G == 2) zdft<2, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+        else zdft<1, false>(f_in, f_z, tw_s, Mz, Lz, Lz, E, dt, n_dt, 1.0, nullptr, 0, 0);
+      }
       dft_sync(n_dt);
       if (dt == 0) {
         mbar_arrive(smem_u32(&fwd_done[buf]));
-        mbar_arrive(smem_u32(&in_empty[ib]));
+        mbar_arrive(smem_u32(&in_empty[buf]));
       }
       if (k >= 1) inverse(k - 1);
     }
-    if (n_cols >= 1) inverse(n_cols - 1);
+    if (n_items >= 1) inverse(n_items - 1);
   }
   __syncthreads();  // the producer stays resident until every copy it issued has landed
 }
@@ -744,7 +850,7 @@ cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream)
 
 namespace {
 size_t zpipe_fields_bytes(int Mz, int Lz, int E) {
-  return sizeof(c64) * (static_cast<size_t>(kPipeInBufs * Mz + 4 * Lz) * E + Lz);
+  return sizeof(c64) * (static_cast<size_t>(4 * Mz + 4 * Lz) * E + Lz);  // inputs and f_z: 2 buffers x 2 columns
 }
 int zpipe_max_ring(int Mz, int Lz, int E, int b) {
   const size_t fields = zpipe_fields_bytes(Mz, Lz, E), per_mode = sizeof(c64) * static_cast<size_t>(b) * b;
@@ -773,9 +879,10 @@ int m2l_zfused_ring(int Mz, int Lz, int E, int b) {
 }
 
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
-                              long long plane, int E, int b, double scale, cudaStream_t stream) {
+                              long long plane, int E, int b, double scale, const int2* items, int n_items,
+                              cudaStream_t stream) {
   const int n_mw = zpipe_mode_warps(Mz, Lz, E, b);
-  if (n_mw == 0) return cudaErrorInvalidValue;
+  if (n_mw == 0 || b > 256) return cudaErrorInvalidValue;
   const int ring = m2l_zfused_ring(Mz, Lz, E, b);
   const size_t smem = zpipe_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
   static size_t configured = 0;
@@ -785,9 +892,40 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  const long long grid = plane < kNumSMs ? plane : kNumSMs;  // persistent: one CTA per SM
-  m2l_zpipe_kernel<<<static_cast<unsigned>(grid), 32 * (1 + n_mw + kPipeMaxDftWarps), smem, stream>>>(
-      in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, kPipeMaxDftWarps, scale);
+  const int grid = n_items < kNumSMs ? n_items : kNumSMs;  // persistent: one CTA per SM
+  if (grid == 0) return cudaSuccess;
+  m2l_zpipe_kernel<<<grid, 32 * (1 + n_mw + kPipeMaxDftWarps), smem, stream>>>(
+      in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, kPipeMaxDftWarps, scale, items, n_items);
+  return cudaGetLastError();
+}
+
+// max |Λ(-q) - D Λ(q) D| and max |Λ| (component-wise, as bit patterns of
+// non-negative doubles) over the whole spectrum
+__global__ void lambda_parity_kernel(const c64* __restrict__ lam, int Lx, int Ly, int Lz, int b,
+                                     unsigned long long* __restrict__ out) {
+  const long long q_total = static_cast<long long>(Lx) * Ly * Lz, b2 = static_cast<long long>(b) * b;
+  double dmax = 0.0, amax = 0.0;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < q_total * b2;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long q = g / b2, e = g - q * b2;
+    const int qx = static_cast<int>(q % Lx), qy = static_cast<int>((q / Lx) % Ly), qz = static_cast<int>(q / Lx / Ly);
+    const long long qm = (static_cast<long long>((Lz - qz) % Lz) * Ly + (Ly - qy) % Ly) * Lx + (Lx - qx) % Lx;
+    const int i = static_cast<int>(e % b), j = static_cast<int>(e / b);  // column-major block
+    int ni = 0, nj = 0;
+    while ((ni + 1) * (ni + 1) <= i) ++ni;
+    while ((nj + 1) * (nj + 1) <= j) ++nj;
+    const double sg = ((ni + nj) & 1) ? -1.0 : 1.0;
+    const c64 a = lam[q * b2 + e], m = lam[qm * b2 + e];
+    dmax = fmax(dmax, fmax(fabs(m.x - sg * a.x), fabs(m.y - sg * a.y)));
+    amax = fmax(amax, fmax(fabs(a.x), fabs(a.y)));
+  }
+  atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+  atomicMax(out + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
+}
+
+cudaError_t launch_lambda_parity(const c64* lam, const int L[3], int b, unsigned long long* out2, cudaStream_t stream) {
+  const long long total = static_cast<long long>(L[0]) * L[1] * L[2] * b * b;
+  lambda_parity_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lam, L[0], L[1], L[2], b, out2);
   return cudaGetLastError();
 }
 
