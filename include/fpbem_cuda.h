@@ -216,6 +216,36 @@ int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int de
 void fpbem_cu_comm_destroy(fpbem_cu_comm* comm);
 int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm);
 
+/* A communicator over a caller-supplied host all-reduce (e.g. a gloo process
+ * group, or MPI): allreduce_sum(ctx, buf, count) must replace the host buffer
+ * of `count` doubles by its element-wise sum over all ranks and return 0. The
+ * library stages device data through pinned host memory; reduce-scatter and
+ * all-gather are built from the all-reduce (an all-gather sums zero-filled
+ * slabs, which is exact). Same semantics as the NCCL communicator: for hosts
+ * whose ranks have no NCCL path between them, and for multi-rank tests. */
+typedef int (*fpbem_cu_allreduce_fn)(void* ctx, double* host_buf, size_t count);
+int fpbem_cu_comm_from_callback(fpbem_cu_allreduce_fn allreduce_sum, void* ctx, int nranks, int rank,
+                                int device, fpbem_cu_comm** out);
+
+/* Distributed restarted GMRES: the Krylov basis, x and
+ * the residual are split over the ranks of the attached communicator in
+ * contiguous slabs of whole cells (fpbem_cu_gmres_dist_rows); per Arnoldi
+ * step the new basis vector is all-gathered for the product, the ranks'
+ * partial products are reduce-scattered back to the slabs, and each
+ * Gram-Schmidt pass is classical (one batched all-reduce of the j+1
+ * projections and ||w||^2) with the reference's own reorthogonalisation test
+ * (second pass iff ||w_post|| < ||w_pre|| / 2, src/solver.cpp:63-69); the
+ * Hessenberg / Givens control flow is the reference's, replicated on every
+ * rank from all-reduced scalars. Every rank passes the full b and receives
+ * the full x (one right-hand side). Without a communicator it runs on one
+ * device with the same arithmetic. Arguments and errors as fpbem_cu_gmres. */
+int fpbem_cu_gmres_dist(fpbem_cu_op* op, const fpbem_c64* b, fpbem_c64* x, double tol, int restart,
+                        int max_iter, int ptr_kind, int* iterations, int* converged, double* history,
+                        int history_cap, int* history_len);
+
+/* This rank's slab [lo, hi) of the global rows under fpbem_cu_gmres_dist. */
+int fpbem_cu_gmres_dist_rows(const fpbem_cu_op* op, long long* lo, long long* hi);
+
 /* The same partition without a communicator: apply() returns this rank's
  * partial product (its near-field pairs; rank 0 adds the far field). Summing
  * the nranks partial products gives the full product. far_pairs: rank 0's

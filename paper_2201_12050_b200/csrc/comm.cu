@@ -1,6 +1,7 @@
-// C-ABI implementation, part 4: the library's NCCL communicator (libnccl
-// loaded at runtime, so single-GPU use has no NCCL dependency) and the
-// near-field pair partition across ranks.
+// C-ABI implementation, part 4: the library's communicator — NCCL (libnccl
+// loaded at runtime, so single-GPU use has no NCCL dependency) or a caller's
+// host all-reduce — its collectives, and the near-field pair partition across
+// ranks.
 #include <dlfcn.h>
 
 #include <cstring>
@@ -17,7 +18,95 @@ void* load_nccl() {
   if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   return lib;
 }
+
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+void nccl_rc(int rc, const char* what) {
+  if (rc != 0) fail(FPBEM_CU_ENCCL, std::string(what) + " failed: " + std::to_string(rc));
+}
+
+// host form: device -> pinned stage -> caller's all-reduce -> device
+double* stage(fpbem_cu_comm* c, size_t count) {
+  if (c->stage_count < count) {
+    if (c->stage) cudaFreeHost(c->stage);
+    c->stage = nullptr;
+    c->stage_count = 0;
+    check(cudaMallocHost(&c->stage, count * sizeof(double)), "comm staging buffer");
+    c->stage_count = count;
+  }
+  return c->stage;
+}
+
+void host_allreduce(fpbem_cu_comm* c, double* h, size_t count) {
+  if (c->cb(c->cb_ctx, h, count) != 0) fail(FPBEM_CU_ENCCL, "host all-reduce callback failed");
+}
 }  // namespace
+
+namespace fpbem_cu {
+
+// A communicator of one rank still runs its collectives (so the NCCL and the
+// staged paths are exercised on one GPU); no communicator = this rank alone.
+void comm_allreduce(fpbem_cu_comm* c, double* buf, size_t count, cudaStream_t s) {
+  if (!c || count == 0) return;
+  if (!c->cb) {
+    nccl_rc(c->allreduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, s), "ncclAllReduce");
+    return;
+  }
+  double* h = stage(c, count);
+  check(cudaMemcpyAsync(h, buf, count * sizeof(double), cudaMemcpyDeviceToHost, s), "comm stage");
+  check(cudaStreamSynchronize(s), "comm stage");
+  host_allreduce(c, h, count);
+  check(cudaMemcpyAsync(buf, h, count * sizeof(double), cudaMemcpyHostToDevice, s), "comm unstage");
+  check(cudaStreamSynchronize(s), "comm unstage");
+}
+
+// full: nranks x per_rank (rank r's slab at r * per_rank), summed over the
+// ranks; this rank's slab of the sum lands in `mine`
+void comm_reduce_scatter(fpbem_cu_comm* c, double* full, double* mine, size_t per_rank, cudaStream_t s) {
+  const int r = c ? c->rank : 0;
+  if (!c) {
+    if (mine != full)
+      check(cudaMemcpyAsync(mine, full, per_rank * sizeof(double), cudaMemcpyDeviceToDevice, s), "slab copy");
+    return;
+  }
+  if (!c->cb) {
+    nccl_rc(c->reduce_scatter(full, mine, per_rank, kNcclFloat64, kNcclSum, c->comm, s), "ncclReduceScatter");
+    return;
+  }
+  const size_t count = per_rank * c->nranks;
+  double* h = stage(c, count);
+  check(cudaMemcpyAsync(h, full, count * sizeof(double), cudaMemcpyDeviceToHost, s), "comm stage");
+  check(cudaStreamSynchronize(s), "comm stage");
+  host_allreduce(c, h, count);
+  check(cudaMemcpyAsync(mine, h + r * per_rank, per_rank * sizeof(double), cudaMemcpyHostToDevice, s),
+        "comm unstage");
+  check(cudaStreamSynchronize(s), "comm unstage");
+}
+
+// every rank's slab `mine` (per_rank doubles) into full[r * per_rank ...]
+void comm_allgather(fpbem_cu_comm* c, const double* mine, double* full, size_t per_rank, cudaStream_t s) {
+  if (!c) {
+    if (mine != full)
+      check(cudaMemcpyAsync(full, mine, per_rank * sizeof(double), cudaMemcpyDeviceToDevice, s), "slab copy");
+    return;
+  }
+  if (!c->cb) {
+    nccl_rc(c->allgather(mine, full, per_rank, kNcclFloat64, c->comm, s), "ncclAllGather");
+    return;
+  }
+  const size_t count = per_rank * c->nranks;
+  double* h = stage(c, count);
+  check(cudaStreamSynchronize(s), "comm stage");
+  std::memset(h, 0, count * sizeof(double));
+  check(cudaMemcpyAsync(h + c->rank * per_rank, mine, per_rank * sizeof(double), cudaMemcpyDeviceToHost, s),
+        "comm stage");
+  check(cudaStreamSynchronize(s), "comm stage");
+  host_allreduce(c, h, count);  // the other slabs are zero here: the sum is exact
+  check(cudaMemcpyAsync(full, h, count * sizeof(double), cudaMemcpyHostToDevice, s), "comm unstage");
+  check(cudaStreamSynchronize(s), "comm unstage");
+}
+
+}  // namespace fpbem_cu
 
 extern "C" {
 
@@ -47,8 +136,12 @@ int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int de
     c->device = device;
     c->allreduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, void*)>(
         dlsym(lib, "ncclAllReduce"));
+    c->reduce_scatter = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, void*)>(
+        dlsym(lib, "ncclReduceScatter"));
+    c->allgather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, void*)>(
+        dlsym(lib, "ncclAllGather"));
     c->destroy = reinterpret_cast<int (*)(void*)>(dlsym(lib, "ncclCommDestroy"));
-    if (!init || !c->allreduce || !c->destroy) {
+    if (!init || !c->allreduce || !c->reduce_scatter || !c->allgather || !c->destroy) {
       delete c;
       fail(FPBEM_CU_ENCCL, "NCCL symbols missing");
     }
@@ -61,9 +154,25 @@ int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int de
   });
 }
 
+int fpbem_cu_comm_from_callback(fpbem_cu_allreduce_fn allreduce_sum, void* ctx, int nranks, int rank, int device,
+                                fpbem_cu_comm** out) {
+  return guard([&] {
+    if (!allreduce_sum || !out || nranks < 1 || rank < 0 || rank >= nranks)
+      fail(FPBEM_CU_EINVAL, "comm_from_callback: bad arguments");
+    auto* c = new fpbem_cu_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    c->cb = allreduce_sum;
+    c->cb_ctx = ctx;
+    *out = c;
+  });
+}
+
 void fpbem_cu_comm_destroy(fpbem_cu_comm* comm) {
   if (!comm) return;
   if (comm->comm && comm->destroy) comm->destroy(comm->comm);
+  if (comm->stage) cudaFreeHost(comm->stage);
   delete comm;
 }
 
@@ -83,8 +192,7 @@ int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm) {
       double* df = dalloc<double>(1, "far pairs");
       std::unique_ptr<double, decltype(&cudaFree)> keep_df(df, &cudaFree);
       h2d(df, &f, sizeof(double), op->stream, "far pairs");
-      const int rc = comm->allreduce(df, df, 1, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm->comm, op->stream);
-      if (rc != 0) fail(FPBEM_CU_ENCCL, "ncclAllReduce failed: " + std::to_string(rc));
+      comm_allreduce(comm, df, 1, op->stream);
       check(cudaMemcpyAsync(&f, df, sizeof(double), cudaMemcpyDeviceToHost, op->stream), "far pairs");
       check(cudaStreamSynchronize(op->stream), "far pairs");
       f /= comm->nranks;

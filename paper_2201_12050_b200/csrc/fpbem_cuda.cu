@@ -371,7 +371,7 @@ double calibrate_far_pairs(fpbem_cu_op* op) {
 // With an offset partition (nranks > 1) this rank computes the product of
 // its own near-field offsets; rank 0 also adds the far field (P2M, M2L,
 // L2P); with a communicator the partial products are all-reduced.
-void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
+void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
   cudaStream_t s = op->stream;
   // FPBEM_SERIAL=1 runs P2M + M2L on the main stream (exact per-stage timing)
   static const bool serial = [] {
@@ -399,11 +399,8 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
                                op->b, op->n_cells, op->N, nrhs, false, s),
         "near reduce + l2p");
   op->launches++;
-  if (op->comm) {  // sum the ranks' partial products, in place, on the same stream
-    const int rc = op->comm->allreduce(y, y, static_cast<size_t>(2) * op->N * nrhs, /*ncclFloat64*/ 8,
-                                       /*ncclSum*/ 0, op->comm->comm, s);
-    if (rc != 0) fail(FPBEM_CU_ENCCL, "ncclAllReduce failed: " + std::to_string(rc));
-  }
+  if (op->comm && reduce)  // sum the ranks' partial products, in place, on the same stream
+    comm_allreduce(op->comm, reinterpret_cast<double*>(y), static_cast<size_t>(2) * op->N * nrhs, s);
   ev_record(op, 6, s);
   if (op->timing) {
     check(cudaEventSynchronize(op->ev[6]), "timing sync");
@@ -422,10 +419,10 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
   }
 }
 
-void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs) {
+void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
   for (int r0 = 0; r0 < nrhs; r0 += op->max_rhs) {
     const int c = std::min(op->max_rhs, nrhs - r0);
-    apply_chunk(op, x + static_cast<long long>(r0) * op->N, y + static_cast<long long>(r0) * op->N, c);
+    apply_chunk(op, x + static_cast<long long>(r0) * op->N, y + static_cast<long long>(r0) * op->N, c, reduce);
   }
 }
 
@@ -676,7 +673,7 @@ int fpbem_cu_fmm_apply(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int nr
       (void)bytes;
       check(cudaMemcpyAsync(op->xin, x + static_cast<size_t>(r0) * op->N, cb, cudaMemcpyHostToDevice, op->stream),
             "x upload");
-      apply_chunk(op, op->xin, op->yout, c);
+      apply_chunk(op, op->xin, op->yout, c, true);
       check(cudaMemcpyAsync(y + static_cast<size_t>(r0) * op->N, op->yout, cb, cudaMemcpyDeviceToHost, op->stream),
             "y download");
     }

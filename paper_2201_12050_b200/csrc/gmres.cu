@@ -10,6 +10,7 @@
 #include <memory>
 #include <vector>
 
+#include "givens.hpp"
 #include "handle.cuh"
 
 using namespace fpbem_cu;
@@ -90,19 +91,15 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
     return rep;
   }
   const int m = std::max(1, restart);
-  std::vector<cd> H(static_cast<size_t>(m + 1) * m, cd(0, 0));
-  auto Hm = [&](int i, int j) -> cd& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
-  std::vector<cd> g(m + 1);
-  std::vector<double> gc(m);
-  std::vector<cd> gs(m);
+  GmresCycle cyc(m);
+  auto Hm = [&](int i, int j) -> cd& { return cyc.h(i, j); };
   const c64* r = b_dev;  // r = b_eff on the first cycle
   double rnorm = bnorm;
 
   while (rep.iterations < max_iter) {
     check(launch_div(r, col(0), n, rnorm, s), "v0");
     op->launches++;
-    std::fill(g.begin(), g.end(), cd(0, 0));
-    g[0] = rnorm;
+    cyc.start(rnorm);
     int j = 0;
     for (; j < m && rep.iterations < max_iter; ++j) {
       c64* w = col(j + 1);
@@ -165,31 +162,8 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
         check(launch_div(w, w, n, hlast, s), "normalise");
         op->launches++;
       }
-      for (int i = 0; i < j; ++i) {  // accumulated rotations (:75-79)
-        cd t = gc[i] * Hm(i, j) + gs[i] * Hm(i + 1, j);
-        Hm(i + 1, j) = -std::conj(gs[i]) * Hm(i, j) + gc[i] * Hm(i + 1, j);
-        Hm(i, j) = t;
-      }
-      const cd a = Hm(j, j);  // new rotation (:80-94)
-      const double bb = std::abs(Hm(j + 1, j));
-      const double denom = std::hypot(std::abs(a), bb);
-      if (denom == 0.0) {
-        gc[j] = 1.0;
-        gs[j] = cd(0, 0);
-      } else if (std::abs(a) == 0.0) {
-        gc[j] = 0.0;
-        gs[j] = cd(1, 0);
-      } else {
-        gc[j] = std::abs(a) / denom;
-        gs[j] = (a / std::abs(a)) * std::conj(Hm(j + 1, j)) / denom;
-      }
-      Hm(j, j) = gc[j] * a + gs[j] * Hm(j + 1, j);
-      Hm(j + 1, j) = cd(0, 0);
-      const cd gj = g[j];
-      g[j] = gc[j] * gj;
-      g[j + 1] = -std::conj(gs[j]) * gj;
       ++rep.iterations;
-      const double est = std::abs(g[j + 1]) / bnorm;
+      const double est = cyc.rotate(j) / bnorm;
       rep.history.push_back(est);
       if (est <= tol || hlast == 0.0) {
         ++j;
@@ -197,12 +171,7 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
       }
     }
     // y = triu(H_jj)^{-1} g ; x += V y (:109-110)
-    std::vector<cd> y(j);
-    for (int i = j - 1; i >= 0; --i) {
-      cd acc = g[i];
-      for (int k = i + 1; k < j; ++k) acc -= Hm(i, k) * y[k];
-      y[i] = acc / Hm(i, i);
-    }
+    const std::vector<cd> y = cyc.solve(j);
     if (j > 0) {
       std::vector<c64> yh(j);
       for (int i = 0; i < j; ++i) yh[i] = cmk(y[i].real(), y[i].imag());
@@ -373,10 +342,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
       done[r] = 1;
     }
   }
-  const size_t hsz = static_cast<size_t>(m + 1) * m;
-  std::vector<std::vector<cd>> H(G, std::vector<cd>(hsz)), g(G, std::vector<cd>(m + 1));
-  std::vector<std::vector<double>> gc(G, std::vector<double>(m));
-  std::vector<std::vector<cd>> gs(G, std::vector<cd>(m));
+  std::vector<GmresCycle> cyc(G, GmresCycle(m));
   std::vector<int> jr(G, 0);
   std::vector<char> inner(G, 0);
   const c64* rsrc = Bd;
@@ -390,9 +356,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
     put(o_d, rnorm.data(), g8);
     check(launch_b_div(rsrc, V, n, n, G, d_mask, d_d, s), "v0");  // v0 = r / ||r||
     for (int r : act) {
-      std::fill(g[r].begin(), g[r].end(), cd(0, 0));
-      g[r][0] = rnorm[r];
-      std::fill(H[r].begin(), H[r].end(), cd(0, 0));
+      cyc[r].start(rnorm[r]);
       jr[r] = 0;
       inner[r] = 1;
     }
@@ -420,8 +384,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
       std::vector<int> reo;
       std::vector<double> wn2(G, 0.0);
       for (int r : it) {
-        for (int i = 0; i <= j; ++i)
-          H[r][static_cast<size_t>(j) * (m + 1) + i] = get_c(o_h, static_cast<size_t>(i) * G + r);
+        for (int i = 0; i <= j; ++i) cyc[r].h(i, j) = get_c(o_h, static_cast<size_t>(i) * G + r);
         wn2[r] = get_d(o_post, r);
         if (std::sqrt(wn2[r]) < 0.5 * std::sqrt(get_d(o_pre, r))) reo.push_back(r);  // (:63-69)
       }
@@ -439,8 +402,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
         fetch(o_post2, g8);
         fetch(o_hc, 16 * static_cast<size_t>(j + 1) * G);
         for (int r : reo) {
-          for (int i = 0; i <= j; ++i)
-            H[r][static_cast<size_t>(j) * (m + 1) + i] += get_c(o_hc, static_cast<size_t>(i) * G + r);
+          for (int i = 0; i <= j; ++i) cyc[r].h(i, j) += get_c(o_hc, static_cast<size_t>(i) * G + r);
           wn2[r] = get_d(o_post2, r);
         }
       }
@@ -457,34 +419,11 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
         op->launches++;
       }
       for (int r : it) {  // rotations, Givens, estimate (:74-105), per RHS
-        auto Hm = [&](int a, int b) -> cd& { return H[r][static_cast<size_t>(b) * (m + 1) + a]; };
         const double hlast = hl[r];
-        Hm(j + 1, j) = hlast;
-        for (int i = 0; i < j; ++i) {
-          cd t = gc[r][i] * Hm(i, j) + gs[r][i] * Hm(i + 1, j);
-          Hm(i + 1, j) = -std::conj(gs[r][i]) * Hm(i, j) + gc[r][i] * Hm(i + 1, j);
-          Hm(i, j) = t;
-        }
-        const cd a = Hm(j, j);
-        const double bb = std::abs(Hm(j + 1, j));
-        const double denom = std::hypot(std::abs(a), bb);
-        if (denom == 0.0) {
-          gc[r][j] = 1.0;
-          gs[r][j] = cd(0, 0);
-        } else if (std::abs(a) == 0.0) {
-          gc[r][j] = 0.0;
-          gs[r][j] = cd(1, 0);
-        } else {
-          gc[r][j] = std::abs(a) / denom;
-          gs[r][j] = (a / std::abs(a)) * std::conj(Hm(j + 1, j)) / denom;
-        }
-        Hm(j, j) = gc[r][j] * a + gs[r][j] * Hm(j + 1, j);
-        Hm(j + 1, j) = cd(0, 0);
-        const cd gj = g[r][j];
-        g[r][j] = gc[r][j] * gj;
-        g[r][j + 1] = -std::conj(gs[r][j]) * gj;
+        cyc[r].h(j + 1, j) = hlast;
+        const double res = cyc[r].rotate(j);
         ++out.iterations[r];
-        const double est = std::abs(g[r][j + 1]) / bnorm[r];
+        const double est = res / bnorm[r];
         out.history[r].push_back(est);
         jr[r] = j + 1;
         if (est <= tol || hlast == 0.0) inner[r] = 0;
@@ -493,14 +432,8 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
     // x_r += V_r y_r for every RHS of the cycle, then the true residuals (:109-116)
     std::vector<c64> yh(static_cast<size_t>(m) * G, cmk(0.0, 0.0));
     for (int r : act) {
-      auto Hm = [&](int a, int b) -> cd& { return H[r][static_cast<size_t>(b) * (m + 1) + a]; };
       const int jj = jr[r];
-      std::vector<cd> y(jj);
-      for (int i = jj - 1; i >= 0; --i) {
-        cd acc = g[r][i];
-        for (int k = i + 1; k < jj; ++k) acc -= Hm(i, k) * y[k];
-        y[i] = acc / Hm(i, i);
-      }
+      const std::vector<cd> y = cyc[r].solve(jj);
       for (int i = 0; i < jj; ++i) yh[static_cast<size_t>(r) * m + i] = cmk(y[i].real(), y[i].imag());
     }
     put(o_y, yh.data(), 16 * yh.size());

@@ -68,14 +68,23 @@ inline int guard(const std::function<void()>& fn) {
 using namespace fpbem_cu;  // internal header: the handle below is written in the kernel types
 
 // --------------------------------------------------------------------------
-// NCCL, loaded at runtime so the library has no hard NCCL dependency.
+// Communicator: NCCL (loaded at runtime, so the library has no hard NCCL
+// dependency) or a caller-supplied host all-reduce (e.g. a gloo group),
+// staged through pinned host memory. comm.cu implements the collectives.
 
 struct fpbem_cu_comm {
   void* lib = nullptr;
   void* comm = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0, device = 0;
   int (*allreduce)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
+  int (*reduce_scatter)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
+  int (*allgather)(const void*, void*, size_t, int, void*, void*) = nullptr;
   int (*destroy)(void*) = nullptr;
+  // host callback form (cb != nullptr)
+  fpbem_cu_allreduce_fn cb = nullptr;
+  void* cb_ctx = nullptr;
+  double* stage = nullptr;  // pinned
+  size_t stage_count = 0;
 };
 
 struct fpbem_cu_op {
@@ -167,6 +176,11 @@ namespace fpbem_cu {
 void pair_range(long long n_pairs, int nranks, int rank, double far_pairs, long long& lo, long long& hi);
 void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs);
 double calibrate_far_pairs(fpbem_cu_op* op);
-void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs);
+// y = A x; reduce = false leaves this rank's partial product un-summed
+void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce = true);
 void ensure_pinned(fpbem_cu_op* op, size_t bytes);
+// collectives over fp64 device buffers, ordered on `s` (comm.cu)
+void comm_allreduce(fpbem_cu_comm* c, double* buf, size_t count, cudaStream_t s);
+void comm_reduce_scatter(fpbem_cu_comm* c, double* full, double* mine, size_t per_rank, cudaStream_t s);
+void comm_allgather(fpbem_cu_comm* c, const double* mine, double* full, size_t per_rank, cudaStream_t s);
 }  // namespace fpbem_cu

@@ -95,6 +95,14 @@ cudaError_t launch_b_residual(const c64* b, const c64* ax, c64* res, long long l
                               const BatchScratch& bs, double* result, int* nonfinite, cudaStream_t s);
 cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, long long n, bool gather,
                           cudaStream_t s);
+// classical Gram-Schmidt passes of the distributed GMRES (krylov.cu):
+// partials hold (cols + 1) x kCgsMaxBlocks complex; cols < kCgsMaxCols
+constexpr int kCgsMaxBlocks = 4 * kNumSMs;
+constexpr int kCgsMaxCols = 1024;
+cudaError_t launch_cgs_dots(const c64* V, long long ld, int cols, const c64* w, long long n, c64* partials,
+                            unsigned* counter, c64* out, cudaStream_t s);
+cudaError_t launch_cgs_update(c64* w, const c64* V, long long ld, int cols, const c64* h, long long n,
+                              double* partials, unsigned* counter, double* result, cudaStream_t s);
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,
                             double* result, cudaStream_t s);
 

@@ -179,6 +179,119 @@ __global__ void __launch_bounds__(RT) residual_kernel(const c64* __restrict__ b,
 }
 
 // ---------------------------------------------------------------------------
+// Classical Gram-Schmidt passes of the distributed GMRES (gmres_dist.cu): one
+// pass is a batched projection h = V^H w (+ ||w||^2 and a non-finite count)
+// followed, after the all-reduce of h over the ranks, by w -= V h (+ the new
+// ||w||^2). Each thread keeps kCgsR entries of w in registers and streams the
+// basis columns past them; per-column sums go warp -> shared memory -> block
+// partial -> the last block folds the partials in block order (deterministic).
+constexpr int kCgsR = 4;
+constexpr int kCgsWarps = RT / 32;
+
+__device__ __forceinline__ c64 warp_sum_c(c64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// out[i] = <V_i, w> (i < cols); out[cols] = (||w||^2, number of non-finite entries of w)
+__global__ void __launch_bounds__(RT) cgs_dots_kernel(const c64* __restrict__ V, long long ld, int cols,
+                                                      const c64* __restrict__ w, long long n,
+                                                      c64* __restrict__ partials, unsigned* counter,
+                                                      c64* __restrict__ out) {
+  extern __shared__ c64 acc[];  // [cols + 1][kCgsWarps]
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (cols + 1) * kCgsWarps; i += RT) acc[i] = cmk(0.0, 0.0);
+  __syncthreads();
+  c64 nrm = cmk(0.0, 0.0);
+  const long long tile = static_cast<long long>(RT) * kCgsR;
+  for (long long t0 = blockIdx.x * tile; t0 < n; t0 += static_cast<long long>(gridDim.x) * tile) {
+    c64 wr[kCgsR];
+#pragma unroll
+    for (int u = 0; u < kCgsR; ++u) {
+      const long long k = t0 + u * RT + threadIdx.x;
+      wr[u] = k < n ? w[k] : cmk(0.0, 0.0);
+      nrm.x = fma(wr[u].x, wr[u].x, nrm.x);
+      nrm.x = fma(wr[u].y, wr[u].y, nrm.x);
+      if (!isfinite(wr[u].x) || !isfinite(wr[u].y)) nrm.y += 1.0;
+    }
+    for (int i = 0; i < cols; ++i) {
+      const c64* v = V + static_cast<long long>(i) * ld;
+      c64 sum = cmk(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < kCgsR; ++u) {
+        const long long k = t0 + u * RT + threadIdx.x;
+        if (k < n) sum = cfma_conj(v[k], wr[u], sum);
+      }
+      sum = warp_sum_c(sum);
+      if (lane == 0) acc[i * kCgsWarps + warp] = cadd(acc[i * kCgsWarps + warp], sum);
+    }
+  }
+  nrm = warp_sum_c(nrm);
+  if (lane == 0) acc[cols * kCgsWarps + warp] = cadd(acc[cols * kCgsWarps + warp], nrm);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= cols; i += RT) {
+    c64 sum = cmk(0.0, 0.0);
+    for (int q = 0; q < kCgsWarps; ++q) sum = cadd(sum, acc[i * kCgsWarps + q]);
+    partials[static_cast<long long>(i) * gridDim.x + blockIdx.x] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i <= cols; i += RT) {
+    c64 sum = cmk(0.0, 0.0);
+    for (unsigned q = 0; q < gridDim.x; ++q) sum = cadd(sum, __ldcg(partials + static_cast<long long>(i) * gridDim.x + q));
+    out[i] = sum;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// w -= sum_i h_i V_i (in column order, as the reference's MGS subtracts);
+// result = ||w||^2
+__global__ void __launch_bounds__(RT) cgs_update_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld,
+                                                        int cols, const c64* __restrict__ h, long long n,
+                                                        double* partials, unsigned* counter, double* result) {
+  __shared__ double sh[RT];
+  double nrm = 0.0;
+  const long long tile = static_cast<long long>(RT) * kCgsR;
+  for (long long t0 = blockIdx.x * tile; t0 < n; t0 += static_cast<long long>(gridDim.x) * tile) {
+    c64 wr[kCgsR];
+#pragma unroll
+    for (int u = 0; u < kCgsR; ++u) {
+      const long long k = t0 + u * RT + threadIdx.x;
+      wr[u] = k < n ? w[k] : cmk(0.0, 0.0);
+    }
+    for (int i = 0; i < cols; ++i) {
+      const c64 hi = __ldg(h + i);
+      const c64* v = V + static_cast<long long>(i) * ld;
+#pragma unroll
+      for (int u = 0; u < kCgsR; ++u) {
+        const long long k = t0 + u * RT + threadIdx.x;
+        if (k < n) wr[u] = csub(wr[u], cmul(hi, v[k]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCgsR; ++u) {
+      const long long k = t0 + u * RT + threadIdx.x;
+      if (k < n) {
+        w[k] = wr[u];
+        nrm = fma(wr[u].x, wr[u].x, nrm);
+        nrm = fma(wr[u].y, wr[u].y, nrm);
+      }
+    }
+  }
+  const double t = block_reduce(nrm, sh);
+  finish_reduce(t, partials, counter, result, sh);
+}
+
+// ---------------------------------------------------------------------------
 // Fused modified Gram-Schmidt of one Arnoldi step in a single cooperative
 // launch: ||w||^2 (+ non-finite flag), then for i = 0..j
 //   h_i = <v_i, w>;  w -= h_i v_i          (src/solver.cpp:58-62, same order)
@@ -585,6 +698,33 @@ cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long lon
   void* args[] = {&w, const_cast<c64**>(&V), &ld, &j, &n, &chunk, &h_out, &norms, &nonfinite, &pc, &pd, &pre};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&mgs_fused_kernel), dim3(static_cast<unsigned>(blocks)),
                                      dim3(RT), args, smem, s);
+}
+
+int cgs_blocks(long long n) {
+  const long long tiles = (n + RT * kCgsR - 1) / (RT * kCgsR);
+  return static_cast<int>(tiles < 1 ? 1 : (tiles > kCgsMaxBlocks ? kCgsMaxBlocks : tiles));
+}
+
+cudaError_t launch_cgs_dots(const c64* V, long long ld, int cols, const c64* w, long long n, c64* partials,
+                            unsigned* counter, c64* out, cudaStream_t s) {
+  if (cols < 0 || cols >= kCgsMaxCols) return cudaErrorInvalidValue;
+  const size_t smem = static_cast<size_t>(cols + 1) * kCgsWarps * sizeof(c64);
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    const size_t cap = static_cast<size_t>(kCgsMaxCols) * kCgsWarps * sizeof(c64);
+    cudaError_t e = cudaFuncSetAttribute(cgs_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(cap));
+    if (e != cudaSuccess) return e;
+    configured = cap;
+  }
+  cgs_dots_kernel<<<cgs_blocks(n), RT, smem, s>>>(V, ld, cols, w, n, partials, counter, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgs_update(c64* w, const c64* V, long long ld, int cols, const c64* h, long long n,
+                              double* partials, unsigned* counter, double* result, cudaStream_t s) {
+  cgs_update_kernel<<<cgs_blocks(n), RT, 0, s>>>(w, V, ld, cols, h, n, partials, counter, result);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_residual(const c64* b, const c64* ax, c64* r, long long n, const RedScratch& rs,

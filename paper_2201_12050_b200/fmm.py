@@ -86,6 +86,33 @@ class Communicator:
             self.handle = None
 
 
+class HostCommunicator(Communicator):
+    """The library's communicator over a torch.distributed process group's
+    host all-reduce (gloo): device data is staged through pinned host memory
+    (fpbem_cu_comm_from_callback). For ranks without an NCCL path between them
+    and for multi-rank tests; the NCCL Communicator is the fast path."""
+
+    def __init__(self, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        lib = _native.cuda()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def allreduce(_ctx, buf, count):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(int(count),))
+                dist.all_reduce(torch.from_numpy(arr), group=group)  # in place on the staged host buffer
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+                return 1
+
+        self._cb = _native.ALLREDUCE_FN(allreduce)  # kept alive with the communicator
+        h = C.c_void_p()
+        _raise(lib.fpbem_cu_comm_from_callback(self._cb, None, world, rank, device, C.byref(h)))
+        self.handle, self.rank, self.nranks = h, rank, world
+
+
 @dataclass
 class SolveReport:
     """include/fpbem/solver.hpp:14-19"""
@@ -307,6 +334,44 @@ def gmres(apply, b, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000,
                             bool(conv[r])) for r in range(nrhs)]
         return reps[0] if nrhs == 1 else reps
     return _gmres_callable(apply, b, tol, restart, max_iter, preconditioner, device)
+
+
+def gmres_distributed(op: FmmOperators, b, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000):
+    """Restarted GMRES with the Krylov basis split over the ranks of the
+    operator's communicator (FmmOperators.set_comm) in slabs of whole cells
+    (SURVEY §8e): per step one all-gather, one reduce-scatter and one batched
+    all-reduce per classical Gram-Schmidt pass, with the reference's
+    reorthogonalisation test (fpbem_cu_gmres_dist). Every rank passes the full
+    right-hand side (numpy or CUDA tensor) and gets the full solution. Without
+    a communicator it runs on the operator's device alone."""
+    lib = _native.cuda()
+    if op._nrhs(b) != 1:
+        raise ValueError("gmres_distributed: one right-hand side")
+    its, conv, hlen = C.c_int(), C.c_int(), C.c_int()
+    cap = max(1, max_iter)
+    hist = np.zeros(cap)
+    hp = hist.ctypes.data_as(_native.c_double_p)
+    if _is_torch(b):
+        import torch
+
+        bx = b.contiguous()
+        x = torch.empty_like(bx)
+        rc = lib.fpbem_cu_gmres_dist(op.handle, bx.data_ptr(), x.data_ptr(), tol, restart, max_iter, PTR_DEVICE,
+                                     C.byref(its), C.byref(conv), hp, cap, C.byref(hlen))
+    else:
+        bx = np.ascontiguousarray(b, np.complex128)
+        x = np.zeros_like(bx)
+        rc = lib.fpbem_cu_gmres_dist(op.handle, bx.ctypes.data, x.ctypes.data, tol, restart, max_iter, PTR_HOST,
+                                     C.byref(its), C.byref(conv), hp, cap, C.byref(hlen))
+    _raise(rc)
+    return SolveReport(x, list(hist[:hlen.value]), its.value, bool(conv.value))
+
+
+def dist_rows(op: FmmOperators) -> tuple[int, int]:
+    """This rank's slab [lo, hi) of the global rows under gmres_distributed."""
+    lo, hi = C.c_longlong(), C.c_longlong()
+    _raise(_native.cuda().fpbem_cu_gmres_dist_rows(op.handle, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 def rhs_shard(n_rhs: int, world: int, rank: int) -> list[int]:
