@@ -14,6 +14,7 @@
 // P2M (src/fmm.cpp:256-259) runs as a job list of the DMMA block GEMM (near_field.cu).
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -310,6 +311,56 @@ __global__ void mode_product_kernel(const c64* __restrict__ lambda, const c64* _
 #pragma unroll 5
     for (int j = 0; j < b; ++j) acc = cfma(__ldg(lam + static_cast<long long>(j) * b), f[j], acc);
     image[g] = acc;
+  }
+}
+
+// Multi-RHS mode product on the FP64 tensor cores: per mode q the field block
+// F_q (nrhs x b, rhs-major, contiguous) times Λ_q^T,
+//   image[q][r][i] = sum_j Λ_q(i, j) F_q[r][j]      (C = F Λ^T: M = rhs, N = K = b),
+// the dense contraction of src/structured.cpp:148-152 batched over right-hand
+// sides. One CTA per (mode, block of kModeRows right-hand sides); Λ_q (one
+// contiguous b x b block) and the F_q rows are staged in shared memory, the
+// product runs as 8 x 8 x 4 DMMA tiles with the complex Gauss 3M split.
+constexpr int kModeRows = 64;
+
+__global__ void __launch_bounds__(256)
+mode_gemm_kernel(const c64* __restrict__ lambda, const c64* __restrict__ field, c64* __restrict__ image, int b,
+                 int nrhs) {
+  extern __shared__ __align__(16) unsigned char mg_smem[];
+  const int pf = odd_pitch(b);
+  c64* lam = reinterpret_cast<c64*>(mg_smem);  // [j * b + i] = Λ(i, j), as stored
+  c64* f = lam + b * b;                        // rows x pf
+  const long long q = blockIdx.x;
+  const int r0 = blockIdx.y * kModeRows, rows = min(kModeRows, nrhs - r0);
+  const c64* lq = lambda + q * b * b;
+  for (int k = threadIdx.x; k < b * b; k += blockDim.x) lam[k] = lq[k];
+  const c64* fq = field + (q * nrhs + r0) * b;
+  for (int k = threadIdx.x; k < rows * b; k += blockDim.x) {
+    const int r = k / b;
+    f[r * pf + (k - r * b)] = fq[k];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int tn_count = (b + 7) / 8, tiles = ((rows + 7) / 8) * tn_count;
+  c64* out = image + (q * nrhs + r0) * b;
+  for (int t = warp; t < tiles; t += n_warps) {
+    const int tm = t / tn_count, tn = t - tm * tn_count;
+    double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
+    const int am = tm * 8 + fr, bn = tn * 8 + fr;
+    for (int k0 = 0; k0 < b; k0 += 4) {
+      const int k = k0 + fk;
+      const c64 av = (am < rows && k < b) ? f[am * pf + k] : cmk(0.0, 0.0);
+      const c64 bv = (k < b && bn < b) ? lam[k * b + bn] : cmk(0.0, 0.0);
+      dmma884(t1[0], t1[1], av.x, bv.x);
+      dmma884(t2[0], t2[1], av.y, bv.y);
+      dmma884(t3[0], t3[1], av.x + av.y, bv.x + bv.y);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tn * 8 + 2 * fk + j;
+      if (am < rows && n < b) out[am * b + n] = cmk(t1[j] - t2[j], t3[j] - t1[j] - t2[j]);
+    }
   }
 }
 
@@ -831,6 +882,24 @@ cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, lon
 
 cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image, long long q_total, int b,
                                 int nrhs, cudaStream_t stream) {
+  // the tensor-core contraction from 4 right-hand sides on (FPBEM_MODE_GEMM=0 disables)
+  static const bool gemm_on = [] {
+    const char* v = std::getenv("FPBEM_MODE_GEMM");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const size_t smem = sizeof(c64) * (static_cast<size_t>(b) * b + static_cast<size_t>(kModeRows) * (b | 1));
+  if (gemm_on && nrhs >= 4 && smem <= 200 * 1024) {
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+      cudaError_t e =
+          cudaFuncSetAttribute(mode_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      configured = smem;
+    }
+    const dim3 grid(static_cast<unsigned>(q_total), static_cast<unsigned>((nrhs + kModeRows - 1) / kModeRows));
+    mode_gemm_kernel<<<grid, 256, smem, stream>>>(lambda, field, image, b, nrhs);
+    return cudaGetLastError();
+  }
   const long long total = q_total * b * nrhs;
   mode_product_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lambda, field, image, q_total, b, nrhs);
   return cudaGetLastError();
