@@ -12,6 +12,7 @@
 // (nrhs x b, contiguous) innermost, so every warp access is coalesced. The
 // per-mode product streams Λ once per apply (the HBM-bound part).
 // P2M (src/fmm.cpp:256-259) runs as a job list of the DMMA block GEMM (near_field.cu).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -360,6 +361,73 @@ mode_gemm_kernel(const c64* __restrict__ lambda, const c64* __restrict__ field, 
     for (int j = 0; j < 2; ++j) {
       const int n = tn * 8 + 2 * fk + j;
       if (am < rows && n < b) out[am * b + n] = cmk(t1[j] - t2[j], t3[j] - t1[j] - t2[j]);
+    }
+  }
+}
+
+// Multi-RHS P2M on the FP64 tensor cores: all right-hand sides and cells are
+// one skinny GEMM sharing V0,
+//   mom[cell nrhs + r][c] = sum_j x[r N + cell n + j] V0[c][j]   (M = cells nrhs, N = b, K = n).
+// Persistent CTAs (one per SM) hold V0^T in shared memory (row pitch = 4 mod 8
+// complex: the 8 x 4 fragment loads hit distinct 16-byte slots); each warp
+// takes 8-row tiles in turn, streams its x rows from HBM in 8 x 4 fragments and
+// keeps four 8 x 8 coefficient tiles in registers (Gauss 3M as in mode_gemm_kernel).
+constexpr int kP2mWarps = 16;
+
+__host__ __device__ inline int p2m_pitch(int n) { return ((n + 3) / 8) * 8 + 4; }
+
+__global__ void __launch_bounds__(kP2mWarps * 32, 1)
+p2m_gemm_kernel(const c64* __restrict__ v0t, const c64* __restrict__ x, c64* __restrict__ mom, int n, int b,
+                long long N, int nrhs, int cells) {
+  extern __shared__ __align__(16) unsigned char p2m_smem[];
+  c64* vs = reinterpret_cast<c64*>(p2m_smem);
+  const int pk = p2m_pitch(n);
+  for (int k = threadIdx.x; k < b * n; k += blockDim.x) {
+    const int c = k / n;
+    vs[c * pk + (k - c * n)] = v0t[k];
+  }
+  __syncthreads();
+  const long long rows = static_cast<long long>(cells) * nrhs, tiles = (rows + 7) / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  for (long long t = static_cast<long long>(blockIdx.x) * kP2mWarps + warp; t < tiles;
+       t += static_cast<long long>(gridDim.x) * kP2mWarps) {
+    const long long rho = t * 8 + fr;  // output row cell * nrhs + r
+    const bool row_ok = rho < rows;
+    const long long cell = row_ok ? rho / nrhs : 0, r = row_ok ? rho - cell * nrhs : 0;
+    const c64* xr = x + r * N + cell * n;
+    for (int tn0 = 0; tn0 < b; tn0 += 32) {  // four 8-wide coefficient tiles at a time
+      double t1[4][2] = {}, t2[4][2] = {}, t3[4][2] = {};
+      for (int k0 = 0; k0 < n; k0 += 16) {
+        c64 av[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int k = k0 + 4 * s + fk;
+          av[s] = (row_ok && k < n) ? __ldcs(xr + k) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int k = k0 + 4 * s + fk;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = tn0 + 8 * u + fr;
+            const c64 bv = (c < b && k < n) ? vs[c * pk + k] : cmk(0.0, 0.0);
+            dmma884(t1[u][0], t1[u][1], av[s].x, bv.x);
+            dmma884(t2[u][0], t2[u][1], av[s].y, bv.y);
+            dmma884(t3[u][0], t3[u][1], av[s].x + av[s].y, bv.x + bv.y);
+          }
+        }
+      }
+      // D fragment: lane (fr, fk) holds row fr, columns 2 fk and 2 fk + 1 of each tile
+      if (row_ok) {
+        c64* out = mom + rho * b;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = tn0 + 8 * u + 2 * fk + j;
+            if (c < b) out[c] = cmk(t1[u][j] - t2[u][j], t3[u][j] - t1[u][j] - t2[u][j]);
+          }
+      }
     }
   }
 }
@@ -870,6 +938,24 @@ cudaError_t launch_xy_plane(const c64* in, c64* out, const c64* twx, const c64* 
 cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, long long N, int nrhs, int cells,
                        cudaStream_t stream) {
   if (cells == 0 || nrhs == 0) return cudaSuccess;
+  static const bool gemm_on = [] {  // FPBEM_P2M_GEMM=0: the FMA kernel for every rhs count
+    const char* v = std::getenv("FPBEM_P2M_GEMM");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const size_t smem = sizeof(c64) * static_cast<size_t>(b) * p2m_pitch(n);
+  if (gemm_on && nrhs >= 4 && smem <= 200 * 1024) {
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+      cudaError_t e =
+          cudaFuncSetAttribute(p2m_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      configured = 200 * 1024;
+    }
+    const long long tiles = (static_cast<long long>(cells) * nrhs + 7) / 8;
+    const int grid = static_cast<int>(std::min<long long>(kNumSMs, (tiles + kP2mWarps - 1) / kP2mWarps));
+    p2m_gemm_kernel<<<grid, kP2mWarps * 32, smem, stream>>>(v0t, x, mom, n, b, N, nrhs, cells);
+    return cudaGetLastError();
+  }
   const long long blocks = static_cast<long long>(cells) * nrhs;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
   if (blocks >= 4LL * kNumSMs) {

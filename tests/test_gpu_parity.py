@@ -187,11 +187,11 @@ def test_multi_rhs_equals_single_rhs(ops, assembled):
         assert rel(y[r * d.N:(r + 1) * d.N], single(P[r])) <= 1e-14
 
 
-@pytest.mark.parametrize("cid,var,nrhs", [(1, 0, 4), (2, 2, 5), (3, 2, 8), (5, 2, 70), (4, 2, 6)])
+@pytest.mark.parametrize("cid,var,nrhs", [(1, 0, 4), (2, 2, 5), (3, 2, 8), (5, 2, 70), (4, 2, 6), (1, 1, 13)])
 def test_multi_rhs_tensor_core_mode_product(ops, assembled, cid, var, nrhs):
     """From 4 right-hand sides the per-mode product is a DMMA contraction
-    (mode_gemm_kernel; 70 rhs = two row blocks): every rhs equals its own
-    single-rhs product and the oracle."""
+    (mode_gemm_kernel), and the P2M (p2m_gemm_kernel); 70 rhs = two
+    row blocks: every rhs equals its own single-rhs product and the oracle."""
     sc, d = assembled(cid, var)
     rng = np.random.default_rng(nrhs)
     P = [uvec(rng, d.N) for _ in range(nrhs)]
