@@ -95,7 +95,17 @@ typedef struct {
                                     `device` (e.g. from fpbem_cu_assemble_near)            */
   int far_on_device;             /* 1: far_blocks / far_hat_blocks are device pointers on
                                     `device` (e.g. from fpbem_cu_m2l_bank)                 */
+  int near_path;                 /* FPBEM_CU_NEAR_*: how the Toeplitz near field S p is
+                                    applied (same product, different arithmetic order)    */
 } fpbem_cu_fmm_desc;
+
+#define FPBEM_CU_NEAR_AUTO 0       /* cost model picks (fpbem_cu_fmm_near_path reports it)   */
+#define FPBEM_CU_NEAR_DIRECT 1     /* one GEMM per stored offset over its valid targets, as
+                                      BlockToeplitzMatrix::matvec (src/assembly.cpp:62-84)  */
+#define FPBEM_CU_NEAR_LATTICE 2    /* circulant embedding of the blocks in an (M + max|o|)
+                                      lattice, DFT'd once at create; per apply: pruned DFT of
+                                      x, one n x n block product per mode, pruned inverse
+                                      (no half-space image pair)                            */
 
 /* Unit cell for the device assembly, BIE-oriented (assembly::bie_oriented,
  * src/assembly.cpp:17-21): flat quads, or triangles with corner 3 == corner 2. */
@@ -186,6 +196,9 @@ int fpbem_cu_gmres_fn(int device, long long n, fpbem_cu_apply_fn apply, void* ap
 /* Device bytes of the operator data, counted like FmmOperators::stored_bytes
  * (S blocks + spectrum + U0 + V0). */
 int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes);
+/* The near-field path in use (FPBEM_CU_NEAR_DIRECT / _LATTICE), its lattice
+ * sizes (1,1,1 for direct) and the device bytes of its block spectrum. */
+int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes);
 
 /* Spectrum readback (sizes[3] always; lambda_out may be NULL). */
 int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out);

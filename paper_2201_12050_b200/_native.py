@@ -55,6 +55,7 @@ class FmmDesc(C.Structure):
         ("lambda_hat", C.c_void_p),
         ("blocks_on_device", C.c_int),
         ("far_on_device", C.c_int),
+        ("near_path", C.c_int),
     ]
 
 
@@ -82,7 +83,7 @@ ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_
 # every symbol include/fpbem_cuda.h declares (checked by tests/test_boundary.py)
 CUDA_SYMBOLS = (
     "fpbem_cu_fmm_create", "fpbem_cu_fmm_destroy", "fpbem_cu_fmm_apply", "fpbem_cu_gmres",
-    "fpbem_cu_gmres_fn", "fpbem_cu_fmm_bytes", "fpbem_cu_spectrum", "fpbem_cu_set_stream",
+    "fpbem_cu_gmres_fn", "fpbem_cu_fmm_bytes", "fpbem_cu_fmm_near_path", "fpbem_cu_spectrum", "fpbem_cu_set_stream",
     "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
     "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
     "fpbem_cu_comm_from_callback", "fpbem_cu_gmres_dist", "fpbem_cu_gmres_dist_rows",
@@ -109,6 +110,7 @@ def cuda() -> C.CDLL:
                                             C.c_int, C.c_int, C.c_int, c_int_p, c_int_p, c_double_p, C.c_int,
                                             c_int_p]),
             "fpbem_cu_fmm_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
+            "fpbem_cu_fmm_near_path": (C.c_int, [vp, c_int_p, c_int_p, C.POINTER(C.c_size_t)]),
             "fpbem_cu_spectrum": (C.c_int, [vp, c_int_p, vp]),
             "fpbem_cu_set_stream": (C.c_int, [vp, vp]),
             "fpbem_cu_enable_stage_timing": (C.c_int, [vp, C.c_int]),

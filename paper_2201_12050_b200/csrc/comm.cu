@@ -213,8 +213,8 @@ int fpbem_cu_fmm_set_partition(fpbem_cu_op* op, int rank, int nranks, double far
 int fpbem_cu_fmm_partition(const fpbem_cu_op* op, long long* lo, long long* hi, double* far_pairs) {
   return guard([&] {
     if (!op || !lo || !hi || !far_pairs) fail(FPBEM_CU_EINVAL, "partition: null argument");
-    *lo = op->pair_lo;
-    *hi = op->pair_hi;
+    *lo = op->near_fft ? op->mode_lo : op->pair_lo;  // the unit range of the near path in use
+    *hi = op->near_fft ? op->mode_hi : op->pair_hi;
     *far_pairs = op->far_pairs;
   });
 }

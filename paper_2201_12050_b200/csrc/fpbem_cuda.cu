@@ -75,10 +75,15 @@ void build_target_csr(fpbem_cu_op* op) {
 void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
   if (nranks < 1 || rank < 0 || rank >= nranks) fail(FPBEM_CU_EINVAL, "partition: bad rank / nranks");
   if (!(far_pairs >= 0.0)) fail(FPBEM_CU_EINVAL, "partition: far_pairs must be >= 0");
-  pair_range(op->n_pairs, nranks, rank, far_pairs, op->pair_lo, op->pair_hi);
   op->far_pairs = far_pairs;
   op->rank = rank;
   op->nranks = nranks;
+  if (op->near_fft) {  // units are the modes of the near-field lattice (each one n x n block product)
+    pair_range(op->qn, nranks, rank, far_pairs, op->mode_lo, op->mode_hi);
+    op->mjobs_nrhs = -1;
+    return;
+  }
+  pair_range(op->n_pairs, nranks, rank, far_pairs, op->pair_lo, op->pair_hi);
   op->jobs_nrhs = -1;  // rebuild the GEMM job list
   build_target_csr(op);
 }
@@ -126,6 +131,124 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
   if (!jobs.empty()) h2d(op->jobs, jobs.data(), jobs.size() * sizeof(int4), op->stream, "jobs upload");
   op->n_jobs = static_cast<int>(jobs.size());
   op->jobs_nrhs = nrhs;
+}
+
+// DMMA jobs of the lattice path: one column tile set (the nrhs right-hand sides)
+// per mode of this rank's range; block slot = mode, unit = mode
+void build_mode_jobs(fpbem_cu_op* op, int nrhs) {
+  if (op->mjobs_nrhs == nrhs) return;
+  std::vector<int4> jobs;
+  for (long long q = op->mode_lo; q < op->mode_hi; ++q)
+    tile_columns(jobs, static_cast<int>(q), nrhs, static_cast<int>(q), true);
+  if (static_cast<int>(jobs.size()) > op->mjobs_cap) {
+    if (op->mjobs) cudaFree(op->mjobs);
+    op->mjobs = dalloc<int4>(jobs.size(), "mode jobs");
+    op->mjobs_cap = static_cast<int>(jobs.size());
+  }
+  if (!jobs.empty()) h2d(op->mjobs, jobs.data(), jobs.size() * sizeof(int4), op->stream, "mode jobs upload");
+  op->n_mjobs = static_cast<int>(jobs.size());
+  op->mjobs_nrhs = nrhs;
+}
+
+void twiddles(fpbem_cu_op* op, int L, c64** out);
+
+// Block spectrum of the near field (the CirculantSpectrum construction,
+// src/structured.cpp:63-108, applied to the Toeplitz blocks): S_o at slot
+// (o mod Ln), forward DFT over every axis. Ln_d = M_d + max|o_d| is the
+// smallest length whose circular convolution reproduces the truncated
+// Toeplitz product (sources t - o in [-R, M-1+R] never alias into [0, M)).
+void build_near_spectrum(fpbem_cu_op* op, int n_toeplitz) {
+  const size_t nn = static_cast<size_t>(op->n) * op->n;
+  const size_t total = static_cast<size_t>(op->qn) * nn;
+  const long long Lx = op->Ln[0], Ly = op->Ln[1], Lz = op->Ln[2];
+  using DevPtr = std::unique_ptr<void, decltype(&cudaFree)>;
+  c64* a = dalloc<c64>(total, "near spectrum");
+  DevPtr keep_a(a, &cudaFree);
+  c64* b = dalloc<c64>(total, "near spectrum scratch");
+  DevPtr keep_b(b, &cudaFree);
+  int* offs = dalloc<int>(static_cast<size_t>(n_toeplitz) * 3, "near offsets");
+  DevPtr keep_offs(offs, &cudaFree);
+  h2d(offs, op->near_offsets.data(), static_cast<size_t>(n_toeplitz) * 3 * sizeof(int), op->stream, "near offsets");
+  for (int k = 0; k < 3; ++k) twiddles(op, op->Ln[k], &op->twn[k]);
+  check(cudaMemsetAsync(a, 0, total * sizeof(c64), op->stream), "near spectrum clear");
+  check(launch_scatter_bank(op->S, offs, n_toeplitz, static_cast<int>(nn), op->Ln[0], op->Ln[1], op->Ln[2], a,
+                            op->stream),
+        "near scatter");
+  c64* cur = a;
+  c64* nxt = b;
+  if (Lx > 1) {
+    check(launch_dft_axis(cur, nxt, op->twn[0], Ly * Lz, op->Ln[0], op->Ln[0], nn, op->Ln[0], false, 1.0, op->stream),
+          "near spectrum dft x");
+    std::swap(cur, nxt);
+  }
+  if (Ly > 1) {
+    check(launch_dft_axis(cur, nxt, op->twn[1], Lz, op->Ln[1], op->Ln[1], Lx * nn, op->Ln[1], false, 1.0, op->stream),
+          "near spectrum dft y");
+    std::swap(cur, nxt);
+  }
+  if (Lz > 1) {
+    check(launch_dft_axis(cur, nxt, op->twn[2], 1, op->Ln[2], op->Ln[2], Lx * Ly * nn, op->Ln[2], false, 1.0,
+                          op->stream),
+          "near spectrum dft z");
+    std::swap(cur, nxt);
+  }
+  check(cudaStreamSynchronize(op->stream), "near spectrum build");
+  if (cur == a)
+    keep_a.release();
+  else
+    keep_b.release();
+  op->shat = cur;
+}
+
+// Lattice-path near field: y = (1/qn) IDFT(Shat . DFT(x)) truncated to the M
+// cells per axis, for this rank's modes (zero elsewhere, so the ranks' partial
+// products sum to the product). Forward passes read only the M nonzero cells
+// per axis, inverse passes write only the M kept cells; the last one writes y.
+void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_t s) {
+  const long long n = op->n, r = nrhs;
+  const int Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
+  const int Lx = op->Ln[0], Ly = op->Ln[1], Lz = op->Ln[2];
+  c64* bufs[2] = {op->nfa, op->nfb};
+  int which = 0;
+  const c64* cur = x;
+  auto fwd = [&](int axis, long long n_a, int m, int l, long long inner) {
+    c64* out = bufs[which];
+    which ^= 1;
+    check(launch_dft_axis(cur, out, op->twn[axis], n_a, m, l, inner, l, false, 1.0, s), "near dft");
+    op->launches++;
+    cur = out;
+  };
+  if (Lx > 1) fwd(0, r * My * Mz, Mx, Lx, n);
+  if (Ly > 1) fwd(1, r * Mz, My, Ly, Lx * n);
+  if (Lz > 1) fwd(2, r, Mz, Lz, static_cast<long long>(Ly) * Lx * n);
+  c64* yh = bufs[which];
+  which ^= 1;
+  if (op->mode_lo > 0 || op->mode_hi < op->qn)
+    check(cudaMemsetAsync(yh, 0, static_cast<size_t>(r * op->qn * n) * sizeof(c64), s), "near spectrum clear");
+  if (nrhs <= kModeGemvMaxRhs) {
+    check(launch_mode_gemv(op->shat, cur, yh, op->n, op->mode_lo, op->mode_hi, op->qn, nrhs, s), "near mode gemv");
+  } else {
+    build_mode_jobs(op, nrhs);
+    check(launch_block_gemm(op->shat, n * n, op->n, op->n, cur, yh, op->n, nullptr, op->mjobs, op->n_mjobs, op->n,
+                            op->n, op->qn * n, nrhs, s, op->qn * n),
+          "near mode gemm");
+  }
+  op->launches++;
+  cur = yh;
+  int left = (Lx > 1) + (Ly > 1) + (Lz > 1);
+  const double scale = 1.0 / static_cast<double>(op->qn);
+  auto inv = [&](int axis, long long n_a, int l, int m, long long inner) {
+    const bool last = --left == 0;
+    c64* out = last ? y : bufs[which];
+    which ^= 1;
+    check(launch_dft_axis(cur, out, op->twn[axis], n_a, l, m, inner, l, true, last ? scale : 1.0, s),
+          "near inverse dft");
+    op->launches++;
+    cur = out;
+  };
+  if (Lz > 1) inv(2, r, Lz, Mz, static_cast<long long>(Ly) * Lx * n);
+  if (Ly > 1) inv(1, r * Mz, Ly, My, Lx * n);
+  if (Lx > 1) inv(0, r * My * Mz, Lx, Mx, n);
 }
 
 void twiddles(fpbem_cu_op* op, int L, c64** out) {
@@ -330,7 +453,7 @@ void far_field(fpbem_cu_op* op, const c64* x, int nrhs, cudaStream_t a) {
 // all on the handle's stream (best of 3 after a warm-up). Rank 0 carries the
 // far field under the pair partition, so it gets this many fewer pairs.
 double calibrate_far_pairs(fpbem_cu_op* op) {
-  if (op->n_pairs == 0) return 0.0;
+  if (op->n_pairs == 0 && !op->near_fft) return 0.0;
   const int rank = op->rank, nranks = op->nranks;
   const double far_pairs = op->far_pairs;
   set_partition(op, 0, 1, 0.0);
@@ -343,13 +466,19 @@ double calibrate_far_pairs(fpbem_cu_op* op) {
   std::unique_ptr<cudaEvent_t, void (*)(cudaEvent_t*)> keep_e(e, [](cudaEvent_t* v) {
     for (int i = 0; i < 3; ++i) cudaEventDestroy(v[i]);
   });
-  build_jobs(op, 1);
+  c64* yc = nullptr;
+  if (op->near_fft) yc = dalloc<c64>(static_cast<size_t>(op->N), "calibration output");
+  std::unique_ptr<c64, decltype(&cudaFree)> keep_y(yc, &cudaFree);
+  if (!op->near_fft) build_jobs(op, 1);
   float best_near = 1e30f, best_far = 1e30f;
   for (int it = 0; it < 4; ++it) {
     check(cudaEventRecord(e[0], s), "calibration");
-    check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n, op->pair_src,
-                            op->jobs, op->n_jobs, op->n, op->n, op->N, 1, s),
-          "calibration gemm");
+    if (op->near_fft)
+      near_fft_apply(op, x, yc, 1, s);
+    else
+      check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n,
+                              op->pair_src, op->jobs, op->n_jobs, op->n, op->n, op->N, 1, s),
+            "calibration gemm");
     check(cudaEventRecord(e[1], s), "calibration");
     far_field(op, x, 1, s);
     check(cudaEventRecord(e[2], s), "calibration");
@@ -363,7 +492,8 @@ double calibrate_far_pairs(fpbem_cu_op* op) {
     }
   }
   set_partition(op, rank, nranks, far_pairs);
-  return best_near > 0.0f ? static_cast<double>(best_far) / best_near * static_cast<double>(op->n_pairs) : 0.0;
+  const double units = op->near_fft ? static_cast<double>(op->qn) : static_cast<double>(op->n_pairs);
+  return best_near > 0.0f ? static_cast<double>(best_far) / best_near * units : 0.0;
 }
 
 // One FMM product for nrhs <= max_rhs right-hand sides, device pointers.
@@ -380,25 +510,36 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
   }();
   cudaStream_t a = serial ? op->stream : op->aux;
   const bool far_here = op->rank == 0;
-  build_jobs(op, nrhs);
-  // fork: P2M + M2L on the aux stream while the near-field GEMM runs on the main one
+  if (!op->near_fft) build_jobs(op, nrhs);
+  // fork: P2M + M2L on the aux stream while the near field runs on the main one
   check(cudaEventRecord(op->fork, s), "fork");
   check(cudaStreamWaitEvent(a, op->fork, 0), "fork");
   ev_record(op, 0, s);
-  check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n, op->pair_src,
-                          op->jobs, op->n_jobs, op->n, op->n, op->N, nrhs, s),
-        "near gemm");
-  op->launches += op->n_jobs > 0;
+  if (op->near_fft) {
+    near_fft_apply(op, x, y, nrhs, s);  // y = S p
+  } else {
+    check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n,
+                            op->pair_src, op->jobs, op->n_jobs, op->n, op->n, op->N, nrhs, s),
+          "near gemm");
+    op->launches += op->n_jobs > 0;
+  }
   ev_record(op, 1, s);
   if (far_here) far_field(op, x, nrhs, a);
   check(cudaEventRecord(op->join, a), "join");
   s = op->stream;
   check(cudaStreamWaitEvent(s, op->join, 0), "join");
   ev_record(op, 5, s);
-  check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, far_here ? op->loc : nullptr, y, op->n,
-                               op->b, op->n_cells, op->N, nrhs, false, s),
-        "near reduce + l2p");
-  op->launches++;
+  if (!op->near_fft) {
+    check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, far_here ? op->loc : nullptr, y, op->n,
+                                 op->b, op->n_cells, op->N, nrhs, false, s),
+          "near reduce + l2p");
+    op->launches++;
+  } else if (far_here) {  // y += U0 L (src/fmm.cpp:265-267): the reduction with no pairs, accumulating
+    check(launch_near_reduce_l2p(nullptr, op->zero_ptr, op->zero_ptr, op->u0, op->loc, y, op->n, op->b, op->n_cells,
+                                 op->N, nrhs, true, s),
+          "l2p");
+    op->launches++;
+  }
   if (op->comm && reduce)  // sum the ranks' partial products, in place, on the same stream
     comm_allreduce(op->comm, reinterpret_cast<double*>(y), static_cast<size_t>(2) * op->N * nrhs, s);
   ev_record(op, 6, s);
@@ -424,6 +565,53 @@ void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) 
     const int c = std::min(op->max_rhs, nrhs - r0);
     apply_chunk(op, x + static_cast<long long>(r0) * op->N, y + static_cast<long long>(r0) * op->N, c, reduce);
   }
+}
+
+// Direct Toeplitz GEMM or lattice convolution for the near field. Cost model
+// (DESIGN.md §3.1b), at the largest batch the handle serves: the direct path is
+// FP64-tensor bound, 8 n^2 flops per (pair, rhs) at ~36 TFLOP/s; the lattice
+// path streams the block spectrum once (16 n^2 bytes per mode, ~6 TB/s) or, for
+// many right-hand sides, is bound by its 8 n^2 flops per (mode, rhs), plus the
+// pruned DFT passes of x and y. Lattice when it is >= 20 % cheaper and its
+// spectrum fits in a third of the free device memory. FPBEM_NEAR=direct|lattice
+// overrides the descriptor (A/B runs).
+void choose_near_path(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
+  int path = d->near_path;
+  if (const char* e = std::getenv("FPBEM_NEAR")) {
+    if (std::strcmp(e, "direct") == 0) path = FPBEM_CU_NEAR_DIRECT;
+    if (std::strcmp(e, "lattice") == 0) path = FPBEM_CU_NEAR_LATTICE;
+  }
+  if (path < FPBEM_CU_NEAR_AUTO || path > FPBEM_CU_NEAR_LATTICE) fail(FPBEM_CU_EINVAL, "create: bad near_path");
+  const bool possible = op->n_hat == 0 && op->n_cells > 1 && d->n_near > 0;
+  if (path == FPBEM_CU_NEAR_LATTICE && !possible)
+    fail(FPBEM_CU_EINVAL, "create: lattice near field needs >= 2 cells, near blocks and no half-space image pair");
+  int R[3] = {0, 0, 0};
+  for (int s = 0; s < d->n_near; ++s)
+    for (int k = 0; k < 3; ++k) R[k] = std::max(R[k], std::abs(op->near_offsets[3 * s + k]));
+  int Ln[3];
+  long long qn = 1;
+  for (int k = 0; k < 3; ++k) {
+    Ln[k] = op->counts[k] == 1 ? 1 : op->counts[k] + R[k];
+    qn *= Ln[k];
+  }
+  const double nn = static_cast<double>(op->n) * op->n;
+  const double spec_bytes = 16.0 * nn * static_cast<double>(qn);
+  bool use = path == FPBEM_CU_NEAR_LATTICE;
+  if (path == FPBEM_CU_NEAR_AUTO && possible) {
+    const double r = op->max_rhs;
+    const double t_direct = 8.0 * nn * op->n_pairs * r / 36e12;
+    int axes = 0;
+    for (int k = 0; k < 3; ++k) axes += Ln[k] > 1;
+    const double t_pass = axes * 2.0 * 32.0 * r * op->n * static_cast<double>(qn + op->n_cells) / 4e12;
+    const double t_lat = std::max(spec_bytes / 6e12, 8.0 * nn * static_cast<double>(qn) * r / 30e12) + t_pass;
+    size_t free_b = 0, total_b = 0;
+    check(cudaMemGetInfo(&free_b, &total_b), "mem info");
+    use = t_lat < 0.8 * t_direct && 2.0 * spec_bytes < static_cast<double>(free_b) / 1.5;
+  }
+  if (!use) return;
+  op->near_fft = true;
+  for (int k = 0; k < 3; ++k) op->Ln[k] = Ln[k];
+  op->qn = qn;
 }
 
 void ensure_pinned(fpbem_cu_op* op, size_t bytes) {
@@ -605,9 +793,22 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
                      &op->lambda_hat);
     }
 
+    choose_near_path(op, d);
+    if (op->near_fft) {
+      build_near_spectrum(op, d->n_near);
+      const size_t f = static_cast<size_t>(op->max_rhs) * op->qn * op->n;
+      op->nfa = dalloc<c64>(f, "near x spectrum");
+      op->nfb = dalloc<c64>(f, "near y spectrum");
+      op->zero_ptr = dalloc<int>(static_cast<size_t>(op->n_cells) + 1, "zero csr");
+      check(cudaMemsetAsync(op->zero_ptr, 0, (static_cast<size_t>(op->n_cells) + 1) * sizeof(int), op->stream),
+            "zero csr");
+      op->mode_lo = 0;
+      op->mode_hi = op->qn;
+    }
+
     // apply buffers
     const long long E = static_cast<long long>(op->max_rhs) * op->b;
-    op->W = dalloc<c64>(static_cast<size_t>(op->n_pairs) * op->max_rhs * op->n, "near workspace");
+    op->W = dalloc<c64>(op->near_fft ? 1 : static_cast<size_t>(op->n_pairs) * op->max_rhs * op->n, "near workspace");
     op->mom = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "moments");
     op->loc = dalloc<c64>(static_cast<size_t>(op->n_cells) * E, "locals");
     op->fa = dalloc<c64>(static_cast<size_t>(op->q_total) * E, "m2l field");
@@ -636,7 +837,10 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
                   static_cast<void*>(op->fb), static_cast<void*>(op->xin), static_cast<void*>(op->yout),
                   static_cast<void*>(op->basis), static_cast<void*>(op->gx), static_cast<void*>(op->gb),
                   static_cast<void*>(op->gt), static_cast<void*>(op->gsol), static_cast<void*>(op->scal_c), static_cast<void*>(op->rs.partial_d),
-                  static_cast<void*>(op->rs.partial_c), static_cast<void*>(op->rs.counter)})
+                  static_cast<void*>(op->rs.partial_c), static_cast<void*>(op->rs.counter),
+                  static_cast<void*>(op->shat), static_cast<void*>(op->twn[0]), static_cast<void*>(op->twn[1]),
+                  static_cast<void*>(op->twn[2]), static_cast<void*>(op->nfa), static_cast<void*>(op->nfb),
+                  static_cast<void*>(op->zero_ptr), static_cast<void*>(op->mjobs)})
     if (p) cudaFree(p);
   if (op->pinned) cudaFreeHost(op->pinned);
   for (auto& e : op->ev)
@@ -691,6 +895,17 @@ int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes) {
   const size_t spectra = op->lambda_hat ? 2 : 1;
   *bytes = c * (static_cast<size_t>(op->n_near) * op->n * op->n +
                 spectra * static_cast<size_t>(op->q_total) * op->b * op->b + 2 * static_cast<size_t>(op->n) * op->b);
+  return FPBEM_CU_OK;
+}
+
+int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes) {
+  if (!op || !path || !sizes || !spectrum_bytes) {
+    g_err = "near_path: null argument";
+    return FPBEM_CU_EINVAL;
+  }
+  *path = op->near_fft ? FPBEM_CU_NEAR_LATTICE : FPBEM_CU_NEAR_DIRECT;
+  for (int k = 0; k < 3; ++k) sizes[k] = op->near_fft ? op->Ln[k] : 1;
+  *spectrum_bytes = op->near_fft ? static_cast<size_t>(op->qn) * op->n * op->n * sizeof(c64) : 0;
   return FPBEM_CU_OK;
 }
 

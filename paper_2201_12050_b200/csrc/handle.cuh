@@ -114,6 +114,21 @@ struct fpbem_cu_op {
   std::vector<int> pair_tgt;    // host copy: target cell of every pair
   int rank = 0, nranks = 1;     // near-field offset partition
 
+  // near field as a lattice convolution: the Toeplitz blocks
+  // embedded in an Ln lattice (Ln = M + max|o| per axis) and DFT'd once, so the
+  // product is pruned DFT -> per-mode block product -> pruned inverse DFT
+  bool near_fft = false;
+  int Ln[3] = {1, 1, 1};
+  long long qn = 0;
+  c64* shat = nullptr;  // qn blocks n x n column-major, q = (qz*Lny + qy)*Lnx + qx
+  c64* twn[3] = {nullptr, nullptr, nullptr};
+  c64* nfa = nullptr;   // spectra of x / y, [rhs][q][n], sized for max_rhs
+  c64* nfb = nullptr;
+  int* zero_ptr = nullptr;  // n_cells + 1 zeros: the L2P-only reduction
+  int4* mjobs = nullptr;    // DMMA jobs over this rank's modes (nrhs > kModeGemvMaxRhs)
+  int mjobs_nrhs = -1, n_mjobs = 0, mjobs_cap = 0;
+  long long mode_lo = 0, mode_hi = 0;  // this rank's modes
+
   // expansions and spectrum
   c64* u0 = nullptr;
   c64* v0 = nullptr;

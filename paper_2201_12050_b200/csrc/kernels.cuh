@@ -10,7 +10,13 @@ namespace fpbem_cu {
 // columns are (pair, rhs) with rhs fastest, or (cell, rhs) when pair_src is null.
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
-                              cudaStream_t stream);
+                              cudaStream_t stream, long long out_rhs_stride = 0);
+// out_rhs_stride > 0: column (unit, rhs) lands at out[rhs * out_rhs_stride + unit * ldo] (rhs-major)
+// near field as a lattice convolution: yh[r][q] = shat_q xh[r][q] for modes q in [q_lo, q_hi),
+// nrhs <= kModeGemvMaxRhs right-hand sides at stride q_stride * n
+constexpr int kModeGemvMaxRhs = 8;
+cudaError_t launch_mode_gemv(const c64* shat, const c64* xh, c64* yh, int n, long long q_lo, long long q_hi,
+                             long long q_stride, int nrhs, cudaStream_t stream);
 cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* tgt_pairs, const c64* u0,
                                    const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
                                    int nrhs, bool accumulate, cudaStream_t stream);

@@ -130,7 +130,7 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
 __global__ void __launch_bounds__(THREADS, 2)
 near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, int M, const c64* __restrict__ x,
                       c64* __restrict__ out, int ldo, const int* __restrict__ pair_src, const int4* __restrict__ jobs,
-                      int K, int n, long long N, int nrhs) {
+                      int K, int n, long long N, int nrhs, long long out_rhs_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   c64* As = reinterpret_cast<c64*>(smem_raw);
   c64* Bs = reinterpret_cast<c64*>(smem_raw + kSmemA);
@@ -151,7 +151,8 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
       const int r = gc % nrhs;
       const long long cell = pair_src ? pair_src[unit] : unit;
       col_src[tid] = static_cast<long long>(r) * N + cell * n;
-      col_out[tid] = (static_cast<long long>(pair_base) * nrhs + gc) * ldo;
+      col_out[tid] = out_rhs_stride > 0 ? r * out_rhs_stride + static_cast<long long>(unit) * ldo
+                                        : (static_cast<long long>(pair_base) * nrhs + gc) * ldo;
     } else {
       col_src[tid] = -1;
       col_out[tid] = -1;
@@ -199,6 +200,61 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
     case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
     default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
   }
+}
+
+// Near field as a lattice convolution: per Fourier mode q of
+// the near-field embedding, yh[r][q] = Shat_q xh[r][q] with Shat_q the n x n
+// column-major block of the lattice DFT of the embedded S_o (the same circulant
+// embedding CirculantSpectrum uses for K, src/structured.cpp:63-108, applied to
+// the Toeplitz blocks of BlockToeplitzMatrix, src/assembly.cpp:62-84). For a few
+// right-hand sides this is a streaming complex GEMV over all modes: one thread
+// per row, the k loop in fixed ascending order (deterministic), Shat read once
+// with 8 independent 16-byte loads in flight per thread, the RHS chunk staged in
+// shared memory. HBM-bound: 16 n^2 bytes per mode.
+constexpr int GEMV_THREADS = 128;
+constexpr int GEMV_KC = 256;  // k chunk of xh staged in shared memory
+constexpr int GEMV_U = 8;     // independent Shat loads per thread
+
+template <int R>
+__global__ void __launch_bounds__(GEMV_THREADS)
+near_mode_gemv_kernel(const c64* __restrict__ shat, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
+                      long long q_lo, long long q_stride, int row_tiles) {
+  __shared__ c64 xs[R][GEMV_KC];
+  const long long q = q_lo + blockIdx.x / row_tiles;
+  const int i = (blockIdx.x % row_tiles) * GEMV_THREADS + threadIdx.x;
+  const bool row_ok = i < n;
+  const size_t nn = static_cast<size_t>(n) * n;
+  const c64* a = shat + static_cast<size_t>(q) * nn + (row_ok ? i : 0);
+  c64 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = cmk(0.0, 0.0);
+  for (int k0 = 0; k0 < n; k0 += GEMV_KC) {
+    const int kc = min(GEMV_KC, n - k0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < R * GEMV_KC; t += GEMV_THREADS) {
+      const int r = t / GEMV_KC, k = t % GEMV_KC;
+      xs[r][k] = k < kc ? xh[r * q_stride * n + q * n + k0 + k] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    int k = 0;
+    for (; k + GEMV_U <= kc; k += GEMV_U) {
+      c64 v[GEMV_U];
+#pragma unroll
+      for (int u = 0; u < GEMV_U; ++u) v[u] = __ldcs(a + static_cast<size_t>(k0 + k + u) * n);
+#pragma unroll
+      for (int u = 0; u < GEMV_U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = cfma(v[u], xs[r][k + u], acc[r]);
+    }
+    for (; k < kc; ++k) {
+      const c64 v = __ldcs(a + static_cast<size_t>(k0 + k) * n);
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = cfma(v, xs[r][k], acc[r]);
+    }
+  }
+  if (!row_ok) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) yh[r * q_stride * n + q * n + i] = acc[r];
 }
 
 // y[r,t,i] = sum_{pairs of t, offset order} W[pair, r, i]  +  sum_m U0[i, m] L[t, r, m]
@@ -253,7 +309,7 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, long long out_rhs_stride) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(near_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -267,7 +323,33 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   dim3 grid(static_cast<unsigned>(ctas));
   near_gemm_dmma_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src, jobs,
-                                                                    K, n, N, nrhs);
+                                                                    K, n, N, nrhs, out_rhs_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mode_gemv(const c64* shat, const c64* xh, c64* yh, int n, long long q_lo, long long q_hi,
+                             long long q_stride, int nrhs, cudaStream_t stream) {
+  if (q_hi <= q_lo) return cudaSuccess;
+  const int row_tiles = (n + GEMV_THREADS - 1) / GEMV_THREADS;
+  const long long blocks = (q_hi - q_lo) * row_tiles;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const dim3 grid(static_cast<unsigned>(blocks));
+  switch (nrhs) {
+#define FPBEM_GEMV_CASE(R)                                                                                     \
+  case R:                                                                                                     \
+    near_mode_gemv_kernel<R><<<grid, GEMV_THREADS, 0, stream>>>(shat, xh, yh, n, q_lo, q_stride, row_tiles); \
+    break;
+    FPBEM_GEMV_CASE(1)
+    FPBEM_GEMV_CASE(2)
+    FPBEM_GEMV_CASE(3)
+    FPBEM_GEMV_CASE(4)
+    FPBEM_GEMV_CASE(5)
+    FPBEM_GEMV_CASE(6)
+    FPBEM_GEMV_CASE(7)
+    FPBEM_GEMV_CASE(8)
+#undef FPBEM_GEMV_CASE
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -129,11 +129,16 @@ class FmmOperators:
     data: an FmmData (host.Scene.assemble_fmm) or any object with the same
     fields (counts, n_dof, n_coef, near_offsets, near_blocks, far_offsets,
     far_blocks, u0, v0). The spectrum is built on the GPU from the far bank
-    unless `lambda_` (reference layout) is given.
+    unless `lambda_` (reference layout) is given. near_path: "auto" (cost
+    model), "direct" (one GEMM per stored offset, BlockToeplitzMatrix::matvec's
+    structure) or "lattice" (circulant embedding of the near blocks, one block
+    product per Fourier mode).
     """
 
+    NEAR_PATHS = {"auto": 0, "direct": 1, "lattice": 2}
+
     def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1, lambda_hat=None,
-                 near_blocks=None, hat_blocks=None, far_blocks=None, far_hat_blocks=None):
+                 near_blocks=None, hat_blocks=None, far_blocks=None, far_hat_blocks=None, near_path: str = "auto"):
         lib = _native.cuda()
         self.counts = tuple(int(c) for c in data.counts)
         self.n_dof = int(data.n_dof)
@@ -177,6 +182,7 @@ class FmmOperators:
         level = int(getattr(data, "mirrored_level", -1))
         d.mirrored_level = level
         d.max_rhs = max_rhs
+        d.near_path = self.NEAR_PATHS[near_path]
         if level >= 0:
             d.n_hat = int(len(data.hat_indices))
             d.hat_indices = ptr(data.hat_indices, np.int32)
@@ -215,6 +221,12 @@ class FmmOperators:
         b = C.c_size_t()
         _raise(_native.cuda().fpbem_cu_fmm_bytes(self._h, C.byref(b)))
         return int(b.value)
+
+    def near_path(self) -> tuple[str, tuple[int, int, int], int]:
+        """(path, lattice sizes, spectrum bytes) of the near field in use."""
+        p, sizes, nb = C.c_int(), (C.c_int * 3)(), C.c_size_t()
+        _raise(_native.cuda().fpbem_cu_fmm_near_path(self._h, C.byref(p), sizes, C.byref(nb)))
+        return {1: "direct", 2: "lattice"}[p.value], tuple(sizes), int(nb.value)
 
     def spectrum(self) -> tuple[tuple[int, int, int], np.ndarray]:
         sizes = (C.c_int * 3)()
