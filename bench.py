@@ -130,11 +130,22 @@ def fp64_peak():
     return float(d["dmma_tflops"]), "profiles/r01_fp64_peak.json (DMMA.8x8x4 microbenchmark, tools/fp64_peak.cu)"
 
 
-def near_gemm_traffic():
+def kernel_traffic(path):
+    """DRAM bytes per launch of the dominant kernel from one committed
+    `ncu --set full` capture (profiles/), or None."""
     try:
-        return json.loads(TRAFFIC_FILE.read_text())
+        return json.loads(path.read_text())
     except (OSError, ValueError):
         return None
+
+
+def hbm_peak():
+    """Measured HBM copy bandwidth (driver-written MEASURED_PEAKS.json), else the
+    B200 profiling guide's fallback."""
+    try:
+        return float(json.loads(PEAKS_FILE.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except (OSError, ValueError, KeyError):
+        return 6500.0, "B200_PROFILING.md fallback"
 
 
 class _WithNear:
@@ -317,7 +328,10 @@ def run_ours(args):
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     ms, e2e_s, gmres_s = (float(v) for v in vals.cpu())
 
-    # roofline of the dominant kernel (near-field DMMA GEMM): algorithmic flops per launch
+    path, lat_sizes, spec_bytes = op.near_path()
+    # roofline of the dominant kernel. Direct path: the near-field DMMA GEMM,
+    # algorithmic flops per launch; lattice path: the per-mode GEMV, HBM-bound,
+    # algorithmic bytes per launch = the block spectrum + x_hat read + y_hat written
     m = data.counts
     n_pairs = int(sum((m[0] - abs(int(o[0]))) * (m[1] - abs(int(o[1]))) * (m[2] - abs(int(o[2])))
                       for o in data.near_offsets))
@@ -327,9 +341,27 @@ def run_ours(args):
         n_pairs = hi - lo
     flops = 8.0 * data.n_dof ** 2 * float(n_pairs)
     gemm_ms = stages["near_gemm"] / max(1, stages["applies"])
-    achieved = flops / (gemm_ms * 1e-3) / 1e12
-    peak, peak_src = fp64_peak()
-    traffic = near_gemm_traffic()
+    if path == "lattice":
+        q_near = int(np.prod(lat_sizes))
+        lo, hi, far_pairs = op.partition()  # modes of this rank
+        mode_bytes = 16.0 * data.n_dof ** 2 * (hi - lo) + 2 * 16.0 * data.n_dof * q_near
+        mode_ms = stages["near_mode_product"] / max(1, stages["applies"])
+        peak, peak_src = hbm_peak()
+        traffic = kernel_traffic(ROOT / "profiles" / "near_mode_gemv_traffic.json")
+        roofline = {"kernel": "near_mode_gemv_kernel", "bound": "hbm", "achieved": mode_bytes / (mode_ms * 1e-3) / 1e9,
+                    "peak": peak, "unit": "GB/s", "peak_source": peak_src, "algorithmic_bytes": mode_bytes,
+                    "launch_ms": mode_ms, "near_stage_ms": gemm_ms,
+                    "near_stage_share_of_step": gemm_ms / (stages["total"] / max(1, stages["applies"]))}
+    else:
+        peak, peak_src = fp64_peak()
+        traffic = kernel_traffic(TRAFFIC_FILE)
+        roofline = {"kernel": "near_gemm_dmma_kernel", "bound": "tensor", "achieved": flops / (gemm_ms * 1e-3) / 1e12,
+                    "peak": peak, "unit": "TFLOP/s", "peak_source": peak_src, "flops_per_launch": flops,
+                    "launch_ms": gemm_ms,
+                    "algorithmic_bytes": 16.0 * data.n_near * data.n_dof ** 2 + 2 * 16.0 * data.N}
+    roofline["frac"] = roofline["achieved"] / peak
+    roofline["traffic"] = (traffic or {}).get("dram_bytes_per_launch")
+    roofline["traffic_source"] = (traffic or {}).get("source")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(_WithNear(data, near.cpu().numpy()), xh)
@@ -346,23 +378,20 @@ def run_ours(args):
             "config": {
                 "workload": desc, "n_dof_total": data.N, "n_dof_cell": data.n_dof, "lattice": list(data.counts),
                 "near_offsets": data.n_near, "far_offsets": data.n_far, "n_t": 4, "nrhs": 1,
-                "parallelism": (f"near-field pairs split over {world} GPUs (rank 0 {n_pairs} pairs, "
-                                f"{far_pairs:.0f} fewer for its far field) + NCCL all-reduce of y" if strong
+                "near_path": path, "near_lattice": list(lat_sizes),
+                "parallelism": (f"near-field {'modes' if path == 'lattice' else 'pairs'} split over {world} GPUs "
+                                f"(rank 0 {hi - lo if path == 'lattice' else n_pairs}, {far_pairs:.0f} fewer for its "
+                                "far field) + NCCL all-reduce of y" if strong
                                 else f"replicas x{world}" if world > 1 else "single GPU"),
-                "l2": f"inputs larger than L2: near-field operator {16 * data.n_near * data.n_dof ** 2 / 1e9:.2f} GB "
-                      "streamed from HBM every step",
+                "l2": (f"inputs larger than L2: near-field block spectrum {spec_bytes / 1e9:.2f} GB streamed from HBM "
+                       "every step" if path == "lattice" else
+                       f"inputs larger than L2: near-field operator {16 * data.n_near * data.n_dof ** 2 / 1e9:.2f} GB "
+                       "streamed from HBM every step"),
                 "assembly_s": round(t_asm, 3), "assembly_host_s": round(t_host_asm, 3),
                 "assembly_device_near_s": round(t_dev_asm, 3), "create_s": round(t_up, 3),
             },
             "stages_ms": {k: (v / max(1, stages["applies"]) if k != "applies" else v) for k, v in stages.items()},
-            "roofline": {
-                "kernel": "near_gemm_dmma_kernel", "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "peak_source": peak_src,
-                "flops_per_launch": flops, "launch_ms": gemm_ms,
-                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                "traffic_source": (traffic or {}).get("source"),
-                "algorithmic_bytes": 16.0 * data.n_near * data.n_dof ** 2 + 2 * 16.0 * data.N,
-            },
+            "roofline": roofline,
             "e2e": {"value": units * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": 16 * data.N, "d2h_bytes_per_step": 16 * data.N},
             "gmres": {"solve_s": gmres_s, "iterations": rep.iterations, "converged": rep.converged,

@@ -208,7 +208,8 @@ int fpbem_cu_set_stream(fpbem_cu_op* op, void* stream);
 
 /* Per-stage CUDA-event timing of applies (0 = off). When on, each apply
  * accumulates milliseconds per stage; fpbem_cu_stage_times copies
- * {near_gemm, near_reduce_l2p, p2m, m2l, total, applies} into ms_out[6]
+ * {near field, near_reduce_l2p (or L2P), p2m, m2l, total, applies,
+ * lattice-path mode product} into ms_out[7]
  * and resets the counters. */
 int fpbem_cu_enable_stage_timing(fpbem_cu_op* op, int enable);
 int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out);

@@ -151,6 +151,7 @@ void build_mode_jobs(fpbem_cu_op* op, int nrhs) {
 }
 
 void twiddles(fpbem_cu_op* op, int L, c64** out);
+void ev_record(fpbem_cu_op* op, int i, cudaStream_t st);
 
 // Block spectrum of the near field (the CirculantSpectrum construction,
 // src/structured.cpp:63-108, applied to the Toeplitz blocks): S_o at slot
@@ -225,6 +226,7 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
   which ^= 1;
   if (op->mode_lo > 0 || op->mode_hi < op->qn)
     check(cudaMemsetAsync(yh, 0, static_cast<size_t>(r * op->qn * n) * sizeof(c64), s), "near spectrum clear");
+  ev_record(op, 7, s);
   if (nrhs <= kModeGemvMaxRhs) {
     check(launch_mode_gemv(op->shat, cur, yh, op->n, op->mode_lo, op->mode_hi, op->qn, nrhs, s), "near mode gemv");
   } else {
@@ -233,6 +235,7 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
                             op->n, op->qn * n, nrhs, s, op->qn * n),
           "near mode gemm");
   }
+  ev_record(op, 8, s);
   op->launches++;
   cur = yh;
   int left = (Lx > 1) + (Ly > 1) + (Lz > 1);
@@ -556,6 +559,10 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
     op->stage_ms[3] += ms;
     cudaEventElapsedTime(&ms, op->ev[0], op->ev[6]);
     op->stage_ms[4] += ms;
+    if (op->near_fft) {
+      cudaEventElapsedTime(&ms, op->ev[7], op->ev[8]);
+      op->stage_ms[5] += ms;
+    }
     op->applies++;
   }
 }
@@ -950,6 +957,7 @@ int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out) {
   if (!op || !ms_out) return FPBEM_CU_EINVAL;
   for (int i = 0; i < 5; ++i) ms_out[i] = op->stage_ms[i];
   ms_out[5] = static_cast<double>(op->applies);
+  ms_out[6] = op->stage_ms[5];
   for (double& v : op->stage_ms) v = 0.0;
   op->applies = 0;
   return FPBEM_CU_OK;

@@ -178,8 +178,8 @@ struct fpbem_cu_op {
 
   // timing
   bool timing = false;
-  cudaEvent_t ev[8] = {};
-  double stage_ms[5] = {0, 0, 0, 0, 0};
+  cudaEvent_t ev[10] = {};
+  double stage_ms[6] = {0, 0, 0, 0, 0, 0};  // + [5]: lattice-path mode product (events 7-8)
   long long applies = 0;
   long long launches = 0;
 

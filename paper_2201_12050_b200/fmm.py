@@ -271,11 +271,12 @@ class FmmOperators:
         _raise(_native.cuda().fpbem_cu_enable_stage_timing(self._h, int(on)))
 
     def stage_times(self) -> dict:
-        ms = (C.c_double * 6)()
+        ms = (C.c_double * 7)()
         _raise(_native.cuda().fpbem_cu_stage_times(self._h, ms))
-        keys = ("near_gemm", "near_reduce_l2p", "p2m", "m2l", "total")
+        keys = ("near_gemm", "near_reduce_l2p", "p2m", "m2l", "total")  # near_gemm: the whole near-field stage
         out = {k: ms[i] for i, k in enumerate(keys)}
         out["applies"] = int(ms[5])
+        out["near_mode_product"] = ms[6]
         return out
 
     def _nrhs(self, p) -> int:

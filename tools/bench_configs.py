@@ -75,6 +75,9 @@ def run_config(cid, args, out):
     t = time.perf_counter()
     op = FmmOperators(data, max_rhs=nrhs)
     rec["upload_s"] = time.perf_counter() - t
+    path, lat, spec_bytes = op.near_path()
+    rec["near_path"] = path
+    rec["near_lattice"] = list(lat)
     sizes, _ = op.spectrum()
     rec["fft_sizes"] = list(sizes)
     q = int(np.prod(sizes))
@@ -95,8 +98,13 @@ def run_config(cid, args, out):
     rec["matvec_ms"] = ms
     rec["matvec_dof_per_s"] = sc.N / (ms * 1e-3)
     rec["stages_ms"] = st
-    rec["near_gemm_tflops"] = flops / (st["near_gemm"] * 1e-3) / 1e12
+    rec["near_gemm_tflops"] = flops / (st["near_gemm"] * 1e-3) / 1e12  # algorithmic (direct-path) flops
     rec["near_gemm_frac_of_fp64_peak"] = flops / (st["near_gemm"] * 1e-3) / FP64
+    if path == "lattice":  # per-mode product streams the block spectrum
+        qn = int(np.prod(lat))
+        mb = spec_bytes + 2 * 16.0 * data.n_dof * qn
+        rec["near_mode_product_gb_per_s"] = mb / (st["near_mode_product"] * 1e-3) / 1e9
+        rec["near_mode_product_frac_of_hbm"] = mb / (st["near_mode_product"] * 1e-3) / HBM
     lam_bytes = 16.0 * q * 625
     rec["m2l_lambda_gb_per_s"] = lam_bytes / (st["m2l"] * 1e-3) / 1e9
     rec["m2l_frac_of_hbm_lambda_only"] = lam_bytes / (st["m2l"] * 1e-3) / HBM
