@@ -56,6 +56,7 @@ class FmmDesc(C.Structure):
         ("blocks_on_device", C.c_int),
         ("far_on_device", C.c_int),
         ("near_path", C.c_int),
+        ("cell_inversion", C.c_void_p),
     ]
 
 
@@ -110,7 +111,7 @@ def cuda() -> C.CDLL:
                                             C.c_int, C.c_int, C.c_int, c_int_p, c_int_p, c_double_p, C.c_int,
                                             c_int_p]),
             "fpbem_cu_fmm_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
-            "fpbem_cu_fmm_near_path": (C.c_int, [vp, c_int_p, c_int_p, C.POINTER(C.c_size_t)]),
+            "fpbem_cu_fmm_near_path": (C.c_int, [vp, c_int_p, c_int_p, C.POINTER(C.c_size_t), c_int_p, c_double_p]),
             "fpbem_cu_spectrum": (C.c_int, [vp, c_int_p, vp]),
             "fpbem_cu_set_stream": (C.c_int, [vp, vp]),
             "fpbem_cu_enable_stage_timing": (C.c_int, [vp, C.c_int]),

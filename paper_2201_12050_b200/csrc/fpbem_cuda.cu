@@ -78,8 +78,8 @@ void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
   op->far_pairs = far_pairs;
   op->rank = rank;
   op->nranks = nranks;
-  if (op->near_fft) {  // units are the modes of the near-field lattice (each one n x n block product)
-    pair_range(op->qn, nranks, rank, far_pairs, op->mode_lo, op->mode_hi);
+  if (op->near_fft) {  // units are the stored blocks of the near-field lattice (one n x n block stream each)
+    pair_range(static_cast<long long>(op->items_h.size()), nranks, rank, far_pairs, op->mode_lo, op->mode_hi);
     op->mjobs_nrhs = -1;
     return;
   }
@@ -91,10 +91,10 @@ void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
 // Column tiles of one offset (or of the P2M columns): as many 64-wide tiles as
 // fit, then the remainder as one 64- (49..63), 32+16- (33..48), 32- (17..32)
 // or 16-wide (1..16) tile. job.z = column count | width class << 8.
-void tile_columns(std::vector<int4>& jobs, int s, int cols, int pair_base, bool narrow) {
+void tile_columns(std::vector<int4>& jobs, int s, int cols, int pair_base, bool narrow, int flags = 0) {
   int c0 = 0;
   auto push = [&](int w, int cls) {
-    jobs.push_back(make_int4(s, c0, w | (cls << 8), pair_base));
+    jobs.push_back(make_int4(s, c0, w | (cls << 8) | flags, pair_base));
     c0 += w;
   };
   while (cols - c0 >= 64) push(64, 0);
@@ -138,8 +138,11 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
 void build_mode_jobs(fpbem_cu_op* op, int nrhs) {
   if (op->mjobs_nrhs == nrhs) return;
   std::vector<int4> jobs;
-  for (long long q = op->mode_lo; q < op->mode_hi; ++q)
-    tile_columns(jobs, static_cast<int>(q), nrhs, static_cast<int>(q), true);
+  for (long long t = op->mode_lo; t < op->mode_hi; ++t) {
+    const int2 it = op->items_h[t];
+    tile_columns(jobs, static_cast<int>(t), nrhs, it.x, true);
+    if (it.y >= 0) tile_columns(jobs, static_cast<int>(t), nrhs, it.y, true, 1 << 12);  // mirror: through P
+  }
   if (static_cast<int>(jobs.size()) > op->mjobs_cap) {
     if (op->mjobs) cudaFree(op->mjobs);
     op->mjobs = dalloc<int4>(jobs.size(), "mode jobs");
@@ -193,12 +196,83 @@ void build_near_spectrum(fpbem_cu_op* op, int n_toeplitz) {
           "near spectrum dft z");
     std::swap(cur, nxt);
   }
+  // work items: (q, -q) pairs sharing Shat_q when the inversion was verified, else every mode
+  op->items_h.clear();
+  for (long long q = 0; q < op->qn; ++q) {
+    if (!op->near_pair) {
+      op->items_h.push_back(make_int2(static_cast<int>(q), -1));
+      continue;
+    }
+    const long long qx = q % Lx, qy = (q / Lx) % Ly, qz = q / (Lx * Ly);
+    const long long qm = (((Lz - qz) % Lz) * Ly + (Ly - qy) % Ly) * Lx + (Lx - qx) % Lx;
+    if (q < qm) op->items_h.push_back(make_int2(static_cast<int>(q), static_cast<int>(qm)));
+    if (q == qm) op->items_h.push_back(make_int2(static_cast<int>(q), -1));
+  }
+  const size_t n_items = op->items_h.size();
+  op->items = dalloc<int2>(n_items, "near items");
+  h2d(op->items, op->items_h.data(), n_items * sizeof(int2), op->stream, "near items");
+  if (op->near_pair) {  // keep only the blocks of the items' first modes
+    c64* compact = dalloc<c64>(n_items * nn, "near spectrum (pairs)");
+    DevPtr keep_c(compact, &cudaFree);
+    for (size_t t = 0; t < n_items; ++t)
+      check(cudaMemcpyAsync(compact + t * nn, cur + static_cast<size_t>(op->items_h[t].x) * nn, nn * sizeof(c64),
+                            cudaMemcpyDeviceToDevice, op->stream),
+            "near spectrum compaction");
+    check(cudaStreamSynchronize(op->stream), "near spectrum compaction");
+    op->shat = static_cast<c64*>(keep_c.release());
+    return;  // a and b freed here
+  }
   check(cudaStreamSynchronize(op->stream), "near spectrum build");
   if (cur == a)
     keep_a.release();
   else
     keep_b.release();
   op->shat = cur;
+}
+
+// Cell-inversion pairing: with P from the caller, every near
+// offset's mirror -o stored, and S_-o[P i, P j] == S_o[i, j] on the device to
+// 1e-12 of max |S|, Shat_-q = P Shat_q P and the lattice path stores / streams
+// one block per mode pair. Sets near_pair and near_sym_dev.
+void check_inversion(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
+  op->near_pair = false;
+  op->near_sym_dev = -1.0;
+  if (!d->cell_inversion || d->n_near == 0) return;
+  std::vector<char> seen(op->n, 0);
+  for (int i = 0; i < op->n; ++i) {
+    const int p = d->cell_inversion[i];
+    if (p < 0 || p >= op->n || seen[p]) fail(FPBEM_CU_EINVAL, "create: cell_inversion is not a permutation");
+    seen[p] = 1;
+  }
+  std::vector<int> mirror(d->n_near, -1);
+  for (int s = 0; s < d->n_near; ++s)
+    for (int t = 0; t < d->n_near && mirror[s] < 0; ++t)
+      if (op->near_offsets[3 * t] == -op->near_offsets[3 * s] &&
+          op->near_offsets[3 * t + 1] == -op->near_offsets[3 * s + 1] &&
+          op->near_offsets[3 * t + 2] == -op->near_offsets[3 * s + 2])
+        mirror[s] = t;
+  for (int s = 0; s < d->n_near; ++s)
+    if (mirror[s] < 0) return;  // offset set not symmetric
+  using DevPtr = std::unique_ptr<void, decltype(&cudaFree)>;
+  int* dm = dalloc<int>(mirror.size(), "mirror slots");
+  DevPtr keep_m(dm, &cudaFree);
+  h2d(dm, mirror.data(), mirror.size() * sizeof(int), op->stream, "mirror slots");
+  if (!op->perm) {
+    op->perm = dalloc<int>(op->n, "cell inversion");
+    h2d(op->perm, d->cell_inversion, op->n * sizeof(int), op->stream, "cell inversion");
+  }
+  unsigned long long* dv = dalloc<unsigned long long>(2, "symmetry check");
+  DevPtr keep_dv(dv, &cudaFree);
+  check(cudaMemsetAsync(dv, 0, 2 * sizeof(unsigned long long), op->stream), "symmetry check");
+  check(launch_near_symmetry(op->S, op->n, d->n_near, dm, op->perm, dv, op->stream), "symmetry check");
+  unsigned long long hv[2];
+  check(cudaMemcpyAsync(hv, dv, sizeof(hv), cudaMemcpyDeviceToHost, op->stream), "symmetry check");
+  check(cudaStreamSynchronize(op->stream), "symmetry check");
+  double dev, amax;
+  std::memcpy(&dev, &hv[0], sizeof(double));
+  std::memcpy(&amax, &hv[1], sizeof(double));
+  op->near_sym_dev = amax > 0.0 ? dev / amax : 0.0;
+  op->near_pair = amax > 0.0 && dev <= 1e-12 * amax;
 }
 
 // Lattice-path near field: y = (1/qn) IDFT(Shat . DFT(x)) truncated to the M
@@ -224,15 +298,17 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
   if (Lz > 1) fwd(2, r, Mz, Lz, static_cast<long long>(Ly) * Lx * n);
   c64* yh = bufs[which];
   which ^= 1;
-  if (op->mode_lo > 0 || op->mode_hi < op->qn)
+  if (op->mode_lo > 0 || op->mode_hi < static_cast<long long>(op->items_h.size()))
     check(cudaMemsetAsync(yh, 0, static_cast<size_t>(r * op->qn * n) * sizeof(c64), s), "near spectrum clear");
   ev_record(op, 7, s);
-  if (nrhs <= kModeGemvMaxRhs) {
-    check(launch_mode_gemv(op->shat, cur, yh, op->n, op->mode_lo, op->mode_hi, op->qn, nrhs, s), "near mode gemv");
+  if (nrhs <= (op->near_pair ? kModeGemvMaxRhsPaired : kModeGemvMaxRhs)) {
+    check(launch_mode_gemv(op->shat, op->items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi, op->qn, nrhs,
+                           op->near_pair, s),
+          "near mode gemv");
   } else {
     build_mode_jobs(op, nrhs);
     check(launch_block_gemm(op->shat, n * n, op->n, op->n, cur, yh, op->n, nullptr, op->mjobs, op->n_mjobs, op->n,
-                            op->n, op->qn * n, nrhs, s, op->qn * n),
+                            op->n, op->qn * n, nrhs, s, op->qn * n, op->perm),
           "near mode gemm");
   }
   ev_record(op, 8, s);
@@ -495,7 +571,7 @@ double calibrate_far_pairs(fpbem_cu_op* op) {
     }
   }
   set_partition(op, rank, nranks, far_pairs);
-  const double units = op->near_fft ? static_cast<double>(op->qn) : static_cast<double>(op->n_pairs);
+  const double units = op->near_fft ? static_cast<double>(op->items_h.size()) : static_cast<double>(op->n_pairs);
   return best_near > 0.0f ? static_cast<double>(best_far) / best_near * units : 0.0;
 }
 
@@ -602,7 +678,9 @@ void choose_near_path(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
     qn *= Ln[k];
   }
   const double nn = static_cast<double>(op->n) * op->n;
-  const double spec_bytes = 16.0 * nn * static_cast<double>(qn);
+  // stored blocks: one per mode, or one per mode pair (q, -q) with a verified inversion
+  const double blocks = op->near_pair ? 0.5 * static_cast<double>(qn) : static_cast<double>(qn);
+  const double spec_bytes = 16.0 * nn * blocks;
   bool use = path == FPBEM_CU_NEAR_LATTICE;
   if (path == FPBEM_CU_NEAR_AUTO && possible) {
     const double r = op->max_rhs;
@@ -611,9 +689,10 @@ void choose_near_path(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
     for (int k = 0; k < 3; ++k) axes += Ln[k] > 1;
     const double t_pass = axes * 2.0 * 32.0 * r * op->n * static_cast<double>(qn + op->n_cells) / 4e12;
     const double t_lat = std::max(spec_bytes / 6e12, 8.0 * nn * static_cast<double>(qn) * r / 30e12) + t_pass;
+    // (build transient: two full spectra)
     size_t free_b = 0, total_b = 0;
     check(cudaMemGetInfo(&free_b, &total_b), "mem info");
-    use = t_lat < 0.8 * t_direct && 2.0 * spec_bytes < static_cast<double>(free_b) / 1.5;
+    use = t_lat < 0.8 * t_direct && 2.5 * 16.0 * nn * qn < static_cast<double>(free_b) / 1.5;
   }
   if (!use) return;
   op->near_fft = true;
@@ -800,6 +879,7 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
                      &op->lambda_hat);
     }
 
+    if (d->n_near > 0 && op->n_hat == 0) check_inversion(op, d);
     choose_near_path(op, d);
     if (op->near_fft) {
       build_near_spectrum(op, d->n_near);
@@ -810,7 +890,9 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
       check(cudaMemsetAsync(op->zero_ptr, 0, (static_cast<size_t>(op->n_cells) + 1) * sizeof(int), op->stream),
             "zero csr");
       op->mode_lo = 0;
-      op->mode_hi = op->qn;
+      op->mode_hi = static_cast<long long>(op->items_h.size());
+    } else {
+      op->near_pair = false;
     }
 
     // apply buffers
@@ -847,7 +929,8 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
                   static_cast<void*>(op->rs.partial_c), static_cast<void*>(op->rs.counter),
                   static_cast<void*>(op->shat), static_cast<void*>(op->twn[0]), static_cast<void*>(op->twn[1]),
                   static_cast<void*>(op->twn[2]), static_cast<void*>(op->nfa), static_cast<void*>(op->nfb),
-                  static_cast<void*>(op->zero_ptr), static_cast<void*>(op->mjobs)})
+                  static_cast<void*>(op->zero_ptr), static_cast<void*>(op->mjobs), static_cast<void*>(op->perm),
+                  static_cast<void*>(op->items)})
     if (p) cudaFree(p);
   if (op->pinned) cudaFreeHost(op->pinned);
   for (auto& e : op->ev)
@@ -905,14 +988,17 @@ int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes) {
   return FPBEM_CU_OK;
 }
 
-int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes) {
-  if (!op || !path || !sizes || !spectrum_bytes) {
+int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes, int* paired,
+                           double* symmetry_dev) {
+  if (!op || !path || !sizes || !spectrum_bytes || !paired || !symmetry_dev) {
     g_err = "near_path: null argument";
     return FPBEM_CU_EINVAL;
   }
   *path = op->near_fft ? FPBEM_CU_NEAR_LATTICE : FPBEM_CU_NEAR_DIRECT;
   for (int k = 0; k < 3; ++k) sizes[k] = op->near_fft ? op->Ln[k] : 1;
-  *spectrum_bytes = op->near_fft ? static_cast<size_t>(op->qn) * op->n * op->n * sizeof(c64) : 0;
+  *spectrum_bytes = op->near_fft ? op->items_h.size() * op->n * op->n * sizeof(c64) : 0;
+  *paired = op->near_fft && op->near_pair;
+  *symmetry_dev = op->near_sym_dev;
   return FPBEM_CU_OK;
 }
 

@@ -125,9 +125,17 @@ struct fpbem_cu_op {
   c64* nfa = nullptr;   // spectra of x / y, [rhs][q][n], sized for max_rhs
   c64* nfb = nullptr;
   int* zero_ptr = nullptr;  // n_cells + 1 zeros: the L2P-only reduction
-  int4* mjobs = nullptr;    // DMMA jobs over this rank's modes (nrhs > kModeGemvMaxRhs)
+  int4* mjobs = nullptr;    // DMMA jobs over this rank's items (many right-hand sides)
   int mjobs_nrhs = -1, n_mjobs = 0, mjobs_cap = 0;
-  long long mode_lo = 0, mode_hi = 0;  // this rank's modes
+  // stored blocks = work items (q, qm): with a verified cell inversion P
+  // (S_-o = P S_o P) one block serves mode q and, through P,
+  // its mirror qm = -q; otherwise every mode is an item (qm = -1)
+  bool near_pair = false;
+  double near_sym_dev = -1.0;  // max |S_-o[P i, P j] - S_o[i, j]| / max |S| (-1: not checked)
+  int* perm = nullptr;
+  int2* items = nullptr;
+  std::vector<int2> items_h;
+  long long mode_lo = 0, mode_hi = 0;  // this rank's items
 
   // expansions and spectrum
   c64* u0 = nullptr;

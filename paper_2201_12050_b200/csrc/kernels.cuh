@@ -10,13 +10,20 @@ namespace fpbem_cu {
 // columns are (pair, rhs) with rhs fastest, or (cell, rhs) when pair_src is null.
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
-                              cudaStream_t stream, long long out_rhs_stride = 0);
-// out_rhs_stride > 0: column (unit, rhs) lands at out[rhs * out_rhs_stride + unit * ldo] (rhs-major)
-// near field as a lattice convolution: yh[r][q] = shat_q xh[r][q] for modes q in [q_lo, q_hi),
-// nrhs <= kModeGemvMaxRhs right-hand sides at stride q_stride * n
+                              cudaStream_t stream, long long out_rhs_stride = 0, const int* perm = nullptr);
+// out_rhs_stride > 0: column (unit, rhs) lands at out[rhs * out_rhs_stride + unit * ldo] (rhs-major);
+// jobs with bit 12 of .z set gather B rows and scatter output rows through perm
+// near field as a lattice convolution: for items t in [t_lo, t_hi) = (q, qm),
+// yh[r][q] = shat_t xh[r][q] and, paired, yh[r][qm] = P shat_t P xh[r][qm];
+// nrhs <= kModeGemvMaxRhs (kModeGemvMaxRhsPaired) at stride q_stride * n
 constexpr int kModeGemvMaxRhs = 8;
-cudaError_t launch_mode_gemv(const c64* shat, const c64* xh, c64* yh, int n, long long q_lo, long long q_hi,
-                             long long q_stride, int nrhs, cudaStream_t stream);
+constexpr int kModeGemvMaxRhsPaired = 4;
+cudaError_t launch_mode_gemv(const c64* shat, const int2* items, const int* perm, const c64* xh, c64* yh, int n,
+                             long long t_lo, long long t_hi, long long q_stride, int nrhs, bool paired,
+                             cudaStream_t stream);
+// cell-inversion check: out2[0] = max |S_mirror[s][P i, P j] - S_s[i, j]|, out2[1] = max |S| (double bits)
+cudaError_t launch_near_symmetry(const c64* S, int n, int n_blk, const int* mirror, const int* perm,
+                                 unsigned long long* out2, cudaStream_t stream);
 cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* tgt_pairs, const c64* u0,
                                    const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
                                    int nrhs, bool accumulate, cudaStream_t stream);

@@ -44,7 +44,8 @@ constexpr size_t kSmemB = sizeof(c64) * STAGES * BN * BP;
 // where every warp loaded all 64 rows: shared-memory bandwidth was the limiter).
 template <int MI, int NI, typename Loader>
 __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& load_stage, int nk, int warp, int lane,
-                                          int ncols, int m0, int M, const long long* col_out, c64* __restrict__ out) {
+                                          int ncols, int m0, int M, const long long* col_out, c64* __restrict__ out,
+                                          const int* __restrict__ prow) {
   constexpr int G = 8 / MI;  // row groups
   const int wm = warp % G, wn = warp / G;
   const int fr = lane >> 2, fk = lane & 3;
@@ -113,7 +114,7 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
       for (int j = 0; j < 2; ++j) {
         const int c = wn * 8 * NI + ni * 8 + 2 * fk + j;
         const long long o = col_out[c];
-        if (o >= 0) out[o + gm] = cmk(t1[mi][ni][j] - t2[mi][ni][j], t3[mi][ni][j] - t1[mi][ni][j] - t2[mi][ni][j]);
+        if (o >= 0) out[o + (prow ? __ldg(prow + gm) : gm)] = cmk(t1[mi][ni][j] - t2[mi][ni][j], t3[mi][ni][j] - t1[mi][ni][j] - t2[mi][ni][j]);
       }
   }
 }
@@ -130,7 +131,7 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
 __global__ void __launch_bounds__(THREADS, 2)
 near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, int M, const c64* __restrict__ x,
                       c64* __restrict__ out, int ldo, const int* __restrict__ pair_src, const int4* __restrict__ jobs,
-                      int K, int n, long long N, int nrhs, long long out_rhs_stride) {
+                      int K, int n, long long N, int nrhs, long long out_rhs_stride, const int* __restrict__ perm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   c64* As = reinterpret_cast<c64*>(smem_raw);
   c64* Bs = reinterpret_cast<c64*>(smem_raw + kSmemA);
@@ -142,7 +143,10 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   const int m_tiles = (M + BM - 1) / BM;
   const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
   const int4 job = jobs[blockIdx.x / m_tiles];  // (block slot, first column, count | class << 8, pair base)
-  const int s = job.x, col0 = job.y, ncols = job.z & 0xff, cls = job.z >> 8, pair_base = job.w;
+  const int s = job.x, col0 = job.y, ncols = job.z & 0xff, cls = (job.z >> 8) & 0xf, pair_base = job.w;
+  // mirrored-mode tile of the lattice near field: rows of B gathered and rows
+  // of the output scattered through the cell inversion P
+  const int* pk = (job.z >> 12) & 1 ? perm : nullptr;
 
   if (tid < BN) {
     if (tid < ncols) {
@@ -186,7 +190,7 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
     for (int i = 0; i < (BN * BK) / THREADS; ++i) {
       const long long src_off = col_src[b_c + i * (THREADS / BK)];
       const bool ok = src_off >= 0 && (k0 + b_k) < K;
-      const c64* src = ok ? x + src_off + k0 + b_k : x;
+      const c64* src = ok ? x + src_off + (pk ? __ldg(pk + k0 + b_k) : k0 + b_k) : x;
       const unsigned dst = smem_b + sizeof(c64) * (stage * BN * BP + i * (THREADS / BK) * BP);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
     }
@@ -196,9 +200,9 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   // 1 -> 32 columns (16 x 16), 2 -> 16 columns (8 x 16): narrow tiles keep
   // all 8 warps busy instead of idling most of them
   switch (cls) {
-    case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-    case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
-    default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out); break;
+    case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, pk); break;
+    case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, pk); break;
+    default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, pk); break;
   }
 }
 
@@ -208,32 +212,47 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
 // embedding CirculantSpectrum uses for K, src/structured.cpp:63-108, applied to
 // the Toeplitz blocks of BlockToeplitzMatrix, src/assembly.cpp:62-84). For a few
 // right-hand sides this is a streaming complex GEMV over all modes: one thread
-// per row, the k loop in fixed ascending order (deterministic), Shat read once
-// with 8 independent 16-byte loads in flight per thread, the RHS chunk staged in
-// shared memory. HBM-bound: 16 n^2 bytes per mode.
+// per row, the k loop in fixed ascending order (deterministic), the block read
+// once with 8 independent 16-byte loads in flight per thread, the RHS chunk
+// staged in shared memory. HBM-bound: 16 n^2 bytes per stored block.
+// Work item t = (q, qm): block t of the stored spectrum is Shat_q; with a cell
+// inversion P (S_-o = P S_o P, so Shat_-q = P Shat_q P) the
+// same stream also gives yh[qm = -q] = P Shat_q P xh[qm]: the second set of
+// accumulators reads xh[qm] gathered through P and its rows land at P[i].
 constexpr int GEMV_THREADS = 128;
 constexpr int GEMV_KC = 256;  // k chunk of xh staged in shared memory
 constexpr int GEMV_U = 8;     // independent Shat loads per thread
 
-template <int R>
+template <int R, bool kPair>
 __global__ void __launch_bounds__(GEMV_THREADS)
-near_mode_gemv_kernel(const c64* __restrict__ shat, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
-                      long long q_lo, long long q_stride, int row_tiles) {
-  __shared__ c64 xs[R][GEMV_KC];
-  const long long q = q_lo + blockIdx.x / row_tiles;
+near_mode_gemv_kernel(const c64* __restrict__ shat, const int2* __restrict__ items, const int* __restrict__ perm,
+                      const c64* __restrict__ xh, c64* __restrict__ yh, int n, long long t_lo, long long q_stride,
+                      int row_tiles) {
+  constexpr int S = kPair ? 2 : 1;
+  __shared__ c64 xs[S * R][GEMV_KC];
+  const long long t = t_lo + blockIdx.x / row_tiles;
+  const int2 it = items[t];
+  const long long q = it.x, qm = kPair ? it.y : -1;
   const int i = (blockIdx.x % row_tiles) * GEMV_THREADS + threadIdx.x;
   const bool row_ok = i < n;
   const size_t nn = static_cast<size_t>(n) * n;
-  const c64* a = shat + static_cast<size_t>(q) * nn + (row_ok ? i : 0);
-  c64 acc[R];
+  const c64* a = shat + static_cast<size_t>(t) * nn + (row_ok ? i : 0);
+  c64 acc[S * R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = cmk(0.0, 0.0);
+  for (int r = 0; r < S * R; ++r) acc[r] = cmk(0.0, 0.0);
   for (int k0 = 0; k0 < n; k0 += GEMV_KC) {
     const int kc = min(GEMV_KC, n - k0);
     __syncthreads();
-    for (int t = threadIdx.x; t < R * GEMV_KC; t += GEMV_THREADS) {
-      const int r = t / GEMV_KC, k = t % GEMV_KC;
-      xs[r][k] = k < kc ? xh[r * q_stride * n + q * n + k0 + k] : cmk(0.0, 0.0);
+    for (int e = threadIdx.x; e < S * R * GEMV_KC; e += GEMV_THREADS) {
+      const int r = e / GEMV_KC, k = e % GEMV_KC;
+      c64 v = cmk(0.0, 0.0);
+      if (k < kc) {
+        if (r < R)
+          v = xh[r * q_stride * n + q * n + k0 + k];
+        else if (qm >= 0)
+          v = xh[(r - R) * q_stride * n + qm * n + __ldg(perm + k0 + k)];
+      }
+      xs[r][k] = v;
     }
     __syncthreads();
     int k = 0;
@@ -244,17 +263,22 @@ near_mode_gemv_kernel(const c64* __restrict__ shat, const c64* __restrict__ xh, 
 #pragma unroll
       for (int u = 0; u < GEMV_U; ++u)
 #pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = cfma(v[u], xs[r][k + u], acc[r]);
+        for (int r = 0; r < S * R; ++r) acc[r] = cfma(v[u], xs[r][k + u], acc[r]);
     }
     for (; k < kc; ++k) {
       const c64 v = __ldcs(a + static_cast<size_t>(k0 + k) * n);
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = cfma(v, xs[r][k], acc[r]);
+      for (int r = 0; r < S * R; ++r) acc[r] = cfma(v, xs[r][k], acc[r]);
     }
   }
   if (!row_ok) return;
 #pragma unroll
   for (int r = 0; r < R; ++r) yh[r * q_stride * n + q * n + i] = acc[r];
+  if (kPair && qm >= 0) {
+    const int pi = __ldg(perm + i);
+#pragma unroll
+    for (int r = 0; r < R; ++r) yh[r * q_stride * n + qm * n + pi] = acc[R + r];
+  }
 }
 
 // y[r,t,i] = sum_{pairs of t, offset order} W[pair, r, i]  +  sum_m U0[i, m] L[t, r, m]
@@ -309,7 +333,7 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
-                              cudaStream_t stream, long long out_rhs_stride) {
+                              cudaStream_t stream, long long out_rhs_stride, const int* perm) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(near_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -323,33 +347,77 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   dim3 grid(static_cast<unsigned>(ctas));
   near_gemm_dmma_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src, jobs,
-                                                                    K, n, N, nrhs, out_rhs_stride);
+                                                                    K, n, N, nrhs, out_rhs_stride, perm);
   return cudaGetLastError();
 }
 
-cudaError_t launch_mode_gemv(const c64* shat, const c64* xh, c64* yh, int n, long long q_lo, long long q_hi,
-                             long long q_stride, int nrhs, cudaStream_t stream) {
-  if (q_hi <= q_lo) return cudaSuccess;
+cudaError_t launch_mode_gemv(const c64* shat, const int2* items, const int* perm, const c64* xh, c64* yh, int n,
+                             long long t_lo, long long t_hi, long long q_stride, int nrhs, bool paired,
+                             cudaStream_t stream) {
+  if (t_hi <= t_lo) return cudaSuccess;
   const int row_tiles = (n + GEMV_THREADS - 1) / GEMV_THREADS;
-  const long long blocks = (q_hi - q_lo) * row_tiles;
+  const long long blocks = (t_hi - t_lo) * row_tiles;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
   const dim3 grid(static_cast<unsigned>(blocks));
-  switch (nrhs) {
-#define FPBEM_GEMV_CASE(R)                                                                                     \
-  case R:                                                                                                     \
-    near_mode_gemv_kernel<R><<<grid, GEMV_THREADS, 0, stream>>>(shat, xh, yh, n, q_lo, q_stride, row_tiles); \
+  const int key = paired ? -nrhs : nrhs;
+  switch (key) {
+#define FPBEM_GEMV_CASE(R, P)                                                                                    \
+  case (P ? -R : R):                                                                                            \
+    near_mode_gemv_kernel<R, P><<<grid, GEMV_THREADS, 0, stream>>>(shat, items, perm, xh, yh, n, t_lo, q_stride, \
+                                                                   row_tiles);                                  \
     break;
-    FPBEM_GEMV_CASE(1)
-    FPBEM_GEMV_CASE(2)
-    FPBEM_GEMV_CASE(3)
-    FPBEM_GEMV_CASE(4)
-    FPBEM_GEMV_CASE(5)
-    FPBEM_GEMV_CASE(6)
-    FPBEM_GEMV_CASE(7)
-    FPBEM_GEMV_CASE(8)
+    FPBEM_GEMV_CASE(1, false)
+    FPBEM_GEMV_CASE(2, false)
+    FPBEM_GEMV_CASE(3, false)
+    FPBEM_GEMV_CASE(4, false)
+    FPBEM_GEMV_CASE(5, false)
+    FPBEM_GEMV_CASE(6, false)
+    FPBEM_GEMV_CASE(7, false)
+    FPBEM_GEMV_CASE(8, false)
+    FPBEM_GEMV_CASE(1, true)
+    FPBEM_GEMV_CASE(2, true)
+    FPBEM_GEMV_CASE(3, true)
+    FPBEM_GEMV_CASE(4, true)
 #undef FPBEM_GEMV_CASE
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// max |S_s'[P i + n P j] - S_s[i + n j]| over blocks s with mirror slot s' (the
+// block of -o) and max |S|, as double bits (non-negative doubles order like
+// their bit patterns): the device check of the cell-inversion symmetry
+__global__ void near_symmetry_kernel(const c64* __restrict__ S, int n, int n_blk, const int* __restrict__ mirror,
+                                     const int* __restrict__ perm, unsigned long long* out2) {
+  const long long nn = static_cast<long long>(n) * n, total = nn * n_blk;
+  double dev = 0.0, amax = 0.0;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(g / nn);
+    const long long e = g % nn;
+    const int i = static_cast<int>(e % n), j = static_cast<int>(e / n);
+    const c64 v = S[g];
+    const c64 w = S[mirror[s] * nn + __ldg(perm + i) + static_cast<long long>(n) * __ldg(perm + j)];
+    dev = fmax(dev, fmax(fabs(v.x - w.x), fabs(v.y - w.y)));
+    amax = fmax(amax, fmax(fabs(v.x), fabs(v.y)));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out2, static_cast<unsigned long long>(__double_as_longlong(dev)));
+    atomicMax(out2 + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
+  }
+}
+
+cudaError_t launch_near_symmetry(const c64* S, int n, int n_blk, const int* mirror, const int* perm,
+                                 unsigned long long* out2, cudaStream_t stream) {
+  const long long total = static_cast<long long>(n) * n * n_blk;
+  if (total == 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 16LL * kNumSMs) blocks = 16LL * kNumSMs;
+  near_symmetry_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(S, n, n_blk, mirror, perm, out2);
   return cudaGetLastError();
 }
 

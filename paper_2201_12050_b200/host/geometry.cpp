@@ -46,6 +46,53 @@ Element make_tri(const V3& a, const V3& b, const V3& c, cd beta) {
   return e;
 }
 
+// Inversion-consistent corner order (extension). When the
+// cell mesh is symmetric under the point reflection x -> 2c - x about its
+// bounding-box centre c (every element's reflected corner set is an element of
+// the mesh, never itself), the reflection partner k = P(j) > j of element j
+// gets the reflected corners in the order (b', a', c') for a triangle (a, b, c)
+// and (b', a', d', c') for a quad (a, b, c, d): its bilinear element map is then
+// j's map reflected with u -> 1 - u, and since the Gauss nodes, the weights and
+// the 4-fold subdivision are symmetric under u -> 1 - u the two elements carry
+// reflected quadrature node sets. Every interaction then satisfies
+// S_{-o}[P i, P j] = S_o[i, j] up to rounding (normals flip, relative vectors
+// flip, all kernel terms are even in both), which the lattice near field uses
+// to stream each Fourier-mode block once for q and -q. The element order, the
+// corner sets and the orientation are unchanged; meshes without the symmetry
+// are left as they are.
+void symmetrize_inversion(Mesh& m) {
+  const int n = m.size();
+  if (n < 2) return;
+  V3 lo, hi;
+  m.bbox(lo, hi);
+  const V3 ctr = 0.5 * (lo + hi);
+  const double tol = 1e-9 * std::max(1e-300, norm(hi - lo));
+  auto refl = [&](const V3& p) { return 2.0 * ctr - p; };
+  std::vector<int> partner(n, -1);
+  for (int j = 0; j < n; ++j) {
+    const V3 r = refl(m.el[j].centroid);
+    for (int k = 0; k < n && partner[j] < 0; ++k)
+      if (m.el[k].nv == m.el[j].nv && norm(m.el[k].centroid - r) < tol) partner[j] = k;
+    const int k = partner[j];
+    if (k < 0 || k == j) return;  // not point-symmetric
+    for (int a = 0; a < m.el[j].nv; ++a) {  // the reflected corners are k's corners
+      bool found = false;
+      for (int b = 0; b < m.el[k].nv && !found; ++b) found = norm(m.el[k].c[b] - refl(m.el[j].c[a])) < tol;
+      if (!found) return;
+    }
+  }
+  for (int j = 0; j < n; ++j)
+    if (partner[partner[j]] != j) return;
+  for (int j = 0; j < n; ++j) {
+    const int k = partner[j];
+    if (k < j) continue;
+    const Element& e = m.el[j];
+    const cd beta = m.el[k].beta;
+    m.el[k] = e.nv == 3 ? make_tri(refl(e.c[1]), refl(e.c[0]), refl(e.c[2]), beta)
+                        : make_quad(refl(e.c[1]), refl(e.c[0]), refl(e.c[3]), refl(e.c[2]), beta);
+  }
+}
+
 void Mesh::bbox(V3& lo, V3& hi) const {
   const double big = std::numeric_limits<double>::max();
   lo = {big, big, big};
@@ -148,11 +195,16 @@ Mesh icosphere(double radius, int subdivisions, cd beta) {
     if (dot(cross(b - a, c - a), a + b + c) < 0.0) std::swap(b, c);
     m.el.push_back(make_tri(a, b, c, beta));
   }
+  symmetrize_inversion(m);
   return m;
 }
 
 // Closed cylinder along z on [0, height]: n_theta x n_z side quads each split
 // into two triangles, plus a triangle fan per cap; 2 n_theta (n_z + 1) triangles.
+// The split diagonal runs (theta_i, z_j)-(theta_i+1, z_j+1) in the lower half and
+// the other way in the upper half (the middle row of an odd n_z: half of the
+// ring each way), so for even n_theta the triangulation is symmetric under the
+// point reflection about the cylinder's centre, like the cylinder itself.
 Mesh closed_cylinder(double radius, double height, int n_theta, int n_z, cd beta) {
   Mesh m;
   auto ring = [&](int i, double z) {
@@ -163,9 +215,15 @@ Mesh closed_cylinder(double radius, double height, int n_theta, int n_z, cd beta
     double z0 = height * j / n_z, z1 = height * (j + 1) / n_z;
     for (int i = 0; i < n_theta; ++i) {
       V3 p00 = ring(i, z0), p10 = ring(i + 1, z0), p11 = ring(i + 1, z1), p01 = ring(i, z1);
+      const bool lower = 2 * j + 1 < n_z || (2 * j + 1 == n_z && 2 * i < n_theta);
       // outward (radial) orientation: theta then z is counter-clockwise seen from outside
-      m.el.push_back(make_tri(p00, p10, p11, beta));
-      m.el.push_back(make_tri(p00, p11, p01, beta));
+      if (lower) {
+        m.el.push_back(make_tri(p00, p10, p11, beta));
+        m.el.push_back(make_tri(p00, p11, p01, beta));
+      } else {
+        m.el.push_back(make_tri(p00, p10, p01, beta));
+        m.el.push_back(make_tri(p10, p11, p01, beta));
+      }
     }
   }
   V3 bottom{0, 0, 0}, top{0, 0, height};
@@ -173,6 +231,7 @@ Mesh closed_cylinder(double radius, double height, int n_theta, int n_z, cd beta
     m.el.push_back(make_tri(bottom, ring(i + 1, 0.0), ring(i, 0.0), beta));      // normal -z
     m.el.push_back(make_tri(top, ring(i, height), ring(i + 1, height), beta));   // normal +z
   }
+  symmetrize_inversion(m);
   return m;
 }
 
@@ -207,6 +266,7 @@ Mesh closed_box(double lx, double ly, double lz, double h, bool split, cd beta) 
           }
         }
     }
+  symmetrize_inversion(m);
   return m;
 }
 

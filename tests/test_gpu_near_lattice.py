@@ -45,9 +45,9 @@ def test_lattice_near_field_matches_oracle_and_direct(ops, counts, n):
     rng = np.random.default_rng(n + 3 * counts[0] + 5 * counts[1] + 7 * counts[2])
     d = toeplitz_only(rng, counts, n)
     lat = ops(d, near_path="lattice")
-    path, sizes, nbytes = lat.near_path()
+    path, sizes, nbytes, paired, dev = lat.near_path()
     R = np.abs(d.near_offsets).max(axis=0)
-    assert path == "lattice"
+    assert path == "lattice" and not paired and dev == -1.0
     assert sizes == tuple(int(m + r) if m > 1 else 1 for m, r in zip(counts, R))
     assert nbytes == 16 * n * n * int(np.prod(sizes))
     p = uvec(rng, d.N)
@@ -87,16 +87,20 @@ def test_lattice_fmm_matvec_matches_oracle(ops, assembled, cid, var):
     assert rel(op.matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("nrhs", [2, 8, 9, 16, 70])
-def test_lattice_multi_rhs_gemv_and_dmma(ops, assembled, nrhs):
-    """<= 8 right-hand sides: streaming per-mode GEMV; more: the per-mode
-    products as DMMA GEMM tiles (rhs-major spectrum). Every rhs equals its own
-    single-rhs product and the oracle."""
+@pytest.mark.parametrize("nrhs,inv", [(2, True), (4, True), (5, True), (8, True), (9, True), (16, True), (70, True),
+                                       (3, False), (8, False), (9, False)])
+def test_lattice_multi_rhs_gemv_and_dmma(ops, assembled, nrhs, inv):
+    """few right-hand sides: streaming per-mode GEMV (<= 4 with mode pairs,
+    <= 8 without); more: the per-mode products as DMMA GEMM tiles (rhs-major
+    spectrum, mirrored-mode tiles gathered / scattered through P). Every rhs
+    equals its own single-rhs product and the oracle."""
     sc, d = assembled(3, 2)
     rng = np.random.default_rng(40 + nrhs)
     P = [uvec(rng, d.N) for _ in range(nrhs)]
-    y = ops(d, max_rhs=nrhs, near_path="lattice").matvec(np.concatenate(P))
-    single = ops(d, near_path="lattice")
+    op = ops(d, max_rhs=nrhs, near_path="lattice", use_inversion=inv)
+    assert op.near_path()[3] == inv
+    y = op.matvec(np.concatenate(P))
+    single = ops(d, near_path="lattice", use_inversion=inv)
     ora = O.OracleFmm(d)
     for r in sorted({0, nrhs // 2, nrhs - 1}):
         yr = y[r * d.N:(r + 1) * d.N]
@@ -119,7 +123,9 @@ def test_lattice_mode_partition_sums_to_product(ops, assembled, nranks):
         lo, hi, _ = op.partition()
         covered += hi - lo
         total += op.matvec(p)
-    assert covered == int(np.prod(op.near_path()[1]))
+    path, sizes, nbytes, paired, _ = op.near_path()
+    assert paired  # the closed cylinder's triangulation is point-symmetric
+    assert covered == nbytes // (16 * d.n_dof ** 2)  # stored blocks (one per mode pair)
     assert rel(total, full) < 1e-13
 
 
@@ -179,9 +185,10 @@ def test_lattice_is_rejected_with_a_half_space_image_pair(ops):
 
 
 def test_cost_model_choices_at_baseline_shapes(ops):
-    """auto picks the lattice path for cfg2 (125 offsets over 4 x 32 cells of
-    1024 DOF: 287 modes stream 4.7 GB against 67 GFLOP of direct GEMM) and the
-    direct GEMM for cfg3 (19 offsets: 17^3 modes would stream 8 GB)"""
+    """without mode pairing (all-zero blocks never verify the inversion) auto
+    picks the lattice path for cfg2 (125 offsets over 4 x 32 cells of 1024 DOF:
+    287 modes stream 4.8 GB against 67 GFLOP of direct GEMM) and the direct GEMM
+    for cfg3 (19 offsets: 17^3 modes would stream 8 GB)"""
     from paper_2201_12050_b200 import Scene
     from test_gpu_parity import Data
 
@@ -194,15 +201,16 @@ def test_cost_model_choices_at_baseline_shapes(ops):
         assert ops(d).near_path()[0] == want
 
 
-@pytest.mark.parametrize("path", ["direct", "lattice"])
-def test_full_size_cfg2_both_paths(ops, path):
-    """configs[1] at its stated size (131,072 DOF) through either near path:
-    parity with the oracle (seed = config id), linearity, determinism, and a
-    4-way partition summing back to the product"""
+@pytest.mark.parametrize("cid,path", [(2, "direct"), (2, "lattice"), (3, "direct"), (3, "lattice")])
+def test_full_size_both_paths(ops, cid, path):
+    """configs[1] (131,072 DOF) and configs[2] (1,310,720 DOF) at their stated
+    sizes through either near path (lattice: mode pairs through the verified
+    cell inversion): parity with the oracle (seed = config id), linearity,
+    determinism, and a 4-way partition summing back to the product"""
     from paper_2201_12050_b200 import Scene
     from paper_2201_12050_b200.fmm import assemble_near_gpu
 
-    sc = Scene(2, 0)
+    sc = Scene(cid, 0)
     d = sc.assemble_fmm(4, skip_near_values=True)
     near = assemble_near_gpu(sc, d)
 
@@ -214,7 +222,11 @@ def test_full_size_cfg2_both_paths(ops, path):
             return getattr(self._d, k)
 
     op = ops(d, near_blocks=near, near_path=path)
-    rng = np.random.default_rng(2)
+    info = op.near_path()
+    assert info[0] == path
+    if path == "lattice":
+        assert info[3] and 0.0 <= info[4] <= 1e-12
+    rng = np.random.default_rng(cid)
     p, q = uvec(rng, d.N), uvec(rng, d.N)
     y = op.matvec(p)
     assert rel(y, O.OracleFmm(WithNear(d, near.cpu().numpy())).matvec(p)) <= MATVEC_TOL
@@ -226,3 +238,75 @@ def test_full_size_cfg2_both_paths(ops, path):
         op.set_partition(r, 4)
         total += op.matvec(p)
     assert rel(total, y) < 1e-13
+
+
+def _symmetric_toeplitz(rng, counts, n, perturb=0.0):
+    """random Toeplitz with S_-o = P S_o P for a fixed-point-free involution P"""
+    idx = rng.permutation(n)
+    perm = np.empty(n, np.int64)
+    perm[idx[0::2]], perm[idx[1::2]] = idx[1::2], idx[0::2]
+    offs = all_offsets(counts)
+    blocks = {}
+    for o in offs:
+        m = tuple(-c for c in o)
+        if m in blocks:
+            blocks[o] = blocks[m][np.ix_(perm, perm)]
+        elif o == m:
+            a = crand(rng, n, n)
+            blocks[o] = 0.5 * (a + a[np.ix_(perm, perm)])
+        else:
+            blocks[o] = crand(rng, n, n)
+    d = toeplitz_only(rng, counts, n)
+    d.near_offsets = np.asarray(offs, np.int32)
+    d.near_blocks = np.stack([blocks[o] for o in offs])
+    if perturb:
+        d.near_blocks[0, 0, 0] += perturb
+    d.cell_inversion = perm.astype(np.int32)
+    return d
+
+
+@pytest.mark.parametrize("counts,n", [((3, 3, 1), 64), ((4, 2, 3), 40), ((1, 7, 1), 130), ((2, 2, 2), 6)])
+def test_lattice_mode_pairs_through_the_cell_inversion(ops, counts, n):
+    """S_-o = P S_o P: one stored block per mode pair (q, -q), the mirror mode
+    through P; parity with the oracle and with the unpaired path"""
+    rng = np.random.default_rng(n + sum(counts))
+    d = _symmetric_toeplitz(rng, counts, n)
+    op = ops(d, near_path="lattice")
+    path, sizes, nbytes, paired, dev = op.near_path()
+    assert paired and dev <= 1e-15
+    q = int(np.prod(sizes))
+    self_mirror = int(np.prod([1 + (L % 2 == 0) if L > 1 else 1 for L in sizes]))  # q = -q modes
+    assert nbytes == 16 * n * n * ((q - self_mirror) // 2 + self_mirror)
+    p = uvec(rng, d.N)
+    y = op.matvec(p)
+    assert rel(y, O.toeplitz_matvec(counts, d.near_offsets, d.near_blocks, p)) <= MATVEC_TOL
+    assert rel(y, ops(d, near_path="lattice", use_inversion=False).matvec(p)) <= MATVEC_TOL
+
+
+def test_lattice_inversion_that_does_not_hold_falls_back(ops):
+    """a cell inversion the blocks do not satisfy (one entry perturbed) is
+    measured and rejected: unpaired spectrum, still the oracle's product"""
+    rng = np.random.default_rng(77)
+    d = _symmetric_toeplitz(rng, (3, 2, 1), 24, perturb=1e-6)
+    op = ops(d, near_path="lattice")
+    path, sizes, nbytes, paired, dev = op.near_path()
+    assert not paired and dev > 1e-9
+    assert nbytes == 16 * 24 * 24 * int(np.prod(sizes))
+    p = uvec(rng, d.N)
+    assert rel(op.matvec(p), O.toeplitz_matvec((3, 2, 1), d.near_offsets, d.near_blocks, p)) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("cid,var,paired", [(3, 2, True), (2, 2, True), (4, 2, True), (1, 1, True)])
+def test_scene_inversion_pairing(ops, assembled, cid, var, paired):
+    """icosphere, point-symmetric cylinder triangulation, closed box and the
+    reference's cube-sphere all verify the inversion on their assembled blocks
+    (rounding-level deviation); the perturbed synthetic case above covers the
+    refusal"""
+    sc, d = assembled(cid, var)
+    assert d.cell_inversion is not None
+    op = ops(d, near_path="lattice")
+    info = op.near_path()
+    assert info[3] == paired
+    assert (0.0 <= info[4] <= 1e-12) if paired else info[4] > 1e-12
+    p = uvec(np.random.default_rng(cid), d.N)
+    assert rel(op.matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL

@@ -75,8 +75,10 @@ def run_config(cid, args, out):
     t = time.perf_counter()
     op = FmmOperators(data, max_rhs=nrhs)
     rec["upload_s"] = time.perf_counter() - t
-    path, lat, spec_bytes = op.near_path()
+    path, lat, spec_bytes, mode_pairs, sym_dev = op.near_path()
     rec["near_path"] = path
+    rec["near_mode_pairs"] = mode_pairs
+    rec["near_inversion_deviation"] = sym_dev
     rec["near_lattice"] = list(lat)
     sizes, _ = op.spectrum()
     rec["fft_sizes"] = list(sizes)
@@ -102,7 +104,7 @@ def run_config(cid, args, out):
     rec["near_gemm_frac_of_fp64_peak"] = flops / (st["near_gemm"] * 1e-3) / FP64
     if path == "lattice":  # per-mode product streams the block spectrum
         qn = int(np.prod(lat))
-        mb = spec_bytes + 2 * 16.0 * data.n_dof * qn
+        mb = spec_bytes + 2 * 16.0 * data.n_dof * qn  # stored blocks + x_hat read + y_hat written
         rec["near_mode_product_gb_per_s"] = mb / (st["near_mode_product"] * 1e-3) / 1e9
         rec["near_mode_product_frac_of_hbm"] = mb / (st["near_mode_product"] * 1e-3) / HBM
     lam_bytes = 16.0 * q * 625
