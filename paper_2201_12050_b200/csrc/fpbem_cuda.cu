@@ -614,9 +614,7 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
           "near reduce + l2p");
     op->launches++;
   } else if (far_here) {  // y += U0 L (src/fmm.cpp:265-267): the reduction with no pairs, accumulating
-    check(launch_near_reduce_l2p(nullptr, op->zero_ptr, op->zero_ptr, op->u0, op->loc, y, op->n, op->b, op->n_cells,
-                                 op->N, nrhs, true, s),
-          "l2p");
+    check(launch_l2p_add(op->u0, op->loc, y, op->n, op->b, op->n_cells, op->N, nrhs, s), "l2p");
     op->launches++;
   }
   if (op->comm && reduce)  // sum the ranks' partial products, in place, on the same stream

@@ -24,6 +24,9 @@ cudaError_t launch_mode_gemv(const c64* shat, const int2* items, const int* perm
 // cell-inversion check: out2[0] = max |S_mirror[s][P i, P j] - S_s[i, j]|, out2[1] = max |S| (double bits)
 cudaError_t launch_near_symmetry(const c64* S, int n, int n_blk, const int* mirror, const int* perm,
                                  unsigned long long* out2, cudaStream_t stream);
+// y += U0 L per (cell, rhs) (the lattice path's L2P; bitwise = the reduction with no pairs)
+cudaError_t launch_l2p_add(const c64* u0, const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
+                           int nrhs, cudaStream_t stream);
 cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* tgt_pairs, const c64* u0,
                                    const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
                                    int nrhs, bool accumulate, cudaStream_t stream);

@@ -247,6 +247,102 @@ p2m_kernel(const c64* __restrict__ v0t, const c64* __restrict__ x, c64* __restri
   }
 }
 
+// The same axis pass as a batched complex GEMM on the FP64 tensor cores:
+// per line a, C (n_out x n_inner) = W (n_out x n_in) B (n_in x n_inner) with
+// W[q][j] = tw[(j q) mod L] (conjugated backward) and B the line's inputs. One
+// warp per (a, 8 consecutive inner indices): the line's inputs for those 8
+// columns are loaded once into registers as m8n8k4 B fragments (8 consecutive
+// inner values per k row: 128-byte coalesced), then every 8-row block of W runs
+// its k steps from fragment-ordered shared memory (conflict-free, expanded once
+// per CTA) in the Gauss 3-multiplication form (T1 = Wr Br, T2 = Wi Bi,
+// T3 = (Wr + Wi)(Br + Bi); C = (T1 - T2, T3 - T1 - T2)). Each output is a fixed-
+// order sum (deterministic). n_in, n_out <= kDftMmaMax.
+constexpr int kDftMmaMax = 64;
+constexpr int kDftMmaWarps = 4;
+
+template <int KTM>
+__global__ void __launch_bounds__(kDftMmaWarps * 32)
+dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ tw, long long n_a,
+                     int n_in, int n_out, long long n_inner, int L, int backward, double scale) {
+  extern __shared__ __align__(16) unsigned char dmma_smem[];
+  const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
+  double* wr = reinterpret_cast<double*>(dmma_smem);  // [mt][kt][lane]
+  double* wi = wr + MT * KT * 32;
+  double* ws = wi + MT * KT * 32;
+  for (int e = threadIdx.x; e < MT * KT * 32; e += blockDim.x) {
+    const int ln = e & 31, f = e >> 5, kt = f % KT, mt = f / KT;
+    const int q = mt * 8 + (ln >> 2), j = kt * 4 + (ln & 3);
+    c64 w = cmk(0.0, 0.0);
+    if (q < n_out && j < n_in) {
+      w = tw[(j * q) % L];
+      if (backward) w.y = -w.y;
+    }
+    wr[e] = w.x;
+    wi[e] = w.y;
+    ws[e] = w.x + w.y;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  const long long n_et = (n_inner + 7) / 8, tiles = n_a * n_et;
+  const long long warp0 = blockIdx.x * static_cast<long long>(kDftMmaWarps) + (threadIdx.x >> 5);
+  const long long nwarps = static_cast<long long>(gridDim.x) * kDftMmaWarps;
+  // B fragments of the next tile are loaded before the current tile's MMAs
+  c64 nb[KTM];
+  auto load = [&](long long t) {
+    const long long a = t / n_et, col = (t % n_et) * 8 + fr;
+    const bool ok = t < tiles && col < n_inner;
+    const c64* src = in + a * n_in * n_inner + col;
+#pragma unroll
+    for (int kt = 0; kt < KTM; ++kt) {
+      const int j = kt * 4 + fk;
+      nb[kt] = (ok && kt < KT && j < n_in) ? src[static_cast<long long>(j) * n_inner] : cmk(0.0, 0.0);
+    }
+  };
+  load(warp0);
+  for (long long t = warp0; t < tiles; t += nwarps) {
+    double br[KTM], bi[KTM], bs[KTM];
+#pragma unroll
+    for (int kt = 0; kt < KTM; ++kt) {
+      br[kt] = nb[kt].x;
+      bi[kt] = nb[kt].y;
+      bs[kt] = nb[kt].x + nb[kt].y;
+    }
+    load(t + nwarps);
+    const long long a = t / n_et, e0 = (t % n_et) * 8;
+    c64* dst = out + a * n_out * n_inner;
+    for (int mt = 0; mt < MT; mt += 2) {  // two row blocks per pass: independent accumulator chains
+      double t1[2][2] = {}, t2[2][2] = {}, t3[2][2] = {};
+      const bool two = mt + 1 < MT;
+#pragma unroll
+      for (int kt = 0; kt < KTM; ++kt) {
+        if (kt < KT) {
+          const int o0 = (mt * KT + kt) * 32 + lane, o1 = o0 + KT * 32;
+          dmma884(t1[0][0], t1[0][1], wr[o0], br[kt]);
+          dmma884(t2[0][0], t2[0][1], wi[o0], bi[kt]);
+          dmma884(t3[0][0], t3[0][1], ws[o0], bs[kt]);
+          if (two) {
+            dmma884(t1[1][0], t1[1][1], wr[o1], br[kt]);
+            dmma884(t2[1][0], t2[1][1], wi[o1], bi[kt]);
+            dmma884(t3[1][0], t3[1][1], ws[o1], bs[kt]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = (mt + u) * 8 + fr;
+        if (q >= n_out) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long long c = e0 + 2 * fk + h;
+          if (c < n_inner)
+            dst[static_cast<long long>(q) * n_inner + c] =
+                cmk((t1[u][h] - t2[u][h]) * scale, (t3[u][h] - t1[u][h] - t2[u][h]) * scale);
+        }
+      }
+    }
+  }
+}
+
 // Long lines with few outputs (e.g. the 256 -> 512 line of a 1 x 256 lattice):
 // one warp per output (a, qo, inner); lane l sums the terms j = l, l + 32, ...
 // then a fixed shuffle tree combines the lanes (deterministic).
@@ -866,6 +962,52 @@ int grid_for(long long total, int threads) {
 cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_a, int n_in, int n_out,
                             long long n_inner, int L, bool backward, double scale, cudaStream_t stream) {
   if (n_a * n_out * n_inner == 0) return cudaSuccess;
+  // short lines: the tensor-core form (FPBEM_DFT=fma keeps the DFMA kernels, A/B)
+  static const bool dft_mma = [] {
+    const char* v = std::getenv("FPBEM_DFT");
+    return !(v && std::strcmp(v, "fma") == 0);
+  }();
+  if (dft_mma && n_in <= kDftMmaMax && n_out <= kDftMmaMax) {
+    const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
+    const size_t smem = sizeof(double) * 3 * MT * KT * 32;
+    static bool raised = false;
+    if (!raised) {
+      for (auto fn : {dft_axis_dmma_kernel<4>, dft_axis_dmma_kernel<8>, dft_axis_dmma_kernel<16>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sizeof(double) * 3 * 8 * 16 * 32));
+        if (e != cudaSuccess) return e;
+      }
+      raised = true;
+    }
+    const long long tiles = n_a * ((n_inner + 7) / 8);
+    long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
+    // one resident wave (W expanded once per CTA), as many CTAs per SM as fit
+    static int occ[3] = {0, 0, 0};
+    const int which = KT <= 4 ? 0 : KT <= 8 ? 1 : 2;
+    if (occ[which] == 0) {
+      const void* fn = which == 0 ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<4>)
+                       : which == 1 ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<8>)
+                                    : reinterpret_cast<const void*>(dft_axis_dmma_kernel<16>);
+      int per_sm = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDftMmaWarps * 32,
+                                                                    sizeof(double) * 3 * 4 * 8 * 32);
+      if (e != cudaSuccess) return e;
+      occ[which] = per_sm > 0 ? per_sm : 1;
+    }
+    const long long cap = static_cast<long long>(kNumSMs) * occ[which];
+    if (blocks > cap) blocks = cap;
+    const int bw = backward ? 1 : 0;
+    if (KT <= 4)
+      dft_axis_dmma_kernel<4><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
+          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
+    else if (KT <= 8)
+      dft_axis_dmma_kernel<8><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
+          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
+    else
+      dft_axis_dmma_kernel<16><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
+          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
+    return cudaGetLastError();
+  }
   // widest output group that still gives >= 2 x 256 threads per SM
   const long long want = 2LL * kNumSMs * 256;
   if (n_in >= 64 && n_a * n_out * n_inner < want) {  // long lines, few outputs: a warp per output
@@ -878,6 +1020,11 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
   }
   int qg = 8;
   while (qg > 1 && n_a * ((n_out + qg - 1) / qg) * n_inner < want) qg /= 2;
+  static const int qg_env = [] {  // FPBEM_DFT_QG: force the outputs per thread (A/B)
+    const char* v = std::getenv("FPBEM_DFT_QG");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (qg_env == 1 || qg_env == 2 || qg_env == 4 || qg_env == 8) qg = qg_env;
   const long long total = n_a * ((n_out + qg - 1) / qg) * n_inner;
   const int grid = grid_for(total, 256), bw = backward ? 1 : 0;
   const size_t smem = sizeof(c64) * static_cast<size_t>(L);

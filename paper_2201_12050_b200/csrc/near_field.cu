@@ -421,6 +421,80 @@ cudaError_t launch_near_symmetry(const c64* S, int n, int n_blk, const int* mirr
   return cudaGetLastError();
 }
 
+// y[r, t, i] += sum_m U0[i, m] L[t, r, m] (src/fmm.cpp:265-267) for the lattice
+// near field, whose product already sits in y. CTA = (128 rows, kL2pCols (cell,
+// rhs) columns): each U0 element is loaded once per CTA and used for all its
+// columns (independent accumulators), the locals come from shared memory as
+// broadcasts; every output sums m in ascending order from zero and is then
+// added to y, the same arithmetic as the reduction kernel with no pairs.
+constexpr int kL2pCols = 8;
+
+__global__ void __launch_bounds__(128)
+l2p_add_kernel(const c64* __restrict__ u0, const c64* __restrict__ local, c64* __restrict__ y, int n, int n_coef,
+               long long n_cols, long long N, int nrhs, int row_tiles) {
+  extern __shared__ __align__(16) unsigned char l2p_smem[];
+  c64* ls = reinterpret_cast<c64*>(l2p_smem);  // [kL2pCols][n_coef]
+  const long long c0 = static_cast<long long>(blockIdx.x / row_tiles) * kL2pCols;
+  const int i = (blockIdx.x % row_tiles) * 128 + threadIdx.x;
+  const int nc = static_cast<int>(min(static_cast<long long>(kL2pCols), n_cols - c0));
+  for (int e = threadIdx.x; e < kL2pCols * n_coef; e += 128)
+    ls[e] = e < nc * n_coef ? local[c0 * n_coef + e] : cmk(0.0, 0.0);
+  __syncthreads();
+  if (i >= n) return;
+  c64 yv[kL2pCols];  // the current y, loaded up front (independent of the sums)
+  long long off[kL2pCols];
+#pragma unroll
+  for (int c = 0; c < kL2pCols; ++c) {
+    const int tr = static_cast<int>(c0) + c;  // t * nrhs + r (< 2^31: checked at launch)
+    off[c] = (tr % nrhs) * N + static_cast<long long>(tr / nrhs) * n + i;
+    yv[c] = c < nc ? y[off[c]] : cmk(0.0, 0.0);
+  }
+  c64 acc[kL2pCols];
+#pragma unroll
+  for (int c = 0; c < kL2pCols; ++c) acc[c] = cmk(0.0, 0.0);
+  int m = 0;
+  for (; m + 4 <= n_coef; m += 4) {
+    c64 u[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) u[v] = __ldg(u0 + static_cast<size_t>(m + v) * n + i);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int c = 0; c < kL2pCols; ++c) acc[c] = cfma(u[v], ls[c * n_coef + m + v], acc[c]);
+  }
+  for (; m < n_coef; ++m) {
+    const c64 u = __ldg(u0 + static_cast<size_t>(m) * n + i);
+#pragma unroll
+    for (int c = 0; c < kL2pCols; ++c) acc[c] = cfma(u, ls[c * n_coef + m], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < kL2pCols; ++c) {
+    if (c >= nc) break;
+    y[off[c]] = cadd(yv[c], cadd(cmk(0.0, 0.0), acc[c]));
+  }
+}
+
+cudaError_t launch_l2p_add(const c64* u0, const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
+                           int nrhs, cudaStream_t stream) {
+  if (n_coef > MAX_COEF) return cudaErrorInvalidValue;
+  const int row_tiles = (n + 127) / 128;
+  const long long cols = static_cast<long long>(n_cells) * nrhs;
+  const long long blocks = (cols + kL2pCols - 1) / kL2pCols * row_tiles;
+  if (blocks > 0x7fffffffLL || cols + kL2pCols > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(c64) * kL2pCols * n_coef;
+  if (smem > 48 * 1024) {
+    static bool raised = false;
+    if (!raised) {
+      cudaError_t e = cudaFuncSetAttribute(l2p_add_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      if (e != cudaSuccess) return e;
+      raised = true;
+    }
+  }
+  l2p_add_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(u0, local, y, n, n_coef, cols, N, nrhs,
+                                                                      row_tiles);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* tgt_pairs, const c64* u0,
                                    const c64* local, c64* y, int n, int n_coef, int n_cells, long long N,
                                    int nrhs, bool accumulate, cudaStream_t stream) {
