@@ -276,7 +276,35 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
   bs.counter = static_cast<unsigned*>(alloc(sizeof(unsigned) * G, "batch counters"));
   check(cudaMemsetAsync(bs.counter, 0, sizeof(unsigned) * G, s), "counters");
   check(cudaMemsetAsync(d_flag, 0, g8, s), "flags");
-  ensure_pinned(op, total + 64);
+  // per-RHS fused MGS (one cooperative launch per right-hand side and step, w
+  // resident in shared memory: each basis vector is streamed once per
+  // projection instead of the batched kernels' four vector passes), when the
+  // vector fits the cooperative grid; FPBEM_GMRES_BMGS=0 keeps the batched kernels
+  static const bool per_rhs_env = [] {
+    const char* v = std::getenv("FPBEM_GMRES_BMGS");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const bool per_rhs = per_rhs_env && mgs_fused_supported(n);
+  // [r][m+1] h, [r][m+1] reorth h, [r][4] norms (pre, post, -, post after reorth)
+  const size_t o_fh = 0, o_fhc = o_fh + 16 * static_cast<size_t>(G) * (m + 1),
+               o_fn = o_fhc + 16 * static_cast<size_t>(G) * (m + 1), ftotal = o_fn + 32 * static_cast<size_t>(G);
+  char* fsc = per_rhs ? static_cast<char*>(alloc(ftotal, "per-rhs mgs scalars")) : nullptr;
+  ensure_pinned(op, total + 64 + (per_rhs ? ftotal : 0));
+  char* fpin = static_cast<char*>(op->pinned) + total + 64;
+  auto ffetch = [&](size_t off, size_t bytes) {
+    check(cudaMemcpyAsync(fpin + off, fsc + off, bytes, cudaMemcpyDeviceToHost, s), "batched readback");
+    check(cudaStreamSynchronize(s), "batched sync");
+  };
+  auto fget_c = [&](size_t off, size_t idx) {
+    c64 v;
+    std::memcpy(&v, fpin + off + 16 * idx, 16);
+    return cd(v.x, v.y);
+  };
+  auto fget_d = [&](size_t idx) {
+    double v;
+    std::memcpy(&v, fpin + o_fn + 8 * idx, 8);
+    return v;
+  };
   char* pin = static_cast<char*>(op->pinned);
   auto fetch = [&](size_t off, size_t bytes) {
     check(cudaMemcpyAsync(pin + off, sc + off, bytes, cudaMemcpyDeviceToHost, s), "batched readback");
@@ -347,6 +375,34 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
   std::vector<char> inner(G, 0);
   const c64* rsrc = Bd;
 
+  // normalise w, then the rotations / Givens / estimate of step j (:74-105) per RHS
+  auto finish_step = [&](int j, const std::vector<int>& it, const std::vector<double>& wn2) {
+    c64* W = V + static_cast<long long>(j + 1) * G * n;
+    std::vector<double> hl(G, 1.0);
+    std::vector<int> norm_set;
+    for (int r : it) {
+      hl[r] = std::sqrt(wn2[r]);
+      if (hl[r] > 0.0) norm_set.push_back(r);
+    }
+    if (!norm_set.empty()) {
+      set_mask(norm_set);
+      put(o_d, hl.data(), g8);
+      check(launch_b_div(W, W, n, n, G, d_mask, d_d, s), "normalise");
+      op->launches++;
+    }
+    for (int r : it) {  // rotations, Givens, estimate (:74-105), per RHS
+      const double hlast = hl[r];
+      cyc[r].h(j + 1, j) = hlast;
+      const double res = cyc[r].rotate(j);
+      ++out.iterations[r];
+      const double est = res / bnorm[r];
+      out.history[r].push_back(est);
+      jr[r] = j + 1;
+      if (est <= tol || hlast == 0.0) inner[r] = 0;
+    }
+  };
+
+
   while (true) {
     std::vector<int> act;
     for (int r = 0; r < G; ++r)
@@ -368,6 +424,44 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
       c64* Vj = V + static_cast<long long>(j) * G * n;
       c64* W = V + static_cast<long long>(j + 1) * G * n;
       apply_set(Vj, W, it);
+      if (per_rhs) {  // the single-RHS MGS of gmres_one for each right-hand side (same arithmetic)
+        const long long ld = static_cast<long long>(G) * n;
+        for (int r : it) {
+          check(launch_mgs_fused(W + static_cast<long long>(r) * n, V + static_cast<long long>(r) * n, ld, j, n,
+                                 reinterpret_cast<c64*>(fsc + o_fh) + static_cast<size_t>(r) * (m + 1),
+                                 reinterpret_cast<double*>(fsc + o_fn) + 4 * static_cast<size_t>(r), d_flag + r,
+                                 op->rs, true, s),
+                "mgs fused");
+          op->launches++;
+        }
+        fetch(0, g8);  // flags
+        flags_of(it);
+        ffetch(0, ftotal);
+        std::vector<int> reo;
+        std::vector<double> wn2(G, 0.0);
+        for (int r : it) {
+          for (int i = 0; i <= j; ++i) cyc[r].h(i, j) = fget_c(o_fh, static_cast<size_t>(r) * (m + 1) + i);
+          wn2[r] = fget_d(4 * static_cast<size_t>(r) + 1);
+          if (std::sqrt(wn2[r]) < 0.5 * std::sqrt(fget_d(4 * static_cast<size_t>(r)))) reo.push_back(r);  // (:63-69)
+        }
+        for (int r : reo) {
+          check(launch_mgs_fused(W + static_cast<long long>(r) * n, V + static_cast<long long>(r) * n, ld, j, n,
+                                 reinterpret_cast<c64*>(fsc + o_fhc) + static_cast<size_t>(r) * (m + 1),
+                                 reinterpret_cast<double*>(fsc + o_fn) + 4 * static_cast<size_t>(r) + 2, d_flag + r,
+                                 op->rs, false, s),
+                "reorth fused");
+          op->launches++;
+        }
+        if (!reo.empty()) {
+          ffetch(0, ftotal);
+          for (int r : reo) {
+            for (int i = 0; i <= j; ++i) cyc[r].h(i, j) += fget_c(o_fhc, static_cast<size_t>(r) * (m + 1) + i);
+            wn2[r] = fget_d(4 * static_cast<size_t>(r) + 3);
+          }
+        }
+        finish_step(j, it, wn2);
+        continue;
+      }
       set_mask(it);
       check(launch_b_sqnorm(W, n, n, G, d_mask, bs, d_pre, d_flag, s), "pre norm");
       check(launch_b_dotc(V, W, n, n, G, d_mask, bs, d_h, s), "mgs dot");
@@ -406,28 +500,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
           wn2[r] = get_d(o_post2, r);
         }
       }
-      std::vector<double> hl(G, 1.0);
-      std::vector<int> norm_set;
-      for (int r : it) {
-        hl[r] = std::sqrt(wn2[r]);
-        if (hl[r] > 0.0) norm_set.push_back(r);
-      }
-      if (!norm_set.empty()) {
-        set_mask(norm_set);
-        put(o_d, hl.data(), g8);
-        check(launch_b_div(W, W, n, n, G, d_mask, d_d, s), "normalise");
-        op->launches++;
-      }
-      for (int r : it) {  // rotations, Givens, estimate (:74-105), per RHS
-        const double hlast = hl[r];
-        cyc[r].h(j + 1, j) = hlast;
-        const double res = cyc[r].rotate(j);
-        ++out.iterations[r];
-        const double est = res / bnorm[r];
-        out.history[r].push_back(est);
-        jr[r] = j + 1;
-        if (est <= tol || hlast == 0.0) inner[r] = 0;
-      }
+      finish_step(j, it, wn2);
     }
     // x_r += V_r y_r for every RHS of the cycle, then the true residuals (:109-116)
     std::vector<c64> yh(static_cast<size_t>(m) * G, cmk(0.0, 0.0));

@@ -295,45 +295,92 @@ __global__ void __launch_bounds__(RT) cgs_update_kernel(c64* __restrict__ w, con
 // Fused modified Gram-Schmidt of one Arnoldi step in a single cooperative
 // launch: ||w||^2 (+ non-finite flag), then for i = 0..j
 //   h_i = <v_i, w>;  w -= h_i v_i          (src/solver.cpp:58-62, same order)
-// and finally ||w||^2. Each block keeps its contiguous chunk of w in shared
-// memory for the whole sequence, each step streams v_i once; a grid-wide sync
-// separates a dot from its update. Every block folds all block partials in
-// index order, so h_i is bitwise identical everywhere and deterministic.
-__global__ void __launch_bounds__(RT, 2)
+// and finally ||w||^2. One block of kMgsThreads per SM keeps its contiguous
+// chunk of w in shared memory for the whole sequence; each thread owns the
+// chunk elements e = tid + k kMgsThreads and holds its slice of v_i in
+// registers: the pass that applies h_i v_i reads v_{i+1} for the next dot and
+// keeps it, so every basis vector is streamed from HBM exactly once per step
+// (the previous kernel re-read v_i). Block partials use a fixed shuffle
+// tree, and every block folds all block partials in index order, so h_i is
+// bitwise identical everywhere and run to run.
+constexpr int kMgsThreads = 512;
+constexpr int kMgsK = 18;  // elements per thread (N <= 148 x 9216)
+constexpr long long kMgsMaxChunk = static_cast<long long>(kMgsThreads) * kMgsK;  // 147 KB of w per block
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ c64 warp_sum(c64 v) {
+  for (int off = 16; off > 0; off >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, off);
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T block_sum_mgs(T v, T* sh) {  // result valid in thread 0
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  T t = zero_v<T>();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < kMgsThreads / 32 ? sh[threadIdx.x] : zero_v<T>();
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kMgsThreads, 1)
 mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, int j, long long n, long long chunk,
                  c64* __restrict__ h_out, double* __restrict__ norms, int* __restrict__ nonfinite,
                  c64* __restrict__ part_c, double* __restrict__ part_d, int do_pre) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   c64* ws = reinterpret_cast<c64*>(smem_raw);
-  __shared__ c64 shc[RT];
-  __shared__ double shd[RT];
+  __shared__ c64 shc[32];
+  __shared__ double shd[32];
   __shared__ c64 bcast_c;
   __shared__ double bcast_d;
-  const int G = gridDim.x;
+  const int G = gridDim.x, tid = threadIdx.x;
   const long long start = blockIdx.x * chunk;
   const int len = static_cast<int>(max(0LL, min(chunk, n - start)));
-  for (int e = threadIdx.x; e < len; e += RT) ws[e] = w[start + e];
+  for (int e = tid; e < len; e += kMgsThreads) ws[e] = w[start + e];
   __syncthreads();
 
   auto fold_d = [&](double v, double* slot) -> double {  // block partial -> grid total
-    const double b = block_reduce(v, shd);
-    if (threadIdx.x == 0) slot[blockIdx.x] = b;
+    const double b = block_sum_mgs(v, shd);
+    if (tid == 0) slot[blockIdx.x] = b;
     grid.sync();
-    if (threadIdx.x < 32) {
+    if (tid < 32) {
       double acc = 0.0;
-      for (int i = threadIdx.x; i < G; i += 32) acc += slot[i];
-      for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-      if (threadIdx.x == 0) bcast_d = acc;
+      for (int i = tid; i < G; i += 32) acc += slot[i];
+      acc = warp_sum(acc);
+      if (tid == 0) bcast_d = acc;
     }
     __syncthreads();
     return bcast_d;
+  };
+  auto fold_c = [&](c64 partial, int i) -> c64 {
+    const c64 b = block_sum_mgs(partial, shc);
+    c64* slot = part_c + (i & 1) * G;
+    if (tid == 0) slot[blockIdx.x] = b;
+    grid.sync();
+    if (tid < 32) {
+      c64 acc = cmk(0.0, 0.0);
+      for (int q = tid; q < G; q += 32) acc = cadd(acc, slot[q]);
+      acc = warp_sum(acc);
+      if (tid == 0) bcast_c = acc;
+    }
+    __syncthreads();
+    return bcast_c;
   };
 
   if (do_pre) {
     double s = 0.0;
     bool bad = false;
-    for (int e = threadIdx.x; e < len; e += RT) {
+    for (int e = tid; e < len; e += kMgsThreads) {
       const c64 v = ws[e];
       bad |= !isfinite(v.x) || !isfinite(v.y);
       s = fma(v.x, v.x, s);
@@ -341,82 +388,58 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
     }
     if (bad) atomicOr(nonfinite, 1);
     const double tot = fold_d(s, part_d);
-    if (blockIdx.x == 0 && threadIdx.x == 0) norms[0] = tot;
+    if (blockIdx.x == 0 && tid == 0) norms[0] = tot;
   }
 
-  // projection i: h_i = <v_i, w> (grid fold), then w -= h_i v_i. The update of
-  // projection i and the dot of projection i + 1 share one pass over the chunk
-  // (same per-thread order as two separate passes, so the same bits).
-  auto dot_pass = [&](const c64* vd, const c64* vu, c64 h) -> c64 {  // vu: update with h first (or null)
-    c64 s = cmk(0.0, 0.0);
-    int e = threadIdx.x;
-    for (; e + 3 * RT < len; e += 4 * RT) {
-      c64 a[4], b[4];
+  c64 vc[kMgsK];  // this thread's slice of v_i
+  {
+    const c64* v = V + start;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (vu) a[u] = vu[e + u * RT];
-        b[u] = vd[e + u * RT];
-      }
+    for (int k = 0; k < kMgsK; ++k) {
+      const int e = tid + k * kMgsThreads;
+      vc[k] = e < len ? v[e] : cmk(0.0, 0.0);
+    }
+  }
+  c64 s = cmk(0.0, 0.0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        c64 wv = ws[e + u * RT];
-        if (vu) {
-          wv = csub(wv, cmul(h, a[u]));
-          ws[e + u * RT] = wv;
-        }
-        s = cfma_conj(b[u], wv, s);
-      }
-    }
-    for (; e < len; e += RT) {
-      c64 wv = ws[e];
-      if (vu) {
-        wv = csub(wv, cmul(h, vu[e]));
-        ws[e] = wv;
-      }
-      s = cfma_conj(vd[e], wv, s);
-    }
-    return s;
-  };
-  auto fold_c = [&](c64 partial, int i) -> c64 {
-    const c64 b = block_reduce(partial, shc);
-    c64* slot = part_c + (i & 1) * G;
-    if (threadIdx.x == 0) slot[blockIdx.x] = b;
-    grid.sync();
-    if (threadIdx.x < 32) {
-      c64 acc = cmk(0.0, 0.0);
-      for (int q = threadIdx.x; q < G; q += 32) acc = cadd(acc, slot[q]);
-      for (int off = 16; off > 0; off >>= 1) {
-        acc.x += __shfl_down_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_down_sync(0xffffffffu, acc.y, off);
-      }
-      if (threadIdx.x == 0) bcast_c = acc;
-    }
-    __syncthreads();
-    return bcast_c;
-  };
-
-  c64 h = fold_c(dot_pass(V + start, nullptr, cmk(0.0, 0.0)), 0);
-  if (blockIdx.x == 0 && threadIdx.x == 0) h_out[0] = h;
+  for (int k = 0; k < kMgsK; ++k) {
+    const int e = tid + k * kMgsThreads;
+    if (e < len) s = cfma_conj(vc[k], ws[e], s);
+  }
+  c64 h = fold_c(s, 0);
+  if (blockIdx.x == 0 && tid == 0) h_out[0] = h;
   for (int i = 0; i < j; ++i) {
-    const c64* vi = V + static_cast<long long>(i) * ld + start;
-    const c64* vn = vi + ld;
-    h = fold_c(dot_pass(vn, vi, h), i + 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0) h_out[i + 1] = h;
+    // w -= h_i v_i (v_i from registers) and the partial <v_{i+1}, w> in one pass;
+    // v_{i+1} is read from HBM once and stays in registers for the next step
+    const c64* v = V + static_cast<long long>(i + 1) * ld + start;
+    s = cmk(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < kMgsK; ++k) {
+      const int e = tid + k * kMgsThreads;
+      if (e < len) {
+        const c64 nx = v[e];
+        const c64 wv = csub(ws[e], cmul(h, vc[k]));
+        ws[e] = wv;
+        s = cfma_conj(nx, wv, s);
+        vc[k] = nx;
+      }
+    }
+    h = fold_c(s, i + 1);
+    if (blockIdx.x == 0 && tid == 0) h_out[i + 1] = h;
   }
-  {  // the last update, w -= h_j v_j
-    const c64* vj = V + static_cast<long long>(j) * ld + start;
-    for (int e = threadIdx.x; e < len; e += RT) ws[e] = csub(ws[e], cmul(h, vj[e]));
+  double q = 0.0;  // the last update, w -= h_j v_j, then ||w||^2 and the write-back
+#pragma unroll
+  for (int k = 0; k < kMgsK; ++k) {
+    const int e = tid + k * kMgsThreads;
+    if (e < len) {
+      const c64 wv = csub(ws[e], cmul(h, vc[k]));
+      q = fma(wv.x, wv.x, q);
+      q = fma(wv.y, wv.y, q);
+      w[start + e] = wv;
+    }
   }
-
-  double s = 0.0;
-  for (int e = threadIdx.x; e < len; e += RT) {
-    const c64 v = ws[e];
-    s = fma(v.x, v.x, s);
-    s = fma(v.y, v.y, s);
-    w[start + e] = v;
-  }
-  const double tot = fold_d(s, part_d + G);
-  if (blockIdx.x == 0 && threadIdx.x == 0) norms[1] = tot;
+  const double tot = fold_d(q, part_d + G);
+  if (blockIdx.x == 0 && tid == 0) norms[1] = tot;
 }
 
 // ---------------------------------------------------------------------------
@@ -628,7 +651,6 @@ cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y
   return cudaGetLastError();
 }
 namespace {
-constexpr long long kMgsMaxChunk = 6500;  // complex per block: 2 x (104 KB + 6 KB static) smem per SM
 }
 
 cudaError_t launch_b_sqnorm(const c64* w, long long ld, long long n, int G, const int* mask, const BatchScratch& bs,
@@ -674,30 +696,30 @@ cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, l
   return cudaGetLastError();
 }
 
-bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kRedBlocks) * kMgsMaxChunk; }
+bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kNumSMs) * kMgsMaxChunk; }
 
 cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
                              int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s) {
-  // cooperative launch: every block co-resident (2 per SM)
-  long long blocks = (n + 1023) / 1024;
-  if (blocks > kRedBlocks) blocks = kRedBlocks;
+  // cooperative launch: every block co-resident (one per SM)
+  long long blocks = (n + 1023) / 1024;  // >= 2 elements per thread before using more SMs
+  if (blocks > kNumSMs) blocks = kNumSMs;
   if (blocks < 1) blocks = 1;
   long long chunk = (n + blocks - 1) / blocks;
   if (chunk > kMgsMaxChunk) return cudaErrorInvalidValue;
   size_t smem = static_cast<size_t>(chunk) * sizeof(c64);
-  static size_t configured = 0;
-  if (smem > configured) {
+  static bool configured = false;
+  if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(mgs_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kMgsMaxChunk * sizeof(c64)));
     if (e != cudaSuccess) return e;
-    configured = kMgsMaxChunk * sizeof(c64);
+    configured = true;
   }
   int pre = do_pre ? 1 : 0;
   c64* pc = rs.partial_c;
   double* pd = rs.partial_d;
   void* args[] = {&w, const_cast<c64**>(&V), &ld, &j, &n, &chunk, &h_out, &norms, &nonfinite, &pc, &pd, &pre};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&mgs_fused_kernel), dim3(static_cast<unsigned>(blocks)),
-                                     dim3(RT), args, smem, s);
+                                     dim3(kMgsThreads), args, smem, s);
 }
 
 int cgs_blocks(long long n) {
