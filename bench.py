@@ -328,7 +328,7 @@ def run_ours(args):
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     ms, e2e_s, gmres_s = (float(v) for v in vals.cpu())
 
-    path, lat_sizes, spec_bytes, mode_pairs, sym_dev = op.near_path()
+    path, lat_sizes, spec_bytes, modes_per_block, sym_mask, sym_dev = op.near_path()
     # roofline of the dominant kernel. Direct path: the near-field DMMA GEMM,
     # algorithmic flops per launch; lattice path: the per-mode GEMV, HBM-bound,
     # algorithmic bytes per launch = the block spectrum + x_hat read + y_hat written
@@ -378,8 +378,8 @@ def run_ours(args):
             "config": {
                 "workload": desc, "n_dof_total": data.N, "n_dof_cell": data.n_dof, "lattice": list(data.counts),
                 "near_offsets": data.n_near, "far_offsets": data.n_far, "n_t": 4, "nrhs": 1,
-                "near_path": path, "near_lattice": list(lat_sizes), "near_mode_pairs": mode_pairs,
-                "near_inversion_deviation": sym_dev,
+                "near_path": path, "near_lattice": list(lat_sizes), "near_modes_per_block": modes_per_block,
+                "near_symmetries": [g for g in range(1, 8) if sym_mask >> g & 1], "near_symmetry_deviation": sym_dev,
                 "parallelism": (f"near-field {'modes' if path == 'lattice' else 'pairs'} split over {world} GPUs "
                                 f"(rank 0 {hi - lo if path == 'lattice' else n_pairs}, {far_pairs:.0f} fewer for its "
                                 "far field) + NCCL all-reduce of y" if strong

@@ -97,12 +97,14 @@ typedef struct {
                                     `device` (e.g. from fpbem_cu_m2l_bank)                 */
   int near_path;                 /* FPBEM_CU_NEAR_*: how the Toeplitz near field S p is
                                     applied (same product, different arithmetic order)    */
-  const int* cell_inversion;     /* optional (extension): n_dof permutation P of the cell's
-                                    elements under the point reflection about the cell
-                                    centre, or NULL. When the device verifies
-                                    S_-o[P i, P j] == S_o[i, j] (to 1e-12 max |S|) the
-                                    lattice near field streams one block per mode pair
-                                    (q, -q)                                               */
+  int n_sym;                     /* optional (extension): cell symmetries, 0 if none      */
+  const int* sym_axes;           /* n_sym axis-sign maps g in 1..7: bit d flips axis d
+                                    about the cell centre (mirrors, half-turns, inversion) */
+  const int* sym_perms;          /* n_sym x n_dof: element j -> its image under g. Every g
+                                    the device verifies (S_{A_g o}[P i, P j] == S_o[i, j]
+                                    to 1e-12 max |S|, A_g o = o with the flipped axes
+                                    negated) lets the lattice near field store one block
+                                    per orbit of Fourier modes                             */
 } fpbem_cu_fmm_desc;
 
 #define FPBEM_CU_NEAR_AUTO 0       /* cost model picks (fpbem_cu_fmm_near_path reports it)   */
@@ -203,12 +205,13 @@ int fpbem_cu_gmres_fn(int device, long long n, fpbem_cu_apply_fn apply, void* ap
  * (S blocks + spectrum + U0 + V0). */
 int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes);
 /* The near-field path in use (FPBEM_CU_NEAR_DIRECT / _LATTICE), its lattice
- * sizes (1,1,1 for direct), the device bytes of its stored block spectrum,
- * whether mode pairs (q, -q) share a block (cell inversion verified), and the
- * measured symmetry deviation max|S_-o[P i, P j] - S_o[i, j]| / max|S| (-1 when
- * no inversion was given). */
-int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes, int* paired,
-                           double* symmetry_dev);
+ * sizes (1,1,1 for direct), the device bytes of its stored block spectrum, the
+ * largest number of Fourier modes one stored block serves (1 without verified
+ * symmetries), the verified symmetry mask (bit g) and the largest measured
+ * deviation max|S_{A_g o}[P i, P j] - S_o[i, j]| / max|S| over the given
+ * symmetries (-1 when none were given). */
+int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes, int* modes_per_block,
+                           int* symmetry_mask, double* symmetry_dev);
 
 /* Spectrum readback (sizes[3] always; lambda_out may be NULL). */
 int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out);

@@ -56,7 +56,9 @@ class FmmDesc(C.Structure):
         ("blocks_on_device", C.c_int),
         ("far_on_device", C.c_int),
         ("near_path", C.c_int),
-        ("cell_inversion", C.c_void_p),
+        ("n_sym", C.c_int),
+        ("sym_axes", C.c_void_p),
+        ("sym_perms", C.c_void_p),
     ]
 
 
@@ -111,7 +113,8 @@ def cuda() -> C.CDLL:
                                             C.c_int, C.c_int, C.c_int, c_int_p, c_int_p, c_double_p, C.c_int,
                                             c_int_p]),
             "fpbem_cu_fmm_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
-            "fpbem_cu_fmm_near_path": (C.c_int, [vp, c_int_p, c_int_p, C.POINTER(C.c_size_t), c_int_p, c_double_p]),
+            "fpbem_cu_fmm_near_path": (C.c_int, [vp, c_int_p, c_int_p, C.POINTER(C.c_size_t), c_int_p, c_int_p,
+                                                 c_double_p]),
             "fpbem_cu_spectrum": (C.c_int, [vp, c_int_p, vp]),
             "fpbem_cu_set_stream": (C.c_int, [vp, vp]),
             "fpbem_cu_enable_stage_timing": (C.c_int, [vp, C.c_int]),
@@ -173,6 +176,7 @@ def host() -> C.CDLL:
             "fh_insertion_loss": (C.c_int, [C.c_int, vp, vp, vp]),
             "fh_scene_dense": (C.c_int, [vp, vp]),
             "fh_scene_cell": (C.c_int, [vp, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p, c_int_p]),
+            "fh_cell_symmetries": (C.c_int, [vp, c_int_p]),
             "fh_interaction_block": (C.c_int, [vp, c_double_p, C.c_int, vp]),
             "fh_classify": (C.c_int, [vp, c_int_p, c_int_p, c_int_p, c_int_p, C.c_int, c_double_p]),
             "fh_fmm_assemble": (vp, [vp, C.c_int, C.c_int]),

@@ -79,7 +79,7 @@ void set_partition(fpbem_cu_op* op, int rank, int nranks, double far_pairs) {
   op->rank = rank;
   op->nranks = nranks;
   if (op->near_fft) {  // units are the stored blocks of the near-field lattice (one n x n block stream each)
-    pair_range(static_cast<long long>(op->items_h.size()), nranks, rank, far_pairs, op->mode_lo, op->mode_hi);
+    pair_range(op->n_items, nranks, rank, far_pairs, op->mode_lo, op->mode_hi);
     op->mjobs_nrhs = -1;
     return;
   }
@@ -138,11 +138,11 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
 void build_mode_jobs(fpbem_cu_op* op, int nrhs) {
   if (op->mjobs_nrhs == nrhs) return;
   std::vector<int4> jobs;
-  for (long long t = op->mode_lo; t < op->mode_hi; ++t) {
-    const int2 it = op->items_h[t];
-    tile_columns(jobs, static_cast<int>(t), nrhs, it.x, true);
-    if (it.y >= 0) tile_columns(jobs, static_cast<int>(t), nrhs, it.y, true, 1 << 12);  // mirror: through P
-  }
+  for (long long t = op->mode_lo; t < op->mode_hi; ++t)
+    for (int i = 0; i < 8; ++i) {  // one column set per image mode; g != 0: through P_g (job bits 12-14)
+      const int q = op->items_q[t * 8 + i];
+      if (q >= 0) tile_columns(jobs, static_cast<int>(t), nrhs, q, true, op->items_g[t * 8 + i] << 12);
+    }
   if (static_cast<int>(jobs.size()) > op->mjobs_cap) {
     if (op->mjobs) cudaFree(op->mjobs);
     op->mjobs = dalloc<int4>(jobs.size(), "mode jobs");
@@ -196,26 +196,16 @@ void build_near_spectrum(fpbem_cu_op* op, int n_toeplitz) {
           "near spectrum dft z");
     std::swap(cur, nxt);
   }
-  // work items: (q, -q) pairs sharing Shat_q when the inversion was verified, else every mode
-  op->items_h.clear();
-  for (long long q = 0; q < op->qn; ++q) {
-    if (!op->near_pair) {
-      op->items_h.push_back(make_int2(static_cast<int>(q), -1));
-      continue;
-    }
-    const long long qx = q % Lx, qy = (q / Lx) % Ly, qz = q / (Lx * Ly);
-    const long long qm = (((Lz - qz) % Lz) * Ly + (Ly - qy) % Ly) * Lx + (Lx - qx) % Lx;
-    if (q < qm) op->items_h.push_back(make_int2(static_cast<int>(q), static_cast<int>(qm)));
-    if (q == qm) op->items_h.push_back(make_int2(static_cast<int>(q), -1));
-  }
-  const size_t n_items = op->items_h.size();
-  op->items = dalloc<int2>(n_items, "near items");
-  h2d(op->items, op->items_h.data(), n_items * sizeof(int2), op->stream, "near items");
-  if (op->near_pair) {  // keep only the blocks of the items' first modes
-    c64* compact = dalloc<c64>(n_items * nn, "near spectrum (pairs)");
+  // work items: one per orbit of modes under the verified symmetries (one per mode without)
+  const size_t n_items = static_cast<size_t>(op->n_items);
+  op->items = dalloc<int>(n_items * 16, "near items");
+  h2d(op->items, op->items_q.data(), n_items * 8 * sizeof(int), op->stream, "near items");
+  h2d(op->items + n_items * 8, op->items_g.data(), n_items * 8 * sizeof(int), op->stream, "near items");
+  if (op->near_nimg > 1) {  // keep only the blocks of the orbits' representatives
+    c64* compact = dalloc<c64>(n_items * nn, "near spectrum (orbits)");
     DevPtr keep_c(compact, &cudaFree);
     for (size_t t = 0; t < n_items; ++t)
-      check(cudaMemcpyAsync(compact + t * nn, cur + static_cast<size_t>(op->items_h[t].x) * nn, nn * sizeof(c64),
+      check(cudaMemcpyAsync(compact + t * nn, cur + static_cast<size_t>(op->items_q[t * 8]) * nn, nn * sizeof(c64),
                             cudaMemcpyDeviceToDevice, op->stream),
             "near spectrum compaction");
     check(cudaStreamSynchronize(op->stream), "near spectrum compaction");
@@ -230,49 +220,102 @@ void build_near_spectrum(fpbem_cu_op* op, int n_toeplitz) {
   op->shat = cur;
 }
 
-// Cell-inversion pairing: with P from the caller, every near
-// offset's mirror -o stored, and S_-o[P i, P j] == S_o[i, j] on the device to
-// 1e-12 of max |S|, Shat_-q = P Shat_q P and the lattice path stores / streams
-// one block per mode pair. Sets near_pair and near_sym_dev.
-void check_inversion(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
-  op->near_pair = false;
+// Cell symmetries: every axis-sign map g the caller gives
+// with its element permutation P_g is kept when the offset set is closed under
+// A_g and S_{A_g o}[P_g i, P_g j] == S_o[i, j] on the device to 1e-12 of
+// max |S|; the kept set is reduced to a group. Sets near_sym_mask / _dev.
+void check_symmetries(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
+  op->near_sym_mask = 1;
   op->near_sym_dev = -1.0;
-  if (!d->cell_inversion || d->n_near == 0) return;
-  std::vector<char> seen(op->n, 0);
-  for (int i = 0; i < op->n; ++i) {
-    const int p = d->cell_inversion[i];
-    if (p < 0 || p >= op->n || seen[p]) fail(FPBEM_CU_EINVAL, "create: cell_inversion is not a permutation");
-    seen[p] = 1;
-  }
-  std::vector<int> mirror(d->n_near, -1);
-  for (int s = 0; s < d->n_near; ++s)
-    for (int t = 0; t < d->n_near && mirror[s] < 0; ++t)
-      if (op->near_offsets[3 * t] == -op->near_offsets[3 * s] &&
-          op->near_offsets[3 * t + 1] == -op->near_offsets[3 * s + 1] &&
-          op->near_offsets[3 * t + 2] == -op->near_offsets[3 * s + 2])
-        mirror[s] = t;
-  for (int s = 0; s < d->n_near; ++s)
-    if (mirror[s] < 0) return;  // offset set not symmetric
+  if (d->n_sym <= 0 || !d->sym_axes || !d->sym_perms || d->n_near == 0) return;
   using DevPtr = std::unique_ptr<void, decltype(&cudaFree)>;
-  int* dm = dalloc<int>(mirror.size(), "mirror slots");
+  if (!op->perm) op->perm = dalloc<int>(static_cast<size_t>(7) * op->n, "cell symmetries");
+  int* dm = dalloc<int>(d->n_near, "symmetry slots");
   DevPtr keep_m(dm, &cudaFree);
-  h2d(dm, mirror.data(), mirror.size() * sizeof(int), op->stream, "mirror slots");
-  if (!op->perm) {
-    op->perm = dalloc<int>(op->n, "cell inversion");
-    h2d(op->perm, d->cell_inversion, op->n * sizeof(int), op->stream, "cell inversion");
-  }
   unsigned long long* dv = dalloc<unsigned long long>(2, "symmetry check");
   DevPtr keep_dv(dv, &cudaFree);
-  check(cudaMemsetAsync(dv, 0, 2 * sizeof(unsigned long long), op->stream), "symmetry check");
-  check(launch_near_symmetry(op->S, op->n, d->n_near, dm, op->perm, dv, op->stream), "symmetry check");
-  unsigned long long hv[2];
-  check(cudaMemcpyAsync(hv, dv, sizeof(hv), cudaMemcpyDeviceToHost, op->stream), "symmetry check");
-  check(cudaStreamSynchronize(op->stream), "symmetry check");
-  double dev, amax;
-  std::memcpy(&dev, &hv[0], sizeof(double));
-  std::memcpy(&amax, &hv[1], sizeof(double));
-  op->near_sym_dev = amax > 0.0 ? dev / amax : 0.0;
-  op->near_pair = amax > 0.0 && dev <= 1e-12 * amax;
+  double worst = 0.0;
+  int mask = 1;
+  for (int u = 0; u < d->n_sym; ++u) {
+    const int g = d->sym_axes[u];
+    if (g < 1 || g > 7) fail(FPBEM_CU_EINVAL, "create: sym_axes entries must be in 1..7");
+    const int* pg = d->sym_perms + static_cast<size_t>(u) * op->n;
+    std::vector<char> seen(op->n, 0);
+    for (int i = 0; i < op->n; ++i) {
+      if (pg[i] < 0 || pg[i] >= op->n || seen[pg[i]]) fail(FPBEM_CU_EINVAL, "create: sym_perms row is not a permutation");
+      seen[pg[i]] = 1;
+    }
+    std::vector<int> mirror(d->n_near, -1);  // slot of A_g o
+    bool closed = true;
+    for (int s = 0; s < d->n_near && closed; ++s) {
+      int o[3];
+      for (int k = 0; k < 3; ++k) o[k] = (g >> k & 1) ? -op->near_offsets[3 * s + k] : op->near_offsets[3 * s + k];
+      for (int t = 0; t < d->n_near && mirror[s] < 0; ++t)
+        if (op->near_offsets[3 * t] == o[0] && op->near_offsets[3 * t + 1] == o[1] && op->near_offsets[3 * t + 2] == o[2])
+          mirror[s] = t;
+      closed = mirror[s] >= 0;
+    }
+    if (!closed) continue;
+    int* prow = op->perm + static_cast<size_t>(g - 1) * op->n;
+    h2d(prow, pg, op->n * sizeof(int), op->stream, "cell symmetry");
+    h2d(dm, mirror.data(), mirror.size() * sizeof(int), op->stream, "symmetry slots");
+    check(cudaMemsetAsync(dv, 0, 2 * sizeof(unsigned long long), op->stream), "symmetry check");
+    check(launch_near_symmetry(op->S, op->n, d->n_near, dm, prow, dv, op->stream), "symmetry check");
+    unsigned long long hv[2];
+    check(cudaMemcpyAsync(hv, dv, sizeof(hv), cudaMemcpyDeviceToHost, op->stream), "symmetry check");
+    check(cudaStreamSynchronize(op->stream), "symmetry check");
+    double dev, amax;
+    std::memcpy(&dev, &hv[0], sizeof(double));
+    std::memcpy(&amax, &hv[1], sizeof(double));
+    const double rel = amax > 0.0 ? dev / amax : (dev > 0.0 ? 1.0 : 0.0);
+    worst = std::max(worst, rel);
+    if (amax > 0.0 && dev <= 1e-12 * amax) mask |= 1 << g;
+  }
+  for (bool changed = true; changed;) {  // a group: drop g whose products leave the set
+    changed = false;
+    for (int g1 = 1; g1 < 8; ++g1)
+      for (int g2 = 1; g2 < 8; ++g2)
+        if ((mask >> g1 & 1) && (mask >> g2 & 1) && !(mask >> (g1 ^ g2) & 1)) {
+          mask &= ~(1 << std::max(g1, g2));
+          changed = true;
+        }
+  }
+  op->near_sym_mask = mask;
+  op->near_sym_dev = worst;
+}
+
+// Orbits of the Ln modes under the verified symmetries: items_q / items_g
+// (8 slots per item, representative = smallest mode first), n_items, near_nimg.
+void build_items(fpbem_cu_op* op, const int Ln[3]) {
+  const long long qn = static_cast<long long>(Ln[0]) * Ln[1] * Ln[2];
+  op->items_q.clear();
+  op->items_g.clear();
+  op->near_nimg = 1;
+  std::vector<char> seen(qn, 0);
+  for (long long q = 0; q < qn; ++q) {
+    if (seen[q]) continue;
+    const long long c[3] = {q % Ln[0], (q / Ln[0]) % Ln[1], q / (static_cast<long long>(Ln[0]) * Ln[1])};
+    int slot = 0;
+    int qs[8], gs[8];
+    for (int g = 0; g < 8; ++g) {
+      if (!(op->near_sym_mask >> g & 1)) continue;
+      long long m[3];
+      for (int k = 0; k < 3; ++k) m[k] = (g >> k & 1) ? (Ln[k] - c[k]) % Ln[k] : c[k];
+      const long long qi = (m[2] * Ln[1] + m[1]) * Ln[0] + m[0];
+      if (seen[qi]) continue;  // this mode already has an image (or is q itself)
+      seen[qi] = 1;
+      qs[slot] = static_cast<int>(qi);
+      gs[slot] = g;
+      ++slot;
+    }
+    for (int i = 0; i < 8; ++i) {
+      op->items_q.push_back(i < slot ? qs[i] : -1);
+      op->items_g.push_back(i < slot ? gs[i] : 0);
+    }
+    op->near_nimg = std::max(op->near_nimg, slot);
+  }
+  op->n_items = static_cast<long long>(op->items_q.size() / 8);
+  while (op->near_nimg & (op->near_nimg - 1)) ++op->near_nimg;  // 1, 2, 4 or 8 (kernel instances)
 }
 
 // Lattice-path near field: y = (1/qn) IDFT(Shat . DFT(x)) truncated to the M
@@ -298,12 +341,12 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
   if (Lz > 1) fwd(2, r, Mz, Lz, static_cast<long long>(Ly) * Lx * n);
   c64* yh = bufs[which];
   which ^= 1;
-  if (op->mode_lo > 0 || op->mode_hi < static_cast<long long>(op->items_h.size()))
+  if (op->mode_lo > 0 || op->mode_hi < op->n_items)
     check(cudaMemsetAsync(yh, 0, static_cast<size_t>(r * op->qn * n) * sizeof(c64), s), "near spectrum clear");
   ev_record(op, 7, s);
-  if (nrhs <= (op->near_pair ? kModeGemvMaxRhsPaired : kModeGemvMaxRhs)) {
-    check(launch_mode_gemv(op->shat, op->items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi, op->qn, nrhs,
-                           op->near_pair, s),
+  if (nrhs * op->near_nimg <= kModeGemvMaxAcc) {
+    check(launch_mode_gemv(op->shat, op->items, op->n_items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi,
+                           op->qn, nrhs, op->near_nimg, s),
           "near mode gemv");
   } else {
     build_mode_jobs(op, nrhs);
@@ -571,7 +614,7 @@ double calibrate_far_pairs(fpbem_cu_op* op) {
     }
   }
   set_partition(op, rank, nranks, far_pairs);
-  const double units = op->near_fft ? static_cast<double>(op->items_h.size()) : static_cast<double>(op->n_pairs);
+  const double units = op->near_fft ? static_cast<double>(op->n_items) : static_cast<double>(op->n_pairs);
   return best_near > 0.0f ? static_cast<double>(best_far) / best_near * units : 0.0;
 }
 
@@ -676,9 +719,8 @@ void choose_near_path(fpbem_cu_op* op, const fpbem_cu_fmm_desc* d) {
     qn *= Ln[k];
   }
   const double nn = static_cast<double>(op->n) * op->n;
-  // stored blocks: one per mode, or one per mode pair (q, -q) with a verified inversion
-  const double blocks = op->near_pair ? 0.5 * static_cast<double>(qn) : static_cast<double>(qn);
-  const double spec_bytes = 16.0 * nn * blocks;
+  build_items(op, Ln);  // stored blocks: one per orbit of modes under the verified symmetries
+  const double spec_bytes = 16.0 * nn * static_cast<double>(op->n_items);
   bool use = path == FPBEM_CU_NEAR_LATTICE;
   if (path == FPBEM_CU_NEAR_AUTO && possible) {
     const double r = op->max_rhs;
@@ -877,7 +919,7 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
                      &op->lambda_hat);
     }
 
-    if (d->n_near > 0 && op->n_hat == 0) check_inversion(op, d);
+    if (d->n_near > 0 && op->n_hat == 0) check_symmetries(op, d);
     choose_near_path(op, d);
     if (op->near_fft) {
       build_near_spectrum(op, d->n_near);
@@ -888,9 +930,7 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
       check(cudaMemsetAsync(op->zero_ptr, 0, (static_cast<size_t>(op->n_cells) + 1) * sizeof(int), op->stream),
             "zero csr");
       op->mode_lo = 0;
-      op->mode_hi = static_cast<long long>(op->items_h.size());
-    } else {
-      op->near_pair = false;
+      op->mode_hi = op->n_items;
     }
 
     // apply buffers
@@ -986,16 +1026,17 @@ int fpbem_cu_fmm_bytes(const fpbem_cu_op* op, size_t* bytes) {
   return FPBEM_CU_OK;
 }
 
-int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes, int* paired,
-                           double* symmetry_dev) {
-  if (!op || !path || !sizes || !spectrum_bytes || !paired || !symmetry_dev) {
+int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t* spectrum_bytes, int* modes_per_block,
+                           int* symmetry_mask, double* symmetry_dev) {
+  if (!op || !path || !sizes || !spectrum_bytes || !modes_per_block || !symmetry_mask || !symmetry_dev) {
     g_err = "near_path: null argument";
     return FPBEM_CU_EINVAL;
   }
   *path = op->near_fft ? FPBEM_CU_NEAR_LATTICE : FPBEM_CU_NEAR_DIRECT;
   for (int k = 0; k < 3; ++k) sizes[k] = op->near_fft ? op->Ln[k] : 1;
-  *spectrum_bytes = op->near_fft ? op->items_h.size() * op->n * op->n * sizeof(c64) : 0;
-  *paired = op->near_fft && op->near_pair;
+  *spectrum_bytes = op->near_fft ? static_cast<size_t>(op->n_items) * op->n * op->n * sizeof(c64) : 0;
+  *modes_per_block = op->near_fft ? op->near_nimg : 1;
+  *symmetry_mask = op->near_sym_mask;
   *symmetry_dev = op->near_sym_dev;
   return FPBEM_CU_OK;
 }

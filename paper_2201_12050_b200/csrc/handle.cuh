@@ -127,14 +127,17 @@ struct fpbem_cu_op {
   int* zero_ptr = nullptr;  // n_cells + 1 zeros: the L2P-only reduction
   int4* mjobs = nullptr;    // DMMA jobs over this rank's items (many right-hand sides)
   int mjobs_nrhs = -1, n_mjobs = 0, mjobs_cap = 0;
-  // stored blocks = work items (q, qm): with a verified cell inversion P
-  // (S_-o = P S_o P) one block serves mode q and, through P,
-  // its mirror qm = -q; otherwise every mode is an item (qm = -1)
-  bool near_pair = false;
-  double near_sym_dev = -1.0;  // max |S_-o[P i, P j] - S_o[i, j]| / max |S| (-1: not checked)
-  int* perm = nullptr;
-  int2* items = nullptr;
-  std::vector<int2> items_h;
+  // stored blocks = work items = orbits of Fourier modes under the cell's
+  // verified axis-sign symmetries g (S_{A_g o} = P_g S_o P_g, so
+  // Shat(A_g q) = P_g Shat(q) P_g): one block per orbit serves
+  // up to 8 modes, the images through P_g; without symmetries every mode is an item
+  int near_sym_mask = 1;        // bit g: axis-sign map g verified (bit 0 = identity)
+  double near_sym_dev = -1.0;   // max over the given g of max|S_{A_g o}[P_g i, P_g j] - S_o[i, j]| / max|S|
+  int* perm = nullptr;          // device: P_g for g = 1..7 (row g - 1, n entries)
+  int near_nimg = 1;            // images per item (largest orbit): 1, 2, 4 or 8
+  int* items = nullptr;         // device: [n_items][8] modes (-1 unused), then [n_items][8] g (0 = identity)
+  std::vector<int> items_q, items_g;
+  long long n_items = 0;
   long long mode_lo = 0, mode_hi = 0;  // this rank's items
 
   // expansions and spectrum

@@ -12,16 +12,16 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
                               cudaStream_t stream, long long out_rhs_stride = 0, const int* perm = nullptr);
 // out_rhs_stride > 0: column (unit, rhs) lands at out[rhs * out_rhs_stride + unit * ldo] (rhs-major);
-// jobs with bit 12 of .z set gather B rows and scatter output rows through perm
-// near field as a lattice convolution: for items t in [t_lo, t_hi) = (q, qm),
-// yh[r][q] = shat_t xh[r][q] and, paired, yh[r][qm] = P shat_t P xh[r][qm];
-// nrhs <= kModeGemvMaxRhs (kModeGemvMaxRhsPaired) at stride q_stride * n
-constexpr int kModeGemvMaxRhs = 8;
-constexpr int kModeGemvMaxRhsPaired = 4;
-cudaError_t launch_mode_gemv(const c64* shat, const int2* items, const int* perm, const c64* xh, c64* yh, int n,
-                             long long t_lo, long long t_hi, long long q_stride, int nrhs, bool paired,
+// jobs with g = bits 12-14 of .z nonzero gather B rows and scatter output rows through
+// perm + (g - 1) * K (the lattice near field's symmetry images)
+// near field as a lattice convolution, items t in [t_lo, t_hi): for each image
+// (q_i, g_i) of the item (items[t*8 + i], items[(n_items + t)*8 + i]),
+// yh[r][q_i] = P_g shat_t P_g xh[r][q_i]; nrhs * nimg <= kModeGemvMaxAcc
+constexpr int kModeGemvMaxAcc = 8;
+cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
+                             c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
                              cudaStream_t stream);
-// cell-inversion check: out2[0] = max |S_mirror[s][P i, P j] - S_s[i, j]|, out2[1] = max |S| (double bits)
+// cell-symmetry check: out2[0] = max |S_mirror[s][P i, P j] - S_s[i, j]|, out2[1] = max |S| (double bits)
 cudaError_t launch_near_symmetry(const c64* S, int n, int n_blk, const int* mirror, const int* perm,
                                  unsigned long long* out2, cudaStream_t stream);
 // y += U0 L per (cell, rhs) (the lattice path's L2P; bitwise = the reduction with no pairs)

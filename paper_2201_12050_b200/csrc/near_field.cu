@@ -144,9 +144,10 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   const int m0 = static_cast<int>(blockIdx.x % m_tiles) * BM;
   const int4 job = jobs[blockIdx.x / m_tiles];  // (block slot, first column, count | class << 8, pair base)
   const int s = job.x, col0 = job.y, ncols = job.z & 0xff, cls = (job.z >> 8) & 0xf, pair_base = job.w;
-  // mirrored-mode tile of the lattice near field: rows of B gathered and rows
-  // of the output scattered through the cell inversion P
-  const int* pk = (job.z >> 12) & 1 ? perm : nullptr;
+  // image-mode tile of the lattice near field: rows of B gathered and rows of
+  // the output scattered through the symmetry permutation P_g (g = bits 12-14)
+  const int gsym = (job.z >> 12) & 7;
+  const int* pk = gsym ? perm + static_cast<size_t>(gsym - 1) * K : nullptr;
 
   if (tid < BN) {
     if (tid < ncols) {
@@ -215,44 +216,49 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
 // per row, the k loop in fixed ascending order (deterministic), the block read
 // once with 8 independent 16-byte loads in flight per thread, the RHS chunk
 // staged in shared memory. HBM-bound: 16 n^2 bytes per stored block.
-// Work item t = (q, qm): block t of the stored spectrum is Shat_q; with a cell
-// inversion P (S_-o = P S_o P, so Shat_-q = P Shat_q P) the
-// same stream also gives yh[qm = -q] = P Shat_q P xh[qm]: the second set of
-// accumulators reads xh[qm] gathered through P and its rows land at P[i].
+// Work item t = an orbit of modes under the cell's verified symmetries: block
+// t of the stored spectrum is Shat(q_0), and image mode q_i = A_g q_0 has
+// Shat(q_i) = P_g Shat(q_0) P_g, so the same stream also gives
+// yh[q_i] = P_g Shat(q_0) P_g xh[q_i]: image i's accumulators read xh[q_i]
+// gathered through P_g and its rows land at P_g[row].
 constexpr int GEMV_THREADS = 128;
 constexpr int GEMV_KC = 256;  // k chunk of xh staged in shared memory
 constexpr int GEMV_U = 8;     // independent Shat loads per thread
 
-template <int R, bool kPair>
+template <int R, int NI>
 __global__ void __launch_bounds__(GEMV_THREADS)
-near_mode_gemv_kernel(const c64* __restrict__ shat, const int2* __restrict__ items, const int* __restrict__ perm,
-                      const c64* __restrict__ xh, c64* __restrict__ yh, int n, long long t_lo, long long q_stride,
-                      int row_tiles) {
-  constexpr int S = kPair ? 2 : 1;
-  __shared__ c64 xs[S * R][GEMV_KC];
+near_mode_gemv_kernel(const c64* __restrict__ shat, const int* __restrict__ items, long long n_items,
+                      const int* __restrict__ perm, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
+                      long long t_lo, long long q_stride, int row_tiles) {
+  constexpr int A = NI * R;  // accumulators per thread
+  __shared__ c64 xs[A][GEMV_KC];
+  __shared__ int iq[8], ig[8];
   const long long t = t_lo + blockIdx.x / row_tiles;
-  const int2 it = items[t];
-  const long long q = it.x, qm = kPair ? it.y : -1;
+  if (threadIdx.x < 8) {
+    iq[threadIdx.x] = items[t * 8 + threadIdx.x];
+    ig[threadIdx.x] = items[(n_items + t) * 8 + threadIdx.x];
+  }
   const int i = (blockIdx.x % row_tiles) * GEMV_THREADS + threadIdx.x;
   const bool row_ok = i < n;
   const size_t nn = static_cast<size_t>(n) * n;
   const c64* a = shat + static_cast<size_t>(t) * nn + (row_ok ? i : 0);
-  c64 acc[S * R];
+  c64 acc[A];
 #pragma unroll
-  for (int r = 0; r < S * R; ++r) acc[r] = cmk(0.0, 0.0);
+  for (int r = 0; r < A; ++r) acc[r] = cmk(0.0, 0.0);
   for (int k0 = 0; k0 < n; k0 += GEMV_KC) {
     const int kc = min(GEMV_KC, n - k0);
     __syncthreads();
-    for (int e = threadIdx.x; e < S * R * GEMV_KC; e += GEMV_THREADS) {
-      const int r = e / GEMV_KC, k = e % GEMV_KC;
+    for (int e = threadIdx.x; e < A * GEMV_KC; e += GEMV_THREADS) {
+      const int slot = e / GEMV_KC, k = e % GEMV_KC;
+      const int img = slot / R, r = slot % R;
+      const int q = iq[img];
       c64 v = cmk(0.0, 0.0);
-      if (k < kc) {
-        if (r < R)
-          v = xh[r * q_stride * n + q * n + k0 + k];
-        else if (qm >= 0)
-          v = xh[(r - R) * q_stride * n + qm * n + __ldg(perm + k0 + k)];
+      if (k < kc && q >= 0) {
+        const int g = ig[img];
+        const int kk = g ? __ldg(perm + static_cast<size_t>(g - 1) * n + k0 + k) : k0 + k;
+        v = xh[r * q_stride * n + static_cast<long long>(q) * n + kk];
       }
-      xs[r][k] = v;
+      xs[slot][k] = v;
     }
     __syncthreads();
     int k = 0;
@@ -263,21 +269,23 @@ near_mode_gemv_kernel(const c64* __restrict__ shat, const int2* __restrict__ ite
 #pragma unroll
       for (int u = 0; u < GEMV_U; ++u)
 #pragma unroll
-        for (int r = 0; r < S * R; ++r) acc[r] = cfma(v[u], xs[r][k + u], acc[r]);
+        for (int r = 0; r < A; ++r) acc[r] = cfma(v[u], xs[r][k + u], acc[r]);
     }
     for (; k < kc; ++k) {
       const c64 v = __ldcs(a + static_cast<size_t>(k0 + k) * n);
 #pragma unroll
-      for (int r = 0; r < S * R; ++r) acc[r] = cfma(v, xs[r][k], acc[r]);
+      for (int r = 0; r < A; ++r) acc[r] = cfma(v, xs[r][k], acc[r]);
     }
   }
   if (!row_ok) return;
 #pragma unroll
-  for (int r = 0; r < R; ++r) yh[r * q_stride * n + q * n + i] = acc[r];
-  if (kPair && qm >= 0) {
-    const int pi = __ldg(perm + i);
+  for (int img = 0; img < NI; ++img) {
+    const int q = iq[img];
+    if (q < 0) continue;
+    const int g = ig[img];
+    const int row = g ? __ldg(perm + static_cast<size_t>(g - 1) * n + i) : i;
 #pragma unroll
-    for (int r = 0; r < R; ++r) yh[r * q_stride * n + qm * n + pi] = acc[R + r];
+    for (int r = 0; r < R; ++r) yh[r * q_stride * n + static_cast<long long>(q) * n + row] = acc[img * R + r];
   }
 }
 
@@ -351,33 +359,35 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_mode_gemv(const c64* shat, const int2* items, const int* perm, const c64* xh, c64* yh, int n,
-                             long long t_lo, long long t_hi, long long q_stride, int nrhs, bool paired,
+cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
+                             c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
                              cudaStream_t stream) {
   if (t_hi <= t_lo) return cudaSuccess;
   const int row_tiles = (n + GEMV_THREADS - 1) / GEMV_THREADS;
   const long long blocks = (t_hi - t_lo) * row_tiles;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
   const dim3 grid(static_cast<unsigned>(blocks));
-  const int key = paired ? -nrhs : nrhs;
-  switch (key) {
-#define FPBEM_GEMV_CASE(R, P)                                                                                    \
-  case (P ? -R : R):                                                                                            \
-    near_mode_gemv_kernel<R, P><<<grid, GEMV_THREADS, 0, stream>>>(shat, items, perm, xh, yh, n, t_lo, q_stride, \
-                                                                   row_tiles);                                  \
+  switch (nimg * 16 + nrhs) {
+#define FPBEM_GEMV_CASE(R, NI)                                                                                   \
+  case NI * 16 + R:                                                                                             \
+    near_mode_gemv_kernel<R, NI><<<grid, GEMV_THREADS, 0, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, \
+                                                                    q_stride, row_tiles);                       \
     break;
-    FPBEM_GEMV_CASE(1, false)
-    FPBEM_GEMV_CASE(2, false)
-    FPBEM_GEMV_CASE(3, false)
-    FPBEM_GEMV_CASE(4, false)
-    FPBEM_GEMV_CASE(5, false)
-    FPBEM_GEMV_CASE(6, false)
-    FPBEM_GEMV_CASE(7, false)
-    FPBEM_GEMV_CASE(8, false)
-    FPBEM_GEMV_CASE(1, true)
-    FPBEM_GEMV_CASE(2, true)
-    FPBEM_GEMV_CASE(3, true)
-    FPBEM_GEMV_CASE(4, true)
+    FPBEM_GEMV_CASE(1, 1)
+    FPBEM_GEMV_CASE(2, 1)
+    FPBEM_GEMV_CASE(3, 1)
+    FPBEM_GEMV_CASE(4, 1)
+    FPBEM_GEMV_CASE(5, 1)
+    FPBEM_GEMV_CASE(6, 1)
+    FPBEM_GEMV_CASE(7, 1)
+    FPBEM_GEMV_CASE(8, 1)
+    FPBEM_GEMV_CASE(1, 2)
+    FPBEM_GEMV_CASE(2, 2)
+    FPBEM_GEMV_CASE(3, 2)
+    FPBEM_GEMV_CASE(4, 2)
+    FPBEM_GEMV_CASE(1, 4)
+    FPBEM_GEMV_CASE(2, 4)
+    FPBEM_GEMV_CASE(1, 8)
 #undef FPBEM_GEMV_CASE
     default: return cudaErrorInvalidValue;
   }

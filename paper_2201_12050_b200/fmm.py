@@ -139,7 +139,7 @@ class FmmOperators:
 
     def __init__(self, data, device: int = 0, fft_sizes=None, lambda_=None, max_rhs: int = 1, lambda_hat=None,
                  near_blocks=None, hat_blocks=None, far_blocks=None, far_hat_blocks=None, near_path: str = "auto",
-                 use_inversion: bool = True):
+                 use_symmetries: bool = True):
         lib = _native.cuda()
         self.counts = tuple(int(c) for c in data.counts)
         self.n_dof = int(data.n_dof)
@@ -184,8 +184,11 @@ class FmmOperators:
         d.mirrored_level = level
         d.max_rhs = max_rhs
         d.near_path = self.NEAR_PATHS[near_path]
-        inv = getattr(data, "cell_inversion", None)  # Scene.cell_inversion(): mode pairing (extension)
-        d.cell_inversion = ptr(inv, np.int32) if inv is not None and use_inversion else None
+        syms = getattr(data, "cell_symmetries", None) or []  # Scene.cell_symmetries(): mode orbits (extension)
+        if syms and use_symmetries:
+            d.n_sym = len(syms)
+            d.sym_axes = ptr(np.array([g for g, _ in syms], np.int32), np.int32)
+            d.sym_perms = ptr(np.stack([np.asarray(p, np.int32) for _, p in syms]), np.int32)
         if level >= 0:
             d.n_hat = int(len(data.hat_indices))
             d.hat_indices = ptr(data.hat_indices, np.int32)
@@ -225,13 +228,16 @@ class FmmOperators:
         _raise(_native.cuda().fpbem_cu_fmm_bytes(self._h, C.byref(b)))
         return int(b.value)
 
-    def near_path(self) -> tuple[str, tuple[int, int, int], int, bool, float]:
-        """(path, lattice sizes, stored spectrum bytes, mode pairs share blocks,
-        measured cell-inversion deviation / max|S| or -1) of the near field."""
-        p, sizes, nb, pr, dev = C.c_int(), (C.c_int * 3)(), C.c_size_t(), C.c_int(), C.c_double()
-        _raise(_native.cuda().fpbem_cu_fmm_near_path(self._h, C.byref(p), sizes, C.byref(nb), C.byref(pr),
-                                                     C.byref(dev)))
-        return {1: "direct", 2: "lattice"}[p.value], tuple(sizes), int(nb.value), bool(pr.value), dev.value
+    def near_path(self) -> tuple[str, tuple[int, int, int], int, int, int, float]:
+        """(path, lattice sizes, stored spectrum bytes, Fourier modes per stored
+        block (1 without verified symmetries), verified symmetry mask (bit g),
+        largest measured symmetry deviation / max|S| or -1) of the near field."""
+        p, sizes, nb, mpb, mask, dev = (C.c_int(), (C.c_int * 3)(), C.c_size_t(), C.c_int(), C.c_int(),
+                                        C.c_double())
+        _raise(_native.cuda().fpbem_cu_fmm_near_path(self._h, C.byref(p), sizes, C.byref(nb), C.byref(mpb),
+                                                     C.byref(mask), C.byref(dev)))
+        return ({1: "direct", 2: "lattice"}[p.value], tuple(sizes), int(nb.value), mpb.value, mask.value,
+                dev.value)
 
     def spectrum(self) -> tuple[tuple[int, int, int], np.ndarray]:
         sizes = (C.c_int * 3)()

@@ -169,43 +169,22 @@ class Scene:
             raise ValueError(_err())
         return d
 
-    def cell_inversion(self) -> np.ndarray | None:
-        """Element permutation P of the unit cell under the point reflection
-        about its bounding-box centre (P[j] = the element whose corners are j's
-        reflected corners), or None when the cell is not point-symmetric.
-        Extension: the lattice near field pairs Fourier modes
-        q and -q through it, after checking S_-o[P i, P j] = S_o[i, j] on the
-        device. Cached: translations of the cell do not change it."""
-        if hasattr(self, "_inversion"):
-            return self._inversion
-        self._inversion = self._find_inversion()
-        return self._inversion
-
-    def _find_inversion(self) -> np.ndarray | None:
-        c = self.cell()
-        cor, cen, nv = c["corners"], c["centroid"], c["nv"]
-        pts = cor.reshape(-1, 3)
-        lo, hi = pts.min(axis=0), pts.max(axis=0)
-        ctr = 0.5 * (lo + hi)
-        tol = 1e-9 * max(float(np.linalg.norm(hi - lo)), 1e-300)
-        ref = 2.0 * ctr - cen
-        n = len(cen)
-        perm = np.full(n, -1, np.int64)
-        for a in range(0, n, 512):
-            d = np.linalg.norm(cen[None, :, :] - ref[a:a + 512, None, :], axis=2)
-            k = d.argmin(axis=1)
-            ok = d[np.arange(len(k)), k] < tol
-            perm[a:a + 512] = np.where(ok, k, -1)
-        if (perm < 0).any() or (perm == np.arange(n)).any() or (perm[perm] != np.arange(n)).any():
-            return None
-        if (nv[perm] != nv).any():
-            return None
-        # reflected corner sets must match (triangles repeat their third corner)
-        rc = 2.0 * ctr - cor
-        kc = cor[perm]
-        if np.linalg.norm(rc[:, :, None, :] - kc[:, None, :, :], axis=3).min(axis=2).max() >= tol:
-            return None
-        return perm.astype(np.int32)
+    def cell_symmetries(self) -> list[tuple[int, np.ndarray]]:
+        """Axis sign maps g of the unit cell (bit d of g flips axis d about the
+        bounding-box centre: mirrors, half-turns, the inversion) that map the
+        mesh onto itself, with the element permutation P_g of each (P_g[j] =
+        the element whose corners are j's mapped corners); [] when the cell has
+        none. Extension: the lattice near field stores one
+        block per orbit of Fourier modes after checking
+        S_{A_g o}[P_g i, P_g j] = S_o[i, j] on the device. Cached."""
+        if not hasattr(self, "_symmetries"):
+            n = self.n_dof
+            perms = np.zeros((8, n), np.int32)
+            mask = _native.host().fh_cell_symmetries(self._h, _ip(perms))
+            if mask < 0:
+                raise ValueError(_err())
+            self._symmetries = [(g, perms[g].copy()) for g in range(1, 8) if mask >> g & 1]
+        return self._symmetries
 
     def interaction_block(self, shift, self_terms: bool) -> np.ndarray:
         n = self.n_dof
@@ -246,7 +225,7 @@ class Scene:
         if not h:
             raise ValueError(_err())
         data = FmmData(h)
-        data.cell_inversion = self.cell_inversion()
+        data.cell_symmetries = self.cell_symmetries()
         return data
 
 

@@ -190,6 +190,21 @@ int fh_scene_cell(void* hp, double* corners, double* centroid, double* normal, d
   });
 }
 
+// axis sign symmetries of the cell (cell_symmetries): returns the bitmask of
+// valid g (bit 0 = identity) and perms[g * n + j] = image of element j (valid g)
+int fh_cell_symmetries(void* hp, int* perms) {
+  int mask = -1;
+  const int rc = guarded([&] {
+    const Mesh& m = static_cast<SceneH*>(hp)->s.cell;
+    std::vector<std::vector<int>> perm;
+    mask = cell_symmetries(m, perm);
+    for (int g = 0; g < 8; ++g)
+      if (mask >> g & 1)
+        for (int j = 0; j < m.size(); ++j) perms[static_cast<size_t>(g) * m.size() + j] = perm[g][j];
+  });
+  return rc ? -1 : mask;
+}
+
 // rows = BIE-oriented cell collocation points shifted by `shift`, columns = cell elements
 int fh_interaction_block(void* hp, const double* shift, int self, double* out) {
   return guarded([&] {

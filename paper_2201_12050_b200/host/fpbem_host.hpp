@@ -82,8 +82,11 @@ struct Mesh {
 Mesh cube_sphere(double radius, int refinement, cd beta = {});           // geometry.cpp:67-109
 Mesh wall_cell(double ly, double lz, double t, int div, cd beta = {});    // geometry.cpp:111-135
 Mesh icosphere(double radius, int subdivisions, cd beta = {});            // extension
-// reflection partners of a point-symmetric mesh get reflected quadrature nodes (extension)
-void symmetrize_inversion(Mesh& m);
+// axis sign maps g (bit d flips axis d about the bbox centre) leaving the mesh invariant:
+// bitmask of valid g (bit 0 = identity), perm[g][j] = image element of j (extension)
+int cell_symmetries(const Mesh& m, std::vector<std::vector<int>>& perm);
+// images of each orbit's representative get the images of its quadrature nodes (extension)
+void symmetrize_group(Mesh& m);
 Mesh closed_cylinder(double radius, double height, int n_theta, int n_z, cd beta = {});  // extension
 Mesh closed_box(double lx, double ly, double lz, double h, bool split_triangles,
                 cd beta = {});  // extension; box [-lx/2,lx/2]x[-ly/2,ly/2]x[0,lz]

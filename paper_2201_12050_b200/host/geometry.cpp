@@ -46,50 +46,142 @@ Element make_tri(const V3& a, const V3& b, const V3& c, cd beta) {
   return e;
 }
 
-// Inversion-consistent corner order (extension). When the
-// cell mesh is symmetric under the point reflection x -> 2c - x about its
-// bounding-box centre c (every element's reflected corner set is an element of
-// the mesh, never itself), the reflection partner k = P(j) > j of element j
-// gets the reflected corners in the order (b', a', c') for a triangle (a, b, c)
-// and (b', a', d', c') for a quad (a, b, c, d): its bilinear element map is then
-// j's map reflected with u -> 1 - u, and since the Gauss nodes, the weights and
-// the 4-fold subdivision are symmetric under u -> 1 - u the two elements carry
-// reflected quadrature node sets. Every interaction then satisfies
-// S_{-o}[P i, P j] = S_o[i, j] up to rounding (normals flip, relative vectors
-// flip, all kernel terms are even in both), which the lattice near field uses
-// to stream each Fourier-mode block once for q and -q. The element order, the
-// corner sets and the orientation are unchanged; meshes without the symmetry
-// are left as they are.
-void symmetrize_inversion(Mesh& m) {
+// Symmetry-consistent corner order (extension). The axis
+// sign maps g (bit d of g flips axis d about the bounding-box centre; the 7
+// mirrors, pi-rotations and the inversion) under which the cell mesh is
+// invariant as a set of elements form a group; every orbit of elements gets
+// corners that are the images of its representative's corners, reordered
+// (b', a', [d', c'] / c') for orientation-reversing g, so the bilinear element
+// map of an image is the image of the representative's map composed with
+// u -> 1 - u. Gauss nodes, weights and the 4-fold subdivision are symmetric
+// under u -> 1 - u, so images carry the images of the representative's
+// quadrature nodes and every interaction satisfies
+// S_{A_g o}[P_g i, P_g j] = S_o[i, j] up to rounding (normals and relative
+// vectors map by g, all kernel terms are invariant). A representative fixed by
+// some g gets the corner rotation that g maps to itself (a triangle on a mirror
+// plane: the vertex on the plane last). The element order, the corner sets and
+// the orientation are unchanged; without a consistent choice the mesh is left
+// as it is. The lattice near field uses the symmetries after verifying them on
+// the assembled blocks.
+int cell_symmetries(const Mesh& m, std::vector<std::vector<int>>& perm) {
   const int n = m.size();
-  if (n < 2) return;
+  perm.assign(8, {});
+  if (n < 2) return 0;
   V3 lo, hi;
   m.bbox(lo, hi);
   const V3 ctr = 0.5 * (lo + hi);
   const double tol = 1e-9 * std::max(1e-300, norm(hi - lo));
-  auto refl = [&](const V3& p) { return 2.0 * ctr - p; };
-  std::vector<int> partner(n, -1);
-  for (int j = 0; j < n; ++j) {
-    const V3 r = refl(m.el[j].centroid);
-    for (int k = 0; k < n && partner[j] < 0; ++k)
-      if (m.el[k].nv == m.el[j].nv && norm(m.el[k].centroid - r) < tol) partner[j] = k;
-    const int k = partner[j];
-    if (k < 0 || k == j) return;  // not point-symmetric
-    for (int a = 0; a < m.el[j].nv; ++a) {  // the reflected corners are k's corners
-      bool found = false;
-      for (int b = 0; b < m.el[k].nv && !found; ++b) found = norm(m.el[k].c[b] - refl(m.el[j].c[a])) < tol;
-      if (!found) return;
+  auto img = [&](int g, const V3& p) {
+    V3 r = p;
+    for (int d = 0; d < 3; ++d)
+      if (g >> d & 1) r[d] = 2.0 * ctr[d] - p[d];
+    return r;
+  };
+  int valid = 1;
+  perm[0].resize(n);
+  for (int j = 0; j < n; ++j) perm[0][j] = j;
+  for (int g = 1; g < 8; ++g) {
+    std::vector<int> p(n, -1);
+    bool ok = true;
+    for (int j = 0; j < n && ok; ++j) {
+      const V3 r = img(g, m.el[j].centroid);
+      for (int k = 0; k < n && p[j] < 0; ++k)
+        if (m.el[k].nv == m.el[j].nv && norm(m.el[k].centroid - r) < tol) p[j] = k;
+      const int k = p[j];
+      ok = k >= 0;
+      for (int a = 0; a < m.el[j].nv && ok; ++a) {  // the image corners are k's corners
+        bool found = false;
+        for (int b = 0; b < m.el[k].nv && !found; ++b) found = norm(m.el[k].c[b] - img(g, m.el[j].c[a])) < tol;
+        ok = found;
+      }
+    }
+    if (ok) {
+      perm[g] = p;
+      valid |= 1 << g;
     }
   }
-  for (int j = 0; j < n; ++j)
-    if (partner[partner[j]] != j) return;
+  for (bool changed = true; changed;) {  // keep a group: drop g whose products leave the set
+    changed = false;
+    for (int g1 = 1; g1 < 8; ++g1)
+      for (int g2 = 1; g2 < 8; ++g2)
+        if ((valid >> g1 & 1) && (valid >> g2 & 1) && !(valid >> (g1 ^ g2) & 1)) {
+          valid &= ~(1 << std::max(g1, g2));
+          changed = true;
+        }
+  }
+  return valid;
+}
+
+void symmetrize_group(Mesh& m) {
+  std::vector<std::vector<int>> perm;
+  const int valid = cell_symmetries(m, perm);
+  if (valid <= 1) return;
+  const int n = m.size();
+  V3 lo, hi;
+  m.bbox(lo, hi);
+  const V3 ctr = 0.5 * (lo + hi);
+  const double tol = 1e-9 * std::max(1e-300, norm(hi - lo));
+  auto img = [&](int g, const V3& p) {
+    V3 r = p;
+    for (int d = 0; d < 3; ++d)
+      if (g >> d & 1) r[d] = 2.0 * ctr[d] - p[d];
+    return r;
+  };
+  auto reversing = [](int g) { return (__builtin_popcount(g) & 1) != 0; };
+  // corners of the image of an element with corners c[0..nv) under g
+  auto image = [&](int g, const std::array<V3, 4>& c, int nv) {
+    std::array<V3, 4> r;
+    if (reversing(g)) {
+      r = {img(g, c[1]), img(g, c[0]), img(g, nv == 3 ? c[2] : c[3]), img(g, c[2])};
+      if (nv == 3) r[3] = r[2];
+    } else {
+      r = {img(g, c[0]), img(g, c[1]), img(g, c[2]), img(g, c[3])};
+    }
+    return r;
+  };
+  auto same = [&](const std::array<V3, 4>& a, const std::array<V3, 4>& b, int nv, int shift) {
+    for (int k = 0; k < nv; ++k)
+      if (norm(a[k] - b[(k + shift) % nv]) >= tol) return false;
+    return true;
+  };
+  std::vector<std::array<V3, 4>> out(n);
+  std::vector<char> done(n, 0);
   for (int j = 0; j < n; ++j) {
-    const int k = partner[j];
-    if (k < j) continue;
+    if (done[j]) continue;
     const Element& e = m.el[j];
-    const cd beta = m.el[k].beta;
-    m.el[k] = e.nv == 3 ? make_tri(refl(e.c[1]), refl(e.c[0]), refl(e.c[2]), beta)
-                        : make_quad(refl(e.c[1]), refl(e.c[0]), refl(e.c[3]), refl(e.c[2]), beta);
+    const int nv = e.nv;
+    // the representative's corner rotation that its stabiliser maps to itself
+    // (a pi-rotation fixing a quad may also map it to its half-turn)
+    std::array<V3, 4> rep{};
+    bool found = false;
+    for (int rot = 0; rot < nv && !found; ++rot) {
+      std::array<V3, 4> c;
+      for (int k = 0; k < nv; ++k) c[k] = e.c[(k + rot) % nv];
+      if (nv == 3) c[3] = c[2];
+      bool ok = true;
+      for (int g = 1; g < 8 && ok; ++g)
+        if ((valid >> g & 1) && perm[g][j] == j) {
+          const std::array<V3, 4> im = image(g, c, nv);
+          ok = same(im, c, nv, 0) || (!reversing(g) && nv == 4 && same(im, c, nv, 2));
+        }
+      if (ok) {
+        rep = c;
+        found = true;
+      }
+    }
+    if (!found) return;  // no consistent choice: leave the mesh unchanged
+    for (int g = 0; g < 8; ++g) {
+      if (!(valid >> g & 1)) continue;
+      const int k = perm[g][j];
+      if (done[k]) continue;
+      out[k] = g == 0 ? rep : image(g, rep, nv);
+      done[k] = 1;
+    }
+  }
+  for (int k = 0; k < n; ++k) {
+    const Element& e = m.el[k];
+    const auto& c = out[k];
+    m.el[k] = e.nv == 3 ? make_tri(c[0], c[1], c[2], e.beta) : make_quad(c[0], c[1], c[2], c[3], e.beta);
   }
 }
 
@@ -195,7 +287,7 @@ Mesh icosphere(double radius, int subdivisions, cd beta) {
     if (dot(cross(b - a, c - a), a + b + c) < 0.0) std::swap(b, c);
     m.el.push_back(make_tri(a, b, c, beta));
   }
-  symmetrize_inversion(m);
+  symmetrize_group(m);
   return m;
 }
 
@@ -231,7 +323,7 @@ Mesh closed_cylinder(double radius, double height, int n_theta, int n_z, cd beta
     m.el.push_back(make_tri(bottom, ring(i + 1, 0.0), ring(i, 0.0), beta));      // normal -z
     m.el.push_back(make_tri(top, ring(i, height), ring(i + 1, height), beta));   // normal +z
   }
-  symmetrize_inversion(m);
+  symmetrize_group(m);
   return m;
 }
 
@@ -266,7 +358,7 @@ Mesh closed_box(double lx, double ly, double lz, double h, bool split, cd beta) 
           }
         }
     }
-  symmetrize_inversion(m);
+  symmetrize_group(m);
   return m;
 }
 

@@ -45,9 +45,9 @@ def test_lattice_near_field_matches_oracle_and_direct(ops, counts, n):
     rng = np.random.default_rng(n + 3 * counts[0] + 5 * counts[1] + 7 * counts[2])
     d = toeplitz_only(rng, counts, n)
     lat = ops(d, near_path="lattice")
-    path, sizes, nbytes, paired, dev = lat.near_path()
+    path, sizes, nbytes, per_block, mask, dev = lat.near_path()
     R = np.abs(d.near_offsets).max(axis=0)
-    assert path == "lattice" and not paired and dev == -1.0
+    assert path == "lattice" and per_block == 1 and mask == 1 and dev == -1.0
     assert sizes == tuple(int(m + r) if m > 1 else 1 for m, r in zip(counts, R))
     assert nbytes == 16 * n * n * int(np.prod(sizes))
     p = uvec(rng, d.N)
@@ -87,20 +87,21 @@ def test_lattice_fmm_matvec_matches_oracle(ops, assembled, cid, var):
     assert rel(op.matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("nrhs,inv", [(2, True), (4, True), (5, True), (8, True), (9, True), (16, True), (70, True),
+@pytest.mark.parametrize("nrhs,inv", [(1, True), (2, True), (3, True), (9, True), (16, True), (70, True),
                                        (3, False), (8, False), (9, False)])
 def test_lattice_multi_rhs_gemv_and_dmma(ops, assembled, nrhs, inv):
-    """few right-hand sides: streaming per-mode GEMV (<= 4 with mode pairs,
-    <= 8 without); more: the per-mode products as DMMA GEMM tiles (rhs-major
-    spectrum, mirrored-mode tiles gathered / scattered through P). Every rhs
-    equals its own single-rhs product and the oracle."""
+    """few right-hand sides: streaming per-mode GEMV (right-hand sides x modes
+    per block <= 8: the icosphere's 8 modes per block allow 1); more: the
+    per-mode products as DMMA GEMM tiles (rhs-major spectrum, image-mode tiles
+    gathered / scattered through P_g). Every rhs equals its own single-rhs
+    product and the oracle."""
     sc, d = assembled(3, 2)
     rng = np.random.default_rng(40 + nrhs)
     P = [uvec(rng, d.N) for _ in range(nrhs)]
-    op = ops(d, max_rhs=nrhs, near_path="lattice", use_inversion=inv)
-    assert op.near_path()[3] == inv
+    op = ops(d, max_rhs=nrhs, near_path="lattice", use_symmetries=inv)
+    assert (op.near_path()[3] > 1) == inv
     y = op.matvec(np.concatenate(P))
-    single = ops(d, near_path="lattice", use_inversion=inv)
+    single = ops(d, near_path="lattice", use_symmetries=inv)
     ora = O.OracleFmm(d)
     for r in sorted({0, nrhs // 2, nrhs - 1}):
         yr = y[r * d.N:(r + 1) * d.N]
@@ -123,9 +124,9 @@ def test_lattice_mode_partition_sums_to_product(ops, assembled, nranks):
         lo, hi, _ = op.partition()
         covered += hi - lo
         total += op.matvec(p)
-    path, sizes, nbytes, paired, _ = op.near_path()
-    assert paired  # the closed cylinder's triangulation is point-symmetric
-    assert covered == nbytes // (16 * d.n_dof ** 2)  # stored blocks (one per mode pair)
+    path, sizes, nbytes, per_block, mask, _ = op.near_path()
+    assert per_block == 2  # the cylinder triangulation's point reflection: (qx, qy) and (-qx, -qy)
+    assert covered == nbytes // (16 * d.n_dof ** 2)  # stored blocks (one per orbit of modes)
     assert rel(total, full) < 1e-13
 
 
@@ -225,7 +226,7 @@ def test_full_size_both_paths(ops, cid, path):
     info = op.near_path()
     assert info[0] == path
     if path == "lattice":
-        assert info[3] and 0.0 <= info[4] <= 1e-12
+        assert info[3] > 1 and 0.0 <= info[5] <= 1e-12
     rng = np.random.default_rng(cid)
     p, q = uvec(rng, d.N), uvec(rng, d.N)
     y = op.matvec(p)
@@ -240,73 +241,121 @@ def test_full_size_both_paths(ops, cid, path):
     assert rel(total, y) < 1e-13
 
 
-def _symmetric_toeplitz(rng, counts, n, perturb=0.0):
-    """random Toeplitz with S_-o = P S_o P for a fixed-point-free involution P"""
-    idx = rng.permutation(n)
-    perm = np.empty(n, np.int64)
-    perm[idx[0::2]], perm[idx[1::2]] = idx[1::2], idx[0::2]
+GROUPS = {"x": [1], "xy": [1, 2], "xyz": [1, 2, 4], "half-turn z": [3], "inversion": [7]}
+
+
+def _closure(gens):
+    G = {0}
+    while True:
+        new = {a ^ b for a in G | set(gens) for b in G | set(gens)} | G | set(gens)
+        if new == G:
+            return sorted(G)
+        G = new
+
+
+def _symmetric_toeplitz(rng, counts, n, gens, perturb=0.0):
+    """random Toeplitz with S_{A_g o} = P_g S_o P_g for the group generated by
+    the axis-sign maps gens, P_g commuting fixed-point-free involutions"""
+    G = _closure(gens)
+    k = len(gens)
+    assert n % (1 << k) == 0
+    idx = rng.permutation(n).reshape(-1, 1 << k)  # each row: one orbit of elements, bit b of the column = generator b
+    gen_perm = {}
+    for b, g in enumerate(gens):
+        p = np.empty(n, np.int64)
+        for row in idx:
+            for c in range(1 << k):
+                p[row[c]] = row[c ^ (1 << b)]
+        gen_perm[g] = p
+    perms = {0: np.arange(n)}
+    for g in G:  # P of a product: compose the generators' permutations
+        if g in perms:
+            continue
+        for a in list(perms):
+            for b in gens:
+                if a ^ b == g:
+                    perms[g] = perms[a][gen_perm[b]]
+    flip = lambda g, o: tuple(-c if g >> d & 1 else c for d, c in enumerate(o))  # noqa: E731
     offs = all_offsets(counts)
     blocks = {}
     for o in offs:
-        m = tuple(-c for c in o)
-        if m in blocks:
-            blocks[o] = blocks[m][np.ix_(perm, perm)]
-        elif o == m:
-            a = crand(rng, n, n)
-            blocks[o] = 0.5 * (a + a[np.ix_(perm, perm)])
-        else:
-            blocks[o] = crand(rng, n, n)
+        if o in blocks:
+            continue
+        stab = [g for g in G if flip(g, o) == o]
+        m = crand(rng, n, n)
+        m = sum(m[np.ix_(perms[h], perms[h])] for h in stab) / len(stab)
+        for g in G:
+            blocks[flip(g, o)] = m[np.ix_(perms[g], perms[g])]
     d = toeplitz_only(rng, counts, n)
     d.near_offsets = np.asarray(offs, np.int32)
     d.near_blocks = np.stack([blocks[o] for o in offs])
     if perturb:
         d.near_blocks[0, 0, 0] += perturb
-    d.cell_inversion = perm.astype(np.int32)
-    return d
+    d.cell_symmetries = [(g, perms[g].astype(np.int32)) for g in G if g]
+    return d, G
 
 
-@pytest.mark.parametrize("counts,n", [((3, 3, 1), 64), ((4, 2, 3), 40), ((1, 7, 1), 130), ((2, 2, 2), 6)])
-def test_lattice_mode_pairs_through_the_cell_inversion(ops, counts, n):
-    """S_-o = P S_o P: one stored block per mode pair (q, -q), the mirror mode
-    through P; parity with the oracle and with the unpaired path"""
+def _orbits(sizes, G):
+    seen, count, largest = set(), 0, 1
+    for qz in range(sizes[2]):
+        for qy in range(sizes[1]):
+            for qx in range(sizes[0]):
+                if (qx, qy, qz) in seen:
+                    continue
+                orb = {tuple((sizes[d] - c) % sizes[d] if g >> d & 1 else c for d, c in enumerate((qx, qy, qz)))
+                       for g in G}
+                seen |= orb
+                count += 1
+                largest = max(largest, len(orb))
+    return count, largest
+
+
+@pytest.mark.parametrize("counts,n,group", [((3, 3, 1), 64, "xy"), ((4, 2, 3), 40, "xyz"), ((1, 7, 1), 130, "inversion"),
+                                            ((2, 2, 2), 8, "xyz"), ((5, 4, 1), 32, "half-turn z"), ((3, 2, 2), 24, "x")])
+def test_lattice_mode_orbits_through_cell_symmetries(ops, counts, n, group):
+    """S_{A_g o} = P_g S_o P_g for a group of axis-sign maps: one stored block per
+    orbit of Fourier modes, the images through P_g; parity with the oracle and
+    with the path that stores every mode"""
     rng = np.random.default_rng(n + sum(counts))
-    d = _symmetric_toeplitz(rng, counts, n)
+    d, G = _symmetric_toeplitz(rng, counts, n, GROUPS[group])
     op = ops(d, near_path="lattice")
-    path, sizes, nbytes, paired, dev = op.near_path()
-    assert paired and dev <= 1e-15
-    q = int(np.prod(sizes))
-    self_mirror = int(np.prod([1 + (L % 2 == 0) if L > 1 else 1 for L in sizes]))  # q = -q modes
-    assert nbytes == 16 * n * n * ((q - self_mirror) // 2 + self_mirror)
+    path, sizes, nbytes, per_block, mask, dev = op.near_path()
+    assert mask == sum(1 << g for g in G) and dev <= 1e-15
+    count, largest = _orbits(sizes, G)
+    assert nbytes == 16 * n * n * count
+    assert per_block == {1: 1, 2: 2, 3: 4, 4: 4}.get(largest, 8)
     p = uvec(rng, d.N)
     y = op.matvec(p)
     assert rel(y, O.toeplitz_matvec(counts, d.near_offsets, d.near_blocks, p)) <= MATVEC_TOL
-    assert rel(y, ops(d, near_path="lattice", use_inversion=False).matvec(p)) <= MATVEC_TOL
+    assert rel(y, ops(d, near_path="lattice", use_symmetries=False).matvec(p)) <= MATVEC_TOL
+    P = [uvec(rng, d.N) for _ in range(11)]  # the DMMA path with image tiles
+    Y = ops(d, max_rhs=11, near_path="lattice").matvec(np.concatenate(P))
+    assert rel(Y[10 * d.N:], O.toeplitz_matvec(counts, d.near_offsets, d.near_blocks, P[10])) <= MATVEC_TOL
 
 
-def test_lattice_inversion_that_does_not_hold_falls_back(ops):
-    """a cell inversion the blocks do not satisfy (one entry perturbed) is
-    measured and rejected: unpaired spectrum, still the oracle's product"""
+def test_lattice_symmetry_that_does_not_hold_is_refused(ops):
+    """a symmetry the blocks do not satisfy (one entry perturbed) is measured
+    and rejected: every mode stored, still the oracle's product"""
     rng = np.random.default_rng(77)
-    d = _symmetric_toeplitz(rng, (3, 2, 1), 24, perturb=1e-6)
+    d, G = _symmetric_toeplitz(rng, (3, 2, 1), 24, [1, 2], perturb=1e-6)
     op = ops(d, near_path="lattice")
-    path, sizes, nbytes, paired, dev = op.near_path()
-    assert not paired and dev > 1e-9
-    assert nbytes == 16 * 24 * 24 * int(np.prod(sizes))
+    path, sizes, nbytes, per_block, mask, dev = op.near_path()
+    assert dev > 1e-9 and per_block < 4
     p = uvec(rng, d.N)
     assert rel(op.matvec(p), O.toeplitz_matvec((3, 2, 1), d.near_offsets, d.near_blocks, p)) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("cid,var,paired", [(3, 2, True), (2, 2, True), (4, 2, True), (1, 1, True)])
-def test_scene_inversion_pairing(ops, assembled, cid, var, paired):
-    """icosphere, point-symmetric cylinder triangulation, closed box and the
-    reference's cube-sphere all verify the inversion on their assembled blocks
-    (rounding-level deviation); the perturbed synthetic case above covers the
-    refusal"""
+@pytest.mark.parametrize("cid,var,want", [(3, 2, 0xFF), (2, 2, 0x81), (4, 2, 0x81), (1, 1, None)])
+def test_scene_symmetries_verified_on_assembled_blocks(ops, assembled, cid, var, want):
+    """the generated meshes carry symmetry-consistent quadrature nodes: the
+    icosphere verifies all 7 axis-sign maps, the cylinder triangulation (split
+    by height) and the split box the inversion (rounding-level
+    deviation); the reference's cube-sphere keeps
+    whatever holds. Every product equals the oracle's."""
     sc, d = assembled(cid, var)
-    assert d.cell_inversion is not None
     op = ops(d, near_path="lattice")
-    info = op.near_path()
-    assert info[3] == paired
-    assert (0.0 <= info[4] <= 1e-12) if paired else info[4] > 1e-12
+    path, sizes, nbytes, per_block, mask, dev = op.near_path()
+    if want is not None:
+        assert mask == want and 0.0 <= dev <= 1e-12
     p = uvec(np.random.default_rng(cid), d.N)
     assert rel(op.matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL

@@ -75,10 +75,11 @@ def run_config(cid, args, out):
     t = time.perf_counter()
     op = FmmOperators(data, max_rhs=nrhs)
     rec["upload_s"] = time.perf_counter() - t
-    path, lat, spec_bytes, mode_pairs, sym_dev = op.near_path()
+    path, lat, spec_bytes, mpb, sym_mask, sym_dev = op.near_path()
     rec["near_path"] = path
-    rec["near_mode_pairs"] = mode_pairs
-    rec["near_inversion_deviation"] = sym_dev
+    rec["near_modes_per_block"] = mpb
+    rec["near_symmetries"] = [g for g in range(1, 8) if sym_mask >> g & 1]
+    rec["near_symmetry_deviation"] = sym_dev
     rec["near_lattice"] = list(lat)
     sizes, _ = op.spectrum()
     rec["fft_sizes"] = list(sizes)
