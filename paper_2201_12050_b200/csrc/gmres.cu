@@ -95,20 +95,79 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
   auto Hm = [&](int i, int j) -> cd& { return cyc.h(i, j); };
   const c64* r = b_dev;  // r = b_eff on the first cycle
   double rnorm = bnorm;
+  const bool fused = mgs_fused_supported(n);
+  // two pinned slots for the pipelined step read-backs (header + h + hc), after
+  // the region fetch() / the y upload use
+  const size_t slot_bytes = 128 + 2 * sizeof(c64) * static_cast<size_t>(op->scal_cap);
+  const size_t slot0 = (sizeof(c64) * (8 + 3 * static_cast<size_t>(op->scal_cap)) + 64 + 255) / 256 * 256;
+  ensure_pinned(op, slot0 + 2 * slot_bytes);
+  pin = static_cast<char*>(op->pinned);
+  char* slot[2] = {pin + slot0, pin + slot0 + slot_bytes};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& e : ev) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "gmres events");
+  std::unique_ptr<cudaEvent_t, void (*)(cudaEvent_t*)> keep_ev(ev, [](cudaEvent_t* e) {
+    cudaEventDestroy(e[0]);
+    cudaEventDestroy(e[1]);
+  });
 
   while (rep.iterations < max_iter) {
     check(launch_div(r, col(0), n, rnorm, s), "v0");
     op->launches++;
     cyc.start(rnorm);
     int j = 0;
-    for (; j < m && rep.iterations < max_iter; ++j) {
-      c64* w = col(j + 1);
-      apply(col(j), w);
-      const bool fused = mgs_fused_supported(n);
-      if (fused) {  // pre-norm + all j+1 MGS steps + post-norm in one cooperative launch
-        check(launch_mgs_fused(w, V, n, j, n, h, sd, op->flag, op->rs, true, s), "mgs fused");
+    if (fused) {
+      // Pipelined Arnoldi: the device completes each step (MGS, the conditional
+      // second pass, h_{j+1,j} and the normalisation: one cooperative launch) and
+      // its scalars come back while the next step's product runs; the host
+      // applies the Givens rotations and the stopping test of step j with the
+      // GPU already on step j + 1. A step enqueued past the stopping point only
+      // writes basis column j + 2, never read: same iterations, same solution.
+      auto enqueue = [&](int jj) {
+        apply(col(jj), col(jj + 1));
+        check(launch_mgs_fused(col(jj + 1), V, n, jj, n, h, sd, op->flag, op->rs, true, s, hc), "mgs step");
         op->launches++;
-      } else {
+        check(cudaMemcpyAsync(slot[jj & 1], sd, slot_bytes, cudaMemcpyDeviceToHost, s), "gmres readback");
+        check(cudaEventRecord(ev[jj & 1], s), "gmres event");
+      };
+      if (rep.iterations < max_iter) enqueue(0);
+      for (; j < m && rep.iterations < max_iter; ++j) {
+        if (j + 1 < m && rep.iterations + 1 < max_iter) enqueue(j + 1);
+        check(cudaEventSynchronize(ev[j & 1]), "gmres sync");
+        const char* p = slot[j & 1];
+        int fl;
+        std::memcpy(&fl, p + 64, sizeof(int));
+        if (fl) {
+          check(cudaStreamSynchronize(s), "gmres sync");
+          check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
+          fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+        }
+        double nr[6];
+        std::memcpy(nr, p, sizeof(nr));
+        for (int i = 0; i <= j; ++i) {
+          c64 v;
+          std::memcpy(&v, p + 128 + i * sizeof(c64), sizeof(c64));
+          Hm(i, j) = cd(v.x, v.y);
+        }
+        if (nr[4] != 0.0)  // reorthogonalised (:63-69): h += hc
+          for (int i = 0; i <= j; ++i) {
+            c64 v;
+            std::memcpy(&v, p + 128 + (op->scal_cap + i) * sizeof(c64), sizeof(c64));
+            Hm(i, j) += cd(v.x, v.y);
+          }
+        const double hlast = nr[5];
+        Hm(j + 1, j) = hlast;
+        ++rep.iterations;
+        const double est = cyc.rotate(j) / bnorm;
+        rep.history.push_back(est);
+        if (est <= tol || hlast == 0.0) {
+          ++j;
+          break;
+        }
+      }
+    } else {
+      for (; j < m && rep.iterations < max_iter; ++j) {
+        c64* w = col(j + 1);
+        apply(col(j), w);
         check(launch_sqnorm(w, n, op->rs, sd + 0, op->flag, s), "pre norm");
         // MGS: h_0 = <v_0,w>; (w -= h_i v_i, h_{i+1} = <v_{i+1}, w>)...; w -= h_j v_j, ||w||^2
         check(launch_dotc(col(0), w, n, op->rs, h + 0, s), "mgs dot");
@@ -116,58 +175,52 @@ GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64
           check(launch_axpy_dotc(w, col(i), h + i, col(i + 1), n, op->rs, h + i + 1, s), "mgs step");
         check(launch_axpy_sqnorm(w, col(j), h + j, n, op->rs, sd + 1, s), "mgs last");
         op->launches += j + 3;
-      }
-      // one read-back: flag, ||w||^2 before and after MGS, h_0..h_j
-      fetch(sd, 128 + sizeof(c64) * (j + 1));
-      {
-        int fl;
-        std::memcpy(&fl, pin + 64, sizeof(int));
-        if (fl) {
-          check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
-          fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+        // one read-back: flag, ||w||^2 before and after MGS, h_0..h_j
+        fetch(sd, 128 + sizeof(c64) * (j + 1));
+        {
+          int fl;
+          std::memcpy(&fl, pin + 64, sizeof(int));
+          if (fl) {
+            check(cudaMemsetAsync(op->flag, 0, sizeof(int), s), "flag reset");
+            fail(FPBEM_CU_ENONFINITE, "gmres: operator returned a non-finite value");
+          }
         }
-      }
-      double pre2, post2;
-      std::memcpy(&pre2, pin, sizeof(double));
-      std::memcpy(&post2, pin + sizeof(double), sizeof(double));
-      for (int i = 0; i <= j; ++i) {
-        c64 v;
-        std::memcpy(&v, pin + 128 + i * sizeof(c64), sizeof(c64));
-        Hm(i, j) = cd(v.x, v.y);
-      }
-      double wnorm2 = post2;
-      if (std::sqrt(post2) < 0.5 * std::sqrt(pre2)) {  // reorthogonalisation (:63-69)
-        if (fused) {
-          check(launch_mgs_fused(w, V, n, j, n, hc, sd + 4, op->flag, op->rs, false, s), "reorth fused");
-          check(cudaMemcpyAsync(sd + 2, sd + 5, sizeof(double), cudaMemcpyDeviceToDevice, s), "reorth norm");
-          op->launches++;
-        } else {
+        double pre2, post2;
+        std::memcpy(&pre2, pin, sizeof(double));
+        std::memcpy(&post2, pin + sizeof(double), sizeof(double));
+        for (int i = 0; i <= j; ++i) {
+          c64 v;
+          std::memcpy(&v, pin + 128 + i * sizeof(c64), sizeof(c64));
+          Hm(i, j) = cd(v.x, v.y);
+        }
+        double wnorm2 = post2;
+        if (std::sqrt(post2) < 0.5 * std::sqrt(pre2)) {  // reorthogonalisation (:63-69)
           check(launch_dotc(col(0), w, n, op->rs, hc + 0, s), "reorth dot");
           for (int i = 0; i < j; ++i)
             check(launch_axpy_dotc(w, col(i), hc + i, col(i + 1), n, op->rs, hc + i + 1, s), "reorth step");
           check(launch_axpy_sqnorm(w, col(j), hc + j, n, op->rs, sd + 2, s), "reorth last");
           op->launches += j + 2;
+          fetch(hc, sizeof(c64) * (j + 1));
+          for (int i = 0; i <= j; ++i) {
+            c64 v;
+            std::memcpy(&v, pin + i * sizeof(c64), sizeof(c64));
+            Hm(i, j) += cd(v.x, v.y);
+          }
+          wnorm2 = fetch_d(2);
         }
-        fetch(hc, sizeof(c64) * (j + 1));
-        for (int i = 0; i <= j; ++i) {
-          c64 v;
-          std::memcpy(&v, pin + i * sizeof(c64), sizeof(c64));
-          Hm(i, j) += cd(v.x, v.y);
+        const double hlast = std::sqrt(wnorm2);
+        Hm(j + 1, j) = hlast;
+        if (hlast > 0.0) {
+          check(launch_div(w, w, n, hlast, s), "normalise");
+          op->launches++;
         }
-        wnorm2 = fetch_d(2);
-      }
-      const double hlast = std::sqrt(wnorm2);
-      Hm(j + 1, j) = hlast;
-      if (hlast > 0.0) {
-        check(launch_div(w, w, n, hlast, s), "normalise");
-        op->launches++;
-      }
-      ++rep.iterations;
-      const double est = cyc.rotate(j) / bnorm;
-      rep.history.push_back(est);
-      if (est <= tol || hlast == 0.0) {
-        ++j;
-        break;
+        ++rep.iterations;
+        const double est = cyc.rotate(j) / bnorm;
+        rep.history.push_back(est);
+        if (est <= tol || hlast == 0.0) {
+          ++j;
+          break;
+        }
       }
     }
     // y = triu(H_jj)^{-1} g ; x += V y (:109-110)

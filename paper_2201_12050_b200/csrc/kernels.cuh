@@ -86,8 +86,12 @@ cudaError_t launch_update_x(c64* x, const c64* basis, long long ld, const c64* y
 // whole MGS sequence of one Arnoldi step in one cooperative launch:
 // norms[0] = ||w||^2 (if do_pre, + non-finite flag), h_out[0..j], norms[1] = ||w||^2 after
 bool mgs_fused_supported(long long n);
+// hc_out != null (needs do_pre): the whole Arnoldi step in the launch — the conditional
+// second pass into hc_out, norms[2] = final ||w||^2, norms[4] = 1 if reorthogonalised,
+// norms[5] = h_{j+1,j} = ||w||, and w normalised by it (if > 0)
 cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
-                             int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s);
+                             int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s,
+                             c64* hc_out = nullptr);
 // ---- batched (lockstep multi-RHS) vector ops: G right-hand sides at stride ld
 constexpr int kBatchBlocks = 64;  // blocks per RHS (upper bound)
 struct BatchScratch {

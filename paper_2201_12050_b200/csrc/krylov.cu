@@ -335,7 +335,7 @@ __device__ __forceinline__ T block_sum_mgs(T v, T* sh) {  // result valid in thr
 __global__ void __launch_bounds__(kMgsThreads, 1)
 mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, int j, long long n, long long chunk,
                  c64* __restrict__ h_out, double* __restrict__ norms, int* __restrict__ nonfinite,
-                 c64* __restrict__ part_c, double* __restrict__ part_d, int do_pre) {
+                 c64* __restrict__ part_c, double* __restrict__ part_d, int do_pre, c64* __restrict__ hc_out) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   c64* ws = reinterpret_cast<c64*>(smem_raw);
@@ -377,6 +377,7 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
     return bcast_c;
   };
 
+  double pre = 0.0;
   if (do_pre) {
     double s = 0.0;
     bool bad = false;
@@ -387,59 +388,83 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
       s = fma(v.y, v.y, s);
     }
     if (bad) atomicOr(nonfinite, 1);
-    const double tot = fold_d(s, part_d);
-    if (blockIdx.x == 0 && tid == 0) norms[0] = tot;
+    pre = fold_d(s, part_d);
+    if (blockIdx.x == 0 && tid == 0) norms[0] = pre;
   }
 
-  c64 vc[kMgsK];  // this thread's slice of v_i
-  {
-    const c64* v = V + start;
+  // one MGS pass over v_0..v_j on the chunk in shared memory: projections to
+  // hout[0..j], returns ||w||^2 after the pass
+  auto pass = [&](c64* __restrict__ hout) -> double {
+    c64 vc[kMgsK];  // this thread's slice of v_i
+    {
+      const c64* v = V + start;
+#pragma unroll
+      for (int k = 0; k < kMgsK; ++k) {
+        const int e = tid + k * kMgsThreads;
+        vc[k] = e < len ? v[e] : cmk(0.0, 0.0);
+      }
+    }
+    c64 s = cmk(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < kMgsK; ++k) {
       const int e = tid + k * kMgsThreads;
-      vc[k] = e < len ? v[e] : cmk(0.0, 0.0);
+      if (e < len) s = cfma_conj(vc[k], ws[e], s);
     }
-  }
-  c64 s = cmk(0.0, 0.0);
+    c64 h = fold_c(s, 0);
+    if (blockIdx.x == 0 && tid == 0) hout[0] = h;
+    for (int i = 0; i < j; ++i) {
+      // w -= h_i v_i (v_i from registers) and the partial <v_{i+1}, w> in one pass;
+      // v_{i+1} is read from HBM once and stays in registers for the next step
+      const c64* v = V + static_cast<long long>(i + 1) * ld + start;
+      s = cmk(0.0, 0.0);
 #pragma unroll
-  for (int k = 0; k < kMgsK; ++k) {
-    const int e = tid + k * kMgsThreads;
-    if (e < len) s = cfma_conj(vc[k], ws[e], s);
-  }
-  c64 h = fold_c(s, 0);
-  if (blockIdx.x == 0 && tid == 0) h_out[0] = h;
-  for (int i = 0; i < j; ++i) {
-    // w -= h_i v_i (v_i from registers) and the partial <v_{i+1}, w> in one pass;
-    // v_{i+1} is read from HBM once and stays in registers for the next step
-    const c64* v = V + static_cast<long long>(i + 1) * ld + start;
-    s = cmk(0.0, 0.0);
+      for (int k = 0; k < kMgsK; ++k) {
+        const int e = tid + k * kMgsThreads;
+        if (e < len) {
+          const c64 nx = v[e];
+          const c64 wv = csub(ws[e], cmul(h, vc[k]));
+          ws[e] = wv;
+          s = cfma_conj(nx, wv, s);
+          vc[k] = nx;
+        }
+      }
+      h = fold_c(s, i + 1);
+      if (blockIdx.x == 0 && tid == 0) hout[i + 1] = h;
+    }
+    double q = 0.0;  // the last update, w -= h_j v_j, then ||w||^2
 #pragma unroll
     for (int k = 0; k < kMgsK; ++k) {
       const int e = tid + k * kMgsThreads;
       if (e < len) {
-        const c64 nx = v[e];
         const c64 wv = csub(ws[e], cmul(h, vc[k]));
+        q = fma(wv.x, wv.x, q);
+        q = fma(wv.y, wv.y, q);
         ws[e] = wv;
-        s = cfma_conj(nx, wv, s);
-        vc[k] = nx;
       }
     }
-    h = fold_c(s, i + 1);
-    if (blockIdx.x == 0 && tid == 0) h_out[i + 1] = h;
-  }
-  double q = 0.0;  // the last update, w -= h_j v_j, then ||w||^2 and the write-back
-#pragma unroll
-  for (int k = 0; k < kMgsK; ++k) {
-    const int e = tid + k * kMgsThreads;
-    if (e < len) {
-      const c64 wv = csub(ws[e], cmul(h, vc[k]));
-      q = fma(wv.x, wv.x, q);
-      q = fma(wv.y, wv.y, q);
-      w[start + e] = wv;
+    return fold_d(q, part_d + G);
+  };
+
+  const double post = pass(h_out);
+  if (blockIdx.x == 0 && tid == 0) norms[1] = post;
+  if (hc_out) {
+    // the whole Arnoldi step (src/solver.cpp:58-73): the conditional second pass
+    // when ||w|| < 0.5 ||w||_pre (the same arithmetic as a second launch on the
+    // written-back w), then h_{j+1,j} = ||w|| and w / h_{j+1,j} (as div_kernel)
+    double wn2 = post;
+    const bool reorth = sqrt(post) < 0.5 * sqrt(pre);
+    if (reorth) wn2 = pass(hc_out);
+    const double hl = sqrt(wn2);
+    if (blockIdx.x == 0 && tid == 0) {
+      norms[2] = wn2;
+      norms[4] = reorth ? 1.0 : 0.0;
+      norms[5] = hl;
     }
+    if (hl > 0.0)
+      for (int e = tid; e < len; e += kMgsThreads) ws[e] = cmk(ws[e].x / hl, ws[e].y / hl);
+    __syncthreads();
   }
-  const double tot = fold_d(q, part_d + G);
-  if (blockIdx.x == 0 && tid == 0) norms[1] = tot;
+  for (int e = tid; e < len; e += kMgsThreads) w[start + e] = ws[e];
 }
 
 // ---------------------------------------------------------------------------
@@ -699,7 +724,7 @@ cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, l
 bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kNumSMs) * kMgsMaxChunk; }
 
 cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
-                             int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s) {
+                             int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s, c64* hc_out) {
   // cooperative launch: every block co-resident (one per SM)
   long long blocks = (n + 1023) / 1024;  // >= 2 elements per thread before using more SMs
   if (blocks > kNumSMs) blocks = kNumSMs;
@@ -717,7 +742,7 @@ cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long lon
   int pre = do_pre ? 1 : 0;
   c64* pc = rs.partial_c;
   double* pd = rs.partial_d;
-  void* args[] = {&w, const_cast<c64**>(&V), &ld, &j, &n, &chunk, &h_out, &norms, &nonfinite, &pc, &pd, &pre};
+  void* args[] = {&w, const_cast<c64**>(&V), &ld, &j, &n, &chunk, &h_out, &norms, &nonfinite, &pc, &pd, &pre, &hc_out};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&mgs_fused_kernel), dim3(static_cast<unsigned>(blocks)),
                                      dim3(kMgsThreads), args, smem, s);
 }
