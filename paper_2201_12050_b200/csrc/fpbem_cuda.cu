@@ -926,9 +926,6 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
       const size_t f = static_cast<size_t>(op->max_rhs) * op->qn * op->n;
       op->nfa = dalloc<c64>(f, "near x spectrum");
       op->nfb = dalloc<c64>(f, "near y spectrum");
-      op->zero_ptr = dalloc<int>(static_cast<size_t>(op->n_cells) + 1, "zero csr");
-      check(cudaMemsetAsync(op->zero_ptr, 0, (static_cast<size_t>(op->n_cells) + 1) * sizeof(int), op->stream),
-            "zero csr");
       op->mode_lo = 0;
       op->mode_hi = op->n_items;
     }
@@ -967,7 +964,7 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
                   static_cast<void*>(op->rs.partial_c), static_cast<void*>(op->rs.counter),
                   static_cast<void*>(op->shat), static_cast<void*>(op->twn[0]), static_cast<void*>(op->twn[1]),
                   static_cast<void*>(op->twn[2]), static_cast<void*>(op->nfa), static_cast<void*>(op->nfb),
-                  static_cast<void*>(op->zero_ptr), static_cast<void*>(op->mjobs), static_cast<void*>(op->perm),
+                  static_cast<void*>(op->mjobs), static_cast<void*>(op->perm),
                   static_cast<void*>(op->items)})
     if (p) cudaFree(p);
   if (op->pinned) cudaFreeHost(op->pinned);

@@ -124,7 +124,6 @@ struct fpbem_cu_op {
   c64* twn[3] = {nullptr, nullptr, nullptr};
   c64* nfa = nullptr;   // spectra of x / y, [rhs][q][n], sized for max_rhs
   c64* nfb = nullptr;
-  int* zero_ptr = nullptr;  // n_cells + 1 zeros: the L2P-only reduction
   int4* mjobs = nullptr;    // DMMA jobs over this rank's items (many right-hand sides)
   int mjobs_nrhs = -1, n_mjobs = 0, mjobs_cap = 0;
   // stored blocks = work items = orbits of Fourier modes under the cell's
