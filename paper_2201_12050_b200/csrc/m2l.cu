@@ -1085,12 +1085,12 @@ cudaError_t launch_xy_plane(const c64* in, c64* out, const c64* twx, const c64* 
 cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, long long N, int nrhs, int cells,
                        cudaStream_t stream) {
   if (cells == 0 || nrhs == 0) return cudaSuccess;
-  static const bool gemm_on = [] {  // FPBEM_P2M_GEMM=0: the FMA kernel for every rhs count
+  static const int gemm_mode = [] {  // FPBEM_P2M_GEMM=0: the FMA kernel for every rhs count; =2: GEMM for all
     const char* v = std::getenv("FPBEM_P2M_GEMM");
-    return !(v && std::strcmp(v, "0") == 0);
+    return v ? std::atoi(v) : 1;
   }();
   const size_t smem = sizeof(c64) * static_cast<size_t>(b) * p2m_pitch(n);
-  if (gemm_on && nrhs >= 4 && smem <= 200 * 1024) {
+  if (gemm_mode != 0 && (nrhs >= 4 || gemm_mode == 2) && smem <= 200 * 1024) {
     static size_t configured = 48 * 1024;
     if (smem > configured) {
       cudaError_t e =
