@@ -1,4 +1,6 @@
-# per-mode product of the lattice near field (serial stage timing)
+# per-mode product of the lattice near field (serial stage timing), two repetitions
+for rep in 1 2; do
 for c in 2 3 5; do
-  echo "cfg$c"; FPBEM_SERIAL=1 python tools/profile_matvec.py --config $c --applies 20 2>&1 | grep near
+  echo "cfg$c"; FPBEM_SERIAL=1 python tools/profile_matvec.py --config $c --applies 30 2>&1 | grep near
+done
 done
