@@ -336,8 +336,27 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
     op->launches++;
     cur = out;
   };
-  if (Lx > 1) fwd(0, r * My * Mz, Mx, Lx, n);
-  if (Ly > 1) fwd(1, r * Mz, My, Ly, Lx * n);
+  // x and y together per (plane, field) for 2-D lattices (the M2L's plane
+  // kernel; measured faster there, slower on the 3-D lattices of cfg3 / cfg5:
+  // tools/ab_near_xy.sh); FPBEM_NEAR_XY=0 keeps the axis passes
+  static const bool xy_env = [] {
+    const char* v = std::getenv("FPBEM_NEAR_XY");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const bool xy = xy_env && Lx > 1 && Ly > 1 && Lz == 1 && n <= 0x7fffffffLL &&
+                  xy_plane_smem(Mx, My, Lx, Ly, false) <= 200 * 1024 && xy_plane_smem(Mx, My, Lx, Ly, true) <= 200 * 1024;
+  if (xy) {
+    c64* out = bufs[which];
+    which ^= 1;
+    check(launch_xy_plane(cur, out, op->twn[0], op->twn[1], Mx, My, Lx, Ly, static_cast<int>(r * Mz),
+                          static_cast<int>(n), false, 1.0, s),
+          "near xy dft");
+    op->launches++;
+    cur = out;
+  } else {
+    if (Lx > 1) fwd(0, r * My * Mz, Mx, Lx, n);
+    if (Ly > 1) fwd(1, r * Mz, My, Ly, Lx * n);
+  }
   if (Lz > 1) fwd(2, r, Mz, Lz, static_cast<long long>(Ly) * Lx * n);
   c64* yh = bufs[which];
   which ^= 1;
@@ -369,8 +388,15 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
     cur = out;
   };
   if (Lz > 1) inv(2, r, Lz, Mz, static_cast<long long>(Ly) * Lx * n);
-  if (Ly > 1) inv(1, r * Mz, Ly, My, Lx * n);
-  if (Lx > 1) inv(0, r * My * Mz, Lx, Mx, n);
+  if (xy) {  // the last inverse pass: writes y with the 1/q scale
+    check(launch_xy_plane(cur, y, op->twn[0], op->twn[1], Mx, My, Lx, Ly, static_cast<int>(r * Mz),
+                          static_cast<int>(n), true, scale, s),
+          "near xy inverse dft");
+    op->launches++;
+  } else {
+    if (Ly > 1) inv(1, r * Mz, Ly, My, Lx * n);
+    if (Lx > 1) inv(0, r * My * Mz, Lx, Mx, n);
+  }
 }
 
 void twiddles(fpbem_cu_op* op, int L, c64** out) {
