@@ -6,6 +6,7 @@
 // The MGS step is fused so that the update w -= h_i v_i and the next
 // projection <v_{i+1}, w> (or the norm ||w|| after the last one) are one pass.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -726,7 +727,11 @@ bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kNumS
 cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
                              int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s, c64* hc_out) {
   // cooperative launch: every block co-resident (one per SM)
-  long long blocks = (n + 1023) / 1024;  // >= 2 elements per thread before using more SMs
+  static const long long per_block = [] {  // elements per block before using more SMs (FPBEM_MGS_PER_BLOCK, A/B)
+    const char* v = std::getenv("FPBEM_MGS_PER_BLOCK");
+    return v ? std::max(1LL, std::atoll(v)) : 1024LL;
+  }();
+  long long blocks = (n + per_block - 1) / per_block;
   if (blocks > kNumSMs) blocks = kNumSMs;
   if (blocks < 1) blocks = 1;
   long long chunk = (n + blocks - 1) / blocks;
