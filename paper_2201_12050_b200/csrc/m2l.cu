@@ -300,12 +300,11 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
   };
   load(warp0);
   for (long long t = warp0; t < tiles; t += nwarps) {
-    double br[KTM], bi[KTM], bs[KTM];
+    double br[KTM], bi[KTM];  // (br + bi is formed at each use: fewer live registers)
 #pragma unroll
     for (int kt = 0; kt < KTM; ++kt) {
       br[kt] = nb[kt].x;
       bi[kt] = nb[kt].y;
-      bs[kt] = nb[kt].x + nb[kt].y;
     }
     load(t + nwarps);
     const long long a = t / n_et, e0 = (t % n_et) * 8;
@@ -319,11 +318,12 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
           const int o0 = (mt * KT + kt) * 32 + lane, o1 = o0 + KT * 32;
           dmma884(t1[0][0], t1[0][1], wr[o0], br[kt]);
           dmma884(t2[0][0], t2[0][1], wi[o0], bi[kt]);
-          dmma884(t3[0][0], t3[0][1], ws[o0], bs[kt]);
+          const double bsum = br[kt] + bi[kt];
+          dmma884(t3[0][0], t3[0][1], ws[o0], bsum);
           if (two) {
             dmma884(t1[1][0], t1[1][1], wr[o1], br[kt]);
             dmma884(t2[1][0], t2[1][1], wi[o1], bi[kt]);
-            dmma884(t3[1][0], t3[1][1], ws[o1], bs[kt]);
+            dmma884(t3[1][0], t3[1][1], ws[o1], bsum);
           }
         }
       }
@@ -972,7 +972,8 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     const size_t smem = sizeof(double) * 3 * MT * KT * 32;
     static bool raised = false;
     if (!raised) {
-      for (auto fn : {dft_axis_dmma_kernel<4>, dft_axis_dmma_kernel<8>, dft_axis_dmma_kernel<16>}) {
+      for (auto fn : {dft_axis_dmma_kernel<4>, dft_axis_dmma_kernel<8>, dft_axis_dmma_kernel<12>,
+                      dft_axis_dmma_kernel<16>}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sizeof(double) * 3 * 8 * 16 * 32));
         if (e != cudaSuccess) return e;
@@ -982,11 +983,12 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     const long long tiles = n_a * ((n_inner + 7) / 8);
     long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
     // one resident wave (W expanded once per CTA), as many CTAs per SM as fit
-    static int occ[3] = {0, 0, 0};
-    const int which = KT <= 4 ? 0 : KT <= 8 ? 1 : 2;
+    static int occ[4] = {0, 0, 0, 0};
+    const int which = KT <= 4 ? 0 : KT <= 8 ? 1 : KT <= 12 ? 2 : 3;
     if (occ[which] == 0) {
-      const void* fn = which == 0 ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<4>)
+      const void* fn = which == 0   ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<4>)
                        : which == 1 ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<8>)
+                       : which == 2 ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<12>)
                                     : reinterpret_cast<const void*>(dft_axis_dmma_kernel<16>);
       int per_sm = 0;
       cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDftMmaWarps * 32,
@@ -1002,6 +1004,9 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
           in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
     else if (KT <= 8)
       dft_axis_dmma_kernel<8><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
+          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
+    else if (KT <= 12)
+      dft_axis_dmma_kernel<12><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
           in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
     else
       dft_axis_dmma_kernel<16><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
