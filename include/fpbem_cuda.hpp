@@ -52,6 +52,17 @@ class DeviceFmm {
     return b;
   }
 
+  // the near-field path chosen at create (FPBEM_CU_NEAR_DIRECT or _LATTICE) and the
+  // Fourier modes per stored block (1 unless cell symmetries were verified)
+  int near_path(int* modes_per_block = nullptr) const {
+    int path = 0, sizes[3], mpb = 1, mask = 0;
+    std::size_t bytes = 0;
+    double dev = 0.0;
+    throw_on(fpbem_cu_fmm_near_path(op_, &path, sizes, &bytes, &mpb, &mask, &dev));
+    if (modes_per_block) *modes_per_block = mpb;
+    return path;
+  }
+
   // y = A p (FmmOperators::matvec): host buffers, synchronous
   template <typename Vec>
   Vec apply(const Vec& p, int nrhs = 1) const {
