@@ -79,10 +79,23 @@ def build_oracle(force: bool = False) -> Path:
     return out
 
 
+def build_driver(force: bool = False) -> Path:
+    """tools/cpp_scene_solve: the C++-only host -> C-ABI path (host assembly, shim, device solve)."""
+    out = LIB / "cpp_scene_solve"
+    src = ROOT / "tools" / "cpp_scene_solve.cpp"
+    deps = [src, LIB / "libfpbem_host.so", LIB / "libfpbem_cuda.so", ROOT / "include" / "fpbem_cuda.hpp",
+            ROOT / "include" / "fpbem_cuda.h"] + list(HOST.glob("*.hpp"))
+    if force or _stale(out, deps):
+        _run(["g++", "-O2", "-std=c++17", "-I", str(ROOT / "include"), "-I", str(HOST), str(src), "-L", str(LIB),
+              "-lfpbem_host", "-lfpbem_cuda", f"-Wl,-rpath,{LIB}", "-fopenmp", "-o", str(out)])
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_host(force)
     build_oracle(force)
     build_cuda(force)
+    build_driver(force)
 
 
 if __name__ == "__main__":
