@@ -190,3 +190,57 @@ def test_mirrored_mesh_keeps_orientation_and_index():
     sc.set_halfspace(2, 0.0, 1e-300)
     assert rel(sc.dense(), a0) < 1e-12
     assert c["nv"][0] == 3
+
+
+@pytest.mark.parametrize("cid,var,want", [(3, 2, [1, 2, 3, 4, 5, 6, 7]), (2, 2, [7]), (4, 2, [7]),
+                                          (1, 0, [1, 2, 3, 4, 5, 6, 7])])
+def test_cell_symmetries_and_symmetric_quadrature_order(cid, var, want):
+    """Scene.cell_symmetries (host C++ cell_symmetries): the axis-sign maps that
+    map the generated unit cell onto itself, each with an element permutation;
+    symmetrize_group gives every image element the images of its source's
+    corners, reordered (b', a', c'[, d']) for orientation-reversing maps — the
+    property that makes S_{A_g o}[P_g i, P_g j] = S_o[i, j] hold to rounding
+    (DESIGN.md §3.1c)."""
+    from paper_2201_12050_b200 import Scene
+
+    sc = Scene(cid, var)
+    syms = sc.cell_symmetries()
+    assert [g for g, _ in syms] == want
+    cell = sc.cell()
+    cor, nv = cell["corners"], cell["nv"]
+    pts = cor.reshape(-1, 3)
+    ctr = 0.5 * (pts.min(axis=0) + pts.max(axis=0))
+    tol = 1e-9 * np.linalg.norm(pts.max(axis=0) - pts.min(axis=0))
+    for g, perm in syms:
+        assert sorted(perm) == list(range(sc.n_dof))
+        sign = np.array([-1.0 if g >> d & 1 else 1.0 for d in range(3)])
+        img = ctr + sign * (cor - ctr)  # corners mapped by g, in the source's order
+        reversing = bin(g).count("1") % 2 == 1
+        for j in range(sc.n_dof):
+            k = perm[j]
+            if reversing:  # (b', a', c') / (b', a', d', c')
+                order = [1, 0, 2, 2] if nv[j] == 3 else [1, 0, 3, 2]
+                want_c = img[j][order]
+            else:
+                want_c = img[j]
+            got = cor[k]
+            ok = np.abs(got - want_c).max() < tol
+            if not ok and not reversing and nv[j] == 4:  # a half-turn may map a quad to its own half-turn
+                ok = np.abs(got - want_c[[2, 3, 0, 1]]).max() < tol
+            assert ok, (g, j, k)
+
+
+def test_reference_quad_cells_report_a_group_of_permutations():
+    """the reference's own generators (wall cell, cube-sphere) are not reordered;
+    their point-set symmetries still come back as a group of permutations (the
+    device decides per map whether the blocks honour it)"""
+    from paper_2201_12050_b200 import Scene
+
+    for sc in (Scene.custom("wall", [1.0, 2.0, 0.1, 3], [1, 4, 1], [0.0, 1.0, 0.0], 2.0), Scene(1, 1)):
+        syms = dict(sc.cell_symmetries())
+        for g, perm in syms.items():
+            assert sorted(perm) == list(range(sc.n_dof))
+            assert np.array_equal(perm[perm], np.arange(sc.n_dof))  # axis-sign maps are involutions
+            for h in syms:
+                if h != g:
+                    assert (g ^ h) in syms  # closed under composition
