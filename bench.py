@@ -360,6 +360,8 @@ def run_ours(args):
                     "launch_ms": gemm_ms,
                     "algorithmic_bytes": 16.0 * data.n_near * data.n_dof ** 2 + 2 * 16.0 * data.N}
     roofline["frac"] = roofline["achieved"] / peak
+    if traffic and traffic.get("config") != args.config:
+        traffic = None  # the committed ncu capture is of another workload
     roofline["traffic"] = (traffic or {}).get("dram_bytes_per_launch")
     roofline["traffic_source"] = (traffic or {}).get("source")
     cpu = None
