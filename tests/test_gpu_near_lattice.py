@@ -359,3 +359,22 @@ def test_scene_symmetries_verified_on_assembled_blocks(ops, assembled, cid, var,
         assert mask == want and 0.0 <= dev <= 1e-12
     p = uvec(np.random.default_rng(cid), d.N)
     assert rel(op.matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+def test_lattice_mode_partition_with_many_right_hand_sides(ops, assembled):
+    """the DMMA job list of the lattice path covers only the rank's stored
+    blocks: partial products of 12 right-hand sides over 3 ranks sum to the
+    product, each right-hand side equal to the oracle's"""
+    sc, d = assembled(3, 2)
+    rng = np.random.default_rng(123)
+    P = np.concatenate([uvec(rng, d.N) for _ in range(12)])
+    op = ops(d, max_rhs=12, near_path="lattice")
+    full = op.matvec(P)
+    total = np.zeros_like(full)
+    for r in range(3):
+        op.set_partition(r, 3)
+        total += op.matvec(P)
+    assert rel(total, full) < 1e-13
+    ora = O.OracleFmm(d)
+    for k in (0, 11):
+        assert rel(full[k * d.N:(k + 1) * d.N], ora.matvec(P[k * d.N:(k + 1) * d.N])) <= MATVEC_TOL
