@@ -394,8 +394,8 @@ cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_item
   return cudaGetLastError();
 }
 
-// max |S_s'[P i + n P j] - S_s[i + n j]| over blocks s with mirror slot s' (the
-// block of -o) and max |S|, as double bits (non-negative doubles order like
+// max |S_s'[P i + n P j] - S_s[i + n j]| over blocks s with image slot s' (the
+// block of A_g o) and max |S|, as double bits (non-negative doubles order like
 // their bit patterns): the device check of one cell symmetry g (mirror = slot of A_g o, perm = P_g)
 __global__ void near_symmetry_kernel(const c64* __restrict__ S, int n, int n_blk, const int* __restrict__ mirror,
                                      const int* __restrict__ perm, unsigned long long* out2) {
