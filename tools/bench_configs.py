@@ -12,9 +12,14 @@ sweep (operator rebuilt per frequency), cfg5 its 64 Fibonacci plane waves
 """
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
+
+# idle OpenMP workers of the oracle sleep instead of spinning, so they do not
+# take host cores from the GPU solves timed after them (set before any load)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
 import numpy as np
 
