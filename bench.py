@@ -1,16 +1,19 @@
 """Benchmark of the periodic-FMBEM GMRES matvec hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
 
 One step = one FMM operator product y = A x (near field + P2M + lattice M2L +
-L2P) of the BASELINE.json configuration (default configs[1] = cfg2: 4 x 32
-closed cylinders, 1024 triangles each, 131,072 DOF, k = 2 pi 1000/343). The
-operator is assembled on the host (C++), uploaded once, and the timed region
-covers K products on inputs resident in HBM (the 2.1 GB near-field operator
-is far larger than the 126 MB L2, so every step streams it from HBM).
-`e2e` times the same product through the C-ABI with pinned host buffers
-(host->device copy of x and device->host copy of y inside every step). A
-GMRES solve (tol 1e-6, restart 50) is timed as the metric's second half.
+L2P) of a BASELINE.json configuration; the default is the largest single-GPU
+single-RHS one, configs[2] = cfg3 (16^3 icosphere cells, 1,310,720 DOF,
+k = 6.0). The operator is assembled once (offsets, U0, V0, M2L bank on the
+host; near-field blocks on the device), and each timed batch covers exactly K
+products on inputs resident in HBM (the near-field block spectrum, 1.2 GB on
+cfg3, is far larger than the 126 MB L2, so every step streams it from HBM).
+Timing follows the reference's protocol (src/scene.cpp:528-544): warm-up,
+batches of >= 20 ms, best of 5 batches. `e2e` times the same product through
+the C-ABI with pinned host buffers (host->device copy of x and device->host
+copy of y inside every step), also best of 5 batches. A GMRES solve (tol 1e-6,
+restart 50) is timed as the metric's second half.
 
 --impl reference times the reference's CPU algorithm (the oracle port,
 oracle/fpbem_oracle.cpp; the reference itself cannot be built here, see
@@ -159,6 +162,14 @@ class _WithNear:
         return getattr(self._d, name)
 
 
+def host_threads():
+    """What the CPU legs ran on: nproc, OMP_NUM_THREADS and the threads OpenMP used."""
+    import oracle as O
+
+    return {"nproc": os.cpu_count(), "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "omp_threads": O.num_threads()}
+
+
 def cpu_baseline(data, x, samples: int = 3):
     """Oracle (reference algorithm, OpenMP over target cells) on the host cores."""
     import oracle as O
@@ -171,7 +182,8 @@ def cpu_baseline(data, x, samples: int = 3):
         t = time.perf_counter()
         ora.matvec(x)
         best = min(best, time.perf_counter() - t)
-    return {"value": data.N / best, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+    th = host_threads()
+    return {"value": data.N / best, "unit": UNIT, "cores": th["omp_threads"], "kind": "port", **th,
             "sample": f"{samples} single-RHS matvecs of the same operator after 1 warm-up, best of {samples} "
                       f"({best:.3f} s each; setup {time.perf_counter() - t0 - (samples + 1) * best:.1f} s)"}
 
@@ -198,20 +210,41 @@ def run_reference(args):
         times.append(time.perf_counter() - t)
     total = sum(times)
     value = data.N * args.steps / total
-    cores = O.num_threads()
+    th = host_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128",
         "data": "synthetic (seeded U[-1,1] input; operator assembled from the config geometry)",
         "config": {"workload": desc, "n_dof_total": data.N, "nrhs": 1, "n_t": 4},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th["omp_threads"], "kind": "port", **th,
                          "sample": "each step = one full single-RHS matvec of the workload on the host "
                                    "(oracle restatement of the reference; reference unbuildable here)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def timed_batches(fn, steps: int, trials: int, stream, barrier):
+    """The reference's protocol (src/scene.cpp:528-544): `trials` batches of
+    exactly `steps` products, each bracketed by a barrier and a device sync and
+    timed with CUDA events on the launching stream; returns every batch's ms."""
+    import torch
+
+    out = []
+    for _ in range(trials):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        out.append(e0.elapsed_time(e1))
+    return out
 
 
 def run_ours(args):
@@ -261,38 +294,35 @@ def run_ours(args):
     rng = np.random.default_rng(args.config)  # the same input on every rank: the all-reduced product is A x
     xh = rng.uniform(-1, 1, data.N) + 1j * rng.uniform(-1, 1, data.N)
     x = torch.from_numpy(xh).to(dev)
-
-    # warm-up
-    for _ in range(max(3, args.warmup)):
-        y = op.matvec(x)
-    torch.cuda.synchronize(dev)
+    warmup = max(3, args.warmup)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
+    from paper_2201_12050_b200 import _native
+
+    lib = _native.cuda()
     sampler = ClockSampler(dev.index)
     with sampler:
+        # ---- warm-up, then the device-resident timed batches
+        for _ in range(warmup):
+            op.matvec(x)
+        torch.cuda.synchronize(dev)
         time.sleep(0.25)  # let the sampler start
-        # ---- device-resident timed region
         launches0 = op.kernel_launches()
-        barrier()
-        torch.cuda.synchronize(dev)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            y = op.matvec(x)
-        ev1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        ms = ev0.elapsed_time(ev1)
-        launches = op.kernel_launches() - launches0
+        trials_ms = timed_batches(lambda: op.matvec(x), args.steps, args.trials, stream, barrier)
+        launches = (op.kernel_launches() - launches0) // args.trials
 
-        # ---- per-stage event timing (same stream) for the roofline
+        # ---- per-stage event timing (same stream); serial: the far field on the main stream
         op.enable_stage_timing(True)
         for _ in range(args.steps):
             op.matvec(x)
         stages = op.stage_times()
+        op.enable_stage_timing(True, serial=True)
+        for _ in range(args.steps):
+            op.matvec(x)
+        stages_serial = op.stage_times()
         op.enable_stage_timing(False)
 
         # ---- end-to-end through the C-ABI with pinned host buffers
@@ -300,21 +330,21 @@ def run_ours(args):
         xp.copy_(torch.from_numpy(xh))
         yp = torch.empty(data.N, dtype=torch.complex128, pin_memory=True)  # empty_like would not pin
         xpn, ypn = xp.numpy(), yp.numpy()
-        from paper_2201_12050_b200 import _native
-
-        lib = _native.cuda()
         op.matvec(xpn)
-        barrier()
-        t = time.perf_counter()
-        for _ in range(args.steps):
-            rc = lib.fpbem_cu_fmm_apply(op.handle, xpn.ctypes.data, ypn.ctypes.data, 1, 0)
-            if rc:
-                raise RuntimeError(lib.fpbem_cu_last_error().decode())
-        e2e_s = time.perf_counter() - t
-        barrier()
+        e2e_trials = []
+        for _ in range(args.trials):
+            barrier()
+            t = time.perf_counter()
+            for _ in range(args.steps):
+                rc = lib.fpbem_cu_fmm_apply(op.handle, xpn.ctypes.data, ypn.ctypes.data, 1, 0)
+                if rc:
+                    raise RuntimeError(lib.fpbem_cu_last_error().decode())
+            e2e_trials.append(time.perf_counter() - t)
+            barrier()
 
-        # ---- GMRES solve (metric's second half)
+        # ---- GMRES solve (metric's second half); warm solve first (workspace allocation)
         b = torch.from_numpy(sc.rhs(0)).to(dev)
+        gmres(op, b, tol=1e-6, restart=50, max_iter=min(5, args.gmres_max_iter))
         torch.cuda.synchronize(dev)
         t = time.perf_counter()
         rep = gmres(op, b, tol=1e-6, restart=50, max_iter=args.gmres_max_iter)
@@ -322,16 +352,34 @@ def run_ours(args):
         gmres_s = time.perf_counter() - t
     clocks = sampler.summary()
 
+    # the same operator without the cell symmetries (a general mesh): the cost
+    # model's path and its time per product
+    nosym = None
+    if world == 1 and not args.no_nosym:
+        op2 = FmmOperators(data, device=dev.index, near_blocks=near, use_symmetries=False)
+        op2.set_stream(stream.cuda_stream)
+        for _ in range(warmup):
+            op2.matvec(x)
+        ms2 = min(timed_batches(lambda: op2.matvec(x), args.steps, args.trials, stream, barrier)) / args.steps
+        p2 = op2.near_path()
+        nosym = {"near_path": p2[0], "near_lattice": list(p2[1]), "ms_per_step": ms2, "value": data.N / (ms2 * 1e-3),
+                 "note": "same operator, cell symmetries not used (one stored block per Fourier mode pair)"}
+        op2.close()
+        del op2
+
     # max over ranks
+    ms = min(trials_ms)
+    e2e_s = min(e2e_trials)
     vals = torch.tensor([ms, e2e_s, gmres_s], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     ms, e2e_s, gmres_s = (float(v) for v in vals.cpu())
 
     path, lat_sizes, spec_bytes, modes_per_block, sym_mask, sym_dev = op.near_path()
+    per = lambda st, k: st[k] / max(1, st["applies"])  # noqa: E731
     # roofline of the dominant kernel. Direct path: the near-field DMMA GEMM,
-    # algorithmic flops per launch; lattice path: the per-mode GEMV, HBM-bound,
-    # algorithmic bytes per launch = the block spectrum + x_hat read + y_hat written
+    # algorithmic flops per launch; lattice path: the per-mode block product, HBM-bound,
+    # algorithmic bytes per launch = the stored block spectrum + x_hat read + y_hat written
     m = data.counts
     n_pairs = int(sum((m[0] - abs(int(o[0]))) * (m[1] - abs(int(o[1]))) * (m[2] - abs(int(o[2])))
                       for o in data.near_offsets))
@@ -340,20 +388,23 @@ def run_ours(args):
         lo, hi, far_pairs = op.partition()
         n_pairs = hi - lo
     flops = 8.0 * data.n_dof ** 2 * float(n_pairs)
-    gemm_ms = stages["near_gemm"] / max(1, stages["applies"])
+    gemm_ms = per(stages, "near_gemm")
     if path == "lattice":
         q_near = int(np.prod(lat_sizes))
-        lo, hi, far_pairs = op.partition()  # modes of this rank
+        lo, hi, far_pairs = op.partition()  # stored blocks of this rank
         mode_bytes = 16.0 * data.n_dof ** 2 * (hi - lo) + 2 * 16.0 * data.n_dof * q_near
-        mode_ms = stages["near_mode_product"] / max(1, stages["applies"])
+        mode_ms = per(stages, "near_mode_product")
         peak, peak_src = hbm_peak()
-        traffic = kernel_traffic(ROOT / "profiles" / "near_mode_gemv_traffic.json")
-        roofline = {"kernel": "near_mode_gemv_kernel", "bound": "hbm", "achieved": mode_bytes / (mode_ms * 1e-3) / 1e9,
+        traffic = kernel_traffic(ROOT / "profiles" / "near_mode_traffic.json")
+        roofline = {"kernel": "near-field mode product", "bound": "hbm",
+                    "achieved": mode_bytes / (mode_ms * 1e-3) / 1e9,
                     "peak": peak, "unit": "GB/s", "peak_source": peak_src, "algorithmic_bytes": mode_bytes,
+                    "bytes_per_unit": f"16 n^2 per stored block ({hi - lo} blocks of n = {data.n_dof}) "
+                                      f"+ 2 x 16 n per near-lattice mode ({q_near} modes)",
                     # a read-only stream can beat the read+write copy figure: also against the nominal HBM3e rate
                     "frac_of_nominal_7700": mode_bytes / (mode_ms * 1e-3) / 1e9 / 7700.0,
                     "launch_ms": mode_ms, "near_stage_ms": gemm_ms,
-                    "near_stage_share_of_step": gemm_ms / (stages["total"] / max(1, stages["applies"]))}
+                    "near_stage_share_of_step": gemm_ms / per(stages, "total")}
     else:
         peak, peak_src = fp64_peak()
         traffic = kernel_traffic(TRAFFIC_FILE)
@@ -366,6 +417,27 @@ def run_ours(args):
         traffic = None  # the committed ncu capture is of another workload
     roofline["traffic"] = (traffic or {}).get("dram_bytes_per_launch")
     roofline["traffic_source"] = (traffic or {}).get("source")
+
+    # M2L stage (pruned lattice DFTs + the Λ stream), timed alone (serial stage timing)
+    fsz, paired = op.far_info()
+    b = data.n_coef
+    q = int(np.prod(fsz))
+    n_cells = int(np.prod(data.counts))
+    m2l_ms = per(stages_serial, "m2l")
+    lam_full = 16.0 * q * b * b
+    lam_read = lam_full / 2 if paired else lam_full
+    io = 2 * 16.0 * b * n_cells
+    hbm, hbm_src = hbm_peak()
+    m2l_roof = {"stage": "M2L (x+y plane DFTs, z-DFT/mode-product pipeline, inverse)", "bound": "hbm",
+                "launch_ms": m2l_ms, "peak": hbm, "unit": "GB/s", "peak_source": hbm_src,
+                "lambda_paired": paired, "fft_sizes": list(fsz),
+                "compulsory_bytes": lam_read + io,
+                "achieved": (lam_read + io) / (m2l_ms * 1e-3) / 1e9,
+                "frac": (lam_read + io) / (m2l_ms * 1e-3) / 1e9 / hbm,
+                "survey_bytes": lam_full + io,
+                "frac_survey_definition": (lam_full + io) / (m2l_ms * 1e-3) / 1e9 / hbm,
+                "note": "compulsory = the Λ blocks an apply must read (half of q b^2 when mirror-paired) + moments "
+                        "in + locals out; survey = SURVEY §8d's 16 q b^2 + 2 x 16 b n_cells"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(_WithNear(data, near.cpu().numpy()), xh)
@@ -376,7 +448,7 @@ def run_ours(args):
         value = units * args.steps / (ms * 1e-3)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "warmup": warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "complex128",
             "data": "synthetic (seeded U[-1,1] input; operator assembled from the config geometry)",
             "config": {
@@ -392,19 +464,31 @@ def run_ours(args):
                        "every step" if path == "lattice" else
                        f"inputs larger than L2: near-field operator {16 * data.n_near * data.n_dof ** 2 / 1e9:.2f} GB "
                        "streamed from HBM every step"),
+                "protocol": f"reference (src/scene.cpp:528-544): {warmup} warm-up products, {args.trials} batches "
+                            f"of exactly {args.steps} products, best batch reported",
                 "assembly_s": round(t_asm, 3), "assembly_host_s": round(t_host_asm, 3),
                 "assembly_device_near_s": round(t_dev_asm, 3), "create_s": round(t_up, 3),
             },
-            "stages_ms": {k: (v / max(1, stages["applies"]) if k != "applies" else v) for k, v in stages.items()},
+            "trials_ms": trials_ms,
+            "batch_ms": ms,
+            "value_median": units * args.steps / (statistics.median(trials_ms) * 1e-3),
+            "stages_ms": {k: (per(stages, k) if k != "applies" else v) for k, v in stages.items()},
+            "stages_serial_ms": {k: (per(stages_serial, k) if k != "applies" else v)
+                                 for k, v in stages_serial.items()},
             "roofline": roofline,
+            "roofline_m2l": m2l_roof,
             "e2e": {"value": units * args.steps / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": 16 * data.N, "d2h_bytes_per_step": 16 * data.N},
+                    "h2d_bytes_per_step": 16 * data.N, "d2h_bytes_per_step": 16 * data.N,
+                    "trials_s": e2e_trials, "fraction_of_device_resident": (units * args.steps / e2e_s) / value},
             "gmres": {"solve_s": gmres_s, "iterations": rep.iterations, "converged": rep.converged,
-                      "tol": 1e-6, "restart": 50, "final_estimate": rep.residual_history[-1]
-                      if rep.residual_history else None},
+                      "tol": 1e-6, "restart": 50, "max_iter": args.gmres_max_iter,
+                      "final_estimate": rep.residual_history[-1] if rep.residual_history else None,
+                      "ms_per_iteration": 1e3 * gmres_s / max(1, rep.iterations)},
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if nosym is not None:
+            line["no_symmetry"] = nosym
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -419,12 +503,14 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--trials", type=int, default=5, help="timed batches of --steps products; best reported")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--gmres-max-iter", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nosym", action="store_true", help="skip the no-symmetry timing")
     ap.add_argument("--parallelism", choices=["pairs", "replicas"], default="pairs",
                     help="N>1: split the near-field pairs (NCCL all-reduce) or run independent replicas")
     args = ap.parse_args()

@@ -216,10 +216,24 @@ int fpbem_cu_fmm_near_path(const fpbem_cu_op* op, int* path, int* sizes, size_t*
 /* Spectrum readback (sizes[3] always; lambda_out may be NULL). */
 int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out);
 
+/* Far-field M2L layout for roofline accounting: *paired = 1 when the spectrum's
+ * mirror parity Λ(-q) = D Λ(q) D was verified and each Λ block is streamed once
+ * for a mode and its mirror, so an apply reads about half of
+ * q b^2 blocks. */
+int fpbem_cu_far_info(const fpbem_cu_op* op, int* sizes, int* paired);
+
 /* Run subsequent device work on an external cudaStream_t (NULL = own stream). */
 int fpbem_cu_set_stream(fpbem_cu_op* op, void* stream);
 
-/* Per-stage CUDA-event timing of applies (0 = off). When on, each apply
+/* The cudaStream_t device work of this handle is ordered on (its own
+ * non-blocking stream unless set_stream gave one). Callers that produce inputs
+ * or consume outputs on another stream order the two with events around
+ * fpbem_cu_fmm_apply(..., FPBEM_CU_PTR_DEVICE). */
+int fpbem_cu_get_stream(const fpbem_cu_op* op, void** stream);
+
+/* Per-stage CUDA-event timing of applies (0 = off, 1 = on, 2 = on with
+ * P2M + M2L moved from the concurrent aux stream onto the main stream, so each
+ * stage is timed alone; the product is unchanged). When on, each apply
  * accumulates milliseconds per stage; fpbem_cu_stage_times copies
  * {near field, near_reduce_l2p (or L2P), p2m, m2l, total, applies,
  * lattice-path mode product} into ms_out[7]

@@ -471,17 +471,63 @@ struct GmresResult {
   std::vector<double> history;
 };
 
+// Level-1 operations. By default single-threaded, like Eigen's level-1 code
+// in the reference (Eigen parallelises only GEMM). CHECKER mode
+// (oracle_set_level1_parallel) splits them into fixed chunks over the OpenMP
+// threads with the partial sums combined in chunk order (deterministic for a
+// fixed thread count): only for stated-size GMRES parity checks, never for the
+// timed CPU baseline.
+int g_level1_parallel = 0;
+
+template <typename T, typename F>
+T chunked_sum(long long n, F f) {
+  if (!g_level1_parallel || n < (1 << 15)) return f(0LL, n);
+#ifdef _OPENMP
+  const int nt = omp_get_max_threads();
+#else
+  const int nt = 1;
+#endif
+  std::vector<T> part(nt, T(0));
+#pragma omp parallel for schedule(static) num_threads(nt)
+  for (int c = 0; c < nt; ++c) part[c] = f(n * c / nt, n * (c + 1) / nt);
+  T s(0);
+  for (int c = 0; c < nt; ++c) s += part[c];
+  return s;
+}
+
+template <typename F>
+void chunked_for(long long n, F f) {
+  if (!g_level1_parallel || n < (1 << 15)) {
+    f(0LL, n);
+    return;
+  }
+#pragma omp parallel for schedule(static)
+  for (long long c = 0; c < 64; ++c) f(n * c / 64, n * (c + 1) / 64);
+}
+
 double norm2(const cd* v, long long n) {
-  double s = 0.0;
-  for (long long i = 0; i < n; ++i) s += std::norm(v[i]);
+  const double s = chunked_sum<double>(n, [&](long long lo, long long hi) {
+    double t = 0.0;
+    for (long long i = lo; i < hi; ++i) t += std::norm(v[i]);
+    return t;
+  });
   return std::sqrt(s);
 }
 
 // Eigen's x.dot(y) conjugates the first argument
 cd dotc(const cd* a, const cd* b, long long n) {
-  cd s(0.0, 0.0);
-  for (long long i = 0; i < n; ++i) s += std::conj(a[i]) * b[i];
-  return s;
+  return chunked_sum<cd>(n, [&](long long lo, long long hi) {
+    cd t(0.0, 0.0);
+    for (long long i = lo; i < hi; ++i) t += std::conj(a[i]) * b[i];
+    return t;
+  });
+}
+
+// w -= h v
+void axpy_sub(cd* w, cd h, const cd* v, long long n) {
+  chunked_for(n, [&](long long lo, long long hi) {
+    for (long long k = lo; k < hi; ++k) w[k] -= h * v[k];
+  });
 }
 
 bool all_finite(const cd* v, long long n) {
@@ -532,7 +578,9 @@ GmresResult gmres(ApplyCb apply, void* actx, ApplyCb precond, void* pctx, const 
   double rnorm = bnorm;
 
   while (rep.iterations < max_iter) {
-    for (long long k = 0; k < n; ++k) col(0)[k] = r[k] / rnorm;
+    chunked_for(n, [&](long long lo, long long hi) {
+      for (long long k = lo; k < hi; ++k) col(0)[k] = r[k] / rnorm;
+    });
     std::fill(g.begin(), g.end(), cd(0.0, 0.0));
     g[0] = rnorm;
     int j = 0;
@@ -542,21 +590,21 @@ GmresResult gmres(ApplyCb apply, void* actx, ApplyCb precond, void* pctx, const 
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt (:58-62)
         cd hij = dotc(col(i), w.data(), n);
         H(i, j) = hij;
-        const cd* vi = col(i);
-        for (long long k = 0; k < n; ++k) w[k] -= hij * vi[k];
+        axpy_sub(w.data(), hij, col(i), n);
       }
       if (norm2(w.data(), n) < 0.5 * pre_norm) {  // one reorthogonalisation pass (:63-69)
         for (int i = 0; i <= j; ++i) {
           cd corr = dotc(col(i), w.data(), n);
           H(i, j) += corr;
-          const cd* vi = col(i);
-          for (long long k = 0; k < n; ++k) w[k] -= corr * vi[k];
+          axpy_sub(w.data(), corr, col(i), n);
         }
       }
       const double hlast = norm2(w.data(), n);
       H(j + 1, j) = hlast;
       if (hlast > 0.0)
-        for (long long k = 0; k < n; ++k) col(j + 1)[k] = w[k] / hlast;
+        chunked_for(n, [&](long long lo, long long hi) {
+          for (long long k = lo; k < hi; ++k) col(j + 1)[k] = w[k] / hlast;
+        });
       for (int i = 0; i < j; ++i) {  // old rotations (:75-79)
         cd t = giv_c[i] * H(i, j) + giv_s[i] * H(i + 1, j);
         H(i + 1, j) = -std::conj(giv_s[i]) * H(i, j) + giv_c[i] * H(i + 1, j);
@@ -599,10 +647,14 @@ GmresResult gmres(ApplyCb apply, void* actx, ApplyCb precond, void* pctx, const 
     for (int i = 0; i < j; ++i) {
       const cd* vi = col(i);
       const cd yi = y[i];
-      for (long long k = 0; k < n; ++k) x[k] += vi[k] * yi;
+      chunked_for(n, [&](long long lo, long long hi) {
+        for (long long k = lo; k < hi; ++k) x[k] += vi[k] * yi;
+      });
     }
     apply_eff(x.data(), w.data());  // true residual (:111-112)
-    for (long long k = 0; k < n; ++k) r[k] = b_eff[k] - w[k];
+    chunked_for(n, [&](long long lo, long long hi) {
+      for (long long k = lo; k < hi; ++k) r[k] = b_eff[k] - w[k];
+    });
     rnorm = norm2(r.data(), n);
     if (rnorm / bnorm <= tol) {
       rep.converged = true;
@@ -643,6 +695,13 @@ void oracle_set_num_threads(int n) {
 }
 
 int oracle_fft_friendly(int n) { return oracle::fft_friendly(n); }
+
+// CHECKER mode of the GMRES level-1 operations (see chunked_sum); returns the previous setting
+int oracle_set_level1_parallel(int on) {
+  const int prev = oracle::g_level1_parallel;
+  oracle::g_level1_parallel = on != 0;
+  return prev;
+}
 
 static oracle::Toeplitz make_toeplitz(const int* counts, int b, int n_off, const int* offsets,
                                       const double* blocks) {

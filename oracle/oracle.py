@@ -36,6 +36,7 @@ def lib() -> C.CDLL:
             "oracle_num_threads": (C.c_int, []),
             "oracle_set_num_threads": (None, [C.c_int]),
             "oracle_fft_friendly": (C.c_int, [C.c_int]),
+            "oracle_set_level1_parallel": (C.c_int, [C.c_int]),
             "oracle_toeplitz_matvec": (C.c_int, [_ip, C.c_int, C.c_int, _ip, vp, vp, vp]),
             "oracle_toeplitz_expand_dense": (C.c_int, [_ip, C.c_int, C.c_int, _ip, vp, vp]),
             "oracle_hankel_matvec": (C.c_int, [_ip, C.c_int, C.c_int, C.c_int, _ip, vp, vp, vp]),
@@ -255,3 +256,141 @@ def gmres(apply, b, tol=1e-4, restart=100, max_iter=1000, preconditioner=None):
         raise errs[0]
     _check(rc)
     return x, its.value, bool(conv.value), list(hist[: hl.value])
+
+
+class _NoNear:
+    """FmmData view with the near field removed (the far-field part of
+    FmmOperators::matvec alone: P2M -> CirculantSpectrum::matvec -> L2P)."""
+
+    def __init__(self, data):
+        self._d = data
+        self.near_offsets = np.zeros((0, 3), np.int32)
+        self.near_blocks = np.zeros((0,), np.complex128)
+        self.hat_indices = np.zeros((0, 3), np.int32)
+        self.hat_blocks = np.zeros((0,), np.complex128)
+
+    def __getattr__(self, k):
+        return getattr(self._d, k)
+
+
+def toeplitz_matvec_blocked(counts, offsets, blocks, p, n) -> np.ndarray:
+    """BlockToeplitzMatrix::matvec (src/assembly.cpp:62-84) regrouped for the
+    CHECKER: per stored offset, in the stored order, one dense product over all
+    of its valid targets (numpy/BLAS zgemm), added to the targets' sums. Every
+    target still sums its offsets in the stored order; only the order inside a
+    block product differs from the reference's GEMV per (target, offset), at
+    rounding level. Used where the GEMV-per-pair restatement is too slow for
+    hundreds of products (stated-size GMRES parity); single matvecs are checked
+    against the restatement itself."""
+    m0, m1, m2 = (int(c) for c in counts)
+    blk = np.asarray(blocks, np.complex128).reshape(-1, n, n)  # blk[s] = S_s^T (column-major storage)
+    X = np.asarray(p, np.complex128).reshape(m2, m1, m0, n)
+    Y = np.zeros_like(X)
+    for s, (ox, oy, oz) in enumerate(np.asarray(offsets, np.int64).reshape(-1, 3)):
+        rng = []
+        for o, m in ((oz, m2), (oy, m1), (ox, m0)):
+            lo, hi = max(0, o), min(m, m + o)  # targets t with 0 <= t - o < m
+            rng.append((lo, hi, o))
+        if any(hi <= lo for lo, hi, _ in rng):
+            continue
+        (z0, z1, oz_), (y0, y1, oy_), (x0, x1, ox_) = rng
+        src = X[z0 - oz_:z1 - oz_, y0 - oy_:y1 - oy_, x0 - ox_:x1 - ox_].reshape(-1, n)
+        Y[z0:z1, y0:y1, x0:x1] += (src @ blk[s]).reshape(z1 - z0, y1 - y0, x1 - x0, n)
+    return Y.reshape(-1)
+
+
+class OracleFmmChecker:
+    """CHECKER-ONLY fast form of FmmOperators::matvec for stated-size GMRES
+    parity: the near field through toeplitz_matvec_blocked (per-offset BLAS
+    products, multi-threaded), the far field (P2M, CirculantSpectrum::matvec,
+    L2P, src/fmm.cpp:256-267) through the restatement in fpbem_oracle.cpp, and
+    GMRES through the restatement's solver::gmres (src/solver.cpp:21-123) with
+    this product as its ApplyFn. Not for half-space operators (the restatement
+    covers those)."""
+
+    def __init__(self, data, near: str = "blas"):
+        if int(getattr(data, "mirrored_level", -1)) >= 0:
+            raise ValueError("OracleFmmChecker: no half-space image terms")
+        if near not in ("blas", "fft"):
+            raise ValueError("OracleFmmChecker: near must be 'blas' or 'fft'")
+        self.counts = tuple(int(c) for c in data.counts)
+        self.n = int(data.n_dof)
+        self.N = int(np.prod(self.counts)) * self.n
+        self.near_offsets = np.asarray(data.near_offsets, np.int32).reshape(-1, 3)
+        self.near_blocks = np.asarray(data.near_blocks, np.complex128).reshape(-1, self.n, self.n)
+        self.far = OracleFmm(_NoNear(data))  # builds the spectrum with the restatement (src/structured.cpp:63-108)
+        self.b = int(data.n_coef)
+        self.v0t = np.asarray(data.v0, np.complex128).reshape(self.n, self.b)  # [j][i] = V0[i][j]
+        self.u0t = np.asarray(data.u0, np.complex128).reshape(self.b, self.n)  # [m][i] = U0[i][m]
+        q = int(np.prod(self.far.sizes))
+        self.lam_t = self.far.lambda_.reshape(q, self.b, self.b).transpose(0, 2, 1)  # [q] = Λ_q (row-major view)
+        self.matvecs = 0
+        self.near_mode = near
+        if near == "fft":
+            self._near_spectrum()
+
+    def _near_spectrum(self) -> None:
+        """Near field by the convolution theorem (CHECKER for many products over
+        many offsets, e.g. cfg2's 125): the S_o embedded at slot o mod Ln with
+        Ln_d = M_d + max|o_d| (no aliasing into the kept targets) and DFT'd once
+        over the lattice axes (scipy.fft, multi-threaded); each product is then a
+        pruned forward DFT, one n x n GEMV per mode and an inverse DFT."""
+        import scipy.fft as sf
+
+        R = np.abs(self.near_offsets).max(axis=0) if len(self.near_offsets) else np.zeros(3, int)
+        self.nl = tuple(int(m + r) if m > 1 else 1 for m, r in zip(self.counts, R))  # (Lx, Ly, Lz)
+        lx, ly, lz = self.nl
+        n = self.n
+        Sh = np.zeros((lz, ly, lx, n, n), np.complex128)
+        for s, (ox, oy, oz) in enumerate(self.near_offsets):
+            Sh[oz % lz, oy % ly, ox % lx] = self.near_blocks[s].T  # S_o (row = target)
+        self.Sh = sf.fftn(Sh, axes=(0, 1, 2), workers=-1, overwrite_x=True).reshape(-1, n, n)
+
+    def near_matvec(self, p) -> np.ndarray:
+        if self.near_mode == "blas":
+            return toeplitz_matvec_blocked(self.counts, self.near_offsets, self.near_blocks, p, self.n)
+        import scipy.fft as sf
+
+        m0, m1, m2 = self.counts
+        lx, ly, lz = self.nl
+        X = np.zeros((lz, ly, lx, self.n), np.complex128)
+        X[:m2, :m1, :m0] = p.reshape(m2, m1, m0, self.n)
+        Xh = sf.fftn(X, axes=(0, 1, 2), workers=-1).reshape(-1, self.n, 1)
+        Yh = np.matmul(self.Sh, Xh).reshape(lz, ly, lx, self.n)
+        Y = sf.ifftn(Yh, axes=(0, 1, 2), workers=-1)
+        return np.ascontiguousarray(Y[:m2, :m1, :m0]).reshape(-1)
+
+    def far_matvec(self, p) -> np.ndarray:
+        """U0 IFFT(Λ FFT(pad(V0 p))) (src/fmm.cpp:256-267, src/structured.cpp:122-166)
+        with multi-threaded transforms (scipy.fft workers) on the restatement's Λ."""
+        import scipy.fft as sf
+
+        m0, m1, m2 = self.counts
+        lx, ly, lz = self.far.sizes
+        P = p.reshape(-1, self.n)
+        mom = P @ self.v0t  # (cells, b): M_c = V0 p_c
+        field = np.zeros((lz, ly, lx, self.b), np.complex128)
+        field[:m2, :m1, :m0] = mom.reshape(m2, m1, m0, self.b)
+        F = sf.fftn(field, axes=(0, 1, 2), workers=-1).reshape(-1, self.b, 1)  # unnormalised, sign -1
+        img = np.matmul(self.lam_t, F).reshape(lz, ly, lx, self.b)
+        back = sf.ifftn(img, axes=(0, 1, 2), workers=-1)  # sign +1 and the 1/q of :156-164
+        loc = np.ascontiguousarray(back[:m2, :m1, :m0]).reshape(-1, self.b)
+        return (loc @ self.u0t).reshape(-1)
+
+    def matvec(self, p) -> np.ndarray:
+        p = np.ascontiguousarray(p, np.complex128)
+        out = []
+        for r in range(p.size // self.N):
+            pr = p[r * self.N:(r + 1) * self.N]
+            y = self.near_matvec(pr)
+            y += self.far_matvec(pr)
+            out.append(y)
+            self.matvecs += 1
+        return np.concatenate(out) if len(out) > 1 else out[0]
+
+    def gmres(self, b, tol=1e-4, restart=100, max_iter=1000):
+        prev = lib().oracle_set_level1_parallel(1)
+        try:
+            return gmres(self.matvec, b, tol=tol, restart=restart, max_iter=max_iter)
+        finally:
+            lib().oracle_set_level1_parallel(prev)

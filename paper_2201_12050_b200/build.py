@@ -7,8 +7,10 @@ with the repo snapshot to the GPU box).
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 import sys
 from pathlib import Path
 
@@ -26,6 +28,10 @@ CUDA_SOURCES = ["near_field.cu", "m2l.cu", "krylov.cu", "assembly.cu", "far_bank
 HOST_SOURCES = ["geometry.cpp", "kernels.cpp", "specfun.cpp", "assembly.cpp", "postproc.cpp", "capi.cpp"]
 # portable x86-64 ISA level: the GPU box CPU may differ from the build container's
 CPU_FLAGS = ["-O3", "-march=x86-64-v3", "-fPIC", "-fopenmp", "-std=c++17"]
+# the oracle's complex products without the C99 Annex G inf/NaN recovery call
+# (__muldc3): identical results for finite operands, and vectorisable like
+# Eigen's complex kernels in the reference
+ORACLE_FLAGS = CPU_FLAGS + ["-fcx-limited-range"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -35,11 +41,27 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError("build failed: " + " ".join(cmd[:4]) + " ...")
 
 
-def _stale(target: Path, sources: list[Path]) -> bool:
-    if not target.exists():
+def _digest(sources: list[Path], flags: list[str]) -> str:
+    h = hashlib.sha256()
+    for f in flags:
+        h.update(f.encode() + b"\0")
+    for s in sorted(sources):
+        h.update(s.name.encode() + b"\0" + s.read_bytes())
+    return h.hexdigest()
+
+
+def _stale(target: Path, sources: list[Path], flags: list[str] = ()) -> bool:
+    """Rebuild unless the target exists and its stamp holds the hash of the
+    current sources and flags (content, not mtimes: a repo snapshot or a fresh
+    checkout may carry an old binary with newer-looking timestamps, or the reverse)."""
+    stamp = target.with_name(target.name + ".stamp")
+    if not target.exists() or not stamp.exists():
         return True
-    t = target.stat().st_mtime
-    return any(s.stat().st_mtime > t for s in sources)
+    return stamp.read_text().strip() != _digest(sources, list(flags))
+
+
+def _stamp(target: Path, sources: list[Path], flags: list[str] = ()) -> None:
+    target.with_name(target.name + ".stamp").write_text(_digest(sources, list(flags)) + "\n")
 
 
 def build_cuda(force: bool = False) -> Path:
@@ -47,16 +69,17 @@ def build_cuda(force: bool = False) -> Path:
     out = LIB / "libfpbem_cuda.so"
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [
         ROOT / "include" / "fpbem_cuda.h"]
-    if force or _stale(out, deps):
-        objs = []
-        for s in CUDA_SOURCES:
-            obj = LIB / (Path(s).stem + ".o")
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                  "-c", str(CSRC / s), "-o", str(obj)])
-            objs.append(str(obj))
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+    if force or _stale(out, deps, flags):
+        objs = [str(LIB / (Path(s).stem + ".o")) for s in CUDA_SOURCES]
+        jobs = max(1, min(len(CUDA_SOURCES), os.cpu_count() or 1))
+        with ThreadPoolExecutor(jobs) as ex:  # one nvcc per translation unit, in parallel
+            list(ex.map(lambda so: _run([NVCC, *flags, "-c", str(CSRC / so[0]), "-o", so[1]]),
+                        zip(CUDA_SOURCES, objs)))
         _run([NVCC, *ARCH, "-shared", "-o", str(out), *objs, "-ldl"])
         for o in objs:
             Path(o).unlink(missing_ok=True)
+        _stamp(out, deps, flags)
     return out
 
 
@@ -64,8 +87,9 @@ def build_host(force: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libfpbem_host.so"
     deps = [HOST / s for s in HOST_SOURCES] + list(HOST.glob("*.hpp")) + [CSRC / "gaunt.hpp"]
-    if force or _stale(out, deps):
+    if force or _stale(out, deps, CPU_FLAGS):
         _run(["g++", *CPU_FLAGS, "-shared", "-o", str(out), *[str(HOST / s) for s in HOST_SOURCES]])
+        _stamp(out, deps, CPU_FLAGS)
     return out
 
 
@@ -74,8 +98,9 @@ def build_oracle(force: bool = False) -> Path:
     out_dir.mkdir(exist_ok=True)
     out = out_dir / "liboracle.so"
     src = ORACLE / "fpbem_oracle.cpp"
-    if force or _stale(out, [src]):
-        _run(["g++", *CPU_FLAGS, "-shared", "-o", str(out), str(src)])
+    if force or _stale(out, [src], ORACLE_FLAGS):
+        _run(["g++", *ORACLE_FLAGS, "-shared", "-o", str(out), str(src)])
+        _stamp(out, [src], ORACLE_FLAGS)
     return out
 
 
@@ -85,9 +110,10 @@ def build_driver(force: bool = False) -> Path:
     src = ROOT / "tools" / "cpp_scene_solve.cpp"
     deps = [src, LIB / "libfpbem_host.so", LIB / "libfpbem_cuda.so", ROOT / "include" / "fpbem_cuda.hpp",
             ROOT / "include" / "fpbem_cuda.h"] + list(HOST.glob("*.hpp"))
-    if force or _stale(out, deps):
+    if force or _stale(out, deps, ["driver"]):
         _run(["g++", "-O2", "-std=c++17", "-I", str(ROOT / "include"), "-I", str(HOST), str(src), "-L", str(LIB),
               "-lfpbem_host", "-lfpbem_cuda", f"-Wl,-rpath,{LIB}", "-fopenmp", "-o", str(out)])
+        _stamp(out, deps, ["driver"])
     return out
 
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace fpbem_cu {
@@ -33,7 +34,36 @@ __host__ __device__ __forceinline__ c64 cfma_conj(c64 a, c64 b, c64 acc) {
 }
 __host__ __device__ __forceinline__ c64 cscale(c64 a, double s) { return cmk(a.x * s, a.y * s); }
 
-constexpr int kNumSMs = 148;
+constexpr int kNumSMs = 148;  // grid-sizing hint only; co-residency checks use device_sms()
+
+// SM count of the current device (cached per device)
+inline int device_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMs;
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = kNumSMs;
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+constexpr int kMaxDynSmem = 227 * 1024;  // sm_100a opt-in limit per CTA
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (call site, device):
+// the attribute is per device context, so a process-wide flag would skip it on
+// a second GPU
+inline cudaError_t ensure_max_smem(std::atomic<unsigned long long>& done, const void* func, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // cp.async 16-byte global->shared copy with zero fill when !valid
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {

@@ -656,7 +656,7 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
     const char* v = std::getenv("FPBEM_SERIAL");
     return v && std::strcmp(v, "1") == 0;
   }();
-  cudaStream_t a = serial ? op->stream : op->aux;
+  cudaStream_t a = (serial || op->serial_timing) ? op->stream : op->aux;
   const bool far_here = op->rank == 0;
   if (!op->near_fft) build_jobs(op, nrhs);
   // fork: P2M + M2L on the aux stream while the near field runs on the main one
@@ -1079,6 +1079,13 @@ int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out) 
   });
 }
 
+int fpbem_cu_far_info(const fpbem_cu_op* op, int* sizes, int* paired) {
+  if (!op || !sizes || !paired) return FPBEM_CU_EINVAL;
+  for (int k = 0; k < 3; ++k) sizes[k] = op->L[k];
+  *paired = op->lam_paired ? 1 : 0;
+  return FPBEM_CU_OK;
+}
+
 int fpbem_cu_set_stream(fpbem_cu_op* op, void* stream) {
   return guard([&] {
     if (!op) fail(FPBEM_CU_EINVAL, "set_stream: null op");
@@ -1095,9 +1102,16 @@ int fpbem_cu_set_stream(fpbem_cu_op* op, void* stream) {
   });
 }
 
+int fpbem_cu_get_stream(const fpbem_cu_op* op, void** stream) {
+  if (!op || !stream) return FPBEM_CU_EINVAL;
+  *stream = static_cast<void*>(op->stream);
+  return FPBEM_CU_OK;
+}
+
 int fpbem_cu_enable_stage_timing(fpbem_cu_op* op, int enable) {
   if (!op) return FPBEM_CU_EINVAL;
   op->timing = enable != 0;
+  op->serial_timing = enable == 2;
   return FPBEM_CU_OK;
 }
 

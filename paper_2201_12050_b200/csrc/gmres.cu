@@ -439,7 +439,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
     }
     if (!norm_set.empty()) {
       set_mask(norm_set);
-      put(o_d, hl.data(), g8);
+      put(o_d, hl.data(), 8 * static_cast<size_t>(G));
       check(launch_b_div(W, W, n, n, G, d_mask, d_d, s), "normalise");
       op->launches++;
     }
@@ -462,7 +462,7 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
       if (!done[r] && out.iterations[r] < max_iter) act.push_back(r);
     if (act.empty()) break;
     set_mask(act);
-    put(o_d, rnorm.data(), g8);
+    put(o_d, rnorm.data(), 8 * static_cast<size_t>(G));
     check(launch_b_div(rsrc, V, n, n, G, d_mask, d_d, s), "v0");  // v0 = r / ||r||
     for (int r : act) {
       cyc[r].start(rnorm[r]);

@@ -188,6 +188,7 @@ struct fpbem_cu_op {
 
   // timing
   bool timing = false;
+  bool serial_timing = false;  // stage timing with the far field on the main stream (exact stage times)
   cudaEvent_t ev[10] = {};
   double stage_ms[6] = {0, 0, 0, 0, 0, 0};  // + [5]: lattice-path mode product (events 7-8)
   long long applies = 0;

@@ -722,7 +722,21 @@ cudaError_t launch_b_pack(const c64* src, c64* dst, const int* idx, int count, l
   return cudaGetLastError();
 }
 
-bool mgs_fused_supported(long long n) { return n <= static_cast<long long>(kNumSMs) * kMgsMaxChunk; }
+// the cooperative grid needs every block co-resident: at most one per SM of the
+// current device, and the occupancy calculator must agree at the largest chunk
+bool mgs_fused_supported(long long n) {
+  static std::atomic<unsigned long long> configured{0};
+  if (ensure_max_smem(configured, reinterpret_cast<const void*>(&mgs_fused_kernel),
+                      static_cast<int>(kMgsMaxChunk * sizeof(c64))) != cudaSuccess)
+    return false;
+  const int sms = device_sms();
+  if (n > static_cast<long long>(sms) * kMgsMaxChunk) return false;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_fused_kernel, kMgsThreads,
+                                                    kMgsMaxChunk * sizeof(c64)) != cudaSuccess)
+    return false;
+  return per_sm >= 1;
+}
 
 cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long long n, c64* h_out, double* norms,
                              int* nonfinite, const RedScratch& rs, bool do_pre, cudaStream_t s, c64* hc_out) {
@@ -732,18 +746,15 @@ cudaError_t launch_mgs_fused(c64* w, const c64* V, long long ld, int j, long lon
     return v ? std::max(1LL, std::atoll(v)) : 1024LL;
   }();
   long long blocks = (n + per_block - 1) / per_block;
-  if (blocks > kNumSMs) blocks = kNumSMs;
+  if (blocks > device_sms()) blocks = device_sms();
   if (blocks < 1) blocks = 1;
   long long chunk = (n + blocks - 1) / blocks;
   if (chunk > kMgsMaxChunk) return cudaErrorInvalidValue;
   size_t smem = static_cast<size_t>(chunk) * sizeof(c64);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(mgs_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kMgsMaxChunk * sizeof(c64)));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<unsigned long long> configured{0};
+  cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&mgs_fused_kernel),
+                                  static_cast<int>(kMgsMaxChunk * sizeof(c64)));
+  if (e != cudaSuccess) return e;
   int pre = do_pre ? 1 : 0;
   c64* pc = rs.partial_c;
   double* pd = rs.partial_d;
@@ -761,13 +772,12 @@ cudaError_t launch_cgs_dots(const c64* V, long long ld, int cols, const c64* w, 
                             unsigned* counter, c64* out, cudaStream_t s) {
   if (cols < 0 || cols >= kCgsMaxCols) return cudaErrorInvalidValue;
   const size_t smem = static_cast<size_t>(cols + 1) * kCgsWarps * sizeof(c64);
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
+  static std::atomic<unsigned long long> configured{0};
+  if (smem > 48 * 1024) {
     const size_t cap = static_cast<size_t>(kCgsMaxCols) * kCgsWarps * sizeof(c64);
-    cudaError_t e = cudaFuncSetAttribute(cgs_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(cap));
+    cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&cgs_dots_kernel),
+                                    static_cast<int>(cap));
     if (e != cudaSuccess) return e;
-    configured = cap;
   }
   cgs_dots_kernel<<<cgs_blocks(n), RT, smem, s>>>(V, ld, cols, w, n, partials, counter, out);
   return cudaGetLastError();

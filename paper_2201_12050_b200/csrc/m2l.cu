@@ -970,15 +970,15 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
   if (dft_mma && n_in <= kDftMmaMax && n_out <= kDftMmaMax) {
     const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
     const size_t smem = sizeof(double) * 3 * MT * KT * 32;
-    static bool raised = false;
-    if (!raised) {
+    static std::atomic<unsigned long long> raised[4];
+    {
+      int i = 0;
       for (auto fn : {dft_axis_dmma_kernel<4>, dft_axis_dmma_kernel<8>, dft_axis_dmma_kernel<12>,
                       dft_axis_dmma_kernel<16>}) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(sizeof(double) * 3 * 8 * 16 * 32));
+        cudaError_t e = ensure_max_smem(raised[i++], reinterpret_cast<const void*>(fn),
+                                        static_cast<int>(sizeof(double) * 3 * 8 * 16 * 32));
         if (e != cudaSuccess) return e;
       }
-      raised = true;
     }
     const long long tiles = n_a * ((n_inner + 7) / 8);
     long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
@@ -1034,13 +1034,11 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
   const int grid = grid_for(total, 256), bw = backward ? 1 : 0;
   const size_t smem = sizeof(c64) * static_cast<size_t>(L);
   if (smem > 48 * 1024) {  // L > 3072: raise the dynamic shared-memory limit once per instantiation
-    static bool raised = false;
-    if (!raised) {
-      for (auto fn : {dft_axis_kernel<8>, dft_axis_kernel<4>, dft_axis_kernel<2>, dft_axis_kernel<1>}) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return e;
-      }
-      raised = true;
+    static std::atomic<unsigned long long> raised[4];
+    int i = 0;
+    for (auto fn : {dft_axis_kernel<8>, dft_axis_kernel<4>, dft_axis_kernel<2>, dft_axis_kernel<1>}) {
+      cudaError_t e = ensure_max_smem(raised[i++], reinterpret_cast<const void*>(fn), 200 * 1024);
+      if (e != cudaSuccess) return e;
     }
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
   }
@@ -1064,12 +1062,13 @@ cudaError_t launch_xy_plane(const c64* in, c64* out, const c64* twx, const c64* 
                             int Mz, int E, bool inverse, double scale, cudaStream_t stream) {
   const size_t smem = xy_plane_smem(Mx, My, Lx, Ly, inverse);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static size_t raised[2] = {0, 0};
-  if (smem > 48 * 1024 && smem > raised[inverse]) {
-    cudaError_t e = cudaFuncSetAttribute(inverse ? xy_plane_kernel<true> : xy_plane_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  static std::atomic<unsigned long long> raised[2];
+  if (smem > 48 * 1024) {
+    cudaError_t e = ensure_max_smem(raised[inverse ? 1 : 0],
+                                    inverse ? reinterpret_cast<const void*>(&xy_plane_kernel<true>)
+                                            : reinterpret_cast<const void*>(&xy_plane_kernel<false>),
+                                    200 * 1024);
     if (e != cudaSuccess) return e;
-    raised[inverse] = smem;
   }
   const long long planes = static_cast<long long>(Mz) * E;
   if (planes > 0x7fffffffLL) return cudaErrorInvalidValue;
@@ -1096,12 +1095,10 @@ cudaError_t launch_p2m(const c64* v0t, const c64* x, c64* mom, int n, int b, lon
   }();
   const size_t smem = sizeof(c64) * static_cast<size_t>(b) * p2m_pitch(n);
   if (gemm_mode != 0 && (nrhs >= 4 || gemm_mode == 2) && smem <= 200 * 1024) {
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-      cudaError_t e =
-          cudaFuncSetAttribute(p2m_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    static std::atomic<unsigned long long> configured{0};
+    if (smem > 48 * 1024) {
+      cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&p2m_gemm_kernel), 200 * 1024);
       if (e != cudaSuccess) return e;
-      configured = 200 * 1024;
     }
     const long long tiles = (static_cast<long long>(cells) * nrhs + 7) / 8;
     const int grid = static_cast<int>(std::min<long long>(kNumSMs, (tiles + kP2mWarps - 1) / kP2mWarps));
@@ -1127,12 +1124,10 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
   }();
   const size_t smem = sizeof(c64) * (static_cast<size_t>(b) * b + static_cast<size_t>(kModeRows) * (b | 1));
   if (gemm_on && nrhs >= 4 && smem <= 200 * 1024) {
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-      cudaError_t e =
-          cudaFuncSetAttribute(mode_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    static std::atomic<unsigned long long> configured{0};
+    if (smem > 48 * 1024) {
+      cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&mode_gemm_kernel), 200 * 1024);
       if (e != cudaSuccess) return e;
-      configured = smem;
     }
     const dim3 grid(static_cast<unsigned>(q_total), static_cast<unsigned>((nrhs + kModeRows - 1) / kModeRows));
     mode_gemm_kernel<<<grid, 256, smem, stream>>>(lambda, field, image, b, nrhs);
@@ -1192,12 +1187,11 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
   if (n_mw == 0 || b > 256) return cudaErrorInvalidValue;
   const int ring = m2l_zfused_ring(Mz, Lz, E, b);
   const size_t smem = zpipe_fields_bytes(Mz, Lz, E) + sizeof(c64) * static_cast<size_t>(ring) * b * b;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(m2l_zpipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  static std::atomic<unsigned long long> configured{0};
+  if (smem > 48 * 1024) {
+    if (smem > static_cast<size_t>(kMaxDynSmem)) return cudaErrorInvalidValue;
+    cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&m2l_zpipe_kernel), kMaxDynSmem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   const int grid = n_items < kNumSMs ? n_items : kNumSMs;  // persistent: one CTA per SM
   if (grid == 0) return cudaSuccess;

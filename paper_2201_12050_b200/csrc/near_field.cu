@@ -303,8 +303,9 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
   const int row_tiles = (n + RED_THREADS - 1) / RED_THREADS;
   const int tr = static_cast<int>(blockIdx.x / row_tiles);  // t * nrhs + r
   const int t = tr / nrhs, r = tr % nrhs;
-  if (local != nullptr && threadIdx.x < n_coef)
-    loc[threadIdx.x] = local[static_cast<size_t>(tr) * n_coef + threadIdx.x];
+  // strided: n_coef may exceed the CTA size (up to MAX_COEF = 256 for n_t <= 15)
+  if (local != nullptr)
+    for (int m = threadIdx.x; m < n_coef; m += RED_THREADS) loc[m] = local[static_cast<size_t>(tr) * n_coef + m];
   __syncthreads();
   const int i = static_cast<int>(blockIdx.x % row_tiles) * RED_THREADS + threadIdx.x;
   if (i >= n) return;
@@ -342,13 +343,10 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
                               cudaStream_t stream, long long out_rhs_stride, const int* perm) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(near_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemA + kSmemB));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<unsigned long long> configured{0};
+  cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&near_gemm_dmma_kernel),
+                                  static_cast<int>(kSmemA + kSmemB));
+  if (e != cudaSuccess) return e;
   if (n_jobs == 0) return cudaSuccess;
   // 1-D grid, m-tiles of one job adjacent (they share the job's B columns in L2)
   const long long ctas = static_cast<long long>((M + BM - 1) / BM) * n_jobs;
@@ -493,12 +491,9 @@ cudaError_t launch_l2p_add(const c64* u0, const c64* local, c64* y, int n, int n
   if (blocks > 0x7fffffffLL || cols + kL2pCols > 0x7fffffffLL) return cudaErrorInvalidValue;
   const size_t smem = sizeof(c64) * kL2pCols * n_coef;
   if (smem > 48 * 1024) {
-    static bool raised = false;
-    if (!raised) {
-      cudaError_t e = cudaFuncSetAttribute(l2p_add_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      if (e != cudaSuccess) return e;
-      raised = true;
-    }
+    static std::atomic<unsigned long long> raised{0};
+    cudaError_t e = ensure_max_smem(raised, reinterpret_cast<const void*>(&l2p_add_kernel), 64 * 1024);
+    if (e != cudaSuccess) return e;
   }
   l2p_add_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(u0, local, y, n, n_coef, cols, N, nrhs,
                                                                       row_tiles);

@@ -35,6 +35,36 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+class _TorchOrdered:
+    """Orders a library stream against torch's current stream around a
+    device-pointer call: the library waits for torch's producers of the inputs,
+    torch's consumers wait for the library's outputs, and the tensors are
+    recorded on the library stream so the caching allocator does not hand
+    their memory out while the library may still use it."""
+
+    def __init__(self, stream_ptr: int | None, device, tensors):
+        import torch
+
+        self.dev = torch.device(device)
+        self.tensors = tensors
+        self.cur = torch.cuda.current_stream(self.dev)
+        self.lib = torch.cuda.ExternalStream(stream_ptr, device=self.dev) if stream_ptr else None
+
+    def __enter__(self):
+        if self.lib is None:  # the call creates its own stream and syncs: order the inputs before it
+            self.cur.synchronize()
+        else:
+            self.lib.wait_stream(self.cur)
+        return self
+
+    def __exit__(self, *exc):
+        if self.lib is not None:
+            self.cur.wait_stream(self.lib)
+            for t in self.tensors:
+                t.record_stream(self.lib)
+        return False
+
+
 def partition_pairs(n_pairs: int, nranks: int, rank: int, far_pairs: float = 0.0) -> tuple[int, int]:
     """The library's multi-GPU split (host only): this rank's [lo, hi) range of
     the near-field (offset, target) pairs in offset-major order; rank 0, which
@@ -247,6 +277,12 @@ class FmmOperators:
         _raise(_native.cuda().fpbem_cu_spectrum(self._h, sizes, lam.ctypes.data))
         return tuple(sizes), lam
 
+    def far_info(self) -> tuple[tuple[int, int, int], bool]:
+        """(M2L lattice sizes, mirror-paired Λ stream)"""
+        sizes, paired = (C.c_int * 3)(), C.c_int()
+        _raise(_native.cuda().fpbem_cu_far_info(self._h, sizes, C.byref(paired)))
+        return tuple(sizes), bool(paired.value)
+
     def set_stream(self, stream_ptr: int | None) -> None:
         _raise(_native.cuda().fpbem_cu_set_stream(self._h, stream_ptr))
 
@@ -278,8 +314,10 @@ class FmmOperators:
     def kernel_launches(self) -> int:
         return int(_native.cuda().fpbem_cu_kernel_launches(self._h))
 
-    def enable_stage_timing(self, on: bool = True) -> None:
-        _raise(_native.cuda().fpbem_cu_enable_stage_timing(self._h, int(on)))
+    def enable_stage_timing(self, on: bool = True, serial: bool = False) -> None:
+        """Per-stage CUDA-event timing; serial=True runs P2M + M2L on the main
+        stream while timing so every stage is timed alone."""
+        _raise(_native.cuda().fpbem_cu_enable_stage_timing(self._h, (2 if serial else 1) if on else 0))
 
     def stage_times(self) -> dict:
         ms = (C.c_double * 7)()
@@ -289,6 +327,15 @@ class FmmOperators:
         out["applies"] = int(ms[5])
         out["near_mode_product"] = ms[6]
         return out
+
+    def stream_ptr(self) -> int:
+        """The cudaStream_t this handle's device work runs on."""
+        st = C.c_void_p()
+        _raise(_native.cuda().fpbem_cu_get_stream(self._h, C.byref(st)))
+        return int(st.value or 0)
+
+    def _ordered(self, *tensors):
+        return _TorchOrdered(self.stream_ptr(), tensors[0].device, tensors)
 
     def _nrhs(self, p) -> int:
         size = int(p.numel()) if _is_torch(p) else int(np.asarray(p).size)
@@ -310,7 +357,8 @@ class FmmOperators:
                 raise ValueError("fmm matvec: expected a complex128 CUDA tensor")
             x = p.contiguous()
             y = torch.empty_like(x)
-            _raise(lib.fpbem_cu_fmm_apply(self._h, x.data_ptr(), y.data_ptr(), nrhs, PTR_DEVICE))
+            with self._ordered(x, y):
+                _raise(lib.fpbem_cu_fmm_apply(self._h, x.data_ptr(), y.data_ptr(), nrhs, PTR_DEVICE))
             return y
         x = np.ascontiguousarray(p, dtype=np.complex128)
         y = np.empty_like(x)
@@ -345,8 +393,9 @@ def gmres(apply, b, tol: float = 1e-4, restart: int = 100, max_iter: int = 1000,
             import torch
 
             x = torch.empty_like(bx)
-            rc = lib.fpbem_cu_gmres(apply.handle, bx.data_ptr(), x.data_ptr(), nrhs, tol, restart, max_iter,
-                                    PTR_DEVICE, its, conv, hist.ctypes.data_as(_native.c_double_p), cap, hlen)
+            with apply._ordered(bx, x):
+                rc = lib.fpbem_cu_gmres(apply.handle, bx.data_ptr(), x.data_ptr(), nrhs, tol, restart, max_iter,
+                                        PTR_DEVICE, its, conv, hist.ctypes.data_as(_native.c_double_p), cap, hlen)
         else:
             bx = np.ascontiguousarray(b, np.complex128)
             x = np.zeros_like(bx)
@@ -380,8 +429,9 @@ def gmres_distributed(op: FmmOperators, b, tol: float = 1e-4, restart: int = 100
 
         bx = b.contiguous()
         x = torch.empty_like(bx)
-        rc = lib.fpbem_cu_gmres_dist(op.handle, bx.data_ptr(), x.data_ptr(), tol, restart, max_iter, PTR_DEVICE,
-                                     C.byref(its), C.byref(conv), hp, cap, C.byref(hlen))
+        with op._ordered(bx, x):
+            rc = lib.fpbem_cu_gmres_dist(op.handle, bx.data_ptr(), x.data_ptr(), tol, restart, max_iter, PTR_DEVICE,
+                                         C.byref(its), C.byref(conv), hp, cap, C.byref(hlen))
     else:
         bx = np.ascontiguousarray(b, np.complex128)
         x = np.zeros_like(bx)
@@ -604,10 +654,20 @@ def evaluate_field_gpu(scene, solution, points, field: int = 0, p_incident=None,
         pinc = np.ascontiguousarray(p_incident, np.complex128)
         out = np.zeros(len(pts), np.complex128)
         args = (sol.ctypes.data, pinc.ctypes.data, out.ctypes.data, PTR_HOST, device)
-    _raise(lib.fpbem_cu_evaluate_field(C.byref(cs), float(scene.wavenumber), pitch.ctypes.data_as(_native.c_double_p),
-                                       counts.ctypes.data_as(_native.c_int_p), args[0], len(pts),
-                                       pts.ctypes.data_as(_native.c_double_p), args[1], int(axis), float(off),
-                                       _native.C64(complex(refl).real, complex(refl).imag), args[4], args[2], args[3]))
+
+    def call():
+        _raise(lib.fpbem_cu_evaluate_field(C.byref(cs), float(scene.wavenumber),
+                                           pitch.ctypes.data_as(_native.c_double_p),
+                                           counts.ctypes.data_as(_native.c_int_p), args[0], len(pts),
+                                           pts.ctypes.data_as(_native.c_double_p), args[1], int(axis), float(off),
+                                           _native.C64(complex(refl).real, complex(refl).imag), args[4], args[2],
+                                           args[3]))
+
+    if _is_torch(solution):
+        with _TorchOrdered(None, sol.device, (sol, pinc, out)):  # the call syncs its own stream
+            call()
+    else:
+        call()
     return out
 
 

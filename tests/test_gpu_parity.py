@@ -216,6 +216,42 @@ def test_device_pointer_apply_matches_host_pointer(ops, assembled):
     assert np.array_equal(yd.cpu().numpy(), yh)
 
 
+@pytest.mark.parametrize("b", [144, 169, 256])
+@pytest.mark.parametrize("path", ["direct", "lattice"])
+def test_large_expansion_order_matches_oracle(ops, b, path):
+    """n_t = 11, 12, 15 (b = (n_t+1)^2 > 128 coefficients, more than one CTA
+    of the reduction / L2P kernels loads at once): full FMM product on both
+    near-field paths against the oracle."""
+    rng = np.random.default_rng(b)
+    counts, n = (3, 2, 2), 40
+    offs = all_offsets(counts)
+    near = [o for o in offs if max(abs(c) for c in o) <= 1]
+    far = [o for o in offs if max(abs(c) for c in o) > 1]
+    d = Data(counts, n, b, near, crand(rng, len(near), n, n), far, 0.01 * crand(rng, len(far), b, b),
+             crand(rng, n, b) / b, crand(rng, b, n) / n)
+    p = uvec(rng, d.N)
+    assert rel(ops(d, near_path=path).matvec(p), O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+def test_device_pointer_apply_is_ordered_against_torch_stream(ops, assembled):
+    """The input is produced on torch's current stream behind a long kernel and
+    the output consumed there, with no explicit synchronisation in between:
+    the library stream waits for the producer and torch waits for the product."""
+    torch = pytest.importorskip("torch")
+    sc, d = assembled(3, 2)
+    op = ops(d)
+    rng = np.random.default_rng(12)
+    p = uvec(rng, d.N)
+    yh = op.matvec(p)
+    big = torch.randn(4096, 4096, device="cuda", dtype=torch.float64)
+    for _ in range(3):
+        big = big @ big / 64.0  # keeps torch's stream busy for a while
+        x = torch.from_numpy(p).cuda(non_blocking=False) * (1.0 + 0.0 * big[0, 0])
+        y = op.matvec(x)
+        z = (y * 1.0).cpu().numpy()
+        assert np.array_equal(z, yh)
+
+
 def test_apply_is_deterministic_and_linear(ops, assembled):
     sc, d = assembled(2, 2)
     op = ops(d)
