@@ -60,6 +60,15 @@ inline cudaError_t ensure_max_smem(std::atomic<unsigned long long>& done, const 
   if (e != cudaSuccess) return e;
   const unsigned long long bit = 1ULL << (dev & 63);
   if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  // the dynamic limit is what the opt-in maximum leaves after the kernel's static shared memory
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, func);
+  if (e != cudaSuccess) return e;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  const int room = optin - static_cast<int>(fa.sharedSizeBytes);
+  if (bytes > room) bytes = room;
   e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
   return e;

@@ -363,7 +363,18 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
   if (op->mode_lo > 0 || op->mode_hi < op->n_items)
     check(cudaMemsetAsync(yh, 0, static_cast<size_t>(r * op->qn * n) * sizeof(c64), s), "near spectrum clear");
   ev_record(op, 7, s);
-  if (nrhs * op->near_nimg <= kModeGemvMaxAcc) {
+  // FPBEM_NEAR_MMA=0 keeps the FMA GEMV where the tensor-core mode product applies (A/B)
+  static const bool mma_env = [] {
+    const char* v = std::getenv("FPBEM_NEAR_MMA");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  int nw_, kc_, ring_;
+  size_t smem_;
+  if (mma_env && mode_mma_shape(op->n, nrhs * op->near_nimg, &nw_, &kc_, &ring_, &smem_)) {
+    check(launch_mode_mma(op->shat, op->items, op->n_items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi,
+                          op->qn, nrhs, op->near_nimg, s),
+          "near mode mma");
+  } else if (nrhs * op->near_nimg <= kModeGemvMaxAcc) {
     check(launch_mode_gemv(op->shat, op->items, op->n_items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi,
                            op->qn, nrhs, op->near_nimg, s),
           "near mode gemv");

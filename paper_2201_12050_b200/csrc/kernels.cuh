@@ -18,6 +18,12 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
 // (q_i, g_i) of the item (items[t*8 + i], items[(n_items + t)*8 + i]),
 // yh[r][q_i] = P_g shat_t P_g xh[r][q_i]; nrhs * nimg <= kModeGemvMaxAcc
 constexpr int kModeGemvMaxAcc = 8;
+// The same product on DMMA tiles with a bulk-copy ring of the stored blocks
+// (nrhs * nimg <= 8 columns, n % 8 == 0; mode_mma_shape says whether it applies)
+bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem);
+cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
+                            c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
+                            cudaStream_t stream);
 cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
                              c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
                              cudaStream_t stream);

@@ -14,6 +14,7 @@
 // Complex arithmetic: the Gauss 3-multiplication form (three real m8n8k4
 // DMMAs per complex 8x8x4 tile instead of four); the algorithmic count stays
 // 8 real flops per complex multiply-add.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -289,6 +290,166 @@ near_mode_gemv_kernel(const c64* __restrict__ shat, const int* __restrict__ item
   }
 }
 
+// Same product as near_mode_gemv_kernel on the FP64 tensor cores, for up to 8
+// columns per stored block (right-hand sides x images, e.g. the 8 images of
+// an orbit under the icosphere's axis-sign group on cfg3/cfg5). The GEMV's
+// 8 complex FMAs per streamed element left it bound between the FP64 pipe and
+// load latency at ~0.5 of HBM. Here:
+//   * persistent CTAs, one per SM, walking the stored blocks t = blockIdx.x,
+//     blockIdx.x + gridDim.x, ...;
+//   * a producer warp streams each block column by column with
+//     cp.async.bulk (evict-first: the 1.2 GB stream must not push x_hat out of
+//     L2) into a ring of KC-column stages (full / empty mbarriers), running
+//     ahead across block boundaries, so HBM never waits on the math;
+//   * NW consumer warps own n / 8 / NW row tiles each: per 4-deep k step one
+//     A fragment per row tile from the ring (column pitch n + 2 complex:
+//     conflict-free 16-byte fragment loads), one B fragment of the block's
+//     8 columns, and the Gauss 3-multiplication complex product on
+//     mma.sync.m8n8k4.f64 (3 DMMAs per complex 8x8x4 tile);
+//   * the block's columns X[c][k] = xh[r][q_img][P_g k] are gathered from L2
+//     into shared memory at the block's start, and the epilogue scatters the
+//     rows through P_g into yh[r][q_img].
+// Fixed summation order (k ascending in groups of 4): bitwise repeatable.
+constexpr int MMA_KC_MAX = 8;
+
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int MT, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items, long long n_items,
+                     const int* __restrict__ perm, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
+                     long long t_lo, long long t_hi, long long q_stride, int nrhs, int ncols, int KC, int ring) {
+  extern __shared__ __align__(128) unsigned char mm_smem[];
+  const int AP = n + 2, XP = n + 4;  // complex pitches: A columns, X columns
+  c64* As = reinterpret_cast<c64*>(mm_smem);
+  c64* Xs = As + static_cast<size_t>(ring) * KC * AP;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Xs + 8 * XP);  // full[ring], empty[ring]
+  __shared__ int iq[8], ig[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + ring);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ring; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, NW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int stages = (n + KC - 1) / KC;  // per stored block
+  const size_t nn = static_cast<size_t>(n) * n;
+
+  if (warp == NW) {  // ---- producer
+    if (lane == 0) {
+      const unsigned long long pol = evict_first_policy();
+      long long g = 0;  // global stage counter over all of this CTA's blocks
+      for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
+        const c64* blk = shat + static_cast<size_t>(t) * nn;
+        for (int st = 0; st < stages; ++st, ++g) {
+          const int slot = static_cast<int>(g % ring);
+          const unsigned ph = static_cast<unsigned>((g / ring) & 1);
+          if (g >= ring) mbar_wait(empty0 + 8 * slot, ph ^ 1);
+          const int k0 = st * KC, kc = min(KC, n - k0);
+          mbar_arrive_expect_tx(full0 + 8 * slot, static_cast<unsigned>(kc * n * sizeof(c64)));
+          const unsigned dst = smem_u32(As + static_cast<size_t>(slot) * KC * AP);
+          for (int c = 0; c < kc; ++c)
+            bulk_g2s_hint(dst + static_cast<unsigned>(c * AP * sizeof(c64)), blk + static_cast<size_t>(k0 + c) * n,
+                          static_cast<unsigned>(n * sizeof(c64)), full0 + 8 * slot, pol);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  const int nthr = 32 * NW;
+  const int fr = lane >> 2, fk = lane & 3;
+  long long g = 0;
+  for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
+    named_bar(1, nthr);  // every warp is done with the previous block's X and (iq, ig)
+    if (threadIdx.x < 8) {
+      iq[threadIdx.x] = items[t * 8 + threadIdx.x];
+      ig[threadIdx.x] = items[(n_items + t) * 8 + threadIdx.x];
+    }
+    named_bar(1, nthr);
+    for (int e = threadIdx.x; e < 8 * n; e += nthr) {  // X[c][k], zero for unused columns
+      const int c = e / n, k = e - c * n;
+      c64 v = cmk(0.0, 0.0);
+      if (c < ncols) {
+        const int img = c / nrhs, r = c - img * nrhs;
+        const int q = iq[img];
+        if (q >= 0) {
+          const int gg = ig[img];
+          const int kk = gg ? __ldg(perm + static_cast<size_t>(gg - 1) * n + k) : k;
+          v = xh[r * q_stride * n + static_cast<long long>(q) * n + kk];
+        }
+      }
+      Xs[c * XP + k] = v;
+    }
+    named_bar(1, nthr);
+
+    double t1[MT][2], t2[MT][2], t3[MT][2];
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) t1[mi][0] = t1[mi][1] = t2[mi][0] = t2[mi][1] = t3[mi][0] = t3[mi][1] = 0.0;
+    const int n_mt = n >> 3;
+    for (int st = 0; st < stages; ++st, ++g) {
+      const int slot = static_cast<int>(g % ring);
+      mbar_wait(full0 + 8 * slot, static_cast<unsigned>((g / ring) & 1));
+      const c64* as = As + static_cast<size_t>(slot) * KC * AP;
+      const int k0 = st * KC, kc = min(KC, n - k0);
+      for (int k4 = 0; k4 < kc; k4 += 4) {
+        const c64 b = Xs[fr * XP + k0 + k4 + fk];
+        const double bsum = b.x + b.y;
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          const int mt = warp + mi * NW;
+          if (mt < n_mt) {
+            const c64 a = as[(k4 + fk) * AP + mt * 8 + fr];
+            dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
+            dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
+            dmma884(t3[mi][0], t3[mi][1], a.x + a.y, bsum);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+    }
+    // epilogue: accumulator (row fr, columns 2 fk + {0, 1}) of each 8 x 8 tile
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+      const int mt = warp + mi * NW;
+      if (mt >= n_mt) continue;
+      const int i = mt * 8 + fr;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = 2 * fk + j;
+        if (c >= ncols) continue;
+        const int img = c / nrhs, r = c - img * nrhs;
+        const int q = iq[img];
+        if (q < 0) continue;
+        const int gg = ig[img];
+        const int row = gg ? __ldg(perm + static_cast<size_t>(gg - 1) * n + i) : i;
+        yh[r * q_stride * n + static_cast<long long>(q) * n + row] =
+            cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
+      }
+    }
+  }
+}
+
 // y[r,t,i] = sum_{pairs of t, offset order} W[pair, r, i]  +  sum_m U0[i, m] L[t, r, m]
 // One thread per row i; grid (row tiles, target cells * nrhs).
 constexpr int RED_THREADS = 128;
@@ -389,6 +550,56 @@ cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_item
 #undef FPBEM_GEMV_CASE
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// Shape of the tensor-core mode product for n rows and `ncols` columns per
+// stored block: consumer warps, k columns per ring stage, ring depth and the
+// dynamic shared memory; false when it does not apply (n % 8, > 8 columns,
+// more than 8 row tiles per warp, or no 2-stage ring fits).
+bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem) {
+  if (n <= 0 || n % 8 || ncols < 1 || ncols > 8) return false;
+  // 8 consumer warps of up to 8 row tiles (n <= 512; larger blocks keep the
+  // GEMV, which streams at the HBM roofline with few columns per block, cfg2)
+  const int n_mt = n / 8;
+  const int NW = 8;
+  if ((n_mt + NW - 1) / NW > 8) return false;
+  const int KC = 8;
+  const size_t stage = sizeof(c64) * KC * static_cast<size_t>(n + 2);
+  const size_t fixed = sizeof(c64) * 8 * static_cast<size_t>(n + 4) + 2 * 8 * 16 + 128;
+  const size_t budget = static_cast<size_t>(kMaxDynSmem) - 1024;  // the kernel's static shared memory
+  if (fixed + 2 * stage > budget) return false;
+  const int R = static_cast<int>(std::min<size_t>(8, (budget - fixed) / stage));
+  *nw = NW;
+  *kc = KC;
+  *ring = R;
+  *smem = sizeof(c64) * (static_cast<size_t>(R) * KC * (n + 2) + 8 * static_cast<size_t>(n + 4)) +
+          2 * sizeof(unsigned long long) * R;
+  return true;
+}
+
+cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
+                            c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
+                            cudaStream_t stream) {
+  if (t_hi <= t_lo) return cudaSuccess;
+  int NW, KC, R;
+  size_t smem;
+  const int ncols = nrhs * nimg;
+  if (!mode_mma_shape(n, ncols, &NW, &KC, &R, &smem)) return cudaErrorInvalidValue;
+  const int MT = (n / 8 + NW - 1) / NW;
+  static std::atomic<unsigned long long> raised[8];
+  using K = void (*)(const c64*, const int*, long long, const int*, const c64*, c64*, int, long long, long long,
+                     long long, int, int, int, int);
+  static const K fns[8] = {near_mode_mma_kernel<1, 8>, near_mode_mma_kernel<2, 8>, near_mode_mma_kernel<3, 8>,
+                           near_mode_mma_kernel<4, 8>, near_mode_mma_kernel<5, 8>, near_mode_mma_kernel<6, 8>,
+                           near_mode_mma_kernel<7, 8>, near_mode_mma_kernel<8, 8>};
+  const int which = MT - 1;
+  cudaError_t e = ensure_max_smem(raised[which], reinterpret_cast<const void*>(fns[which]), kMaxDynSmem);
+  if (e != cudaSuccess) return e;
+  const long long blocks = t_hi - t_lo;
+  const int grid = static_cast<int>(std::min<long long>(blocks, device_sms()));
+  fns[which]<<<grid, 32 * (NW + 1), smem, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, t_hi, q_stride,
+                                                     nrhs, ncols, KC, R);
   return cudaGetLastError();
 }
 

@@ -378,3 +378,26 @@ def test_lattice_mode_partition_with_many_right_hand_sides(ops, assembled):
     ora = O.OracleFmm(d)
     for k in (0, 11):
         assert rel(full[k * d.N:(k + 1) * d.N], ora.matvec(P[k * d.N:(k + 1) * d.N])) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("counts,n,group,nrhs", [((4, 2, 3), 40, "xyz", 1), ((3, 3, 2), 64, "xy", 2),
+                                                 ((2, 3, 2), 320, "xyz", 1), ((3, 1, 2), 512, "x", 4)])
+def test_tensor_core_mode_product_with_partition(ops, counts, n, group, nrhs):
+    """the DMMA mode product with the bulk-copy block ring (n % 8 == 0, up to 8
+    columns per stored block = right-hand sides x images): each right-hand
+    side equals the oracle's product, and partial products of a 3-way
+    stored-block partition sum to the full product"""
+    rng = np.random.default_rng(n + nrhs)
+    d, G = _symmetric_toeplitz(rng, counts, n, GROUPS[group])
+    op = ops(d, near_path="lattice", max_rhs=nrhs)
+    P = np.concatenate([uvec(rng, d.N) for _ in range(nrhs)])
+    full = op.matvec(P)
+    for r in range(nrhs):
+        ref = O.toeplitz_matvec(counts, d.near_offsets, d.near_blocks, P[r * d.N:(r + 1) * d.N])
+        assert rel(full[r * d.N:(r + 1) * d.N], ref) <= MATVEC_TOL
+    assert np.array_equal(full, op.matvec(P))
+    total = np.zeros_like(full)
+    for r in range(3):
+        op.set_partition(r, 3)
+        total += op.matvec(P)
+    assert rel(total, full) < 1e-13
