@@ -38,9 +38,10 @@ def _is_torch(x) -> bool:
 class _TorchOrdered:
     """Orders a library stream against torch's current stream around a
     device-pointer call: the library waits for torch's producers of the inputs,
-    torch's consumers wait for the library's outputs, and the tensors are
-    recorded on the library stream so the caching allocator does not hand
-    their memory out while the library may still use it."""
+    and torch's stream waits for the library's work before anything enqueued
+    after the call, so memory the caching allocator recycles (on this stream)
+    is reused only after the library is done with it. (No record_stream: the
+    library's stream can be destroyed before the tensors are freed.)"""
 
     def __init__(self, stream_ptr: int | None, device, tensors):
         import torch
@@ -60,8 +61,6 @@ class _TorchOrdered:
     def __exit__(self, *exc):
         if self.lib is not None:
             self.cur.wait_stream(self.lib)
-            for t in self.tensors:
-                t.record_stream(self.lib)
         return False
 
 
