@@ -333,6 +333,12 @@ __device__ __forceinline__ T block_sum_mgs(T v, T* sh) {  // result valid in thr
   return t;
 }
 
+// bulk prefetch of `count` complex values into L2 (no registers, no completion tracking)
+__device__ __forceinline__ void prefetch_l2(const c64* p, int count) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(static_cast<unsigned>(count * sizeof(c64)))
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kMgsThreads, 1)
 mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, int j, long long n, long long chunk,
                  c64* __restrict__ h_out, double* __restrict__ norms, int* __restrict__ nonfinite,
@@ -411,12 +417,16 @@ mgs_fused_kernel(c64* __restrict__ w, const c64* __restrict__ V, long long ld, i
       const int e = tid + k * kMgsThreads;
       if (e < len) s = cfma_conj(vc[k], ws[e], s);
     }
+    if (tid == 0 && j >= 1 && len > 0) prefetch_l2(V + ld + start, len);
     c64 h = fold_c(s, 0);
     if (blockIdx.x == 0 && tid == 0) hout[0] = h;
     for (int i = 0; i < j; ++i) {
       // w -= h_i v_i (v_i from registers) and the partial <v_{i+1}, w> in one pass;
       // v_{i+1} is read from HBM once and stays in registers for the next step
       const c64* v = V + static_cast<long long>(i + 1) * ld + start;
+      // v_{i+2}'s chunk is pulled into L2 while this pass and the grid-wide fold
+      // of h_{i+1} run, so the next pass's loads hit L2 instead of waiting on HBM
+      if (tid == 0 && i + 2 <= j && len > 0) prefetch_l2(V + static_cast<long long>(i + 2) * ld + start, len);
       s = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < kMgsK; ++k) {

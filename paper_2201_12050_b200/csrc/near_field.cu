@@ -310,8 +310,6 @@ near_mode_gemv_kernel(const c64* __restrict__ shat, const int* __restrict__ item
 //     into shared memory at the block's start, and the epilogue scatters the
 //     rows through P_g into yh[r][q_img].
 // Fixed summation order (k ascending in groups of 4): bitwise repeatable.
-constexpr int MMA_KC_MAX = 8;
-
 __device__ __forceinline__ unsigned long long evict_first_policy() {
   unsigned long long pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -329,23 +327,40 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16_zfill(unsigned dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+// arrive on `bar` when all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive_noinc(unsigned bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+
 template <int MT, int NW>
-__global__ void __launch_bounds__(32 * (NW + 1), 1)
+__global__ void __launch_bounds__(32 * (NW + 2), 1)
 near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items, long long n_items,
                      const int* __restrict__ perm, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
                      long long t_lo, long long t_hi, long long q_stride, int nrhs, int ncols, int KC, int ring) {
   extern __shared__ __align__(128) unsigned char mm_smem[];
   const int AP = n + 2, XP = n + 4;  // complex pitches: A columns, X columns
   c64* As = reinterpret_cast<c64*>(mm_smem);
-  c64* Xs = As + static_cast<size_t>(ring) * KC * AP;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Xs + 8 * XP);  // full[ring], empty[ring]
-  __shared__ int iq[8], ig[8];
+  c64* Xs = As + static_cast<size_t>(ring) * KC * AP;  // two X buffers of 8 columns
+  // barriers: full[ring], empty[ring], xfull[2], xempty[2]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Xs + 2 * 8 * XP);
+  __shared__ int iq[2][8], ig[2][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + ring);
+  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + ring), xfull0 = smem_u32(bars + 2 * ring),
+                 xempty0 = smem_u32(bars + 2 * ring + 2);
   if (threadIdx.x == 0) {
     for (int i = 0; i < ring; ++i) {
       mbar_init(full0 + 8 * i, 1);
       mbar_init(empty0 + 8 * i, NW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      // the producer warp's 32 lanes through cp.async.mbarrier.arrive.noinc (their gathers
+      // landed) + one plain release arrive after the block's (iq, ig) were written
+      mbar_init(xfull0 + 8 * i, 33);
+      mbar_init(xempty0 + 8 * i, NW);
     }
     mbar_fence_init();
   }
@@ -353,22 +368,66 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
   const int stages = (n + KC - 1) / KC;  // per stored block
   const size_t nn = static_cast<size_t>(n) * n;
 
-  if (warp == NW) {  // ---- producer
+  if (warp == NW + 1) {  // ---- X producer: the blocks' columns, up to two blocks ahead of the consumers
+    int it = 0;
+    for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x, ++it) {
+      // X[c][k] = xh[r][q_img][P_g k] into X buffer it & 1, 16-byte cp.async per element
+      const int xb = it & 1;
+      if (it >= 2) mbar_wait(xempty0 + 8 * xb, ((it >> 1) - 1) & 1);
+      int q8 = -1, g8 = 0;
+      if (lane < 8) {
+        q8 = items[t * 8 + lane];
+        g8 = items[(n_items + t) * 8 + lane];
+        iq[xb][lane] = q8;
+        ig[xb][lane] = g8;
+      }
+      c64* xdst = Xs + xb * 8 * XP;
+      for (int c = 0; c < 8; ++c) {
+        const int img = c / nrhs, r = c - img * nrhs;
+        const int q = __shfl_sync(0xffffffffu, q8, img), gg = __shfl_sync(0xffffffffu, g8, img);
+        const bool ok = c < ncols && q >= 0;
+        const c64* src = xh + (ok ? r * q_stride * n + static_cast<long long>(q) * n : 0);
+        const int* pg = gg ? perm + static_cast<size_t>(gg - 1) * n : nullptr;
+        constexpr int B = 8;  // permutation indices in flight per lane
+        for (int k0 = 0; k0 < n; k0 += 32 * B) {
+          int idx[B];
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const int k = k0 + lane + 32 * u;
+            idx[u] = (k < n && pg) ? __ldg(pg + k) : k;
+          }
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const int k = k0 + lane + 32 * u;
+            if (k < n) cp_async16_zfill(smem_u32(xdst + c * XP + k), ok ? src + idx[u] : xh, ok);
+          }
+        }
+      }
+      cp_async_arrive_noinc(xfull0 + 8 * xb);
+      __syncwarp();  // orders lanes 0-7's (iq, ig) stores before lane 0's release arrive
+      if (lane == 0) mbar_arrive(xfull0 + 8 * xb);
+    }
+    return;
+  }
+  if (warp == NW) {  // ---- block producer: each stored block column by column into the ring
     if (lane == 0) {
       const unsigned long long pol = evict_first_policy();
-      long long g = 0;  // global stage counter over all of this CTA's blocks
+      int slot = 0;
+      unsigned ph = 0;
       for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
         const c64* blk = shat + static_cast<size_t>(t) * nn;
-        for (int st = 0; st < stages; ++st, ++g) {
-          const int slot = static_cast<int>(g % ring);
-          const unsigned ph = static_cast<unsigned>((g / ring) & 1);
-          if (g >= ring) mbar_wait(empty0 + 8 * slot, ph ^ 1);
+        for (int st = 0; st < stages; ++st) {
+          mbar_wait(empty0 + 8 * slot, ph ^ 1);
           const int k0 = st * KC, kc = min(KC, n - k0);
           mbar_arrive_expect_tx(full0 + 8 * slot, static_cast<unsigned>(kc * n * sizeof(c64)));
           const unsigned dst = smem_u32(As + static_cast<size_t>(slot) * KC * AP);
           for (int c = 0; c < kc; ++c)
             bulk_g2s_hint(dst + static_cast<unsigned>(c * AP * sizeof(c64)), blk + static_cast<size_t>(k0 + c) * n,
                           static_cast<unsigned>(n * sizeof(c64)), full0 + 8 * slot, pol);
+          if (++slot == ring) {
+            slot = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -376,57 +435,47 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
   }
 
   // ---- consumers
-  const int nthr = 32 * NW;
   const int fr = lane >> 2, fk = lane & 3;
-  long long g = 0;
-  for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
-    named_bar(1, nthr);  // every warp is done with the previous block's X and (iq, ig)
-    if (threadIdx.x < 8) {
-      iq[threadIdx.x] = items[t * 8 + threadIdx.x];
-      ig[threadIdx.x] = items[(n_items + t) * 8 + threadIdx.x];
-    }
-    named_bar(1, nthr);
-    for (int e = threadIdx.x; e < 8 * n; e += nthr) {  // X[c][k], zero for unused columns
-      const int c = e / n, k = e - c * n;
-      c64 v = cmk(0.0, 0.0);
-      if (c < ncols) {
-        const int img = c / nrhs, r = c - img * nrhs;
-        const int q = iq[img];
-        if (q >= 0) {
-          const int gg = ig[img];
-          const int kk = gg ? __ldg(perm + static_cast<size_t>(gg - 1) * n + k) : k;
-          v = xh[r * q_stride * n + static_cast<long long>(q) * n + kk];
-        }
-      }
-      Xs[c * XP + k] = v;
-    }
-    named_bar(1, nthr);
+  const int n_mt = n >> 3;
+  int slot = 0;
+  unsigned ph = 0;
+  int it = 0;
+  for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x, ++it) {
+    const int xb = it & 1;
+    mbar_wait(xfull0 + 8 * xb, (it >> 1) & 1);
+    const c64* xs = Xs + xb * 8 * XP + fr * XP + fk;
 
     double t1[MT][2], t2[MT][2], t3[MT][2];
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi) t1[mi][0] = t1[mi][1] = t2[mi][0] = t2[mi][1] = t3[mi][0] = t3[mi][1] = 0.0;
-    const int n_mt = n >> 3;
-    for (int st = 0; st < stages; ++st, ++g) {
-      const int slot = static_cast<int>(g % ring);
-      mbar_wait(full0 + 8 * slot, static_cast<unsigned>((g / ring) & 1));
-      const c64* as = As + static_cast<size_t>(slot) * KC * AP;
+    for (int st = 0; st < stages; ++st) {
+      mbar_wait(full0 + 8 * slot, ph);
+      const c64* as = As + static_cast<size_t>(slot) * KC * AP + fk * AP + fr;
       const int k0 = st * KC, kc = min(KC, n - k0);
       for (int k4 = 0; k4 < kc; k4 += 4) {
-        const c64 b = Xs[fr * XP + k0 + k4 + fk];
+        const c64 b = xs[k0 + k4];
         const double bsum = b.x + b.y;
+        c64 a[MT];
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi) {
           const int mt = warp + mi * NW;
-          if (mt < n_mt) {
-            const c64 a = as[(k4 + fk) * AP + mt * 8 + fr];
-            dmma884(t1[mi][0], t1[mi][1], a.x, b.x);
-            dmma884(t2[mi][0], t2[mi][1], a.y, b.y);
-            dmma884(t3[mi][0], t3[mi][1], a.x + a.y, bsum);
+          a[mi] = mt < n_mt ? as[k4 * AP + mt * 8] : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          if (warp + mi * NW < n_mt) {
+            dmma884(t1[mi][0], t1[mi][1], a[mi].x, b.x);
+            dmma884(t2[mi][0], t2[mi][1], a[mi].y, b.y);
+            dmma884(t3[mi][0], t3[mi][1], a[mi].x + a[mi].y, bsum);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+      if (++slot == ring) {
+        slot = 0;
+        ph ^= 1;
+      }
     }
     // epilogue: accumulator (row fr, columns 2 fk + {0, 1}) of each 8 x 8 tile
 #pragma unroll
@@ -439,14 +488,16 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
         const int c = 2 * fk + j;
         if (c >= ncols) continue;
         const int img = c / nrhs, r = c - img * nrhs;
-        const int q = iq[img];
+        const int q = iq[xb][img];
         if (q < 0) continue;
-        const int gg = ig[img];
+        const int gg = ig[xb][img];
         const int row = gg ? __ldg(perm + static_cast<size_t>(gg - 1) * n + i) : i;
         yh[r * q_stride * n + static_cast<long long>(q) * n + row] =
             cmk(t1[mi][j] - t2[mi][j], t3[mi][j] - t1[mi][j] - t2[mi][j]);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xempty0 + 8 * xb);  // X buffer and (iq, ig)[xb] free for block it + 2
   }
 }
 
@@ -559,22 +610,35 @@ cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_item
 // more than 8 row tiles per warp, or no 2-stage ring fits).
 bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem) {
   if (n <= 0 || n % 8 || ncols < 1 || ncols > 8) return false;
-  // 8 consumer warps of up to 8 row tiles (n <= 512; larger blocks keep the
-  // GEMV, which streams at the HBM roofline with few columns per block, cfg2)
+  // consumer warps of up to 8 row tiles each (n <= 512; larger blocks keep the
+  // GEMV, which streams at the HBM roofline with few columns per block, cfg2):
+  // 10 warps x 4 tiles where the rows split evenly that way (n = 320), else 8
+  // (FPBEM_MMA_NW=8|10|20 forces one, A/B)
+  static const int nw_env = [] {
+    const char* v = std::getenv("FPBEM_MMA_NW");
+    return v ? std::atoi(v) : 0;
+  }();
   const int n_mt = n / 8;
-  const int NW = 8;
+  int NW = (n_mt % 10 == 0 && n_mt / 10 <= 8) ? 10 : 8;
+  if (nw_env == 8 || nw_env == 10 || nw_env == 20) NW = nw_env;
+  if ((n_mt + NW - 1) / NW > 8) NW = 8;
   if ((n_mt + NW - 1) / NW > 8) return false;
-  const int KC = 8;
+  static const int kc_env = [] {  // FPBEM_MMA_KC=4|8|16: columns per ring stage (A/B)
+    const char* v = std::getenv("FPBEM_MMA_KC");
+    const int k = v ? std::atoi(v) : 8;
+    return (k == 4 || k == 8 || k == 16) ? k : 8;
+  }();
+  const int KC = kc_env;
   const size_t stage = sizeof(c64) * KC * static_cast<size_t>(n + 2);
-  const size_t fixed = sizeof(c64) * 8 * static_cast<size_t>(n + 4) + 2 * 8 * 16 + 128;
+  const size_t fixed = 2 * sizeof(c64) * 8 * static_cast<size_t>(n + 4) + 4 * 8 * 16 + 128;
   const size_t budget = static_cast<size_t>(kMaxDynSmem) - 1024;  // the kernel's static shared memory
   if (fixed + 2 * stage > budget) return false;
-  const int R = static_cast<int>(std::min<size_t>(8, (budget - fixed) / stage));
+  const int R = static_cast<int>(std::min<size_t>(16, (budget - fixed) / stage));
   *nw = NW;
   *kc = KC;
   *ring = R;
-  *smem = sizeof(c64) * (static_cast<size_t>(R) * KC * (n + 2) + 8 * static_cast<size_t>(n + 4)) +
-          2 * sizeof(unsigned long long) * R;
+  *smem = sizeof(c64) * (static_cast<size_t>(R) * KC * (n + 2) + 2 * 8 * static_cast<size_t>(n + 4)) +
+          sizeof(unsigned long long) * (2 * R + 4);
   return true;
 }
 
@@ -587,18 +651,22 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   const int ncols = nrhs * nimg;
   if (!mode_mma_shape(n, ncols, &NW, &KC, &R, &smem)) return cudaErrorInvalidValue;
   const int MT = (n / 8 + NW - 1) / NW;
-  static std::atomic<unsigned long long> raised[8];
+  static std::atomic<unsigned long long> raised[18];
   using K = void (*)(const c64*, const int*, long long, const int*, const c64*, c64*, int, long long, long long,
                      long long, int, int, int, int);
-  static const K fns[8] = {near_mode_mma_kernel<1, 8>, near_mode_mma_kernel<2, 8>, near_mode_mma_kernel<3, 8>,
-                           near_mode_mma_kernel<4, 8>, near_mode_mma_kernel<5, 8>, near_mode_mma_kernel<6, 8>,
-                           near_mode_mma_kernel<7, 8>, near_mode_mma_kernel<8, 8>};
-  const int which = MT - 1;
+  static const K fns[18] = {near_mode_mma_kernel<1, 8>,  near_mode_mma_kernel<2, 8>,  near_mode_mma_kernel<3, 8>,
+                            near_mode_mma_kernel<4, 8>,  near_mode_mma_kernel<5, 8>,  near_mode_mma_kernel<6, 8>,
+                            near_mode_mma_kernel<7, 8>,  near_mode_mma_kernel<8, 8>,  near_mode_mma_kernel<1, 10>,
+                            near_mode_mma_kernel<2, 10>, near_mode_mma_kernel<3, 10>, near_mode_mma_kernel<4, 10>,
+                            near_mode_mma_kernel<5, 10>, near_mode_mma_kernel<6, 10>, near_mode_mma_kernel<7, 10>,
+                            near_mode_mma_kernel<8, 10>, near_mode_mma_kernel<1, 20>, near_mode_mma_kernel<2, 20>};
+  if (NW == 20 && MT > 2) return cudaErrorInvalidValue;
+  const int which = (NW == 8 ? 0 : NW == 10 ? 8 : 16) + MT - 1;
   cudaError_t e = ensure_max_smem(raised[which], reinterpret_cast<const void*>(fns[which]), kMaxDynSmem);
   if (e != cudaSuccess) return e;
   const long long blocks = t_hi - t_lo;
   const int grid = static_cast<int>(std::min<long long>(blocks, device_sms()));
-  fns[which]<<<grid, 32 * (NW + 1), smem, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, t_hi, q_stride,
+  fns[which]<<<grid, 32 * (NW + 2), smem, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, t_hi, q_stride,
                                                      nrhs, ncols, KC, R);
   return cudaGetLastError();
 }
