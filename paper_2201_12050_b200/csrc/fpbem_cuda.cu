@@ -589,11 +589,27 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
   }
 }
 
+// P2M / L2P as per-cell DMMA GEMMs (csrc/cellwise.cu); FPBEM_CELLWISE=0 keeps
+// the FMA kernels (A/B)
+bool cellwise_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("FPBEM_CELLWISE");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  return on;
+}
+
 // Far field of one product: P2M (events 2-3) and M2L into op->loc (events 3-4);
 // the Hankel image pair adds the K_hat term (src/fmm.cpp:256-263)
 void far_field(fpbem_cu_op* op, const c64* x, int nrhs, cudaStream_t a) {
   ev_record(op, 2, a);
-  check(launch_p2m(op->v0t, x, op->mom, op->n, op->b, op->N, nrhs, op->n_cells, a), "p2m");
+  if (cellwise_on() && cellwise_supported(op->b, op->n))  // M_c = V0 p_c: V0[m][k] = v0t[m n + k]
+    check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, op->N, op->n, op->mom, op->b,
+                          static_cast<long long>(nrhs) * op->b, nrhs, static_cast<long long>(op->n_cells) * nrhs,
+                          false, a),
+          "p2m");
+  else
+    check(launch_p2m(op->v0t, x, op->mom, op->n, op->b, op->N, nrhs, op->n_cells, a), "p2m");
   op->launches++;
   ev_record(op, 3, a);
   m2l_apply(op, nrhs, a, op->mom, op->lambda, op->loc);
@@ -694,7 +710,12 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
           "near reduce + l2p");
     op->launches++;
   } else if (far_here) {  // y += U0 L (src/fmm.cpp:265-267): the reduction with no pairs, accumulating
-    check(launch_l2p_add(op->u0, op->loc, y, op->n, op->b, op->n_cells, op->N, nrhs, s), "l2p");
+    if (cellwise_on() && cellwise_supported(op->n, op->b))  // y_c += U0 L_c: U0[i][m] = u0[m n + i]
+      check(launch_cellwise(op->u0, 1, op->n, op->n, op->b, op->loc, op->b, static_cast<long long>(nrhs) * op->b, y,
+                            op->N, op->n, nrhs, static_cast<long long>(op->n_cells) * nrhs, true, s),
+            "l2p");
+    else
+      check(launch_l2p_add(op->u0, op->loc, y, op->n, op->b, op->n_cells, op->N, nrhs, s), "l2p");
     op->launches++;
   }
   if (op->comm && reduce)  // sum the ranks' partial products, in place, on the same stream

@@ -24,6 +24,12 @@ bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem)
 cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
                             c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
                             cudaStream_t stream);
+// out[col] (+)= A in[col] per (cell, rhs) column col = cell * nrhs + r, A[m][k] =
+// a[m a_ms + k a_ks] (M x K): the P2M and L2P products on DMMA (csrc/cellwise.cu)
+bool cellwise_supported(int M, int K);
+cudaError_t launch_cellwise(const c64* a, long long a_ms, long long a_ks, int M, int K, const c64* in, long long in_rs,
+                            long long in_cs, c64* out, long long out_rs, long long out_cs, int nrhs, long long ncols,
+                            bool accumulate, cudaStream_t stream);
 cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_items, const int* perm, const c64* xh,
                              c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
                              cudaStream_t stream);
