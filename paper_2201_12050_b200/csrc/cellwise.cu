@@ -1,18 +1,17 @@
-// P2M and L2P of the single-level FMM as one per-cell GEMM on the FP64 tensor
-// cores (DMMA):
-//   P2M  M_c = V0 p_c        (src/fmm.cpp:256-259; V0: b x n)
-//   L2P  y_c += U0 L_c       (src/fmm.cpp:265-267; U0: n x b)
-// i.e. out[col] (+)= A in[col] for every (cell, rhs) column with one shared
-// matrix A. The previous kernels streamed A from L2 per cell (p2m_kernel) or
-// per 128-row tile (l2p_add_kernel) and were latency-bound at 65 / 25 us on
-// cfg3 for 21 MB of vector traffic. Here:
+// P2M of the single-level FMM as one per-cell GEMM on the FP64 tensor cores
+// (DMMA): M_c = V0 p_c (src/fmm.cpp:256-259; V0: b x n), i.e. out[col] (+)=
+// A in[col] for every (cell, rhs) column with one shared matrix A. The FMA
+// kernel streamed V0 from L2 per cell and took 66 us on cfg3 for 21 MB of
+// input (now 29 us). (The L2P is fused into the last inverse near-field DFT
+// pass, csrc/m2l.cu.) Here:
 //   * persistent CTAs hold A in shared memory ([m][k], pitch = 4 mod 8
 //     complex: conflict-free m8n8k4 fragments), loaded once per CTA;
 //   * the columns come in chunks of 8 (one DMMA n-tile), double-buffered with
 //     16-byte cp.async, so the next chunk's HBM reads overlap this chunk's math;
-//   * warps own A's 8-row tiles; with fewer row tiles than warps (P2M: b = 25
-//     -> 4 tiles) the k range is split over warp groups and the partial tiles
-//     are added in a fixed order through shared memory (deterministic);
+//   * warps own A's 8-row tiles; the k range is split over warp groups (b = 25
+//     -> 4 row tiles, 16 warps: 4 groups) with two accumulator sets each, and
+//     the partial tiles are added in a fixed order through shared memory
+//     (deterministic);
 //   * Gauss 3-multiplication complex product (3 DMMAs per complex 8x8x4 tile).
 #include <algorithm>
 
@@ -23,7 +22,7 @@ namespace fpbem_cu {
 
 namespace {
 
-constexpr int kCwWarps = 8;
+constexpr int kCwWarps = 16;
 
 __host__ __device__ constexpr int cw_pitch(int k) { return ((k + 3) / 4 * 4 + 4 - 1) / 8 * 8 + 4; }  // >= k, = 4 mod 8
 
@@ -96,11 +95,35 @@ cellwise_gemm_kernel(const c64* __restrict__ a, long long a_ms, long long a_ks, 
           prev[u][j] = out[r * out_rs + cell * out_cs + m];
         }
       }
-    double t1[MTW][2], t2[MTW][2], t3[MTW][2];
+    // two accumulator sets over alternating k steps: twice the independent DMMA
+    // chains per warp (the single-set version waited on DMMA latency, ncu)
+    double t1[2][MTW][2], t2[2][MTW][2], t3[2][MTW][2];
 #pragma unroll
-    for (int u = 0; u < MTW; ++u) t1[u][0] = t1[u][1] = t2[u][0] = t2[u][1] = t3[u][0] = t3[u][1] = 0.0;
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < MTW; ++u)
+        t1[h][u][0] = t1[h][u][1] = t2[h][u][0] = t2[h][u][1] = t3[h][u][0] = t3[h][u][1] = 0.0;
     if (active) {
-      for (int s = ks0; s < ks1; ++s) {
+      int s = ks0;
+      for (; s + 1 < ks1; s += 2) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const c64 b = bs[4 * (s + h)];
+          const double bsum = b.x + b.y;
+#pragma unroll
+          for (int u = 0; u < MTW; ++u) {
+            const int mt = wt + u * kCwWarps;
+            if (mt < MT) {
+              const int m = mt * 8 + fr;
+              const c64 av = m < M ? As[m * KP + 4 * (s + h) + fk] : cmk(0.0, 0.0);
+              dmma884(t1[h][u][0], t1[h][u][1], av.x, b.x);
+              dmma884(t2[h][u][0], t2[h][u][1], av.y, b.y);
+              dmma884(t3[h][u][0], t3[h][u][1], av.x + av.y, bsum);
+            }
+          }
+        }
+      }
+      if (s < ks1) {
         const c64 b = bs[4 * s];
         const double bsum = b.x + b.y;
 #pragma unroll
@@ -109,18 +132,22 @@ cellwise_gemm_kernel(const c64* __restrict__ a, long long a_ms, long long a_ks, 
           if (mt < MT) {
             const int m = mt * 8 + fr;
             const c64 av = m < M ? As[m * KP + 4 * s + fk] : cmk(0.0, 0.0);
-            dmma884(t1[u][0], t1[u][1], av.x, b.x);
-            dmma884(t2[u][0], t2[u][1], av.y, b.y);
-            dmma884(t3[u][0], t3[u][1], av.x + av.y, bsum);
+            dmma884(t1[0][u][0], t1[0][u][1], av.x, b.x);
+            dmma884(t2[0][u][0], t2[0][u][1], av.y, b.y);
+            dmma884(t3[0][u][0], t3[0][u][1], av.x + av.y, bsum);
           }
         }
       }
     }
+    auto tile = [&](int u, int j) {  // this warp's partial C entry (set 0 + set 1)
+      const double a1 = t1[0][u][j] + t1[1][u][j], a2 = t2[0][u][j] + t2[1][u][j], a3 = t3[0][u][j] + t3[1][u][j];
+      return cmk(a1 - a2, a3 - a1 - a2);
+    };
     // k-split: groups 1.. hand their tiles to group 0, which adds them in group order
     if (G > 1) {
       if (active && grp > 0) {
         c64* r = Red + (static_cast<size_t>(warp) * 32 + lane) * 2;
-        for (int j = 0; j < 2; ++j) r[j] = cmk(t1[0][j] - t2[0][j], t3[0][j] - t1[0][j] - t2[0][j]);
+        for (int j = 0; j < 2; ++j) r[j] = tile(0, j);
       }
       __syncthreads();
     }
@@ -132,7 +159,7 @@ cellwise_gemm_kernel(const c64* __restrict__ a, long long a_ms, long long a_ks, 
         const int m = mt * 8 + fr;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          c64 v = cmk(t1[u][j] - t2[u][j], t3[u][j] - t1[u][j] - t2[u][j]);
+          c64 v = tile(u, j);
           for (int g = 1; g < G; ++g) v = cadd(v, Red[(static_cast<size_t>(g * MT + wt) * 32 + lane) * 2 + j]);
           const long long col = ch * 8 + 2 * fk + j;
           if (m < M && col < ncols) {
@@ -154,7 +181,7 @@ size_t cw_smem(int M, int K) {
 }  // namespace
 
 bool cellwise_supported(int M, int K) {
-  return M >= 1 && K >= 1 && (M + 7) / 8 <= 8 * kCwWarps && cw_smem(M, K) <= static_cast<size_t>(kMaxDynSmem) - 1024;
+  return M >= 1 && K >= 1 && (M + 7) / 8 <= kCwWarps && cw_smem(M, K) <= static_cast<size_t>(kMaxDynSmem) - 1024;
 }
 
 cudaError_t launch_cellwise(const c64* a, long long a_ms, long long a_ks, int M, int K, const c64* in, long long in_rs,
@@ -162,22 +189,15 @@ cudaError_t launch_cellwise(const c64* a, long long a_ms, long long a_ks, int M,
                             bool accumulate, cudaStream_t stream) {
   if (ncols <= 0) return cudaSuccess;
   if (!cellwise_supported(M, K)) return cudaErrorInvalidValue;
-  const int MT = (M + 7) / 8;
-  const int mtw = MT >= kCwWarps ? (MT + kCwWarps - 1) / kCwWarps : 1;
   const size_t smem = cw_smem(M, K);
-  using Kfn = void (*)(const c64*, long long, long long, int, int, const c64*, long long, long long, c64*, long long,
-                       long long, int, long long, int);
-  static const Kfn fns[8] = {cellwise_gemm_kernel<1>, cellwise_gemm_kernel<2>, cellwise_gemm_kernel<3>,
-                             cellwise_gemm_kernel<4>, cellwise_gemm_kernel<5>, cellwise_gemm_kernel<6>,
-                             cellwise_gemm_kernel<7>, cellwise_gemm_kernel<8>};
-  static std::atomic<unsigned long long> raised[8];
-  cudaError_t e = ensure_max_smem(raised[mtw - 1], reinterpret_cast<const void*>(fns[mtw - 1]), kMaxDynSmem);
+  static std::atomic<unsigned long long> raised{0};
+  cudaError_t e = ensure_max_smem(raised, reinterpret_cast<const void*>(&cellwise_gemm_kernel<1>), kMaxDynSmem);
   if (e != cudaSuccess) return e;
   const long long chunks = (ncols + 7) / 8;
-  // persistent: one CTA per SM (A fills most of the shared memory; 130-180 registers)
+  // persistent: one CTA per SM (A fills most of the shared memory)
   const int grid = static_cast<int>(std::min<long long>(chunks, device_sms()));
-  fns[mtw - 1]<<<grid, kCwWarps * 32, smem, stream>>>(a, a_ms, a_ks, M, K, in, in_rs, in_cs, out, out_rs, out_cs,
-                                                      nrhs, ncols, accumulate ? 1 : 0);
+  cellwise_gemm_kernel<1><<<grid, kCwWarps * 32, smem, stream>>>(a, a_ms, a_ks, M, K, in, in_rs, in_cs, out, out_rs,
+                                                                   out_cs, nrhs, ncols, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

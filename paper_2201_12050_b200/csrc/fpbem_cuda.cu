@@ -322,7 +322,11 @@ void build_items(fpbem_cu_op* op, const int Ln[3]) {
 // cells per axis, for this rank's modes (zero elsewhere, so the ranks' partial
 // products sum to the product). Forward passes read only the M nonzero cells
 // per axis, inverse passes write only the M kept cells; the last one writes y.
-void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_t s) {
+// Lattice near field y = S x. With `fuse_loc` (the far field's locals, complete
+// once `join` fires on the aux stream) the L2P y += U0 L is fused into the last
+// inverse pass when that pass is an x-axis DMMA DFT; returns whether it was.
+bool near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_t s, const c64* fuse_loc = nullptr,
+                    cudaEvent_t join = nullptr) {
   const long long n = op->n, r = nrhs;
   const int Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const int Lx = op->Ln[0], Ly = op->Ln[1], Lz = op->Ln[2];
@@ -389,12 +393,21 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
   cur = yh;
   int left = (Lx > 1) + (Ly > 1) + (Lz > 1);
   const double scale = 1.0 / static_cast<double>(op->qn);
+  bool fused = false;
   auto inv = [&](int axis, long long n_a, int l, int m, long long inner) {
     const bool last = --left == 0;
     c64* out = last ? y : bufs[which];
     which ^= 1;
-    check(launch_dft_axis(cur, out, op->twn[axis], n_a, l, m, inner, l, true, last ? scale : 1.0, s),
-          "near inverse dft");
+    if (last && axis == 0 && fuse_loc && dft_l2p_supported(l, m, op->b)) {
+      check(cudaStreamWaitEvent(s, join, 0), "join");  // the locals of the far field
+      check(launch_dft_axis_l2p(cur, out, op->twn[axis], n_a, l, m, inner, l, scale, op->u0, fuse_loc, op->b, nrhs,
+                                s),
+            "near inverse dft + l2p");
+      fused = true;
+    } else {
+      check(launch_dft_axis(cur, out, op->twn[axis], n_a, l, m, inner, l, true, last ? scale : 1.0, s),
+            "near inverse dft");
+    }
     op->launches++;
     cur = out;
   };
@@ -408,6 +421,7 @@ void near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
     if (Ly > 1) inv(1, r * Mz, Ly, My, Lx * n);
     if (Lx > 1) inv(0, r * My * Mz, Lx, Mx, n);
   }
+  return fused;
 }
 
 void twiddles(fpbem_cu_op* op, int L, c64** out) {
@@ -690,7 +704,20 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
   check(cudaEventRecord(op->fork, s), "fork");
   check(cudaStreamWaitEvent(a, op->fork, 0), "fork");
   ev_record(op, 0, s);
-  if (op->near_fft) {
+  bool l2p_done = false;
+  // the L2P fused into the last inverse near pass (FPBEM_FUSE_L2P=0 keeps it separate);
+  // not under serial stage timing, where the far field runs on this stream
+  static const bool fuse_env = [] {
+    const char* v = std::getenv("FPBEM_FUSE_L2P");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const bool fuse = op->near_fft && far_here && fuse_env && a != s;
+  if (fuse) {  // far field first on the aux stream, joined inside the near field before its last pass
+    far_field(op, x, nrhs, a);
+    check(cudaEventRecord(op->join, a), "join");
+    l2p_done = near_fft_apply(op, x, y, nrhs, s, op->loc, op->join);  // y = S p (+ U0 L)
+    ev_record(op, 1, s);
+  } else if (op->near_fft) {
     near_fft_apply(op, x, y, nrhs, s);  // y = S p
   } else {
     check(launch_block_gemm(op->S, static_cast<long long>(op->n) * op->n, op->n, op->n, x, op->W, op->n,
@@ -698,24 +725,23 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
           "near gemm");
     op->launches += op->n_jobs > 0;
   }
-  ev_record(op, 1, s);
-  if (far_here) far_field(op, x, nrhs, a);
-  check(cudaEventRecord(op->join, a), "join");
+  if (!fuse) {
+    ev_record(op, 1, s);
+    if (far_here) far_field(op, x, nrhs, a);
+    check(cudaEventRecord(op->join, a), "join");
+  }
   s = op->stream;
   check(cudaStreamWaitEvent(s, op->join, 0), "join");
   ev_record(op, 5, s);
-  if (!op->near_fft) {
+  if (l2p_done) {
+    // y already holds S p + U0 L
+  } else if (!op->near_fft) {
     check(launch_near_reduce_l2p(op->W, op->tgt_ptr, op->tgt_pairs, op->u0, far_here ? op->loc : nullptr, y, op->n,
                                  op->b, op->n_cells, op->N, nrhs, false, s),
           "near reduce + l2p");
     op->launches++;
   } else if (far_here) {  // y += U0 L (src/fmm.cpp:265-267): the reduction with no pairs, accumulating
-    if (cellwise_on() && cellwise_supported(op->n, op->b))  // y_c += U0 L_c: U0[i][m] = u0[m n + i]
-      check(launch_cellwise(op->u0, 1, op->n, op->n, op->b, op->loc, op->b, static_cast<long long>(nrhs) * op->b, y,
-                            op->N, op->n, nrhs, static_cast<long long>(op->n_cells) * nrhs, true, s),
-            "l2p");
-    else
-      check(launch_l2p_add(op->u0, op->loc, y, op->n, op->b, op->n_cells, op->N, nrhs, s), "l2p");
+    check(launch_l2p_add(op->u0, op->loc, y, op->n, op->b, op->n_cells, op->N, nrhs, s), "l2p");
     op->launches++;
   }
   if (op->comm && reduce)  // sum the ranks' partial products, in place, on the same stream

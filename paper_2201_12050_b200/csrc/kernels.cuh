@@ -25,7 +25,7 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
                             c64* yh, int n, long long t_lo, long long t_hi, long long q_stride, int nrhs, int nimg,
                             cudaStream_t stream);
 // out[col] (+)= A in[col] per (cell, rhs) column col = cell * nrhs + r, A[m][k] =
-// a[m a_ms + k a_ks] (M x K): the P2M and L2P products on DMMA (csrc/cellwise.cu)
+// a[m a_ms + k a_ks] (M x K): the P2M product on DMMA (csrc/cellwise.cu)
 bool cellwise_supported(int M, int K);
 cudaError_t launch_cellwise(const c64* a, long long a_ms, long long a_ks, int M, int K, const c64* in, long long in_rs,
                             long long in_cs, c64* out, long long out_rs, long long out_cs, int nrhs, long long ncols,
@@ -44,6 +44,12 @@ cudaError_t launch_near_reduce_l2p(const c64* W, const int* tgt_ptr, const int* 
                                    int nrhs, bool accumulate, cudaStream_t stream);
 
 // ---- M2L / P2M (m2l.cu)
+// The last inverse near-field pass (x axis) with the L2P fused: out = scale DFT(in)
+// + U0 L_cell (n_in <= 32, b <= 32; lines a = r * (My Mz) + line, nrhs | n_a)
+bool dft_l2p_supported(int n_in, int n_out, int b);
+cudaError_t launch_dft_axis_l2p(const c64* in, c64* out, const c64* tw, long long n_a, int n_in, int n_out,
+                                long long n_inner, int L, double scale, const c64* u0, const c64* loc, int b, int nrhs,
+                                cudaStream_t stream);
 cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_a, int n_in, int n_out,
                             long long n_inner, int L, bool backward, double scale, cudaStream_t stream);
 cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image, long long q_total, int b,

@@ -260,10 +260,22 @@ p2m_kernel(const c64* __restrict__ v0t, const c64* __restrict__ x, c64* __restri
 constexpr int kDftMmaMax = 64;
 constexpr int kDftMmaWarps = 4;
 
-template <int KTM>
+// EPI: the L2P of the lattice near field fused into its last inverse pass (the
+// x axis: line a = r * cpl + (z My + y), output q = cell x index, inner = row i
+// of the cell): out += U0 L_cell (src/fmm.cpp:265-267) as a second small DMMA
+// product per tile, C[q][i] += sum_m L[cell(q)][r][m] U0[i][m], unscaled and
+// added after the scaled transform (y = S p, then y += U0 L).
+struct L2pEpi {
+  const c64* u0 = nullptr;   // n x b column-major: u0[m n + i]
+  const c64* loc = nullptr;  // [cell][rhs][b]
+  int b = 0, nrhs = 1;
+  long long cpl = 1;  // lines per right-hand side (My Mz)
+};
+
+template <int KTM, bool EPI = false>
 __global__ void __launch_bounds__(kDftMmaWarps * 32)
 dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ tw, long long n_a,
-                     int n_in, int n_out, long long n_inner, int L, int backward, double scale) {
+                     int n_in, int n_out, long long n_inner, int L, int backward, double scale, L2pEpi epi = {}) {
   extern __shared__ __align__(16) unsigned char dmma_smem[];
   const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
   double* wr = reinterpret_cast<double*>(dmma_smem);  // [mt][kt][lane]
@@ -309,9 +321,39 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
     load(t + nwarps);
     const long long a = t / n_et, e0 = (t % n_et) * 8;
     c64* dst = out + a * n_out * n_inner;
+    constexpr int KB = 8;  // L2P k steps (b <= 32)
+    c64 ub[EPI ? KB : 1];  // U0 B fragments of this tile's 8 rows i
+    long long lbase = 0;
+    int kb_n = 0;
+    if constexpr (EPI) {
+      kb_n = (epi.b + 3) / 4;
+      const long long r = a / epi.cpl, line = a - r * epi.cpl;
+      lbase = (line * n_out * epi.nrhs + r) * epi.b;  // loc of cell (line, q = 0), rhs r
+      const long long i = e0 + fr;
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+        const int m = kb * 4 + fk;
+        ub[kb] = (kb < kb_n && m < epi.b && i < n_inner) ? __ldg(epi.u0 + static_cast<long long>(m) * n_inner + i)
+                                                         : cmk(0.0, 0.0);
+      }
+    }
     for (int mt = 0; mt < MT; mt += 2) {  // two row blocks per pass: independent accumulator chains
       double t1[2][2] = {}, t2[2][2] = {}, t3[2][2] = {};
       const bool two = mt + 1 < MT;
+      c64 la[EPI ? 2 : 1][EPI ? KB : 1];
+      if constexpr (EPI) {  // L A fragments: row q = cell, k = coefficient m
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int q = (mt + u) * 8 + fr;
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+            const int m = kb * 4 + fk;
+            la[u][kb] = (kb < kb_n && m < epi.b && q < n_out)
+                            ? __ldg(epi.loc + lbase + static_cast<long long>(q) * epi.nrhs * epi.b + m)
+                            : cmk(0.0, 0.0);
+          }
+        }
+      }
 #pragma unroll
       for (int kt = 0; kt < KTM; ++kt) {
         if (kt < KT) {
@@ -327,6 +369,21 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
           }
         }
       }
+      double s1[2][2] = {}, s2[2][2] = {}, s3[2][2] = {};
+      if constexpr (EPI) {
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+          if (kb < kb_n) {
+            const double usum = ub[kb].x + ub[kb].y;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              dmma884(s1[u][0], s1[u][1], la[u][kb].x, ub[kb].x);
+              dmma884(s2[u][0], s2[u][1], la[u][kb].y, ub[kb].y);
+              dmma884(s3[u][0], s3[u][1], la[u][kb].x + la[u][kb].y, usum);
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int q = (mt + u) * 8 + fr;
@@ -334,9 +391,11 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const long long c = e0 + 2 * fk + h;
-          if (c < n_inner)
-            dst[static_cast<long long>(q) * n_inner + c] =
-                cmk((t1[u][h] - t2[u][h]) * scale, (t3[u][h] - t1[u][h] - t2[u][h]) * scale);
+          if (c < n_inner) {
+            c64 v = cmk((t1[u][h] - t2[u][h]) * scale, (t3[u][h] - t1[u][h] - t2[u][h]) * scale);
+            if constexpr (EPI) v = cadd(v, cmk(s1[u][h] - s2[u][h], s3[u][h] - s1[u][h] - s2[u][h]));
+            dst[static_cast<long long>(q) * n_inner + c] = v;
+          }
         }
       }
     }
@@ -1048,6 +1107,47 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     case 2: dft_axis_kernel<2><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
     default: dft_axis_kernel<1><<<grid, 256, smem, stream>>>(in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale); break;
   }
+  return cudaGetLastError();
+}
+
+bool dft_l2p_supported(int n_in, int n_out, int b) {
+  static const bool dft_mma = [] {
+    const char* v = std::getenv("FPBEM_DFT");
+    return !(v && std::strcmp(v, "fma") == 0);
+  }();
+  return dft_mma && n_in <= 32 && n_out <= kDftMmaMax && b >= 1 && b <= 32;
+}
+
+cudaError_t launch_dft_axis_l2p(const c64* in, c64* out, const c64* tw, long long n_a, int n_in, int n_out,
+                                long long n_inner, int L, double scale, const c64* u0, const c64* loc, int b, int nrhs,
+                                cudaStream_t stream) {
+  if (n_a * n_out * n_inner == 0) return cudaSuccess;
+  if (!dft_l2p_supported(n_in, n_out, b) || n_a % nrhs) return cudaErrorInvalidValue;
+  const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
+  const size_t smem = sizeof(double) * 3 * MT * KT * 32;
+  static std::atomic<unsigned long long> raised[2];
+  cudaError_t e = ensure_max_smem(raised[0], reinterpret_cast<const void*>(&dft_axis_dmma_kernel<4, true>),
+                                  static_cast<int>(sizeof(double) * 3 * 8 * 16 * 32));
+  if (e != cudaSuccess) return e;
+  e = ensure_max_smem(raised[1], reinterpret_cast<const void*>(&dft_axis_dmma_kernel<8, true>),
+                      static_cast<int>(sizeof(double) * 3 * 8 * 16 * 32));
+  if (e != cudaSuccess) return e;
+  L2pEpi epi;
+  epi.u0 = u0;
+  epi.loc = loc;
+  epi.b = b;
+  epi.nrhs = nrhs;
+  epi.cpl = n_a / nrhs;
+  const long long tiles = n_a * ((n_inner + 7) / 8);
+  long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
+  const long long cap = static_cast<long long>(device_sms()) * 4;
+  if (blocks > cap) blocks = cap;
+  if (KT <= 4)
+    dft_axis_dmma_kernel<4, true><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
+        in, out, tw, n_a, n_in, n_out, n_inner, L, 1, scale, epi);
+  else
+    dft_axis_dmma_kernel<8, true><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
+        in, out, tw, n_a, n_in, n_out, n_inner, L, 1, scale, epi);
   return cudaGetLastError();
 }
 
