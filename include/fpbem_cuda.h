@@ -241,6 +241,20 @@ int fpbem_cu_get_stream(const fpbem_cu_op* op, void** stream);
 int fpbem_cu_enable_stage_timing(fpbem_cu_op* op, int enable);
 int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out);
 
+/* Slab-distributed product (lattice near field only):
+ * rank r of `comm` (NULL = one rank) owns whole planes of cells along the slab
+ * axis (the highest lattice axis with more than one cell), rows [lo, hi) of
+ * the reference's cell-major vector layout. apply_slab takes x[lo:hi) and
+ * returns (A x)[lo:hi); inside, the pruned lattice DFTs below the slab axis run
+ * on the rank's planes, one grouped NCCL all-to-all per direction transposes to
+ * the rank's columns, where the DFTs along the slab axis, the near-field block
+ * products (the rank's share of the stored blocks) and the M2L (the rank's share
+ * of Λ) run. fpbem_cu_gmres_dist uses the plan when it is set (slab vectors, no
+ * all-gather). Every rank calls set_slabs / apply_slab collectively. */
+int fpbem_cu_fmm_set_slabs(fpbem_cu_op* op, fpbem_cu_comm* comm);
+int fpbem_cu_fmm_slab_rows(const fpbem_cu_op* op, long long* lo, long long* hi);
+int fpbem_cu_fmm_apply_slab(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int ptr_kind);
+
 /* Number of CUDA kernels this handle launched since creation. */
 long long fpbem_cu_kernel_launches(const fpbem_cu_op* op);
 

@@ -87,7 +87,8 @@ ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_
 CUDA_SYMBOLS = (
     "fpbem_cu_fmm_create", "fpbem_cu_fmm_destroy", "fpbem_cu_fmm_apply", "fpbem_cu_gmres",
     "fpbem_cu_gmres_fn", "fpbem_cu_fmm_bytes", "fpbem_cu_fmm_near_path", "fpbem_cu_spectrum", "fpbem_cu_set_stream",
-    "fpbem_cu_get_stream", "fpbem_cu_far_info",    "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
+    "fpbem_cu_get_stream", "fpbem_cu_far_info", "fpbem_cu_fmm_set_slabs", "fpbem_cu_fmm_slab_rows",
+    "fpbem_cu_fmm_apply_slab",    "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
     "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
     "fpbem_cu_comm_from_callback", "fpbem_cu_gmres_dist", "fpbem_cu_gmres_dist_rows",
     "fpbem_cu_fmm_set_partition", "fpbem_cu_fmm_partition", "fpbem_cu_fmm_far_pairs", "fpbem_cu_partition_pairs", "fpbem_cu_assemble_near", "fpbem_cu_assemble_hat",
@@ -119,6 +120,9 @@ def cuda() -> C.CDLL:
             "fpbem_cu_set_stream": (C.c_int, [vp, vp]),
             "fpbem_cu_get_stream": (C.c_int, [vp, C.POINTER(vp)]),
             "fpbem_cu_far_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "fpbem_cu_fmm_set_slabs": (C.c_int, [vp, vp]),
+            "fpbem_cu_fmm_slab_rows": (C.c_int, [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+            "fpbem_cu_fmm_apply_slab": (C.c_int, [vp, vp, vp, C.c_int]),
             "fpbem_cu_enable_stage_timing": (C.c_int, [vp, C.c_int]),
             "fpbem_cu_stage_times": (C.c_int, [vp, c_double_p]),
             "fpbem_cu_kernel_launches": (C.c_longlong, [vp]),

@@ -24,7 +24,7 @@ ORACLE = ROOT / "oracle"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_SOURCES = ["near_field.cu", "m2l.cu", "krylov.cu", "assembly.cu", "far_bank.cu", "fpbem_cuda.cu", "gmres.cu",
-                "device_assembly.cu", "comm.cu", "gmres_dist.cu", "cellwise.cu"]
+                "device_assembly.cu", "comm.cu", "gmres_dist.cu", "cellwise.cu", "slab.cu"]
 HOST_SOURCES = ["geometry.cpp", "kernels.cpp", "specfun.cpp", "assembly.cpp", "postproc.cpp", "capi.cpp"]
 # portable x86-64 ISA level: the GPU box CPU may differ from the build container's
 CPU_FLAGS = ["-O3", "-march=x86-64-v3", "-fPIC", "-fopenmp", "-std=c++17"]

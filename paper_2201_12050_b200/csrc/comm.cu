@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "handle.cuh"
 
@@ -106,6 +107,57 @@ void comm_allgather(fpbem_cu_comm* c, const double* mine, double* full, size_t p
   check(cudaStreamSynchronize(s), "comm unstage");
 }
 
+void comm_alltoallv(fpbem_cu_comm* c, const A2aPart* parts, int n_parts, cudaStream_t s) {
+  if (!c) {  // a single rank: its own blocks
+    for (int k = 0; k < n_parts; ++k) {
+      const A2aPart& p = parts[k];
+      if (p.scount[0])
+        check(cudaMemcpyAsync(p.recv + p.rdisp[0], p.send + p.sdisp[0], p.scount[0] * sizeof(double),
+                              cudaMemcpyDeviceToDevice, s),
+              "slab exchange (one rank)");
+    }
+    return;
+  }
+  const int P = c->nranks, me = c->rank;
+  if (!c->cb) {
+    nccl_rc(c->group_start(), "ncclGroupStart");
+    for (int k = 0; k < n_parts; ++k) {
+      const A2aPart& p = parts[k];
+      for (int d = 0; d < P; ++d) {
+        if (p.scount[d]) nccl_rc(c->send(p.send + p.sdisp[d], p.scount[d], kNcclFloat64, d, c->comm, s), "ncclSend");
+        if (p.rcount[d]) nccl_rc(c->recv(p.recv + p.rdisp[d], p.rcount[d], kNcclFloat64, d, c->comm, s), "ncclRecv");
+      }
+    }
+    nccl_rc(c->group_end(), "ncclGroupEnd");
+    return;
+  }
+  // host-staged: every (src, dst) block at its place in one zero-filled buffer,
+  // summed over the ranks (each block has exactly one non-zero contributor)
+  for (int k = 0; k < n_parts; ++k) {
+    const A2aPart& p = parts[k];
+    std::vector<size_t> off(static_cast<size_t>(P) * P + 1, 0);
+    for (size_t i = 0; i < static_cast<size_t>(P) * P; ++i) off[i + 1] = off[i] + p.all[i];
+    const size_t total = off.back();
+    if (total == 0) continue;
+    double* h = stage(c, total);
+    check(cudaStreamSynchronize(s), "comm stage");
+    std::memset(h, 0, total * sizeof(double));
+    for (int d = 0; d < P; ++d)
+      if (p.scount[d])
+        check(cudaMemcpyAsync(h + off[static_cast<size_t>(me) * P + d], p.send + p.sdisp[d],
+                              p.scount[d] * sizeof(double), cudaMemcpyDeviceToHost, s),
+              "comm stage");
+    check(cudaStreamSynchronize(s), "comm stage");
+    host_allreduce(c, h, total);
+    for (int r = 0; r < P; ++r)
+      if (p.rcount[r])
+        check(cudaMemcpyAsync(p.recv + p.rdisp[r], h + off[static_cast<size_t>(r) * P + me],
+                              p.rcount[r] * sizeof(double), cudaMemcpyHostToDevice, s),
+              "comm unstage");
+    check(cudaStreamSynchronize(s), "comm unstage");
+  }
+}
+
 }  // namespace fpbem_cu
 
 extern "C" {
@@ -141,7 +193,12 @@ int fpbem_cu_comm_init(const unsigned char id[128], int nranks, int rank, int de
     c->allgather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, void*)>(
         dlsym(lib, "ncclAllGather"));
     c->destroy = reinterpret_cast<int (*)(void*)>(dlsym(lib, "ncclCommDestroy"));
-    if (!init || !c->allreduce || !c->reduce_scatter || !c->allgather || !c->destroy) {
+    c->send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, void*)>(dlsym(lib, "ncclSend"));
+    c->recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, void*)>(dlsym(lib, "ncclRecv"));
+    c->group_start = reinterpret_cast<int (*)()>(dlsym(lib, "ncclGroupStart"));
+    c->group_end = reinterpret_cast<int (*)()>(dlsym(lib, "ncclGroupEnd"));
+    if (!init || !c->allreduce || !c->reduce_scatter || !c->allgather || !c->destroy || !c->send || !c->recv ||
+        !c->group_start || !c->group_end) {
       delete c;
       fail(FPBEM_CU_ENCCL, "NCCL symbols missing");
     }

@@ -1035,6 +1035,7 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
   if (!op) return;
   cudaSetDevice(op->device);
   if (op->stream) cudaStreamSynchronize(op->stream);
+  slab_destroy(op);
   for (void* p : {static_cast<void*>(op->S), static_cast<void*>(op->pair_src), static_cast<void*>(op->tgt_ptr),
                   static_cast<void*>(op->tgt_pairs), static_cast<void*>(op->jobs), static_cast<void*>(op->u0),
                   static_cast<void*>(op->v0), static_cast<void*>(op->v0t), static_cast<void*>(op->z_items_pair),

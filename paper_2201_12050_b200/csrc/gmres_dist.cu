@@ -34,11 +34,22 @@ struct Slab {
   long long lo = 0, hi = 0;  // this rank's global rows [lo, hi)
 };
 
+// the communicator of the distributed solve: the slab plan's, else the pair partition's
+fpbem_cu_comm* dist_comm(const fpbem_cu_op* op) { return op->slab ? slab_comm(op) : op->comm; }
+
 Slab slab_of(const fpbem_cu_op* op) {
   Slab sl;
-  if (op->comm) {
-    sl.nranks = op->comm->nranks;
-    sl.rank = op->comm->rank;
+  if (fpbem_cu_comm* c = dist_comm(op)) {
+    sl.nranks = c->nranks;
+    sl.rank = c->rank;
+  }
+  if (op->slab) {  // whole planes of the slab plan: ceil(planes / P) per rank
+    long long lo = 0, hi = 0, per = 0;
+    slab_range(op, sl.rank, &lo, &hi, &per);
+    sl.rows = per;
+    sl.lo = lo;
+    sl.hi = hi;
+    return sl;
   }
   const long long cells = (op->n_cells + sl.nranks - 1) / sl.nranks;
   sl.rows = cells * op->n;
@@ -57,7 +68,7 @@ DistOut gmres_dist(fpbem_cu_op* op, const c64* b, bool b_host, c64* x, bool x_ho
                    int max_iter) {
   using cd = std::complex<double>;
   cudaStream_t s = op->stream;
-  fpbem_cu_comm* comm = op->comm;
+  fpbem_cu_comm* comm = dist_comm(op);
   const Slab sl = slab_of(op);
   const long long ns = sl.rows;
   const long long nfull = ns * sl.nranks;
@@ -99,6 +110,7 @@ DistOut gmres_dist(fpbem_cu_op* op, const c64* b, bool b_host, c64* x, bool x_ho
   check(cudaMemsetAsync(pfull, 0, static_cast<size_t>(nfull) * sizeof(c64), s), "pad rows");
   check(cudaMemsetAsync(bl, 0, vb, s), "b slab");
   check(cudaMemsetAsync(xl, 0, vb, s), "x0");
+  check(cudaMemsetAsync(tl, 0, vb, s), "Ax");  // padding rows of the slab product stay zero
   check(cudaMemsetAsync(V, 0, vb * (m + 1), s), "basis");
   const size_t mine = static_cast<size_t>(sl.hi - sl.lo) * sizeof(c64);
   if (mine)
@@ -125,6 +137,10 @@ DistOut gmres_dist(fpbem_cu_op* op, const c64* b, bool b_host, c64* x, bool x_ho
   auto col = [&](int j) { return V + static_cast<long long>(j) * ns; };
   // out (slab) = A in (slab): gather, this rank's partial product, reduce-scatter
   auto product = [&](const c64* in, c64* out) {
+    if (op->slab) {  // slab in, slab out: the all-to-all transposes live inside the product
+      slab_apply(op, in, out);
+      return;
+    }
     comm_allgather(comm, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(pfull), 2 * ns, s);
     apply_device(op, pfull, ypart, 1, false);
     comm_reduce_scatter(comm, reinterpret_cast<double*>(ypart), reinterpret_cast<double*>(out), 2 * ns, s);
@@ -239,7 +255,7 @@ int fpbem_cu_gmres_dist(fpbem_cu_op* op, const fpbem_c64* b, fpbem_c64* x, doubl
                         int* history_len) {
   return guard([&] {
     if (!op || !b || !x || !iterations || !converged) fail(FPBEM_CU_EINVAL, "gmres_dist: null argument");
-    if (!op->comm && op->nranks > 1)
+    if (!op->slab && !op->comm && op->nranks > 1)
       fail(FPBEM_CU_EINVAL, "gmres_dist: a pair partition needs a communicator (fpbem_cu_fmm_set_comm)");
     check(cudaSetDevice(op->device), "set device");
     const bool host = ptr_kind != FPBEM_CU_PTR_DEVICE;

@@ -80,6 +80,10 @@ struct fpbem_cu_comm {
   int (*reduce_scatter)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
   int (*allgather)(const void*, void*, size_t, int, void*, void*) = nullptr;
   int (*destroy)(void*) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, void*) = nullptr;  // ncclSend(buf, count, type, peer, comm, stream)
+  int (*recv)(void*, size_t, int, int, void*, void*) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
   // host callback form (cb != nullptr)
   fpbem_cu_allreduce_fn cb = nullptr;
   void* cb_ctx = nullptr;
@@ -195,6 +199,7 @@ struct fpbem_cu_op {
   long long launches = 0;
 
   fpbem_cu_comm* comm = nullptr;
+  struct SlabPlan* slab = nullptr;  // slab-distributed product (slab.cu), set by fpbem_cu_fmm_set_slabs
 };
 
 namespace fpbem_cu {
@@ -209,4 +214,21 @@ void ensure_pinned(fpbem_cu_op* op, size_t bytes);
 void comm_allreduce(fpbem_cu_comm* c, double* buf, size_t count, cudaStream_t s);
 void comm_reduce_scatter(fpbem_cu_comm* c, double* full, double* mine, size_t per_rank, cudaStream_t s);
 void comm_allgather(fpbem_cu_comm* c, const double* mine, double* full, size_t per_rank, cudaStream_t s);
+// one block of an all-to-all: this rank sends send + sdisp[d] (scount[d] doubles)
+// to every rank d and receives rcount[s] doubles from rank s at recv + rdisp[s];
+// `all` is the P x P matrix of block sizes [src * P + dst] (every rank's view,
+// for the host-staged form)
+struct A2aPart {
+  const double* send;
+  double* recv;
+  const size_t *scount, *sdisp, *rcount, *rdisp, *all;
+};
+// the parts' transfers in one NCCL group (send/recv), or host-staged one after another
+void comm_alltoallv(fpbem_cu_comm* c, const A2aPart* parts, int n_parts, cudaStream_t s);
+void slab_destroy(fpbem_cu_op* op);
+// slab plan (slab.cu): y = (A x) on this rank's planes, device pointers, one right-hand side
+void slab_apply(fpbem_cu_op* op, const c64* x, c64* y);
+fpbem_cu_comm* slab_comm(const fpbem_cu_op* op);
+// rank r's rows [lo, hi) and the padded rows per rank (ceil(planes / P) planes)
+void slab_range(const fpbem_cu_op* op, int r, long long* lo, long long* hi, long long* per_rank_rows);
 }  // namespace fpbem_cu

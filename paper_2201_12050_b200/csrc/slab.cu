@@ -1,0 +1,565 @@
+// C-ABI implementation, part 6: the slab-distributed product (SURVEY.md §8e,
+// cfg3 row; north_star: "Fourier modes and near-field cell slabs are split per
+// GPU, and the FFT transpose is an NCCL all-to-all over NVLink").
+//
+// FmmOperators::matvec (src/fmm.cpp:246-271) with the lattice near field and
+// the M2L both applied as DFT convolutions (CirculantSpectrum::matvec,
+// src/structured.cpp:122-166, and its application to the Toeplitz blocks of
+// BlockToeplitzMatrix::matvec, src/assembly.cpp:62-84). The vectors are split
+// into slabs of whole planes along the slab axis s (the highest lattice axis
+// with more than one cell: rows of the reference's cell-major layout stay
+// contiguous). Per product, each rank:
+//   1. P2M on its cells; DFTs along the axes below s on its planes (near field
+//      over n fields, far field over b coefficients);
+//   2. forward exchange (one grouped NCCL send/recv set for both fields): the
+//      transposition from "my planes, every column" to "every plane, my
+//      columns", a column being the set of modes with equal indices below s;
+//   3. on its columns: the DFT along s, the per-mode block products with this
+//      rank's share of the stored near-field blocks (one per orbit of modes;
+//      the orbits of a column class never leave it) and of Λ, the inverse DFT
+//      along s (with 1/q);
+//   4. backward exchange, the inverse DFTs below s on its planes, L2P.
+// A column class is a column with its images under the sign flips of the axes
+// below s: closed under the cell symmetries' orbits and under the Λ mirror
+// pairing, so every work item of a rank reads and writes only its columns.
+// Classes go to ranks by longest-processing-time on the stored-block (near) /
+// column (far) counts; every rank derives the same plan from the same data,
+// so the plan needs no communication. Λ and the near-field block spectrum are
+// stored per rank only for its columns (sharded, 1/P of the HBM each).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <vector>
+
+#include "handle.cuh"
+
+// (global scope: fpbem_cu_op holds a `struct SlabPlan*`)
+struct SlabSide {
+  long long Ls = 1;          // lattice length along the slab axis
+  long long cx = 1, cy = 1;  // lattice extents of the column axes (cy = 1 unless the slab axis is z)
+  long long C = 1;           // columns per plane = cx cy
+  int E = 0;                 // complex values per (plane, column): n (near) or b (far)
+  std::vector<std::vector<int>> cols;  // per rank: its global columns in local order
+  std::vector<int> lc;                 // global column -> local index on its owner
+  int* idx = nullptr;                  // device: pack order, (z_local, column) as z * C + col, by destination
+  long long n_idx = 0;
+  std::vector<size_t> fsc, fsd, frc, frd, fall;  // forward exchange (doubles)
+  std::vector<size_t> bsc, bsd, brc, brd, ball;  // backward exchange
+  c64* pack = nullptr;  // ms C E
+  c64* recv = nullptr;  // max(Ms, Ls) |cols_me| E
+  c64* work = nullptr;  // Ls |cols_me| E
+};
+
+struct SlabPlan {
+  fpbem_cu_comm* comm = nullptr;
+  int P = 1, rank = 0, axis = 0;
+  long long Ms = 1;  // cells along the slab axis
+  long long Cm = 1;  // cells per plane (axes below s)
+  long long mx = 1, my = 1;  // cell extents of the column axes
+  std::vector<long long> zlo;  // plane range per rank (P + 1 entries)
+  long long ms = 0;            // this rank's planes
+  SlabSide nr, fr;             // near-field lattice, far-field (M2L) lattice
+  c64* shat = nullptr;         // this rank's stored near-field blocks
+  int* items = nullptr;        // [n_items][8] local modes, then [n_items][8] g
+  long long n_items = 0;
+  c64* lambda = nullptr;       // Λ of this rank's columns, [qs][column][b b]
+  int2* zitems = nullptr;      // fused z-kernel items over local columns
+  int n_zitems = 0;
+  bool zfused = false;
+  c64* a = nullptr;  // plane buffers, ms * max(near, far) plane sizes
+  c64* b = nullptr;
+  c64* mom = nullptr;
+  c64* loc = nullptr;
+  std::vector<void*> owned;
+};
+
+namespace fpbem_cu {
+
+void slab_destroy(fpbem_cu_op* op) {
+  if (!op || !op->slab) return;
+  for (void* p : op->slab->owned) cudaFree(p);
+  delete op->slab;
+  op->slab = nullptr;
+}
+
+}  // namespace fpbem_cu
+
+using namespace fpbem_cu;
+
+namespace {
+
+__global__ void gather_rows_kernel(const c64* __restrict__ src, c64* __restrict__ dst, const int* __restrict__ idx,
+                                   long long rows, int E) {
+  const long long total = rows * E;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = g / E;
+    dst[g] = src[static_cast<long long>(idx[r]) * E + (g - r * E)];
+  }
+}
+
+__global__ void scatter_rows_kernel(const c64* __restrict__ src, c64* __restrict__ dst, const int* __restrict__ idx,
+                                    long long rows, int E) {
+  const long long total = rows * E;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = g / E;
+    dst[static_cast<long long>(idx[r]) * E + (g - r * E)] = src[g];
+  }
+}
+
+int rows_grid(long long total) {
+  const long long blocks = (total + 255) / 256;
+  return static_cast<int>(std::max(1LL, std::min(blocks, 8LL * device_sms())));
+}
+
+void gather_rows(const c64* src, c64* dst, const int* idx, long long rows, int E, cudaStream_t s) {
+  if (rows * E == 0) return;
+  gather_rows_kernel<<<rows_grid(rows * E), 256, 0, s>>>(src, dst, idx, rows, E);
+  check(cudaGetLastError(), "slab pack");
+}
+
+void scatter_rows(const c64* src, c64* dst, const int* idx, long long rows, int E, cudaStream_t s) {
+  if (rows * E == 0) return;
+  scatter_rows_kernel<<<rows_grid(rows * E), 256, 0, s>>>(src, dst, idx, rows, E);
+  check(cudaGetLastError(), "slab unpack");
+}
+
+template <typename T>
+T* palloc(SlabPlan* sp, size_t count, const char* what) {
+  T* p = dalloc<T>(count, what);
+  sp->owned.push_back(p);
+  return p;
+}
+
+// column classes of a cx x cy column lattice under the sign flips of its axes,
+// each class sorted, classes in order of their smallest column
+std::vector<std::vector<int>> column_classes(long long cx, long long cy) {
+  std::vector<int> cls(static_cast<size_t>(cx * cy), -1);
+  std::vector<std::vector<int>> out;
+  for (long long c = 0; c < cx * cy; ++c) {
+    if (cls[c] >= 0) continue;
+    const long long qx = c % cx, qy = c / cx;
+    std::vector<int> ids;
+    for (int f = 0; f < 4; ++f) {
+      const long long x = (f & 1) ? (cx - qx) % cx : qx, y = (f & 2) ? (cy - qy) % cy : qy;
+      ids.push_back(static_cast<int>(y * cx + x));
+    }
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    for (int i : ids) cls[i] = static_cast<int>(out.size());
+    out.push_back(ids);
+  }
+  return out;
+}
+
+// longest processing time first: classes by cost (desc, then index), each to
+// the least loaded rank (lowest index on ties); deterministic on every rank
+std::vector<int> assign_classes(const std::vector<double>& cost, int P) {
+  std::vector<int> order(cost.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(P, 0.0);
+  std::vector<int> owner(cost.size(), 0);
+  for (int k : order) {
+    const int r = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+    owner[k] = r;
+    load[r] += cost[k];
+  }
+  return owner;
+}
+
+// the side's columns per rank, local indices, pack order and exchange sizes
+void build_side(SlabPlan* sp, SlabSide& sd, const std::vector<std::vector<int>>& classes, const std::vector<int>& owner,
+                cudaStream_t s) {
+  const int P = sp->P, me = sp->rank;
+  sd.cols.assign(P, {});
+  sd.lc.assign(static_cast<size_t>(sd.C), -1);
+  for (size_t k = 0; k < classes.size(); ++k)
+    for (int c : classes[k]) sd.cols[owner[k]].push_back(c);
+  for (int r = 0; r < P; ++r) {
+    std::sort(sd.cols[r].begin(), sd.cols[r].end());
+    for (size_t i = 0; i < sd.cols[r].size(); ++i) sd.lc[sd.cols[r][i]] = static_cast<int>(i);
+  }
+  const long long ms = sp->ms;
+  std::vector<int> idx;
+  idx.reserve(static_cast<size_t>(ms * sd.C));
+  for (int d = 0; d < P; ++d)
+    for (long long z = 0; z < ms; ++z)
+      for (int c : sd.cols[d]) idx.push_back(static_cast<int>(z * sd.C + c));
+  sd.n_idx = static_cast<long long>(idx.size());
+  sd.idx = palloc<int>(sp, idx.size(), "slab pack order");
+  h2d(sd.idx, idx.data(), idx.size() * sizeof(int), s, "slab pack order");
+  const size_t E2 = 2 * static_cast<size_t>(sd.E);
+  auto planes = [&](int r) { return static_cast<size_t>(sp->zlo[r + 1] - sp->zlo[r]); };
+  const size_t mycols = sd.cols[me].size();
+  sd.fsc.assign(P, 0);
+  sd.fsd.assign(P, 0);
+  sd.frc.assign(P, 0);
+  sd.frd.assign(P, 0);
+  sd.bsc.assign(P, 0);
+  sd.bsd.assign(P, 0);
+  sd.brc.assign(P, 0);
+  sd.brd.assign(P, 0);
+  sd.fall.assign(static_cast<size_t>(P) * P, 0);
+  sd.ball.assign(static_cast<size_t>(P) * P, 0);
+  size_t off = 0;
+  for (int d = 0; d < P; ++d) {
+    sd.fsc[d] = planes(me) * sd.cols[d].size() * E2;  // my planes, d's columns
+    sd.fsd[d] = off;
+    off += sd.fsc[d];
+    sd.frc[d] = planes(d) * mycols * E2;  // d's planes, my columns
+    sd.frd[d] = static_cast<size_t>(sp->zlo[d]) * mycols * E2;
+    sd.bsc[d] = sd.frc[d];  // back: d's planes of my columns
+    sd.bsd[d] = sd.frd[d];
+    sd.brc[d] = sd.fsc[d];  // my planes of d's columns, in pack order
+    sd.brd[d] = sd.fsd[d];
+    for (int r = 0; r < P; ++r) {
+      sd.fall[static_cast<size_t>(r) * P + d] = planes(r) * sd.cols[d].size() * E2;
+      sd.ball[static_cast<size_t>(d) * P + r] = planes(r) * sd.cols[d].size() * E2;
+    }
+  }
+  const size_t rows_loc = static_cast<size_t>(std::max(sp->Ms, sd.Ls)) * mycols;
+  sd.pack = palloc<c64>(sp, static_cast<size_t>(ms * sd.C) * sd.E, "slab pack");
+  sd.recv = palloc<c64>(sp, rows_loc * sd.E, "slab columns");
+  sd.work = palloc<c64>(sp, rows_loc * sd.E, "slab column spectra");
+}
+
+void build_plan(fpbem_cu_op* op, fpbem_cu_comm* comm) {
+  if (!op->near_fft) fail(FPBEM_CU_EINVAL, "set_slabs: needs the lattice near field (near_path = lattice)");
+  if (op->mirrored_level >= 0) fail(FPBEM_CU_EINVAL, "set_slabs: not with a half-space image pair");
+  auto* sp = new SlabPlan();
+  op->slab = sp;  // owned by the handle from here (freed on failure by the caller's slab_destroy)
+  cudaStream_t s = op->stream;
+  sp->comm = comm;
+  sp->P = comm ? comm->nranks : 1;
+  sp->rank = comm ? comm->rank : 0;
+  const int* M = op->counts;
+  int ax = 0;
+  for (int k = 2; k >= 0; --k)
+    if (M[k] > 1) {
+      ax = k;
+      break;
+    }
+  sp->axis = ax;
+  sp->Ms = M[ax];
+  sp->mx = ax > 0 ? M[0] : 1;
+  sp->my = ax > 1 ? M[1] : 1;
+  sp->Cm = sp->mx * sp->my;
+  const long long per = (sp->Ms + sp->P - 1) / sp->P;
+  sp->zlo.resize(sp->P + 1);
+  for (int r = 0; r <= sp->P; ++r) sp->zlo[r] = std::min(sp->Ms, per * r);
+  sp->ms = sp->zlo[sp->rank + 1] - sp->zlo[sp->rank];
+
+  // ---- near field: columns of the Ln lattice below the slab axis
+  SlabSide& nr = sp->nr;
+  nr.Ls = op->Ln[ax];
+  nr.cx = ax > 0 ? op->Ln[0] : 1;
+  nr.cy = ax > 1 ? op->Ln[1] : 1;
+  nr.C = nr.cx * nr.cy;
+  nr.E = op->n;
+  const auto ncls = column_classes(nr.cx, nr.cy);
+  std::vector<int> ncls_of(static_cast<size_t>(nr.C));
+  for (size_t k = 0; k < ncls.size(); ++k)
+    for (int c : ncls[k]) ncls_of[c] = static_cast<int>(k);
+  std::vector<double> ncost(ncls.size(), 0.0);
+  for (long long t = 0; t < op->n_items; ++t) ncost[ncls_of[op->items_q[t * 8] % nr.C]] += 1.0;
+  const auto nown = assign_classes(ncost, sp->P);
+  build_side(sp, nr, ncls, nown, s);
+  // this rank's items (orbits never leave a column class): local modes
+  // q = qs |cols| + local column, and their stored blocks
+  const long long mycols = static_cast<long long>(nr.cols[sp->rank].size());
+  std::vector<int> iq, ig;
+  std::vector<long long> mine;
+  for (long long t = 0; t < op->n_items; ++t) {
+    if (nown[ncls_of[op->items_q[t * 8] % nr.C]] != sp->rank) continue;
+    mine.push_back(t);
+    for (int i = 0; i < 8; ++i) {
+      const int q = op->items_q[t * 8 + i];
+      iq.push_back(q < 0 ? -1 : static_cast<int>((q / nr.C) * mycols + nr.lc[q % nr.C]));
+      ig.push_back(op->items_g[t * 8 + i]);
+    }
+  }
+  sp->n_items = static_cast<long long>(mine.size());
+  std::vector<int> items(iq);
+  items.insert(items.end(), ig.begin(), ig.end());
+  sp->items = palloc<int>(sp, items.size(), "slab items");
+  h2d(sp->items, items.data(), items.size() * sizeof(int), s, "slab items");
+  const size_t nn = static_cast<size_t>(op->n) * op->n;
+  sp->shat = palloc<c64>(sp, mine.size() * nn, "slab near spectrum");
+  for (size_t i = 0; i < mine.size(); ++i)
+    check(cudaMemcpyAsync(sp->shat + i * nn, op->shat + static_cast<size_t>(mine[i]) * nn, nn * sizeof(c64),
+                          cudaMemcpyDeviceToDevice, s),
+          "slab near spectrum");
+
+  // ---- far field: columns of the M2L lattice below the slab axis
+  SlabSide& fr = sp->fr;
+  fr.Ls = op->L[ax];
+  fr.cx = ax > 0 ? op->L[0] : 1;
+  fr.cy = ax > 1 ? op->L[1] : 1;
+  fr.C = fr.cx * fr.cy;
+  fr.E = op->b;
+  const auto fcls = column_classes(fr.cx, fr.cy);
+  std::vector<double> fcost(fcls.size());
+  for (size_t k = 0; k < fcls.size(); ++k) fcost[k] = static_cast<double>(fcls[k].size());
+  const auto fown = assign_classes(fcost, sp->P);
+  build_side(sp, fr, fcls, fown, s);
+  const std::vector<int>& fcols = fr.cols[sp->rank];
+  const long long fmy = static_cast<long long>(fcols.size());
+  const size_t b2 = static_cast<size_t>(op->b) * op->b;
+  std::vector<int> lam_idx;  // local Λ rows (qs, local column) <- global q = qs C + col
+  for (long long qs = 0; qs < fr.Ls; ++qs)
+    for (int c : fcols) lam_idx.push_back(static_cast<int>(qs * fr.C + c));
+  sp->lambda = palloc<c64>(sp, lam_idx.size() * b2, "slab spectrum");
+  if (!lam_idx.empty()) {
+    int* d_idx = dalloc<int>(lam_idx.size(), "slab spectrum rows");
+    std::unique_ptr<int, decltype(&cudaFree)> keep(d_idx, &cudaFree);
+    h2d(d_idx, lam_idx.data(), lam_idx.size() * sizeof(int), s, "slab spectrum rows");
+    gather_rows(op->lambda, sp->lambda, d_idx, static_cast<long long>(lam_idx.size()), static_cast<int>(b2), s);
+    check(cudaStreamSynchronize(s), "slab spectrum");
+  }
+  // the fused z kernel's items over local columns: a column with its mirror
+  // (the Λ parity, when verified) or alone
+  sp->zfused = fr.Ls > 1 && m2l_zfused_ring(static_cast<int>(sp->Ms), static_cast<int>(fr.Ls), op->b, op->b) > 0;
+  if (sp->zfused) {
+    std::vector<int2> zi;
+    for (int c : fcols) {
+      const long long qx = c % fr.cx, qy = c / fr.cx;
+      const int cm = static_cast<int>(((fr.cy - qy) % fr.cy) * fr.cx + (fr.cx - qx) % fr.cx);
+      const int l = fr.lc[c], lm = fr.lc[cm];
+      if (!op->lam_paired)
+        zi.push_back(make_int2(l, -1));
+      else if (c < cm)
+        zi.push_back(make_int2(l, lm));
+      else if (c == cm)
+        zi.push_back(make_int2(l, -1));
+    }
+    sp->n_zitems = static_cast<int>(zi.size());
+    sp->zitems = palloc<int2>(sp, zi.size(), "slab z items");
+    h2d(sp->zitems, zi.data(), zi.size() * sizeof(int2), s, "slab z items");
+  }
+  (void)fmy;
+  const size_t plane_max = static_cast<size_t>(std::max(nr.C * nr.E, fr.C * fr.E));
+  sp->a = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes");
+  sp->b = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes");
+  sp->mom = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab moments");
+  sp->loc = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab locals");
+  check(cudaStreamSynchronize(s), "slab plan");
+}
+
+// forward DFTs along the column axes (x, then y when the slab axis is z) of
+// this rank's planes: [ms][my][mx][E] -> [ms][cy][cx][E]; returns the result
+const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* const* tw, cudaStream_t s) {
+  const c64* cur = in;
+  c64* bufs[2] = {sp->a, sp->b};
+  int which = 0;
+  if (sp->ms == 0) return cur;
+  if (sd.cx > 1) {
+    check(launch_dft_axis(cur, bufs[which], tw[0], sp->my * sp->ms, static_cast<int>(sp->mx), static_cast<int>(sd.cx),
+                          sd.E, static_cast<int>(sd.cx), false, 1.0, s),
+          "slab dft x");
+    cur = bufs[which];
+    which ^= 1;
+    op->launches++;
+  }
+  if (sd.cy > 1) {
+    check(launch_dft_axis(cur, bufs[which], tw[1], sp->ms, static_cast<int>(sp->my), static_cast<int>(sd.cy),
+                          sd.cx * sd.E, static_cast<int>(sd.cy), false, 1.0, s),
+          "slab dft y");
+    cur = bufs[which];
+    op->launches++;
+  }
+  return cur;
+}
+
+// inverse of local_forward from the unpacked planes `in` into `out`
+void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* out, c64* const* tw,
+                   cudaStream_t s) {
+  if (sp->ms == 0) return;
+  const c64* cur = in;
+  c64* tmp = in == sp->a ? sp->b : sp->a;
+  const int passes = (sd.cy > 1) + (sd.cx > 1);
+  int done = 0;
+  if (sd.cy > 1) {
+    c64* dst = ++done == passes ? out : tmp;
+    check(launch_dft_axis(cur, dst, tw[1], sp->ms, static_cast<int>(sd.cy), static_cast<int>(sp->my), sd.cx * sd.E,
+                          static_cast<int>(sd.cy), true, 1.0, s),
+          "slab inverse dft y");
+    cur = dst;
+    op->launches++;
+  }
+  if (sd.cx > 1) {
+    check(launch_dft_axis(cur, out, tw[0], sp->my * sp->ms, static_cast<int>(sd.cx), static_cast<int>(sp->mx), sd.E,
+                          static_cast<int>(sd.cx), true, 1.0, s),
+          "slab inverse dft x");
+    op->launches++;
+  }
+}
+
+// y_loc = (A x)[this rank's planes] from x_loc = x[this rank's planes], one right-hand side
+void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
+  SlabPlan* sp = op->slab;
+  cudaStream_t s = op->stream;
+  const long long cells = sp->ms * sp->Cm;
+  SlabSide& nr = sp->nr;
+  SlabSide& fr = sp->fr;
+  const long long ncols = static_cast<long long>(nr.cols[sp->rank].size());
+  const long long fcols = static_cast<long long>(fr.cols[sp->rank].size());
+
+  // ---- 1. P2M, DFTs below the slab axis, pack (far, then near)
+  if (cells > 0) {
+    if (cellwise_supported(op->b, op->n))
+      check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, cells * op->n, op->n, sp->mom, op->b, op->b, 1, cells,
+                            false, s),
+            "slab p2m");
+    else
+      check(launch_p2m(op->v0t, x, sp->mom, op->n, op->b, cells * op->n, 1, static_cast<int>(cells), s), "slab p2m");
+    op->launches++;
+  }
+  const c64* fplanes = local_forward(op, sp, fr, sp->mom, op->tw, s);
+  gather_rows(fplanes, fr.pack, fr.idx, fr.n_idx, fr.E, s);
+  const c64* nplanes = local_forward(op, sp, nr, x, op->twn, s);
+  gather_rows(nplanes, nr.pack, nr.idx, nr.n_idx, nr.E, s);
+  op->launches += 2;
+
+  // ---- 2. forward exchange: every plane of my columns
+  {
+    const A2aPart parts[2] = {
+        {reinterpret_cast<const double*>(fr.pack), reinterpret_cast<double*>(fr.recv), fr.fsc.data(), fr.fsd.data(),
+         fr.frc.data(), fr.frd.data(), fr.fall.data()},
+        {reinterpret_cast<const double*>(nr.pack), reinterpret_cast<double*>(nr.recv), nr.fsc.data(), nr.fsd.data(),
+         nr.frc.data(), nr.frd.data(), nr.fall.data()}};
+    comm_alltoallv(sp->comm, parts, 2, s);
+  }
+
+  // ---- 3. along the slab axis on my columns: far (M2L) then near
+  const double fscale = 1.0 / static_cast<double>(op->q_total), nscale = 1.0 / static_cast<double>(op->qn);
+  const int ax = sp->axis;
+  if (fcols > 0) {
+    if (sp->zfused) {
+      check(launch_m2l_zfused(fr.recv, fr.work, sp->lambda, op->tw[ax], static_cast<int>(sp->Ms),
+                              static_cast<int>(fr.Ls), fcols, op->b, op->b, fscale, sp->zitems, sp->n_zitems, s),
+            "slab m2l z-fused");
+      std::swap(fr.recv, fr.work);  // result in recv
+      op->launches++;
+    } else {
+      check(launch_dft_axis(fr.recv, fr.work, op->tw[ax], 1, static_cast<int>(sp->Ms), static_cast<int>(fr.Ls),
+                            fcols * op->b, static_cast<int>(fr.Ls), false, 1.0, s),
+            "slab m2l dft");
+      check(launch_mode_product(sp->lambda, fr.work, fr.recv, fr.Ls * fcols, op->b, 1, s), "slab mode product");
+      check(launch_dft_axis(fr.recv, fr.work, op->tw[ax], 1, static_cast<int>(fr.Ls), static_cast<int>(sp->Ms),
+                            fcols * op->b, static_cast<int>(fr.Ls), true, fscale, s),
+            "slab m2l inverse dft");
+      std::swap(fr.recv, fr.work);
+      op->launches += 3;
+    }
+  }
+  if (ncols > 0) {
+    check(launch_dft_axis(nr.recv, nr.work, op->twn[ax], 1, static_cast<int>(sp->Ms), static_cast<int>(nr.Ls),
+                          ncols * op->n, static_cast<int>(nr.Ls), false, 1.0, s),
+          "slab near dft");
+    int nw_, kc_, ring_;
+    size_t smem_;
+    const long long qs = nr.Ls * ncols;  // rhs stride (one right-hand side)
+    if (mode_mma_shape(op->n, op->near_nimg, &nw_, &kc_, &ring_, &smem_))
+      check(launch_mode_mma(sp->shat, sp->items, sp->n_items, op->perm, nr.work, nr.recv, op->n, 0, sp->n_items, qs, 1,
+                            op->near_nimg, s),
+            "slab near mode product");
+    else
+      check(launch_mode_gemv(sp->shat, sp->items, sp->n_items, op->perm, nr.work, nr.recv, op->n, 0, sp->n_items, qs,
+                             1, op->near_nimg, s),
+            "slab near mode product");
+    check(launch_dft_axis(nr.recv, nr.work, op->twn[ax], 1, static_cast<int>(nr.Ls), static_cast<int>(sp->Ms),
+                          ncols * op->n, static_cast<int>(nr.Ls), true, nscale, s),
+          "slab near inverse dft");
+    std::swap(nr.recv, nr.work);
+    op->launches += 3;
+  }
+
+  // ---- 4. backward exchange, unpack, inverse DFTs below the slab axis, L2P
+  {
+    const A2aPart parts[2] = {
+        {reinterpret_cast<const double*>(fr.recv), reinterpret_cast<double*>(fr.pack), fr.bsc.data(), fr.bsd.data(),
+         fr.brc.data(), fr.brd.data(), fr.ball.data()},
+        {reinterpret_cast<const double*>(nr.recv), reinterpret_cast<double*>(nr.pack), nr.bsc.data(), nr.bsd.data(),
+         nr.brc.data(), nr.brd.data(), nr.ball.data()}};
+    comm_alltoallv(sp->comm, parts, 2, s);
+  }
+  if (cells == 0) return;
+  const bool f_local = fr.cx > 1 || fr.cy > 1, n_local = nr.cx > 1 || nr.cy > 1;
+  scatter_rows(fr.pack, f_local ? sp->a : sp->loc, fr.idx, fr.n_idx, fr.E, s);
+  if (f_local) local_inverse(op, sp, fr, sp->a, sp->loc, op->tw, s);
+  scatter_rows(nr.pack, n_local ? sp->a : y, nr.idx, nr.n_idx, nr.E, s);
+  if (n_local) local_inverse(op, sp, nr, sp->a, y, op->twn, s);
+  check(launch_l2p_add(op->u0, sp->loc, y, op->n, op->b, static_cast<int>(cells), cells * op->n, 1, s), "slab l2p");
+  op->launches += 3;
+}
+
+}  // namespace
+
+namespace fpbem_cu {
+void slab_apply(fpbem_cu_op* op, const c64* x, c64* y) { apply_slab(op, x, y); }
+fpbem_cu_comm* slab_comm(const fpbem_cu_op* op) { return op->slab ? op->slab->comm : nullptr; }
+void slab_range(const fpbem_cu_op* op, int r, long long* lo, long long* hi, long long* per_rank_rows) {
+  const SlabPlan* sp = op->slab;
+  const long long row = sp->Cm * op->n;
+  *lo = sp->zlo[r] * row;
+  *hi = sp->zlo[r + 1] * row;
+  *per_rank_rows = (sp->Ms + sp->P - 1) / sp->P * row;
+}
+}  // namespace fpbem_cu
+
+extern "C" {
+
+int fpbem_cu_fmm_set_slabs(fpbem_cu_op* op, fpbem_cu_comm* comm) {
+  return guard([&] {
+    if (!op) fail(FPBEM_CU_EINVAL, "set_slabs: null op");
+    check(cudaSetDevice(op->device), "set device");
+    check(cudaStreamSynchronize(op->stream), "sync");
+    slab_destroy(op);
+    try {
+      build_plan(op, comm);
+    } catch (...) {
+      slab_destroy(op);
+      throw;
+    }
+  });
+}
+
+int fpbem_cu_fmm_slab_rows(const fpbem_cu_op* op, long long* lo, long long* hi) {
+  return guard([&] {
+    if (!op || !lo || !hi) fail(FPBEM_CU_EINVAL, "slab_rows: null argument");
+    if (!op->slab) fail(FPBEM_CU_EINVAL, "slab_rows: no slab plan (fpbem_cu_fmm_set_slabs)");
+    const SlabPlan* sp = op->slab;
+    const long long row = sp->Cm * op->n;
+    *lo = sp->zlo[sp->rank] * row;
+    *hi = sp->zlo[sp->rank + 1] * row;
+  });
+}
+
+int fpbem_cu_fmm_apply_slab(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int ptr_kind) {
+  return guard([&] {
+    if (!op) fail(FPBEM_CU_EINVAL, "apply_slab: null op");
+    if (!op->slab) fail(FPBEM_CU_EINVAL, "apply_slab: no slab plan (fpbem_cu_fmm_set_slabs)");
+    check(cudaSetDevice(op->device), "set device");
+    SlabPlan* sp = op->slab;
+    const size_t rows = static_cast<size_t>(sp->ms * sp->Cm * op->n);
+    if (rows > 0 && (!x || !y)) fail(FPBEM_CU_EINVAL, "apply_slab: null vector");
+    cudaStream_t s = op->stream;
+    if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
+      apply_slab(op, reinterpret_cast<const c64*>(x), reinterpret_cast<c64*>(y));
+      return;
+    }
+    c64* dx = dalloc<c64>(rows, "slab x");
+    std::unique_ptr<c64, decltype(&cudaFree)> kx(dx, &cudaFree);
+    c64* dy = dalloc<c64>(rows, "slab y");
+    std::unique_ptr<c64, decltype(&cudaFree)> ky(dy, &cudaFree);
+    if (rows) check(cudaMemcpyAsync(dx, x, rows * sizeof(c64), cudaMemcpyHostToDevice, s), "slab x upload");
+    apply_slab(op, dx, dy);
+    if (rows) check(cudaMemcpyAsync(y, dy, rows * sizeof(c64), cudaMemcpyDeviceToHost, s), "slab y download");
+    check(cudaStreamSynchronize(s), "apply_slab");
+  });
+}
+
+}  // extern "C"

@@ -310,6 +310,40 @@ class FmmOperators:
         _raise(_native.cuda().fpbem_cu_fmm_set_comm(self._h, comm.handle if comm is not None else None))
         self._comm = comm
 
+    def set_slabs(self, comm=None) -> None:
+        """Slab-distributed product (lattice near field): this rank owns whole
+        planes of cells along the slab axis; matvec_slab maps x[lo:hi) to
+        (A x)[lo:hi) with one all-to-all per direction inside, and
+        gmres_distributed runs on the slabs. Collective over comm's ranks."""
+        _raise(_native.cuda().fpbem_cu_fmm_set_slabs(self._h, comm.handle if comm is not None else None))
+        self._slab_comm = comm
+
+    def slab_rows(self) -> tuple[int, int]:
+        lo, hi = C.c_longlong(), C.c_longlong()
+        _raise(_native.cuda().fpbem_cu_fmm_slab_rows(self._h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def matvec_slab(self, p):
+        """(A x)[lo:hi) from x[lo:hi) (numpy, or a CUDA complex128 tensor)."""
+        lo, hi = self.slab_rows()
+        lib = _native.cuda()
+        if _is_torch(p):
+            import torch
+
+            x = p.contiguous()
+            if x.numel() != hi - lo or x.dtype != torch.complex128:
+                raise ValueError("matvec_slab: expected this rank's rows as complex128")
+            y = torch.empty_like(x)
+            with self._ordered(x, y):
+                _raise(lib.fpbem_cu_fmm_apply_slab(self._h, x.data_ptr(), y.data_ptr(), PTR_DEVICE))
+            return y
+        x = np.ascontiguousarray(p, dtype=np.complex128)
+        if x.size != hi - lo:
+            raise ValueError("matvec_slab: expected this rank's rows")
+        y = np.empty_like(x)
+        _raise(lib.fpbem_cu_fmm_apply_slab(self._h, x.ctypes.data, y.ctypes.data, PTR_HOST))
+        return y
+
     def kernel_launches(self) -> int:
         return int(_native.cuda().fpbem_cu_kernel_launches(self._h))
 
