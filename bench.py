@@ -251,6 +251,7 @@ def run_ours(args):
     import torch
 
     from paper_2201_12050_b200 import FmmOperators, gmres
+    from paper_2201_12050_b200.fmm import gmres_distributed
 
     rank, world, local = dist_env()
     if world > 1:
@@ -283,17 +284,32 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     op.set_stream(stream.cuda_stream)
     comm = None
-    if world > 1 and args.parallelism == "pairs":
-        # near-field (offset, target) pairs split evenly across the GPUs,
-        # partial products all-reduced over NCCL inside every matvec (strong scaling)
+    slabs = False
+    if world == 1 and args.slabs:  # the slab product with one rank (tests the N>1 code path on one GPU)
+        op.set_slabs(None)
+        slabs = True
+    if world > 1 and args.parallelism in ("slabs", "pairs"):
         from paper_2201_12050_b200.fmm import Communicator
 
         comm = Communicator(dev.index)
-        op.set_comm(comm)
+        if args.parallelism == "slabs" and op.near_path()[0] == "lattice":
+            # SURVEY §8e cfg3 row / north_star: whole cell planes per GPU, the lattice DFTs
+            # below the slab axis on the rank's planes, one grouped NCCL all-to-all per
+            # direction, the DFTs along the slab axis + the rank's share of the near-field
+            # block spectrum and of Λ on its columns (strong scaling, no all-reduce of y)
+            op.set_slabs(comm)
+            slabs = True
+        else:
+            # direct near path: (offset, target) pairs split evenly across the GPUs,
+            # partial products all-reduced over NCCL inside every matvec (strong scaling)
+            op.set_comm(comm)
 
     rng = np.random.default_rng(args.config)  # the same input on every rank: the all-reduced product is A x
     xh = rng.uniform(-1, 1, data.N) + 1j * rng.uniform(-1, 1, data.N)
     x = torch.from_numpy(xh).to(dev)
+    lo_r, hi_r = op.slab_rows() if slabs else (0, data.N)
+    xs = x[lo_r:hi_r].contiguous()
+    apply = (lambda: op.matvec_slab(xs)) if slabs else (lambda: op.matvec(x))
     warmup = max(3, args.warmup)
 
     def barrier():
@@ -307,47 +323,59 @@ def run_ours(args):
     with sampler:
         # ---- warm-up, then the device-resident timed batches
         for _ in range(warmup):
-            op.matvec(x)
+            apply()
         torch.cuda.synchronize(dev)
         time.sleep(0.25)  # let the sampler start
         launches0 = op.kernel_launches()
-        trials_ms = timed_batches(lambda: op.matvec(x), args.steps, args.trials, stream, barrier)
+        trials_ms = timed_batches(apply, args.steps, args.trials, stream, barrier)
         launches = (op.kernel_launches() - launches0) // args.trials
 
         # ---- per-stage event timing (same stream); serial: the far field on the main stream
         op.enable_stage_timing(True)
         for _ in range(args.steps):
-            op.matvec(x)
+            apply()
         stages = op.stage_times()
-        op.enable_stage_timing(True, serial=True)
-        for _ in range(args.steps):
-            op.matvec(x)
+        if not slabs:
+            op.enable_stage_timing(True, serial=True)
+            for _ in range(args.steps):
+                apply()
         stages_serial = op.stage_times()
         op.enable_stage_timing(False)
 
-        # ---- end-to-end through the C-ABI with pinned host buffers
-        xp = torch.empty(data.N, dtype=torch.complex128, pin_memory=True)
-        xp.copy_(torch.from_numpy(xh))
-        yp = torch.empty(data.N, dtype=torch.complex128, pin_memory=True)  # empty_like would not pin
+        # ---- end-to-end through the C-ABI with pinned host buffers (this rank's rows)
+        n_loc = hi_r - lo_r
+        xp = torch.empty(n_loc, dtype=torch.complex128, pin_memory=True)
+        xp.copy_(torch.from_numpy(xh[lo_r:hi_r]))
+        yp = torch.empty(n_loc, dtype=torch.complex128, pin_memory=True)  # empty_like would not pin
         xpn, ypn = xp.numpy(), yp.numpy()
-        op.matvec(xpn)
+
+        def host_apply():
+            if slabs:
+                rc = lib.fpbem_cu_fmm_apply_slab(op.handle, xpn.ctypes.data, ypn.ctypes.data, 0)
+            else:
+                rc = lib.fpbem_cu_fmm_apply(op.handle, xpn.ctypes.data, ypn.ctypes.data, 1, 0)
+            if rc:
+                raise RuntimeError(lib.fpbem_cu_last_error().decode())
+
+        host_apply()
         e2e_trials = []
         for _ in range(args.trials):
             barrier()
             t = time.perf_counter()
             for _ in range(args.steps):
-                rc = lib.fpbem_cu_fmm_apply(op.handle, xpn.ctypes.data, ypn.ctypes.data, 1, 0)
-                if rc:
-                    raise RuntimeError(lib.fpbem_cu_last_error().decode())
+                host_apply()
             e2e_trials.append(time.perf_counter() - t)
             barrier()
 
         # ---- GMRES solve (metric's second half); warm solve first (workspace allocation)
         b = torch.from_numpy(sc.rhs(0)).to(dev)
-        gmres(op, b, tol=1e-6, restart=50, max_iter=min(5, args.gmres_max_iter))
+        solve = (lambda mi: gmres_distributed(op, b, tol=1e-6, restart=50, max_iter=mi)) if slabs else \
+            (lambda mi: gmres(op, b, tol=1e-6, restart=50, max_iter=mi))
+        solve(min(5, args.gmres_max_iter))
         torch.cuda.synchronize(dev)
+        barrier()
         t = time.perf_counter()
-        rep = gmres(op, b, tol=1e-6, restart=50, max_iter=args.gmres_max_iter)
+        rep = solve(args.gmres_max_iter)
         torch.cuda.synchronize(dev)
         gmres_s = time.perf_counter() - t
     clocks = sampler.summary()
@@ -392,6 +420,9 @@ def run_ours(args):
     if path == "lattice":
         q_near = int(np.prod(lat_sizes))
         lo, hi, far_pairs = op.partition()  # stored blocks of this rank
+        if slabs:  # this rank's stored blocks and the near-field modes of its columns
+            si = op.slab_info()
+            lo, hi, q_near = 0, si["near_blocks"], si["near_modes"]
         mode_bytes = 16.0 * data.n_dof ** 2 * (hi - lo) + 2 * 16.0 * data.n_dof * q_near
         mode_ms = per(stages, "near_mode_product")
         peak, peak_src = hbm_peak()
@@ -412,6 +443,11 @@ def run_ours(args):
                     "peak": peak, "unit": "TFLOP/s", "peak_source": peak_src, "flops_per_launch": flops,
                     "launch_ms": gemm_ms,
                     "algorithmic_bytes": 16.0 * data.n_near * data.n_dof ** 2 + 2 * 16.0 * data.N}
+    if slabs:  # the slab product's stage timing: [near_gemm] = the two exchanges, [total] = the product
+        roofline.pop("near_stage_ms", None)
+        roofline.pop("near_stage_share_of_step", None)
+        roofline["exchange_ms"] = gemm_ms
+        roofline["exchange_share_of_step"] = gemm_ms / per(stages, "total")
     roofline["frac"] = roofline["achieved"] / peak
     if traffic and traffic.get("config") != args.config:
         traffic = None  # the committed ncu capture is of another workload
@@ -423,7 +459,7 @@ def run_ours(args):
     b = data.n_coef
     q = int(np.prod(fsz))
     n_cells = int(np.prod(data.counts))
-    m2l_ms = per(stages_serial, "m2l")
+    m2l_ms = per(stages_serial, "m2l") if not slabs else float("nan")
     lam_full = 16.0 * q * b * b
     lam_read = lam_full / 2 if paired else lam_full
     io = 2 * 16.0 * b * n_cells
@@ -456,7 +492,11 @@ def run_ours(args):
                 "near_offsets": data.n_near, "far_offsets": data.n_far, "n_t": 4, "nrhs": 1,
                 "near_path": path, "near_lattice": list(lat_sizes), "near_modes_per_block": modes_per_block,
                 "near_symmetries": [g for g in range(1, 8) if sym_mask >> g & 1], "near_symmetry_deviation": sym_dev,
-                "parallelism": (f"near-field {'modes' if path == 'lattice' else 'pairs'} split over {world} GPUs "
+                "parallelism": (f"slabs x{world}: whole cell planes per GPU along axis {si['axis']} (rank 0: "
+                                f"{si['planes']} planes, {si['near_blocks']} stored near-field blocks, {si['far_modes']} "
+                                "far modes); one grouped NCCL send/recv all-to-all per direction per product; "
+                                "distributed GMRES on the slabs" if slabs else
+                                f"near-field {'modes' if path == 'lattice' else 'pairs'} split over {world} GPUs "
                                 f"(rank 0 {hi - lo if path == 'lattice' else n_pairs}, {far_pairs:.0f} fewer for its "
                                 "far field) + NCCL all-reduce of y" if strong
                                 else f"replicas x{world}" if world > 1 else "single GPU"),
@@ -476,7 +516,7 @@ def run_ours(args):
             "stages_serial_ms": {k: (per(stages_serial, k) if k != "applies" else v)
                                  for k, v in stages_serial.items()},
             "roofline": roofline,
-            "roofline_m2l": m2l_roof,
+            "roofline_m2l": m2l_roof if not slabs else None,
             "e2e": {"value": units * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": 16 * data.N, "d2h_bytes_per_step": 16 * data.N,
                     "trials_s": e2e_trials, "fraction_of_device_resident": (units * args.steps / e2e_s) / value},
@@ -511,8 +551,10 @@ def main():
     ap.add_argument("--gmres-max-iter", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nosym", action="store_true", help="skip the no-symmetry timing")
-    ap.add_argument("--parallelism", choices=["pairs", "replicas"], default="pairs",
-                    help="N>1: split the near-field pairs (NCCL all-reduce) or run independent replicas")
+    ap.add_argument("--parallelism", choices=["slabs", "pairs", "replicas"], default="slabs",
+                    help="N>1: cell slabs with NCCL all-to-all transposes (lattice near field; the direct path "
+                         "falls back to pairs), near-field pairs (NCCL all-reduce of y) or independent replicas")
+    ap.add_argument("--slabs", action="store_true", help="N=1: run the slab-distributed product with one rank")
     args = ap.parse_args()
     if args.impl == "reference":
         # bounded CPU sample: each step is a full CPU matvec

@@ -254,6 +254,9 @@ int fpbem_cu_stage_times(fpbem_cu_op* op, double* ms_out);
 int fpbem_cu_fmm_set_slabs(fpbem_cu_op* op, fpbem_cu_comm* comm);
 int fpbem_cu_fmm_slab_rows(const fpbem_cu_op* op, long long* lo, long long* hi);
 int fpbem_cu_fmm_apply_slab(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int ptr_kind);
+/* The plan of this rank: info[0..7] = rank, ranks, slab axis, planes, stored
+ * near-field blocks, near-field modes, far-field (Λ) modes, fused z kernel. */
+int fpbem_cu_fmm_slab_info(const fpbem_cu_op* op, long long info[8]);
 
 /* Number of CUDA kernels this handle launched since creation. */
 long long fpbem_cu_kernel_launches(const fpbem_cu_op* op);
@@ -281,6 +284,17 @@ int fpbem_cu_fmm_set_comm(fpbem_cu_op* op, fpbem_cu_comm* comm);
 typedef int (*fpbem_cu_allreduce_fn)(void* ctx, double* host_buf, size_t count);
 int fpbem_cu_comm_from_callback(fpbem_cu_allreduce_fn allreduce_sum, void* ctx, int nranks, int rank,
                                 int device, fpbem_cu_comm** out);
+
+/* A simulated communicator: rank `rank` of `nranks`, alone on `device`. Every
+ * collective moves only this rank's own block (device to device) and counts
+ * the bytes the real collective would send from this rank (ring all-reduce:
+ * 2 (P-1)/P of the buffer; reduce-scatter / all-gather: (P-1) slabs;
+ * all-to-all: the blocks addressed to other ranks). Results are partial, so
+ * it is for timing one rank's share of a multi-GPU product or solve on one
+ * GPU (tools/model_scaling.py), never for answers. comm_traffic reads (and
+ * with reset != 0 clears) the counters; it fails on a real communicator. */
+int fpbem_cu_comm_simulated(int nranks, int rank, int device, fpbem_cu_comm** out);
+int fpbem_cu_comm_traffic(fpbem_cu_comm* comm, unsigned long long* bytes_sent, long long* collectives, int reset);
 
 /* Distributed restarted GMRES: the Krylov basis, x and
  * the residual are split over the ranks of the attached communicator in

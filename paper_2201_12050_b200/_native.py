@@ -88,9 +88,9 @@ CUDA_SYMBOLS = (
     "fpbem_cu_fmm_create", "fpbem_cu_fmm_destroy", "fpbem_cu_fmm_apply", "fpbem_cu_gmres",
     "fpbem_cu_gmres_fn", "fpbem_cu_fmm_bytes", "fpbem_cu_fmm_near_path", "fpbem_cu_spectrum", "fpbem_cu_set_stream",
     "fpbem_cu_get_stream", "fpbem_cu_far_info", "fpbem_cu_fmm_set_slabs", "fpbem_cu_fmm_slab_rows",
-    "fpbem_cu_fmm_apply_slab",    "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
+    "fpbem_cu_fmm_apply_slab", "fpbem_cu_fmm_slab_info",    "fpbem_cu_enable_stage_timing", "fpbem_cu_stage_times", "fpbem_cu_kernel_launches",
     "fpbem_cu_comm_unique_id", "fpbem_cu_comm_init", "fpbem_cu_comm_destroy", "fpbem_cu_fmm_set_comm",
-    "fpbem_cu_comm_from_callback", "fpbem_cu_gmres_dist", "fpbem_cu_gmres_dist_rows",
+    "fpbem_cu_comm_from_callback", "fpbem_cu_comm_simulated", "fpbem_cu_comm_traffic", "fpbem_cu_gmres_dist", "fpbem_cu_gmres_dist_rows",
     "fpbem_cu_fmm_set_partition", "fpbem_cu_fmm_partition", "fpbem_cu_fmm_far_pairs", "fpbem_cu_partition_pairs", "fpbem_cu_assemble_near", "fpbem_cu_assemble_hat",
     "fpbem_cu_m2l_bank", "fpbem_cu_evaluate_field", "fpbem_cu_last_error", "fpbem_cu_version",
 )
@@ -123,6 +123,7 @@ def cuda() -> C.CDLL:
             "fpbem_cu_fmm_set_slabs": (C.c_int, [vp, vp]),
             "fpbem_cu_fmm_slab_rows": (C.c_int, [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
             "fpbem_cu_fmm_apply_slab": (C.c_int, [vp, vp, vp, C.c_int]),
+            "fpbem_cu_fmm_slab_info": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
             "fpbem_cu_enable_stage_timing": (C.c_int, [vp, C.c_int]),
             "fpbem_cu_stage_times": (C.c_int, [vp, c_double_p]),
             "fpbem_cu_kernel_launches": (C.c_longlong, [vp]),
@@ -131,6 +132,8 @@ def cuda() -> C.CDLL:
             "fpbem_cu_comm_destroy": (None, [vp]),
             "fpbem_cu_fmm_set_comm": (C.c_int, [vp, vp]),
             "fpbem_cu_comm_from_callback": (C.c_int, [ALLREDUCE_FN, vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+            "fpbem_cu_comm_simulated": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+            "fpbem_cu_comm_traffic": (C.c_int, [vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_longlong), C.c_int]),
             "fpbem_cu_gmres_dist": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.c_int, c_int_p, c_int_p,
                                               c_double_p, C.c_int, c_int_p]),
             "fpbem_cu_gmres_dist_rows": (C.c_int, [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),

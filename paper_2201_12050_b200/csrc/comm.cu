@@ -49,6 +49,11 @@ namespace fpbem_cu {
 // staged paths are exercised on one GPU); no communicator = this rank alone.
 void comm_allreduce(fpbem_cu_comm* c, double* buf, size_t count, cudaStream_t s) {
   if (!c || count == 0) return;
+  if (c->sim) {  // a ring all-reduce sends 2 (P-1)/P of the buffer per rank
+    c->sim_bytes += 2ull * (c->nranks - 1) * count * sizeof(double) / c->nranks;
+    c->sim_calls++;
+    return;
+  }
   if (!c->cb) {
     nccl_rc(c->allreduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, s), "ncclAllReduce");
     return;
@@ -70,6 +75,14 @@ void comm_reduce_scatter(fpbem_cu_comm* c, double* full, double* mine, size_t pe
       check(cudaMemcpyAsync(mine, full, per_rank * sizeof(double), cudaMemcpyDeviceToDevice, s), "slab copy");
     return;
   }
+  if (c->sim) {
+    c->sim_bytes += static_cast<unsigned long long>(c->nranks - 1) * per_rank * sizeof(double);
+    c->sim_calls++;
+    if (mine != full + r * per_rank)
+      check(cudaMemcpyAsync(mine, full + r * per_rank, per_rank * sizeof(double), cudaMemcpyDeviceToDevice, s),
+            "slab copy");
+    return;
+  }
   if (!c->cb) {
     nccl_rc(c->reduce_scatter(full, mine, per_rank, kNcclFloat64, kNcclSum, c->comm, s), "ncclReduceScatter");
     return;
@@ -89,6 +102,14 @@ void comm_allgather(fpbem_cu_comm* c, const double* mine, double* full, size_t p
   if (!c) {
     if (mine != full)
       check(cudaMemcpyAsync(full, mine, per_rank * sizeof(double), cudaMemcpyDeviceToDevice, s), "slab copy");
+    return;
+  }
+  if (c->sim) {
+    c->sim_bytes += static_cast<unsigned long long>(c->nranks - 1) * per_rank * sizeof(double);
+    c->sim_calls++;
+    if (full + c->rank * per_rank != mine)
+      check(cudaMemcpyAsync(full + c->rank * per_rank, mine, per_rank * sizeof(double), cudaMemcpyDeviceToDevice, s),
+            "slab copy");
     return;
   }
   if (!c->cb) {
@@ -119,6 +140,19 @@ void comm_alltoallv(fpbem_cu_comm* c, const A2aPart* parts, int n_parts, cudaStr
     return;
   }
   const int P = c->nranks, me = c->rank;
+  if (c->sim) {  // this rank's own block moves; the others are counted, not sent
+    for (int k = 0; k < n_parts; ++k) {
+      const A2aPart& p = parts[k];
+      for (int d = 0; d < P; ++d)
+        if (d != me) c->sim_bytes += p.scount[d] * sizeof(double);
+      if (p.scount[me])
+        check(cudaMemcpyAsync(p.recv + p.rdisp[me], p.send + p.sdisp[me], p.scount[me] * sizeof(double),
+                              cudaMemcpyDeviceToDevice, s),
+              "slab exchange (own block)");
+    }
+    c->sim_calls++;
+    return;
+  }
   if (!c->cb) {
     nccl_rc(c->group_start(), "ncclGroupStart");
     for (int k = 0; k < n_parts; ++k) {
@@ -223,6 +257,31 @@ int fpbem_cu_comm_from_callback(fpbem_cu_allreduce_fn allreduce_sum, void* ctx, 
     c->cb = allreduce_sum;
     c->cb_ctx = ctx;
     *out = c;
+  });
+}
+
+int fpbem_cu_comm_simulated(int nranks, int rank, int device, fpbem_cu_comm** out) {
+  return guard([&] {
+    if (!out || nranks < 1 || rank < 0 || rank >= nranks) fail(FPBEM_CU_EINVAL, "comm_simulated: bad arguments");
+    auto* c = new fpbem_cu_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    c->sim = true;
+    *out = c;
+  });
+}
+
+int fpbem_cu_comm_traffic(fpbem_cu_comm* comm, unsigned long long* bytes_sent, long long* collectives, int reset) {
+  return guard([&] {
+    if (!comm || !bytes_sent || !collectives) fail(FPBEM_CU_EINVAL, "comm_traffic: null argument");
+    if (!comm->sim) fail(FPBEM_CU_EINVAL, "comm_traffic: only a simulated communicator counts its traffic");
+    *bytes_sent = comm->sim_bytes;
+    *collectives = comm->sim_calls;
+    if (reset) {
+      comm->sim_bytes = 0;
+      comm->sim_calls = 0;
+    }
   });
 }
 

@@ -89,6 +89,12 @@ struct fpbem_cu_comm {
   void* cb_ctx = nullptr;
   double* stage = nullptr;  // pinned
   size_t stage_count = 0;
+  // simulated form (fpbem_cu_comm_simulated): rank `rank` of `nranks` alone on
+  // this device; collectives move only this rank's own blocks and count the
+  // bytes the real exchange would send (per-rank timing on one GPU)
+  bool sim = false;
+  unsigned long long sim_bytes = 0;
+  long long sim_calls = 0;
 };
 
 struct fpbem_cu_op {
@@ -226,6 +232,8 @@ struct A2aPart {
 // the parts' transfers in one NCCL group (send/recv), or host-staged one after another
 void comm_alltoallv(fpbem_cu_comm* c, const A2aPart* parts, int n_parts, cudaStream_t s);
 void slab_destroy(fpbem_cu_op* op);
+// event i of the handle's stage timing (no-op unless timing is enabled)
+void ev_record(fpbem_cu_op* op, int i, cudaStream_t st);
 // slab plan (slab.cu): y = (A x) on this rank's planes, device pointers, one right-hand side
 void slab_apply(fpbem_cu_op* op, const c64* x, c64* y);
 fpbem_cu_comm* slab_comm(const fpbem_cu_op* op);

@@ -397,6 +397,26 @@ void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c
   }
 }
 
+// stage timing of a slab product: [0] the two exchanges, [4] the whole
+// product, [5] the near-field mode product (events 7-8)
+void slab_timing(fpbem_cu_op* op, bool has_modes) {
+  if (!op->timing) return;
+  cudaStream_t s = op->stream;
+  ev_record(op, 6, s);
+  check(cudaEventSynchronize(op->ev[6]), "timing sync");
+  float a = 0.f, b = 0.f;
+  cudaEventElapsedTime(&a, op->ev[1], op->ev[2]);
+  cudaEventElapsedTime(&b, op->ev[3], op->ev[4]);
+  op->stage_ms[0] += a + b;
+  cudaEventElapsedTime(&a, op->ev[0], op->ev[6]);
+  op->stage_ms[4] += a;
+  if (has_modes) {
+    cudaEventElapsedTime(&a, op->ev[7], op->ev[8]);
+    op->stage_ms[5] += a;
+  }
+  op->applies++;
+}
+
 // y_loc = (A x)[this rank's planes] from x_loc = x[this rank's planes], one right-hand side
 void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
   SlabPlan* sp = op->slab;
@@ -406,6 +426,7 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
   SlabSide& fr = sp->fr;
   const long long ncols = static_cast<long long>(nr.cols[sp->rank].size());
   const long long fcols = static_cast<long long>(fr.cols[sp->rank].size());
+  ev_record(op, 0, s);
 
   // ---- 1. P2M, DFTs below the slab axis, pack (far, then near)
   if (cells > 0) {
@@ -430,7 +451,9 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
          fr.frc.data(), fr.frd.data(), fr.fall.data()},
         {reinterpret_cast<const double*>(nr.pack), reinterpret_cast<double*>(nr.recv), nr.fsc.data(), nr.fsd.data(),
          nr.frc.data(), nr.frd.data(), nr.fall.data()}};
+    ev_record(op, 1, s);
     comm_alltoallv(sp->comm, parts, 2, s);
+    ev_record(op, 2, s);
   }
 
   // ---- 3. along the slab axis on my columns: far (M2L) then near
@@ -462,6 +485,7 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
     int nw_, kc_, ring_;
     size_t smem_;
     const long long qs = nr.Ls * ncols;  // rhs stride (one right-hand side)
+    ev_record(op, 7, s);
     if (mode_mma_shape(op->n, op->near_nimg, &nw_, &kc_, &ring_, &smem_))
       check(launch_mode_mma(sp->shat, sp->items, sp->n_items, op->perm, nr.work, nr.recv, op->n, 0, sp->n_items, qs, 1,
                             op->near_nimg, s),
@@ -470,6 +494,7 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
       check(launch_mode_gemv(sp->shat, sp->items, sp->n_items, op->perm, nr.work, nr.recv, op->n, 0, sp->n_items, qs,
                              1, op->near_nimg, s),
             "slab near mode product");
+    ev_record(op, 8, s);
     check(launch_dft_axis(nr.recv, nr.work, op->twn[ax], 1, static_cast<int>(nr.Ls), static_cast<int>(sp->Ms),
                           ncols * op->n, static_cast<int>(nr.Ls), true, nscale, s),
           "slab near inverse dft");
@@ -484,9 +509,14 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
          fr.brc.data(), fr.brd.data(), fr.ball.data()},
         {reinterpret_cast<const double*>(nr.recv), reinterpret_cast<double*>(nr.pack), nr.bsc.data(), nr.bsd.data(),
          nr.brc.data(), nr.brd.data(), nr.ball.data()}};
+    ev_record(op, 3, s);
     comm_alltoallv(sp->comm, parts, 2, s);
+    ev_record(op, 4, s);
   }
-  if (cells == 0) return;
+  if (cells == 0) {
+    slab_timing(op, ncols > 0);
+    return;
+  }
   const bool f_local = fr.cx > 1 || fr.cy > 1, n_local = nr.cx > 1 || nr.cy > 1;
   scatter_rows(fr.pack, f_local ? sp->a : sp->loc, fr.idx, fr.n_idx, fr.E, s);
   if (f_local) local_inverse(op, sp, fr, sp->a, sp->loc, op->tw, s);
@@ -494,6 +524,7 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
   if (n_local) local_inverse(op, sp, nr, sp->a, y, op->twn, s);
   check(launch_l2p_add(op->u0, sp->loc, y, op->n, op->b, static_cast<int>(cells), cells * op->n, 1, s), "slab l2p");
   op->launches += 3;
+  slab_timing(op, ncols > 0);
 }
 
 }  // namespace
@@ -535,6 +566,22 @@ int fpbem_cu_fmm_slab_rows(const fpbem_cu_op* op, long long* lo, long long* hi) 
     const long long row = sp->Cm * op->n;
     *lo = sp->zlo[sp->rank] * row;
     *hi = sp->zlo[sp->rank + 1] * row;
+  });
+}
+
+int fpbem_cu_fmm_slab_info(const fpbem_cu_op* op, long long info[8]) {
+  return guard([&] {
+    if (!op || !info) fail(FPBEM_CU_EINVAL, "slab_info: null argument");
+    if (!op->slab) fail(FPBEM_CU_EINVAL, "slab_info: no slab plan (fpbem_cu_fmm_set_slabs)");
+    const SlabPlan* sp = op->slab;
+    info[0] = sp->rank;
+    info[1] = sp->P;
+    info[2] = sp->axis;
+    info[3] = sp->ms;
+    info[4] = sp->n_items;
+    info[5] = static_cast<long long>(sp->nr.cols[sp->rank].size()) * sp->nr.Ls;  // near modes on this rank
+    info[6] = static_cast<long long>(sp->fr.cols[sp->rank].size()) * sp->fr.Ls;  // far modes on this rank
+    info[7] = sp->zfused ? 1 : 0;
   });
 }
 

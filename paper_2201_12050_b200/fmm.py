@@ -142,6 +142,24 @@ class HostCommunicator(Communicator):
         self.handle, self.rank, self.nranks = h, rank, world
 
 
+class SimulatedCommunicator(Communicator):
+    """Rank `rank` of `nranks` alone on one device (fpbem_cu_comm_simulated):
+    collectives move only this rank's own blocks and count the bytes the real
+    exchange would send. For timing one rank's share of a multi-GPU product on
+    one GPU (tools/model_scaling.py); its products are partial, never answers."""
+
+    def __init__(self, device: int, nranks: int, rank: int):
+        h = C.c_void_p()
+        _raise(_native.cuda().fpbem_cu_comm_simulated(nranks, rank, device, C.byref(h)))
+        self.handle, self.rank, self.nranks = h, rank, nranks
+
+    def traffic(self, reset: bool = False) -> tuple[int, int]:
+        """(bytes this rank would have sent, collectives) since the last reset."""
+        b, n = C.c_ulonglong(), C.c_longlong()
+        _raise(_native.cuda().fpbem_cu_comm_traffic(self.handle, C.byref(b), C.byref(n), int(reset)))
+        return int(b.value), int(n.value)
+
+
 @dataclass
 class SolveReport:
     """include/fpbem/solver.hpp:14-19"""
@@ -322,6 +340,13 @@ class FmmOperators:
         lo, hi = C.c_longlong(), C.c_longlong()
         _raise(_native.cuda().fpbem_cu_fmm_slab_rows(self._h, C.byref(lo), C.byref(hi)))
         return lo.value, hi.value
+
+    def slab_info(self) -> dict:
+        """This rank's slab plan: planes, stored near-field blocks, near and far modes."""
+        v = (C.c_longlong * 8)()
+        _raise(_native.cuda().fpbem_cu_fmm_slab_info(self._h, v))
+        keys = ("rank", "ranks", "axis", "planes", "near_blocks", "near_modes", "far_modes", "z_fused")
+        return {k: int(v[i]) for i, k in enumerate(keys)}
 
     def matvec_slab(self, p):
         """(A x)[lo:hi) from x[lo:hi) (numpy, or a CUDA complex128 tensor)."""
