@@ -27,6 +27,7 @@
 // so the plan needs no communication. Λ and the near-field block spectrum are
 // stored per rank only for its columns (sharded, 1/P of the HBM each).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -72,12 +73,22 @@ struct SlabPlan {
   c64* mom = nullptr;
   c64* loc = nullptr;
   std::vector<void*> owned;
+  // the product captured as one CUDA graph on hx -> hy: at a few planes
+  // per rank its ~20 small launches would otherwise leave the GPU waiting on
+  // the host's enqueue rate
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  long long graph_launches = 0;
+  // the graph's (and host-pointer products') slab vectors
+  c64* hx = nullptr;
+  c64* hy = nullptr;
 };
 
 namespace fpbem_cu {
 
 void slab_destroy(fpbem_cu_op* op) {
   if (!op || !op->slab) return;
+  if (op->slab->graph) cudaGraphExecDestroy(op->slab->graph);
   for (void* p : op->slab->owned) cudaFree(p);
   delete op->slab;
   op->slab = nullptr;
@@ -527,10 +538,62 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
   slab_timing(op, ncols > 0);
 }
 
+// apply_slab through a CUDA graph when it can be captured: not under stage
+// timing (event syncs), not with a host-staged communicator (stream syncs
+// around the caller's all-reduce); FPBEM_SLAB_GRAPH=0 disables it. The graph
+// runs on the plan's own slab buffers (hx -> hy), captured once per stream; a
+// caller's vectors are copied in and out around it (device to device, one
+// slab each), so the Krylov solver's changing basis columns reuse it
+void apply_slab_graph(fpbem_cu_op* op, const c64* x, c64* y) {
+  static const bool env = [] {
+    const char* v = std::getenv("FPBEM_SLAB_GRAPH");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  SlabPlan* sp = op->slab;
+  cudaStream_t s = op->stream;
+  if (!env || op->timing || (sp->comm && sp->comm->cb) || s == nullptr) {
+    apply_slab(op, x, y);
+    return;
+  }
+  const size_t rows = static_cast<size_t>(sp->ms * sp->Cm * op->n);
+  if (!sp->hx) {
+    sp->hx = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab x");
+    sp->hy = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab y");
+  }
+  if (!sp->graph || sp->graph_stream != s) {
+    if (sp->graph) {
+      check(cudaGraphExecDestroy(sp->graph), "slab graph");
+      sp->graph = nullptr;
+    }
+    const long long l0 = op->launches;
+    cudaGraph_t g = nullptr;
+    check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "slab graph capture");
+    try {
+      apply_slab(op, sp->hx, sp->hy);
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    check(cudaStreamEndCapture(s, &g), "slab graph capture");
+    std::unique_ptr<CUgraph_st, decltype(&cudaGraphDestroy)> keep(g, &cudaGraphDestroy);
+    check(cudaGraphInstantiate(&sp->graph, g, 0), "slab graph instantiate");
+    sp->graph_stream = s;
+    sp->graph_launches = op->launches - l0;
+    op->launches = l0;
+  }
+  if (rows && x != sp->hx)
+    check(cudaMemcpyAsync(sp->hx, x, rows * sizeof(c64), cudaMemcpyDeviceToDevice, s), "slab x in");
+  check(cudaGraphLaunch(sp->graph, s), "slab graph launch");
+  if (rows && y != sp->hy)
+    check(cudaMemcpyAsync(y, sp->hy, rows * sizeof(c64), cudaMemcpyDeviceToDevice, s), "slab y out");
+  op->launches += sp->graph_launches;
+}
+
 }  // namespace
 
 namespace fpbem_cu {
-void slab_apply(fpbem_cu_op* op, const c64* x, c64* y) { apply_slab(op, x, y); }
+void slab_apply(fpbem_cu_op* op, const c64* x, c64* y) { apply_slab_graph(op, x, y); }
 fpbem_cu_comm* slab_comm(const fpbem_cu_op* op) { return op->slab ? op->slab->comm : nullptr; }
 void slab_range(const fpbem_cu_op* op, int r, long long* lo, long long* hi, long long* per_rank_rows) {
   const SlabPlan* sp = op->slab;
@@ -595,16 +658,17 @@ int fpbem_cu_fmm_apply_slab(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, i
     if (rows > 0 && (!x || !y)) fail(FPBEM_CU_EINVAL, "apply_slab: null vector");
     cudaStream_t s = op->stream;
     if (ptr_kind == FPBEM_CU_PTR_DEVICE) {
-      apply_slab(op, reinterpret_cast<const c64*>(x), reinterpret_cast<c64*>(y));
+      apply_slab_graph(op, reinterpret_cast<const c64*>(x), reinterpret_cast<c64*>(y));
       return;
     }
-    c64* dx = dalloc<c64>(rows, "slab x");
-    std::unique_ptr<c64, decltype(&cudaFree)> kx(dx, &cudaFree);
-    c64* dy = dalloc<c64>(rows, "slab y");
-    std::unique_ptr<c64, decltype(&cudaFree)> ky(dy, &cudaFree);
-    if (rows) check(cudaMemcpyAsync(dx, x, rows * sizeof(c64), cudaMemcpyHostToDevice, s), "slab x upload");
-    apply_slab(op, dx, dy);
-    if (rows) check(cudaMemcpyAsync(y, dy, rows * sizeof(c64), cudaMemcpyDeviceToHost, s), "slab y download");
+    if (!sp->hx) {
+      sp->hx = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab x");
+      sp->hy = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab y");
+    }
+    // pinned host pointers overlap nothing here (one slab in, one out), so no chunking
+    if (rows) check(cudaMemcpyAsync(sp->hx, x, rows * sizeof(c64), cudaMemcpyHostToDevice, s), "slab x upload");
+    apply_slab_graph(op, sp->hx, sp->hy);
+    if (rows) check(cudaMemcpyAsync(y, sp->hy, rows * sizeof(c64), cudaMemcpyDeviceToHost, s), "slab y download");
     check(cudaStreamSynchronize(s), "apply_slab");
   });
 }
