@@ -327,6 +327,7 @@ void build_items(fpbem_cu_op* op, const int Ln[3]) {
 // inverse pass when that pass is an x-axis DMMA DFT; returns whether it was.
 bool near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_t s, const c64* fuse_loc = nullptr,
                     cudaEvent_t join = nullptr) {
+  Nvtx range("near field (lattice convolution)");
   const long long n = op->n, r = nrhs;
   const int Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const int Lx = op->Ln[0], Ly = op->Ln[1], Lz = op->Ln[2];
@@ -616,6 +617,7 @@ bool cellwise_on() {
 // Far field of one product: P2M (events 2-3) and M2L into op->loc (events 3-4);
 // the Hankel image pair adds the K_hat term (src/fmm.cpp:256-263)
 void far_field(fpbem_cu_op* op, const c64* x, int nrhs, cudaStream_t a) {
+  Nvtx range("far field (P2M + M2L)");
   ev_record(op, 2, a);
   if (cellwise_on() && cellwise_supported(op->b, op->n))  // M_c = V0 p_c: V0[m][k] = v0t[m n + k]
     check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, op->N, op->n, op->mom, op->b,
@@ -691,6 +693,7 @@ double calibrate_far_pairs(fpbem_cu_op* op) {
 // its own near-field offsets; rank 0 also adds the far field (P2M, M2L,
 // L2P); with a communicator the partial products are all-reduced.
 void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
+  Nvtx range("fpbem apply (FmmOperators::matvec)");
   cudaStream_t s = op->stream;
   // FPBEM_SERIAL=1 runs P2M + M2L on the main stream (exact per-stage timing)
   static const bool serial = [] {

@@ -58,6 +58,7 @@ using ApplyDev = std::function<void(const c64*, c64*)>;
 
 GmresOut gmres_one(fpbem_cu_op* op, const ApplyDev& apply, const c64* b_dev, c64* x_dev, double tol, int restart,
                    int max_iter) {
+  Nvtx range("gmres (solver::gmres, one right-hand side)");
   using cd = std::complex<double>;
   cudaStream_t s = op->stream;
   const long long n = op->N;
@@ -274,6 +275,7 @@ struct BatchOut {
 };
 
 BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double tol, int restart, int max_iter) {
+  Nvtx range("gmres (lockstep batch)");
   using cd = std::complex<double>;
   cudaStream_t s = op->stream;
   const long long n = op->N;

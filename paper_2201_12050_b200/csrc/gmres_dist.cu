@@ -66,6 +66,7 @@ struct DistOut {
 
 DistOut gmres_dist(fpbem_cu_op* op, const c64* b, bool b_host, c64* x, bool x_host, double tol, int restart,
                    int max_iter) {
+  Nvtx range("gmres (distributed, classical Gram-Schmidt)");
   using cd = std::complex<double>;
   cudaStream_t s = op->stream;
   fpbem_cu_comm* comm = dist_comm(op);

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3: no-ops unless a profiler injects itself
 
 #include <functional>
 #include <string>
@@ -17,6 +18,14 @@
 namespace fpbem_cu {
 
 inline thread_local std::string g_err;  // fpbem_cu_last_error
+
+// host-side stage range on the NVTX timeline (nsys / ncu --nvtx), scoped
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 struct Fail {
   int code;

@@ -11,7 +11,8 @@
 // streaming kernel over [outer][axis][inner][fields] with the fields
 // (nrhs x b, contiguous) innermost, so every warp access is coalesced. The
 // per-mode product streams Λ once per apply (the HBM-bound part).
-// P2M (src/fmm.cpp:256-259) runs as a job list of the DMMA block GEMM (near_field.cu).
+// P2M (src/fmm.cpp:256-259) runs as the per-cell DMMA GEMM with V0 resident in
+// shared memory (cellwise_gemm_kernel, cellwise.cu), else p2m_kernel below.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>

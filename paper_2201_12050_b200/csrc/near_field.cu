@@ -340,7 +340,10 @@ template <int MT, int NW>
 __global__ void __launch_bounds__(32 * (NW + 2), 1)
 near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items, long long n_items,
                      const int* __restrict__ perm, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
-                     long long t_lo, long long t_hi, long long q_stride, int nrhs, int ncols, int KC, int ring) {
+                     long long t_lo, long long t_hi, long long q_stride, int nrhs, int ncols, int KC, int ring,
+                     int rsplit) {
+  // work unit u = (stored block t, row part h): rsplit parts of the block's row
+  // tiles per block, so that few blocks (a slab rank's share) still fill every SM
   extern __shared__ __align__(128) unsigned char mm_smem[];
   const int AP = n + 2, XP = n + 4;  // complex pitches: A columns, X columns
   c64* As = reinterpret_cast<c64*>(mm_smem);
@@ -367,10 +370,18 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
   __syncthreads();
   const int stages = (n + KC - 1) / KC;  // per stored block
   const size_t nn = static_cast<size_t>(n) * n;
+  const long long u_lo = t_lo * rsplit, u_hi = t_hi * rsplit;
+  const int n_mt_all = n >> 3;
+  auto part_rows = [&](long long u, int* m0, int* m1) {  // row tiles [m0, m1) of unit u
+    const int h = static_cast<int>(u % rsplit);
+    *m0 = h * n_mt_all / rsplit;
+    *m1 = (h + 1) * n_mt_all / rsplit;
+  };
 
   if (warp == NW + 1) {  // ---- X producer: the blocks' columns, up to two blocks ahead of the consumers
     int it = 0;
-    for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x, ++it) {
+    for (long long u = u_lo + blockIdx.x; u < u_hi; u += gridDim.x, ++it) {
+      const long long t = u / rsplit;
       // X[c][k] = xh[r][q_img][P_g k] into X buffer it & 1, 16-byte cp.async per element
       const int xb = it & 1;
       if (it >= 2) mbar_wait(xempty0 + 8 * xb, ((it >> 1) - 1) & 1);
@@ -414,16 +425,19 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
       const unsigned long long pol = evict_first_policy();
       int slot = 0;
       unsigned ph = 0;
-      for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
-        const c64* blk = shat + static_cast<size_t>(t) * nn;
+      for (long long u = u_lo + blockIdx.x; u < u_hi; u += gridDim.x) {
+        int m0, m1;
+        part_rows(u, &m0, &m1);
+        const int rows = 8 * (m1 - m0);
+        const c64* blk = shat + static_cast<size_t>(u / rsplit) * nn + 8 * m0;
         for (int st = 0; st < stages; ++st) {
           mbar_wait(empty0 + 8 * slot, ph ^ 1);
           const int k0 = st * KC, kc = min(KC, n - k0);
-          mbar_arrive_expect_tx(full0 + 8 * slot, static_cast<unsigned>(kc * n * sizeof(c64)));
+          mbar_arrive_expect_tx(full0 + 8 * slot, static_cast<unsigned>(kc * rows * sizeof(c64)));
           const unsigned dst = smem_u32(As + static_cast<size_t>(slot) * KC * AP);
           for (int c = 0; c < kc; ++c)
             bulk_g2s_hint(dst + static_cast<unsigned>(c * AP * sizeof(c64)), blk + static_cast<size_t>(k0 + c) * n,
-                          static_cast<unsigned>(n * sizeof(c64)), full0 + 8 * slot, pol);
+                          static_cast<unsigned>(rows * sizeof(c64)), full0 + 8 * slot, pol);
           if (++slot == ring) {
             slot = 0;
             ph ^= 1;
@@ -436,11 +450,13 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
 
   // ---- consumers
   const int fr = lane >> 2, fk = lane & 3;
-  const int n_mt = n >> 3;
   int slot = 0;
   unsigned ph = 0;
   int it = 0;
-  for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x, ++it) {
+  for (long long u = u_lo + blockIdx.x; u < u_hi; u += gridDim.x, ++it) {
+    int m0, m1;
+    part_rows(u, &m0, &m1);
+    const int n_mt = m1 - m0;  // this unit's row tiles; the ring holds rows 8 m0 ..
     const int xb = it & 1;
     mbar_wait(xfull0 + 8 * xb, (it >> 1) & 1);
     const c64* xs = Xs + xb * 8 * XP + fr * XP + fk;
@@ -482,7 +498,7 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
     for (int mi = 0; mi < MT; ++mi) {
       const int mt = warp + mi * NW;
       if (mt >= n_mt) continue;
-      const int i = mt * 8 + fr;
+      const int i = (m0 + mt) * 8 + fr;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int c = 2 * fk + j;
@@ -650,10 +666,22 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   size_t smem;
   const int ncols = nrhs * nimg;
   if (!mode_mma_shape(n, ncols, &NW, &KC, &R, &smem)) return cudaErrorInvalidValue;
-  const int MT = (n / 8 + NW - 1) / NW;
+  // FPBEM_MMA_RSPLIT=2|4 splits each block's row tiles over that many CTAs (A/B for
+  // few blocks, e.g. a slab rank's share). Off by default: the per-block DMMA work
+  // bounds an SM, so a split only pays when the units fill whole waves, and cfg3's
+  // 8-rank share (99 blocks -> 198 units on 148 SMs) measured 46 -> 63 us
+  static const int rsplit_env = [] {
+    const char* v = std::getenv("FPBEM_MMA_RSPLIT");
+    const int r = v ? std::atoi(v) : 1;
+    return (r == 2 || r == 4) ? r : 1;
+  }();
+  const long long n_blk = t_hi - t_lo;
+  const int sms = device_sms();
+  const int rsplit = ((n / 8) / rsplit_env >= NW) ? rsplit_env : 1;
+  const int MT = ((n / 8 + rsplit - 1) / rsplit + NW - 1) / NW;
   static std::atomic<unsigned long long> raised[18];
   using K = void (*)(const c64*, const int*, long long, const int*, const c64*, c64*, int, long long, long long,
-                     long long, int, int, int, int);
+                     long long, int, int, int, int, int);
   static const K fns[18] = {near_mode_mma_kernel<1, 8>,  near_mode_mma_kernel<2, 8>,  near_mode_mma_kernel<3, 8>,
                             near_mode_mma_kernel<4, 8>,  near_mode_mma_kernel<5, 8>,  near_mode_mma_kernel<6, 8>,
                             near_mode_mma_kernel<7, 8>,  near_mode_mma_kernel<8, 8>,  near_mode_mma_kernel<1, 10>,
@@ -664,10 +692,10 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   const int which = (NW == 8 ? 0 : NW == 10 ? 8 : 16) + MT - 1;
   cudaError_t e = ensure_max_smem(raised[which], reinterpret_cast<const void*>(fns[which]), kMaxDynSmem);
   if (e != cudaSuccess) return e;
-  const long long blocks = t_hi - t_lo;
-  const int grid = static_cast<int>(std::min<long long>(blocks, device_sms()));
+  const long long units = n_blk * rsplit;
+  const int grid = static_cast<int>(std::min<long long>(units, sms));
   fns[which]<<<grid, 32 * (NW + 2), smem, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, t_hi, q_stride,
-                                                     nrhs, ncols, KC, R);
+                                                     nrhs, ncols, KC, R, rsplit);
   return cudaGetLastError();
 }
 

@@ -73,10 +73,8 @@ struct SlabPlan {
   c64* mom = nullptr;
   c64* loc = nullptr;
   std::vector<void*> owned;
-  // the product captured as one CUDA graph on hx -> hy: at a few planes
-  // per rank its ~20 small launches would otherwise leave the GPU waiting on
-  // the host's enqueue rate
-  cudaGraphExec_t graph = nullptr;
+  // the product's compute phases captured as CUDA graphs on hx -> hy (apply_slab_graph)
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};  // the three compute phases
   cudaStream_t graph_stream = nullptr;
   long long graph_launches = 0;
   // the graph's (and host-pointer products') slab vectors
@@ -88,7 +86,8 @@ namespace fpbem_cu {
 
 void slab_destroy(fpbem_cu_op* op) {
   if (!op || !op->slab) return;
-  if (op->slab->graph) cudaGraphExecDestroy(op->slab->graph);
+  for (auto g : op->slab->graph)
+    if (g) cudaGraphExecDestroy(g);
   for (void* p : op->slab->owned) cudaFree(p);
   delete op->slab;
   op->slab = nullptr;
@@ -138,9 +137,12 @@ void scatter_rows(const c64* src, c64* dst, const int* idx, long long rows, int 
 }
 
 template <typename T>
-T* palloc(SlabPlan* sp, size_t count, const char* what) {
+T* palloc(SlabPlan* sp, size_t count, const char* what, cudaStream_t s) {
   T* p = dalloc<T>(count, what);
   sp->owned.push_back(p);
+  // zeroed once, ordered on the plan's stream before any upload into it: blocks
+  // a simulated communicator does not deliver stay finite
+  check(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(T), s), what);
   return p;
 }
 
@@ -200,7 +202,7 @@ void build_side(SlabPlan* sp, SlabSide& sd, const std::vector<std::vector<int>>&
     for (long long z = 0; z < ms; ++z)
       for (int c : sd.cols[d]) idx.push_back(static_cast<int>(z * sd.C + c));
   sd.n_idx = static_cast<long long>(idx.size());
-  sd.idx = palloc<int>(sp, idx.size(), "slab pack order");
+  sd.idx = palloc<int>(sp, idx.size(), "slab pack order", s);
   h2d(sd.idx, idx.data(), idx.size() * sizeof(int), s, "slab pack order");
   const size_t E2 = 2 * static_cast<size_t>(sd.E);
   auto planes = [&](int r) { return static_cast<size_t>(sp->zlo[r + 1] - sp->zlo[r]); };
@@ -232,12 +234,13 @@ void build_side(SlabPlan* sp, SlabSide& sd, const std::vector<std::vector<int>>&
     }
   }
   const size_t rows_loc = static_cast<size_t>(std::max(sp->Ms, sd.Ls)) * mycols;
-  sd.pack = palloc<c64>(sp, static_cast<size_t>(ms * sd.C) * sd.E, "slab pack");
-  sd.recv = palloc<c64>(sp, rows_loc * sd.E, "slab columns");
-  sd.work = palloc<c64>(sp, rows_loc * sd.E, "slab column spectra");
+  sd.pack = palloc<c64>(sp, static_cast<size_t>(ms * sd.C) * sd.E, "slab pack", s);
+  sd.recv = palloc<c64>(sp, rows_loc * sd.E, "slab columns", s);
+  sd.work = palloc<c64>(sp, rows_loc * sd.E, "slab column spectra", s);
 }
 
 void build_plan(fpbem_cu_op* op, fpbem_cu_comm* comm) {
+  Nvtx range("slab plan");
   if (!op->near_fft) fail(FPBEM_CU_EINVAL, "set_slabs: needs the lattice near field (near_path = lattice)");
   if (op->mirrored_level >= 0) fail(FPBEM_CU_EINVAL, "set_slabs: not with a half-space image pair");
   auto* sp = new SlabPlan();
@@ -295,10 +298,10 @@ void build_plan(fpbem_cu_op* op, fpbem_cu_comm* comm) {
   sp->n_items = static_cast<long long>(mine.size());
   std::vector<int> items(iq);
   items.insert(items.end(), ig.begin(), ig.end());
-  sp->items = palloc<int>(sp, items.size(), "slab items");
+  sp->items = palloc<int>(sp, items.size(), "slab items", s);
   h2d(sp->items, items.data(), items.size() * sizeof(int), s, "slab items");
   const size_t nn = static_cast<size_t>(op->n) * op->n;
-  sp->shat = palloc<c64>(sp, mine.size() * nn, "slab near spectrum");
+  sp->shat = palloc<c64>(sp, mine.size() * nn, "slab near spectrum", s);
   for (size_t i = 0; i < mine.size(); ++i)
     check(cudaMemcpyAsync(sp->shat + i * nn, op->shat + static_cast<size_t>(mine[i]) * nn, nn * sizeof(c64),
                           cudaMemcpyDeviceToDevice, s),
@@ -322,7 +325,7 @@ void build_plan(fpbem_cu_op* op, fpbem_cu_comm* comm) {
   std::vector<int> lam_idx;  // local Λ rows (qs, local column) <- global q = qs C + col
   for (long long qs = 0; qs < fr.Ls; ++qs)
     for (int c : fcols) lam_idx.push_back(static_cast<int>(qs * fr.C + c));
-  sp->lambda = palloc<c64>(sp, lam_idx.size() * b2, "slab spectrum");
+  sp->lambda = palloc<c64>(sp, lam_idx.size() * b2, "slab spectrum", s);
   if (!lam_idx.empty()) {
     int* d_idx = dalloc<int>(lam_idx.size(), "slab spectrum rows");
     std::unique_ptr<int, decltype(&cudaFree)> keep(d_idx, &cudaFree);
@@ -347,25 +350,48 @@ void build_plan(fpbem_cu_op* op, fpbem_cu_comm* comm) {
         zi.push_back(make_int2(l, -1));
     }
     sp->n_zitems = static_cast<int>(zi.size());
-    sp->zitems = palloc<int2>(sp, zi.size(), "slab z items");
+    sp->zitems = palloc<int2>(sp, zi.size(), "slab z items", s);
     h2d(sp->zitems, zi.data(), zi.size() * sizeof(int2), s, "slab z items");
   }
   (void)fmy;
   const size_t plane_max = static_cast<size_t>(std::max(nr.C * nr.E, fr.C * fr.E));
-  sp->a = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes");
-  sp->b = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes");
-  sp->mom = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab moments");
-  sp->loc = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab locals");
+  sp->a = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes", s);
+  sp->b = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes", s);
+  sp->mom = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab moments", s);
+  sp->loc = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab locals", s);
   check(cudaStreamSynchronize(s), "slab plan");
 }
 
 // forward DFTs along the column axes (x, then y when the slab axis is z) of
 // this rank's planes: [ms][my][mx][E] -> [ms][cy][cx][E]; returns the result
+// both column axes in one plane kernel (x and y DFTs per (plane, field) in
+// shared memory) when the slab axis is z and the planes fit: half the launches
+// of the axis passes, which matters at a few planes per rank (FPBEM_SLAB_XY=0:
+// axis passes)
+bool slab_xy(const SlabPlan* sp, const SlabSide& sd) {
+  static const bool env = [] {
+    const char* v = std::getenv("FPBEM_SLAB_XY");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const int mx = static_cast<int>(sp->mx), my = static_cast<int>(sp->my);
+  const int cx = static_cast<int>(sd.cx), cy = static_cast<int>(sd.cy);
+  return env && sd.cx > 1 && sd.cy > 1 && sp->ms * sd.E <= 0x7fffffffLL &&
+         xy_plane_smem(mx, my, cx, cy, false) <= 200 * 1024 && xy_plane_smem(mx, my, cx, cy, true) <= 200 * 1024;
+}
+
 const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* const* tw, cudaStream_t s) {
   const c64* cur = in;
   c64* bufs[2] = {sp->a, sp->b};
   int which = 0;
   if (sp->ms == 0) return cur;
+  if (slab_xy(sp, sd)) {
+    check(launch_xy_plane(cur, bufs[0], tw[0], tw[1], static_cast<int>(sp->mx), static_cast<int>(sp->my),
+                          static_cast<int>(sd.cx), static_cast<int>(sd.cy), static_cast<int>(sp->ms), sd.E, false, 1.0,
+                          s),
+          "slab xy dft");
+    op->launches++;
+    return bufs[0];
+  }
   if (sd.cx > 1) {
     check(launch_dft_axis(cur, bufs[which], tw[0], sp->my * sp->ms, static_cast<int>(sp->mx), static_cast<int>(sd.cx),
                           sd.E, static_cast<int>(sd.cx), false, 1.0, s),
@@ -388,6 +414,14 @@ const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64*
 void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* out, c64* const* tw,
                    cudaStream_t s) {
   if (sp->ms == 0) return;
+  if (slab_xy(sp, sd)) {
+    check(launch_xy_plane(in, out, tw[0], tw[1], static_cast<int>(sp->mx), static_cast<int>(sp->my),
+                          static_cast<int>(sd.cx), static_cast<int>(sd.cy), static_cast<int>(sp->ms), sd.E, true, 1.0,
+                          s),
+          "slab inverse xy dft");
+    op->launches++;
+    return;
+  }
   const c64* cur = in;
   c64* tmp = in == sp->a ? sp->b : sp->a;
   const int passes = (sd.cy > 1) + (sd.cx > 1);
@@ -428,18 +462,13 @@ void slab_timing(fpbem_cu_op* op, bool has_modes) {
   op->applies++;
 }
 
-// y_loc = (A x)[this rank's planes] from x_loc = x[this rank's planes], one right-hand side
-void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
+// phase 0: P2M, DFTs below the slab axis on this rank's planes, pack (far, then near)
+void slab_phase0(fpbem_cu_op* op, const c64* x) {
   SlabPlan* sp = op->slab;
   cudaStream_t s = op->stream;
   const long long cells = sp->ms * sp->Cm;
   SlabSide& nr = sp->nr;
   SlabSide& fr = sp->fr;
-  const long long ncols = static_cast<long long>(nr.cols[sp->rank].size());
-  const long long fcols = static_cast<long long>(fr.cols[sp->rank].size());
-  ev_record(op, 0, s);
-
-  // ---- 1. P2M, DFTs below the slab axis, pack (far, then near)
   if (cells > 0) {
     if (cellwise_supported(op->b, op->n))
       check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, cells * op->n, op->n, sp->mom, op->b, op->b, 1, cells,
@@ -454,20 +483,36 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
   const c64* nplanes = local_forward(op, sp, nr, x, op->twn, s);
   gather_rows(nplanes, nr.pack, nr.idx, nr.n_idx, nr.E, s);
   op->launches += 2;
+}
 
-  // ---- 2. forward exchange: every plane of my columns
-  {
-    const A2aPart parts[2] = {
-        {reinterpret_cast<const double*>(fr.pack), reinterpret_cast<double*>(fr.recv), fr.fsc.data(), fr.fsd.data(),
-         fr.frc.data(), fr.frd.data(), fr.fall.data()},
-        {reinterpret_cast<const double*>(nr.pack), reinterpret_cast<double*>(nr.recv), nr.fsc.data(), nr.fsd.data(),
-         nr.frc.data(), nr.frd.data(), nr.fall.data()}};
-    ev_record(op, 1, s);
-    comm_alltoallv(sp->comm, parts, 2, s);
-    ev_record(op, 2, s);
-  }
+// forward exchange (pack -> recv: every plane of my columns) or backward
+// (work -> pack: my planes of every column), far and near in one group
+void slab_exchange(fpbem_cu_op* op, bool forward) {
+  SlabPlan* sp = op->slab;
+  SlabSide& nr = sp->nr;
+  SlabSide& fr = sp->fr;
+  auto part = [&](SlabSide& sd) -> A2aPart {
+    if (forward)
+      return {reinterpret_cast<const double*>(sd.pack), reinterpret_cast<double*>(sd.recv), sd.fsc.data(),
+              sd.fsd.data(), sd.frc.data(), sd.frd.data(), sd.fall.data()};
+    return {reinterpret_cast<const double*>(sd.work), reinterpret_cast<double*>(sd.pack), sd.bsc.data(), sd.bsd.data(),
+            sd.brc.data(), sd.brd.data(), sd.ball.data()};
+  };
+  const A2aPart parts[2] = {part(fr), part(nr)};
+  ev_record(op, forward ? 1 : 3, op->stream);
+  comm_alltoallv(sp->comm, parts, 2, op->stream);
+  ev_record(op, forward ? 2 : 4, op->stream);
+}
 
-  // ---- 3. along the slab axis on my columns: far (M2L) then near
+// phase 1: along the slab axis on my columns, recv -> work: far (M2L) then
+// near (DFT, block products, inverse DFT)
+void slab_phase1(fpbem_cu_op* op) {
+  SlabPlan* sp = op->slab;
+  cudaStream_t s = op->stream;
+  SlabSide& nr = sp->nr;
+  SlabSide& fr = sp->fr;
+  const long long ncols = static_cast<long long>(nr.cols[sp->rank].size());
+  const long long fcols = static_cast<long long>(fr.cols[sp->rank].size());
   const double fscale = 1.0 / static_cast<double>(op->q_total), nscale = 1.0 / static_cast<double>(op->qn);
   const int ax = sp->axis;
   if (fcols > 0) {
@@ -475,9 +520,8 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
       check(launch_m2l_zfused(fr.recv, fr.work, sp->lambda, op->tw[ax], static_cast<int>(sp->Ms),
                               static_cast<int>(fr.Ls), fcols, op->b, op->b, fscale, sp->zitems, sp->n_zitems, s),
             "slab m2l z-fused");
-      std::swap(fr.recv, fr.work);  // result in recv
       op->launches++;
-    } else {
+    } else {  // recv -> work -> recv -> work
       check(launch_dft_axis(fr.recv, fr.work, op->tw[ax], 1, static_cast<int>(sp->Ms), static_cast<int>(fr.Ls),
                             fcols * op->b, static_cast<int>(fr.Ls), false, 1.0, s),
             "slab m2l dft");
@@ -485,11 +529,10 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
       check(launch_dft_axis(fr.recv, fr.work, op->tw[ax], 1, static_cast<int>(fr.Ls), static_cast<int>(sp->Ms),
                             fcols * op->b, static_cast<int>(fr.Ls), true, fscale, s),
             "slab m2l inverse dft");
-      std::swap(fr.recv, fr.work);
       op->launches += 3;
     }
   }
-  if (ncols > 0) {
+  if (ncols > 0) {  // recv -> work -> recv -> work
     check(launch_dft_axis(nr.recv, nr.work, op->twn[ax], 1, static_cast<int>(sp->Ms), static_cast<int>(nr.Ls),
                           ncols * op->n, static_cast<int>(nr.Ls), false, 1.0, s),
           "slab near dft");
@@ -509,25 +552,18 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
     check(launch_dft_axis(nr.recv, nr.work, op->twn[ax], 1, static_cast<int>(nr.Ls), static_cast<int>(sp->Ms),
                           ncols * op->n, static_cast<int>(nr.Ls), true, nscale, s),
           "slab near inverse dft");
-    std::swap(nr.recv, nr.work);
     op->launches += 3;
   }
+}
 
-  // ---- 4. backward exchange, unpack, inverse DFTs below the slab axis, L2P
-  {
-    const A2aPart parts[2] = {
-        {reinterpret_cast<const double*>(fr.recv), reinterpret_cast<double*>(fr.pack), fr.bsc.data(), fr.bsd.data(),
-         fr.brc.data(), fr.brd.data(), fr.ball.data()},
-        {reinterpret_cast<const double*>(nr.recv), reinterpret_cast<double*>(nr.pack), nr.bsc.data(), nr.bsd.data(),
-         nr.brc.data(), nr.brd.data(), nr.ball.data()}};
-    ev_record(op, 3, s);
-    comm_alltoallv(sp->comm, parts, 2, s);
-    ev_record(op, 4, s);
-  }
-  if (cells == 0) {
-    slab_timing(op, ncols > 0);
-    return;
-  }
+// phase 2: unpack, the inverse DFTs below the slab axis on my planes, L2P
+void slab_phase2(fpbem_cu_op* op, c64* y) {
+  SlabPlan* sp = op->slab;
+  cudaStream_t s = op->stream;
+  const long long cells = sp->ms * sp->Cm;
+  if (cells == 0) return;
+  SlabSide& nr = sp->nr;
+  SlabSide& fr = sp->fr;
   const bool f_local = fr.cx > 1 || fr.cy > 1, n_local = nr.cx > 1 || nr.cy > 1;
   scatter_rows(fr.pack, f_local ? sp->a : sp->loc, fr.idx, fr.n_idx, fr.E, s);
   if (f_local) local_inverse(op, sp, fr, sp->a, sp->loc, op->tw, s);
@@ -535,15 +571,53 @@ void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
   if (n_local) local_inverse(op, sp, nr, sp->a, y, op->twn, s);
   check(launch_l2p_add(op->u0, sp->loc, y, op->n, op->b, static_cast<int>(cells), cells * op->n, 1, s), "slab l2p");
   op->launches += 3;
-  slab_timing(op, ncols > 0);
 }
 
-// apply_slab through a CUDA graph when it can be captured: not under stage
-// timing (event syncs), not with a host-staged communicator (stream syncs
-// around the caller's all-reduce); FPBEM_SLAB_GRAPH=0 disables it. The graph
-// runs on the plan's own slab buffers (hx -> hy), captured once per stream; a
-// caller's vectors are copied in and out around it (device to device, one
-// slab each), so the Krylov solver's changing basis columns reuse it
+// y_loc = (A x)[this rank's planes] from x_loc = x[this rank's planes], one right-hand side
+void apply_slab(fpbem_cu_op* op, const c64* x, c64* y) {
+  Nvtx range("slab product");
+  ev_record(op, 0, op->stream);
+  slab_phase0(op, x);
+  slab_exchange(op, true);
+  slab_phase1(op);
+  slab_exchange(op, false);
+  slab_phase2(op, y);
+  slab_timing(op, !op->slab->nr.cols[op->slab->rank].empty());
+}
+
+// capture one phase of the product (on the plan's slab vectors) as a graph
+cudaGraphExec_t capture_phase(fpbem_cu_op* op, int ph, long long* launches) {
+  SlabPlan* sp = op->slab;
+  cudaStream_t s = op->stream;
+  const long long l0 = op->launches;
+  cudaGraph_t g = nullptr;
+  check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "slab graph capture");
+  try {
+    if (ph == 0) slab_phase0(op, sp->hx);
+    if (ph == 1) slab_phase1(op);
+    if (ph == 2) slab_phase2(op, sp->hy);
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  check(cudaStreamEndCapture(s, &g), "slab graph capture");
+  std::unique_ptr<CUgraph_st, decltype(&cudaGraphDestroy)> keep(g, &cudaGraphDestroy);
+  cudaGraphExec_t exec = nullptr;
+  check(cudaGraphInstantiate(&exec, g, 0), "slab graph instantiate");
+  *launches = op->launches - l0;
+  op->launches = l0;
+  return exec;
+}
+
+// The product with each compute phase replayed as a CUDA graph: at a few planes
+// per rank its ~20 small launches would otherwise leave the GPU waiting on the
+// host's enqueue rate. The exchanges stay eager NCCL group calls between the
+// graphs. Not under stage timing (event syncs) or with a host-staged
+// communicator; FPBEM_SLAB_GRAPH=0 disables it. The graphs run on the plan's
+// own slab vectors (hx -> hy), captured once per stream; a caller's vectors
+// are copied in and out around them (device to device, one slab each), so the
+// Krylov solver's changing basis columns reuse them.
 void apply_slab_graph(fpbem_cu_op* op, const c64* x, c64* y) {
   static const bool env = [] {
     const char* v = std::getenv("FPBEM_SLAB_GRAPH");
@@ -555,36 +629,33 @@ void apply_slab_graph(fpbem_cu_op* op, const c64* x, c64* y) {
     apply_slab(op, x, y);
     return;
   }
+  Nvtx range("slab product (graphs)");
   const size_t rows = static_cast<size_t>(sp->ms * sp->Cm * op->n);
   if (!sp->hx) {
-    sp->hx = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab x");
-    sp->hy = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab y");
+    sp->hx = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab x", s);
+    sp->hy = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab y", s);
   }
-  if (!sp->graph || sp->graph_stream != s) {
-    if (sp->graph) {
-      check(cudaGraphExecDestroy(sp->graph), "slab graph");
-      sp->graph = nullptr;
+  if (!sp->graph[0] || sp->graph_stream != s) {
+    for (auto& g : sp->graph)
+      if (g) {
+        check(cudaGraphExecDestroy(g), "slab graph");
+        g = nullptr;
+      }
+    sp->graph_launches = 0;
+    for (int ph = 0; ph < 3; ++ph) {
+      long long l = 0;
+      sp->graph[ph] = capture_phase(op, ph, &l);
+      sp->graph_launches += l;
     }
-    const long long l0 = op->launches;
-    cudaGraph_t g = nullptr;
-    check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "slab graph capture");
-    try {
-      apply_slab(op, sp->hx, sp->hy);
-    } catch (...) {
-      cudaStreamEndCapture(s, &g);
-      if (g) cudaGraphDestroy(g);
-      throw;
-    }
-    check(cudaStreamEndCapture(s, &g), "slab graph capture");
-    std::unique_ptr<CUgraph_st, decltype(&cudaGraphDestroy)> keep(g, &cudaGraphDestroy);
-    check(cudaGraphInstantiate(&sp->graph, g, 0), "slab graph instantiate");
     sp->graph_stream = s;
-    sp->graph_launches = op->launches - l0;
-    op->launches = l0;
   }
   if (rows && x != sp->hx)
     check(cudaMemcpyAsync(sp->hx, x, rows * sizeof(c64), cudaMemcpyDeviceToDevice, s), "slab x in");
-  check(cudaGraphLaunch(sp->graph, s), "slab graph launch");
+  check(cudaGraphLaunch(sp->graph[0], s), "slab graph launch");
+  slab_exchange(op, true);
+  check(cudaGraphLaunch(sp->graph[1], s), "slab graph launch");
+  slab_exchange(op, false);
+  check(cudaGraphLaunch(sp->graph[2], s), "slab graph launch");
   if (rows && y != sp->hy)
     check(cudaMemcpyAsync(y, sp->hy, rows * sizeof(c64), cudaMemcpyDeviceToDevice, s), "slab y out");
   op->launches += sp->graph_launches;
@@ -662,8 +733,8 @@ int fpbem_cu_fmm_apply_slab(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, i
       return;
     }
     if (!sp->hx) {
-      sp->hx = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab x");
-      sp->hy = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab y");
+      sp->hx = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab x", s);
+      sp->hy = palloc<c64>(sp, std::max<size_t>(rows, 1), "slab y", s);
     }
     // pinned host pointers overlap nothing here (one slab in, one out), so no chunking
     if (rows) check(cudaMemcpyAsync(sp->hx, x, rows * sizeof(c64), cudaMemcpyHostToDevice, s), "slab x upload");
