@@ -297,6 +297,14 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
   __syncthreads();
   const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
   const long long n_et = (n_inner + 7) / 8, tiles = n_a * n_et;
+  // a lone last input (n_in = 4k + 1, e.g. the 17 modes of a 16-cell near lattice)
+  // or a lone last output (n_out = 8k + 1) would cost a whole k step / row block of
+  // DMMAs for one useful term: it is added with FMAs instead (xcol: the input
+  // j = n_in - 1 into every output of the lane; xrow: output n_out - 1 as a sum
+  // over the B fragments, reduced across the 4 lanes of a column)
+  const bool xcol = n_in % 4 == 1 && n_in > 4;
+  const bool xrow = !EPI && !xcol && n_out % 8 == 1 && n_out > 8;
+  const int KTd = xcol ? KT - 1 : KT, MTd = xrow ? MT - 1 : MT;
   const long long warp0 = blockIdx.x * static_cast<long long>(kDftMmaWarps) + (threadIdx.x >> 5);
   const long long nwarps = static_cast<long long>(gridDim.x) * kDftMmaWarps;
   // B fragments of the next tile are loaded before the current tile's MMAs
@@ -308,7 +316,7 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
 #pragma unroll
     for (int kt = 0; kt < KTM; ++kt) {
       const int j = kt * 4 + fk;
-      nb[kt] = (ok && kt < KT && j < n_in) ? src[static_cast<long long>(j) * n_inner] : cmk(0.0, 0.0);
+      nb[kt] = (ok && kt < KTd && j < n_in) ? src[static_cast<long long>(j) * n_inner] : cmk(0.0, 0.0);
     }
   };
   load(warp0);
@@ -319,8 +327,15 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
       br[kt] = nb[kt].x;
       bi[kt] = nb[kt].y;
     }
-    load(t + nwarps);
     const long long a = t / n_et, e0 = (t % n_et) * 8;
+    c64 xc[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};  // xcol: input n_in - 1 at the lane's two output columns
+    if (xcol)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long c = e0 + 2 * fk + h;
+        if (c < n_inner) xc[h] = in[(a * n_in + n_in - 1) * n_inner + c];
+      }
+    load(t + nwarps);
     c64* dst = out + a * n_out * n_inner;
     constexpr int KB = 8;  // L2P k steps (b <= 32)
     c64 ub[EPI ? KB : 1];  // U0 B fragments of this tile's 8 rows i
@@ -338,9 +353,9 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
                                                          : cmk(0.0, 0.0);
       }
     }
-    for (int mt = 0; mt < MT; mt += 2) {  // two row blocks per pass: independent accumulator chains
+    for (int mt = 0; mt < MTd; mt += 2) {  // two row blocks per pass: independent accumulator chains
       double t1[2][2] = {}, t2[2][2] = {}, t3[2][2] = {};
-      const bool two = mt + 1 < MT;
+      const bool two = mt + 1 < MTd;
       c64 la[EPI ? 2 : 1][EPI ? KB : 1];
       if constexpr (EPI) {  // L A fragments: row q = cell, k = coefficient m
 #pragma unroll
@@ -357,7 +372,7 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
       }
 #pragma unroll
       for (int kt = 0; kt < KTM; ++kt) {
-        if (kt < KT) {
+        if (kt < KTd) {
           const int o0 = (mt * KT + kt) * 32 + lane, o1 = o0 + KT * 32;
           dmma884(t1[0][0], t1[0][1], wr[o0], br[kt]);
           dmma884(t2[0][0], t2[0][1], wi[o0], bi[kt]);
@@ -393,12 +408,33 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
         for (int h = 0; h < 2; ++h) {
           const long long c = e0 + 2 * fk + h;
           if (c < n_inner) {
-            c64 v = cmk((t1[u][h] - t2[u][h]) * scale, (t3[u][h] - t1[u][h] - t2[u][h]) * scale);
+            c64 d = cmk(t1[u][h] - t2[u][h], t3[u][h] - t1[u][h] - t2[u][h]);
+            if (xcol) {  // + W[q][n_in - 1] x[n_in - 1][c]: W at (row block, last k step, k lane 0)
+              const int ow = ((mt + u) * KT + KT - 1) * 32 + fr * 4;
+              d = cfma(cmk(wr[ow], wi[ow]), xc[h], d);
+            }
+            c64 v = cmk(d.x * scale, d.y * scale);
             if constexpr (EPI) v = cadd(v, cmk(s1[u][h] - s2[u][h], s3[u][h] - s1[u][h] - s2[u][h]));
             dst[static_cast<long long>(q) * n_inner + c] = v;
           }
         }
       }
+    }
+    if (xrow) {  // output n_out - 1 = 8 (MT - 1): row 0 of the last row block of W, column fr
+      c64 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int kt = 0; kt < KTM; ++kt)
+        if (kt < KTd) {
+          const int ow = ((MT - 1) * KT + kt) * 32 + fk;
+          acc = cfma(cmk(wr[ow], wi[ow]), cmk(br[kt], bi[kt]), acc);
+        }
+      // fixed tree over the column's four k lanes (deterministic)
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+      const long long c = e0 + fr;
+      if (fk == 0 && c < n_inner) dst[static_cast<long long>(n_out - 1) * n_inner + c] = cmk(acc.x * scale, acc.y * scale);
     }
   }
 }
@@ -1029,6 +1065,7 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
   }();
   if (dft_mma && n_in <= kDftMmaMax && n_out <= kDftMmaMax) {
     const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
+    const int KTd = (n_in % 4 == 1 && n_in > 4) ? KT - 1 : KT;  // the kernel's DMMA k steps (xcol)
     const size_t smem = sizeof(double) * 3 * MT * KT * 32;
     static std::atomic<unsigned long long> raised[4];
     {
@@ -1044,7 +1081,7 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
     // one resident wave (W expanded once per CTA), as many CTAs per SM as fit
     static int occ[4] = {0, 0, 0, 0};
-    const int which = KT <= 4 ? 0 : KT <= 8 ? 1 : KT <= 12 ? 2 : 3;
+    const int which = KTd <= 4 ? 0 : KTd <= 8 ? 1 : KTd <= 12 ? 2 : 3;
     if (occ[which] == 0) {
       const void* fn = which == 0   ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<4>)
                        : which == 1 ? reinterpret_cast<const void*>(dft_axis_dmma_kernel<8>)
@@ -1059,13 +1096,13 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     const long long cap = static_cast<long long>(kNumSMs) * occ[which];
     if (blocks > cap) blocks = cap;
     const int bw = backward ? 1 : 0;
-    if (KT <= 4)
+    if (KTd <= 4)
       dft_axis_dmma_kernel<4><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
           in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
-    else if (KT <= 8)
+    else if (KTd <= 8)
       dft_axis_dmma_kernel<8><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
           in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
-    else if (KT <= 12)
+    else if (KTd <= 12)
       dft_axis_dmma_kernel<12><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
           in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
     else
@@ -1143,7 +1180,8 @@ cudaError_t launch_dft_axis_l2p(const c64* in, c64* out, const c64* tw, long lon
   long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
   const long long cap = static_cast<long long>(device_sms()) * 4;
   if (blocks > cap) blocks = cap;
-  if (KT <= 4)
+  const int KTd = (n_in % 4 == 1 && n_in > 4) ? KT - 1 : KT;  // the kernel's DMMA k steps (xcol)
+  if (KTd <= 4)
     dft_axis_dmma_kernel<4, true><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
         in, out, tw, n_a, n_in, n_out, n_inner, L, 1, scale, epi);
   else

@@ -68,8 +68,11 @@ struct SlabPlan {
   int2* zitems = nullptr;      // fused z-kernel items over local columns
   int n_zitems = 0;
   bool zfused = false;
-  c64* a = nullptr;  // plane buffers, ms * max(near, far) plane sizes
+  c64* a = nullptr;  // near-field plane buffers, ms near planes each
   c64* b = nullptr;
+  c64* fa = nullptr;  // far-field plane buffers (the far side runs concurrently on the aux stream)
+  c64* fb = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   c64* mom = nullptr;
   c64* loc = nullptr;
   std::vector<void*> owned;
@@ -86,6 +89,8 @@ namespace fpbem_cu {
 
 void slab_destroy(fpbem_cu_op* op) {
   if (!op || !op->slab) return;
+  if (op->slab->fork) cudaEventDestroy(op->slab->fork);
+  if (op->slab->join) cudaEventDestroy(op->slab->join);
   for (auto g : op->slab->graph)
     if (g) cudaGraphExecDestroy(g);
   for (void* p : op->slab->owned) cudaFree(p);
@@ -354,9 +359,13 @@ void build_plan(fpbem_cu_op* op, fpbem_cu_comm* comm) {
     h2d(sp->zitems, zi.data(), zi.size() * sizeof(int2), s, "slab z items");
   }
   (void)fmy;
-  const size_t plane_max = static_cast<size_t>(std::max(nr.C * nr.E, fr.C * fr.E));
-  sp->a = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes", s);
-  sp->b = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms)) * plane_max, "slab planes", s);
+  const size_t planes = static_cast<size_t>(std::max(1LL, sp->ms));
+  sp->a = palloc<c64>(sp, planes * static_cast<size_t>(nr.C * nr.E), "slab planes", s);
+  sp->b = palloc<c64>(sp, planes * static_cast<size_t>(nr.C * nr.E), "slab planes", s);
+  sp->fa = palloc<c64>(sp, planes * static_cast<size_t>(fr.C * fr.E), "slab far planes", s);
+  sp->fb = palloc<c64>(sp, planes * static_cast<size_t>(fr.C * fr.E), "slab far planes", s);
+  check(cudaEventCreateWithFlags(&sp->fork, cudaEventDisableTiming), "slab events");
+  check(cudaEventCreateWithFlags(&sp->join, cudaEventDisableTiming), "slab events");
   sp->mom = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab moments", s);
   sp->loc = palloc<c64>(sp, static_cast<size_t>(std::max(1LL, sp->ms * sp->Cm)) * op->b, "slab locals", s);
   check(cudaStreamSynchronize(s), "slab plan");
@@ -379,9 +388,10 @@ bool slab_xy(const SlabPlan* sp, const SlabSide& sd) {
          xy_plane_smem(mx, my, cx, cy, false) <= 200 * 1024 && xy_plane_smem(mx, my, cx, cy, true) <= 200 * 1024;
 }
 
-const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* const* tw, cudaStream_t s) {
+const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* const* tw, cudaStream_t s,
+                         c64* buf0, c64* buf1) {
   const c64* cur = in;
-  c64* bufs[2] = {sp->a, sp->b};
+  c64* bufs[2] = {buf0, buf1};
   int which = 0;
   if (sp->ms == 0) return cur;
   if (slab_xy(sp, sd)) {
@@ -412,7 +422,7 @@ const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64*
 
 // inverse of local_forward from the unpacked planes `in` into `out`
 void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* out, c64* const* tw,
-                   cudaStream_t s) {
+                   cudaStream_t s, c64* spare) {
   if (sp->ms == 0) return;
   if (slab_xy(sp, sd)) {
     check(launch_xy_plane(in, out, tw[0], tw[1], static_cast<int>(sp->mx), static_cast<int>(sp->my),
@@ -423,7 +433,7 @@ void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c
     return;
   }
   const c64* cur = in;
-  c64* tmp = in == sp->a ? sp->b : sp->a;
+  c64* tmp = spare;
   const int passes = (sd.cy > 1) + (sd.cx > 1);
   int done = 0;
   if (sd.cy > 1) {
@@ -463,26 +473,39 @@ void slab_timing(fpbem_cu_op* op, bool has_modes) {
 }
 
 // phase 0: P2M, DFTs below the slab axis on this rank's planes, pack (far, then near)
+// the far side of a phase runs on the aux stream, concurrently with the near
+// side on the main one (independent buffers); fork before, join after
+void slab_fork(fpbem_cu_op* op) {
+  check(cudaEventRecord(op->slab->fork, op->stream), "slab fork");
+  check(cudaStreamWaitEvent(op->aux, op->slab->fork, 0), "slab fork");
+}
+void slab_join(fpbem_cu_op* op) {
+  check(cudaEventRecord(op->slab->join, op->aux), "slab join");
+  check(cudaStreamWaitEvent(op->stream, op->slab->join, 0), "slab join");
+}
+
 void slab_phase0(fpbem_cu_op* op, const c64* x) {
   SlabPlan* sp = op->slab;
-  cudaStream_t s = op->stream;
+  cudaStream_t s = op->stream, a = op->aux;
   const long long cells = sp->ms * sp->Cm;
   SlabSide& nr = sp->nr;
   SlabSide& fr = sp->fr;
+  slab_fork(op);
   if (cells > 0) {
     if (cellwise_supported(op->b, op->n))
       check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, cells * op->n, op->n, sp->mom, op->b, op->b, 1, cells,
-                            false, s),
+                            false, a),
             "slab p2m");
     else
-      check(launch_p2m(op->v0t, x, sp->mom, op->n, op->b, cells * op->n, 1, static_cast<int>(cells), s), "slab p2m");
+      check(launch_p2m(op->v0t, x, sp->mom, op->n, op->b, cells * op->n, 1, static_cast<int>(cells), a), "slab p2m");
     op->launches++;
   }
-  const c64* fplanes = local_forward(op, sp, fr, sp->mom, op->tw, s);
-  gather_rows(fplanes, fr.pack, fr.idx, fr.n_idx, fr.E, s);
-  const c64* nplanes = local_forward(op, sp, nr, x, op->twn, s);
+  const c64* fplanes = local_forward(op, sp, fr, sp->mom, op->tw, a, sp->fa, sp->fb);
+  gather_rows(fplanes, fr.pack, fr.idx, fr.n_idx, fr.E, a);
+  const c64* nplanes = local_forward(op, sp, nr, x, op->twn, s, sp->a, sp->b);
   gather_rows(nplanes, nr.pack, nr.idx, nr.n_idx, nr.E, s);
   op->launches += 2;
+  slab_join(op);
 }
 
 // forward exchange (pack -> recv: every plane of my columns) or backward
@@ -508,7 +531,8 @@ void slab_exchange(fpbem_cu_op* op, bool forward) {
 // near (DFT, block products, inverse DFT)
 void slab_phase1(fpbem_cu_op* op) {
   SlabPlan* sp = op->slab;
-  cudaStream_t s = op->stream;
+  cudaStream_t s = op->stream, a = op->aux;
+  slab_fork(op);
   SlabSide& nr = sp->nr;
   SlabSide& fr = sp->fr;
   const long long ncols = static_cast<long long>(nr.cols[sp->rank].size());
@@ -518,16 +542,16 @@ void slab_phase1(fpbem_cu_op* op) {
   if (fcols > 0) {
     if (sp->zfused) {
       check(launch_m2l_zfused(fr.recv, fr.work, sp->lambda, op->tw[ax], static_cast<int>(sp->Ms),
-                              static_cast<int>(fr.Ls), fcols, op->b, op->b, fscale, sp->zitems, sp->n_zitems, s),
+                              static_cast<int>(fr.Ls), fcols, op->b, op->b, fscale, sp->zitems, sp->n_zitems, a),
             "slab m2l z-fused");
       op->launches++;
     } else {  // recv -> work -> recv -> work
       check(launch_dft_axis(fr.recv, fr.work, op->tw[ax], 1, static_cast<int>(sp->Ms), static_cast<int>(fr.Ls),
-                            fcols * op->b, static_cast<int>(fr.Ls), false, 1.0, s),
+                            fcols * op->b, static_cast<int>(fr.Ls), false, 1.0, a),
             "slab m2l dft");
-      check(launch_mode_product(sp->lambda, fr.work, fr.recv, fr.Ls * fcols, op->b, 1, s), "slab mode product");
+      check(launch_mode_product(sp->lambda, fr.work, fr.recv, fr.Ls * fcols, op->b, 1, a), "slab mode product");
       check(launch_dft_axis(fr.recv, fr.work, op->tw[ax], 1, static_cast<int>(fr.Ls), static_cast<int>(sp->Ms),
-                            fcols * op->b, static_cast<int>(fr.Ls), true, fscale, s),
+                            fcols * op->b, static_cast<int>(fr.Ls), true, fscale, a),
             "slab m2l inverse dft");
       op->launches += 3;
     }
@@ -554,6 +578,7 @@ void slab_phase1(fpbem_cu_op* op) {
           "slab near inverse dft");
     op->launches += 3;
   }
+  slab_join(op);
 }
 
 // phase 2: unpack, the inverse DFTs below the slab axis on my planes, L2P
@@ -565,10 +590,13 @@ void slab_phase2(fpbem_cu_op* op, c64* y) {
   SlabSide& nr = sp->nr;
   SlabSide& fr = sp->fr;
   const bool f_local = fr.cx > 1 || fr.cy > 1, n_local = nr.cx > 1 || nr.cy > 1;
-  scatter_rows(fr.pack, f_local ? sp->a : sp->loc, fr.idx, fr.n_idx, fr.E, s);
-  if (f_local) local_inverse(op, sp, fr, sp->a, sp->loc, op->tw, s);
+  cudaStream_t a = op->aux;
+  slab_fork(op);
+  scatter_rows(fr.pack, f_local ? sp->fa : sp->loc, fr.idx, fr.n_idx, fr.E, a);
+  if (f_local) local_inverse(op, sp, fr, sp->fa, sp->loc, op->tw, a, sp->fb);
   scatter_rows(nr.pack, n_local ? sp->a : y, nr.idx, nr.n_idx, nr.E, s);
-  if (n_local) local_inverse(op, sp, nr, sp->a, y, op->twn, s);
+  if (n_local) local_inverse(op, sp, nr, sp->a, y, op->twn, s, sp->b);
+  slab_join(op);
   check(launch_l2p_add(op->u0, sp->loc, y, op->n, op->b, static_cast<int>(cells), cells * op->n, 1, s), "slab l2p");
   op->launches += 3;
 }
