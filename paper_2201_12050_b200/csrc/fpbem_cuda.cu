@@ -325,6 +325,38 @@ void build_items(fpbem_cu_op* op, const int Ln[3]) {
 // Lattice near field y = S x. With `fuse_loc` (the far field's locals, complete
 // once `join` fires on the aux stream) the L2P y += U0 L is fused into the last
 // inverse pass when that pass is an x-axis DMMA DFT; returns whether it was.
+// the per-mode block products of the lattice near field: x_hat -> y_hat over
+// this handle's stored blocks (DMMA ring, FMA GEMV or the block GEMM by shape)
+void near_mode_stage(fpbem_cu_op* op, const c64* xh, c64* yh, int nrhs, cudaStream_t s) {
+  const long long n = op->n;
+  if (op->mode_lo > 0 || op->mode_hi < op->n_items)
+    check(cudaMemsetAsync(yh, 0, static_cast<size_t>(nrhs * op->qn * n) * sizeof(c64), s), "near spectrum clear");
+  ev_record(op, 7, s);
+  // FPBEM_NEAR_MMA=0 keeps the FMA GEMV where the tensor-core mode product applies (A/B)
+  static const bool mma_env = [] {
+    const char* v = std::getenv("FPBEM_NEAR_MMA");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  int nw_, kc_, ring_;
+  size_t smem_;
+  if (mma_env && mode_mma_shape(op->n, nrhs * op->near_nimg, &nw_, &kc_, &ring_, &smem_)) {
+    check(launch_mode_mma(op->shat, op->items, op->n_items, op->perm, xh, yh, op->n, op->mode_lo, op->mode_hi,
+                          op->qn, nrhs, op->near_nimg, s),
+          "near mode mma");
+  } else if (nrhs * op->near_nimg <= kModeGemvMaxAcc) {
+    check(launch_mode_gemv(op->shat, op->items, op->n_items, op->perm, xh, yh, op->n, op->mode_lo, op->mode_hi,
+                           op->qn, nrhs, op->near_nimg, s),
+          "near mode gemv");
+  } else {
+    build_mode_jobs(op, nrhs);
+    check(launch_block_gemm(op->shat, n * n, op->n, op->n, xh, yh, op->n, nullptr, op->mjobs, op->n_mjobs, op->n,
+                            op->n, op->qn * n, nrhs, s, op->qn * n, op->perm),
+          "near mode gemm");
+  }
+  ev_record(op, 8, s);
+  op->launches++;
+}
+
 bool near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_t s, const c64* fuse_loc = nullptr,
                     cudaEvent_t join = nullptr) {
   Nvtx range("near field (lattice convolution)");
@@ -365,32 +397,7 @@ bool near_fft_apply(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, cudaStream_
   if (Lz > 1) fwd(2, r, Mz, Lz, static_cast<long long>(Ly) * Lx * n);
   c64* yh = bufs[which];
   which ^= 1;
-  if (op->mode_lo > 0 || op->mode_hi < op->n_items)
-    check(cudaMemsetAsync(yh, 0, static_cast<size_t>(r * op->qn * n) * sizeof(c64), s), "near spectrum clear");
-  ev_record(op, 7, s);
-  // FPBEM_NEAR_MMA=0 keeps the FMA GEMV where the tensor-core mode product applies (A/B)
-  static const bool mma_env = [] {
-    const char* v = std::getenv("FPBEM_NEAR_MMA");
-    return !(v && std::strcmp(v, "0") == 0);
-  }();
-  int nw_, kc_, ring_;
-  size_t smem_;
-  if (mma_env && mode_mma_shape(op->n, nrhs * op->near_nimg, &nw_, &kc_, &ring_, &smem_)) {
-    check(launch_mode_mma(op->shat, op->items, op->n_items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi,
-                          op->qn, nrhs, op->near_nimg, s),
-          "near mode mma");
-  } else if (nrhs * op->near_nimg <= kModeGemvMaxAcc) {
-    check(launch_mode_gemv(op->shat, op->items, op->n_items, op->perm, cur, yh, op->n, op->mode_lo, op->mode_hi,
-                           op->qn, nrhs, op->near_nimg, s),
-          "near mode gemv");
-  } else {
-    build_mode_jobs(op, nrhs);
-    check(launch_block_gemm(op->shat, n * n, op->n, op->n, cur, yh, op->n, nullptr, op->mjobs, op->n_mjobs, op->n,
-                            op->n, op->qn * n, nrhs, s, op->qn * n, op->perm),
-          "near mode gemm");
-  }
-  ev_record(op, 8, s);
-  op->launches++;
+  near_mode_stage(op, cur, yh, nrhs, s);
   cur = yh;
   int left = (Lx > 1) + (Ly > 1) + (Lz > 1);
   const double scale = 1.0 / static_cast<double>(op->qn);
@@ -502,20 +509,24 @@ void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {
 // Pruned separable lattice DFT, per-mode product, pruned inverse:
 // moments (op->mom) -> locals (op->loc), CirculantSpectrum::matvec restated
 // (src/structured.cpp:122-166), everything enqueued on `s`.
-void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, const c64* lambda, c64* locals) {
+struct M2lPass {
+  int kind;  // 0 dft, 1 mode product, 2 fused z-dft + mode product + inverse z-dft,
+             // 3 / 4 forward / inverse x+y plane DFTs (one kernel each)
+  long long n_a;
+  int n_in, n_out;
+  long long inner;
+  int L;
+  int axis;
+  bool back;
+};
+
+// the M2L's pass list for nrhs right-hand sides (CirculantSpectrum::matvec as
+// pruned separable DFT passes, src/structured.cpp:122-166)
+std::vector<M2lPass> m2l_plan(fpbem_cu_op* op, int nrhs) {
   const long long E = static_cast<long long>(nrhs) * op->b;
   const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
   const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
-  struct Pass {
-    int kind;  // 0 dft, 1 mode product, 2 fused z-dft + mode product + inverse z-dft,
-               // 3 / 4 forward / inverse x+y plane DFTs (one kernel each)
-    long long n_a;
-    int n_in, n_out;
-    long long inner;
-    int L;
-    int axis;
-    bool back;
-  };
+  using Pass = M2lPass;
   std::vector<Pass> passes;
   long long cx = Mx, cy = My;  // current x / y extents
   // z forward + mode product + z inverse fused into one kernel when the
@@ -567,13 +578,26 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
     if (Lx > 1)
       passes.push_back({0, My * Mz, static_cast<int>(Lx), static_cast<int>(Mx), E, static_cast<int>(Lx), 0, true});
   }
+  return passes;
+}
+
+// M2L moments -> locals. xy_done: the first pass (the forward x+y plane DFTs,
+// kind 3) already ran into op->fa (the pipelined host apply does it slab by slab)
+void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, const c64* lambda, c64* locals,
+               bool xy_done = false) {
+  const long long E = static_cast<long long>(nrhs) * op->b;
+  const long long Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
+  const long long Lx = op->L[0], Ly = op->L[1], Lz = op->L[2];
+  using Pass = M2lPass;
+  const std::vector<Pass> passes = m2l_plan(op, nrhs);
+  if (xy_done && (passes.empty() || passes[0].kind != 3)) fail(FPBEM_CU_EINVAL, "m2l: no x+y plane pass to skip");
   int last_dft = -1;  // the pass that applies the 1/q scale
   for (int i = 0; i < static_cast<int>(passes.size()); ++i)
     if ((passes[i].kind == 0 && passes[i].back) || passes[i].kind == 2 || passes[i].kind == 4) last_dft = i;
-  const c64* cur = moments;
+  const c64* cur = xy_done ? op->fa : moments;
   c64* bufs[2] = {op->fa, op->fb};
-  int which = 0;
-  for (int i = 0; i < static_cast<int>(passes.size()); ++i) {
+  int which = xy_done ? 1 : 0;
+  for (int i = xy_done ? 1 : 0; i < static_cast<int>(passes.size()); ++i) {
     const Pass& p = passes[i];
     const bool final = i + 1 == static_cast<int>(passes.size());
     c64* out = final ? locals : bufs[which];
@@ -769,6 +793,114 @@ void apply_chunk(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
     }
     op->applies++;
   }
+}
+
+// Host-pointer product of one right-hand side with the copies overlapped
+// (the C-ABI's synchronous FPBEM_CU_PTR_HOST apply, src/fmm.cpp:246-271 as an
+// ApplyFn). x arrives in slabs of z-planes on a copy stream while the near
+// field's x and y DFT passes run on the slabs already there; the far field
+// starts once x is complete; after the z passes and the block products, the
+// inverse y and x (+ L2P) passes run slab by slab and each slab of y goes back
+// on a second copy stream while the next is computed. Same kernels, same
+// arithmetic as apply_chunk. Applies to 3-D lattices on the lattice near
+// field (cfg3, cfg5) with the fused L2P; returns false (nothing done) otherwise.
+bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
+  static const bool env = [] {
+    const char* v = std::getenv("FPBEM_PIPE_H2D");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  const int Mx = op->counts[0], My = op->counts[1], Mz = op->counts[2];
+  const int Lx = op->Ln[0], Ly = op->Ln[1], Lz = op->Ln[2];
+  if (!env || !op->near_fft || op->nranks > 1 || op->comm || op->mirrored_level >= 0 || op->timing ||
+      Mz < 4 || Lx < 2 || Ly < 2 || Lz < 2 || !dft_l2p_supported(Lx, Mx, op->b) ||
+      op->mode_lo > 0 || op->mode_hi < op->n_items)
+    return false;
+  const long long n = op->n;
+  const int chunks = std::min(4, Mz);
+  cudaStream_t s = op->stream, a = op->aux;
+  if (!op->cin) {
+    check(cudaStreamCreateWithFlags(&op->cin, cudaStreamNonBlocking), "copy-in stream");
+    check(cudaStreamCreateWithFlags(&op->cout, cudaStreamNonBlocking), "copy-out stream");
+    for (int i = 0; i < 8; ++i) {
+      check(cudaEventCreateWithFlags(&op->pev_in[i], cudaEventDisableTiming), "pipeline events");
+      check(cudaEventCreateWithFlags(&op->pev_out[i], cudaEventDisableTiming), "pipeline events");
+    }
+  }
+  auto z0_of = [&](int c) { return static_cast<long long>(Mz) * c / chunks; };
+  const long long xplane = static_cast<long long>(My) * Mx * n;  // one z-plane of x / y
+  // the copy-in stream starts after whatever the handle's stream has queued (staging reuse)
+  check(cudaEventRecord(op->fork, s), "pipeline fork");
+  check(cudaStreamWaitEvent(op->cin, op->fork, 0), "pipeline fork");
+  for (int c = 0; c < chunks; ++c) {
+    const long long z0 = z0_of(c), z1 = z0_of(c + 1);
+    check(cudaMemcpyAsync(op->xin + z0 * xplane, xh + z0 * xplane, static_cast<size_t>((z1 - z0) * xplane) * sizeof(c64),
+                          cudaMemcpyHostToDevice, op->cin),
+          "x upload");
+    check(cudaEventRecord(op->pev_in[c], op->cin), "pipeline event");
+  }
+  // far field (aux stream): P2M and the forward x+y plane DFTs of the M2L slab
+  // by slab as x arrives, the rest once x is complete; joined before the first L2P
+  const std::vector<M2lPass> plan = m2l_plan(op, 1);
+  const bool far_xy = !plan.empty() && plan[0].kind == 3;
+  const int fLx = op->L[0], fLy = op->L[1];
+  for (int c = 0; c < chunks; ++c) {
+    const long long z0 = z0_of(c), z1 = z0_of(c + 1);
+    const long long c0 = z0 * My * Mx, nc = (z1 - z0) * My * Mx;  // the slab's cells
+    check(cudaStreamWaitEvent(a, op->pev_in[c], 0), "pipeline far");
+    if (cellwise_on() && cellwise_supported(op->b, op->n))  // M_c = V0 p_c (src/fmm.cpp:256-259)
+      check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, op->xin + c0 * n, op->N, op->n, op->mom + c0 * op->b,
+                            op->b, op->b, 1, nc, false, a),
+            "p2m");
+    else
+      check(launch_p2m(op->v0t, op->xin + c0 * n, op->mom + c0 * op->b, op->n, op->b, op->N, 1, static_cast<int>(nc),
+                       a),
+            "p2m");
+    op->launches++;
+    if (far_xy) {
+      check(launch_xy_plane(op->mom + c0 * op->b, op->fa + z0 * fLy * fLx * op->b, op->tw[0], op->tw[1], Mx, My, fLx,
+                            fLy, static_cast<int>(z1 - z0), op->b, false, 1.0, a),
+            "lattice xy dft");
+      op->launches++;
+    }
+  }
+  m2l_apply(op, 1, a, op->mom, op->lambda, op->loc, far_xy);
+  check(cudaEventRecord(op->join, a), "pipeline join");
+  // near field: x and y passes slab by slab (buffers as near_fft_apply: x -> nfa -> nfb)
+  for (int c = 0; c < chunks; ++c) {
+    const long long z0 = z0_of(c), z1 = z0_of(c + 1), m = z1 - z0;
+    check(cudaStreamWaitEvent(s, op->pev_in[c], 0), "pipeline in");
+    check(launch_dft_axis(op->xin + z0 * xplane, op->nfa + z0 * My * Lx * n, op->twn[0], m * My, Mx, Lx, n, Lx, false,
+                          1.0, s),
+          "near dft x");
+    check(launch_dft_axis(op->nfa + z0 * My * Lx * n, op->nfb + z0 * static_cast<long long>(Ly) * Lx * n, op->twn[1],
+                          m, My, Ly, static_cast<long long>(Lx) * n, Ly, false, 1.0, s),
+          "near dft y");
+    op->launches += 2;
+  }
+  const long long zstride = static_cast<long long>(Ly) * Lx * n;
+  check(launch_dft_axis(op->nfb, op->nfa, op->twn[2], 1, Mz, Lz, zstride, Lz, false, 1.0, s), "near dft z");
+  near_mode_stage(op, op->nfa, op->nfb, 1, s);
+  check(launch_dft_axis(op->nfb, op->nfa, op->twn[2], 1, Lz, Mz, zstride, Lz, true, 1.0, s), "near inverse dft z");
+  op->launches += 2;
+  const double scale = 1.0 / static_cast<double>(op->qn);
+  check(cudaStreamWaitEvent(s, op->join, 0), "pipeline join");  // the locals of the far field
+  for (int c = 0; c < chunks; ++c) {
+    const long long z0 = z0_of(c), z1 = z0_of(c + 1), m = z1 - z0;
+    check(launch_dft_axis(op->nfa + z0 * zstride, op->nfb + z0 * My * Lx * n, op->twn[1], m, Ly, My,
+                          static_cast<long long>(Lx) * n, Ly, true, 1.0, s),
+          "near inverse dft y");
+    check(launch_dft_axis_l2p(op->nfb + z0 * My * Lx * n, op->yout + z0 * xplane, op->twn[0], m * My, Lx, Mx, n, Lx,
+                              scale, op->u0, op->loc + z0 * My * Mx * op->b, op->b, 1, s),
+          "near inverse dft x + l2p");
+    op->launches += 2;
+    check(cudaEventRecord(op->pev_out[c], s), "pipeline event");
+    check(cudaStreamWaitEvent(op->cout, op->pev_out[c], 0), "pipeline out");
+    check(cudaMemcpyAsync(yh + z0 * xplane, op->yout + z0 * xplane, static_cast<size_t>(m * xplane) * sizeof(c64),
+                          cudaMemcpyDeviceToHost, op->cout),
+          "y download");
+  }
+  check(cudaStreamSynchronize(op->cout), "apply sync");
+  return true;
 }
 
 void apply_device(fpbem_cu_op* op, const c64* x, c64* y, int nrhs, bool reduce) {
@@ -1058,6 +1190,14 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
   if (op->pinned) cudaFreeHost(op->pinned);
   for (auto& e : op->ev)
     if (e) cudaEventDestroy(e);
+  for (auto* evs : {op->pev_in, op->pev_out})
+    for (int i = 0; i < 8; ++i)
+      if (evs[i]) cudaEventDestroy(evs[i]);
+  for (cudaStream_t cs : {op->cin, op->cout})
+    if (cs) {
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+    }
   if (op->aux) {
     cudaStreamSynchronize(op->aux);
     cudaStreamDestroy(op->aux);
@@ -1084,6 +1224,7 @@ int fpbem_cu_fmm_apply(fpbem_cu_op* op, const fpbem_c64* x, fpbem_c64* y, int nr
       op->xin = dalloc<c64>(static_cast<size_t>(op->N) * op->max_rhs, "x staging");
       op->yout = dalloc<c64>(static_cast<size_t>(op->N) * op->max_rhs, "y staging");
     }
+    if (nrhs == 1 && apply_host_pipelined(op, reinterpret_cast<const c64*>(x), reinterpret_cast<c64*>(y))) return;
     for (int r0 = 0; r0 < nrhs; r0 += op->max_rhs) {
       const int c = std::min(op->max_rhs, nrhs - r0);
       const size_t cb = static_cast<size_t>(op->N) * c * sizeof(c64);

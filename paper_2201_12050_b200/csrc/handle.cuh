@@ -189,6 +189,10 @@ struct fpbem_cu_op {
   c64* fb = nullptr;
   c64* xin = nullptr;   // host-pointer staging
   c64* yout = nullptr;
+  // pipelined host-pointer product (apply_host_pipelined): copy-in / copy-out
+  // streams and per-chunk events
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t pev_in[8] = {}, pev_out[8] = {};
 
   // GMRES
   c64* basis = nullptr;

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+./tools/_gsp > gpurun_out/gsp.txt 2>&1
+echo done

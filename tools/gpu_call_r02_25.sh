@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+export PYTHONFAULTHANDLER=1
+timeout 1500 python -m pytest tests -m gpu -q -x -rf -p no:cacheprovider > gpurun_out/pytest_all.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_all.log
+timeout 600 python bench.py --no-cpu-baseline --no-nosym --gmres-max-iter 300 > gpurun_out/bench_pipe.json 2> gpurun_out/bench_pipe.err
+FPBEM_PIPE_H2D=0 timeout 600 python bench.py --no-cpu-baseline --no-nosym --gmres-max-iter 300 > gpurun_out/bench_nopipe.json 2> gpurun_out/bench_nopipe.err
+echo done
