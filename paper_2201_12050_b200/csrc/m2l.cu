@@ -698,6 +698,53 @@ __device__ __forceinline__ void zdft(const c64* __restrict__ src, c64* __restric
   }
 }
 
+// The same z-DFT of the item's columns as small complex GEMMs on DMMA (the
+// FMA form above spends its time on shared-memory twiddle / input loads and
+// dependent FMA chains): per column C[n_out][E] = W[n_out][n_in] B[n_in][E] with
+// W[q][j] = tw[(q j) mod L] (conjugated backward), tiles of 8 outputs x 8
+// fields over the DFT warps, A fragments formed from the twiddle table, Gauss
+// 3-multiplication form. Forward: C into f_z (shared); backward: C * scale
+// into the global output of column col. The tile sums run in a fixed order.
+template <bool kBack>
+__device__ __forceinline__ void zdft_mma(const c64* const* src, c64* const* dst, const long long* cols, int nc,
+                                         const c64* __restrict__ tw_s, int n_in, int n_out, int L, int E, int w,
+                                         int n_w, int lane, double scale, c64* __restrict__ out, long long plane) {
+  const int fr = lane >> 2, fk = lane & 3;
+  const int MT = (n_out + 7) / 8, NT = (E + 7) / 8, KT = (n_in + 3) / 4;
+  const int per_col = MT * NT;
+  for (int t = w; t < nc * per_col; t += n_w) {
+    const int s = t / per_col, r = t - s * per_col, mt = r / NT, nt = r - mt * NT;
+    const c64* B = src[s];
+    const int q = mt * 8 + fr, cb = nt * 8 + fr;
+    double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
+    for (int kt = 0; kt < KT; ++kt) {
+      const int j = kt * 4 + fk;
+      c64 a = cmk(0.0, 0.0), bv = cmk(0.0, 0.0);
+      if (j < n_in) {
+        if (q < n_out) {
+          a = tw_s[(q * j) % L];
+          if (kBack) a.y = -a.y;
+        }
+        if (cb < E) bv = B[j * E + cb];
+      }
+      dmma884(t1[0], t1[1], a.x, bv.x);
+      dmma884(t2[0], t2[1], a.y, bv.y);
+      dmma884(t3[0], t3[1], a.x + a.y, bv.x + bv.y);
+    }
+    if (q >= n_out) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = nt * 8 + 2 * fk + h;
+      if (c >= E) continue;
+      const c64 v = cmk(t1[h] - t2[h], t3[h] - t1[h] - t2[h]);
+      if (kBack)
+        out[(static_cast<long long>(q) * plane + cols[s]) * E + c] = cscale(v, scale);
+      else
+        dst[s][q * E + c] = v;
+    }
+  }
+}
+
 // one mode's product for the lanes of a warp: g[ri] = sum_c lam[i + b c] f[r b + c]
 __device__ __forceinline__ void mode_product_warp(const c64* __restrict__ lam_blk, const c64* __restrict__ f_mode,
                                                   c64* __restrict__ g_mode, int E, int b, int lane) {
@@ -849,7 +896,8 @@ __device__ __forceinline__ void mode_pair_small(const c64* __restrict__ lam_blk,
 __global__ void __launch_bounds__(32 * (1 + kPipeMaxModeWarps + kPipeMaxDftWarps), 1)
 m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ lambda,
                  const c64* __restrict__ tw, int Mz, int Lz, long long plane, int E, int b, int n_mw,
-                 int ring, int n_dw, double scale, const int2* __restrict__ items, int n_items_total) {
+                 int ring, int n_dw, double scale, const int2* __restrict__ items, int n_items_total,
+                 int use_mma) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b2 = b * b;
   c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
@@ -966,10 +1014,19 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
     }
   } else {  // ---- DFT warps
     const int dt = tid - 32 * (1 + n_mw), n_dt = 32 * n_dw;
+    const bool mma = use_mma != 0;  // the z-DFTs on DMMA (FPBEM_ZF_DFT=fma: the FMA form, A/B)
     auto inverse = [&](int c) {  // inverse z of item c (its modes are finished)
       const int buf = c & 1;
       mbar_wait(smem_u32(&col_done[buf]), static_cast<unsigned>((c >> 1) & 1));
       const int2 it = item(c);
+      if (mma) {
+        const c64* srcs[2] = {f_z0 + (buf * 2) * Lz * E, f_z0 + (buf * 2 + 1) * Lz * E};
+        const long long cols[2] = {it.x, it.y};
+        zdft_mma<true>(srcs, nullptr, cols, it.y >= 0 ? 2 : 1, tw_s, Lz, Mz, Lz, E, dt >> 5, n_dw, lane, scale, out,
+                       plane);
+        dft_sync(n_dt);
+        return;
+      }
       for (int s = 0; s < (it.y >= 0 ? 2 : 1); ++s) {
         const long long col = s ? it.y : it.x;
         const c64* g_z = f_z0 + (buf * 2 + s) * Lz * E;
@@ -986,7 +1043,12 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
       // in inverse(k - 2)) and its inverse ran before this forward pass
       mbar_wait(smem_u32(&in_full[buf]), static_cast<unsigned>((k >> 1) & 1));
       const int nc = item(k).y >= 0 ? 2 : 1;
-      for (int s = 0; s < nc; ++s) {
+      if (mma) {
+        const c64* srcs[2] = {f_in0 + (buf * 2) * Mz * E, f_in0 + (buf * 2 + 1) * Mz * E};
+        c64* dsts[2] = {f_z0 + (buf * 2) * Lz * E, f_z0 + (buf * 2 + 1) * Lz * E};
+        zdft_mma<false>(srcs, dsts, nullptr, nc, tw_s, Mz, Lz, Lz, E, dt >> 5, n_dw, lane, 1.0, nullptr, 0);
+      }
+      for (int s = 0; s < (mma ? 0 : nc); ++s) {
         c64* f_z = f_z0 + (buf * 2 + s) * Lz * E;
         const c64* f_in = f_in0 + (buf * 2 + s) * Mz * E;
         const int G = zdft_group(Lz * E, n_dt);
@@ -1334,8 +1396,12 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
   }
   const int grid = n_items < kNumSMs ? n_items : kNumSMs;  // persistent: one CTA per SM
   if (grid == 0) return cudaSuccess;
+  static const int use_mma = [] {
+    const char* v = std::getenv("FPBEM_ZF_DFT");
+    return (v && std::strcmp(v, "fma") == 0) ? 0 : 1;
+  }();
   m2l_zpipe_kernel<<<grid, 32 * (1 + n_mw + kPipeMaxDftWarps), smem, stream>>>(
-      in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, kPipeMaxDftWarps, scale, items, n_items);
+      in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, kPipeMaxDftWarps, scale, items, n_items, use_mma);
   return cudaGetLastError();
 }
 
