@@ -125,6 +125,10 @@ __device__ __forceinline__ void cp_async16_u32(unsigned dst, const void* src, bo
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // D += A * B on one 8x8x4 fp64 tensor-core tile (DMMA.8x8x4 in SASS)
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {

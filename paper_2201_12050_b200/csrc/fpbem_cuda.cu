@@ -138,11 +138,25 @@ void build_jobs(fpbem_cu_op* op, int nrhs) {
 void build_mode_jobs(fpbem_cu_op* op, int nrhs) {
   if (op->mjobs_nrhs == nrhs) return;
   std::vector<int4> jobs;
-  for (long long t = op->mode_lo; t < op->mode_hi; ++t)
+  // FPBEM_ORBIT_JOBS=0: one job per image mode even when the orbit fits one column tile (A/B)
+  static const bool orbit_env = [] {
+    const char* v = std::getenv("FPBEM_ORBIT_JOBS");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  for (long long t = op->mode_lo; t < op->mode_hi; ++t) {
+    int nimg = 0;
+    for (int i = 0; i < 8; ++i) nimg += op->items_q[t * 8 + i] >= 0;
+    if (orbit_env) {
+      // the orbit's (image, rhs) columns in tiles of 64 (job bit 15): the block is
+      // streamed once per tile instead of once per image (8 images x 8 rhs: once)
+      tile_columns(jobs, static_cast<int>(t), nimg * nrhs, 0, true, 1 << 15);
+      continue;
+    }
     for (int i = 0; i < 8; ++i) {  // one column set per image mode; g != 0: through P_g (job bits 12-14)
       const int q = op->items_q[t * 8 + i];
       if (q >= 0) tile_columns(jobs, static_cast<int>(t), nrhs, q, true, op->items_g[t * 8 + i] << 12);
     }
+  }
   if (static_cast<int>(jobs.size()) > op->mjobs_cap) {
     if (op->mjobs) cudaFree(op->mjobs);
     op->mjobs = dalloc<int4>(jobs.size(), "mode jobs");
@@ -350,7 +364,7 @@ void near_mode_stage(fpbem_cu_op* op, const c64* xh, c64* yh, int nrhs, cudaStre
   } else {
     build_mode_jobs(op, nrhs);
     check(launch_block_gemm(op->shat, n * n, op->n, op->n, xh, yh, op->n, nullptr, op->mjobs, op->n_mjobs, op->n,
-                            op->n, op->qn * n, nrhs, s, op->qn * n, op->perm),
+                            op->n, op->qn * n, nrhs, s, op->qn * n, op->perm, op->items, op->n_items),
           "near mode gemm");
   }
   ev_record(op, 8, s);
@@ -1185,7 +1199,7 @@ void fpbem_cu_fmm_destroy(fpbem_cu_op* op) {
                   static_cast<void*>(op->shat), static_cast<void*>(op->twn[0]), static_cast<void*>(op->twn[1]),
                   static_cast<void*>(op->twn[2]), static_cast<void*>(op->nfa), static_cast<void*>(op->nfb),
                   static_cast<void*>(op->mjobs), static_cast<void*>(op->perm),
-                  static_cast<void*>(op->items)})
+                  static_cast<void*>(op->items), op->bws, op->dws})
     if (p) cudaFree(p);
   if (op->pinned) cudaFreeHost(op->pinned);
   for (auto& e : op->ev)

@@ -299,11 +299,22 @@ BatchOut gmres_batched(fpbem_cu_op* op, const c64* Bd, c64* Xd, int G, double to
     return p;
   };
   const size_t vecb = static_cast<size_t>(n) * sizeof(c64);
-  c64* V = static_cast<c64*>(alloc(vecb * G * (m + 1), "batched basis"));
-  c64* R = static_cast<c64*>(alloc(vecb * G, "batched residual"));
-  c64* T = static_cast<c64*>(alloc(vecb * G, "batched A x"));
-  c64* P = static_cast<c64*>(alloc(vecb * G, "batched pack in"));
-  c64* Q = static_cast<c64*>(alloc(vecb * G, "batched pack out"));
+  // the basis and the four work vectors stay with the handle between solves
+  // (64 right-hand sides of cfg5 at restart 50: 72 GB, whose cudaMalloc / cudaFree
+  // per call cost more than many Arnoldi steps)
+  const size_t ws_bytes = vecb * G * (m + 5);
+  if (op->bws_bytes < ws_bytes) {
+    if (op->bws) check(cudaFree(op->bws), "batched workspace");
+    op->bws = nullptr;
+    op->bws_bytes = 0;
+    check(cudaMalloc(&op->bws, ws_bytes), "batched workspace");
+    op->bws_bytes = ws_bytes;
+  }
+  c64* V = static_cast<c64*>(op->bws);
+  c64* R = V + static_cast<size_t>(n) * G * (m + 1);
+  c64* T = R + static_cast<size_t>(n) * G;
+  c64* P = T + static_cast<size_t>(n) * G;
+  c64* Q = P + static_cast<size_t>(n) * G;
   // scalars: [flags G int (8 B slots)][pre2 G][post2 G][post2b G][rn2 G][bn2 G][d G]
   //          [h (m+1)G c64][hc (m+1)G][y mG][jr G int][mask G int][idx G int]
   const size_t g8 = 8 * static_cast<size_t>((G + 1) & ~1);  // even count: c64 sections stay 16-byte aligned

@@ -192,6 +192,11 @@ struct fpbem_cu_op {
   // pipelined host-pointer product (apply_host_pipelined): copy-in / copy-out
   // streams and per-chunk events
   cudaStream_t cin = nullptr, cout = nullptr;
+  // lockstep GMRES workspace (basis + work vectors), kept between solves
+  void* bws = nullptr;
+  size_t bws_bytes = 0;
+  void* dws = nullptr;  // distributed GMRES arena
+  size_t dws_bytes = 0;
   cudaEvent_t pev_in[8] = {}, pev_out[8] = {};
 
   // GMRES

@@ -10,7 +10,8 @@ namespace fpbem_cu {
 // columns are (pair, rhs) with rhs fastest, or (cell, rhs) when pair_src is null.
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
-                              cudaStream_t stream, long long out_rhs_stride = 0, const int* perm = nullptr);
+                              cudaStream_t stream, long long out_rhs_stride = 0, const int* perm = nullptr,
+                              const int* items = nullptr, long long n_items = 0);
 // out_rhs_stride > 0: column (unit, rhs) lands at out[rhs * out_rhs_stride + unit * ldo] (rhs-major);
 // jobs with g = bits 12-14 of .z nonzero gather B rows and scatter output rows through
 // perm + (g - 1) * K (the lattice near field's symmetry images)

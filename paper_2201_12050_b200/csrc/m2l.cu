@@ -997,7 +997,9 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
         const c64* blk = ring_buf + slot * b2;
         c64* m1 = fz + qz * E;
         c64* m2 = fz + (Lz + (qz ? Lz - qz : 0)) * E;  // the mirror column's mode -qz
-        if (b <= 32) {
+        if (use_mma & 2) {
+          // FPBEM_ZF_PROBE=1 (diagnostic, wrong results): the Λ stream without the mode products
+        } else if (b <= 32) {
           if (pair)
             mode_pair_small<true>(blk, m1, m2, E, b, lane, dsg);
           else
@@ -1014,11 +1016,16 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
     }
   } else {  // ---- DFT warps
     const int dt = tid - 32 * (1 + n_mw), n_dt = 32 * n_dw;
-    const bool mma = use_mma != 0;  // the z-DFTs on DMMA (FPBEM_ZF_DFT=fma: the FMA form, A/B)
+    const bool mma = (use_mma & 1) != 0;  // the z-DFTs on DMMA (FPBEM_ZF_DFT=fma: the FMA form, A/B)
+    const bool skip = (use_mma & 4) != 0;  // FPBEM_ZF_PROBE=2 (diagnostic, wrong results): no z-DFT work
     auto inverse = [&](int c) {  // inverse z of item c (its modes are finished)
       const int buf = c & 1;
       mbar_wait(smem_u32(&col_done[buf]), static_cast<unsigned>((c >> 1) & 1));
       const int2 it = item(c);
+      if (skip) {
+        dft_sync(n_dt);
+        return;
+      }
       if (mma) {
         const c64* srcs[2] = {f_z0 + (buf * 2) * Lz * E, f_z0 + (buf * 2 + 1) * Lz * E};
         const long long cols[2] = {it.x, it.y};
@@ -1043,12 +1050,12 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
       // in inverse(k - 2)) and its inverse ran before this forward pass
       mbar_wait(smem_u32(&in_full[buf]), static_cast<unsigned>((k >> 1) & 1));
       const int nc = item(k).y >= 0 ? 2 : 1;
-      if (mma) {
+      if (mma && !skip) {
         const c64* srcs[2] = {f_in0 + (buf * 2) * Mz * E, f_in0 + (buf * 2 + 1) * Mz * E};
         c64* dsts[2] = {f_z0 + (buf * 2) * Lz * E, f_z0 + (buf * 2 + 1) * Lz * E};
         zdft_mma<false>(srcs, dsts, nullptr, nc, tw_s, Mz, Lz, Lz, E, dt >> 5, n_dw, lane, 1.0, nullptr, 0);
       }
-      for (int s = 0; s < (mma ? 0 : nc); ++s) {
+      for (int s = 0; s < (mma || skip ? 0 : nc); ++s) {
         c64* f_z = f_z0 + (buf * 2 + s) * Lz * E;
         const c64* f_in = f_in0 + (buf * 2 + s) * Mz * E;
         const int G = zdft_group(Lz * E, n_dt);
@@ -1398,7 +1405,9 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
   if (grid == 0) return cudaSuccess;
   static const int use_mma = [] {
     const char* v = std::getenv("FPBEM_ZF_DFT");
-    return (v && std::strcmp(v, "fma") == 0) ? 0 : 1;
+    const char* pr = std::getenv("FPBEM_ZF_PROBE");
+    const int probe = pr ? std::atoi(pr) : 0;
+    return ((v && std::strcmp(v, "fma") == 0) ? 0 : 1) | (probe == 1 ? 2 : 0) | (probe == 2 ? 4 : 0);
   }();
   m2l_zpipe_kernel<<<grid, 32 * (1 + n_mw + kPipeMaxDftWarps), smem, stream>>>(
       in, out, lambda, tw, Mz, Lz, plane, E, b, n_mw, ring, kPipeMaxDftWarps, scale, items, n_items, use_mma);

@@ -46,7 +46,7 @@ constexpr size_t kSmemB = sizeof(c64) * STAGES * BN * BP;
 template <int MI, int NI, typename Loader>
 __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& load_stage, int nk, int warp, int lane,
                                           int ncols, int m0, int M, const long long* col_out, c64* __restrict__ out,
-                                          const int* __restrict__ prow) {
+                                          const int* col_g, const int* __restrict__ perm) {
   constexpr int G = 8 / MI;  // row groups
   const int wm = warp % G, wn = warp / G;
   const int fr = lane >> 2, fk = lane & 3;
@@ -115,7 +115,10 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
       for (int j = 0; j < 2; ++j) {
         const int c = wn * 8 * NI + ni * 8 + 2 * fk + j;
         const long long o = col_out[c];
-        if (o >= 0) out[o + (prow ? __ldg(prow + gm) : gm)] = cmk(t1[mi][ni][j] - t2[mi][ni][j], t3[mi][ni][j] - t1[mi][ni][j] - t2[mi][ni][j]);
+        const int g = col_g[c];  // image column: its rows land at P_g[row]
+        if (o >= 0)
+          out[o + (g ? __ldg(perm + static_cast<size_t>(g - 1) * M + gm) : gm)] =
+              cmk(t1[mi][ni][j] - t2[mi][ni][j], t3[mi][ni][j] - t1[mi][ni][j] - t2[mi][ni][j]);
       }
   }
 }
@@ -132,12 +135,14 @@ __device__ __forceinline__ void gemm_main(const c64* As, const c64* Bs, Loader& 
 __global__ void __launch_bounds__(THREADS, 2)
 near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, int M, const c64* __restrict__ x,
                       c64* __restrict__ out, int ldo, const int* __restrict__ pair_src, const int4* __restrict__ jobs,
-                      int K, int n, long long N, int nrhs, long long out_rhs_stride, const int* __restrict__ perm) {
+                      int K, int n, long long N, int nrhs, long long out_rhs_stride, const int* __restrict__ perm,
+                      const int* __restrict__ items, long long n_items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   c64* As = reinterpret_cast<c64*>(smem_raw);
   c64* Bs = reinterpret_cast<c64*>(smem_raw + kSmemA);
   __shared__ long long col_src[BN];
   __shared__ long long col_out[BN];
+  __shared__ int col_g[BN];  // symmetry map of the column (0: none)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -148,20 +153,42 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   // image-mode tile of the lattice near field: rows of B gathered and rows of
   // the output scattered through the symmetry permutation P_g (g = bits 12-14)
   const int gsym = (job.z >> 12) & 7;
-  const int* pk = gsym ? perm + static_cast<size_t>(gsym - 1) * K : nullptr;
+  // bit 15: the columns are (image, rhs) pairs of stored block s's whole orbit
+  // (items[s]: its up-to-8 image modes and maps), so the block is read once
+  // for every image instead of once per image
+  const bool orbit = (job.z >> 15) & 1;
 
   if (tid < BN) {
     if (tid < ncols) {
       const int gc = col0 + tid;
-      const int unit = pair_base + gc / nrhs;  // pair (near field) or cell (P2M)
       const int r = gc % nrhs;
-      const long long cell = pair_src ? pair_src[unit] : unit;
-      col_src[tid] = static_cast<long long>(r) * N + cell * n;
-      col_out[tid] = out_rhs_stride > 0 ? r * out_rhs_stride + static_cast<long long>(unit) * ldo
-                                        : (static_cast<long long>(pair_base) * nrhs + gc) * ldo;
+      if (orbit) {
+        const int v = gc / nrhs;  // the v-th image of the orbit with a mode
+        int q = -1, g = 0;
+        for (int i = 0, cnt = 0; i < 8; ++i) {
+          const int qi = items[static_cast<long long>(s) * 8 + i];
+          if (qi < 0) continue;
+          if (cnt++ == v) {
+            q = qi;
+            g = items[(n_items + s) * 8 + i];
+            break;
+          }
+        }
+        col_src[tid] = static_cast<long long>(r) * N + static_cast<long long>(q) * n;
+        col_out[tid] = r * out_rhs_stride + static_cast<long long>(q) * ldo;
+        col_g[tid] = g;
+      } else {
+        const int unit = pair_base + gc / nrhs;  // pair (near field) or cell (P2M)
+        const long long cell = pair_src ? pair_src[unit] : unit;
+        col_src[tid] = static_cast<long long>(r) * N + cell * n;
+        col_out[tid] = out_rhs_stride > 0 ? r * out_rhs_stride + static_cast<long long>(unit) * ldo
+                                          : (static_cast<long long>(pair_base) * nrhs + gc) * ldo;
+        col_g[tid] = gsym;
+      }
     } else {
       col_src[tid] = -1;
       col_out[tid] = -1;
+      col_g[tid] = 0;
     }
   }
   __syncthreads();
@@ -191,8 +218,9 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
 #pragma unroll
     for (int i = 0; i < (BN * BK) / THREADS; ++i) {
       const long long src_off = col_src[b_c + i * (THREADS / BK)];
+      const int g = col_g[b_c + i * (THREADS / BK)];  // B rows gathered through P_g
       const bool ok = src_off >= 0 && (k0 + b_k) < K;
-      const c64* src = ok ? x + src_off + (pk ? __ldg(pk + k0 + b_k) : k0 + b_k) : x;
+      const c64* src = ok ? x + src_off + (g ? __ldg(perm + static_cast<size_t>(g - 1) * K + k0 + b_k) : k0 + b_k) : x;
       const unsigned dst = smem_b + sizeof(c64) * (stage * BN * BP + i * (THREADS / BK) * BP);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
     }
@@ -202,9 +230,9 @@ near_gemm_dmma_kernel(const c64* __restrict__ A, long long a_stride, int lda, in
   // 1 -> 32 columns (16 x 16), 2 -> 16 columns (8 x 16): narrow tiles keep
   // all 8 warps busy instead of idling most of them
   switch (cls) {
-    case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, pk); break;
-    case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, pk); break;
-    default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, pk); break;
+    case 0: gemm_main<4, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, col_g, perm); break;
+    case 1: gemm_main<2, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, col_g, perm); break;
+    default: gemm_main<1, 2>(As, Bs, load_stage, nk, warp, lane, ncols, m0, M, col_out, out, col_g, perm); break;
   }
 }
 
@@ -570,7 +598,8 @@ near_reduce_l2p_kernel(const c64* __restrict__ W, const int* __restrict__ tgt_pt
 
 cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, const c64* x, c64* out, int ldo,
                               const int* pair_src, const int4* jobs, int n_jobs, int K, int n, long long N, int nrhs,
-                              cudaStream_t stream, long long out_rhs_stride, const int* perm) {
+                              cudaStream_t stream, long long out_rhs_stride, const int* perm, const int* items,
+                              long long n_items) {
   static std::atomic<unsigned long long> configured{0};
   cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&near_gemm_dmma_kernel),
                                   static_cast<int>(kSmemA + kSmemB));
@@ -581,7 +610,8 @@ cudaError_t launch_block_gemm(const c64* A, long long a_stride, int lda, int M, 
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   dim3 grid(static_cast<unsigned>(ctas));
   near_gemm_dmma_kernel<<<grid, THREADS, kSmemA + kSmemB, stream>>>(A, a_stride, lda, M, x, out, ldo, pair_src, jobs,
-                                                                    K, n, N, nrhs, out_rhs_stride, perm);
+                                                                    K, n, N, nrhs, out_rhs_stride, perm, items,
+                                                                    n_items);
   return cudaGetLastError();
 }
 

@@ -134,3 +134,64 @@ def test_slab_plan_refuses_the_direct_path():
         op.set_slabs(None)
     with pytest.raises(RuntimeError, match="slab plan"):
         op.slab_rows()
+
+
+def test_slab_graph_replay_equals_eager_product():
+    """the slab product replayed as CUDA graphs (the default with no or an NCCL
+    communicator) equals the eager launch sequence bitwise (stage timing runs
+    the eager path), for host and device pointers, repeatedly"""
+    torch = pytest.importorskip("torch")
+    from paper_2201_12050_b200 import FmmOperators, Scene
+
+    sc = Scene(3, 2)
+    d = sc.assemble_fmm(4)
+    op = FmmOperators(d, near_path="lattice")
+    op.set_slabs(None)
+    p = uvec(np.random.default_rng(5), d.N)
+    y_graph = op.matvec_slab(p)
+    op.enable_stage_timing(True)
+    y_eager = op.matvec_slab(p)
+    op.enable_stage_timing(False)
+    assert np.array_equal(y_graph, y_eager)
+    xd = torch.from_numpy(p).cuda()
+    for _ in range(3):
+        assert np.array_equal(op.matvec_slab(xd).cpu().numpy(), y_graph)
+    assert rel(y_graph, O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_simulated_communicator_counts_the_exchange(P):
+    """fpbem_cu_comm_simulated: rank r of P alone on one GPU. Its two exchanges
+    per product send exactly the bytes of the slab plan — forward: its planes
+    of the other ranks' columns; backward: the other ranks' planes of its
+    columns; both lattices (n values per near-field column entry, b per
+    far-field one) — and its partial product stays finite. 3 ranks on the
+    4 planes of a 4 x 4 x 4 lattice leave one rank without planes."""
+    from paper_2201_12050_b200 import FmmOperators, Scene
+    from paper_2201_12050_b200.fmm import SimulatedCommunicator
+
+    sc = Scene(3, 2)
+    d = sc.assemble_fmm(4)
+    op = FmmOperators(d, near_path="lattice")
+    Ln = op.near_path()[1]
+    Lf = op.far_info()[0]
+    n, b, Mz = d.n_dof, d.n_coef, d.counts[2]
+    Cn, Cf = Ln[0] * Ln[1], Lf[0] * Lf[1]
+    for r in range(P):
+        comm = SimulatedCommunicator(0, P, r)
+        op.set_slabs(comm)
+        info = op.slab_info()
+        assert info["rank"] == r and info["ranks"] == P and info["axis"] == 2
+        lo, hi = op.slab_rows()
+        assert hi - lo == info["planes"] * d.counts[0] * d.counts[1] * n
+        comm.traffic(reset=True)
+        y = op.matvec_slab(uvec(np.random.default_rng(r), d.N)[lo:hi])
+        assert np.isfinite(y).all()
+        sent, exchanges = comm.traffic(reset=True)
+        assert exchanges == 2  # one grouped exchange per direction
+        cn, cf, pl = info["near_modes"] // Ln[2], info["far_modes"] // Lf[2], info["planes"]
+        fwd = pl * ((Cn - cn) * n + (Cf - cf) * b)
+        bwd = (Mz - pl) * (cn * n + cf * b)
+        assert sent == 16 * (fwd + bwd)
+        op.set_slabs(None)
+        comm.close()
