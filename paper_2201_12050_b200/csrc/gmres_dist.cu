@@ -77,20 +77,30 @@ DistOut gmres_dist(fpbem_cu_op* op, const c64* b, bool b_host, c64* x, bool x_ho
   if (m + 1 >= kCgsMaxCols) fail(FPBEM_CU_EINVAL, "gmres_dist: restart must be < " + std::to_string(kCgsMaxCols - 1));
   DistOut rep;
 
-  std::vector<void*> owned;  // device buffers scoped to the call
-  struct Free {
-    std::vector<void*>& v;
-    ~Free() {
-      for (void* p : v) cudaFree(p);
-    }
-  } free_all{owned};
-  auto alloc = [&](size_t bytes, const char* what) {
-    void* p = nullptr;
-    check(cudaMalloc(&p, bytes ? bytes : 1), what);
-    owned.push_back(p);
+  // the solver's device buffers live in one arena kept with the handle between
+  // solves (the basis alone is (restart + 1) slabs; allocating and freeing it per
+  // call cost more than a short solve)
+  const size_t vb = static_cast<size_t>(ns) * sizeof(c64);
+  const size_t cols_ = static_cast<size_t>(m) + 2;
+  auto round256 = [](size_t b) { return (std::max<size_t>(b, 1) + 255) & ~static_cast<size_t>(255); };
+  const size_t arena_parts[] = {vb * (m + 1), vb, vb, vb, vb, static_cast<size_t>(nfull) * sizeof(c64),
+                                static_cast<size_t>(nfull) * sizeof(c64), (2 * cols_ + 4) * sizeof(c64),
+                                cols_ * kCgsMaxBlocks * sizeof(c64), sizeof(unsigned)};
+  size_t arena = 0;
+  for (size_t b : arena_parts) arena += round256(b);
+  if (op->dws_bytes < arena) {
+    if (op->dws) check(cudaFree(op->dws), "dist workspace");
+    op->dws = nullptr;
+    op->dws_bytes = 0;
+    check(cudaMalloc(&op->dws, arena), "dist workspace");
+    op->dws_bytes = arena;
+  }
+  size_t arena_off = 0;
+  auto alloc = [&](size_t bytes, const char*) {
+    void* p = static_cast<char*>(op->dws) + arena_off;
+    arena_off += round256(bytes);
     return p;
   };
-  const size_t vb = static_cast<size_t>(ns) * sizeof(c64);
   c64* V = static_cast<c64*>(alloc(vb * (m + 1), "dist basis"));
   c64* xl = static_cast<c64*>(alloc(vb, "dist x"));
   c64* bl = static_cast<c64*>(alloc(vb, "dist b"));
