@@ -657,7 +657,10 @@ bool cellwise_on() {
 void far_field(fpbem_cu_op* op, const c64* x, int nrhs, cudaStream_t a) {
   Nvtx range("far field (P2M + M2L)");
   ev_record(op, 2, a);
-  if (cellwise_on() && cellwise_supported(op->b, op->n))  // M_c = V0 p_c: V0[m][k] = v0t[m n + k]
+  // the per-cell DMMA GEMM stages V0 in shared memory per CTA: it pays with enough cells to
+  // fill the GPU (cfg1's 8 cells: 16 us against the FMA kernel's few)
+  if (cellwise_on() && cellwise_supported(op->b, op->n) &&
+      static_cast<long long>(op->n_cells) * nrhs >= 2LL * device_sms())  // M_c = V0 p_c: V0[m][k] = v0t[m n + k]
     check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, op->N, op->n, op->mom, op->b,
                           static_cast<long long>(nrhs) * op->b, nrhs, static_cast<long long>(op->n_cells) * nrhs,
                           false, a),

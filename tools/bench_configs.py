@@ -163,7 +163,10 @@ def run_config(cid, args, out):
                        "final_estimate": rep.residual_history[-1] if rep.residual_history else None})
     g = {"config": f"cfg{cid}", "gmres": "tol 1e-6 restart 50" + (" (64 RHS lockstep batch)" if cid == 5 else ""),
          "max_iter": args.max_iter, "solves": solves if len(solves) <= 4 else None,
-         "n_solves": len(solves), "total_solve_s": time.perf_counter() - t_all,
+         "n_solves": len(solves),
+         # the solve calls only (cfg5: one lockstep batch); host RHS assembly and the warm-up excluded
+         "total_solve_s": solves[0]["solve_s"] if cid == 5 else sum(s["solve_s"] for s in solves),
+         "wall_incl_rhs_assembly_s": time.perf_counter() - t_all,
          "iterations_min_max": [min(s["iterations"] for s in solves), max(s["iterations"] for s in solves)],
          "all_converged": all(s["converged"] for s in solves)}
     # capped-iteration GMRES parity at full size (the oracle's full solve is hours on a CPU)
