@@ -654,13 +654,18 @@ bool cellwise_on() {
 
 // Far field of one product: P2M (events 2-3) and M2L into op->loc (events 3-4);
 // the Hankel image pair adds the K_hat term (src/fmm.cpp:256-263)
+// P2M as the per-cell DMMA GEMM (V0 staged in shared memory per CTA) when there are
+// enough cells to fill the GPU (cfg1's 8 cells: 16 us against the FMA kernel's 8);
+// every product of a handle makes the same choice (same arithmetic, same bits)
+bool p2m_cellwise(const fpbem_cu_op* op, int nrhs) {
+  return cellwise_on() && cellwise_supported(op->b, op->n) &&
+         static_cast<long long>(op->n_cells) * nrhs >= 2LL * device_sms();
+}
+
 void far_field(fpbem_cu_op* op, const c64* x, int nrhs, cudaStream_t a) {
   Nvtx range("far field (P2M + M2L)");
   ev_record(op, 2, a);
-  // the per-cell DMMA GEMM stages V0 in shared memory per CTA: it pays with enough cells to
-  // fill the GPU (cfg1's 8 cells: 16 us against the FMA kernel's few)
-  if (cellwise_on() && cellwise_supported(op->b, op->n) &&
-      static_cast<long long>(op->n_cells) * nrhs >= 2LL * device_sms())  // M_c = V0 p_c: V0[m][k] = v0t[m n + k]
+  if (p2m_cellwise(op, nrhs))  // M_c = V0 p_c: V0[m][k] = v0t[m n + k]
     check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, x, op->N, op->n, op->mom, op->b,
                           static_cast<long long>(nrhs) * op->b, nrhs, static_cast<long long>(op->n_cells) * nrhs,
                           false, a),
@@ -864,7 +869,7 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
     const long long z0 = z0_of(c), z1 = z0_of(c + 1);
     const long long c0 = z0 * My * Mx, nc = (z1 - z0) * My * Mx;  // the slab's cells
     check(cudaStreamWaitEvent(a, op->pev_in[c], 0), "pipeline far");
-    if (cellwise_on() && cellwise_supported(op->b, op->n))  // M_c = V0 p_c (src/fmm.cpp:256-259)
+    if (p2m_cellwise(op, 1))  // M_c = V0 p_c (src/fmm.cpp:256-259), as far_field decides
       check(launch_cellwise(op->v0t, op->n, 1, op->b, op->n, op->xin + c0 * n, op->N, op->n, op->mom + c0 * op->b,
                             op->b, op->b, 1, nc, false, a),
             "p2m");
