@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(32 * (NW + 2), 1)
 near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items, long long n_items,
                      const int* __restrict__ perm, const c64* __restrict__ xh, c64* __restrict__ yh, int n,
                      long long t_lo, long long t_hi, long long q_stride, int nrhs, int ncols, int KC, int ring,
-                     int rsplit) {
+                     int rsplit, int nxb) {
   // work unit u = (stored block t, row part h): rsplit parts of the block's row
   // tiles per block, so that few blocks (a slab rank's share) still fill every SM
   extern __shared__ __align__(128) unsigned char mm_smem[];
@@ -377,7 +377,7 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
   c64* As = reinterpret_cast<c64*>(mm_smem);
   c64* Xs = As + static_cast<size_t>(ring) * KC * AP;  // two X buffers of 8 columns
   // barriers: full[ring], empty[ring], xfull[2], xempty[2]
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Xs + 2 * 8 * XP);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Xs + nxb * 8 * XP);  // nxb X buffers
   __shared__ int iq[2][8], ig[2][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + ring), xfull0 = smem_u32(bars + 2 * ring),
@@ -411,8 +411,8 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
     for (long long u = u_lo + blockIdx.x; u < u_hi; u += gridDim.x, ++it) {
       const long long t = u / rsplit;
       // X[c][k] = xh[r][q_img][P_g k] into X buffer it & 1, 16-byte cp.async per element
-      const int xb = it & 1;
-      if (it >= 2) mbar_wait(xempty0 + 8 * xb, ((it >> 1) - 1) & 1);
+      const int xb = it % nxb;
+      if (it >= nxb) mbar_wait(xempty0 + 8 * xb, ((it / nxb) - 1) & 1);
       int q8 = -1, g8 = 0;
       if (lane < 8) {
         q8 = items[t * 8 + lane];
@@ -485,8 +485,8 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
     int m0, m1;
     part_rows(u, &m0, &m1);
     const int n_mt = m1 - m0;  // this unit's row tiles; the ring holds rows 8 m0 ..
-    const int xb = it & 1;
-    mbar_wait(xfull0 + 8 * xb, (it >> 1) & 1);
+    const int xb = it % nxb;
+    mbar_wait(xfull0 + 8 * xb, (it / nxb) & 1);
     const c64* xs = Xs + xb * 8 * XP + fr * XP + fk;
 
     double t1[MT][2], t2[MT][2], t3[MT][2];
@@ -654,6 +654,17 @@ cudaError_t launch_mode_gemv(const c64* shat, const int* items, long long n_item
 // stored block: consumer warps, k columns per ring stage, ring depth and the
 // dynamic shared memory; false when it does not apply (n % 8, > 8 columns,
 // more than 8 row tiles per warp, or no 2-stage ring fits).
+// X (image-column) buffers of the mode product: 2 lets the gather of the next block's
+// columns run under the current block; 1 frees 41 KB (n = 320) for one more ring
+// stage of the block stream (FPBEM_MMA_XBUF=1|2, A/B)
+int mode_mma_xbufs() {
+  static const int xb = [] {
+    const char* v = std::getenv("FPBEM_MMA_XBUF");
+    return (v && std::atoi(v) == 1) ? 1 : 2;
+  }();
+  return xb;
+}
+
 bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem) {
   if (n <= 0 || n % 8 || ncols < 1 || ncols > 8) return false;
   // consumer warps of up to 8 row tiles each (n <= 512; larger blocks keep the
@@ -675,15 +686,16 @@ bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem)
     return (k == 4 || k == 8 || k == 16) ? k : 8;
   }();
   const int KC = kc_env;
+  const int XB = mode_mma_xbufs();
   const size_t stage = sizeof(c64) * KC * static_cast<size_t>(n + 2);
-  const size_t fixed = 2 * sizeof(c64) * 8 * static_cast<size_t>(n + 4) + 4 * 8 * 16 + 128;
+  const size_t fixed = XB * sizeof(c64) * 8 * static_cast<size_t>(n + 4) + 4 * 8 * 16 + 128;
   const size_t budget = static_cast<size_t>(kMaxDynSmem) - 1024;  // the kernel's static shared memory
   if (fixed + 2 * stage > budget) return false;
   const int R = static_cast<int>(std::min<size_t>(16, (budget - fixed) / stage));
   *nw = NW;
   *kc = KC;
   *ring = R;
-  *smem = sizeof(c64) * (static_cast<size_t>(R) * KC * (n + 2) + 2 * 8 * static_cast<size_t>(n + 4)) +
+  *smem = sizeof(c64) * (static_cast<size_t>(R) * KC * (n + 2) + XB * 8 * static_cast<size_t>(n + 4)) +
           sizeof(unsigned long long) * (2 * R + 4);
   return true;
 }
@@ -711,7 +723,7 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   const int MT = ((n / 8 + rsplit - 1) / rsplit + NW - 1) / NW;
   static std::atomic<unsigned long long> raised[18];
   using K = void (*)(const c64*, const int*, long long, const int*, const c64*, c64*, int, long long, long long,
-                     long long, int, int, int, int, int);
+                     long long, int, int, int, int, int, int);
   static const K fns[18] = {near_mode_mma_kernel<1, 8>,  near_mode_mma_kernel<2, 8>,  near_mode_mma_kernel<3, 8>,
                             near_mode_mma_kernel<4, 8>,  near_mode_mma_kernel<5, 8>,  near_mode_mma_kernel<6, 8>,
                             near_mode_mma_kernel<7, 8>,  near_mode_mma_kernel<8, 8>,  near_mode_mma_kernel<1, 10>,
@@ -725,7 +737,7 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   const long long units = n_blk * rsplit;
   const int grid = static_cast<int>(std::min<long long>(units, sms));
   fns[which]<<<grid, 32 * (NW + 2), smem, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, t_hi, q_stride,
-                                                     nrhs, ncols, KC, R, rsplit);
+                                                     nrhs, ncols, KC, R, rsplit, mode_mma_xbufs());
   return cudaGetLastError();
 }
 
