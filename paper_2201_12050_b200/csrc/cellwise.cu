@@ -14,6 +14,8 @@
 //     (deterministic);
 //   * Gauss 3-multiplication complex product (3 DMMAs per complex 8x8x4 tile).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -173,6 +175,70 @@ cellwise_gemm_kernel(const c64* __restrict__ a, long long a_ms, long long a_ks, 
   }
 }
 
+// The same product with no shared-memory staging of the columns and no block-wide
+// barrier in the loop: the CTA's warps form G = 16 / MT groups of MT warps (one
+// 8-row tile of A each); every group walks its own chunks of 8 columns over the
+// whole k range, loading its B fragments straight from global memory 8 k steps
+// ahead (the group's warps read the same fragments: L1 hits after the first).
+// The barrier-per-chunk form above ran only ~3.5 chunks per CTA on cfg3 and was
+// bound by the chunk latency (29 us for 21 MB of input).
+__global__ void __launch_bounds__(kCwWarps * 32, 1)
+cellwise_stream_kernel(const c64* __restrict__ a, long long a_ms, int M, int K, const c64* __restrict__ in,
+                       long long in_rs, long long in_cs, c64* __restrict__ out, long long out_rs, long long out_cs,
+                       int nrhs, long long ncols) {
+  extern __shared__ __align__(16) unsigned char cw_raw[];
+  const int KP = cw_pitch(K), MT = (M + 7) / 8, KS = (K + 3) / 4;
+  c64* As = reinterpret_cast<c64*>(cw_raw);  // [M][KP], rows contiguous in global (a_ks = 1)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
+  for (int e = tid; e < M * KP; e += blockDim.x) {
+    const int m = e / KP, k = e - m * KP;
+    cp_async16(As + e, a + (k < K ? m * a_ms + k : 0), k < K);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int G = kCwWarps / MT, grp = warp / MT, mt = warp % MT;
+  if (grp >= G) return;
+  const int m = mt * 8 + fr;
+  const c64* arow = As + (m < M ? m : 0) * KP + fk;
+  const long long chunks = (ncols + 7) / 8;
+  constexpr int U = 16;  // k steps of B fragments in flight
+  for (long long ch = static_cast<long long>(blockIdx.x) * G + grp; ch < chunks;
+       ch += static_cast<long long>(gridDim.x) * G) {
+    const long long col = ch * 8 + fr;  // this lane's B column
+    const bool cok = col < ncols;
+    const long long cell = cok ? col / nrhs : 0, r = cok ? col - cell * nrhs : 0;
+    const c64* bcol = in + r * in_rs + cell * in_cs + fk;
+    double t1[2][2] = {}, t2[2][2] = {}, t3[2][2] = {};
+    for (int s0 = 0; s0 < KS; s0 += U) {
+      c64 bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = 4 * (s0 + u) + fk;
+        bv[u] = (cok && s0 + u < KS && k < K) ? __ldg(bcol + 4 * (s0 + u)) : cmk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (s0 + u >= KS) break;
+        const int h = u & 1;
+        const c64 av = m < M ? arow[4 * (s0 + u)] : cmk(0.0, 0.0);
+        dmma884(t1[h][0], t1[h][1], av.x, bv[u].x);
+        dmma884(t2[h][0], t2[h][1], av.y, bv[u].y);
+        dmma884(t3[h][0], t3[h][1], av.x + av.y, bv[u].x + bv[u].y);
+      }
+    }
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const long long oc = ch * 8 + 2 * fk + j;
+      if (oc >= ncols) continue;
+      const double a1 = t1[0][j] + t1[1][j], a2 = t2[0][j] + t2[1][j], a3 = t3[0][j] + t3[1][j];
+      const long long ocell = oc / nrhs, orr = oc - ocell * nrhs;
+      out[orr * out_rs + ocell * out_cs + m] = cmk(a1 - a2, a3 - a1 - a2);
+    }
+  }
+}
+
 size_t cw_smem(int M, int K) {
   const size_t KP = cw_pitch(K);
   return sizeof(c64) * (static_cast<size_t>(M) * KP + 2 * 8 * KP + static_cast<size_t>(kCwWarps) * 32 * 2);
@@ -194,6 +260,22 @@ cudaError_t launch_cellwise(const c64* a, long long a_ms, long long a_ks, int M,
   cudaError_t e = ensure_max_smem(raised, reinterpret_cast<const void*>(&cellwise_gemm_kernel<1>), kMaxDynSmem);
   if (e != cudaSuccess) return e;
   const long long chunks = (ncols + 7) / 8;
+  // FPBEM_CELLWISE_V1=1: the staged, barrier-per-chunk form (A/B)
+  static const bool v1 = [] {
+    const char* v = std::getenv("FPBEM_CELLWISE_V1");
+    return v && std::strcmp(v, "1") == 0;
+  }();
+  if (!v1 && a_ks == 1 && !accumulate) {
+    static std::atomic<unsigned long long> raised2{0};
+    e = ensure_max_smem(raised2, reinterpret_cast<const void*>(&cellwise_stream_kernel), kMaxDynSmem);
+    if (e != cudaSuccess) return e;
+    const int G = kCwWarps / ((M + 7) / 8);
+    const int grid = static_cast<int>(std::min<long long>((chunks + G - 1) / G, device_sms()));
+    const size_t smem_s = sizeof(c64) * static_cast<size_t>(M) * cw_pitch(K);
+    cellwise_stream_kernel<<<grid, kCwWarps * 32, smem_s, stream>>>(a, a_ms, M, K, in, in_rs, in_cs, out, out_rs,
+                                                                     out_cs, nrhs, ncols);
+    return cudaGetLastError();
+  }
   // persistent: one CTA per SM (A fills most of the shared memory)
   const int grid = static_cast<int>(std::min<long long>(chunks, device_sms()));
   cellwise_gemm_kernel<1><<<grid, kCwWarps * 32, smem, stream>>>(a, a_ms, a_ks, M, K, in, in_rs, in_cs, out, out_rs,
