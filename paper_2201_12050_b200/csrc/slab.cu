@@ -384,7 +384,10 @@ bool slab_xy(const SlabPlan* sp, const SlabSide& sd) {
   }();
   const int mx = static_cast<int>(sp->mx), my = static_cast<int>(sp->my);
   const int cx = static_cast<int>(sd.cx), cy = static_cast<int>(sd.cy);
-  return env && sd.cx > 1 && sd.cy > 1 && sp->ms * sd.E <= 0x7fffffffLL &&
+  // the near side (E = n, hundreds of inner values) only for a few planes per rank: its
+  // per-(plane, field) CTAs read n-strided values, which the axis passes beat from ~8
+  // planes on (cfg3 at 2 ranks: 0.298 -> 0.286 ms with axis passes; 4, 8 ranks: the plane kernel)
+  return env && sd.cx > 1 && sd.cy > 1 && sp->ms * sd.E <= 0x7fffffffLL && (sd.E <= 64 || sp->ms <= 4) &&
          xy_plane_smem(mx, my, cx, cy, false) <= 200 * 1024 && xy_plane_smem(mx, my, cx, cy, true) <= 200 * 1024;
 }
 
@@ -421,16 +424,18 @@ const c64* local_forward(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64*
 }
 
 // inverse of local_forward from the unpacked planes `in` into `out`
-void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* out, c64* const* tw,
-                   cudaStream_t s, c64* spare) {
-  if (sp->ms == 0) return;
+// fuse_loc (near side): the L2P y += U0 L fused into the last (x) pass as its DMMA epilogue,
+// after `join` (the far side's locals); returns whether it was fused
+bool local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c64* out, c64* const* tw,
+                   cudaStream_t s, c64* spare, const c64* fuse_loc = nullptr, cudaEvent_t join = nullptr) {
+  if (sp->ms == 0) return false;
   if (slab_xy(sp, sd)) {
     check(launch_xy_plane(in, out, tw[0], tw[1], static_cast<int>(sp->mx), static_cast<int>(sp->my),
                           static_cast<int>(sd.cx), static_cast<int>(sd.cy), static_cast<int>(sp->ms), sd.E, true, 1.0,
                           s),
           "slab inverse xy dft");
     op->launches++;
-    return;
+    return false;
   }
   const c64* cur = in;
   c64* tmp = spare;
@@ -444,12 +449,22 @@ void local_inverse(fpbem_cu_op* op, SlabPlan* sp, SlabSide& sd, const c64* in, c
     cur = dst;
     op->launches++;
   }
+  bool fused = false;
   if (sd.cx > 1) {
-    check(launch_dft_axis(cur, out, tw[0], sp->my * sp->ms, static_cast<int>(sd.cx), static_cast<int>(sp->mx), sd.E,
-                          static_cast<int>(sd.cx), true, 1.0, s),
-          "slab inverse dft x");
+    if (fuse_loc && dft_l2p_supported(static_cast<int>(sd.cx), static_cast<int>(sp->mx), op->b)) {
+      check(cudaStreamWaitEvent(s, join, 0), "slab join");
+      check(launch_dft_axis_l2p(cur, out, tw[0], sp->my * sp->ms, static_cast<int>(sd.cx), static_cast<int>(sp->mx),
+                                sd.E, static_cast<int>(sd.cx), 1.0, op->u0, fuse_loc, op->b, 1, s),
+            "slab inverse dft x + l2p");
+      fused = true;
+    } else {
+      check(launch_dft_axis(cur, out, tw[0], sp->my * sp->ms, static_cast<int>(sd.cx), static_cast<int>(sp->mx),
+                            sd.E, static_cast<int>(sd.cx), true, 1.0, s),
+            "slab inverse dft x");
+    }
     op->launches++;
   }
+  return fused;
 }
 
 // stage timing of a slab product: [0] the two exchanges, [4] the whole
@@ -594,11 +609,15 @@ void slab_phase2(fpbem_cu_op* op, c64* y) {
   slab_fork(op);
   scatter_rows(fr.pack, f_local ? sp->fa : sp->loc, fr.idx, fr.n_idx, fr.E, a);
   if (f_local) local_inverse(op, sp, fr, sp->fa, sp->loc, op->tw, a, sp->fb);
+  check(cudaEventRecord(sp->join, a), "slab join");  // the far side's locals
   scatter_rows(nr.pack, n_local ? sp->a : y, nr.idx, nr.n_idx, nr.E, s);
-  if (n_local) local_inverse(op, sp, nr, sp->a, y, op->twn, s, sp->b);
-  slab_join(op);
-  check(launch_l2p_add(op->u0, sp->loc, y, op->n, op->b, static_cast<int>(cells), cells * op->n, 1, s), "slab l2p");
-  op->launches += 3;
+  const bool fused = n_local && local_inverse(op, sp, nr, sp->a, y, op->twn, s, sp->b, sp->loc, sp->join);
+  check(cudaStreamWaitEvent(s, sp->join, 0), "slab join");
+  if (!fused) {
+    check(launch_l2p_add(op->u0, sp->loc, y, op->n, op->b, static_cast<int>(cells), cells * op->n, 1, s), "slab l2p");
+    op->launches++;
+  }
+  op->launches += 2;
 }
 
 // y_loc = (A x)[this rank's planes] from x_loc = x[this rank's planes], one right-hand side
