@@ -461,19 +461,31 @@ def run_ours(args):
     n_cells = int(np.prod(data.counts))
     m2l_ms = per(stages_serial, "m2l") if not slabs else float("nan")
     lam_full = 16.0 * q * b * b
+    parity = op.far_parity()
+    # the flat Λ stream (single GPU, Lz > 1, <= 64 fields per mode) reads qz <= Lz/2 of half the columns
+    # when the spectrum has both parities; the fused z kernel (FPBEM_M2L_Z=fused, slabs) half of Λ
+    z_stream = (not slabs and fsz[2] > 1 and b <= 32 and b <= 64
+                and os.environ.get("FPBEM_M2L_Z") != "fused")
+    quad = z_stream and parity == 2 and os.environ.get("FPBEM_M2L_QUAD") != "0"
     lam_read = lam_full / 2 if paired else lam_full
+    if quad:
+        lam_read *= (fsz[2] // 2 + 1) / fsz[2]
     io = 2 * 16.0 * b * n_cells
     hbm, hbm_src = hbm_peak()
-    m2l_roof = {"stage": "M2L (x+y plane DFTs, z-DFT/mode-product pipeline, inverse)", "bound": "hbm",
+    m2l_roof = {"stage": ("M2L (x+y plane DFTs, z-DFT axis pass, flat Λ stream, inverse z pass, inverse x+y)"
+                          if z_stream else "M2L (x+y plane DFTs, z-DFT/mode-product pipeline, inverse)"),
+                "bound": "hbm",
                 "launch_ms": m2l_ms, "peak": hbm, "unit": "GB/s", "peak_source": hbm_src,
-                "lambda_paired": paired, "fft_sizes": list(fsz),
+                "lambda_paired": paired, "lambda_parity": parity, "z_form": "stream" if z_stream else "fused",
+                "modes_per_streamed_block": 4 if quad else (2 if paired else 1), "fft_sizes": list(fsz),
                 "compulsory_bytes": lam_read + io,
                 "achieved": (lam_read + io) / (m2l_ms * 1e-3) / 1e9,
                 "frac": (lam_read + io) / (m2l_ms * 1e-3) / 1e9 / hbm,
                 "survey_bytes": lam_full + io,
                 "frac_survey_definition": (lam_full + io) / (m2l_ms * 1e-3) / 1e9 / hbm,
-                "note": "compulsory = the Λ blocks an apply must read (half of q b^2 when mirror-paired) + moments "
-                        "in + locals out; survey = SURVEY §8d's 16 q b^2 + 2 x 16 b n_cells"}
+                "note": "compulsory = the Λ blocks this apply reads (half of q b^2 when mirror-paired, qz <= Lz/2 "
+                        "of those with the z-reflection parity) + moments in + locals out; survey = SURVEY §8d's "
+                        "16 q b^2 + 2 x 16 b n_cells, the stream the reference's algorithm reads"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(_WithNear(data, near.cpu().numpy()), xh)

@@ -219,7 +219,8 @@ int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out);
 /* Far-field M2L layout for roofline accounting: *paired = 1 when the spectrum's
  * mirror parity Λ(-q) = D Λ(q) D was verified and each Λ block is streamed once
  * for a mode and its mirror, so an apply reads about half of
- * q b^2 blocks. */
+ * q b^2 blocks; *paired = 2 when the reflection parity Λ(qx, qy, -qz) = Dz Λ(q) Dz
+ * holds as well and the flat stream reads about a quarter of them. */
 int fpbem_cu_far_info(const fpbem_cu_op* op, int* sizes, int* paired);
 
 /* Run subsequent device work on an external cudaStream_t (NULL = own stream). */

@@ -525,7 +525,8 @@ void ev_record(fpbem_cu_op* op, int i, cudaStream_t st) {
 // (src/structured.cpp:122-166), everything enqueued on `s`.
 struct M2lPass {
   int kind;  // 0 dft, 1 mode product, 2 fused z-dft + mode product + inverse z-dft,
-             // 3 / 4 forward / inverse x+y plane DFTs (one kernel each)
+             // 3 / 4 forward / inverse x+y plane DFTs (one kernel each),
+             // 5 the flat Λ stream in place on the z-extended field
   long long n_a;
   int n_in, n_out;
   long long inner;
@@ -546,7 +547,13 @@ std::vector<M2lPass> m2l_plan(fpbem_cu_op* op, int nrhs) {
   // z forward + mode product + z inverse fused into one kernel when the
   // column's fields fit in shared memory (FPBEM_M2L_FUSE=0 disables)
   static const char* fz = std::getenv("FPBEM_M2L_FUSE");
-  const bool fuse_z = Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
+  // the z stage as z-DFT axis passes around one flat Λ stream over all modes (kind 5) wherever the
+  // stream kernel applies; FPBEM_M2L_Z=fused keeps the per-column fused kernel (A/B, and the form
+  // the slab plan uses). Read per plan, not cached: the parity tests switch it within one process
+  const char* zenv = std::getenv("FPBEM_M2L_Z");
+  const bool z_stream_env = !(zenv && std::strcmp(zenv, "fused") == 0);
+  const bool z_stream = z_stream_env && Lz > 1 && mode_stream_ring(static_cast<int>(E), op->b) >= 2;
+  const bool fuse_z = !z_stream && Lz > 1 && !(fz && std::strcmp(fz, "0") == 0) &&
                       m2l_zfused_ring(static_cast<int>(Mz), static_cast<int>(Lz), static_cast<int>(E), op->b) > 0;
   // x and y together in shared memory per z-plane when the plane fits (FPBEM_M2L_XY=0: per-axis passes)
   static const int xy_env = [] {  // 0: per-axis passes; 2: plane kernels wherever they fit; else the rule below
@@ -580,7 +587,7 @@ std::vector<M2lPass> m2l_plan(fpbem_cu_op* op, int nrhs) {
   } else {
     if (Lz > 1)
       passes.push_back({0, 1, static_cast<int>(Mz), static_cast<int>(Lz), cy * cx * E, static_cast<int>(Lz), 2, false});
-    passes.push_back({1, 0, 0, 0, 0, 0, -1, false});
+    passes.push_back({z_stream ? 5 : 1, 0, 0, 0, 0, 0, -1, false});
     if (Lz > 1)
       passes.push_back({0, 1, static_cast<int>(Lz), static_cast<int>(Mz), Ly * Lx * E, static_cast<int>(Lz), 2, true});
   }
@@ -593,6 +600,12 @@ std::vector<M2lPass> m2l_plan(fpbem_cu_op* op, int nrhs) {
       passes.push_back({0, My * Mz, static_cast<int>(Lx), static_cast<int>(Mx), E, static_cast<int>(Lx), 0, true});
   }
   return passes;
+}
+
+// FPBEM_M2L_QUAD=0: the flat Λ stream without the z-reflection parity (A/B; read per call)
+bool zquad_on() {
+  const char* v = std::getenv("FPBEM_M2L_QUAD");
+  return !(v && std::strcmp(v, "0") == 0);
 }
 
 // M2L moments -> locals. xy_done: the first pass (the forward x+y plane DFTs,
@@ -621,6 +634,16 @@ void m2l_apply(fpbem_cu_op* op, int nrhs, cudaStream_t s, const c64* moments, co
                             static_cast<int>(Lx), static_cast<int>(Ly), static_cast<int>(Mz), static_cast<int>(E),
                             p.kind == 4, scale, s),
             "lattice xy dft");
+    } else if (p.kind == 5) {
+      // in place on the z-extended field the forward z pass just wrote (one of op->fa / op->fb)
+      const bool paired = lambda == op->lambda && op->lam_paired;
+      check(launch_mode_stream(const_cast<c64*>(cur), lambda, static_cast<int>(Lz), Ly * Lx, static_cast<int>(E),
+                               op->b, paired ? op->z_items_pair : op->z_items_single,
+                               paired ? op->n_z_items_pair : op->n_z_items_single, paired && op->lam_zsym && zquad_on(),
+                               s),
+            "mode stream");
+      op->launches++;
+      continue;
     } else if (p.kind == 1) {
       check(launch_mode_product(lambda, cur, out, op->q_total, op->b, nrhs, s), "mode product");
     } else if (p.kind == 2) {
@@ -1137,18 +1160,22 @@ int fpbem_cu_fmm_create(const fpbem_cu_fmm_desc* d, int device, fpbem_cu_op** ou
       h2d(op->z_items_single, singles.data(), singles.size() * sizeof(int2), op->stream, "z items");
       op->n_z_items_pair = static_cast<int>(pairs.size());
       op->n_z_items_single = static_cast<int>(singles.size());
-      // parity Λ(-q) = D Λ(q) D of the spectrum actually built (or handed over)
-      unsigned long long* dv = dalloc<unsigned long long>(2, "parity check");
+      // parities of the spectrum actually built (or handed over): Λ(-q) = D Λ(q) D, and the
+      // reflection Λ(qx, qy, -qz) = Dz Λ(q) Dz
+      unsigned long long* dv = dalloc<unsigned long long>(4, "parity check");
       std::unique_ptr<unsigned long long, decltype(&cudaFree)> keep_dv(dv, &cudaFree);
-      check(cudaMemsetAsync(dv, 0, 2 * sizeof(unsigned long long), op->stream), "parity check");
-      check(launch_lambda_parity(op->lambda, op->L, op->b, dv, op->stream), "parity check");
-      unsigned long long hv[2];
+      check(cudaMemsetAsync(dv, 0, 4 * sizeof(unsigned long long), op->stream), "parity check");
+      check(launch_lambda_parity(op->lambda, op->L, op->b, false, dv, op->stream), "parity check");
+      check(launch_lambda_parity(op->lambda, op->L, op->b, true, dv + 2, op->stream), "parity check");
+      unsigned long long hv[4];
       check(cudaMemcpyAsync(hv, dv, sizeof(hv), cudaMemcpyDeviceToHost, op->stream), "parity check");
       check(cudaStreamSynchronize(op->stream), "parity check");
-      double dev, amax;
+      double dev, amax, devz;
       std::memcpy(&dev, &hv[0], sizeof(double));
       std::memcpy(&amax, &hv[1], sizeof(double));
+      std::memcpy(&devz, &hv[2], sizeof(double));
       op->lam_paired = amax > 0.0 && dev <= 1e-12 * amax;
+      op->lam_zsym = op->lam_paired && devz <= 1e-12 * amax;
     }
     if (op->mirrored_level >= 0) {
       // spectrum of K_hat P: Toeplitz offsets o = idx with o[a] = idx[a] - (M_a - 1)
@@ -1307,7 +1334,7 @@ int fpbem_cu_spectrum(const fpbem_cu_op* op, int* sizes, fpbem_c64* lambda_out) 
 int fpbem_cu_far_info(const fpbem_cu_op* op, int* sizes, int* paired) {
   if (!op || !sizes || !paired) return FPBEM_CU_EINVAL;
   for (int k = 0; k < 3; ++k) sizes[k] = op->L[k];
-  *paired = op->lam_paired ? 1 : 0;
+  *paired = op->lam_zsym ? 2 : (op->lam_paired ? 1 : 0);  // 2: also the z-reflection parity
   return FPBEM_CU_OK;
 }
 

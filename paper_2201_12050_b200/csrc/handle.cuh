@@ -169,6 +169,7 @@ struct fpbem_cu_op {
   int2* z_items_single = nullptr;
   int n_z_items_pair = 0, n_z_items_single = 0;
   bool lam_paired = false;
+  bool lam_zsym = false;  // also Λ(qx, qy, -qz) = Dz Λ(q) Dz (the flat stream reads a quarter of Λ)
   int L[3] = {1, 1, 1};
   long long q_total = 1;
   c64* lambda = nullptr;

@@ -58,12 +58,18 @@ cudaError_t launch_mode_product(const c64* lambda, const c64* field, c64* image,
 // fused forward-z DFT + mode product + inverse-z DFT, one CTA per (qy, qx) column
 // ring depth (Λ mode blocks in shared memory) of the fused z kernel, 0 when
 // the column's fields leave no room for >= 4 (then the unfused passes run)
+// the flat Λ stream (in place on the z-extended field): ring slots, 0 when the shape is not supported
+int mode_stream_ring(int E, int b);
+// quad: the spectrum also has the z-reflection parity, units run over qz <= Lz/2 only
+cudaError_t launch_mode_stream(c64* field, const c64* lambda, int Lz, long long plane, int E, int b,
+                               const int2* items, int n_items, bool quad, cudaStream_t stream);
 int m2l_zfused_ring(int Mz, int Lz, int E, int b);
 cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const c64* tw, int Mz, int Lz,
                               long long plane, int E, int b, double scale, const int2* items, int n_items,
                               cudaStream_t stream);
 // Λ(-q) = D Λ(q) D check (D = diag((-1)^n)): out2[0] = max deviation, out2[1] = max |Λ|, as double bits
-cudaError_t launch_lambda_parity(const c64* lam, const int L[3], int b, unsigned long long* out2, cudaStream_t stream);
+cudaError_t launch_lambda_parity(const c64* lam, const int L[3], int b, bool zflip, unsigned long long* out2,
+                                 cudaStream_t stream);
 cudaError_t launch_mirror_permute(const c64* in, c64* out, const int counts[3], int level, long long E,
                                   cudaStream_t stream);
 cudaError_t launch_add(c64* acc, const c64* v, long long n, cudaStream_t stream);

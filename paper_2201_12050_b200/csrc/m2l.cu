@@ -1075,6 +1075,229 @@ m2l_zpipe_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* _
   __syncthreads();  // the producer stays resident until every copy it issued has landed
 }
 
+// The per-mode products of the far field as ONE FLAT STREAM over Λ, in place on
+// the z-extended field (the unfused form of the z kernel above: the z-DFTs run
+// as axis passes before and after, and the 2 x 13 MB field of cfg3 stays in the
+// 126 MB L2). Unit u = qz * n_items + k: the Λ block of mode qz of column
+// c = items[k].x, used for every mode whose block it determines
+// (src/structured.cpp:148-152, one block read for up to four modes):
+//   (qz, c)     Λ
+//   (-qz, c')   D Λ D          c' = items[k].y the mirror column, D = diag((-1)^n)
+//                              (Λ(-q) = D Λ(q) D, the pairing of the z kernel)
+//   (-qz, c)    Dz Λ Dz        quad only: Dz = diag((-1)^(n+m)), the reflection z -> -z
+//   (qz, c')    (D Dz) Λ (Dz D)   (K(Rz δ) = Dz K(δ) Dz and far offsets symmetric in z;
+//                              checked on the spectrum actually built, lambda_parity_kernel)
+// so quad streams only qz <= Lz/2: a quarter of Λ. The signs are applied to the
+// vectors when they are staged and when they are written back; the products
+// themselves share every Λ load (mode_multi). CTA c takes the units c, c + G,
+// c + 2G, ...: at any time the CTAs read neighbouring blocks, the access order
+// that reached the copy bandwidth in the stream probe (profiles/r01_m2l_probes.md;
+// the per-column walk of the fused kernel ran at 4 TB/s). Warp 0 lane 0 is the
+// producer (one cp.async.bulk per block into a ring, full / empty mbarriers);
+// consumer warp w takes the CTA's units j = w (mod n_w): the fields of its next
+// unit are loaded into registers before the wait on the current block, staged
+// in a warp-private shared buffer, multiplied in place and written back coalesced.
+// ring is a multiple of n_w, so a slot's successive blocks go to ONE warp in
+// order: it waits for a slot's phase only after it consumed the phase before
+// (a parity wait two phases ahead would pass at once on the stale phase).
+constexpr int kStreamWarps = 11;  // most consumer warps (12 warps with the producer: 168 registers each)
+constexpr int kStreamMaxRing = 32;
+constexpr int kStreamRegs = 2;  // E <= 32 * kStreamRegs
+
+// s[v] <- Λ s[v] for NV staged vectors of E = nrhs x b fields (b <= 32: one output per lane)
+template <int NV>
+__device__ __forceinline__ void mode_multi(const c64* __restrict__ lam_blk, c64* __restrict__ s0, int E, int b,
+                                           int lane) {
+  const c64* lam = lam_blk + (lane < b ? lane : 0);
+  for (int r0 = 0; r0 < E; r0 += b) {
+    c64 a0[NV], a1[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) a0[v] = a1[v] = cmk(0.0, 0.0);
+    int c = 0;
+    for (; c + 2 <= b; c += 2) {
+      const c64 l0 = lam[c * b], l1 = lam[(c + 1) * b];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const c64* x = s0 + v * E + r0 + c;
+        a0[v] = cfma(l0, x[0], a0[v]);
+        a1[v] = cfma(l1, x[1], a1[v]);
+      }
+    }
+    if (c < b) {
+      const c64 l0 = lam[c * b];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) a0[v] = cfma(l0, s0[v * E + r0 + c], a0[v]);
+    }
+    __syncwarp();  // every lane has read this right-hand side's inputs
+    if (lane < b) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) s0[v * E + r0 + lane] = cadd(a0[v], a1[v]);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(32 * (1 + kStreamWarps), 1)
+mode_stream_kernel(c64* __restrict__ field, const c64* __restrict__ lambda, int Lz, int qz_count, long long plane,
+                   int E, int b, int ring, const int2* __restrict__ items, int n_items, int quad, int probe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b2 = b * b;
+  c64* ring_buf = reinterpret_cast<c64*>(smem_raw);  // ring x b2
+  c64* stage0 = ring_buf + ring * b2;                 // [warp][4][E]
+  __shared__ double sgn[4][32];  // sign of coefficient i under: none, D, Dz, D Dz
+  __shared__ __align__(8) unsigned long long full[kStreamMaxRing], empty[kStreamMaxRing];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_w = (blockDim.x >> 5) - 1;  // consumer warps; ring % n_w == 0
+  const long long total = static_cast<long long>(n_items) * qz_count;
+  const int n_units = static_cast<int>((total - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  if (tid == 0) {
+    for (int s = 0; s < ring; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_fence_init();
+  }
+  if (tid < 32) {  // coefficient i = n^2 + n + m: (-1)^n, (-1)^(n+m) = (-1)^(i - n^2)
+    int n = 0;
+    while ((n + 1) * (n + 1) <= tid) ++n;
+    const double d = (n & 1) ? -1.0 : 1.0, dz = ((tid - n * n) & 1) ? -1.0 : 1.0;
+    sgn[0][tid] = 1.0;
+    sgn[1][tid] = d;
+    sgn[2][tid] = dz;
+    sgn[3][tid] = d * dz;
+  }
+  __syncthreads();
+  const unsigned g = gridDim.x, ni = static_cast<unsigned>(n_items);
+  if (warp == 0) {
+    // ---- producer (lane 0): the items[] load and index arithmetic of one unit take longer than
+    // its 10 KB copy takes to stream, so the block addresses are looked up four units ahead
+    // of the copies (four independent loads in flight while four copies are issued)
+    if (lane == 0) {
+      const unsigned lam_bytes = static_cast<unsigned>(b2 * sizeof(c64));
+      auto lookup = [&](int j) -> long long {  // element offset of unit j's Λ block (units < 2^31)
+        if (j >= n_units) return 0;
+        const unsigned u = blockIdx.x + static_cast<unsigned>(j) * g;
+        const unsigned qz = u / ni, k = u - qz * ni;
+        return (static_cast<long long>(qz) * plane + items[k].x) * b2;
+      };
+      long long nxt[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) nxt[i] = lookup(i);
+      int slot = 0;
+      unsigned phase = 0;
+      for (int j0 = 0; j0 < n_units; j0 += 4) {
+        long long cur[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) nxt[i] = lookup(j0 + 4 + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (j0 + i >= n_units) break;
+          if (j0 + i >= ring) mbar_wait(smem_u32(&empty[slot]), phase ^ 1u);
+          const unsigned bar = smem_u32(&full[slot]);
+          mbar_arrive_expect_tx(bar, lam_bytes);
+          bulk_g2s(smem_u32(ring_buf + slot * b2), lambda + cur[i], lam_bytes, bar);
+          if (++slot == ring) {
+            slot = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else {  // ---- consumers
+    const int w = warp - 1;
+    c64* st = stage0 + static_cast<long long>(w) * 4 * E;
+    // the unit in registers: its vectors' addresses (null: absent) and values. Vector 0 is mode
+    // (qz, c) [sign type 0]; vector 1 the mirror column's (-qz, c') [type 1] or, for a column that
+    // is its own mirror, the z-reflected (-qz, c) [type 2]; vectors 2, 3 are (-qz, c) [2] and
+    // (qz, c') [3]: a unit has 1, 2 or 4 vectors
+    c64* ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+    int typ1 = 1;
+    c64 reg[4][kStreamRegs];
+    // items[] of a unit is loaded one unit ahead of its fields (two dependent loads in a row
+    // would leave their latencies exposed in front of every unit)
+    int2 it_ahead = make_int2(0, -1);
+    auto item_of = [&](int j) {
+      if (j >= n_units) return;
+      const unsigned u = blockIdx.x + static_cast<unsigned>(j) * g;
+      it_ahead = items[u % ni];
+    };
+    auto fetch = [&](int j) {  // fields of unit j (its item is in it_ahead); then the next unit's item
+      const unsigned u = blockIdx.x + static_cast<unsigned>(j) * g;
+      const int qz = static_cast<int>(u / ni);
+      const int zm = qz ? Lz - qz : 0;
+      const int2 it = it_ahead;
+      item_of(j + n_w);
+      const bool zpair = quad && zm != qz;
+      ptr[0] = field + (qz * plane + it.x) * E;
+      ptr[1] = ptr[2] = ptr[3] = nullptr;
+      typ1 = 1;
+      if (it.y >= 0) {
+        ptr[1] = field + (zm * plane + it.y) * E;
+        if (zpair) {
+          ptr[2] = field + (zm * plane + it.x) * E;
+          ptr[3] = field + (qz * plane + it.y) * E;
+        }
+      } else if (zpair) {
+        ptr[1] = field + (zm * plane + it.x) * E;
+        typ1 = 2;
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (ptr[v]) {
+#pragma unroll
+          for (int t = 0; t < kStreamRegs; ++t) {
+            const int i = lane + 32 * t;
+            if (i < E) reg[v][t] = ptr[v][i];
+          }
+        }
+    };
+    item_of(w);
+    if (w < n_units) fetch(w);
+    for (int j = w; j < n_units; j += n_w) {
+      c64* q[4];
+      const int ty[4] = {0, typ1, 2, 3};
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        q[v] = ptr[v];
+        if (ptr[v]) {
+#pragma unroll
+          for (int t = 0; t < kStreamRegs; ++t) {
+            const int i = lane + 32 * t;
+            if (i < E) st[v * E + i] = cscale(reg[v][t], sgn[ty[v]][i % b]);
+          }
+        }
+      }
+      const int nv = q[2] ? 4 : (q[1] ? 2 : 1);
+      if (j + n_w < n_units) fetch(j + n_w);
+      __syncwarp();
+      const int slot = j % ring;
+      mbar_wait(smem_u32(&full[slot]), static_cast<unsigned>((j / ring) & 1));
+      const c64* blk = ring_buf + slot * b2;
+      if (probe & 1) {
+        // FPBEM_MS_PROBE=1 (diagnostic, wrong results): the stream without the products
+      } else if (nv == 4) {
+        mode_multi<4>(blk, st, E, b, lane);
+      } else if (nv == 2) {
+        mode_multi<2>(blk, st, E, b, lane);
+      } else {
+        mode_multi<1>(blk, st, E, b, lane);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
+      if (!(probe & 2)) {  // FPBEM_MS_PROBE=2 (diagnostic): no write-back
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (q[v])
+            for (int i = lane; i < E; i += 32) q[v][i] = cscale(st[v * E + i], sgn[ty[v]][i % b]);
+      }
+      __syncwarp();  // the staging buffer is rewritten at the top of the next unit
+    }
+  }
+  __syncthreads();  // the producer stays resident until every copy it issued has landed
+}
+
 // zero the embedded field and place each K_o at slot (o mod L) (src/structured.cpp:73-86)
 __global__ void scatter_bank_kernel(const c64* __restrict__ blocks, const int* __restrict__ offsets, int n_blk,
                                     int b2, int lx, int ly, int lz, c64* __restrict__ field) {
@@ -1414,9 +1637,81 @@ cudaError_t launch_m2l_zfused(const c64* in, c64* out, const c64* lambda, const 
   return cudaGetLastError();
 }
 
+// consumer warps and ring of the flat mode stream: the most warps (FPBEM_MS_WARPS, default 11)
+// that still get FPBEM_MS_SPW (default 1) slots each, ring = the largest multiple that fits.
+// Measured on cfg3 (M2L stage, serial): 9 warps x 2 slots 84.6 us, 9 x 1 84.5, 11 x 1 78.4 —
+// with four products per block the consumers bind, not the ring depth (0: shape not
+// supported — b > 32 or too many fields per mode)
+namespace {
+void mode_stream_shape(int E, int b, int* n_w, int* ring) {
+  *n_w = *ring = 0;
+  if (b < 1 || b > 32 || E > 32 * kStreamRegs) return;
+  static const int want = [] {
+    const char* v = std::getenv("FPBEM_MS_WARPS");
+    const int w = v ? std::atoi(v) : kStreamWarps;
+    return w < 1 ? 1 : (w > kStreamWarps ? kStreamWarps : w);
+  }();
+  static const int spw_min = [] {  // FPBEM_MS_SPW: least slots per warp (A/B)
+    const char* v = std::getenv("FPBEM_MS_SPW");
+    const int w = v ? std::atoi(v) : 1;
+    return w < 1 ? 1 : w;
+  }();
+  static const int ring_cap = [] {  // FPBEM_MS_RING: most ring slots (a small ring lets the kernel share an SM)
+    const char* v = std::getenv("FPBEM_MS_RING");
+    return v ? std::atoi(v) : 0;
+  }();
+  const size_t per_mode = sizeof(c64) * static_cast<size_t>(b) * b;
+  for (int w = want; w >= 1; --w) {
+    const size_t stage = sizeof(c64) * static_cast<size_t>(w) * 4 * E;
+    long long r = static_cast<long long>((200 * 1024 - stage) / per_mode);
+    if (r > kStreamMaxRing) r = kStreamMaxRing;
+    if (ring_cap > 0 && r > ring_cap) r = ring_cap;
+    if (r >= static_cast<long long>(spw_min) * w || (w == 1 && r >= 2)) {
+      *n_w = w;
+      *ring = static_cast<int>(r / w) * w;
+      return;
+    }
+  }
+}
+}  // namespace
+
+int mode_stream_ring(int E, int b) {
+  int n_w, ring;
+  mode_stream_shape(E, b, &n_w, &ring);
+  return ring;
+}
+
+cudaError_t launch_mode_stream(c64* field, const c64* lambda, int Lz, long long plane, int E, int b,
+                               const int2* items, int n_items, bool quad, cudaStream_t stream) {
+  int n_w, ring;
+  mode_stream_shape(E, b, &n_w, &ring);
+  if (ring < 2) return cudaErrorInvalidValue;
+  const int qz_count = quad ? Lz / 2 + 1 : Lz;  // quad: the modes qz <= Lz/2 determine the rest
+  const long long total = static_cast<long long>(n_items) * qz_count;
+  if (total == 0) return cudaSuccess;
+  if (total > 0x7fffffffLL) return cudaErrorInvalidValue;  // 32-bit unit arithmetic in the kernel
+  const size_t smem = sizeof(c64) * (static_cast<size_t>(ring) * b * b + static_cast<size_t>(n_w) * 4 * E);
+  static std::atomic<unsigned long long> configured{0};
+  if (smem > 48 * 1024) {
+    cudaError_t e = ensure_max_smem(configured, reinterpret_cast<const void*>(&mode_stream_kernel), kMaxDynSmem);
+    if (e != cudaSuccess) return e;
+  }
+  const int sms = device_sms();
+  const int grid = static_cast<int>(total < sms ? total : sms);  // persistent: one CTA per SM
+  static const int probe = [] {
+    const char* v = std::getenv("FPBEM_MS_PROBE");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (probe & 8) return cudaSuccess;  // FPBEM_MS_PROBE=8 (diagnostic, wrong results): the DFT passes alone
+  mode_stream_kernel<<<grid, 32 * (1 + n_w), smem, stream>>>(field, lambda, Lz, qz_count, plane, E, b, ring, items,
+                                                              n_items, quad ? 1 : 0, probe);
+  return cudaGetLastError();
+}
+
 // max |Λ(-q) - D Λ(q) D| and max |Λ| (component-wise, as bit patterns of
-// non-negative doubles) over the whole spectrum
-__global__ void lambda_parity_kernel(const c64* __restrict__ lam, int Lx, int Ly, int Lz, int b,
+// non-negative doubles) over the whole spectrum; zflip: the reflection parity
+// max |Λ(qx, qy, -qz) - Dz Λ(q) Dz| with Dz = diag((-1)^(n+m)) instead
+__global__ void lambda_parity_kernel(const c64* __restrict__ lam, int Lx, int Ly, int Lz, int b, int zflip,
                                      unsigned long long* __restrict__ out) {
   const long long q_total = static_cast<long long>(Lx) * Ly * Lz, b2 = static_cast<long long>(b) * b;
   double dmax = 0.0, amax = 0.0;
@@ -1424,12 +1719,15 @@ __global__ void lambda_parity_kernel(const c64* __restrict__ lam, int Lx, int Ly
        g += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long q = g / b2, e = g - q * b2;
     const int qx = static_cast<int>(q % Lx), qy = static_cast<int>((q / Lx) % Ly), qz = static_cast<int>(q / Lx / Ly);
-    const long long qm = (static_cast<long long>((Lz - qz) % Lz) * Ly + (Ly - qy) % Ly) * Lx + (Lx - qx) % Lx;
+    const long long qm = zflip ? (static_cast<long long>((Lz - qz) % Lz) * Ly + qy) * Lx + qx
+                               : (static_cast<long long>((Lz - qz) % Lz) * Ly + (Ly - qy) % Ly) * Lx + (Lx - qx) % Lx;
     const int i = static_cast<int>(e % b), j = static_cast<int>(e / b);  // column-major block
     int ni = 0, nj = 0;
     while ((ni + 1) * (ni + 1) <= i) ++ni;
     while ((nj + 1) * (nj + 1) <= j) ++nj;
-    const double sg = ((ni + nj) & 1) ? -1.0 : 1.0;
+    // coefficient i = n^2 + n + m: n + m = i - n^2
+    const int par = zflip ? (i - ni * ni) + (j - nj * nj) : ni + nj;
+    const double sg = (par & 1) ? -1.0 : 1.0;
     const c64 a = lam[q * b2 + e], m = lam[qm * b2 + e];
     dmax = fmax(dmax, fmax(fabs(m.x - sg * a.x), fabs(m.y - sg * a.y)));
     amax = fmax(amax, fmax(fabs(a.x), fabs(a.y)));
@@ -1438,9 +1736,10 @@ __global__ void lambda_parity_kernel(const c64* __restrict__ lam, int Lx, int Ly
   atomicMax(out + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
 }
 
-cudaError_t launch_lambda_parity(const c64* lam, const int L[3], int b, unsigned long long* out2, cudaStream_t stream) {
+cudaError_t launch_lambda_parity(const c64* lam, const int L[3], int b, bool zflip, unsigned long long* out2,
+                                 cudaStream_t stream) {
   const long long total = static_cast<long long>(L[0]) * L[1] * L[2] * b * b;
-  lambda_parity_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lam, L[0], L[1], L[2], b, out2);
+  lambda_parity_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lam, L[0], L[1], L[2], b, zflip ? 1 : 0, out2);
   return cudaGetLastError();
 }
 

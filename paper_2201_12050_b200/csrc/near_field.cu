@@ -691,7 +691,12 @@ bool mode_mma_shape(int n, int ncols, int* nw, int* kc, int* ring, size_t* smem)
   const size_t fixed = XB * sizeof(c64) * 8 * static_cast<size_t>(n + 4) + 4 * 8 * 16 + 128;
   const size_t budget = static_cast<size_t>(kMaxDynSmem) - 1024;  // the kernel's static shared memory
   if (fixed + 2 * stage > budget) return false;
-  const int R = static_cast<int>(std::min<size_t>(16, (budget - fixed) / stage));
+  static const int ring_env = [] {  // FPBEM_MMA_RING: most ring stages (A/B: shared memory left to a co-resident kernel)
+    const char* v = std::getenv("FPBEM_MMA_RING");
+    return v ? std::atoi(v) : 0;
+  }();
+  int R = static_cast<int>(std::min<size_t>(16, (budget - fixed) / stage));
+  if (ring_env >= 2 && R > ring_env) R = ring_env;
   *nw = NW;
   *kc = KC;
   *ring = R;

@@ -314,6 +314,13 @@ class FmmOperators:
         _raise(_native.cuda().fpbem_cu_far_info(self._h, sizes, C.byref(paired)))
         return tuple(sizes), bool(paired.value)
 
+    def far_parity(self) -> int:
+        """0: no parity of Λ; 1: Λ(-q) = D Λ(q) D (a streamed block serves a mode and its mirror);
+        2: also Λ(qx, qy, -qz) = Dz Λ(q) Dz (the flat stream reads a quarter of Λ)"""
+        sizes, paired = (C.c_int * 3)(), C.c_int()
+        _raise(_native.cuda().fpbem_cu_far_info(self._h, sizes, C.byref(paired)))
+        return int(paired.value)
+
     def set_stream(self, stream_ptr: int | None) -> None:
         _raise(_native.cuda().fpbem_cu_set_stream(self._h, stream_ptr))
 

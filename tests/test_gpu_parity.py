@@ -110,6 +110,67 @@ def test_circulant_m2l_matches_oracle(ops, counts, b):
         assert rel(op.matvec(p), dense @ p) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("zmode", ["fused", "stream"])
+@pytest.mark.parametrize("counts,b", [((3, 3, 2), 25), ((4, 4, 4), 9), ((2, 3, 5), 25), ((1, 4, 3), 4), ((6, 5, 9), 16)])
+def test_m2l_z_forms_match_oracle(ops, monkeypatch, counts, b, zmode):
+    """The two forms of the far field's z stage — the fused per-column kernel and the z axis passes
+    around the flat Λ stream (the default; FPBEM_M2L_Z=fused selects the other) — both equal CirculantSpectrum::matvec
+    (src/structured.cpp:122-166); random blocks have no mirror parity, so every column is its own item."""
+    monkeypatch.setenv("FPBEM_M2L_Z", zmode)
+    rng = np.random.default_rng(b + sum(counts))
+    d = circulant_only(rng, counts, b)
+    op = ops(d)
+    p = uvec(rng, d.N)
+    ref = O.toeplitz_matvec(counts, d.far_offsets, d.far_blocks, p)
+    y = op.matvec(p)
+    assert rel(y, ref) <= MATVEC_TOL
+    assert np.array_equal(y, op.matvec(p))
+
+
+@pytest.mark.parametrize("zmode", ["fused", "stream"])
+def test_m2l_z_forms_many_modes_per_cta(ops, monkeypatch, zmode):
+    """32 x 32 x 8 modes: every CTA of the persistent kernels takes several times its ring of Λ blocks,
+    so the ring slots wrap and their mbarrier phases are reused (bitwise repeatable, = the oracle's
+    FFT-based CirculantSpectrum::matvec)."""
+    monkeypatch.setenv("FPBEM_M2L_Z", zmode)
+    rng = np.random.default_rng(99)
+    counts, b = (16, 16, 4), 25
+    d = circulant_only(rng, counts, b)
+    op = ops(d)
+    p = uvec(rng, d.N)
+    sizes, lam = O.spectrum_build(counts, d.far_offsets, d.far_blocks)
+    ref = O.spectrum_matvec(counts, sizes, b, lam, p)
+    y = op.matvec(p)
+    assert rel(y, ref) <= MATVEC_TOL
+    for _ in range(5):
+        assert np.array_equal(y, op.matvec(p))
+
+
+@pytest.mark.parametrize("cid,var", [(3, 2), (5, 2)])
+def test_m2l_flat_stream_on_paired_spectrum(ops, assembled, monkeypatch, cid, var):
+    """An assembled operator's Λ has the mirror parity Λ(-q) = D Λ(q) D and the reflection parity
+    Λ(qx, qy, -qz) = Dz Λ(q) Dz: one streamed block serves a mode and its mirror (two modes per block,
+    FPBEM_M2L_QUAD=0) or four modes (the default); both equal the oracle and the fused z kernel,
+    2 right-hand sides included (E = 2 b fields per mode)."""
+    sc, d = assembled(cid, var)
+    ora = O.OracleFmm(d)
+    rng = np.random.default_rng(17 + cid)
+    P = [uvec(rng, d.N) for _ in range(2)]
+    refs = [ora.matvec(p) for p in P]
+    monkeypatch.setenv("FPBEM_M2L_Z", "fused")
+    y_fused = ops(d).matvec(P[0])
+    monkeypatch.setenv("FPBEM_M2L_Z", "stream")
+    for quad in ("0", "1"):
+        monkeypatch.setenv("FPBEM_M2L_QUAD", quad)
+        op = ops(d, max_rhs=2)
+        assert op.far_info()[1] and op.far_parity() == 2
+        y = op.matvec(np.concatenate(P))
+        for r in range(2):
+            assert rel(y[r * d.N:(r + 1) * d.N], refs[r]) <= MATVEC_TOL
+        assert rel(y[:d.N], y_fused) <= 1e-14
+        assert np.array_equal(y, op.matvec(np.concatenate(P)))
+
+
 def test_scalar_toeplitz_known_answer_on_device(ops):
     """test_structured.cpp:84-98 through the device M2L: T=[[2,1],[3,2]], T(1,1)=(3,5)"""
     d = Data((2, 1, 1), 1, 1, [(0, 0, 0)], np.zeros((1, 1, 1)), [(0, 0, 0), (1, 0, 0), (-1, 0, 0)],

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_near_lattice.py -m gpu -q -x -k "full_size or pipelined or matches_oracle_and_direct" -p no:cacheprovider > gpurun_out/pytest_lb.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_lb.log
-timeout 600 python bench.py --no-cpu-baseline --no-nosym --gmres-max-iter 5 > gpurun_out/bench_lb8.json 2> gpurun_out/bench_lb8.err
-timeout 600 python bench.py --config 5 --no-cpu-baseline --no-nosym --gmres-max-iter 5 > gpurun_out/bench_c5_lb8.json 2> gpurun_out/bench_c5_lb8.err
-echo done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_s4.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_s4.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_s4.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke_s4.log
+timeout 900 python bench.py > gpurun_out/bench_s4.json 2> gpurun_out/bench_s4.err
+tail -3 gpurun_out/pytest_gpu_s4.log; tail -2 gpurun_out/smoke_s4.log; cat gpurun_out/bench_s4.json | cut -c1-600

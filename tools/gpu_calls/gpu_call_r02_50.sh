@@ -1,8 +1,12 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_near_lattice.py -m gpu -q -x -k "full_size or pipelined" -p no:cacheprovider > gpurun_out/pytest_xyt.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_xyt.log
-rm -f gpurun_out/xyt_summary.txt
-for v in 1 0; do FPBEM_NEAR_XYT=$v timeout 600 python bench.py --no-cpu-baseline --no-nosym --gmres-max-iter 5 --trials 3 > gpurun_out/bench_xyt$v.json 2> gpurun_out/bench_xyt$v.err; python -c "
-import json;d=json.load(open('gpurun_out/bench_xyt$v.json'))
-print($v, round(d['ms_per_step'],4), 'near serial', round(d['stages_serial_ms']['near_gemm'],4), 'e2e %.4g' % d['e2e']['value'])" >> gpurun_out/xyt_summary.txt; done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"xy_tile" -c 3 --csv --log-file gpurun_out/launches_xyt.csv python bench.py --steps 3 --warmup 3 --trials 1 --no-cpu-baseline --no-nosym --gmres-max-iter 5 > gpurun_out/ncu_xyt.log 2>&1
-echo done
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "m2l_z_forms or flat_stream or fmm_matvec_matches" 2>&1 | tail -5
+for mode in "fused 1" "stream 0" "stream 1"; do set -- $mode
+  for cfg in 3 5; do
+    FPBEM_M2L_Z=$1 FPBEM_M2L_QUAD=$2 timeout 600 python bench.py --config $cfg --no-cpu-baseline --no-nosym > gpurun_out/bench_z_$1$2_$cfg.json 2> gpurun_out/bench_z_$1$2_$cfg.err
+    python - <<P
+import json
+d=json.load(open("gpurun_out/bench_z_$1$2_$cfg.json"))
+print("$1 quad$2 cfg$cfg", round(d["ms_per_step"],4), "serial m2l", round(d["stages_serial_ms"]["m2l"],4), "gmres", d["gmres"]["solve_s"], d["gmres"]["iterations"], d.get("roofline_m2l",{}).get("frac_survey_definition"))
+P
+  done
+done
