@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 namespace fpbem_cu {
 
@@ -47,6 +48,46 @@ inline int device_sms() {
     cache[dev & 63].store(v, std::memory_order_relaxed);
   }
   return v;
+}
+
+// ---- programmatic dependent launch (PDL). A kernel launched through launch_ex(..., pdl = true)
+// may start while the kernel before it on the stream is still draining: its CTAs become resident as
+// SMs free up and run their prologue (twiddle tables, barrier init, copies of operator data that no
+// earlier kernel writes), and pdl_wait() — griddepcontrol.wait: returns when every kernel before it
+// on the stream has completed and its writes are visible — must precede the first access to data an
+// earlier kernel produces or still reads. Launched normally, pdl_wait() / pdl_trigger() are no-ops.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// lets the next kernel's CTAs be scheduled once every CTA of this grid has issued it (or exited)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+#endif
+
+// FPBEM_PDL=1 enables it (read once); never while the stream is being captured into a graph
+inline bool pdl_enabled(cudaStream_t stream) {
+  static const bool on = [] {
+    const char* v = std::getenv("FPBEM_PDL");
+    return v && std::atoi(v) != 0;
+  }();
+  if (!on) return false;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &st) != cudaSuccess) return false;
+  return st == cudaStreamCaptureStatusNone;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, bool pdl,
+                             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 constexpr int kMaxDynSmem = 227 * 1024;  // sm_100a opt-in limit per CTA

@@ -278,11 +278,12 @@ __global__ void __launch_bounds__(kDftMmaWarps * 32)
 dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c64* __restrict__ tw, long long n_a,
                      int n_in, int n_out, long long n_inner, int L, int backward, double scale, L2pEpi epi = {}) {
   extern __shared__ __align__(16) unsigned char dmma_smem[];
+  pdl_trigger();
   const int MT = (n_out + 7) / 8, KT = (n_in + 3) / 4;
   double* wr = reinterpret_cast<double*>(dmma_smem);  // [mt][kt][lane]
   double* wi = wr + MT * KT * 32;
   double* ws = wi + MT * KT * 32;
-  for (int e = threadIdx.x; e < MT * KT * 32; e += blockDim.x) {
+  for (int e = threadIdx.x; e < MT * KT * 32; e += blockDim.x) {  // (tw is constant: before pdl_wait)
     const int ln = e & 31, f = e >> 5, kt = f % KT, mt = f / KT;
     const int q = mt * 8 + (ln >> 2), j = kt * 4 + (ln & 3);
     c64 w = cmk(0.0, 0.0);
@@ -319,6 +320,7 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
       nb[kt] = (ok && kt < KTd && j < n_in) ? src[static_cast<long long>(j) * n_inner] : cmk(0.0, 0.0);
     }
   };
+  pdl_wait();  // `in` is the previous kernel's output, `out` may be its input
   load(warp0);
   for (long long t = warp0; t < tiles; t += nwarps) {
     double br[KTM], bi[KTM];  // (br + bi is formed at each use: fewer live registers)
@@ -1104,16 +1106,20 @@ constexpr int kStreamWarps = 11;  // most consumer warps (12 warps with the prod
 constexpr int kStreamMaxRing = 32;
 constexpr int kStreamRegs = 2;  // E <= 32 * kStreamRegs
 
-// s[v] <- Λ s[v] for NV staged vectors of E = nrhs x b fields (b <= 32: one output per lane)
-template <int NV>
-__device__ __forceinline__ void mode_multi(const c64* __restrict__ lam_blk, c64* __restrict__ s0, int E, int b,
+// s[v] <- Λ s[v] for NV staged vectors of E = nrhs x b fields (b <= 32: one output per lane).
+// BC > 0: b = BC at compile time (the reference's default order n_t = 4, b = 25: the column loop
+// unrolls fully and its shared-memory loads are issued ahead of the FMA chains); BC = 0: any b.
+template <int NV, int BC>
+__device__ __forceinline__ void mode_multi(const c64* __restrict__ lam_blk, c64* __restrict__ s0, int E, int b_rt,
                                            int lane) {
+  const int b = BC > 0 ? BC : b_rt;
   const c64* lam = lam_blk + (lane < b ? lane : 0);
   for (int r0 = 0; r0 < E; r0 += b) {
     c64 a0[NV], a1[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) a0[v] = a1[v] = cmk(0.0, 0.0);
     int c = 0;
+#pragma unroll(BC > 0 ? 4 : 1)
     for (; c + 2 <= b; c += 2) {
       const c64 l0 = lam[c * b], l1 = lam[(c + 1) * b];
 #pragma unroll
@@ -1135,6 +1141,17 @@ __device__ __forceinline__ void mode_multi(const c64* __restrict__ lam_blk, c64*
     }
     __syncwarp();
   }
+}
+
+template <int BC>
+__device__ __forceinline__ void mode_multi_nv(int nv, const c64* __restrict__ blk, c64* __restrict__ st, int E, int b,
+                                              int lane) {
+  if (nv == 4)
+    mode_multi<4, BC>(blk, st, E, b, lane);
+  else if (nv == 2)
+    mode_multi<2, BC>(blk, st, E, b, lane);
+  else
+    mode_multi<1, BC>(blk, st, E, b, lane);
 }
 
 __global__ void __launch_bounds__(32 * (1 + kStreamWarps), 1)
@@ -1265,7 +1282,7 @@ mode_stream_kernel(c64* __restrict__ field, const c64* __restrict__ lambda, int 
 #pragma unroll
           for (int t = 0; t < kStreamRegs; ++t) {
             const int i = lane + 32 * t;
-            if (i < E) st[v * E + i] = cscale(reg[v][t], sgn[ty[v]][i % b]);
+            if (i < E) st[v * E + i] = cscale(reg[v][t], sgn[ty[v]][E == b ? i : i % b]);
           }
         }
       }
@@ -1277,12 +1294,10 @@ mode_stream_kernel(c64* __restrict__ field, const c64* __restrict__ lambda, int 
       const c64* blk = ring_buf + slot * b2;
       if (probe & 1) {
         // FPBEM_MS_PROBE=1 (diagnostic, wrong results): the stream without the products
-      } else if (nv == 4) {
-        mode_multi<4>(blk, st, E, b, lane);
-      } else if (nv == 2) {
-        mode_multi<2>(blk, st, E, b, lane);
+      } else if (b == 25) {
+        mode_multi_nv<25>(nv, blk, st, E, b, lane);
       } else {
-        mode_multi<1>(blk, st, E, b, lane);
+        mode_multi_nv<0>(nv, blk, st, E, b, lane);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
@@ -1290,7 +1305,7 @@ mode_stream_kernel(c64* __restrict__ field, const c64* __restrict__ lambda, int 
 #pragma unroll
         for (int v = 0; v < 4; ++v)
           if (q[v])
-            for (int i = lane; i < E; i += 32) q[v][i] = cscale(st[v * E + i], sgn[ty[v]][i % b]);
+            for (int i = lane; i < E; i += 32) q[v][i] = cscale(st[v * E + i], sgn[ty[v]][E == b ? i : i % b]);
       }
       __syncwarp();  // the staging buffer is rewritten at the top of the next unit
     }
@@ -1388,18 +1403,19 @@ cudaError_t launch_dft_axis(const c64* in, c64* out, const c64* tw, long long n_
     const long long cap = static_cast<long long>(kNumSMs) * occ[which];
     if (blocks > cap) blocks = cap;
     const int bw = backward ? 1 : 0;
+    const bool pdl = pdl_enabled(stream);
+    const dim3 g(static_cast<unsigned>(blocks)), blk(kDftMmaWarps * 32);
     if (KTd <= 4)
-      dft_axis_dmma_kernel<4><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
-          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
-    else if (KTd <= 8)
-      dft_axis_dmma_kernel<8><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
-          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
-    else if (KTd <= 12)
-      dft_axis_dmma_kernel<12><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
-          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
-    else
-      dft_axis_dmma_kernel<16><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
-          in, out, tw, n_a, n_in, n_out, n_inner, L, bw, scale);
+      return launch_ex(dft_axis_dmma_kernel<4>, g, blk, smem, stream, pdl, in, out, tw, n_a, n_in, n_out, n_inner, L, bw,
+                       scale, L2pEpi{});
+    if (KTd <= 8)
+      return launch_ex(dft_axis_dmma_kernel<8>, g, blk, smem, stream, pdl, in, out, tw, n_a, n_in, n_out, n_inner, L, bw,
+                       scale, L2pEpi{});
+    if (KTd <= 12)
+      return launch_ex(dft_axis_dmma_kernel<12>, g, blk, smem, stream, pdl, in, out, tw, n_a, n_in, n_out, n_inner, L,
+                       bw, scale, L2pEpi{});
+    return launch_ex(dft_axis_dmma_kernel<16>, g, blk, smem, stream, pdl, in, out, tw, n_a, n_in, n_out, n_inner, L, bw,
+                     scale, L2pEpi{});
     return cudaGetLastError();
   }
   // widest output group that still gives >= 2 x 256 threads per SM

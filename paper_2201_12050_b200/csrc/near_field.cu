@@ -380,6 +380,7 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(Xs + nxb * 8 * XP);  // nxb X buffers
   __shared__ int iq[2][8], ig[2][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
   const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + ring), xfull0 = smem_u32(bars + 2 * ring),
                  xempty0 = smem_u32(bars + 2 * ring + 2);
   if (threadIdx.x == 0) {
@@ -407,6 +408,9 @@ near_mode_mma_kernel(const c64* __restrict__ shat, const int* __restrict__ items
   };
 
   if (warp == NW + 1) {  // ---- X producer: the blocks' columns, up to two blocks ahead of the consumers
+    // xh is the previous kernel's output (the block producer streams operator data and starts at
+    // once; the consumers touch global memory only after an X buffer has arrived)
+    pdl_wait();
     int it = 0;
     for (long long u = u_lo + blockIdx.x; u < u_hi; u += gridDim.x, ++it) {
       const long long t = u / rsplit;
@@ -741,9 +745,8 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   if (e != cudaSuccess) return e;
   const long long units = n_blk * rsplit;
   const int grid = static_cast<int>(std::min<long long>(units, sms));
-  fns[which]<<<grid, 32 * (NW + 2), smem, stream>>>(shat, items, n_items, perm, xh, yh, n, t_lo, t_hi, q_stride,
-                                                     nrhs, ncols, KC, R, rsplit, mode_mma_xbufs());
-  return cudaGetLastError();
+  return launch_ex(fns[which], dim3(grid), dim3(32 * (NW + 2)), smem, stream, pdl_enabled(stream), shat, items, n_items,
+                   perm, xh, yh, n, t_lo, t_hi, q_stride, nrhs, ncols, KC, R, rsplit, mode_mma_xbufs());
 }
 
 // max |S_s'[P i + n P j] - S_s[i + n j]| over blocks s with image slot s' (the
