@@ -171,6 +171,25 @@ def test_m2l_flat_stream_on_paired_spectrum(ops, assembled, monkeypatch, cid, va
         assert np.array_equal(y, op.matvec(np.concatenate(P)))
 
 
+@pytest.mark.parametrize("n_t", [2, 3])
+def test_m2l_flat_stream_other_orders(ops, monkeypatch, n_t):
+    """Expansion orders other than the default n_t = 4 (b = 9, 16: the stream kernel's generic column
+    loop, four modes per block) against the oracle and the fused z kernel."""
+    from paper_2201_12050_b200 import Scene
+
+    d = Scene(3, 2).assemble_fmm(n_t)
+    ora = O.OracleFmm(d)
+    p = uvec(np.random.default_rng(n_t), d.N)
+    monkeypatch.setenv("FPBEM_M2L_Z", "fused")
+    y_fused = ops(d).matvec(p)
+    monkeypatch.setenv("FPBEM_M2L_Z", "stream")
+    op = ops(d)
+    assert op.far_parity() == 2
+    y = op.matvec(p)
+    assert rel(y, ora.matvec(p)) <= MATVEC_TOL
+    assert rel(y, y_fused) <= 1e-14
+
+
 def test_scalar_toeplitz_known_answer_on_device(ops):
     """test_structured.cpp:84-98 through the device M2L: T=[[2,1],[3,2]], T(1,1)=(3,5)"""
     d = Data((2, 1, 1), 1, 1, [(0, 0, 0)], np.zeros((1, 1, 1)), [(0, 0, 0), (1, 0, 0), (-1, 0, 0)],
