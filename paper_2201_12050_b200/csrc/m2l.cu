@@ -283,19 +283,6 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
   double* wr = reinterpret_cast<double*>(dmma_smem);  // [mt][kt][lane]
   double* wi = wr + MT * KT * 32;
   double* ws = wi + MT * KT * 32;
-  for (int e = threadIdx.x; e < MT * KT * 32; e += blockDim.x) {  // (tw is constant: before pdl_wait)
-    const int ln = e & 31, f = e >> 5, kt = f % KT, mt = f / KT;
-    const int q = mt * 8 + (ln >> 2), j = kt * 4 + (ln & 3);
-    c64 w = cmk(0.0, 0.0);
-    if (q < n_out && j < n_in) {
-      w = tw[(j * q) % L];
-      if (backward) w.y = -w.y;
-    }
-    wr[e] = w.x;
-    wi[e] = w.y;
-    ws[e] = w.x + w.y;
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
   const long long n_et = (n_inner + 7) / 8, tiles = n_a * n_et;
   // a lone last input (n_in = 4k + 1, e.g. the 17 modes of a 16-cell near lattice)
@@ -320,8 +307,23 @@ dft_axis_dmma_kernel(const c64* __restrict__ in, c64* __restrict__ out, const c6
       nb[kt] = (ok && kt < KTd && j < n_in) ? src[static_cast<long long>(j) * n_inner] : cmk(0.0, 0.0);
     }
   };
+  // the first tile's loads are in flight while the twiddle table is expanded (both are
+  // L2 round trips of about a microsecond; in series they cost every short pass both)
   pdl_wait();  // `in` is the previous kernel's output, `out` may be its input
   load(warp0);
+  for (int e = threadIdx.x; e < MT * KT * 32; e += blockDim.x) {
+    const int ln = e & 31, f = e >> 5, kt = f % KT, mt = f / KT;
+    const int q = mt * 8 + (ln >> 2), j = kt * 4 + (ln & 3);
+    c64 w = cmk(0.0, 0.0);
+    if (q < n_out && j < n_in) {
+      w = tw[(j * q) % L];
+      if (backward) w.y = -w.y;
+    }
+    wr[e] = w.x;
+    wi[e] = w.y;
+    ws[e] = w.x + w.y;
+  }
+  __syncthreads();
   for (long long t = warp0; t < tiles; t += nwarps) {
     double br[KTM], bi[KTM];  // (br + bi is formed at each use: fewer live registers)
 #pragma unroll
