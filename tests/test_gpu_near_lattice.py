@@ -421,3 +421,36 @@ def test_pipelined_host_product_equals_device_product(ops, assembled, cid, var):
     assert rel(y_host, O.OracleFmm(d).matvec(p)) <= MATVEC_TOL
     for _ in range(3):  # repeated calls reuse the staging buffers and events
         assert np.array_equal(op.matvec(p), y_host)
+
+
+def test_programmatic_dependent_launch_gives_the_same_bits(tmp_path):
+    """FPBEM_PDL=1 (the DFT passes and the mode product launched as programmatic dependents,
+    griddepcontrol.wait in front of their first dependent access; read once per process, hence the
+    subprocesses): the product and a GMRES solve of the shrunk cfg3 lattice are bitwise those of the
+    ordinary launches, product after product."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = (
+        "import sys, numpy as np\n"
+        "from paper_2201_12050_b200 import Scene, FmmOperators, gmres\n"
+        "d = Scene(3, 2).assemble_fmm(4)\n"
+        "op = FmmOperators(d, near_path='lattice')\n"
+        "rng = np.random.default_rng(5)\n"
+        "p = rng.uniform(-1, 1, d.N) + 1j * rng.uniform(-1, 1, d.N)\n"
+        "ys = [op.matvec(p) for _ in range(6)]\n"
+        "assert all(np.array_equal(ys[0], y) for y in ys)\n"
+        "rep = gmres(op, p, tol=1e-8, restart=20, max_iter=200)\n"
+        "np.save(sys.argv[1], np.concatenate([ys[0], np.asarray(rep.solution), [rep.iterations]]))\n"
+    )
+    root = Path(__file__).resolve().parents[1]
+    outs = []
+    for pdl in ("0", "1"):
+        f = tmp_path / f"pdl{pdl}.npy"
+        env = dict(os.environ, FPBEM_PDL=pdl, PYTHONPATH=str(root))
+        r = subprocess.run([sys.executable, "-c", code, str(f)], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
