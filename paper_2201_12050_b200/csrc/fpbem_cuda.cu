@@ -861,7 +861,12 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
       op->mode_lo > 0 || op->mode_hi < op->n_items)
     return false;
   const long long n = op->n;
-  const int chunks = std::min(4, Mz);
+  static const int chunks_env = [] {  // FPBEM_PIPE_CHUNKS: z-plane slabs per product (A/B), at most 8
+    const char* v = std::getenv("FPBEM_PIPE_CHUNKS");
+    const int c = v ? std::atoi(v) : 4;
+    return c < 1 ? 1 : (c > 8 ? 8 : c);
+  }();
+  const int chunks = std::min(chunks_env, Mz);
   cudaStream_t s = op->stream, a = op->aux;
   if (!op->cin) {
     check(cudaStreamCreateWithFlags(&op->cin, cudaStreamNonBlocking), "copy-in stream");
@@ -873,6 +878,21 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
   }
   auto z0_of = [&](int c) { return static_cast<long long>(Mz) * c / chunks; };
   const long long xplane = static_cast<long long>(My) * Mx * n;  // one z-plane of x / y
+  // FPBEM_PIPE_TRACE=1: the product's timeline on stderr (timed events; diagnostic)
+  static const bool trace = [] {
+    const char* v = std::getenv("FPBEM_PIPE_TRACE");
+    return v && std::atoi(v) != 0;
+  }();
+  static cudaEvent_t tev[8];
+  static bool tev_ok = false;
+  if (trace && !tev_ok) {
+    for (auto& e : tev) check(cudaEventCreate(&e), "trace events");
+    tev_ok = true;
+  }
+  auto mark = [&](int i, cudaStream_t st) {
+    if (trace) check(cudaEventRecord(tev[i], st), "trace");
+  };
+  mark(0, s);
   // the copy-in stream starts after whatever the handle's stream has queued (staging reuse)
   check(cudaEventRecord(op->fork, s), "pipeline fork");
   check(cudaStreamWaitEvent(op->cin, op->fork, 0), "pipeline fork");
@@ -883,6 +903,7 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
           "x upload");
     check(cudaEventRecord(op->pev_in[c], op->cin), "pipeline event");
   }
+  mark(1, op->cin);  // x uploaded
   // far field (aux stream): P2M and the forward x+y plane DFTs of the M2L slab
   // by slab as x arrives, the rest once x is complete; joined before the first L2P
   const std::vector<M2lPass> plan = m2l_plan(op, 1);
@@ -909,6 +930,7 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
     }
   }
   m2l_apply(op, 1, a, op->mom, op->lambda, op->loc, far_xy);
+  mark(2, a);  // far field done
   check(cudaEventRecord(op->join, a), "pipeline join");
   // near field: x and y passes slab by slab (buffers as near_fft_apply: x -> nfa -> nfb)
   for (int c = 0; c < chunks; ++c) {
@@ -923,9 +945,11 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
     op->launches += 2;
   }
   const long long zstride = static_cast<long long>(Ly) * Lx * n;
+  mark(3, s);  // near x, y passes done
   check(launch_dft_axis(op->nfb, op->nfa, op->twn[2], 1, Mz, Lz, zstride, Lz, false, 1.0, s), "near dft z");
   near_mode_stage(op, op->nfa, op->nfb, 1, s);
   check(launch_dft_axis(op->nfb, op->nfa, op->twn[2], 1, Lz, Mz, zstride, Lz, true, 1.0, s), "near inverse dft z");
+  mark(4, s);  // near inverse z done
   op->launches += 2;
   const double scale = 1.0 / static_cast<double>(op->qn);
   check(cudaStreamWaitEvent(s, op->join, 0), "pipeline join");  // the locals of the far field
@@ -939,12 +963,23 @@ bool apply_host_pipelined(fpbem_cu_op* op, const c64* xh, c64* yh) {
           "near inverse dft x + l2p");
     op->launches += 2;
     check(cudaEventRecord(op->pev_out[c], s), "pipeline event");
+    if (c == 0) mark(5, s);  // first slab of y ready
+    if (c == chunks - 1) mark(6, s);  // last slab of y ready
     check(cudaStreamWaitEvent(op->cout, op->pev_out[c], 0), "pipeline out");
     check(cudaMemcpyAsync(yh + z0 * xplane, op->yout + z0 * xplane, static_cast<size_t>(m * xplane) * sizeof(c64),
                           cudaMemcpyDeviceToHost, op->cout),
           "y download");
   }
+  mark(7, op->cout);  // y downloaded
   check(cudaStreamSynchronize(op->cout), "apply sync");
+  if (trace) {
+    float t[8] = {0};
+    for (int i = 1; i < 8; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+    std::fprintf(stderr,
+                 "[fpbem pipe] x up %.3f | far done %.3f | near xy %.3f | near z-inv %.3f | y slab0 %.3f | y last %.3f | "
+                 "y down %.3f ms\n",
+                 t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+  }
   return true;
 }
 
