@@ -1488,9 +1488,28 @@ cudaError_t launch_dft_axis_l2p(const c64* in, c64* out, const c64* tw, long lon
   epi.cpl = n_a / nrhs;
   const long long tiles = n_a * ((n_inner + 7) / 8);
   long long blocks = (tiles + kDftMmaWarps - 1) / kDftMmaWarps;
-  const long long cap = static_cast<long long>(device_sms()) * 4;
-  if (blocks > cap) blocks = cap;
   const int KTd = (n_in % 4 == 1 && n_in > 4) ? KT - 1 : KT;  // the kernel's DMMA k steps (xcol)
+  // one resident wave: as many CTAs per SM as the kernel's registers allow (a fixed 4 per SM left
+  // a second, thin wave once the epilogue's registers brought the kernel to 3 CTAs per SM);
+  // FPBEM_L2P_CTAS forces the CTAs per SM (A/B)
+  static int occ[2] = {0, 0};
+  const int which = KTd <= 4 ? 0 : 1;
+  if (occ[which] == 0) {
+    static const int occ_env = [] {
+      const char* v = std::getenv("FPBEM_L2P_CTAS");
+      return v ? std::atoi(v) : 0;
+    }();
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm,
+        which == 0 ? reinterpret_cast<const void*>(&dft_axis_dmma_kernel<4, true>)
+                   : reinterpret_cast<const void*>(&dft_axis_dmma_kernel<8, true>),
+        kDftMmaWarps * 32, smem);
+    if (e != cudaSuccess) return e;
+    occ[which] = occ_env > 0 ? occ_env : (per_sm > 0 ? per_sm : 1);
+  }
+  const long long cap = static_cast<long long>(device_sms()) * occ[which];
+  if (blocks > cap) blocks = cap;
   if (KTd <= 4)
     dft_axis_dmma_kernel<4, true><<<static_cast<int>(blocks), kDftMmaWarps * 32, smem, stream>>>(
         in, out, tw, n_a, n_in, n_out, n_inner, L, 1, scale, epi);
