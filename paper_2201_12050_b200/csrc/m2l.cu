@@ -1110,7 +1110,8 @@ constexpr int kStreamRegs = 2;  // E <= 32 * kStreamRegs
 
 // s[v] <- Λ s[v] for NV staged vectors of E = nrhs x b fields (b <= 32: one output per lane).
 // BC > 0: b = BC at compile time (the reference's default order n_t = 4, b = 25: the column loop
-// unrolls fully and its shared-memory loads are issued ahead of the FMA chains); BC = 0: any b.
+// is unrolled by 4 pairs — a full unroll spills — so its shared-memory loads run ahead of the FMA
+// chains); BC = 0: any b.
 template <int NV, int BC>
 __device__ __forceinline__ void mode_multi(const c64* __restrict__ lam_blk, c64* __restrict__ s0, int E, int b_rt,
                                            int lane) {
