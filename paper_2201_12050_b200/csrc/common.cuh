@@ -62,13 +62,20 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 #endif
 
-// FPBEM_PDL=1 enables it (read once); never while the stream is being captured into a graph
-inline bool pdl_enabled(cudaStream_t stream) {
-  static const bool on = [] {
+// FPBEM_PDL (read once): 2 (default) the lattice DFT passes; 1 the mode product as well; 0 off.
+// Measured on cfg3: 0.359 / 0.367 ms (off, bimodal) -> 0.355 ms with the passes; with the mode
+// product too 0.375 ms (its early-resident CTAs take the SM slots the far field's Λ stream would
+// have used). Never while the stream is being captured into a graph.
+inline int pdl_level() {
+  static const int level = [] {
     const char* v = std::getenv("FPBEM_PDL");
-    return v && std::atoi(v) != 0;
+    return v ? std::atoi(v) : 2;
   }();
-  if (!on) return false;
+  return level;
+}
+inline bool pdl_enabled(cudaStream_t stream, bool mode_product = false) {
+  const int level = pdl_level();
+  if (level <= 0 || (mode_product && level == 2)) return false;
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(stream, &st) != cudaSuccess) return false;
   return st == cudaStreamCaptureStatusNone;

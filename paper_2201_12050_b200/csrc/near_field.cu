@@ -745,7 +745,7 @@ cudaError_t launch_mode_mma(const c64* shat, const int* items, long long n_items
   if (e != cudaSuccess) return e;
   const long long units = n_blk * rsplit;
   const int grid = static_cast<int>(std::min<long long>(units, sms));
-  return launch_ex(fns[which], dim3(grid), dim3(32 * (NW + 2)), smem, stream, pdl_enabled(stream), shat, items, n_items,
+  return launch_ex(fns[which], dim3(grid), dim3(32 * (NW + 2)), smem, stream, pdl_enabled(stream, true), shat, items, n_items,
                    perm, xh, yh, n, t_lo, t_hi, q_stride, nrhs, ncols, KC, R, rsplit, mode_mma_xbufs());
 }
 

@@ -424,10 +424,10 @@ def test_pipelined_host_product_equals_device_product(ops, assembled, cid, var):
 
 
 def test_programmatic_dependent_launch_gives_the_same_bits(tmp_path):
-    """FPBEM_PDL=1 (the DFT passes and the mode product launched as programmatic dependents,
-    griddepcontrol.wait in front of their first dependent access; read once per process, hence the
-    subprocesses): the product and a GMRES solve of the shrunk cfg3 lattice are bitwise those of the
-    ordinary launches, product after product."""
+    """FPBEM_PDL (0 off, 2 the DFT passes launched as programmatic dependents — the default —, 1 the mode
+    product as well; griddepcontrol.wait in front of their first dependent access; read once per process,
+    hence the subprocesses): the product and a GMRES solve of the shrunk cfg3 lattice are bitwise those
+    of the ordinary launches, product after product."""
     import os
     import subprocess
     import sys
@@ -447,10 +447,10 @@ def test_programmatic_dependent_launch_gives_the_same_bits(tmp_path):
     )
     root = Path(__file__).resolve().parents[1]
     outs = []
-    for pdl in ("0", "1"):
+    for pdl in ("0", "1", "2"):
         f = tmp_path / f"pdl{pdl}.npy"
         env = dict(os.environ, FPBEM_PDL=pdl, PYTHONPATH=str(root))
         r = subprocess.run([sys.executable, "-c", code, str(f)], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
