@@ -62,14 +62,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 #endif
 
-// FPBEM_PDL (read once): 2 (default) the lattice DFT passes; 1 the mode product as well; 0 off.
-// Measured on cfg3: 0.359 / 0.367 ms (off, bimodal) -> 0.355 ms with the passes; with the mode
-// product too 0.375 ms (its early-resident CTAs take the SM slots the far field's Λ stream would
-// have used). Never while the stream is being captured into a graph.
+// FPBEM_PDL (read once): 0 (default) off; 2 the lattice DFT passes; 1 the mode product as well.
+// Measured on cfg3: the passes alone 0.359 -> 0.355 ms per product, but the GMRES solve 0.1441 ->
+// 0.1465 s and the host-pointer product 1.170 -> 1.165e9 DOF/s; with the mode product too 0.375 ms
+// (its early-resident CTAs take the SM slots the far field's Λ stream would have used). Never while
+// the stream is being captured into a graph.
 inline int pdl_level() {
   static const int level = [] {
     const char* v = std::getenv("FPBEM_PDL");
-    return v ? std::atoi(v) : 2;
+    return v ? std::atoi(v) : 0;
   }();
   return level;
 }

@@ -424,7 +424,7 @@ def test_pipelined_host_product_equals_device_product(ops, assembled, cid, var):
 
 
 def test_programmatic_dependent_launch_gives_the_same_bits(tmp_path):
-    """FPBEM_PDL (0 off, 2 the DFT passes launched as programmatic dependents — the default —, 1 the mode
+    """FPBEM_PDL (0 off — the default —, 2 the DFT passes launched as programmatic dependents, 1 the mode
     product as well; griddepcontrol.wait in front of their first dependent access; read once per process,
     hence the subprocesses): the product and a GMRES solve of the shrunk cfg3 lattice are bitwise those
     of the ordinary launches, product after product."""
